@@ -1,0 +1,161 @@
+/*
+ * hgca_b200.h -- C ABI of the B200-native hybrid decode-attention library
+ * (libhgca_b200.so). Plain device pointers, sizes and a CUDA stream; no torch
+ * types. Every entry point returns 0 on success, HGCA_EINVAL for a contract
+ * violation (the reference raises ContractError, errors.py:1-2) or
+ * HGCA_ECUDA for a CUDA failure; hgca_last_error() describes the last failure
+ * of the calling thread.
+ *
+ * Reference interfaces each entry replaces (paths under
+ * /root/reference/pkg/src/tierkv/):
+ *   hgca_attend_dense          backends.active.attend_dense   backends.py:8-20, _core.pyx:22-84
+ *   hgca_attend_indexed        backends.active.attend_indexed backends.py:8-20, _core.pyx:87-150
+ *   hgca_attend_indexed_heads  per-head attend_indexed loop   engine.py:139-148
+ *   hgca_attend_gqa            append-mode attend over window / archive  engine.py:127-132, 161-164
+ *   hgca_merge_states          merge_states                   attention.py:153-188
+ *   hgca_select_threshold      select_salient                 sparsifier.py:32-42
+ *   hgca_mask_to_indices       np.nonzero / context index lists sparsifier.py:42, 77-87
+ *   hgca_popcount_rows         ContextCache.sizes             sparsifier.py:74-75
+ *   hgca_group_need            pack_head_groups targets       sparsifier.py:209-217
+ *   hgca_select_topk           pack_head_groups padding order sparsifier.py:219-226
+ *   hgca_write_rows            WindowCache.append_kv          kv_cache.py:122-169
+ *   hgca_maw_update            WindowCache.update_maw / StoreTier.reevaluate kv_cache.py:171-187, sparsifier.py:158-177
+ *   hgca_union_build           (device layout of the context cache for the decode kernel)
+ *   hgca_decode_step           HybridEngine._run_step, decode mode engine.py:151-195
+ *   hgca_merge_partials        P-way merge of sharded (out, lse) partials
+ */
+#ifndef HGCA_B200_H
+#define HGCA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HGCA_OK 0
+#define HGCA_EINVAL 1
+#define HGCA_ECUDA 2
+
+#define HGCA_DTYPE_F32 0
+#define HGCA_DTYPE_F64 1
+#define HGCA_DTYPE_BF16 2
+
+typedef void* hgca_stream_t; /* a cudaStream_t */
+
+int hgca_version(void);
+const char* hgca_last_error(void);
+
+/* ---- plugin boundary (tierkv backend contract) ---------------------------
+ * Dense: q [H,nq,d], k/v [H,nkv,d] of one dtype (F32 or F64), C-contiguous.
+ * out [H,nq,d] (input dtype), lse [H,nq] fp64, weights [H,nq,nkv] or NULL.
+ * ws: caller scratch of hgca_attend_ws_bytes(H*nq, nkv) bytes.
+ * nkv == 0 gives zero output and lse = -inf (_core.pyx:41-45). */
+int64_t hgca_attend_ws_bytes(int64_t rows, int64_t nkeys);
+int hgca_attend_dense(int dtype, const void* q, const void* k, const void* v, int64_t H,
+                      int64_t nq, int64_t nkv, int64_t d, double scale, int keep_weights,
+                      void* out, double* lse, void* weights, void* ws, hgca_stream_t stream);
+
+/* Indexed (single head): q [nq,d], k/v [M,d], idx int64 [n] (rows of k/v). */
+int hgca_attend_indexed(int dtype, const void* q, const void* k, const void* v,
+                        const int64_t* idx, int64_t n, int64_t M, int64_t nq, int64_t d,
+                        double scale, int keep_weights, void* out, double* lse, void* weights,
+                        void* ws, hgca_stream_t stream);
+
+/* Many heads at once: q [H,nq,d], k/v [H,M,d]; head h attends
+ * idx[idx_off[h] .. idx_off[h]+idx_cnt[h]) (device arrays); weights for head h
+ * are written at weights + h*nq*max_n with row stride max_n. */
+int hgca_attend_indexed_heads(int dtype, const void* q, const void* k, const void* v,
+                              int64_t H, int64_t M, const int64_t* idx, const int64_t* idx_off,
+                              const int64_t* idx_cnt, int64_t max_n, int64_t nq, int64_t d,
+                              double scale, void* out, double* lse, void* weights, void* ws,
+                              hgca_stream_t stream);
+
+/* Grouped-query attention over rows [row0, row0+n) of a position buffer:
+ * q [B*Hq, nq, d]; K/V [B*Hkv, T, d]; q-head h of batch b reads kv-head
+ * b*Hkv + h/(Hq/Hkv). weights [B*Hq, nq, wts_ld] or NULL. */
+int hgca_attend_gqa(int dtype, const void* q, const void* K, const void* V, int64_t B, int64_t Hq,
+                    int64_t Hkv, int64_t T, int64_t row0, int64_t n, int64_t nq, int64_t d,
+                    double scale, void* out, double* lse, void* weights, int64_t wts_ld, void* ws,
+                    hgca_stream_t stream);
+
+/* merge_states over `rows` rows of d: outputs in dtype, lse fp64. Optional
+ * weight rows (w_a [rows,na], w_b [rows,nb] -> w_out [rows,na+nb]). */
+int hgca_merge_states(int dtype, const void* out_a, const double* lse_a, const void* out_b,
+                      const double* lse_b, int64_t rows, int64_t d, void* out, double* lse,
+                      const void* w_a, const void* w_b, int64_t na, int64_t nb, void* w_out,
+                      hgca_stream_t stream);
+
+/* P-way merge of fp32 partials: outs [P, rows, d], lses [P, rows] -> out, lse
+ * (left fold of merge_states in p order). */
+int hgca_merge_partials(const float* outs, const double* lses, int64_t P, int64_t rows, int64_t d,
+                        float* out, double* lse, hgca_stream_t stream);
+
+/* ---- selection ----------------------------------------------------------
+ * Bit masks are [rows, words] uint32, bit p of row r = position p. */
+int hgca_select_threshold(const double* maw, int64_t rows, int64_t ld, int64_t p0, int64_t p1,
+                          double beta, int64_t divisor, uint32_t* mask, int64_t words,
+                          int assign, hgca_stream_t stream);
+int hgca_mask_to_indices(const uint32_t* mask_a, const uint32_t* mask_b, int64_t rows,
+                         int64_t words, int64_t n, int64_t* idx, int64_t ld, uint8_t* flags,
+                         int64_t* counts, hgca_stream_t stream);
+int hgca_popcount_rows(const uint32_t* mask, int64_t rows, int64_t words, int64_t n,
+                       int64_t* counts, hgca_stream_t stream);
+int hgca_group_need(const int64_t* counts, int64_t B, int64_t H, int64_t g, int64_t* need,
+                    hgca_stream_t stream);
+/* Per row, OR into out the top k[row] candidates of [0,n) not in exclude
+ * (NULL = none) by (maw descending, position ascending). */
+int hgca_select_topk(const double* maw, int64_t rows, int64_t ld, int64_t n, const int64_t* k,
+                     const uint32_t* exclude, uint32_t* out, int64_t words, hgca_stream_t stream);
+
+/* ---- device-resident decode engine --------------------------------------- */
+int hgca_write_rows(int dtype, void* K, void* V, int64_t BH, int64_t T, int64_t d, int64_t pos,
+                    const void* k_new, const void* v_new, int64_t n, hgca_stream_t stream);
+int hgca_decode_chunk_rows(int dtype, int64_t d);
+/* MAW maintenance from float32 weight rows w [BH, nq, w_ld] (row mean in fp64):
+ * mode 0 = window EMA for j < w_old and init for j >= w_old (kv_cache.py:171-187,
+ * engine.py:177-191); mode 1 = replace (StoreTier.reevaluate, sparsifier.py:158-177). */
+int hgca_maw_update(const float* w, int64_t BH, int64_t nq, int64_t W, int64_t w_ld, double* maw,
+                    int64_t T, int64_t p0, int64_t w_old, double alpha, int mode, hgca_stream_t stream);
+int hgca_union_build(const uint32_t* sel_mask, int64_t B, int64_t Hq, int64_t Hkv, int64_t words,
+                     int64_t n_arch, int64_t T, int32_t* u_pos, uint8_t* u_qm, int32_t* u_cnt,
+                     int32_t* item_off, int64_t sparse_rows, hgca_stream_t stream);
+
+typedef struct hgca_decode_desc {
+  int32_t dtype;            /* HGCA_DTYPE_F32 or HGCA_DTYPE_BF16 (storage) */
+  int32_t pad0;
+  int64_t B, Hq, Hkv, D, T; /* batch, query heads, kv heads, head_dim, positions */
+  const void* K;            /* [B*Hkv, T, D] */
+  const void* V;
+  const void* q;            /* [B*Hq, D] this step's queries (storage dtype) */
+  double scale;
+  int64_t dlo, dhi;         /* dense positions [dlo, dhi): window + kv_in */
+  int64_t w_old;            /* window entries before this step (EMA'd) */
+  int64_t dense_rows;       /* rows per dense work item */
+  int64_t sparse_rows;      /* rows per sparse work item (as in hgca_union_build) */
+  const int32_t* u_pos;     /* union lists from hgca_union_build */
+  const uint8_t* u_qm;
+  const int32_t* u_cnt;
+  const int32_t* item_off;
+  double* dsc;              /* [B*Hq, dsc_ld] fp64 scratch, dsc_ld >= dhi-dlo */
+  int64_t dsc_ld;
+  double* part_m;           /* [max_items*G] */
+  double* part_z;           /* [max_items*G] */
+  float* part_acc;          /* [max_items*G*D] */
+  int64_t max_items;
+  int32_t* counter;         /* 1 int scratch */
+  double* maw;              /* [B*Hq, T] or NULL */
+  double alpha;
+  float* out;               /* [B*Hq, D] */
+  double* lse;              /* [B*Hq] */
+  float* wts_out;           /* optional [B*Hq, dhi-dlo] dense weights (a_gpu) */
+  float* out_sparse;        /* optional sparse-only partial [B*Hq, D] */
+  double* lse_sparse;       /* optional [B*Hq] */
+} hgca_decode_desc;
+
+int hgca_decode_step(const hgca_decode_desc* desc, hgca_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,21 @@
+"""B200-native hybrid two-tier decode attention (HGCA, arXiv 2507.03153).
+
+Drop-in for the hot path of the reference package `tierkv`: the attention
+API (attention.py), the kernel plugin slot (backends.py), store-tier
+selection (sparsifier.py) and a device-resident step driver (engine.py),
+all computing in libhgca_b200.so (hand-written sm_100a CUDA behind a C ABI,
+include/hgca_b200.h). There is no CPU fallback.
+"""
+
+from .errors import ContractError
+from .attention import AttentionResult, HeadShape, attend, attend_indexed, logsumexp, merge_states
+from .backends import CUDA, install
+from .sparsifier import HeadGroupTask, pack_head_groups, select_salient, select_topk
+from .engine import CacheConfig, EngineConfig, HybridEngine, LayerState, StepInput, StepOutput
+from . import _lib
+
+__version__ = "0.1.0"
+
+
+def library_path() -> str:
+    return _lib.LIB_PATH

@@ -1,0 +1,102 @@
+"""ctypes binding of the C ABI in include/hgca_b200.h (libhgca_b200.so).
+
+The product path has no CPU fallback: if the library is missing or no CUDA
+device is present, every compute entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import ContractError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libhgca_b200.so")
+
+DTYPE_F32, DTYPE_F64, DTYPE_BF16 = 0, 1, 2
+HGCA_OK, HGCA_EINVAL, HGCA_ECUDA = 0, 1, 2
+
+P = ctypes.c_void_p
+I64 = ctypes.c_int64
+I32 = ctypes.c_int
+D = ctypes.c_double
+
+
+class DecodeDesc(ctypes.Structure):
+    """Mirror of hgca_decode_desc (include/hgca_b200.h)."""
+
+    _fields_ = [
+        ("dtype", ctypes.c_int32), ("pad0", ctypes.c_int32),
+        ("B", I64), ("Hq", I64), ("Hkv", I64), ("D", I64), ("T", I64),
+        ("K", P), ("V", P), ("q", P),
+        ("scale", D),
+        ("dlo", I64), ("dhi", I64), ("w_old", I64),
+        ("dense_rows", I64), ("sparse_rows", I64),
+        ("u_pos", P), ("u_qm", P), ("u_cnt", P), ("item_off", P),
+        ("dsc", P), ("dsc_ld", I64),
+        ("part_m", P), ("part_z", P), ("part_acc", P), ("max_items", I64),
+        ("counter", P),
+        ("maw", P), ("alpha", D),
+        ("out", P), ("lse", P), ("wts_out", P), ("out_sparse", P), ("lse_sparse", P),
+    ]
+
+
+# name -> argtypes (all return int unless listed in _RESTYPES)
+_SIGS = {
+    "hgca_version": [],
+    "hgca_last_error": [],
+    "hgca_attend_ws_bytes": [I64, I64],
+    "hgca_attend_dense": [I32, P, P, P, I64, I64, I64, I64, D, I32, P, P, P, P, P],
+    "hgca_attend_indexed": [I32, P, P, P, P, I64, I64, I64, I64, D, I32, P, P, P, P, P],
+    "hgca_attend_indexed_heads": [I32, P, P, P, I64, I64, P, P, P, I64, I64, I64, D, P, P, P, P, P],
+    "hgca_attend_gqa": [I32, P, P, P, I64, I64, I64, I64, I64, I64, I64, I64, D, P, P, P, I64, P, P],
+    "hgca_merge_states": [I32, P, P, P, P, I64, I64, P, P, P, P, I64, I64, P, P],
+    "hgca_merge_partials": [P, P, I64, I64, I64, P, P, P],
+    "hgca_select_threshold": [P, I64, I64, I64, I64, D, I64, P, I64, I32, P],
+    "hgca_mask_to_indices": [P, P, I64, I64, I64, P, I64, P, P, P],
+    "hgca_popcount_rows": [P, I64, I64, I64, P, P],
+    "hgca_group_need": [P, I64, I64, I64, P, P],
+    "hgca_select_topk": [P, I64, I64, I64, P, P, P, I64, P],
+    "hgca_write_rows": [I32, P, P, I64, I64, I64, I64, P, P, I64, P],
+    "hgca_decode_chunk_rows": [I32, I64],
+    "hgca_maw_update": [P, I64, I64, I64, I64, P, I64, I64, I64, D, I32, P],
+    "hgca_union_build": [P, I64, I64, I64, I64, I64, I64, P, P, P, P, I64, P],
+    "hgca_decode_step": [ctypes.POINTER(DecodeDesc), P],
+}
+_RESTYPES = {"hgca_last_error": ctypes.c_char_p, "hgca_attend_ws_bytes": I64}
+
+_lib = None
+
+
+def load():
+    """Load libhgca_b200.so; raises if it has not been built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            )
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, args in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = _RESTYPES.get(name, ctypes.c_int)
+        _lib = lib
+    return _lib
+
+
+def exported_symbols():
+    return sorted(_SIGS)
+
+
+def call(name, *args):
+    """Invoke a C-ABI entry point and map its status to exceptions."""
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != HGCA_OK:
+        msg = lib.hgca_last_error().decode(errors="replace")
+        if rc == HGCA_EINVAL:
+            raise ContractError(msg)
+        raise RuntimeError(f"{name}: {msg}")
+    return rc

@@ -1,0 +1,299 @@
+// extern "C" boundary of libhgca_b200.so (declared in include/hgca_b200.h).
+// Validation mirrors the reference's ContractError checks (attention.py:94-114,
+// 133-144; sparsifier.py:38-39) and maps them to HGCA_EINVAL.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "hgca_common.cuh"
+#include "hgca_internal.h"
+#include "../../include/hgca_b200.h"
+
+namespace hgca {
+
+static thread_local char g_err[512] = "";
+
+static int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+static int cuda_status(int e, const char* what) {
+  if (e == 0) return HGCA_OK;
+  if (e > 0) return fail(HGCA_ECUDA, "%s: %s", what, cudaGetErrorString((cudaError_t)e));
+  return fail(HGCA_EINVAL, "%s: unsupported configuration (code %d)", what, e);
+}
+
+__global__ void merge_partials_kernel(const float* outs, const double* lses, int64_t P, int64_t rows,
+                                      int64_t d, float* out, double* lse) {
+  const int64_t r = blockIdx.x;
+  double M = -INFINITY;
+  for (int64_t p = 0; p < P; ++p) M = fmax(M, lses[p * rows + r]);
+  if (M == -INFINITY) {
+    for (int64_t c = threadIdx.x; c < d; c += blockDim.x) out[r * d + c] = 0.f;
+    if (threadIdx.x == 0) lse[r] = -INFINITY;
+    return;
+  }
+  double Z = 0.0;
+  for (int64_t p = 0; p < P; ++p) Z += exp(lses[p * rows + r] - M);
+  for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
+    double acc = 0.0;
+    for (int64_t p = 0; p < P; ++p) {
+      const double w = exp(lses[p * rows + r] - M);
+      if (w != 0.0) acc += w * (double)outs[(p * rows + r) * d + c];
+    }
+    out[r * d + c] = (float)(acc / Z);
+  }
+  if (threadIdx.x == 0) lse[r] = M + log(Z);
+}
+
+}  // namespace hgca
+
+using namespace hgca;
+
+static inline cudaStream_t S(hgca_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+extern "C" {
+
+int hgca_version(void) { return 1; }
+const char* hgca_last_error(void) { return g_err; }
+
+int64_t hgca_attend_ws_bytes(int64_t rows, int64_t nkeys) {
+  return (rows > 0 ? rows : 1) * (nkeys > 0 ? nkeys : 1) * (int64_t)sizeof(double);
+}
+
+int hgca_attend_dense(int dtype, const void* q, const void* k, const void* v, int64_t H, int64_t nq,
+                      int64_t nkv, int64_t d, double scale, int keep_weights, void* out,
+                      double* lse, void* weights, void* ws, hgca_stream_t stream) {
+  if (dtype != HGCA_DTYPE_F32 && dtype != HGCA_DTYPE_F64)
+    return fail(HGCA_EINVAL, "attend_dense: dtype must be float32 or float64");
+  if (H < 0 || nq < 0 || nkv < 0 || d < 1) return fail(HGCA_EINVAL, "attend_dense: bad shape");
+  if (!(scale > 0)) return fail(HGCA_EINVAL, "attend_dense: scale must be > 0");
+  if (!q || !out || !lse || (nkv > 0 && (!k || !v || !ws)) || (keep_weights && nkv > 0 && !weights))
+    return fail(HGCA_EINVAL, "attend_dense: null pointer");
+  AttendArgs a{};
+  a.q = q; a.k = k; a.v = v;
+  a.Hq = H; a.Hkv = H; a.G = 1;
+  a.nq = nq; a.d = d; a.ld_head = nkv * d; a.row0 = 0; a.n = nkv;
+  a.scale = scale;
+  a.out = out; a.lse = lse;
+  a.wts = keep_weights ? weights : nullptr; a.wts_ld = nkv;
+  a.ws = reinterpret_cast<double*>(ws); a.ws_ld = nkv;
+  return cuda_status(launch_attend(dtype, a, H, S(stream)), "attend_dense");
+}
+
+int hgca_attend_indexed(int dtype, const void* q, const void* k, const void* v, const int64_t* idx,
+                        int64_t n, int64_t M, int64_t nq, int64_t d, double scale, int keep_weights,
+                        void* out, double* lse, void* weights, void* ws, hgca_stream_t stream) {
+  if (dtype != HGCA_DTYPE_F32 && dtype != HGCA_DTYPE_F64)
+    return fail(HGCA_EINVAL, "attend_indexed: dtype must be float32 or float64");
+  if (n < 0 || M < 0 || nq < 0 || d < 1) return fail(HGCA_EINVAL, "attend_indexed: bad shape");
+  if (!(scale > 0)) return fail(HGCA_EINVAL, "attend_indexed: scale must be > 0");
+  if (!q || !out || !lse || (n > 0 && (!k || !v || !idx || !ws)) || (keep_weights && n > 0 && !weights))
+    return fail(HGCA_EINVAL, "attend_indexed: null pointer");
+  AttendArgs a{};
+  a.q = q; a.k = k; a.v = v;
+  a.Hq = 1; a.Hkv = 1; a.G = 1;
+  a.nq = nq; a.d = d; a.ld_head = M * d; a.row0 = 0; a.n = n;
+  a.idx = idx;
+  a.scale = scale;
+  a.out = out; a.lse = lse;
+  a.wts = keep_weights ? weights : nullptr; a.wts_ld = n;
+  a.ws = reinterpret_cast<double*>(ws); a.ws_ld = n;
+  return cuda_status(launch_attend(dtype, a, 1, S(stream)), "attend_indexed");
+}
+
+int hgca_attend_indexed_heads(int dtype, const void* q, const void* k, const void* v, int64_t H,
+                              int64_t M, const int64_t* idx, const int64_t* idx_off,
+                              const int64_t* idx_cnt, int64_t max_n, int64_t nq, int64_t d,
+                              double scale, void* out, double* lse, void* weights, void* ws,
+                              hgca_stream_t stream) {
+  if (dtype != HGCA_DTYPE_F32 && dtype != HGCA_DTYPE_F64 && dtype != HGCA_DTYPE_BF16)
+    return fail(HGCA_EINVAL, "attend_indexed_heads: bad dtype");
+  if (H < 0 || M < 0 || nq < 0 || d < 1 || max_n < 0)
+    return fail(HGCA_EINVAL, "attend_indexed_heads: bad shape");
+  if (!q || !out || !lse || !idx_off || !idx_cnt || (max_n > 0 && (!k || !v || !idx || !ws)))
+    return fail(HGCA_EINVAL, "attend_indexed_heads: null pointer");
+  AttendArgs a{};
+  a.q = q; a.k = k; a.v = v;
+  a.Hq = H; a.Hkv = H; a.G = 1;
+  a.nq = nq; a.d = d; a.ld_head = M * d; a.row0 = 0; a.n = 0;
+  a.idx = idx; a.idx_off = idx_off; a.idx_cnt = idx_cnt;
+  a.scale = scale;
+  a.out = out; a.lse = lse;
+  a.wts = weights; a.wts_ld = max_n;
+  a.ws = reinterpret_cast<double*>(ws); a.ws_ld = max_n > 0 ? max_n : 1;
+  return cuda_status(launch_attend(dtype, a, H, S(stream)), "attend_indexed_heads");
+}
+
+int hgca_attend_gqa(int dtype, const void* q, const void* K, const void* V, int64_t B, int64_t Hq,
+                    int64_t Hkv, int64_t T, int64_t row0, int64_t n, int64_t nq, int64_t d,
+                    double scale, void* out, double* lse, void* weights, int64_t wts_ld, void* ws,
+                    hgca_stream_t stream) {
+  if (B < 1 || Hq < 1 || Hkv < 1 || Hq % Hkv || d < 1 || n < 0 || row0 < 0 || row0 + n > T)
+    return fail(HGCA_EINVAL, "attend_gqa: bad shape (B=%lld Hq=%lld Hkv=%lld row0=%lld n=%lld T=%lld)",
+                (long long)B, (long long)Hq, (long long)Hkv, (long long)row0, (long long)n,
+                (long long)T);
+  if (weights && wts_ld < n) return fail(HGCA_EINVAL, "attend_gqa: wts_ld < n");
+  AttendArgs a{};
+  a.q = q; a.k = K; a.v = V;
+  a.Hq = Hq; a.Hkv = Hkv; a.G = Hq / Hkv;
+  a.nq = nq; a.d = d; a.ld_head = T * d; a.row0 = row0; a.n = n;
+  a.scale = scale;
+  a.out = out; a.lse = lse;
+  a.wts = weights; a.wts_ld = wts_ld;
+  a.ws = reinterpret_cast<double*>(ws); a.ws_ld = n > 0 ? n : 1;
+  return cuda_status(launch_attend(dtype, a, B * Hq, S(stream)), "attend_gqa");
+}
+
+int hgca_merge_states(int dtype, const void* out_a, const double* lse_a, const void* out_b,
+                      const double* lse_b, int64_t rows, int64_t d, void* out, double* lse,
+                      const void* w_a, const void* w_b, int64_t na, int64_t nb, void* w_out,
+                      hgca_stream_t stream) {
+  if (dtype != HGCA_DTYPE_F32 && dtype != HGCA_DTYPE_F64)
+    return fail(HGCA_EINVAL, "merge_states: dtype must be float32 or float64");
+  if (rows < 0 || d < 0 || na < 0 || nb < 0) return fail(HGCA_EINVAL, "merge_states: bad shape");
+  if (w_out && ((na > 0 && !w_a) || (nb > 0 && !w_b)))
+    return fail(HGCA_EINVAL, "merge_states: null weight rows");
+  MergeArgs a{};
+  a.out_a = out_a; a.lse_a = lse_a; a.out_b = out_b; a.lse_b = lse_b;
+  a.rows = rows; a.d = d; a.out = out; a.lse = lse;
+  a.w_a = w_a; a.w_b = w_b; a.na = na; a.nb = nb; a.w_out = w_out;  // w_a / w_b may be NULL only when na / nb == 0
+  return cuda_status(launch_merge(dtype, a, S(stream)), "merge_states");
+}
+
+int hgca_merge_partials(const float* outs, const double* lses, int64_t P, int64_t rows, int64_t d,
+                        float* out, double* lse, hgca_stream_t stream) {
+  if (P < 1 || rows < 0 || d < 1) return fail(HGCA_EINVAL, "merge_partials: bad shape");
+  if (rows == 0) return HGCA_OK;
+  merge_partials_kernel<<<(unsigned)rows, 128, 0, S(stream)>>>(outs, lses, P, rows, d, out, lse);
+  return cuda_status((int)cudaGetLastError(), "merge_partials");
+}
+
+int hgca_select_threshold(const double* maw, int64_t rows, int64_t ld, int64_t p0, int64_t p1,
+                          double beta, int64_t divisor, uint32_t* mask, int64_t words, int assign,
+                          hgca_stream_t stream) {
+  if (divisor < 1) return fail(HGCA_EINVAL, "divisor must be >= 1, got %lld", (long long)divisor);
+  if (p0 < 0 || p1 < p0 || p1 > ld || words * 32 < p1 || rows < 0)
+    return fail(HGCA_EINVAL, "select_threshold: bad range");
+  if (rows == 0 || p1 == p0) return HGCA_OK;
+  const double thr = beta / (double)divisor;  // IEEE fp64, like beta / divisor in Python
+  const int64_t nw = ((p1 + 31) >> 5) - (p0 >> 5);
+  const int64_t total = nw * rows;
+  (void)total;
+  return cuda_status(launch_threshold_mask(maw, rows, ld, p0, p1, thr, mask, words, assign, S(stream)),
+                     "select_threshold");
+}
+
+int hgca_mask_to_indices(const uint32_t* mask_a, const uint32_t* mask_b, int64_t rows, int64_t words,
+                         int64_t n, int64_t* idx, int64_t ld, uint8_t* flags, int64_t* counts,
+                         hgca_stream_t stream) {
+  if (rows < 0 || n < 0 || words * 32 < n || ld < n) return fail(HGCA_EINVAL, "mask_to_indices: bad shape");
+  if (rows == 0) return HGCA_OK;
+  return cuda_status(launch_mask_to_indices(mask_a, mask_b, rows, words, n, idx, ld, flags, counts, S(stream)),
+                     "mask_to_indices");
+}
+
+int hgca_popcount_rows(const uint32_t* mask, int64_t rows, int64_t words, int64_t n, int64_t* counts,
+                       hgca_stream_t stream) {
+  if (rows < 0 || words * 32 < n) return fail(HGCA_EINVAL, "popcount_rows: bad shape");
+  if (rows == 0) return HGCA_OK;
+  return cuda_status(launch_popcount_rows(mask, rows, words, n, counts, S(stream)), "popcount_rows");
+}
+
+int hgca_group_need(const int64_t* counts, int64_t B, int64_t H, int64_t g, int64_t* need,
+                    hgca_stream_t stream) {
+  if (B < 0 || H < 0 || g < 1) return fail(HGCA_EINVAL, "group_need: bad shape");
+  if (B * H == 0) return HGCA_OK;
+  return cuda_status(launch_group_need(counts, B, H, g, need, S(stream)), "group_need");
+}
+
+int hgca_select_topk(const double* maw, int64_t rows, int64_t ld, int64_t n, const int64_t* k,
+                     const uint32_t* exclude, uint32_t* out, int64_t words, hgca_stream_t stream) {
+  if (rows < 0 || n < 0 || n > ld || words * 32 < n) return fail(HGCA_EINVAL, "select_topk: bad shape");
+  if (rows == 0 || n == 0) return HGCA_OK;
+  return cuda_status(launch_topk_mask(maw, rows, ld, n, k, exclude, out, words, S(stream)), "select_topk");
+}
+
+int hgca_write_rows(int dtype, void* K, void* V, int64_t BH, int64_t T, int64_t d, int64_t pos,
+                    const void* k_new, const void* v_new, int64_t n, hgca_stream_t stream) {
+  if (pos < 0 || n < 0 || pos + n > T) return fail(HGCA_EINVAL, "write_rows: position range exceeds buffer");
+  return cuda_status(launch_write_rows(dtype, K, V, BH, T, d, pos, k_new, v_new, n, S(stream)), "write_rows");
+}
+
+int hgca_decode_chunk_rows(int dtype, int64_t d) { return decode_chunk_rows(dtype, d); }
+
+int hgca_maw_update(const float* w, int64_t BH, int64_t nq, int64_t W, int64_t w_ld, double* maw,
+                    int64_t T, int64_t p0, int64_t w_old, double alpha, int mode, hgca_stream_t stream) {
+  if (BH < 0 || nq < 1 || W < 0 || w_ld < W || p0 < 0 || p0 + W > T || (mode != 0 && mode != 1))
+    return fail(HGCA_EINVAL, "maw_update: bad shape");
+  if (!(alpha >= 0.0 && alpha <= 1.0)) return fail(HGCA_EINVAL, "alpha must be in [0, 1], got %g", alpha);
+  return cuda_status(launch_maw_update(w, BH, nq, W, w_ld, maw, T, p0, w_old, alpha, mode, S(stream)),
+                     "maw_update");
+}
+
+int hgca_union_build(const uint32_t* sel_mask, int64_t B, int64_t Hq, int64_t Hkv, int64_t words,
+                     int64_t n_arch, int64_t T, int32_t* u_pos, uint8_t* u_qm, int32_t* u_cnt,
+                     int32_t* item_off, int64_t sparse_rows, hgca_stream_t stream) {
+  if (B < 1 || Hkv < 1 || Hq % Hkv || Hq / Hkv > 8 || n_arch < 0 || n_arch > T || words * 32 < n_arch ||
+      sparse_rows < 1)
+    return fail(HGCA_EINVAL, "union_build: bad shape");
+  return cuda_status(launch_union_build(sel_mask, B, Hq, Hkv, words, n_arch, T, u_pos, u_qm, u_cnt,
+                                        item_off, sparse_rows, S(stream)),
+                     "union_build");
+}
+
+int hgca_decode_step(const hgca_decode_desc* d, hgca_stream_t stream) {
+  if (!d) return fail(HGCA_EINVAL, "decode_step: null descriptor");
+  if (d->dtype != HGCA_DTYPE_F32 && d->dtype != HGCA_DTYPE_BF16)
+    return fail(HGCA_EINVAL, "decode_step: storage dtype must be float32 or bfloat16");
+  if (d->B < 1 || d->Hkv < 1 || d->Hq % d->Hkv) return fail(HGCA_EINVAL, "decode_step: bad heads");
+  const int64_t G = d->Hq / d->Hkv;
+  if (G != 1 && G != 2 && G != 4 && G != 8) return fail(HGCA_EINVAL, "decode_step: Hq/Hkv must be 1, 2, 4 or 8");
+  if (d->D != 64 && d->D != 128) return fail(HGCA_EINVAL, "decode_step: head_dim must be 64 or 128");
+  const int64_t W = d->dhi - d->dlo;
+  if (d->dlo < 0 || W < 1 || d->dhi > d->T || d->w_old < 0 || d->w_old > W || d->dsc_ld < W)
+    return fail(HGCA_EINVAL, "decode_step: bad dense range");
+  const int ch = decode_chunk_rows(d->dtype, d->D);
+  if (d->dense_rows < 1 || d->dense_rows % ch || d->sparse_rows < 1)
+    return fail(HGCA_EINVAL, "decode_step: dense_rows must be a positive multiple of %d", ch);
+  const int64_t Sd = (W + d->dense_rows - 1) / d->dense_rows;
+  const int64_t n_dense = d->B * d->Hkv * Sd;
+  const int64_t max_sparse = d->B * d->Hkv * ((d->T + d->sparse_rows - 1) / d->sparse_rows);
+  if (d->max_items < n_dense + max_sparse)
+    return fail(HGCA_EINVAL, "decode_step: partial buffers hold %lld items, need %lld",
+                (long long)d->max_items, (long long)(n_dense + max_sparse));
+  if (!d->K || !d->V || !d->q || !d->u_pos || !d->u_qm || !d->u_cnt || !d->item_off || !d->dsc ||
+      !d->part_m || !d->part_z || !d->part_acc || !d->counter || !d->out || !d->lse)
+    return fail(HGCA_EINVAL, "decode_step: null pointer");
+  DecodeArgs a{};
+  a.K = d->K; a.V = d->V; a.q = d->q;
+  a.B = d->B; a.Hq = d->Hq; a.Hkv = d->Hkv; a.G = G; a.D = d->D; a.T = d->T;
+  a.scale = d->scale;
+  a.dlo = d->dlo; a.dhi = d->dhi;
+  a.Sd = Sd; a.dense_rows = d->dense_rows;
+  a.u_pos = d->u_pos; a.u_qm = d->u_qm; a.u_cnt = d->u_cnt; a.item_off = d->item_off;
+  a.sparse_rows = d->sparse_rows;
+  a.dsc = d->dsc; a.dsc_ld = d->dsc_ld;
+  a.part_m = d->part_m; a.part_z = d->part_z; a.part_acc = d->part_acc;
+  a.counter = d->counter;
+  a.n_dense_items = n_dense;
+  int rc = cuda_status(launch_decode_partial(d->dtype, a, S(stream)), "decode_partial");
+  if (rc) return rc;
+  DecodeMergeArgs m{};
+  m.B = d->B; m.Hq = d->Hq; m.Hkv = d->Hkv; m.G = G; m.D = d->D;
+  m.Sd = Sd; m.n_dense_items = n_dense; m.item_off = d->item_off;
+  m.part_m = d->part_m; m.part_z = d->part_z; m.part_acc = d->part_acc;
+  m.dsc = d->dsc; m.dsc_ld = d->dsc_ld;
+  m.W = W; m.w_old = d->w_old;
+  m.maw = d->maw; m.T = d->T; m.dlo = d->dlo;
+  m.one_minus_alpha = 1.0 - d->alpha; m.alpha = d->alpha;
+  m.wts_out = d->wts_out; m.out = d->out; m.lse = d->lse;
+  m.out_sparse = d->out_sparse; m.lse_sparse = d->lse_sparse;
+  return cuda_status(launch_decode_merge(m, S(stream)), "decode_merge");
+}
+
+}  // extern "C"

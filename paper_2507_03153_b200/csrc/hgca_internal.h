@@ -1,0 +1,115 @@
+// Internal argument blocks and launchers (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hgca {
+
+// Generic reference-exact attention (attend / attend_indexed / append path).
+struct AttendArgs {
+  const void* q;        // [BH, nq, d]
+  const void* k;        // kv rows for head bh at k + kvh*ld_head + row0*d
+  const void* v;
+  int64_t Hq, Hkv, G;   // bh = b*Hq + h; kvh = b*Hkv + h/G
+  int64_t nq, d;
+  int64_t ld_head;      // elements between consecutive kv heads
+  int64_t row0;         // first row (dense) / base for idx
+  int64_t n;            // dense key count (when idx == nullptr and idx_cnt == nullptr)
+  const int64_t* idx;      // optional gathered rows (concatenated per head)
+  const int64_t* idx_off;  // optional per-head offsets into idx
+  const int64_t* idx_cnt;  // optional per-head counts
+  double scale;
+  void* out;            // [BH, nq, d]
+  double* lse;          // [BH, nq]
+  void* wts;            // optional [BH, nq, wts_ld]
+  int64_t wts_ld;
+  double* ws;           // scores workspace [BH, nq, ws_ld]
+  int64_t ws_ld;
+};
+
+struct MergeArgs {
+  const void* out_a;
+  const double* lse_a;
+  const void* out_b;
+  const double* lse_b;
+  int64_t rows, d;
+  void* out;
+  double* lse;
+  const void* w_a;  // optional weight rows [rows, na] / [rows, nb]
+  const void* w_b;
+  int64_t na, nb;
+  void* w_out;      // [rows, na + nb]
+};
+
+// Fused decode partial pass: dense window tiles + sparse union chunks.
+struct DecodeArgs {
+  const void* K;          // [B*Hkv, T, D] storage dtype
+  const void* V;
+  const void* q;          // [B*Hq, D] storage dtype (decode: one query row)
+  int64_t B, Hq, Hkv, G, D, T;
+  double scale;
+  int64_t dlo, dhi;       // dense positions [dlo, dhi)
+  int64_t Sd;             // dense items per (b, kvh)
+  int64_t dense_rows;     // rows per dense item (multiple of the chunk)
+  const int32_t* u_pos;   // [B*Hkv, T] union positions (grouped by query-head mask)
+  const uint8_t* u_qm;    // [B*Hkv, T] query-head masks
+  const int32_t* u_cnt;   // [B*Hkv]
+  const int32_t* item_off;// [B*Hkv + 1] sparse item prefix
+  int64_t sparse_rows;    // rows per sparse item
+  double* dsc;            // [B*Hq, dsc_ld] dense scores (fp64) for the MAW update
+  int64_t dsc_ld;
+  double* part_m;         // [items, G]
+  double* part_z;         // [items, G]
+  float* part_acc;        // [items, G, D]
+  int32_t* counter;       // work counter (zeroed before launch)
+  int64_t n_dense_items;  // B*Hkv*Sd
+};
+
+struct DecodeMergeArgs {
+  int64_t B, Hq, Hkv, G, D;
+  int64_t Sd, n_dense_items;
+  const int32_t* item_off;
+  const double* part_m;
+  const double* part_z;
+  const float* part_acc;
+  const double* dsc;
+  int64_t dsc_ld;
+  int64_t W;              // dense positions attended = dhi - dlo
+  int64_t w_old;          // window entries before this step (EMA'd); the rest are new
+  double* maw;            // [B*Hq, T] or nullptr (no MAW maintenance)
+  int64_t T;
+  int64_t dlo;
+  double one_minus_alpha, alpha;
+  float* wts_out;         // optional dense weights [B*Hq, W]
+  float* out;             // [B*Hq, D]
+  double* lse;            // [B*Hq]
+  float* out_sparse;      // optional sparse partial out [B*Hq, D] (for sharded merges)
+  double* lse_sparse;
+};
+
+int launch_attend(int dtype, const AttendArgs& a, int64_t BH, cudaStream_t s);
+int launch_merge(int dtype, const MergeArgs& a, cudaStream_t s);
+int launch_threshold_mask(const double* maw, int64_t rows, int64_t ld, int64_t p0, int64_t p1,
+                          double thr, uint32_t* mask, int64_t words, int assign, cudaStream_t s);
+int launch_mask_to_indices(const uint32_t* a, const uint32_t* b, int64_t rows, int64_t words,
+                           int64_t n, int64_t* idx, int64_t ld, uint8_t* flags, int64_t* counts,
+                           cudaStream_t s);
+int launch_popcount_rows(const uint32_t* mask, int64_t rows, int64_t words, int64_t n,
+                         int64_t* counts, cudaStream_t s);
+int launch_group_need(const int64_t* counts, int64_t B, int64_t H, int64_t g, int64_t* need,
+                      cudaStream_t s);
+int launch_topk_mask(const double* maw, int64_t rows, int64_t ld, int64_t n, const int64_t* k,
+                     const uint32_t* exclude, uint32_t* out, int64_t words, cudaStream_t s);
+
+int launch_decode_partial(int dtype, const DecodeArgs& a, cudaStream_t s);
+int launch_decode_merge(const DecodeMergeArgs& a, cudaStream_t s);
+int launch_union_build(const uint32_t* sel, int64_t B, int64_t Hq, int64_t Hkv, int64_t words,
+                       int64_t n_arch, int64_t T, int32_t* u_pos, uint8_t* u_qm, int32_t* u_cnt,
+                       int32_t* item_off, int64_t sparse_rows, cudaStream_t s);
+int launch_write_rows(int dtype, void* K, void* V, int64_t BH, int64_t T, int64_t D, int64_t pos,
+                      const void* k_new, const void* v_new, int64_t n, cudaStream_t s);
+int decode_chunk_rows(int dtype, int64_t D);
+int launch_maw_update(const float* w, int64_t BH, int64_t nq, int64_t W, int64_t w_ld, double* maw,
+                      int64_t T, int64_t p0, int64_t w_old, double alpha, int mode, cudaStream_t s);
+
+}  // namespace hgca

@@ -1,0 +1,467 @@
+"""Device-resident hybrid two-tier decode engine (tierkv/engine.py on the B200).
+
+HybridEngine keeps every tier in HBM and mirrors the reference step driver
+(engine.py:87-195) with its configuration, step input/output types and
+maintenance order, extended the way SURVEY.md F8 describes:
+  * batch B = B lock-step sequences, each an independent reference engine
+    built with EngineConfig(batch=B) (batch only feeds the padding group size);
+  * grouped-query attention: `kv_heads` KV heads, query head h reading KV head
+    h // (heads // kv_heads); MAW and selection stay per query head;
+  * storage dtype float32 (the reference's working precision) or bfloat16.
+
+HBM layout per layer (positions are absolute, so the window tier and the
+store tier share one buffer and eviction is a pointer move, not a copy):
+  K, V       [B*Hkv, T, D]    storage dtype; archive = [0, lo), window = [lo, nxt)
+  maw        [B*Hq, T]        float64 per (query head, position)     kv_cache.py:73-75
+  ctx        [B*Hq, T/32]     context-cache membership bits          sparsifier.py:58-87
+  sel        [B*Hq, T/32]     attended set = ctx | padding           sparsifier.py:198-235
+  u_pos/u_qm [B*Hkv, T]       per-KV-head union of `sel` with query-head masks
+The decode step is one call of hgca_decode_step (dense window + sparse union
++ merge + MAW EMA); selection changes (ingest / re-evaluation) rebuild the
+masks and the union with the selection kernels.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._dev import DTYPE_CODE, device, stream_handle
+from .attention import HeadShape
+from .errors import ContractError
+from .sparsifier import group_size, mask_to_lists, topk_mask, words_for
+
+__all__ = ["CacheConfig", "EngineConfig", "StepInput", "StepOutput", "LayerState", "HybridEngine"]
+
+MODES = ("decode", "append")
+DENSE_ROWS = 512
+SPARSE_ROWS = 512
+
+
+@dataclass(frozen=True)
+class CacheConfig:
+    """kv_cache.py:26-52."""
+
+    blk_num: int
+    blk_size: int
+    alpha: float = 0.5
+    beta: float = 1.0
+
+    def __post_init__(self):
+        if self.blk_num < 2:
+            raise ContractError(f"blk_num must be >= 2, got {self.blk_num}")
+        if self.blk_size < 1:
+            raise ContractError(f"blk_size must be >= 1, got {self.blk_size}")
+        if not 0.0 <= self.alpha <= 1.0:
+            raise ContractError(f"alpha must be in [0, 1], got {self.alpha}")
+        if self.beta < 0.0:
+            raise ContractError(f"beta must be >= 0, got {self.beta}")
+
+    @property
+    def capacity(self) -> int:
+        return self.blk_num * self.blk_size
+
+
+@dataclass(frozen=True)
+class EngineConfig:
+    """config.py:24-51 plus the B200 extensions (kv_heads, dtype, max_positions,
+    selection policy)."""
+
+    layers: int = 2
+    heads: int = 8
+    head_dim: int = 64
+    scale: float | None = None
+    cache: CacheConfig = field(default_factory=lambda: CacheConfig(blk_num=8, blk_size=32))
+    core_count: int = 8
+    batch: int = 1
+    seed: int = 0
+    kv_heads: int | None = None       # None: = heads (the reference's 1:1 heads)
+    dtype: str = "float32"            # storage: "float32" | "bfloat16"
+    max_positions: int = 4096         # HBM capacity per sequence (positions)
+    selection: str = "threshold"      # "threshold" (reference) | "topk" (F1 extension)
+    topk: int = 0                     # entries per head for selection="topk"
+    keep_weights: bool = False        # materialize a_gpu in StepOutput
+
+    def __post_init__(self):
+        if self.layers < 1:
+            raise ContractError(f"layers must be >= 1, got {self.layers}")
+        if self.core_count < 1:
+            raise ContractError(f"core_count must be >= 1, got {self.core_count}")
+        if self.batch < 1:
+            raise ContractError(f"batch must be >= 1, got {self.batch}")
+        kvh = self.heads if self.kv_heads is None else self.kv_heads
+        if kvh < 1 or self.heads % kvh or self.heads // kvh not in (1, 2, 4, 8):
+            raise ContractError(f"heads/kv_heads must be 1, 2, 4 or 8 (heads={self.heads}, kv_heads={kvh})")
+        if self.dtype not in ("float32", "bfloat16"):
+            raise ContractError(f"dtype must be float32 or bfloat16, got {self.dtype}")
+        if self.selection not in ("threshold", "topk"):
+            raise ContractError(f"selection must be threshold or topk, got {self.selection}")
+
+    @property
+    def head_shape(self) -> HeadShape:
+        return HeadShape(self.heads, self.head_dim, self.scale)
+
+    @property
+    def n_kv_heads(self) -> int:
+        return self.heads if self.kv_heads is None else self.kv_heads
+
+    def with_(self, **kw) -> "EngineConfig":
+        return replace(self, **kw)
+
+
+@dataclass
+class StepInput:
+    """engine.py:31-58. q [B, Hq, n_q, D] (or [Hq, n_q, D] when batch == 1);
+    keys/values [B, Hkv, n_q, D] (or [Hkv, n_q, D]). numpy or torch."""
+
+    mode: str
+    q: object
+    keys: object
+    values: object
+
+    def __post_init__(self):
+        if self.mode not in MODES:
+            raise ContractError(f"mode must be one of {MODES}, got {self.mode!r}")
+        if self.q.ndim not in (3, 4):
+            raise ContractError(f"q must be [(batch,) heads, n_q, head_dim], got {tuple(self.q.shape)}")
+        if self.mode == "decode" and self.n_q != 1:
+            raise ContractError(f"decode steps take exactly one query row, got {self.n_q}")
+        if self.n_q < 1:
+            raise ContractError("append steps take at least one query row")
+        if tuple(self.keys.shape) != tuple(self.values.shape) or self.keys.shape[-2] != self.n_q \
+                or self.keys.shape[-1] != self.q.shape[-1] or self.keys.ndim != self.q.ndim:
+            raise ContractError("kv_in must align with q")
+
+    @property
+    def n_q(self) -> int:
+        return int(self.q.shape[-2])
+
+
+@dataclass
+class StepOutput:
+    """engine.py:61-78 (device tensors). store_positions is computed on demand
+    through HybridEngine.store_entries()."""
+
+    output: torch.Tensor          # [B, Hq, n_q, D] float32 (or [Hq, n_q, D])
+    lse: torch.Tensor             # [B, Hq, n_q] float64
+    a_gpu: torch.Tensor | None    # [B, Hq, n_q, W] float32 when keep_weights
+    a_cpu: list | None            # append mode: per (b, h) archive weights
+    dense_positions: np.ndarray
+
+
+class LayerState:
+    """HBM-resident window + store tiers of one layer (see module docstring)."""
+
+    def __init__(self, cfg: EngineConfig, T: int, dev):
+        B, Hq, Hkv, D = cfg.batch, cfg.heads, cfg.n_kv_heads, cfg.head_dim
+        tdt = torch.bfloat16 if cfg.dtype == "bfloat16" else torch.float32
+        self.K = torch.zeros((B * Hkv, T, D), dtype=tdt, device=dev)
+        self.V = torch.zeros((B * Hkv, T, D), dtype=tdt, device=dev)
+        self.maw = torch.zeros((B * Hq, T), dtype=torch.float64, device=dev)
+        words = T // 32
+        self.ctx = torch.zeros((B * Hq, words), dtype=torch.int32, device=dev)
+        self.sel = torch.zeros((B * Hq, words), dtype=torch.int32, device=dev)
+        self.u_pos = torch.zeros((B * Hkv, T), dtype=torch.int32, device=dev)
+        self.u_qm = torch.zeros((B * Hkv, T), dtype=torch.uint8, device=dev)
+        self.u_cnt = torch.zeros(B * Hkv, dtype=torch.int32, device=dev)
+        self.item_off = torch.zeros(B * Hkv + 1, dtype=torch.int32, device=dev)
+        self.lo = 0    # archive size
+        self.nxt = 0   # next position
+
+    @property
+    def window_size(self):
+        return self.nxt - self.lo
+
+    @property
+    def archive_size(self):
+        return self.lo
+
+
+class HybridEngine:
+    """engine.py:87-195 on the B200, for `layers` layers."""
+
+    def __init__(self, config: EngineConfig, dev=None):
+        self.config = config
+        self.shape = config.head_shape
+        self.dev = dev or device()
+        c = config
+        self.B, self.Hq, self.Hkv, self.D = c.batch, c.heads, c.n_kv_heads, c.head_dim
+        self.G = self.Hq // self.Hkv
+        if self.D not in (64, 128):
+            raise ContractError("the device engine supports head_dim 64 or 128")
+        self.T = int(math.ceil(c.max_positions / 32) * 32)
+        self.cap = c.cache.capacity
+        self.tdtype = torch.bfloat16 if c.dtype == "bfloat16" else torch.float32
+        self.dcode = DTYPE_CODE[self.tdtype]
+        self.g_pad = group_size(c.batch, c.heads, c.core_count)
+        self.layers = [LayerState(c, self.T, self.dev) for _ in range(c.layers)]
+        # shared per-step scratch (steps run in stream order)
+        BHq = self.B * self.Hq
+        self.dsc_ld = self.cap + 1
+        self.dsc = torch.zeros((BHq, self.dsc_ld), dtype=torch.float64, device=self.dev)
+        n_dense = self.B * self.Hkv * math.ceil(self.dsc_ld / DENSE_ROWS)
+        n_sparse = self.B * self.Hkv * math.ceil(self.T / SPARSE_ROWS)
+        self.max_items = n_dense + n_sparse
+        self.part_m = torch.empty(self.max_items * self.G, dtype=torch.float64, device=self.dev)
+        self.part_z = torch.empty(self.max_items * self.G, dtype=torch.float64, device=self.dev)
+        self.part_acc = torch.empty(self.max_items * self.G * self.D, dtype=torch.float32, device=self.dev)
+        self.counter = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self._desc = _lib.DecodeDesc()
+
+    # ------------------------------------------------------------ helpers
+    def _stream(self):
+        return stream_handle(self.dev)
+
+    def _as_dev(self, x, heads):
+        """[B, heads, n, D] (or [heads, n, D] when B == 1) -> contiguous device tensor."""
+        t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))
+        if t.dim() == 3:
+            if self.B != 1:
+                raise ContractError(f"3-D step input needs batch == 1 (batch={self.B})")
+            t = t[None]
+        if tuple(t.shape[:2]) != (self.B, heads) or t.shape[-1] != self.D:
+            raise ContractError(f"step tensor shape {tuple(t.shape)} does not match "
+                                f"({self.B}, {heads}, n, {self.D})")
+        return t.to(device=self.dev, dtype=self.tdtype, non_blocking=True).contiguous()
+
+    def _refresh_selection(self, ls: LayerState):
+        """Padding / top-k and the union lists after the context changed."""
+        n = ls.lo
+        s = self._stream()
+        words = ls.ctx.shape[1]
+        if self.config.selection == "topk":
+            ls.ctx.zero_()
+            if n:
+                topk_mask(ls.maw, min(self.config.topk, n), n=n, out=ls.ctx)
+        if self.g_pad > 1 and n:
+            counts = torch.zeros(self.B * self.Hq, dtype=torch.int64, device=self.dev)
+            _lib.call("hgca_popcount_rows", ls.ctx.data_ptr(), self.B * self.Hq, words, n,
+                      counts.data_ptr(), s)
+            need = torch.zeros_like(counts)
+            _lib.call("hgca_group_need", counts.data_ptr(), self.B, self.Hq, self.g_pad,
+                      need.data_ptr(), s)
+            ls.sel.copy_(ls.ctx)
+            topk_mask(ls.maw, need, n=n, exclude=ls.ctx, out=ls.sel)
+        else:
+            ls.sel.copy_(ls.ctx)
+        _lib.call("hgca_union_build", ls.sel.data_ptr(), self.B, self.Hq, self.Hkv, words, n, self.T,
+                  ls.u_pos.data_ptr(), ls.u_qm.data_ptr(), ls.u_cnt.data_ptr(), ls.item_off.data_ptr(),
+                  SPARSE_ROWS, s)
+
+    def _ingest(self, ls: LayerState, lo, hi, divisor):
+        """StoreTier.ingest_evicted of positions [lo, hi) (sparsifier.py:127-156)."""
+        if self.config.selection == "threshold" and hi > lo:
+            _lib.call("hgca_select_threshold", ls.maw.data_ptr(), self.B * self.Hq, self.T, lo, hi,
+                      float(self.config.cache.beta), int(divisor), ls.ctx.data_ptr(), ls.ctx.shape[1], 0,
+                      self._stream())
+        ls.lo = hi
+        self._refresh_selection(ls)
+
+    def _evict_range(self, ls: LayerState, incoming):
+        """WindowCache.evict_if_full (kv_cache.py:189-221) -> [lo, lo+freed)."""
+        cap, blk = self.cap, self.config.cache.blk_size
+        if incoming < 0:
+            raise ContractError("incoming_count must be >= 0")
+        if incoming > cap:
+            raise ContractError(f"a single step of {incoming} entries exceeds the whole window ({cap}); unsupported")
+        size = ls.window_size
+        l_cur = size + incoming
+        if l_cur < cap:
+            return ls.lo, ls.lo
+        n_blocks = math.ceil((l_cur - cap + 1) / blk)
+        full_blocks = size // blk
+        n_blocks = min(n_blocks, full_blocks)
+        freed = n_blocks * blk
+        if cap - (size - freed) < incoming:
+            raise ContractError(f"cannot free room for {incoming} entries: only {full_blocks} full blocks are evictable")
+        return ls.lo, ls.lo + freed
+
+    # ------------------------------------------------------------ staging
+    def bulk_ingest(self, layer_idx, keys, values, maw, divisor):
+        """Archive n positions at once: StoreTier.ingest_evicted(blocks, beta,
+        window_size=divisor) with the blocks' keys/values/MAW given directly
+        (sparsifier.py:127-156). keys/values [B, Hkv, n, D], maw [B, Hq, n].
+        Requires an empty window (stages long contexts)."""
+        ls = self.layers[layer_idx]
+        if ls.window_size:
+            raise ContractError("bulk_ingest requires an empty window")
+        k = self._as_dev(keys, self.Hkv)
+        v = self._as_dev(values, self.Hkv)
+        n = k.shape[2]
+        if ls.nxt + n > self.T:
+            raise ContractError("max_positions exceeded")
+        m = maw if isinstance(maw, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(maw))
+        m = m.to(device=self.dev, dtype=torch.float64).reshape(self.B * self.Hq, n)
+        p0 = ls.nxt
+        _lib.call("hgca_write_rows", self.dcode, ls.K.data_ptr(), ls.V.data_ptr(), self.B * self.Hkv,
+                  self.T, self.D, p0, k.data_ptr(), v.data_ptr(), n, self._stream())
+        ls.maw[:, p0:p0 + n].copy_(m)
+        ls.nxt = p0 + n
+        self._ingest(ls, p0, p0 + n, divisor)
+
+    # ------------------------------------------------------------ steps
+    def step(self, layer_idx: int, inp: StepInput) -> StepOutput:
+        if inp.mode == "decode":
+            return self.decode_step(layer_idx, inp)
+        return self.append_step(layer_idx, inp)
+
+    def decode_step(self, layer_idx: int, inp: StepInput) -> StepOutput:
+        if inp.mode != "decode":
+            raise ContractError(f"decode_step got mode {inp.mode!r}")
+        return self._decode(layer_idx, inp)
+
+    def append_step(self, layer_idx: int, inp: StepInput) -> StepOutput:
+        if inp.mode != "append":
+            raise ContractError(f"append_step got mode {inp.mode!r}")
+        return self._append(layer_idx, inp)
+
+    def _decode(self, layer_idx, inp, out=None, lse=None):
+        ls = self.layers[layer_idx]
+        squeeze = inp.q.ndim == 3
+        q = self._as_dev(inp.q, self.Hq)
+        k = self._as_dev(inp.keys, self.Hkv)
+        v = self._as_dev(inp.values, self.Hkv)
+        o, l, w = self.decode_device(layer_idx, q, k, v, out=out, lse=lse)
+        o = o.view(self.B, self.Hq, 1, self.D)
+        l = l.view(self.B, self.Hq, 1)
+        if w is not None:
+            w = w.view(self.B, self.Hq, 1, -1)
+        if squeeze:
+            o, l = o[0], l[0]
+            w = w[0] if w is not None else None
+        return StepOutput(o, l, w, None, self._last_dense_positions)
+
+    def decode_device(self, layer_idx, q, k, v, out=None, lse=None, wts=None):
+        """The decode hot path on device tensors: q [B, Hq, 1, D], k/v
+        [B, Hkv, 1, D] (storage dtype). Returns (out [B*Hq, D] f32,
+        lse [B*Hq] f64, a_gpu or None). Launches only; no host sync."""
+        ls = self.layers[layer_idx]
+        s = self._stream()
+        if ls.nxt + 1 > self.T:
+            raise ContractError("max_positions exceeded")
+        # kv_in lands at position nxt before the dense pass (append_kv's slot)
+        _lib.call("hgca_write_rows", self.dcode, ls.K.data_ptr(), ls.V.data_ptr(), self.B * self.Hkv,
+                  self.T, self.D, ls.nxt, k.data_ptr(), v.data_ptr(), 1, s)
+        w_size = ls.window_size
+        W = w_size + 1
+        BHq = self.B * self.Hq
+        if out is None:
+            out = torch.empty((BHq, self.D), dtype=torch.float32, device=self.dev)
+        if lse is None:
+            lse = torch.empty(BHq, dtype=torch.float64, device=self.dev)
+        if wts is None and self.config.keep_weights:
+            wts = torch.empty((BHq, W), dtype=torch.float32, device=self.dev)
+        d = self._desc
+        d.dtype = self.dcode
+        d.B, d.Hq, d.Hkv, d.D, d.T = self.B, self.Hq, self.Hkv, self.D, self.T
+        d.K, d.V, d.q = ls.K.data_ptr(), ls.V.data_ptr(), q.data_ptr()
+        d.scale = float(self.shape.scale)
+        d.dlo, d.dhi, d.w_old = ls.lo, ls.nxt + 1, w_size
+        d.dense_rows, d.sparse_rows = DENSE_ROWS, SPARSE_ROWS
+        d.u_pos, d.u_qm, d.u_cnt, d.item_off = (ls.u_pos.data_ptr(), ls.u_qm.data_ptr(),
+                                                ls.u_cnt.data_ptr(), ls.item_off.data_ptr())
+        d.dsc, d.dsc_ld = self.dsc.data_ptr(), self.dsc_ld
+        d.part_m, d.part_z, d.part_acc = self.part_m.data_ptr(), self.part_z.data_ptr(), self.part_acc.data_ptr()
+        d.max_items = self.max_items
+        d.counter = self.counter.data_ptr()
+        d.maw, d.alpha = ls.maw.data_ptr(), float(self.config.cache.alpha)
+        d.out, d.lse = out.data_ptr(), lse.data_ptr()
+        d.wts_out = wts.data_ptr() if wts is not None else None
+        d.out_sparse = None
+        d.lse_sparse = None
+        _lib.call("hgca_decode_step", d, s)
+        self._last_dense_positions = np.arange(ls.lo, ls.nxt + 1, dtype=np.int64)
+        # maintenance after the merge (engine.py:175-191): EMA + init done in
+        # the merge kernel; eviction/offload here; append_kv = the position move.
+        ev_lo, ev_hi = self._evict_range(ls, 1)
+        ls.nxt += 1
+        if ev_hi > ev_lo:
+            self._ingest(ls, ev_lo, ev_hi, w_size + 1)
+        return out, lse, wts
+
+    def _append(self, layer_idx, inp):
+        """Append step (engine.py:111-114 -> _run_step with the full archive)."""
+        ls = self.layers[layer_idx]
+        squeeze = inp.q.ndim == 3
+        q = self._as_dev(inp.q, self.Hq)
+        k = self._as_dev(inp.keys, self.Hkv)
+        v = self._as_dev(inp.values, self.Hkv)
+        nq = q.shape[2]
+        s = self._stream()
+        if ls.nxt + nq > self.T:
+            raise ContractError("max_positions exceeded")
+        _lib.call("hgca_write_rows", self.dcode, ls.K.data_ptr(), ls.V.data_ptr(), self.B * self.Hkv,
+                  self.T, self.D, ls.nxt, k.data_ptr(), v.data_ptr(), nq, s)
+        BHq = self.B * self.Hq
+        lo, nxt = ls.lo, ls.nxt
+        w_size = nxt - lo
+        W = w_size + nq
+        odt = torch.float32
+        # sparse partial over the whole archive, with weights (engine.py:127-132)
+        s_out = torch.zeros((BHq, nq, self.D), dtype=odt, device=self.dev)
+        s_lse = torch.full((BHq, nq), -math.inf, dtype=torch.float64, device=self.dev)
+        a_cpu = None
+        if lo:
+            a_cpu = torch.empty((BHq, nq, lo), dtype=odt, device=self.dev)
+            ws = torch.empty(BHq * nq * lo, dtype=torch.float64, device=self.dev)
+            _lib.call("hgca_attend_gqa", self.dcode, q.data_ptr(), ls.K.data_ptr(), ls.V.data_ptr(),
+                      self.B, self.Hq, self.Hkv, self.T, 0, lo, nq, self.D, float(self.shape.scale),
+                      s_out.data_ptr(), s_lse.data_ptr(), a_cpu.data_ptr(), lo, ws.data_ptr(), s)
+        # dense over window + kv_in (engine.py:161-164)
+        d_out = torch.empty((BHq, nq, self.D), dtype=odt, device=self.dev)
+        d_lse = torch.empty((BHq, nq), dtype=torch.float64, device=self.dev)
+        a_gpu = torch.empty((BHq, nq, W), dtype=odt, device=self.dev)
+        ws = torch.empty(BHq * nq * W, dtype=torch.float64, device=self.dev)
+        _lib.call("hgca_attend_gqa", self.dcode, q.data_ptr(), ls.K.data_ptr(), ls.V.data_ptr(),
+                  self.B, self.Hq, self.Hkv, self.T, lo, W, nq, self.D, float(self.shape.scale),
+                  d_out.data_ptr(), d_lse.data_ptr(), a_gpu.data_ptr(), W, ws.data_ptr(), s)
+        # merge (engine.py:166-169)
+        out = torch.empty_like(d_out)
+        lse = torch.empty_like(d_lse)
+        _lib.call("hgca_merge_states", _lib.DTYPE_F32, s_out.data_ptr(), s_lse.data_ptr(), d_out.data_ptr(),
+                  d_lse.data_ptr(), BHq * nq, self.D, out.data_ptr(), lse.data_ptr(), None, None, 0, 0,
+                  None, s)
+        # maintenance (engine.py:175-186)
+        _lib.call("hgca_maw_update", a_gpu.data_ptr(), BHq, nq, W, W, ls.maw.data_ptr(), self.T, lo, w_size,
+                  float(self.config.cache.alpha), 0, s)
+        ev_lo, ev_hi = self._evict_range(ls, nq)
+        if lo:
+            # StoreTier.reevaluate(mean_rows(a_cpu), beta) (sparsifier.py:158-177)
+            _lib.call("hgca_maw_update", a_cpu.data_ptr(), BHq, nq, lo, lo, ls.maw.data_ptr(), self.T, 0, 0,
+                      float(self.config.cache.alpha), 1, s)
+            if self.config.selection == "threshold":
+                _lib.call("hgca_select_threshold", ls.maw.data_ptr(), BHq, self.T, 0, lo,
+                          float(self.config.cache.beta), int(lo), ls.ctx.data_ptr(), ls.ctx.shape[1], 1, s)
+        if ev_hi > ev_lo:
+            self._ingest(ls, ev_lo, ev_hi, w_size + nq)
+        elif lo:
+            self._refresh_selection(ls)
+        if ls.window_size + nq > self.cap:
+            raise ContractError(f"append of {nq} entries overflows window capacity {self.cap}")
+        ls.nxt += nq
+        o = out.view(self.B, self.Hq, nq, self.D)
+        l = lse.view(self.B, self.Hq, nq)
+        ag = a_gpu.view(self.B, self.Hq, nq, W)
+        if squeeze:
+            o, l, ag = o[0], l[0], ag[0]
+        return StepOutput(o, l, ag, a_cpu, np.arange(lo, nxt + nq, dtype=np.int64))
+
+    # ------------------------------------------------------------ inspection
+    def context_indices(self, layer_idx=0):
+        """Per (b*Hq + h) context-cache index lists (sparsifier.py ContextCache.indices)."""
+        ls = self.layers[layer_idx]
+        return mask_to_lists(ls.ctx, ls.lo)
+
+    def store_entries(self, layer_idx=0):
+        """Per (b*Hq + h) attended archive entries (context + padding) and flags."""
+        ls = self.layers[layer_idx]
+        return mask_to_lists(ls.ctx, ls.lo, mask_b=ls.sel, want_flags=True)
+
+    def maw_host(self, layer_idx=0):
+        ls = self.layers[layer_idx]
+        return ls.maw[:, : ls.nxt].cpu().numpy()
+

@@ -1,0 +1,171 @@
+"""Store-tier selection on the B200 (tierkv/sparsifier.py:32-42, 198-235).
+
+Selections are kept on the device as per-head bit masks ([rows, words]
+uint32, bit p = archive position p): the strict threshold rule fills a mask
+in one pass, padding / top-k are a radix select over the fp64 MAW keyed by
+(maw descending, position ascending), and index lists are a compaction of
+the mask. The list-returning functions here keep the reference signatures.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._dev import as_device, device, stream_handle
+from .errors import ContractError
+
+__all__ = ["HeadGroupTask", "select_salient", "select_topk", "pack_head_groups", "group_size",
+           "indices_to_mask", "mask_to_lists", "words_for"]
+
+
+def words_for(n: int) -> int:
+    return max(1, (int(n) + 31) // 32)
+
+
+def group_size(batch: int, heads: int, core_count: int) -> int:
+    """sparsifier.py:209."""
+    return max(1, int(batch * heads / core_count + 0.5))
+
+
+@dataclass
+class HeadGroupTask:
+    """sparsifier.py:90-102."""
+
+    heads: list
+    entries: list
+    padding: list = field(default_factory=list)
+
+
+def _maw_dev(maw):
+    t, is_np = as_device(maw)
+    t = t.to(torch.float64)
+    if t.dim() != 2:
+        raise ContractError(f"maw must be [num_heads, n], got {tuple(t.shape)}")
+    return t.contiguous(), is_np
+
+
+def threshold_mask(maw_t, beta, divisor, p0=0, p1=None, mask=None, assign=True):
+    """Device mask of maw > beta/divisor over [p0, p1) (sparsifier.py:41-42)."""
+    rows, n = maw_t.shape
+    p1 = n if p1 is None else p1
+    words = words_for(n)
+    if mask is None:
+        mask = torch.zeros((rows, words), dtype=torch.int32, device=maw_t.device)
+    _lib.call("hgca_select_threshold", maw_t.data_ptr(), rows, maw_t.stride(0), p0, p1, float(beta),
+              int(divisor), mask.data_ptr(), mask.shape[1], int(assign), stream_handle(maw_t.device))
+    return mask
+
+
+def mask_to_lists(mask_a, n, mask_b=None, want_flags=False):
+    """Compact masks (a | b) over [0, n) into per-row ascending int64 lists."""
+    rows = mask_a.shape[0]
+    dev = mask_a.device
+    idx = torch.empty((rows, max(n, 1)), dtype=torch.int64, device=dev)
+    cnt = torch.zeros(rows, dtype=torch.int64, device=dev)
+    flags = torch.empty((rows, max(n, 1)), dtype=torch.uint8, device=dev) if want_flags else None
+    if rows:
+        _lib.call("hgca_mask_to_indices", mask_a.data_ptr(), mask_b.data_ptr() if mask_b is not None else None,
+                  rows, mask_a.shape[1], n, idx.data_ptr(), idx.shape[1],
+                  flags.data_ptr() if flags is not None else None, cnt.data_ptr(), stream_handle(dev))
+    cnt_h = cnt.cpu().numpy()
+    idx_h = idx.cpu().numpy()
+    lists = [idx_h[r, : cnt_h[r]].copy() for r in range(rows)]
+    if not want_flags:
+        return lists
+    fl_h = flags.cpu().numpy().astype(bool)
+    return lists, [fl_h[r, : cnt_h[r]].copy() for r in range(rows)]
+
+
+def indices_to_mask(index_lists, n, dev=None):
+    """Per-row index lists -> device bit mask [rows, words] (host packing)."""
+    rows = len(index_lists)
+    words = words_for(n)
+    bits = np.zeros((rows, words * 32), dtype=bool)
+    for r, idx in enumerate(index_lists):
+        idx = np.asarray(idx.detach().cpu() if isinstance(idx, torch.Tensor) else idx, dtype=np.int64)
+        if idx.size:
+            bits[r, idx] = True
+    packed = np.packbits(bits, axis=1, bitorder="little").view(np.uint32).view(np.int32)
+    return torch.from_numpy(np.ascontiguousarray(packed)).to(dev or device())
+
+
+def _out(lists, like_numpy, dev):
+    if like_numpy:
+        return [a.astype(np.int64) for a in lists]
+    return [torch.from_numpy(a).to(dev) for a in lists]
+
+
+def select_salient(maw, beta: float, divisor: int):
+    """Per-head sorted int64 indices with maw > beta/divisor (sparsifier.py:32-42)."""
+    if divisor < 1:
+        raise ContractError(f"divisor must be >= 1, got {divisor}")
+    maw_t, is_np = _maw_dev(maw)
+    n = maw_t.shape[1]
+    mask = threshold_mask(maw_t, beta, divisor)
+    return _out(mask_to_lists(mask, n), is_np, maw_t.device)
+
+
+def topk_mask(maw_t, k, n=None, exclude=None, out=None):
+    """OR into `out` the top-k[row] of [0, n) by (maw desc, position asc), skipping `exclude`."""
+    rows, ld = maw_t.shape
+    n = ld if n is None else n
+    dev = maw_t.device
+    if out is None:
+        out = torch.zeros((rows, words_for(ld)), dtype=torch.int32, device=dev)
+    if not isinstance(k, torch.Tensor):
+        k = torch.as_tensor(np.broadcast_to(np.asarray(k, dtype=np.int64), (rows,)).copy())
+    k = k.to(device=dev, dtype=torch.int64).contiguous()
+    if rows and n:
+        _lib.call("hgca_select_topk", maw_t.data_ptr(), rows, maw_t.stride(0), n, k.data_ptr(),
+                  exclude.data_ptr() if exclude is not None else None, out.data_ptr(), out.shape[1],
+                  stream_handle(dev))
+    return out
+
+
+def select_topk(maw, k: int):
+    """F1 extension: per head the k highest-MAW entries, ties by
+    ascending position (the order of sparsifier.py:224-225), sorted."""
+    maw_t, is_np = _maw_dev(maw)
+    mask = topk_mask(maw_t, int(k))
+    return _out(mask_to_lists(mask, maw_t.shape[1]), is_np, maw_t.device)
+
+
+def pack_head_groups(store, batch: int, core_count: int) -> list:
+    """sparsifier.py:198-235 on the device.
+
+    `store` is duck-typed like the reference StoreTier: `.shape.num_heads`,
+    `.context.indices` (per-head position-sorted lists), `.maw` [H, N] and
+    `.archive_size`. Each head is padded up to its group's longest selection
+    with its own highest-MAW below-threshold entries (ties by position).
+    """
+    if core_count < 1:
+        raise ContractError(f"core_count must be >= 1, got {core_count}")
+    h = store.shape.num_heads
+    g = group_size(batch, h, core_count)
+    n = int(store.archive_size)
+    dev = device()
+    if n == 0:
+        empty = np.zeros(0, np.int64)
+        return [HeadGroupTask(heads=list(range(lo, min(lo + g, h))),
+                              entries=[empty.copy() for _ in range(lo, min(lo + g, h))],
+                              padding=[np.zeros(0, bool) for _ in range(lo, min(lo + g, h))])
+                for lo in range(0, h, g)]
+    ctx = indices_to_mask(store.context.indices, n, dev)
+    maw_t, _ = _maw_dev(store.maw)
+    maw_t = maw_t[:, :n].contiguous()
+    counts = torch.zeros(h, dtype=torch.int64, device=dev)
+    _lib.call("hgca_popcount_rows", ctx.data_ptr(), h, ctx.shape[1], n, counts.data_ptr(), stream_handle(dev))
+    need = torch.zeros(h, dtype=torch.int64, device=dev)
+    _lib.call("hgca_group_need", counts.data_ptr(), 1, h, g, need.data_ptr(), stream_handle(dev))
+    pad = topk_mask(maw_t, need, n=n, exclude=ctx)
+    lists, flags = mask_to_lists(ctx, n, mask_b=pad, want_flags=True)
+    tasks = []
+    for lo in range(0, h, g):
+        heads = list(range(lo, min(lo + g, h)))
+        tasks.append(HeadGroupTask(heads=heads, entries=[lists[x] for x in heads],
+                                   padding=[flags[x] for x in heads]))
+    return tasks

@@ -1,0 +1,178 @@
+"""Generate the golden fixtures in tests/golden/ by running the REFERENCE
+package (tierkv, /root/reference/pkg) with its compiled Cython backend.
+
+Run in the build container only (the reference does not exist on the GPU
+box); the resulting .npz files are committed. Usage:
+
+    python tests/golden/make_golden.py [--ref-src /tmp/refbuild/pkg/src]
+
+If --ref-src has no built tierkv._core, the reference package is copied to
+/tmp/refbuild and built there (`python setup.py build_ext --inplace`);
+/root/reference itself is never written to.
+"""
+
+from __future__ import annotations
+
+import argparse
+import glob
+import hashlib
+import os
+import shutil
+import subprocess
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def ensure_ref(src):
+    if glob.glob(os.path.join(src, "tierkv", "_core*.so")):
+        return src
+    pkg = "/tmp/refbuild/pkg"
+    if not os.path.exists(pkg):
+        os.makedirs("/tmp/refbuild", exist_ok=True)
+        shutil.copytree("/root/reference/pkg", pkg)
+    subprocess.run([sys.executable, "setup.py", "build_ext", "--inplace"], cwd=pkg, check=True,
+                   capture_output=True)
+    return os.path.join(pkg, "src")
+
+
+def kernels(tk, out):
+    """Reference outputs for the kernel cases of tests/golden/cases.py (inputs
+    are regenerated from per-case seeds, so only outputs are stored)."""
+    from cases import DENSE_CASES, INDEXED_CASES, dense_inputs, indexed_inputs
+
+    be = tk.backends.get_backend("compiled")
+    rec = {}
+    for key in DENSE_CASES:
+        q, k, v, scale = dense_inputs(key)
+        o, l, w = be.attend_dense(q, k, v, scale, True)
+        rec.update({f"{key}_out": o, f"{key}_lse": l, f"{key}_w": w})
+    for key in INDEXED_CASES:
+        q, k, v, idx, scale = indexed_inputs(key)
+        o, l, w = be.attend_indexed(q, k, v, idx, scale, True)
+        rec.update({f"{key}_out": o, f"{key}_lse": l, f"{key}_w": w})
+    rng = np.random.default_rng(0xC0FFEE)
+    # merge_states: random partitions at magnitudes {1, 10, 1e3} (test_attention.py:238-262)
+    for ci, mag in enumerate((1.0, 10.0, 1e3)):
+        H, n, d = 3, 24, 16
+        q = mag * rng.standard_normal((H, 2, d))
+        k = rng.standard_normal((H, n, d))
+        v = rng.standard_normal((H, n, d))
+        cut = 9
+        shape = tk.HeadShape(H, d)
+        a = tk.attend(q, k[:, :cut], v[:, :cut], shape, keep_weights=True)
+        b = tk.attend(q, k[:, cut:], v[:, cut:], shape, keep_weights=True)
+        m = tk.merge_states(a, b)
+        key = f"merge{ci}"
+        rec.update({f"{key}_oa": a.output, f"{key}_la": a.lse, f"{key}_wa": a.weights,
+                    f"{key}_ob": b.output, f"{key}_lb": b.lse, f"{key}_wb": b.weights,
+                    f"{key}_out": m.output, f"{key}_lse": m.lse, f"{key}_w": m.weights})
+    np.savez_compressed(out, **rec)
+
+
+def selection(tk, out):
+    rng = np.random.default_rng(2027)
+    rec = {}
+    # select_salient: random rows incl. exact ties at the threshold
+    maw = rng.random((4, 300))
+    maw[:, ::7] = 1.0 / 13.0
+    for i, (beta, div) in enumerate([(1.0, 13), (0.5, 40), (0.0, 5), (2.0, 300)]):
+        sel = tk.select_salient(maw, beta, div)
+        rec[f"sal{i}_maw"] = maw
+        rec[f"sal{i}_beta"] = np.array(beta)
+        rec[f"sal{i}_div"] = np.array(div)
+        rec[f"sal{i}_mask"] = np.stack([np.isin(np.arange(300), s) for s in sel])
+    # pack_head_groups over a StoreTier with quantized MAW (many exact ties)
+    shape = tk.HeadShape(8, 4)
+    for i, (cores, batch, n) in enumerate([(1, 1, 200), (2, 1, 333), (4, 3, 64), (8, 1, 50)]):
+        st = tk.StoreTier(shape)
+        mw = np.round(rng.random((8, n)) * 20) / 20 * rng.choice([0.0, 1.0], size=(8, n), p=[0.2, 0.8])
+        kv = np.zeros((8, n, 4), np.float32)
+        blk = tk.KvBlock(keys=kv, values=kv.copy(), maw=mw, start=0, occupancy=n)
+        st.ingest_evicted([blk], beta=1.0, window_size=int(rng.integers(2, 12)))
+        tasks = tk.pack_head_groups(st, batch=batch, core_count=cores)
+        ent = np.zeros((8, n), bool)
+        pad = np.zeros((8, n), bool)
+        for t in tasks:
+            for hd, e, p in zip(t.heads, t.entries, t.padding):
+                ent[hd, e] = True
+                pad[hd, e[p]] = True
+        ctx = np.stack([np.isin(np.arange(n), st.context.indices[h]) for h in range(8)])
+        rec.update({f"pack{i}_maw": st.maw, f"pack{i}_ctx": ctx, f"pack{i}_entries": ent,
+                    f"pack{i}_padding": pad, f"pack{i}_cores": np.array(cores),
+                    f"pack{i}_batch": np.array(batch)})
+    np.savez_compressed(out, **rec)
+
+
+ENGINE_CASES = {
+    # name: (layers, heads, head_dim, blk_num, blk_size, alpha, beta, core_count, spec kwargs, stride)
+    "e1_g1": (1, 4, 64, 4, 16, 0.5, 1.0, 8, dict(seed=7, steps=300, prefill_len=16), 1),
+    "e2_pad": (1, 4, 64, 4, 16, 0.5, 1.0, 1, dict(seed=7, steps=300, prefill_len=16,
+                                                   append_events=((150, 8),)), 1),
+    "e3_d128": (1, 8, 128, 8, 32, 0.5, 0.5, 8, dict(seed=11, steps=400, prefill_len=64,
+                                                    append_events=((200, 16),)), 10),
+}
+
+
+def engine(tk, out):
+    rec = {}
+    for name, (L, H, d, bn, bs, alpha, beta, cores, spec_kw, stride) in ENGINE_CASES.items():
+        cfg = tk.EngineConfig(layers=L, heads=H, head_dim=d,
+                              cache=tk.CacheConfig(blk_num=bn, blk_size=bs, alpha=alpha, beta=beta),
+                              core_count=cores)
+        wl = tk.gen_workload(tk.WorkloadSpec(**spec_kw), cfg.head_shape, cfg.layers)
+        eng, outs = tk.run_sequence(cfg, wl, collect=True)
+        sel = [i for i in range(len(outs)) if i % stride == 0 or i == len(outs) - 1]
+        o = np.stack([np.ascontiguousarray(outs[i][0].output[:, -1, :]) for i in sel])
+        l = np.stack([outs[i][0].lse[:, -1] for i in sel])
+        st = eng.layers[0].store
+        win = eng.layers[0].window
+        n = st.archive_size
+        ctx = np.stack([np.isin(np.arange(n), st.context.indices[h]) for h in range(H)])
+        rec.update({f"{name}_steps": np.array(sel), f"{name}_out": o, f"{name}_lse": l,
+                    f"{name}_store_maw": st.maw, f"{name}_window_maw": win.maw_matrix(),
+                    f"{name}_ctx": ctx, f"{name}_sizes": np.array([win.size, n])})
+    np.savez_compressed(out, **rec)
+
+
+def workload(tk, out):
+    rec = {}
+    spec = tk.WorkloadSpec(seed=3, steps=40, prefill_len=8, append_events=((20, 4),))
+    wl = tk.gen_workload(spec, tk.HeadShape(2, 8), 2)
+    rec["small_q"] = np.concatenate([s.q for s in wl], axis=2)
+    rec["small_k"] = np.concatenate([s.keys for s in wl], axis=2)
+    rec["small_v"] = np.concatenate([s.values for s in wl], axis=2)
+    spec = tk.WorkloadSpec(seed=7, steps=3968, prefill_len=128)
+    wl = tk.gen_workload(spec, tk.HeadShape(32, 128), 1)
+    h = hashlib.sha256()
+    for s in wl:
+        h.update(s.q.tobytes())
+        h.update(s.keys.tobytes())
+        h.update(s.values.tobytes())
+    rec["c1_sha256"] = np.frombuffer(h.digest(), dtype=np.uint8)
+    np.savez_compressed(out, **rec)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--ref-src", default="/tmp/refbuild/pkg/src")
+    args = ap.parse_args()
+    src = ensure_ref(args.ref_src)
+    sys.path.insert(0, src)
+    sys.path.insert(0, HERE)
+    os.environ["TIERKV_BACKEND"] = "compiled"
+    import tierkv as tk
+
+    assert tk.backends.active.name == "compiled"
+    kernels(tk, os.path.join(HERE, "kernels.npz"))
+    selection(tk, os.path.join(HERE, "selection.npz"))
+    engine(tk, os.path.join(HERE, "engine.npz"))
+    workload(tk, os.path.join(HERE, "workload.npz"))
+    for f in sorted(glob.glob(os.path.join(HERE, "*.npz"))):
+        print(f, os.path.getsize(f))
+
+
+if __name__ == "__main__":
+    main()
