@@ -1,0 +1,333 @@
+#!/usr/bin/env python
+"""Hybrid decode-attention benchmark (BASELINE.json metric).
+
+Workload (N=1): BASELINE.json configs[1] = "C2": Llama-3-8B GQA shape
+(32 query / 8 KV heads, d=128), batch 16, 32K context, bf16, one attention
+layer; 512-token dense window (16 blocks x 32) + per-head threshold-selected
+context over the 32,256-entry archive with ~10% of entries per query head
+selected (SURVEY.md §8(d) Config 2). A "step" is one decode layer-step of the
+whole batch through the device engine: kv_in write, fused dense + sparse
+partial kernel, merge + MAW EMA kernel, and (every 32 steps) eviction ->
+ingest -> union rebuild. tokens/s = batch / step time.
+
+value : inputs resident in HBM, CUDA events on the launching stream.
+e2e   : the same step through HybridEngine.decode_host (C ABI) with pinned HOST
+        q/k/v copied in and out/lse copied back + synchronized every step.
+L2    : K/V (2.1 GB) >> L2 (126 MB): inputs larger than L2, no flush needed.
+
+--impl reference: the reference's own CPU hot path (oracle/_ref compiled from
+the reference's _core.pyx, else the oracle's C restatement) on every host
+core, same workload/metric (bench arm for the driver's ratio).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+C2 = dict(batch=16, heads=32, kv_heads=8, head_dim=128, context=32768, blk_num=16, blk_size=32,
+          beta=1.0, alpha=0.5, frac=0.10, dtype="bfloat16")
+WORKLOAD = ("C2: Llama-3-8B GQA 32q/8kv d128, batch 16, 32K context, bf16, 512-token dense window "
+            "+ threshold-selected 10%/head archive context, 1 layer")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the GPU is busy."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        time.sleep(0.05)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append((time.perf_counter(), [x.strip() for x in line.split(",")]))
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self, t0, t1):
+        rows = [r for t, r in self.rows if t0 <= t <= t1] or [r for _, r in self.rows]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[3:7]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ----------------------------------------------------------------- ours
+def stage_engine(hg, torch, cfgd, max_positions, seed=0):
+    """Build the engine and stage a 32K context: bulk-ingest the archive with
+    MAW drawn so that ~frac of entries per query head pass beta/divisor, then
+    decode until the window reaches its steady state."""
+    B, Hq, Hkv, D = cfgd["batch"], cfgd["heads"], cfgd["kv_heads"], cfgd["head_dim"]
+    cap = cfgd["blk_num"] * cfgd["blk_size"]
+    cfg = hg.EngineConfig(layers=1, heads=Hq, kv_heads=Hkv, head_dim=D, batch=B, dtype=cfgd["dtype"],
+                          cache=hg.CacheConfig(blk_num=cfgd["blk_num"], blk_size=cfgd["blk_size"],
+                                               alpha=cfgd["alpha"], beta=cfgd["beta"]),
+                          core_count=10 ** 6, max_positions=max_positions)
+    eng = hg.HybridEngine(cfg)
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    tdt = eng.tdtype
+    n_arch = cfgd["context"] - cap
+    k = torch.randn((B, Hkv, n_arch, D), generator=g, device="cuda").to(tdt)
+    v = torch.randn((B, Hkv, n_arch, D), generator=g, device="cuda").to(tdt)
+    divisor = cap
+    thr = cfgd["beta"] / divisor
+    u = torch.rand((B, Hq, n_arch), generator=g, device="cuda", dtype=torch.float64)
+    maw = torch.where(u < cfgd["frac"], thr * (1.0 + u), thr * u)
+    eng.bulk_ingest(0, k, v, maw, divisor)
+    del k, v, u, maw
+    for _ in range(cap - 1):
+        q = torch.randn((B, Hq, 1, D), generator=g, device="cuda").to(tdt)
+        kk = torch.randn((B, Hkv, 1, D), generator=g, device="cuda").to(tdt)
+        eng.decode_device(0, q, kk, kk)
+    torch.cuda.synchronize()
+    return eng, g
+
+
+def partial_bytes(eng, W_avg, U_avg):
+    """Algorithmic HBM bytes of one decode_partial launch:
+    dense K+V rows, unique union K+V rows + their (pos, mask) entries, the
+    queries, the dense fp64 scores and the per-item partials written."""
+    B, Hq, Hkv, D, G = eng.B, eng.Hq, eng.Hkv, eng.D, eng.G
+    e = 2 if eng.tdtype.itemsize == 2 else 4
+    dense = B * Hkv * W_avg * D * 2 * e
+    sparse = U_avg * (D * 2 * e + 5)
+    q = B * Hq * D * e
+    dsc = B * Hq * W_avg * 8
+    items = B * Hkv * (math.ceil(W_avg / 512) + U_avg / (B * Hkv) / 512)
+    partials = items * G * (D * 4 + 16)
+    return dense + sparse + q + dsc + partials, dense, sparse
+
+
+def run_ours(args, rank, world):
+    import numpy as np
+    import torch
+
+    import paper_2507_03153_b200 as hg
+
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist  # noqa: F811
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfgd = dict(C2)
+    K, Wm = args.steps, args.warmup
+    e2e_steps = args.e2e_steps if args.e2e_steps is not None else min(K, 200)
+    cap = cfgd["blk_num"] * cfgd["blk_size"]
+    max_positions = cfgd["context"] + Wm + K + e2e_steps + 64
+    clocks = ClockSampler(local)
+    clocks.start()
+    eng, g = stage_engine(hg, torch, cfgd, max_positions, seed=1234 + rank)
+    B, Hq, Hkv, D = eng.B, eng.Hq, eng.Hkv, eng.D
+    tdt = eng.tdtype
+    qs = torch.randn((Wm + K, B, Hq, 1, D), generator=g, device="cuda").to(tdt)
+    ks = torch.randn((Wm + K, B, Hkv, 1, D), generator=g, device="cuda").to(tdt)
+    vs = torch.randn((Wm + K, B, Hkv, 1, D), generator=g, device="cuda").to(tdt)
+    out = torch.empty((B * Hq, D), dtype=torch.float32, device="cuda")
+    lse = torch.empty(B * Hq, dtype=torch.float64, device="cuda")
+    ls = eng.layers[0]
+    for i in range(Wm):
+        eng.decode_device(0, qs[i], ks[i], vs[i], out=out, lse=lse)
+    torch.cuda.synchronize()
+    U0 = int(ls.u_cnt.sum())
+    Ws = []
+    eng.partial_events = []
+    launches0 = eng.launches
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_wall0 = time.perf_counter()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(Wm, Wm + K):
+        Ws.append(ls.window_size + 1)
+        eng.decode_device(0, qs[i], ks[i], vs[i], out=out, lse=lse)
+    e1.record()
+    torch.cuda.synchronize()
+    t_wall1 = time.perf_counter()
+    if dist:
+        dist.barrier()
+    launches = eng.launches - launches0
+    ms = e0.elapsed_time(e1) / K
+    part_ms = statistics.mean(a.elapsed_time(b) for a, b in eng.partial_events)
+    eng.partial_events = None
+    U1 = int(ls.u_cnt.sum())
+    ms_max = ms
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t)
+    # ---- e2e through the C ABI with host buffers
+    qh = torch.empty((B, Hq, 1, D), dtype=tdt).pin_memory()
+    kh = torch.empty((B, Hkv, 1, D), dtype=tdt).pin_memory()
+    vh = torch.empty((B, Hkv, 1, D), dtype=tdt).pin_memory()
+    qh.copy_(qs[0].cpu())
+    kh.copy_(ks[0].cpu())
+    vh.copy_(vs[0].cpu())
+    oh = torch.empty((B * Hq, D), dtype=torch.float32).pin_memory()
+    lh = torch.empty(B * Hq, dtype=torch.float64).pin_memory()
+    staging = (torch.empty_like(qs[0]), torch.empty_like(ks[0]), torch.empty_like(vs[0]))
+    for _ in range(3):
+        eng.decode_host(0, qh, kh, vh, oh, lh, staging)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        eng.decode_host(0, qh, kh, vh, oh, lh, staging)
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / max(e2e_steps, 1)
+    if dist:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t)
+    clocks.stop()
+    if not np.isfinite(oh.numpy()).all():
+        raise RuntimeError("non-finite decode output")
+    # ---- roofline of the dominant kernel (decode_partial)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = peaks.get("hbm_gbs", 6650.0)
+    W_avg = statistics.mean(Ws)
+    U_avg = (U0 + U1) / 2
+    pbytes, dense_b, sparse_b = partial_bytes(eng, W_avg, U_avg)
+    achieved = pbytes / (part_ms * 1e-3) / 1e9
+    result = None
+    if rank == 0:
+        tok_s = world * B / (ms_max * 1e-3)
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            from oracle import cpu_bench  # checker / baseline only
+            cpu = cpu_bench.time_single(Hq, Hkv, D, cfgd["context"] - cap, cap, cfgd["frac"],
+                                        sequences=4, reps=4)
+        result = {
+            "metric": "hybrid-attn decode tokens/s (1 layer, C2)",
+            "value": round(tok_s, 1),
+            "unit": "tokens/s",
+            "n_gpus": world,
+            "steps": K,
+            "warmup": Wm,
+            "ms_per_step": round(ms_max, 5),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "bf16 storage; fp64 QK scores + fp64 softmax stats, fp32 P.V",
+            "data": "synthetic (torch.randn K/V/q, MAW drawn for 10% threshold selection per query head)",
+            "config": {"workload": WORKLOAD, "batch": B, "q_heads": Hq, "kv_heads": Hkv, "head_dim": D,
+                       "context": cfgd["context"], "window_blocks": f"{cfgd['blk_num']}x{cfgd['blk_size']}",
+                       "selected_frac": cfgd["frac"], "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "l2": "inputs larger than L2 (K/V 2.1 GB per GPU), no flush"},
+            "hbm_gbs_step": round((pbytes + B * Hq * W_avg * 16) / (ms_max * 1e-3) / 1e9, 1),
+            "roofline": {"bound": "hbm", "kernel": "hgca::decode_partial_kernel",
+                         "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": None,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)",
+                         "kernel_ms": round(part_ms, 5), "bytes_per_launch": int(pbytes),
+                         "dense_bytes": int(dense_b), "sparse_unique_bytes": int(sparse_b),
+                         "kernel_share_of_step": round(part_ms / ms, 3)},
+            "e2e": {"value": round(world * B / (e2e_ms * 1e-3), 1), "unit": "tokens/s",
+                    "ms_per_step": round(e2e_ms, 4), "steps": e2e_steps,
+                    "h2d_bytes_per_step": int((qh.numel() + kh.numel() + vh.numel()) * qh.element_size()),
+                    "d2h_bytes_per_step": int(oh.numel() * 4 + lh.numel() * 8)},
+            "gpu_launches": launches,
+            "clocks": clocks.summary(t_wall0 - 1.0, t_wall1),
+            "cpu_baseline": cpu,
+        }
+        if cpu:
+            result["cpu_baseline"]["speedup_e2e"] = round(result["e2e"]["value"] / cpu["value"], 1)
+    if dist:
+        dist.destroy_process_group()
+    return result
+
+
+# ----------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    from oracle import cpu_bench
+
+    cfgd = dict(C2)
+    cap = cfgd["blk_num"] * cfgd["blk_size"]
+    steps = max(1, min(args.steps, 5))
+    warm = 1
+    r = cpu_bench.pool_bench(cfgd["heads"], cfgd["kv_heads"], cfgd["head_dim"], cfgd["context"] - cap, cap,
+                             cfgd["frac"], batch=cfgd["batch"], steps=steps, warmup=warm)
+    ms = statistics.mean(r["times"]) * 1e3
+    tok = cfgd["batch"] / (ms * 1e-3)
+    return {
+        "impl": "reference",
+        "metric": "hybrid-attn decode tokens/s (1 layer, C2)",
+        "value": round(tok, 3), "unit": "tokens/s", "n_gpus": world, "steps": steps, "warmup": warm,
+        "ms_per_step": round(ms, 2), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "fp32 (bf16-rounded values upcast), fp64 accumulation (reference _core)",
+        "data": "synthetic", "config": {"workload": WORKLOAD, "batch": cfgd["batch"]},
+        "cpu_baseline": {"value": round(tok, 3), "unit": "tokens/s", "cores": r["workers"], "kind": r["kind"],
+                         "sample": f"{steps} step(s) x full batch of {cfgd['batch']} sequences, one process "
+                                   f"per sequence over {r['workers']} host cores (reference is single-threaded "
+                                   f"per engine, engine.py:10-11)"},
+        "e2e": {"value": round(tok, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if args.impl == "reference":
+        res = run_reference(args, rank, world)
+    else:
+        res = run_ours(args, rank, world)
+    if rank == 0 and res is not None:
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -153,7 +153,12 @@ typedef struct hgca_decode_desc {
   double* lse_sparse;       /* optional [B*Hq] */
 } hgca_decode_desc;
 
+/* One decode step = hgca_decode_partial (dense window items + sparse union
+ * items -> per-item (m, z, acc) partials) then hgca_decode_merge (fixed-order
+ * fold, merge_states, MAW EMA). The halves are exported for per-kernel timing. */
 int hgca_decode_step(const hgca_decode_desc* desc, hgca_stream_t stream);
+int hgca_decode_partial(const hgca_decode_desc* desc, hgca_stream_t stream);
+int hgca_decode_merge(const hgca_decode_desc* desc, hgca_stream_t stream);
 
 #ifdef __cplusplus
 }

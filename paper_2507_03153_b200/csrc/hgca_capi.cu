@@ -246,7 +246,7 @@ int hgca_union_build(const uint32_t* sel_mask, int64_t B, int64_t Hq, int64_t Hk
                      "union_build");
 }
 
-int hgca_decode_step(const hgca_decode_desc* d, hgca_stream_t stream) {
+static int decode_prepare(const hgca_decode_desc* d, DecodeArgs& a, DecodeMergeArgs& m) {
   if (!d) return fail(HGCA_EINVAL, "decode_step: null descriptor");
   if (d->dtype != HGCA_DTYPE_F32 && d->dtype != HGCA_DTYPE_BF16)
     return fail(HGCA_EINVAL, "decode_step: storage dtype must be float32 or bfloat16");
@@ -269,7 +269,7 @@ int hgca_decode_step(const hgca_decode_desc* d, hgca_stream_t stream) {
   if (!d->K || !d->V || !d->q || !d->u_pos || !d->u_qm || !d->u_cnt || !d->item_off || !d->dsc ||
       !d->part_m || !d->part_z || !d->part_acc || !d->counter || !d->out || !d->lse)
     return fail(HGCA_EINVAL, "decode_step: null pointer");
-  DecodeArgs a{};
+  a = DecodeArgs{};
   a.K = d->K; a.V = d->V; a.q = d->q;
   a.B = d->B; a.Hq = d->Hq; a.Hkv = d->Hkv; a.G = G; a.D = d->D; a.T = d->T;
   a.scale = d->scale;
@@ -281,9 +281,7 @@ int hgca_decode_step(const hgca_decode_desc* d, hgca_stream_t stream) {
   a.part_m = d->part_m; a.part_z = d->part_z; a.part_acc = d->part_acc;
   a.counter = d->counter;
   a.n_dense_items = n_dense;
-  int rc = cuda_status(launch_decode_partial(d->dtype, a, S(stream)), "decode_partial");
-  if (rc) return rc;
-  DecodeMergeArgs m{};
+  m = DecodeMergeArgs{};
   m.B = d->B; m.Hq = d->Hq; m.Hkv = d->Hkv; m.G = G; m.D = d->D;
   m.Sd = Sd; m.n_dense_items = n_dense; m.item_off = d->item_off;
   m.part_m = d->part_m; m.part_z = d->part_z; m.part_acc = d->part_acc;
@@ -293,6 +291,32 @@ int hgca_decode_step(const hgca_decode_desc* d, hgca_stream_t stream) {
   m.one_minus_alpha = 1.0 - d->alpha; m.alpha = d->alpha;
   m.wts_out = d->wts_out; m.out = d->out; m.lse = d->lse;
   m.out_sparse = d->out_sparse; m.lse_sparse = d->lse_sparse;
+  return HGCA_OK;
+}
+
+int hgca_decode_partial(const hgca_decode_desc* d, hgca_stream_t stream) {
+  DecodeArgs a;
+  DecodeMergeArgs m;
+  int rc = decode_prepare(d, a, m);
+  if (rc) return rc;
+  return cuda_status(launch_decode_partial(d->dtype, a, S(stream)), "decode_partial");
+}
+
+int hgca_decode_merge(const hgca_decode_desc* d, hgca_stream_t stream) {
+  DecodeArgs a;
+  DecodeMergeArgs m;
+  int rc = decode_prepare(d, a, m);
+  if (rc) return rc;
+  return cuda_status(launch_decode_merge(m, S(stream)), "decode_merge");
+}
+
+int hgca_decode_step(const hgca_decode_desc* d, hgca_stream_t stream) {
+  DecodeArgs a;
+  DecodeMergeArgs m;
+  int rc = decode_prepare(d, a, m);
+  if (rc) return rc;
+  rc = cuda_status(launch_decode_partial(d->dtype, a, S(stream)), "decode_partial");
+  if (rc) return rc;
   return cuda_status(launch_decode_merge(m, S(stream)), "decode_merge");
 }
 

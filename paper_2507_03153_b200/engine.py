@@ -211,6 +211,8 @@ class HybridEngine:
         self.part_acc = torch.empty(self.max_items * self.G * self.D, dtype=torch.float32, device=self.dev)
         self.counter = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self._desc = _lib.DecodeDesc()
+        self.launches = 0          # kernels of libhgca_b200 launched by this engine
+        self.partial_events = None  # list -> (start, end) CUDA events around the partial kernel
 
     # ------------------------------------------------------------ helpers
     def _stream(self):
@@ -248,6 +250,7 @@ class HybridEngine:
             topk_mask(ls.maw, need, n=n, exclude=ls.ctx, out=ls.sel)
         else:
             ls.sel.copy_(ls.ctx)
+        self.launches += 2 + (3 if (self.g_pad > 1 and n) else 0) + (1 if self.config.selection == "topk" and n else 0)
         _lib.call("hgca_union_build", ls.sel.data_ptr(), self.B, self.Hq, self.Hkv, words, n, self.T,
                   ls.u_pos.data_ptr(), ls.u_qm.data_ptr(), ls.u_cnt.data_ptr(), ls.item_off.data_ptr(),
                   SPARSE_ROWS, s)
@@ -255,6 +258,7 @@ class HybridEngine:
     def _ingest(self, ls: LayerState, lo, hi, divisor):
         """StoreTier.ingest_evicted of positions [lo, hi) (sparsifier.py:127-156)."""
         if self.config.selection == "threshold" and hi > lo:
+            self.launches += 1
             _lib.call("hgca_select_threshold", ls.maw.data_ptr(), self.B * self.Hq, self.T, lo, hi,
                       float(self.config.cache.beta), int(divisor), ls.ctx.data_ptr(), ls.ctx.shape[1], 0,
                       self._stream())
@@ -373,7 +377,17 @@ class HybridEngine:
         d.wts_out = wts.data_ptr() if wts is not None else None
         d.out_sparse = None
         d.lse_sparse = None
-        _lib.call("hgca_decode_step", d, s)
+        if self.partial_events is None:
+            _lib.call("hgca_decode_step", d, s)
+        else:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            _lib.call("hgca_decode_partial", d, s)
+            e1.record()
+            _lib.call("hgca_decode_merge", d, s)
+            self.partial_events.append((e0, e1))
+        self.launches += 3  # write_rows, decode_partial, decode_merge
         self._last_dense_positions = np.arange(ls.lo, ls.nxt + 1, dtype=np.int64)
         # maintenance after the merge (engine.py:175-191): EMA + init done in
         # the merge kernel; eviction/offload here; append_kv = the position move.
@@ -382,6 +396,25 @@ class HybridEngine:
         if ev_hi > ev_lo:
             self._ingest(ls, ev_lo, ev_hi, w_size + 1)
         return out, lse, wts
+
+    def decode_host(self, layer_idx, q_host, k_host, v_host, out_host, lse_host, staging=None):
+        """End-to-end decode through the C ABI with HOST buffers: pinned
+        q [B,Hq,1,D] / k, v [B,Hkv,1,D] are copied to HBM, the step runs, and
+        out [B*Hq, D] f32 / lse [B*Hq] f64 are copied back and synchronized
+        (the host reads the step's result)."""
+        if staging is None:
+            staging = (torch.empty(q_host.shape, dtype=self.tdtype, device=self.dev),
+                       torch.empty(k_host.shape, dtype=self.tdtype, device=self.dev),
+                       torch.empty(v_host.shape, dtype=self.tdtype, device=self.dev))
+        q, k, v = staging
+        q.copy_(q_host, non_blocking=True)
+        k.copy_(k_host, non_blocking=True)
+        v.copy_(v_host, non_blocking=True)
+        out, lse, _ = self.decode_device(layer_idx, q, k, v)
+        out_host.copy_(out, non_blocking=True)
+        lse_host.copy_(lse, non_blocking=True)
+        torch.cuda.current_stream(self.dev).synchronize()
+        return out_host, lse_host
 
     def _append(self, layer_idx, inp):
         """Append step (engine.py:111-114 -> _run_step with the full archive)."""
