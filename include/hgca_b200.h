@@ -112,6 +112,10 @@ int hgca_select_topk(const double* maw, int64_t rows, int64_t ld, int64_t n, con
 int hgca_write_rows(int dtype, void* K, void* V, int64_t BH, int64_t T, int64_t d, int64_t pos,
                     const void* k_new, const void* v_new, int64_t n, hgca_stream_t stream);
 int hgca_decode_chunk_rows(int dtype, int64_t d);
+/* Launch configuration of the decode kernel for (dtype, head_dim, Hq/Hkv):
+ * out5 = {warps per CTA, smem bytes per warp, cp.async stages, rows per
+ * sub-chunk, smem bytes per CTA}. */
+int hgca_decode_config(int dtype, int64_t d, int64_t group, int64_t* out5);
 /* MAW maintenance from float32 weight rows w [BH, nq, w_ld] (row mean in fp64):
  * mode 0 = window EMA for j < w_old and init for j >= w_old (kv_cache.py:171-187,
  * engine.py:177-191); mode 1 = replace (StoreTier.reevaluate, sparsifier.py:158-177). */

@@ -226,6 +226,11 @@ int hgca_write_rows(int dtype, void* K, void* V, int64_t BH, int64_t T, int64_t 
 
 int hgca_decode_chunk_rows(int dtype, int64_t d) { return decode_chunk_rows(dtype, d); }
 
+int hgca_decode_config(int dtype, int64_t d, int64_t group, int64_t* out5) {
+  if (!out5 || decode_config(dtype, d, group, out5)) return fail(HGCA_EINVAL, "decode_config: unsupported");
+  return HGCA_OK;
+}
+
 int hgca_maw_update(const float* w, int64_t BH, int64_t nq, int64_t W, int64_t w_ld, double* maw,
                     int64_t T, int64_t p0, int64_t w_old, double alpha, int mode, hgca_stream_t stream) {
   if (BH < 0 || nq < 1 || W < 0 || w_ld < W || p0 < 0 || p0 + W > T || (mode != 0 && mode != 1))

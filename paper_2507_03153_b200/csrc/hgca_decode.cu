@@ -30,45 +30,52 @@ template <typename T, int D, int G>
 struct DecodeCfg {
   static constexpr int ESZ = (int)sizeof(T);
   static constexpr int ROWB = D * ESZ;
-  static constexpr int CH = ROWB <= 256 ? 128 : 64;    // rows per stage (<= consumer threads)
-  static constexpr int KRS = ROWB + 16;                 // padded K row: conflict-free row-per-thread reads
-  static constexpr int VRS = ROWB;
+  static constexpr int SUB = 32;                        // rows per sub-chunk (one per lane)
   static constexpr int PIECES = ROWB / 16;
   static constexpr int E = 16 / ESZ;                    // elements per 16-byte piece
-  static constexpr int QB = G * ROWB;                   // raw query bytes staged per chunk
-  static constexpr int OFF_V = CH * KRS;
-  static constexpr int OFF_Q = OFF_V + CH * VRS;
-  static constexpr int OFF_POS = OFF_Q + QB;
-  static constexpr int OFF_QM = OFF_POS + CH * 4;
-  static constexpr int STAGE = ((OFF_QM + CH) + 127) / 128 * 128;
-  static constexpr int GW = G < 4 ? G : 4;              // distinct heads across the 4 PV warps
-  static constexpr int NPV = 4 / GW;                    // warps sharing one head in P.V
-  static constexpr int HPW = G > 4 ? G / 4 : 1;         // heads per PV warp
+  // bf16: fp32 partial per 16-byte piece (8 exact products), fp64 across
+  // pieces. fp32: per-element fp64 DFMA in the reference's sequential order.
+  static constexpr bool PIECE32 = ESZ == 2;
+  static constexpr bool V_SMEM = ESZ == 4;              // fp32: V staged in smem; bf16: V in registers
   static constexpr int DPL = D / 32;                    // dims per lane in P.V
-  static constexpr int FIXED = G * D * 8 + G * CH * 8 + G * CH * 4 + 4 * D * 4 + 256;
-  static constexpr int SMAX = 232448 - 1024;
-  static constexpr int S0 = (SMAX - FIXED) / STAGE;
-  static constexpr int S = S0 > 4 ? 4 : S0;
-  static constexpr int SMEM = S * STAGE + FIXED;
-  static_assert(S >= 2, "decode stage does not fit shared memory");
+  static constexpr int S = 2;                           // K stages per warp
+  static constexpr int OFF_V = SUB * ROWB;              // K rows are XOR-swizzled per 16-byte piece
+  static constexpr int OFF_POS = OFF_V + (V_SMEM ? SUB * ROWB : 0);
+  static constexpr int OFF_QM = OFF_POS + SUB * 4;
+  static constexpr int STAGE = ((OFF_QM + SUB) + 15) / 16 * 16;
+  static constexpr int QRAW = G * ROWB;                 // raw query block of one item
+  static constexpr int QK_ESZ = PIECE32 ? 4 : 8;
+  static constexpr int OFF_QRAW = S * STAGE;
+  static constexpr int OFF_QK = OFF_QRAW + S * QRAW;    // queries [G][D] (fp32 or fp64)
+  static constexpr int OFF_SC = OFF_QK + G * D * QK_ESZ;// scores [G][32] fp64
+  static constexpr int OFF_ACC = OFF_SC + G * SUB * 8;  // P.V accumulators [G][D] fp32
+  static constexpr int OFF_MZ = OFF_ACC + G * D * 4;    // running (m, z) [G][2] fp64
+  static constexpr int OFF_DESC = OFF_MZ + G * 16;
+  static constexpr int WARP_SMEM = ((OFF_DESC + S * 32) + 127) / 128 * 128;
+  static constexpr int NC0 = (232448 - 2048) / WARP_SMEM;
+  static constexpr int NC = NC0 > 16 ? 16 : NC0;        // warps per CTA
+  static constexpr int SMEM = NC * WARP_SMEM;
+  static_assert(NC >= 1, "decode warp pipeline does not fit shared memory");
   static_assert(D % 32 == 0, "head_dim must be a multiple of 32");
 };
 
+// Per-stage descriptor (smem, written by the warp that issued the stage).
+struct StageDesc {
+  int item, bk, r0, n;
+  int first, last, dense, qbuf;
+};
+
+__device__ __forceinline__ int swz(int r, int p) { return (p & ~7) | ((p ^ r) & 7); }
+
 template <typename T>
-__device__ __forceinline__ void load_piece_f64(const unsigned char* p, double* out);
+__device__ __forceinline__ void unpack8(const uint4 v, float* f);
 template <>
-__device__ __forceinline__ void load_piece_f64<float>(const unsigned char* p, double* out) {
-  const float4 v = *reinterpret_cast<const float4*>(p);
-  out[0] = (double)v.x; out[1] = (double)v.y; out[2] = (double)v.z; out[3] = (double)v.w;
-}
-template <>
-__device__ __forceinline__ void load_piece_f64<__nv_bfloat16>(const unsigned char* p, double* out) {
-  const uint4 v = *reinterpret_cast<const uint4*>(p);
+__device__ __forceinline__ void unpack8<__nv_bfloat16>(const uint4 v, float* f) {
   const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    out[2 * i] = (double)__uint_as_float(w[i] << 16);
-    out[2 * i + 1] = (double)__uint_as_float(w[i] & 0xffff0000u);
+    f[2 * i] = __uint_as_float(w[i] << 16);
+    f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
   }
 }
 
@@ -84,275 +91,274 @@ __device__ __forceinline__ void load_v_f32<float, 2>(const unsigned char* p, flo
   const float2 v = *reinterpret_cast<const float2*>(p);
   out[0] = v.x; out[1] = v.y;
 }
-template <>
-__device__ __forceinline__ void load_v_f32<__nv_bfloat16, 4>(const unsigned char* p, float* out) {
-  const uint2 v = *reinterpret_cast<const uint2*>(p);
-  out[0] = __uint_as_float(v.x << 16); out[1] = __uint_as_float(v.x & 0xffff0000u);
-  out[2] = __uint_as_float(v.y << 16); out[3] = __uint_as_float(v.y & 0xffff0000u);
-}
-template <>
-__device__ __forceinline__ void load_v_f32<__nv_bfloat16, 2>(const unsigned char* p, float* out) {
-  const uint32_t v = *reinterpret_cast<const uint32_t*>(p);
-  out[0] = __uint_as_float(v << 16); out[1] = __uint_as_float(v & 0xffff0000u);
-}
 
 template <typename T, int D, int G>
-__global__ void __launch_bounds__(160, 1) decode_partial_kernel(const DecodeArgs a) {
+__global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) __maxnreg__((DecodeCfg<T, D, G>::NC * 32 > 256 ? 224 : 255)) decode_partial_kernel(const DecodeArgs a) {
   using C = DecodeCfg<T, D, G>;
   extern __shared__ __align__(128) unsigned char sm[];
-  unsigned char* stages = sm;
-  double* qsh = reinterpret_cast<double*>(sm + C::S * C::STAGE);  // [G][D]
-  double* sc = qsh + G * D;                                        // [G][CH]
-  float* pf = reinterpret_cast<float*>(sc + G * C::CH);            // [G][CH]
-  float* accbuf = pf + G * C::CH;                                  // [4][D]
-  __shared__ __align__(8) uint64_t full[C::S], empty[C::S];
-  __shared__ int st_item[C::S], st_chunk[C::S], st_nvalid[C::S], st_last[C::S];
-  __shared__ double m_sh[G], z_sh[G], scal_sh[G];
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t FULL = 0xffffffffu;
+  unsigned char* wsm = sm + warp * C::WARP_SMEM;
+  StageDesc* desc = reinterpret_cast<StageDesc*>(wsm + C::OFF_DESC);
+  double* sc = reinterpret_cast<double*>(wsm + C::OFF_SC);
+  float* accs = reinterpret_cast<float*>(wsm + C::OFF_ACC);
+  double* mz = reinterpret_cast<double*>(wsm + C::OFF_MZ);
   const int64_t BK = a.B * a.Hkv;
   const int64_t W = a.dhi - a.dlo;
-  if (tid == 0) {
-    for (int s = 0; s < C::S; ++s) {
-      mbar_init(&full[s], 64);
-      mbar_init(&empty[s], 4);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
+  const int total = (int)(a.n_dense_items + (int64_t)a.item_off[BK]);
+  const unsigned char* Kg = reinterpret_cast<const unsigned char*>(a.K);
+  const unsigned char* Vg = reinterpret_cast<const unsigned char*>(a.V);
+  const unsigned char* Qg = reinterpret_cast<const unsigned char*>(a.q);
 
-  if (warp == 4) {
-    // ---------------------------------------------------------------- producer
-    const int64_t total = a.n_dense_items + (int64_t)a.item_off[BK];
-    const unsigned char* Kg = reinterpret_cast<const unsigned char*>(a.K);
-    const unsigned char* Vg = reinterpret_cast<const unsigned char*>(a.V);
-    const unsigned char* Qg = reinterpret_cast<const unsigned char*>(a.q);
-    int k = 0;
-    while (true) {
-      int item = 0;
-      if (lane == 0) item = atomicAdd(a.counter, 1);
-      item = __shfl_sync(0xffffffffu, item, 0);
-      if (item >= total) {
-        const int s = k % C::S;
-        if (k >= C::S) mbar_wait(&empty[s], ((k / C::S) - 1) & 1);
-        if (lane == 0) st_item[s] = -1;
-        __syncwarp();
-        cp_async_mbar_arrive_noinc(&full[s]);
-        mbar_arrive(&full[s]);
-        break;
+  // ---------------------------------------------------------- load cursor
+  // Each warp streams whole work items (dynamic, global counter) through its
+  // own S-stage cp.async ring. The cursor runs ahead across item boundaries;
+  // the union entries (position, query-head mask) of the next sub-chunk are
+  // prefetched into registers one issue ahead.
+  int next_item = 0;
+  if (lane == 0) next_item = atomicAdd(a.counter, 1);
+  next_item = __shfl_sync(FULL, next_item, 0);
+  int L_item = -1, L_bk = 0, L_hi = 0, L_row = 0, L_lo = 0, L_dense = 0, L_qbuf = C::S - 1;
+  StageDesc pd;      // pending descriptor (next sub-chunk to issue)
+  int32_t pd_pos = 0;
+  uint32_t pd_qm = 0;
+
+  auto advance = [&]() {  // form pd for the next sub-chunk and start its metadata loads
+    if (L_item < 0 || L_row >= L_hi) {
+      if (next_item >= total) {
+        pd.item = -1;
+        return;
       }
-      int64_t bk, lo, hi;
-      const bool dense = item < a.n_dense_items;
-      if (dense) {
-        bk = item / a.Sd;
-        lo = (item % a.Sd) * a.dense_rows;
-        hi = min(W, lo + a.dense_rows);
+      L_item = next_item;
+      if (lane == 0) next_item = atomicAdd(a.counter, 1);
+      next_item = __shfl_sync(FULL, next_item, 0);
+      if (L_item < a.n_dense_items) {
+        L_dense = 1;
+        L_bk = (int)(L_item / a.Sd);
+        L_lo = (int)((L_item % a.Sd) * a.dense_rows);
+        L_hi = (int)min(W, (int64_t)L_lo + a.dense_rows);
       } else {
-        const int x = item - (int)a.n_dense_items;
+        L_dense = 0;
+        const int x = L_item - (int)a.n_dense_items;
         int64_t l = 0, r = BK;  // largest bk with item_off[bk] <= x
         while (r - l > 1) {
           const int64_t mid = (l + r) >> 1;
           if (a.item_off[mid] <= x) l = mid; else r = mid;
         }
-        bk = l;
-        lo = (int64_t)(x - a.item_off[bk]) * a.sparse_rows;
-        hi = min((int64_t)a.u_cnt[bk], lo + a.sparse_rows);
+        L_bk = (int)l;
+        L_lo = (int)((x - a.item_off[l]) * a.sparse_rows);
+        L_hi = (int)min((int64_t)a.u_cnt[l], (int64_t)L_lo + a.sparse_rows);
       }
-      const int64_t b = bk / a.Hkv, kvh = bk % a.Hkv;
-      const int nchunks = (int)((hi - lo + C::CH - 1) / C::CH);
+      L_row = L_lo;
+      L_qbuf = (L_qbuf + 1) % C::S;
+      const int64_t b = L_bk / a.Hkv, kvh = L_bk % a.Hkv;
       const unsigned char* qsrc = Qg + (b * a.Hq + kvh * G) * (int64_t)C::ROWB;
-      const unsigned char* kbase = Kg + bk * a.T * (int64_t)C::ROWB;
-      const unsigned char* vbase = Vg + bk * a.T * (int64_t)C::ROWB;
-      for (int c = 0; c < nchunks; ++c, ++k) {
-        const int s = k % C::S;
-        if (k >= C::S) mbar_wait(&empty[s], ((k / C::S) - 1) & 1);
-        unsigned char* st = stages + s * C::STAGE;
-        int32_t* pos_s = reinterpret_cast<int32_t*>(st + C::OFF_POS);
-        uint8_t* qm_s = st + C::OFF_QM;
-        const int64_t r0 = lo + (int64_t)c * C::CH;
-        const int nvalid = (int)min((int64_t)C::CH, hi - r0);
-        for (int r = lane; r < C::CH; r += 32) {
-          int32_t pos = 0;
-          uint8_t qm = 0;
-          if (r < nvalid) {
-            if (dense) {
-              pos = (int32_t)(a.dlo + r0 + r);
-              qm = (uint8_t)((1u << G) - 1u);
-            } else {
-              pos = a.u_pos[bk * a.T + r0 + r];
-              qm = a.u_qm[bk * a.T + r0 + r];
-            }
-          }
-          pos_s[r] = pos;
-          qm_s[r] = qm;
-        }
-        if (lane == 0) {
-          st_item[s] = item;
-          st_chunk[s] = c;
-          st_nvalid[s] = nvalid;
-          st_last[s] = (c == nchunks - 1) ? (dense ? 2 : 1) : 0;
-        }
-        __syncwarp();
-        for (int t = lane; t < nvalid * C::PIECES; t += 32) {
-          const int r = t / C::PIECES, p = t % C::PIECES;
-          const int64_t off = (int64_t)pos_s[r] * C::ROWB + p * 16;
-          cp_async16(st + r * C::KRS + p * 16, kbase + off);
-          cp_async16(st + C::OFF_V + r * C::VRS + p * 16, vbase + off);
-        }
-        for (int t = lane; t < C::QB / 16; t += 32) cp_async16(st + C::OFF_Q + t * 16, qsrc + t * 16);
-        cp_async_mbar_arrive_noinc(&full[s]);
-        mbar_arrive(&full[s]);
+      unsigned char* qdst = wsm + C::OFF_QRAW + L_qbuf * C::QRAW;
+      for (int t = lane; t < C::QRAW / 16; t += 32) cp_async16(qdst + t * 16, qsrc + t * 16);
+    }
+    pd.item = L_item;
+    pd.bk = L_bk;
+    pd.r0 = L_row;
+    pd.n = min(C::SUB, L_hi - L_row);
+    pd.first = L_row == L_lo;
+    pd.last = L_row + C::SUB >= L_hi;
+    pd.dense = L_dense;
+    pd.qbuf = L_qbuf;
+    pd_pos = 0;  // rows past the end read position 0 (valid memory, masked by qm = 0)
+    pd_qm = 0;
+    if (lane < pd.n) {
+      if (L_dense) {
+        pd_pos = (int32_t)(a.dlo + L_row + lane);
+        pd_qm = (1u << G) - 1u;
+      } else {
+        pd_pos = __ldg(a.u_pos + (int64_t)L_bk * a.T + L_row + lane);
+        pd_qm = __ldg(a.u_qm + (int64_t)L_bk * a.T + L_row + lane);
       }
     }
-    return;
-  }
+    L_row += C::SUB;
+  };
 
-  // ------------------------------------------------------------------ consumers
-  float acc[C::HPW][C::DPL];
-  const int g0 = warp % C::GW, rsub = warp / C::GW;
-  int k = 0;
-  while (true) {
-    const int s = k % C::S;
-    mbar_wait(&full[s], (k / C::S) & 1);
-    const int item = st_item[s];
-    if (item < 0) break;
-    const unsigned char* st = stages + s * C::STAGE;
-    const int32_t* pos_s = reinterpret_cast<const int32_t*>(st + C::OFF_POS);
-    const uint8_t* qm_s = st + C::OFF_QM;
-    const int c = st_chunk[s], nvalid = st_nvalid[s], last = st_last[s];
-    if (c == 0) {
-      for (int t = tid; t < G * D; t += 128) {
-        const T* qr = reinterpret_cast<const T*>(st + C::OFF_Q);
-        qsh[t] = to_f64(qr[t]);
+  auto issue = [&](int s) {
+    unsigned char* st = wsm + s * C::STAGE;
+    if (lane == 0) desc[s] = pd;
+    if (pd.item >= 0) {
+      reinterpret_cast<int32_t*>(st + C::OFF_POS)[lane] = pd_pos;
+      st[C::OFF_QM + lane] = (uint8_t)pd_qm;
+      const unsigned char* kbase = Kg + (int64_t)pd.bk * a.T * C::ROWB;
+      const unsigned char* vbase = Vg + (int64_t)pd.bk * a.T * C::ROWB;
+#pragma unroll 4
+      for (int t = lane; t < C::SUB * C::PIECES; t += 32) {
+        const int r = t / C::PIECES, p = t % C::PIECES;
+        const int32_t pr = __shfl_sync(FULL, pd_pos, r);
+        if (r < pd.n) {
+          cp_async16(st + r * C::ROWB + swz(r, p) * 16, kbase + (int64_t)pr * C::ROWB + p * 16);
+          if (C::V_SMEM) cp_async16(st + C::OFF_V + r * C::ROWB + p * 16, vbase + (int64_t)pr * C::ROWB + p * 16);
+        }
       }
-      if (tid < G) {
-        m_sh[tid] = -INFINITY;
-        z_sh[tid] = 0.0;
-      }
-#pragma unroll
-      for (int j = 0; j < C::HPW; ++j)
-#pragma unroll
-        for (int i = 0; i < C::DPL; ++i) acc[j][i] = 0.f;
-      named_sync(1, 128);
     }
-    // ---- scores: one row per thread, fp64, sequential over d
-    if (tid < C::CH) {
-      const int r = tid;
-      const uint32_t qm = qm_s[r];
-      const uint32_t wq = __reduce_or_sync(0xffffffffu, qm);
-      double sacc[G];
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    if (pd.item >= 0) advance();
+  };
+
+  advance();
 #pragma unroll
-      for (int g = 0; g < G; ++g) sacc[g] = 0.0;
-      if (wq) {
-        const unsigned char* krow = st + r * C::KRS;
-#pragma unroll 2
-        for (int p = 0; p < C::PIECES; ++p) {
-          double kd[C::E];
-          load_piece_f64<T>(krow + p * 16, kd);
+  for (int s = 0; s < C::S; ++s) issue(s);
+
+  // ---------------------------------------------------------- compute
+  for (int k = 0;; ++k) {
+    const int s = k % C::S;
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(C::S - 1) : "memory");
+    __syncwarp();
+    const StageDesc d = desc[s];
+    if (d.item < 0) break;
+    const unsigned char* st = wsm + s * C::STAGE;
+    const int32_t mypos = reinterpret_cast<const int32_t*>(st + C::OFF_POS)[lane];
+    const uint32_t qm = st[C::OFF_QM + lane];
+    const uint32_t wq = __reduce_or_sync(FULL, qm);
+    // ---- V rows of this sub-chunk into registers (bf16), unconditional
+    uint2 vreg[C::V_SMEM ? 1 : C::SUB];
+    if constexpr (!C::V_SMEM) {
+      const unsigned char* vbase = Vg + (int64_t)d.bk * a.T * C::ROWB + lane * C::DPL * C::ESZ;
+#pragma unroll
+      for (int r = 0; r < C::SUB; ++r) {
+        const int32_t pr = __shfl_sync(FULL, mypos, r);
+        if constexpr (C::DPL * C::ESZ == 8) {
+          vreg[r] = __ldg(reinterpret_cast<const uint2*>(vbase + (int64_t)pr * C::ROWB));
+        } else {
+          vreg[r].x = __ldg(reinterpret_cast<const uint32_t*>(vbase + (int64_t)pr * C::ROWB));
+        }
+      }
+    }
+    if (d.first) {
+      const T* qr = reinterpret_cast<const T*>(wsm + C::OFF_QRAW + d.qbuf * C::QRAW);
+      if constexpr (C::PIECE32) {
+        float* qk = reinterpret_cast<float*>(wsm + C::OFF_QK);
+        for (int t = lane; t < G * D; t += 32) qk[t] = to_f32(qr[t]);
+      } else {
+        double* qk = reinterpret_cast<double*>(wsm + C::OFF_QK);
+        for (int t = lane; t < G * D; t += 32) qk[t] = to_f64(qr[t]);
+      }
+      for (int t = lane; t < G * D; t += 32) accs[t] = 0.f;
+      if (lane < G) {
+        mz[2 * lane] = -INFINITY;
+        mz[2 * lane + 1] = 0.0;
+      }
+      __syncwarp();
+    }
+    // ---- scores: lane = row
+    double sacc[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) sacc[g] = 0.0;
+    {
+      const unsigned char* krow = st + lane * C::ROWB;
+#pragma unroll 4
+      for (int p = 0; p < C::PIECES; ++p) {
+        const uint4 raw = *reinterpret_cast<const uint4*>(krow + swz(lane, p) * 16);
+        if constexpr (C::PIECE32) {
+          float kf[8];
+          unpack8<T>(raw, kf);
+          const float* qk = reinterpret_cast<const float*>(wsm + C::OFF_QK);
 #pragma unroll
           for (int g = 0; g < G; ++g) {
             if ((wq >> g) & 1u) {
-              const double* qg = qsh + g * D + p * C::E;
+              const float4 qa = *reinterpret_cast<const float4*>(qk + g * D + p * 8);
+              const float4 qb = *reinterpret_cast<const float4*>(qk + g * D + p * 8 + 4);
+              float part = qa.x * kf[0];
+              part = fmaf(qa.y, kf[1], part);
+              part = fmaf(qa.z, kf[2], part);
+              part = fmaf(qa.w, kf[3], part);
+              part = fmaf(qb.x, kf[4], part);
+              part = fmaf(qb.y, kf[5], part);
+              part = fmaf(qb.z, kf[6], part);
+              part = fmaf(qb.w, kf[7], part);
+              sacc[g] += (double)part;
+            }
+          }
+        } else {
+          const float kk[4] = {__uint_as_float(raw.x), __uint_as_float(raw.y), __uint_as_float(raw.z),
+                               __uint_as_float(raw.w)};
+          double kd[4];
 #pragma unroll
-              for (int e = 0; e < C::E; ++e) sacc[g] = fma(qg[e], kd[e], sacc[g]);
+          for (int e = 0; e < 4; ++e) kd[e] = (double)kk[e];
+          const double* qk = reinterpret_cast<const double*>(wsm + C::OFF_QK);
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            if ((wq >> g) & 1u) {
+              const double2 qa = *reinterpret_cast<const double2*>(qk + g * D + p * 4);
+              const double2 qb = *reinterpret_cast<const double2*>(qk + g * D + p * 4 + 2);
+              sacc[g] = fma(qa.x, kd[0], sacc[g]);  // exact products: reference order
+              sacc[g] = fma(qa.y, kd[1], sacc[g]);
+              sacc[g] = fma(qb.x, kd[2], sacc[g]);
+              sacc[g] = fma(qb.y, kd[3], sacc[g]);
             }
           }
         }
       }
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const double sv = ((qm >> g) & 1u) ? sacc[g] * a.scale : -INFINITY;
-        sc[g * C::CH + r] = sv;
-      }
-      if (item < a.n_dense_items && r < nvalid) {
-        const int64_t bk = item / a.Sd;
-        const int64_t b = bk / a.Hkv, kvh = bk % a.Hkv;
-        const int64_t j = pos_s[r] - a.dlo;
-#pragma unroll
-        for (int g = 0; g < G; ++g) a.dsc[(b * a.Hq + kvh * G + g) * a.dsc_ld + j] = sc[g * C::CH + r];
-      }
     }
-    named_sync(1, 128);
-    // ---- online softmax update (fp64), warp w owns heads w, w+4
-    for (int g = warp; g < G; g += 4) {
-      double cm = -INFINITY;
-      for (int r = lane; r < C::CH; r += 32) cm = fmax(cm, sc[g * C::CH + r]);
-      cm = warp_max_f64(cm);
-      const double m_old = m_sh[g];
+    const int64_t b = d.bk / a.Hkv, kvh = d.bk % a.Hkv;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const double sv = ((qm >> g) & 1u) ? sacc[g] * a.scale : -INFINITY;
+      sc[g * C::SUB + lane] = sv;
+      if (d.dense && lane < d.n) a.dsc[(b * a.Hq + kvh * G + g) * a.dsc_ld + (mypos - a.dlo)] = sv;
+    }
+    __syncwarp();
+    // ---- per active head (rolled loop): online softmax (fp64) + P.V (fp32)
+    for (uint32_t hm = wq; hm; hm &= hm - 1) {
+      const int g = __ffs(hm) - 1;
+      const double sv = sc[g * C::SUB + lane];
+      const double cm = warp_max_f64(sv);
+      const double m_old = mz[2 * g];
       const double mnew = fmax(m_old, cm);
-      double zs = 0.0;
-      double scal = 1.0;
-      if (mnew == -INFINITY) {
-        for (int r = lane; r < C::CH; r += 32) pf[g * C::CH + r] = 0.f;
-      } else {
-        scal = exp(m_old - mnew);
-        for (int r = lane; r < C::CH; r += 32) {
-          const double p = exp(sc[g * C::CH + r] - mnew);
-          zs += p;
-          pf[g * C::CH + r] = (float)p;
+      if (mnew == -INFINITY) continue;
+      const double scal = exp(m_old - mnew);
+      const double p = exp(sv - mnew);
+      const double zs = warp_sum_f64(p);
+      const float pf = (float)p;
+      const float sf = (float)scal;
+      float acc[C::DPL];
+      float* ag = accs + g * D + lane * C::DPL;
+#pragma unroll
+      for (int i = 0; i < C::DPL; ++i) acc[i] = ag[i] * sf;
+#pragma unroll
+      for (int r = 0; r < C::SUB; ++r) {
+        const float pr = __shfl_sync(FULL, pf, r);
+        if (pr != 0.f) {
+          float vv[C::DPL];
+          if constexpr (C::V_SMEM) {
+            load_v_f32<T, C::DPL>(st + C::OFF_V + r * C::ROWB + lane * C::DPL * C::ESZ, vv);
+          } else {
+            vv[0] = __uint_as_float(vreg[r].x << 16);
+            vv[1] = __uint_as_float(vreg[r].x & 0xffff0000u);
+            if constexpr (C::DPL == 4) {
+              vv[C::DPL > 2 ? 2 : 0] = __uint_as_float(vreg[r].y << 16);
+              vv[C::DPL > 3 ? 3 : 0] = __uint_as_float(vreg[r].y & 0xffff0000u);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < C::DPL; ++i) acc[i] = fmaf(pr, vv[i], acc[i]);
         }
       }
-      zs = warp_sum_f64(zs);
+#pragma unroll
+      for (int i = 0; i < C::DPL; ++i) ag[i] = acc[i];
       __syncwarp();
       if (lane == 0) {
-        z_sh[g] = z_sh[g] * scal + zs;
-        m_sh[g] = mnew;
-        scal_sh[g] = scal;
+        mz[2 * g] = mnew;
+        mz[2 * g + 1] = mz[2 * g + 1] * scal + zs;
       }
+      __syncwarp();
     }
-    named_sync(1, 128);
-    // ---- P.V (fp32): warp handles heads g0 + 4j over rows r = rsub (mod NPV)
-#pragma unroll
-    for (int j = 0; j < C::HPW; ++j) {
-      const int g = g0 + 4 * j;
-      const float sf = (float)scal_sh[g];
-#pragma unroll
-      for (int i = 0; i < C::DPL; ++i) acc[j][i] *= sf;
-      const float* pg = pf + g * C::CH;
-      for (int r = rsub; r < nvalid; r += C::NPV) {
-        const float p = pg[r];
-        if (p != 0.f) {
-          float vv[C::DPL];
-          load_v_f32<T, C::DPL>(st + C::OFF_V + r * C::VRS + lane * C::DPL * C::ESZ, vv);
-#pragma unroll
-          for (int i = 0; i < C::DPL; ++i) acc[j][i] = fmaf(p, vv[i], acc[j][i]);
-        }
+    if (d.last) {
+      for (int t = lane; t < G * D; t += 32) a.part_acc[(int64_t)d.item * G * D + t] = accs[t];
+      if (lane < G) {
+        a.part_m[(int64_t)d.item * G + lane] = mz[2 * lane];
+        a.part_z[(int64_t)d.item * G + lane] = mz[2 * lane + 1];
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-    if (last) {
-      // ---- emit this item's partial (fixed slot `item`)
-      if (C::NPV == 1) {
-#pragma unroll
-        for (int j = 0; j < C::HPW; ++j) {
-          const int g = g0 + 4 * j;
-          float* dst = a.part_acc + ((int64_t)item * G + g) * D + lane * C::DPL;
-#pragma unroll
-          for (int i = 0; i < C::DPL; ++i) dst[i] = acc[j][i];
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < C::DPL; ++i) accbuf[warp * D + lane * C::DPL + i] = acc[0][i];
-        named_sync(1, 128);
-        if (rsub == 0) {
-          float* dst = a.part_acc + ((int64_t)item * G + g0) * D + lane * C::DPL;
-#pragma unroll
-          for (int i = 0; i < C::DPL; ++i) {
-            float t = 0.f;
-            for (int w2 = 0; w2 < C::NPV; ++w2) t += accbuf[(g0 + w2 * C::GW) * D + lane * C::DPL + i];
-            dst[i] = t;
-          }
-        }
-      }
-      if (tid < G) {
-        a.part_m[(int64_t)item * G + tid] = m_sh[tid];
-        a.part_z[(int64_t)item * G + tid] = z_sh[tid];
-      }
-      named_sync(1, 128);
-    }
-    ++k;
+    issue(s);
   }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
 // --------------------------------------------------------------------- merge
@@ -592,7 +598,7 @@ static int launch_decode_t(const DecodeArgs& a, cudaStream_t s) {
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  decode_partial_kernel<T, D, G><<<nsm, 160, C::SMEM, s>>>(a);
+  decode_partial_kernel<T, D, G><<<nsm, C::NC * 32, C::SMEM, s>>>(a);
   return (int)cudaGetLastError();
 }
 
@@ -608,8 +614,9 @@ static int launch_decode_g(const DecodeArgs& a, cudaStream_t s) {
 }
 
 int decode_chunk_rows(int dtype, int64_t D) {
-  const int64_t esz = dtype == kBF16 ? 2 : 4;
-  return D * esz <= 256 ? 128 : 64;
+  (void)dtype;
+  (void)D;
+  return 32;
 }
 
 int launch_decode_partial(int dtype, const DecodeArgs& a, cudaStream_t s) {
@@ -656,4 +663,28 @@ int launch_write_rows(int dtype, void* K, void* V, int64_t BH, int64_t T, int64_
   return (int)cudaGetLastError();
 }
 
+}  // namespace hgca
+
+namespace hgca {
+template <typename T, int D, int G>
+static void cfg_of(int64_t* o) {
+  using C = DecodeCfg<T, D, G>;
+  o[0] = C::NC; o[1] = C::WARP_SMEM; o[2] = C::S; o[3] = C::SUB; o[4] = C::SMEM;
+}
+int decode_config(int dtype, int64_t D, int64_t G, int64_t* o) {
+#define HG_CFG(TT, DD)                                       \
+  switch (G) {                                               \
+    case 1: cfg_of<TT, DD, 1>(o); return 0;                  \
+    case 2: cfg_of<TT, DD, 2>(o); return 0;                  \
+    case 4: cfg_of<TT, DD, 4>(o); return 0;                  \
+    case 8: cfg_of<TT, DD, 8>(o); return 0;                  \
+  }                                                          \
+  return -1;
+  if (dtype == kBF16 && D == 128) { HG_CFG(__nv_bfloat16, 128) }
+  if (dtype == kBF16 && D == 64) { HG_CFG(__nv_bfloat16, 64) }
+  if (dtype == kF32 && D == 128) { HG_CFG(float, 128) }
+  if (dtype == kF32 && D == 64) { HG_CFG(float, 64) }
+#undef HG_CFG
+  return -1;
+}
 }  // namespace hgca

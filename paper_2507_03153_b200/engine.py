@@ -38,8 +38,8 @@ from .sparsifier import group_size, mask_to_lists, topk_mask, words_for
 __all__ = ["CacheConfig", "EngineConfig", "StepInput", "StepOutput", "LayerState", "HybridEngine"]
 
 MODES = ("decode", "append")
-DENSE_ROWS = 512
-SPARSE_ROWS = 512
+DENSE_ROWS = 256
+SPARSE_ROWS = 256
 
 
 @dataclass(frozen=True)
