@@ -119,14 +119,17 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) __maxnreg__((D
   if (lane == 0) next_item = atomicAdd(a.counter, 1);
   next_item = __shfl_sync(FULL, next_item, 0);
   int L_item = -1, L_bk = 0, L_hi = 0, L_row = 0, L_lo = 0, L_dense = 0, L_qbuf = C::S - 1;
-  StageDesc pd;      // pending descriptor (next sub-chunk to issue)
-  int32_t pd_pos = 0;
-  uint32_t pd_qm = 0;
+  // Two pending descriptors: pd1 = next sub-chunk to cp.async (positions
+  // known, its rows already prefetched into L2), pd2 = the one after (its
+  // position/mask loads in flight).
+  StageDesc pd1, pd2;
+  int32_t pd1_pos = 0, pd2_pos = 0;
+  uint32_t pd1_qm = 0, pd2_qm = 0;
 
-  auto advance = [&]() {  // form pd for the next sub-chunk and start its metadata loads
+  auto advance = [&]() {  // form pd2 for the next sub-chunk and start its metadata loads
     if (L_item < 0 || L_row >= L_hi) {
       if (next_item >= total) {
-        pd.item = -1;
+        pd2.item = -1;
         return;
       }
       L_item = next_item;
@@ -150,57 +153,80 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) __maxnreg__((D
         L_hi = (int)min((int64_t)a.u_cnt[l], (int64_t)L_lo + a.sparse_rows);
       }
       L_row = L_lo;
-      L_qbuf = (L_qbuf + 1) % C::S;
-      const int64_t b = L_bk / a.Hkv, kvh = L_bk % a.Hkv;
-      const unsigned char* qsrc = Qg + (b * a.Hq + kvh * G) * (int64_t)C::ROWB;
-      unsigned char* qdst = wsm + C::OFF_QRAW + L_qbuf * C::QRAW;
-      for (int t = lane; t < C::QRAW / 16; t += 32) cp_async16(qdst + t * 16, qsrc + t * 16);
     }
-    pd.item = L_item;
-    pd.bk = L_bk;
-    pd.r0 = L_row;
-    pd.n = min(C::SUB, L_hi - L_row);
-    pd.first = L_row == L_lo;
-    pd.last = L_row + C::SUB >= L_hi;
-    pd.dense = L_dense;
-    pd.qbuf = L_qbuf;
-    pd_pos = 0;  // rows past the end read position 0 (valid memory, masked by qm = 0)
-    pd_qm = 0;
-    if (lane < pd.n) {
+    pd2.item = L_item;
+    pd2.bk = L_bk;
+    pd2.r0 = L_row;
+    pd2.n = min(C::SUB, L_hi - L_row);
+    pd2.first = L_row == L_lo;
+    pd2.last = L_row + C::SUB >= L_hi;
+    pd2.dense = L_dense;
+    pd2.qbuf = 0;
+    pd2_pos = 0;  // rows past the end read position 0 (valid memory, masked by qm = 0)
+    pd2_qm = 0;
+    if (lane < pd2.n) {
       if (L_dense) {
-        pd_pos = (int32_t)(a.dlo + L_row + lane);
-        pd_qm = (1u << G) - 1u;
+        pd2_pos = (int32_t)(a.dlo + L_row + lane);
+        pd2_qm = (1u << G) - 1u;
       } else {
-        pd_pos = __ldg(a.u_pos + (int64_t)L_bk * a.T + L_row + lane);
-        pd_qm = __ldg(a.u_qm + (int64_t)L_bk * a.T + L_row + lane);
+        pd2_pos = __ldg(a.u_pos + (int64_t)L_bk * a.T + L_row + lane);
+        pd2_qm = __ldg(a.u_qm + (int64_t)L_bk * a.T + L_row + lane);
       }
     }
     L_row += C::SUB;
   };
 
+  // pd1 <- pd2, prefetch pd1's K and V rows into L2, advance pd2.
+  auto shift = [&]() {
+    pd1 = pd2;
+    pd1_pos = pd2_pos;
+    pd1_qm = pd2_qm;
+    if (pd1.item >= 0) {
+      if (lane < pd1.n) {
+        const int64_t off = ((int64_t)pd1.bk * a.T + pd1_pos) * C::ROWB;
+#pragma unroll
+        for (int l = 0; l < C::ROWB; l += 128) {
+          asm volatile("prefetch.global.L2 [%0];\n" ::"l"(Kg + off + l));
+          asm volatile("prefetch.global.L2 [%0];\n" ::"l"(Vg + off + l));
+        }
+      }
+      advance();
+    }
+  };
+
   auto issue = [&](int s) {
     unsigned char* st = wsm + s * C::STAGE;
-    if (lane == 0) desc[s] = pd;
-    if (pd.item >= 0) {
-      reinterpret_cast<int32_t*>(st + C::OFF_POS)[lane] = pd_pos;
-      st[C::OFF_QM + lane] = (uint8_t)pd_qm;
-      const unsigned char* kbase = Kg + (int64_t)pd.bk * a.T * C::ROWB;
-      const unsigned char* vbase = Vg + (int64_t)pd.bk * a.T * C::ROWB;
+    if (pd1.item >= 0 && pd1.first) {  // the item's queries ride along with its first sub-chunk
+      L_qbuf = (L_qbuf + 1) % C::S;
+      pd1.qbuf = L_qbuf;
+      const int64_t b = pd1.bk / a.Hkv, kvh = pd1.bk % a.Hkv;
+      const unsigned char* qsrc = Qg + (b * a.Hq + kvh * G) * (int64_t)C::ROWB;
+      unsigned char* qdst = wsm + C::OFF_QRAW + L_qbuf * C::QRAW;
+      for (int t = lane; t < C::QRAW / 16; t += 32) cp_async16(qdst + t * 16, qsrc + t * 16);
+    }
+    if (lane == 0) desc[s] = pd1;
+    if (pd1.item >= 0) {
+      reinterpret_cast<int32_t*>(st + C::OFF_POS)[lane] = pd1_pos;
+      st[C::OFF_QM + lane] = (uint8_t)pd1_qm;
+      const unsigned char* kbase = Kg + (int64_t)pd1.bk * a.T * C::ROWB;
+      const unsigned char* vbase = Vg + (int64_t)pd1.bk * a.T * C::ROWB;
 #pragma unroll 4
       for (int t = lane; t < C::SUB * C::PIECES; t += 32) {
         const int r = t / C::PIECES, p = t % C::PIECES;
-        const int32_t pr = __shfl_sync(FULL, pd_pos, r);
-        if (r < pd.n) {
+        const int32_t pr = __shfl_sync(FULL, pd1_pos, r);
+        if (r < pd1.n) {
           cp_async16(st + r * C::ROWB + swz(r, p) * 16, kbase + (int64_t)pr * C::ROWB + p * 16);
           if (C::V_SMEM) cp_async16(st + C::OFF_V + r * C::ROWB + p * 16, vbase + (int64_t)pr * C::ROWB + p * 16);
         }
       }
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
-    if (pd.item >= 0) advance();
+    shift();
   };
 
+  pd2.item = 0;
   advance();
+  shift();
 #pragma unroll
   for (int s = 0; s < C::S; ++s) issue(s);
 
