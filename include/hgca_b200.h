@@ -121,9 +121,12 @@ int hgca_decode_config(int dtype, int64_t d, int64_t group, int64_t* out5);
  * engine.py:177-191); mode 1 = replace (StoreTier.reevaluate, sparsifier.py:158-177). */
 int hgca_maw_update(const float* w, int64_t BH, int64_t nq, int64_t W, int64_t w_ld, double* maw,
                     int64_t T, int64_t p0, int64_t w_old, double alpha, int mode, hgca_stream_t stream);
+/* Union of the Hq/Hkv query heads' selection masks per (batch, kv-head),
+ * grouped by query-head mask; also the sparse work-item prefix item_off
+ * [B*Hkv+1] and table item_tab [max items][4] = (bk, lo, hi, 0). */
 int hgca_union_build(const uint32_t* sel_mask, int64_t B, int64_t Hq, int64_t Hkv, int64_t words,
                      int64_t n_arch, int64_t T, int32_t* u_pos, uint8_t* u_qm, int32_t* u_cnt,
-                     int32_t* item_off, int64_t sparse_rows, hgca_stream_t stream);
+                     int32_t* item_off, int32_t* item_tab, int64_t sparse_rows, hgca_stream_t stream);
 
 typedef struct hgca_decode_desc {
   int32_t dtype;            /* HGCA_DTYPE_F32 or HGCA_DTYPE_BF16 (storage) */
@@ -141,6 +144,7 @@ typedef struct hgca_decode_desc {
   const uint8_t* u_qm;
   const int32_t* u_cnt;
   const int32_t* item_off;
+  const int32_t* item_tab;  /* [items][4] from hgca_union_build */
   double* dsc;              /* [B*Hq, dsc_ld] fp64 scratch, dsc_ld >= dhi-dlo */
   int64_t dsc_ld;
   double* part_m;           /* [max_items*G] */

@@ -33,7 +33,7 @@ class DecodeDesc(ctypes.Structure):
         ("scale", D),
         ("dlo", I64), ("dhi", I64), ("w_old", I64),
         ("dense_rows", I64), ("sparse_rows", I64),
-        ("u_pos", P), ("u_qm", P), ("u_cnt", P), ("item_off", P),
+        ("u_pos", P), ("u_qm", P), ("u_cnt", P), ("item_off", P), ("item_tab", P),
         ("dsc", P), ("dsc_ld", I64),
         ("part_m", P), ("part_z", P), ("part_acc", P), ("max_items", I64),
         ("counter", P),
@@ -62,7 +62,7 @@ _SIGS = {
     "hgca_decode_chunk_rows": [I32, I64],
     "hgca_decode_config": [I32, I64, I64, P],
     "hgca_maw_update": [P, I64, I64, I64, I64, P, I64, I64, I64, D, I32, P],
-    "hgca_union_build": [P, I64, I64, I64, I64, I64, I64, P, P, P, P, I64, P],
+    "hgca_union_build": [P, I64, I64, I64, I64, I64, I64, P, P, P, P, P, I64, P],
     "hgca_decode_step": [ctypes.POINTER(DecodeDesc), P],
     "hgca_decode_partial": [ctypes.POINTER(DecodeDesc), P],
     "hgca_decode_merge": [ctypes.POINTER(DecodeDesc), P],

@@ -242,12 +242,13 @@ int hgca_maw_update(const float* w, int64_t BH, int64_t nq, int64_t W, int64_t w
 
 int hgca_union_build(const uint32_t* sel_mask, int64_t B, int64_t Hq, int64_t Hkv, int64_t words,
                      int64_t n_arch, int64_t T, int32_t* u_pos, uint8_t* u_qm, int32_t* u_cnt,
-                     int32_t* item_off, int64_t sparse_rows, hgca_stream_t stream) {
+                     int32_t* item_off, int32_t* item_tab, int64_t sparse_rows, hgca_stream_t stream) {
   if (B < 1 || Hkv < 1 || Hq % Hkv || Hq / Hkv > 8 || n_arch < 0 || n_arch > T || words * 32 < n_arch ||
       sparse_rows < 1)
     return fail(HGCA_EINVAL, "union_build: bad shape");
+  if (!item_tab) return fail(HGCA_EINVAL, "union_build: null item table");
   return cuda_status(launch_union_build(sel_mask, B, Hq, Hkv, words, n_arch, T, u_pos, u_qm, u_cnt,
-                                        item_off, sparse_rows, S(stream)),
+                                        item_off, reinterpret_cast<int4*>(item_tab), sparse_rows, S(stream)),
                      "union_build");
 }
 
@@ -271,7 +272,7 @@ static int decode_prepare(const hgca_decode_desc* d, DecodeArgs& a, DecodeMergeA
   if (d->max_items < n_dense + max_sparse)
     return fail(HGCA_EINVAL, "decode_step: partial buffers hold %lld items, need %lld",
                 (long long)d->max_items, (long long)(n_dense + max_sparse));
-  if (!d->K || !d->V || !d->q || !d->u_pos || !d->u_qm || !d->u_cnt || !d->item_off || !d->dsc ||
+  if (!d->K || !d->V || !d->q || !d->u_pos || !d->u_qm || !d->u_cnt || !d->item_off || !d->item_tab || !d->dsc ||
       !d->part_m || !d->part_z || !d->part_acc || !d->counter || !d->out || !d->lse)
     return fail(HGCA_EINVAL, "decode_step: null pointer");
   a = DecodeArgs{};
@@ -281,6 +282,7 @@ static int decode_prepare(const hgca_decode_desc* d, DecodeArgs& a, DecodeMergeA
   a.dlo = d->dlo; a.dhi = d->dhi;
   a.Sd = Sd; a.dense_rows = d->dense_rows;
   a.u_pos = d->u_pos; a.u_qm = d->u_qm; a.u_cnt = d->u_cnt; a.item_off = d->item_off;
+  a.item_tab = reinterpret_cast<const int4*>(d->item_tab);
   a.sparse_rows = d->sparse_rows;
   a.dsc = d->dsc; a.dsc_ld = d->dsc_ld;
   a.part_m = d->part_m; a.part_z = d->part_z; a.part_acc = d->part_acc;

@@ -53,7 +53,10 @@ struct DecodeCfg {
   static constexpr int OFF_DESC = OFF_MZ + G * 16;
   static constexpr int WARP_SMEM = ((OFF_DESC + S * 32) + 127) / 128 * 128;
   static constexpr int NC0 = (232448 - 2048) / WARP_SMEM;
-  static constexpr int NC = NC0 > 16 ? 16 : NC0;        // warps per CTA
+  // warps per CTA: a multiple of 4 so every SM sub-partition holds the same
+  // number of warps (a 9th warp would cap registers at 168/thread)
+  static constexpr int NC1 = NC0 > 16 ? 16 : NC0;
+  static constexpr int NC = NC1 >= 4 ? (NC1 / 4) * 4 : NC1;
   static constexpr int SMEM = NC * WARP_SMEM;
   static_assert(NC >= 1, "decode warp pipeline does not fit shared memory");
   static_assert(D % 32 == 0, "head_dim must be a multiple of 32");
@@ -93,7 +96,7 @@ __device__ __forceinline__ void load_v_f32<float, 2>(const unsigned char* p, flo
 }
 
 template <typename T, int D, int G>
-__global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) __maxnreg__((DecodeCfg<T, D, G>::NC * 32 > 256 ? 224 : 255)) decode_partial_kernel(const DecodeArgs a) {
+__global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial_kernel(const DecodeArgs a) {
   using C = DecodeCfg<T, D, G>;
   extern __shared__ __align__(128) unsigned char sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -115,9 +118,10 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) __maxnreg__((D
   // own S-stage cp.async ring. The cursor runs ahead across item boundaries;
   // the union entries (position, query-head mask) of the next sub-chunk are
   // prefetched into registers one issue ahead.
+  // next_item: lane 0 holds the id of the item after the current one (its
+  // atomic was issued one item earlier, so reading it never waits).
   int next_item = 0;
   if (lane == 0) next_item = atomicAdd(a.counter, 1);
-  next_item = __shfl_sync(FULL, next_item, 0);
   int L_item = -1, L_bk = 0, L_hi = 0, L_row = 0, L_lo = 0, L_dense = 0, L_qbuf = C::S - 1;
   // Two pending descriptors: pd1 = next sub-chunk to cp.async (positions
   // known, its rows already prefetched into L2), pd2 = the one after (its
@@ -128,13 +132,13 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) __maxnreg__((D
 
   auto advance = [&]() {  // form pd2 for the next sub-chunk and start its metadata loads
     if (L_item < 0 || L_row >= L_hi) {
-      if (next_item >= total) {
+      const int item = __shfl_sync(FULL, next_item, 0);
+      if (item >= total) {
         pd2.item = -1;
         return;
       }
-      L_item = next_item;
+      L_item = item;
       if (lane == 0) next_item = atomicAdd(a.counter, 1);
-      next_item = __shfl_sync(FULL, next_item, 0);
       if (L_item < a.n_dense_items) {
         L_dense = 1;
         L_bk = (int)(L_item / a.Sd);
@@ -142,15 +146,10 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) __maxnreg__((D
         L_hi = (int)min(W, (int64_t)L_lo + a.dense_rows);
       } else {
         L_dense = 0;
-        const int x = L_item - (int)a.n_dense_items;
-        int64_t l = 0, r = BK;  // largest bk with item_off[bk] <= x
-        while (r - l > 1) {
-          const int64_t mid = (l + r) >> 1;
-          if (a.item_off[mid] <= x) l = mid; else r = mid;
-        }
-        L_bk = (int)l;
-        L_lo = (int)((x - a.item_off[l]) * a.sparse_rows);
-        L_hi = (int)min((int64_t)a.u_cnt[l], (int64_t)L_lo + a.sparse_rows);
+        const int4 e = __ldg(a.item_tab + (L_item - (int)a.n_dense_items));  // (bk, lo, hi, -)
+        L_bk = e.x;
+        L_lo = e.y;
+        L_hi = e.z;
       }
       L_row = L_lo;
     }
@@ -593,6 +592,18 @@ __global__ void item_offsets_kernel(const int32_t* u_cnt, int64_t BK, int64_t ro
   if (tid == 0) off[BK] = carry;
 }
 
+// item_tab[item_off[bk] + i] = (bk, i*rows, min(u_cnt[bk], (i+1)*rows), 0)
+__global__ void item_table_kernel(const int32_t* u_cnt, const int32_t* off, int64_t BK, int64_t rows,
+                                  int4* tab) {
+  const int64_t bk = blockIdx.x;
+  if (bk >= BK) return;
+  const int n = off[bk + 1] - off[bk];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int lo = (int)(i * rows);
+    tab[off[bk] + i] = make_int4((int)bk, lo, (int)min((int64_t)u_cnt[bk], (int64_t)lo + rows), 0);
+  }
+}
+
 // K/V[bh, pos + i, :] = new[bh, i, :]  (append_kv into the position buffer)
 __global__ void write_rows_kernel(unsigned char* K, unsigned char* V, int64_t BH, int64_t T,
                                   int64_t rowb, int64_t pos, const unsigned char* kn,
@@ -665,13 +676,16 @@ int launch_decode_merge(const DecodeMergeArgs& a, cudaStream_t s) {
 
 int launch_union_build(const uint32_t* sel, int64_t B, int64_t Hq, int64_t Hkv, int64_t words,
                        int64_t n_arch, int64_t T, int32_t* u_pos, uint8_t* u_qm, int32_t* u_cnt,
-                       int32_t* item_off, int64_t sparse_rows, cudaStream_t s) {
+                       int32_t* item_off, int4* item_tab, int64_t sparse_rows, cudaStream_t s) {
   const int64_t G = Hq / Hkv;
   union_build_kernel<<<(unsigned)(B * Hkv), 1024, 0, s>>>(sel, Hq, Hkv, G, words, n_arch, T, u_pos,
                                                           u_qm, u_cnt);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
   item_offsets_kernel<<<1, 1024, 0, s>>>(u_cnt, B * Hkv, sparse_rows, item_off);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return (int)e;
+  item_table_kernel<<<(unsigned)(B * Hkv), 128, 0, s>>>(u_cnt, item_off, B * Hkv, sparse_rows, item_tab);
   return (int)cudaGetLastError();
 }
 

@@ -55,6 +55,7 @@ struct DecodeArgs {
   const uint8_t* u_qm;    // [B*Hkv, T] query-head masks
   const int32_t* u_cnt;   // [B*Hkv]
   const int32_t* item_off;// [B*Hkv + 1] sparse item prefix
+  const int4* item_tab;   // [sparse items] (bk, lo, hi, 0)
   int64_t sparse_rows;    // rows per sparse item
   double* dsc;            // [B*Hq, dsc_ld] dense scores (fp64) for the MAW update
   int64_t dsc_ld;
@@ -105,7 +106,7 @@ int launch_decode_partial(int dtype, const DecodeArgs& a, cudaStream_t s);
 int launch_decode_merge(const DecodeMergeArgs& a, cudaStream_t s);
 int launch_union_build(const uint32_t* sel, int64_t B, int64_t Hq, int64_t Hkv, int64_t words,
                        int64_t n_arch, int64_t T, int32_t* u_pos, uint8_t* u_qm, int32_t* u_cnt,
-                       int32_t* item_off, int64_t sparse_rows, cudaStream_t s);
+                       int32_t* item_off, int4* item_tab, int64_t sparse_rows, cudaStream_t s);
 int launch_write_rows(int dtype, void* K, void* V, int64_t BH, int64_t T, int64_t D, int64_t pos,
                       const void* k_new, const void* v_new, int64_t n, cudaStream_t s);
 int decode_chunk_rows(int dtype, int64_t D);

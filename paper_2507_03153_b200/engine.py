@@ -169,6 +169,7 @@ class LayerState:
         self.u_qm = torch.zeros((B * Hkv, T), dtype=torch.uint8, device=dev)
         self.u_cnt = torch.zeros(B * Hkv, dtype=torch.int32, device=dev)
         self.item_off = torch.zeros(B * Hkv + 1, dtype=torch.int32, device=dev)
+        self.item_tab = torch.zeros((B * Hkv * (T // 32 + 1), 4), dtype=torch.int32, device=dev)
         self.lo = 0    # archive size
         self.nxt = 0   # next position
 
@@ -253,7 +254,7 @@ class HybridEngine:
         self.launches += 2 + (3 if (self.g_pad > 1 and n) else 0) + (1 if self.config.selection == "topk" and n else 0)
         _lib.call("hgca_union_build", ls.sel.data_ptr(), self.B, self.Hq, self.Hkv, words, n, self.T,
                   ls.u_pos.data_ptr(), ls.u_qm.data_ptr(), ls.u_cnt.data_ptr(), ls.item_off.data_ptr(),
-                  SPARSE_ROWS, s)
+                  ls.item_tab.data_ptr(), SPARSE_ROWS, s)
 
     def _ingest(self, ls: LayerState, lo, hi, divisor):
         """StoreTier.ingest_evicted of positions [lo, hi) (sparsifier.py:127-156)."""
@@ -368,6 +369,7 @@ class HybridEngine:
         d.dense_rows, d.sparse_rows = DENSE_ROWS, SPARSE_ROWS
         d.u_pos, d.u_qm, d.u_cnt, d.item_off = (ls.u_pos.data_ptr(), ls.u_qm.data_ptr(),
                                                 ls.u_cnt.data_ptr(), ls.item_off.data_ptr())
+        d.item_tab = ls.item_tab.data_ptr()
         d.dsc, d.dsc_ld = self.dsc.data_ptr(), self.dsc_ld
         d.part_m, d.part_z, d.part_acc = self.part_m.data_ptr(), self.part_z.data_ptr(), self.part_acc.data_ptr()
         d.max_items = self.max_items
