@@ -393,30 +393,82 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial
 //   w   = float32(exp(s - m) / z)                     (_core.pyx:81-82)
 //   maw = (1-alpha)*maw + alpha*w   (3 roundings)     (kv_cache.py:186)
 //   new entries: maw = w                              (engine.py:191)
-__global__ void __launch_bounds__(128) decode_merge_kernel(const DecodeMergeArgs a) {
+constexpr int MERGE_THREADS = 512;
+
+__device__ __forceinline__ double block_reduce_max(double v, double* red) {
+  v = warp_max_f64(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double r = -INFINITY;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) r = fmax(r, red[i]);
+  return r;
+}
+
+__device__ __forceinline__ double block_reduce_sum(double v, double* red) {
+  v = warp_sum_f64(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) r += red[i];  // fixed order
+  return r;
+}
+
+// One CTA (512 threads) per (batch, query head).
+__global__ void __launch_bounds__(MERGE_THREADS) decode_merge_kernel(const DecodeMergeArgs a) {
+  __shared__ double wgt[MERGE_THREADS];
+  __shared__ double red[32];
+  __shared__ double part[MERGE_THREADS];
   const int64_t bq = blockIdx.x;
   const int64_t b = bq / a.Hq, h = bq % a.Hq;
   const int64_t kvh = h / a.G, g = h % a.G;
   const int64_t bk = b * a.Hkv + kvh;
   const int tid = threadIdx.x;
-  __shared__ double Md_s, Zd_s;
-  // dense fold
-  double Md = -INFINITY;
-  for (int64_t i = 0; i < a.Sd; ++i) Md = fmax(Md, a.part_m[(bk * a.Sd + i) * a.G + g]);
-  double Zd = 0.0;
-  for (int64_t i = 0; i < a.Sd; ++i) {
-    const double mi = a.part_m[(bk * a.Sd + i) * a.G + g];
-    if (mi != -INFINITY) Zd += a.part_z[(bk * a.Sd + i) * a.G + g] * exp(mi - Md);
-  }
-  // sparse fold
-  const int64_t i0 = a.n_dense_items + a.item_off[bk], i1 = a.n_dense_items + a.item_off[bk + 1];
-  double Ms = -INFINITY;
-  for (int64_t i = i0; i < i1; ++i) Ms = fmax(Ms, a.part_m[i * a.G + g]);
-  double Zs = 0.0;
-  for (int64_t i = i0; i < i1; ++i) {
-    const double mi = a.part_m[i * a.G + g];
-    if (mi != -INFINITY) Zs += a.part_z[i * a.G + g] * exp(mi - Ms);
-  }
+  const int64_t D = a.D;
+  const int P = (int)(MERGE_THREADS / D);  // item lanes per dim
+  const int c = tid % (int)D, pl = tid / (int)D;
+  const int64_t d0 = bk * a.Sd, d1 = d0 + a.Sd;
+  const int64_t s0 = a.n_dense_items + a.item_off[bk], s1 = a.n_dense_items + a.item_off[bk + 1];
+  // fold items [i0, i1): M = max m_i, w_i = exp(m_i - M), Z = sum z_i w_i, acc_c = sum w_i acc_i[c]
+  auto fold = [&](int64_t i0, int64_t i1, double& M, double& Z) -> double {
+    double mx = -INFINITY;
+    for (int64_t i = i0 + tid; i < i1; i += MERGE_THREADS) mx = fmax(mx, a.part_m[i * a.G + g]);
+    M = block_reduce_max(mx, red);
+    double zl = 0.0, acc = 0.0;
+    for (int64_t c0 = i0; c0 < i1; c0 += MERGE_THREADS) {
+      const int64_t n = min((int64_t)MERGE_THREADS, i1 - c0);
+      __syncthreads();
+      if (tid < n) {
+        const double mi = a.part_m[(c0 + tid) * a.G + g];
+        const double w = (mi == -INFINITY) ? 0.0 : exp(mi - M);
+        wgt[tid] = w;
+        zl += w == 0.0 ? 0.0 : a.part_z[(c0 + tid) * a.G + g] * w;
+      }
+      __syncthreads();
+      if (pl < P) {
+        const float* pa = a.part_acc + (c0 * a.G + g) * D + c;
+#pragma unroll 8
+        for (int64_t j = pl; j < n; j += P) {
+          const double w = wgt[j];
+          if (w != 0.0) acc += w * (double)pa[j * a.G * D];
+        }
+      }
+    }
+    Z = block_reduce_sum(zl, red);
+    __syncthreads();
+    part[tid] = acc;
+    __syncthreads();
+    double t = 0.0;
+    if (tid < D)
+      for (int q = 0; q < P; ++q) t += part[q * D + tid];  // fixed order over item lanes
+    return t;
+  };
+  double Md, Zd, Ms, Zs;
+  const double acc_d = fold(d0, d1, Md, Zd);
+  const double acc_s = fold(s0, s1, Ms, Zs);
   const bool s_empty = !(Zs > 0.0);
   const bool d_empty = !(Zd > 0.0);
   const double lse_s = s_empty ? -INFINITY : Ms + log(Zs);
@@ -428,31 +480,19 @@ __global__ void __launch_bounds__(128) decode_merge_kernel(const DecodeMergeArgs
   const double wa = exp(lse_s - ms), wb = exp(lse_d - ms);
   const double zs = both_empty ? 1.0 : wa + wb;
   const float ca = (float)(wa / zs), cb = (float)(wb / zs);
-  for (int64_t c = tid; c < a.D; c += blockDim.x) {
-    double ad = 0.0, as = 0.0;
-    for (int64_t i = 0; i < a.Sd; ++i) {
-      const double mi = a.part_m[(bk * a.Sd + i) * a.G + g];
-      if (mi != -INFINITY) ad += (double)a.part_acc[((bk * a.Sd + i) * a.G + g) * a.D + c] * exp(mi - Md);
-    }
-    for (int64_t i = i0; i < i1; ++i) {
-      const double mi = a.part_m[i * a.G + g];
-      if (mi != -INFINITY) as += (double)a.part_acc[(i * a.G + g) * a.D + c] * exp(mi - Ms);
-    }
-    const float od = d_empty ? 0.f : (float)(ad / Zd);
-    const float os = s_empty ? 0.f : (float)(as / Zs);
-    a.out[bq * a.D + c] = __fadd_rn(__fmul_rn(ca, os), __fmul_rn(cb, od));
-    if (a.out_sparse) a.out_sparse[bq * a.D + c] = os;
+  if (tid < D) {
+    const float od = d_empty ? 0.f : (float)(acc_d / Zd);
+    const float os = s_empty ? 0.f : (float)(acc_s / Zs);
+    a.out[bq * D + tid] = __fadd_rn(__fmul_rn(ca, os), __fmul_rn(cb, od));
+    if (a.out_sparse) a.out_sparse[bq * D + tid] = os;
   }
   if (tid == 0) {
     a.lse[bq] = both_empty ? -INFINITY : ms + log(zs);
     if (a.lse_sparse) a.lse_sparse[bq] = lse_s;
-    Md_s = Md;
-    Zd_s = Zd;
   }
-  __syncthreads();
   if (a.maw == nullptr && a.wts_out == nullptr) return;
-  for (int64_t j = tid; j < a.W; j += blockDim.x) {
-    const float w32 = d_empty ? 0.f : (float)(exp(a.dsc[bq * a.dsc_ld + j] - Md_s) / Zd_s);
+  for (int64_t j = tid; j < a.W; j += MERGE_THREADS) {
+    const float w32 = d_empty ? 0.f : (float)(exp(a.dsc[bq * a.dsc_ld + j] - Md) / Zd);
     if (a.wts_out) a.wts_out[bq * a.W + j] = w32;
     if (a.maw) {
       double* mp = a.maw + bq * a.T + a.dlo + j;
@@ -670,7 +710,7 @@ int launch_decode_partial(int dtype, const DecodeArgs& a, cudaStream_t s) {
 }
 
 int launch_decode_merge(const DecodeMergeArgs& a, cudaStream_t s) {
-  decode_merge_kernel<<<(unsigned)(a.B * a.Hq), 128, 0, s>>>(a);
+  decode_merge_kernel<<<(unsigned)(a.B * a.Hq), MERGE_THREADS, 0, s>>>(a);
   return (int)cudaGetLastError();
 }
 
