@@ -24,6 +24,8 @@
 #include "hgca_common.cuh"
 #include "hgca_internal.h"
 
+#include <cuda.h>
+
 namespace hgca {
 
 template <typename T, int D, int G>
@@ -33,30 +35,34 @@ struct DecodeCfg {
   static constexpr int SUB = 32;                        // rows per sub-chunk (one per lane)
   static constexpr int PIECES = ROWB / 16;
   static constexpr int E = 16 / ESZ;                    // elements per 16-byte piece
-  // bf16: fp32 partial per 16-byte piece (8 exact products), fp64 across
-  // pieces. fp32: per-element fp64 DFMA in the reference's sequential order.
+  // bf16: K rows gathered by TMA (tile::gather4, 4 rows per op) into dense
+  // rows, read with a per-lane piece rotation; QK in fp32 per 16-byte piece
+  // (8 exact products) accumulated in fp64; V rows gathered into registers.
+  // fp32 (reference-exact path): cp.async into XOR-swizzled rows, per-element
+  // fp64 DFMA in the reference's sequential order, V staged in smem.
+  static constexpr bool TMA = ESZ == 2;
   static constexpr bool PIECE32 = ESZ == 2;
-  static constexpr bool V_SMEM = ESZ == 4;              // fp32: V staged in smem; bf16: V in registers
+  static constexpr bool V_SMEM = ESZ == 4;
   static constexpr int DPL = D / 32;                    // dims per lane in P.V
-  static constexpr int S = 2;                           // K stages per warp
-  static constexpr int OFF_V = SUB * ROWB;              // K rows are XOR-swizzled per 16-byte piece
+  static constexpr int S = TMA ? 3 : 2;                 // stages per warp
+  static constexpr int OFF_V = SUB * ROWB;
   static constexpr int OFF_POS = OFF_V + (V_SMEM ? SUB * ROWB : 0);
   static constexpr int OFF_QM = OFF_POS + SUB * 4;
-  static constexpr int STAGE = ((OFF_QM + SUB) + 15) / 16 * 16;
+  static constexpr int STAGE = ((OFF_QM + SUB) + 127) / 128 * 128;
   static constexpr int QRAW = G * ROWB;                 // raw query block of one item
+  static constexpr int NQB = S;                         // raw query buffers
   static constexpr int QK_ESZ = PIECE32 ? 4 : 8;
   static constexpr int OFF_QRAW = S * STAGE;
-  static constexpr int OFF_QK = OFF_QRAW + S * QRAW;    // queries [G][D] (fp32 or fp64)
+  static constexpr int OFF_QK = OFF_QRAW + NQB * QRAW;  // queries [G][D] (fp32 or fp64)
   static constexpr int OFF_SC = OFF_QK + G * D * QK_ESZ;// scores [G][32] fp64
   static constexpr int OFF_ACC = OFF_SC + G * SUB * 8;  // P.V accumulators [G][D] fp32
   static constexpr int OFF_MZ = OFF_ACC + G * D * 4;    // running (m, z) [G][2] fp64
-  static constexpr int OFF_DESC = OFF_MZ + G * 16;
+  static constexpr int OFF_BAR = OFF_MZ + G * 16;       // mbarriers [S]
+  static constexpr int OFF_DESC = OFF_BAR + S * 8;
   static constexpr int WARP_SMEM = ((OFF_DESC + S * 32) + 127) / 128 * 128;
   static constexpr int NC0 = (232448 - 2048) / WARP_SMEM;
-  // warps per CTA: a multiple of 4 so every SM sub-partition holds the same
-  // number of warps (a 9th warp would cap registers at 168/thread)
-  static constexpr int NC1 = NC0 > 16 ? 16 : NC0;
-  static constexpr int NC = NC1 >= 4 ? (NC1 / 4) * 4 : NC1;
+  // <= 8 warps: at most 2 per SM sub-partition, so 255 registers per thread
+  static constexpr int NC = NC0 > 8 ? 8 : NC0;
   static constexpr int SMEM = NC * WARP_SMEM;
   static_assert(NC >= 1, "decode warp pipeline does not fit shared memory");
   static_assert(D % 32 == 0, "head_dim must be a multiple of 32");
@@ -95,37 +101,56 @@ __device__ __forceinline__ void load_v_f32<float, 2>(const unsigned char* p, flo
   out[0] = v.x; out[1] = v.y;
 }
 
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, int col, int r0, int r1, int r2,
+                                            int r3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 template <typename T, int D, int G>
-__global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial_kernel(const DecodeArgs a) {
+__global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial_kernel(const __grid_constant__ DecodeArgs a) {
   using C = DecodeCfg<T, D, G>;
   extern __shared__ __align__(128) unsigned char sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t FULL = 0xffffffffu;
   unsigned char* wsm = sm + warp * C::WARP_SMEM;
   StageDesc* desc = reinterpret_cast<StageDesc*>(wsm + C::OFF_DESC);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wsm + C::OFF_BAR);
   double* sc = reinterpret_cast<double*>(wsm + C::OFF_SC);
   float* accs = reinterpret_cast<float*>(wsm + C::OFF_ACC);
   double* mz = reinterpret_cast<double*>(wsm + C::OFF_MZ);
-  const int64_t BK = a.B * a.Hkv;
   const int64_t W = a.dhi - a.dlo;
-  const int total = (int)(a.n_dense_items + (int64_t)a.item_off[BK]);
+  const int total = (int)(a.n_dense_items + (int64_t)a.item_off[a.B * a.Hkv]);
   const unsigned char* Kg = reinterpret_cast<const unsigned char*>(a.K);
   const unsigned char* Vg = reinterpret_cast<const unsigned char*>(a.V);
   const unsigned char* Qg = reinterpret_cast<const unsigned char*>(a.q);
+  if constexpr (C::TMA) {
+    if (lane < C::S) mbar_init(&bar[lane], 1);
+    fence_mbar_init();
+    __syncwarp();
+  }
 
   // ---------------------------------------------------------- load cursor
   // Each warp streams whole work items (dynamic, global counter) through its
-  // own S-stage cp.async ring. The cursor runs ahead across item boundaries;
-  // the union entries (position, query-head mask) of the next sub-chunk are
-  // prefetched into registers one issue ahead.
-  // next_item: lane 0 holds the id of the item after the current one (its
-  // atomic was issued one item earlier, so reading it never waits).
-  int next_item = 0;
+  // own S-stage ring. The cursor runs ahead across item boundaries; the union
+  // entries (position, query-head mask) of a sub-chunk are loaded one issue
+  // ahead (pd2) and its rows are prefetched into L2 (bf16: V) when it becomes
+  // pd1, the next sub-chunk to issue.
+  int next_item = 0;  // lane 0: id of the item after the current one
   if (lane == 0) next_item = atomicAdd(a.counter, 1);
-  int L_item = -1, L_bk = 0, L_hi = 0, L_row = 0, L_lo = 0, L_dense = 0, L_qbuf = C::S - 1;
-  // Two pending descriptors: pd1 = next sub-chunk to cp.async (positions
-  // known, its rows already prefetched into L2), pd2 = the one after (its
-  // position/mask loads in flight).
+  int L_item = -1, L_bk = 0, L_hi = 0, L_row = 0, L_lo = 0, L_dense = 0, L_qbuf = C::NQB - 1;
   StageDesc pd1, pd2;
   int32_t pd1_pos = 0, pd2_pos = 0;
   uint32_t pd1_qm = 0, pd2_qm = 0;
@@ -175,18 +200,16 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial
     L_row += C::SUB;
   };
 
-  // pd1 <- pd2, prefetch pd1's K and V rows into L2, advance pd2.
-  auto shift = [&]() {
+  auto shift = [&]() {  // pd1 <- pd2; warm L2 with pd1's V rows (bf16); advance pd2
     pd1 = pd2;
     pd1_pos = pd2_pos;
     pd1_qm = pd2_qm;
     if (pd1.item >= 0) {
-      if (lane < pd1.n) {
-        const int64_t off = ((int64_t)pd1.bk * a.T + pd1_pos) * C::ROWB;
+      if constexpr (!C::V_SMEM) {
+        if (lane < pd1.n) {
+          const int64_t off = ((int64_t)pd1.bk * a.T + pd1_pos) * C::ROWB;
 #pragma unroll
-        for (int l = 0; l < C::ROWB; l += 128) {
-          asm volatile("prefetch.global.L2 [%0];\n" ::"l"(Kg + off + l));
-          asm volatile("prefetch.global.L2 [%0];\n" ::"l"(Vg + off + l));
+          for (int l = 0; l < C::ROWB; l += 128) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(Vg + off + l));
         }
       }
       advance();
@@ -195,31 +218,47 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial
 
   auto issue = [&](int s) {
     unsigned char* st = wsm + s * C::STAGE;
-    if (pd1.item >= 0 && pd1.first) {  // the item's queries ride along with its first sub-chunk
-      L_qbuf = (L_qbuf + 1) % C::S;
+    if (pd1.item >= 0 && pd1.first) {
+      L_qbuf = (L_qbuf + 1) % C::NQB;
       pd1.qbuf = L_qbuf;
-      const int64_t b = pd1.bk / a.Hkv, kvh = pd1.bk % a.Hkv;
-      const unsigned char* qsrc = Qg + (b * a.Hq + kvh * G) * (int64_t)C::ROWB;
-      unsigned char* qdst = wsm + C::OFF_QRAW + L_qbuf * C::QRAW;
-      for (int t = lane; t < C::QRAW / 16; t += 32) cp_async16(qdst + t * 16, qsrc + t * 16);
     }
     if (lane == 0) desc[s] = pd1;
     if (pd1.item >= 0) {
       reinterpret_cast<int32_t*>(st + C::OFF_POS)[lane] = pd1_pos;
       st[C::OFF_QM + lane] = (uint8_t)pd1_qm;
-      const unsigned char* kbase = Kg + (int64_t)pd1.bk * a.T * C::ROWB;
-      const unsigned char* vbase = Vg + (int64_t)pd1.bk * a.T * C::ROWB;
+      const int64_t b = pd1.bk / a.Hkv, kvh = pd1.bk % a.Hkv;
+      const unsigned char* qsrc = Qg + (b * a.Hq + kvh * G) * (int64_t)C::ROWB;
+      unsigned char* qdst = wsm + C::OFF_QRAW + pd1.qbuf * C::QRAW;
+      if constexpr (C::TMA) {
+        // 8 gather4 ops (4 rows each) + the item's queries on this stage's mbarrier
+        const int rowbase = pd1.bk * (int)a.T;
+        const int q0 = __shfl_sync(FULL, pd1_pos, (lane & 7) * 4 + 0);
+        const int q1 = __shfl_sync(FULL, pd1_pos, (lane & 7) * 4 + 1);
+        const int q2 = __shfl_sync(FULL, pd1_pos, (lane & 7) * 4 + 2);
+        const int q3 = __shfl_sync(FULL, pd1_pos, (lane & 7) * 4 + 3);
+        if (lane == 0) mbar_expect_tx(&bar[s], C::SUB * C::ROWB + (pd1.first ? C::QRAW : 0));
+        __syncwarp();
+        if (lane < 8)
+          tma_gather4(st + lane * 4 * C::ROWB, &a.kmap, 0, rowbase + q0, rowbase + q1, rowbase + q2,
+                      rowbase + q3, &bar[s]);
+        if (lane == 8 && pd1.first) bulk_g2s(qdst, qsrc, C::QRAW, &bar[s]);
+      } else {
+        if (pd1.first)
+          for (int t = lane; t < C::QRAW / 16; t += 32) cp_async16(qdst + t * 16, qsrc + t * 16);
+        const unsigned char* kbase = Kg + (int64_t)pd1.bk * a.T * C::ROWB;
+        const unsigned char* vbase = Vg + (int64_t)pd1.bk * a.T * C::ROWB;
 #pragma unroll 4
-      for (int t = lane; t < C::SUB * C::PIECES; t += 32) {
-        const int r = t / C::PIECES, p = t % C::PIECES;
-        const int32_t pr = __shfl_sync(FULL, pd1_pos, r);
-        if (r < pd1.n) {
-          cp_async16(st + r * C::ROWB + swz(r, p) * 16, kbase + (int64_t)pr * C::ROWB + p * 16);
-          if (C::V_SMEM) cp_async16(st + C::OFF_V + r * C::ROWB + p * 16, vbase + (int64_t)pr * C::ROWB + p * 16);
+        for (int t = lane; t < C::SUB * C::PIECES; t += 32) {
+          const int r = t / C::PIECES, p = t % C::PIECES;
+          const int32_t pr = __shfl_sync(FULL, pd1_pos, r);
+          if (r < pd1.n) {
+            cp_async16(st + r * C::ROWB + swz(r, p) * 16, kbase + (int64_t)pr * C::ROWB + p * 16);
+            if (C::V_SMEM) cp_async16(st + C::OFF_V + r * C::ROWB + p * 16, vbase + (int64_t)pr * C::ROWB + p * 16);
+          }
         }
       }
     }
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    if constexpr (!C::TMA) asm volatile("cp.async.commit_group;\n" ::: "memory");
     shift();
   };
 
@@ -232,7 +271,11 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial
   // ---------------------------------------------------------- compute
   for (int k = 0;; ++k) {
     const int s = k % C::S;
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(C::S - 1) : "memory");
+    if constexpr (C::TMA) {
+      if (desc[s].item >= 0) mbar_wait(&bar[s], (k / C::S) & 1);
+    } else {
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(C::S - 1) : "memory");
+    }
     __syncwarp();
     const StageDesc d = desc[s];
     if (d.item < 0) break;
@@ -276,36 +319,61 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial
     for (int g = 0; g < G; ++g) sacc[g] = 0.0;
     {
       const unsigned char* krow = st + lane * C::ROWB;
+      if constexpr (C::PIECE32) {
+        const float* qk = reinterpret_cast<const float*>(wsm + C::OFF_QK);
+        if (__popc(wq) == 1) {  // single query head (most union chunks): no per-piece branching
+          const int g = __ffs(wq) - 1;
+          double s1 = 0.0;
 #pragma unroll 4
-      for (int p = 0; p < C::PIECES; ++p) {
-        const uint4 raw = *reinterpret_cast<const uint4*>(krow + swz(lane, p) * 16);
-        if constexpr (C::PIECE32) {
-          float kf[8];
-          unpack8<T>(raw, kf);
-          const float* qk = reinterpret_cast<const float*>(wsm + C::OFF_QK);
+          for (int i = 0; i < C::PIECES; ++i) {
+            const int p = (i + lane) & (C::PIECES - 1);  // rotation: conflict-free dense rows
+            float kf[8];
+            unpack8<T>(*reinterpret_cast<const uint4*>(krow + p * 16), kf);
+            const float4 qa = *reinterpret_cast<const float4*>(qk + g * D + p * 8);
+            const float4 qb = *reinterpret_cast<const float4*>(qk + g * D + p * 8 + 4);
+            float part = qa.x * kf[0];
+            part = fmaf(qa.y, kf[1], part);
+            part = fmaf(qa.z, kf[2], part);
+            part = fmaf(qa.w, kf[3], part);
+            part = fmaf(qb.x, kf[4], part);
+            part = fmaf(qb.y, kf[5], part);
+            part = fmaf(qb.z, kf[6], part);
+            part = fmaf(qb.w, kf[7], part);
+            s1 += (double)part;
+          }
 #pragma unroll
-          for (int g = 0; g < G; ++g) {
-            if ((wq >> g) & 1u) {
-              const float4 qa = *reinterpret_cast<const float4*>(qk + g * D + p * 8);
-              const float4 qb = *reinterpret_cast<const float4*>(qk + g * D + p * 8 + 4);
-              float part = qa.x * kf[0];
-              part = fmaf(qa.y, kf[1], part);
-              part = fmaf(qa.z, kf[2], part);
-              part = fmaf(qa.w, kf[3], part);
-              part = fmaf(qb.x, kf[4], part);
-              part = fmaf(qb.y, kf[5], part);
-              part = fmaf(qb.z, kf[6], part);
-              part = fmaf(qb.w, kf[7], part);
-              sacc[g] += (double)part;
+          for (int gg = 0; gg < G; ++gg) sacc[gg] = (gg == g) ? s1 : 0.0;
+        } else {
+#pragma unroll 2
+          for (int i = 0; i < C::PIECES; ++i) {
+            const int p = (i + lane) & (C::PIECES - 1);
+            float kf[8];
+            unpack8<T>(*reinterpret_cast<const uint4*>(krow + p * 16), kf);
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+              if ((wq >> g) & 1u) {
+                const float4 qa = *reinterpret_cast<const float4*>(qk + g * D + p * 8);
+                const float4 qb = *reinterpret_cast<const float4*>(qk + g * D + p * 8 + 4);
+                float part = qa.x * kf[0];
+                part = fmaf(qa.y, kf[1], part);
+                part = fmaf(qa.z, kf[2], part);
+                part = fmaf(qa.w, kf[3], part);
+                part = fmaf(qb.x, kf[4], part);
+                part = fmaf(qb.y, kf[5], part);
+                part = fmaf(qb.z, kf[6], part);
+                part = fmaf(qb.w, kf[7], part);
+                sacc[g] += (double)part;
+              }
             }
           }
-        } else {
-          const float kk[4] = {__uint_as_float(raw.x), __uint_as_float(raw.y), __uint_as_float(raw.z),
-                               __uint_as_float(raw.w)};
-          double kd[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) kd[e] = (double)kk[e];
-          const double* qk = reinterpret_cast<const double*>(wsm + C::OFF_QK);
+        }
+      } else {
+        const double* qk = reinterpret_cast<const double*>(wsm + C::OFF_QK);
+#pragma unroll 4
+        for (int p = 0; p < C::PIECES; ++p) {
+          const uint4 raw = *reinterpret_cast<const uint4*>(krow + swz(lane, p) * 16);
+          const double kd[4] = {(double)__uint_as_float(raw.x), (double)__uint_as_float(raw.y),
+                                (double)__uint_as_float(raw.z), (double)__uint_as_float(raw.w)};
 #pragma unroll
           for (int g = 0; g < G; ++g) {
             if ((wq >> g) & 1u) {
@@ -323,6 +391,7 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial
     const int64_t b = d.bk / a.Hkv, kvh = d.bk % a.Hkv;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
+      if (!((wq >> g) & 1u)) continue;
       const double sv = ((qm >> g) & 1u) ? sacc[g] * a.scale : -INFINITY;
       sc[g * C::SUB + lane] = sv;
       if (d.dense && lane < d.n) a.dsc[(b * a.Hq + kvh * G + g) * a.dsc_ld + (mypos - a.dlo)] = sv;
@@ -348,21 +417,19 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial
 #pragma unroll
       for (int r = 0; r < C::SUB; ++r) {
         const float pr = __shfl_sync(FULL, pf, r);
-        if (pr != 0.f) {
-          float vv[C::DPL];
-          if constexpr (C::V_SMEM) {
-            load_v_f32<T, C::DPL>(st + C::OFF_V + r * C::ROWB + lane * C::DPL * C::ESZ, vv);
-          } else {
-            vv[0] = __uint_as_float(vreg[r].x << 16);
-            vv[1] = __uint_as_float(vreg[r].x & 0xffff0000u);
-            if constexpr (C::DPL == 4) {
-              vv[C::DPL > 2 ? 2 : 0] = __uint_as_float(vreg[r].y << 16);
-              vv[C::DPL > 3 ? 3 : 0] = __uint_as_float(vreg[r].y & 0xffff0000u);
-            }
+        float vv[C::DPL];
+        if constexpr (C::V_SMEM) {
+          load_v_f32<T, C::DPL>(st + C::OFF_V + r * C::ROWB + lane * C::DPL * C::ESZ, vv);
+        } else {
+          vv[0] = __uint_as_float(vreg[r].x << 16);
+          vv[1] = __uint_as_float(vreg[r].x & 0xffff0000u);
+          if constexpr (C::DPL == 4) {
+            vv[C::DPL > 2 ? 2 : 0] = __uint_as_float(vreg[r].y << 16);
+            vv[C::DPL > 3 ? 3 : 0] = __uint_as_float(vreg[r].y & 0xffff0000u);
           }
-#pragma unroll
-          for (int i = 0; i < C::DPL; ++i) acc[i] = fmaf(pr, vv[i], acc[i]);
         }
+#pragma unroll
+        for (int i = 0; i < C::DPL; ++i) acc[i] = fmaf(pr, vv[i], acc[i]);
       }
 #pragma unroll
       for (int i = 0; i < C::DPL; ++i) ag[i] = acc[i];
@@ -383,7 +450,7 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial
     __syncwarp();
     issue(s);
   }
-  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  if constexpr (!C::TMA) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
 // --------------------------------------------------------------------- merge
@@ -662,9 +729,48 @@ __global__ void write_rows_kernel(unsigned char* K, unsigned char* V, int64_t BH
 }
 
 // ------------------------------------------------------------------ launchers
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// 2-D tensor map over the K buffer [B*Hkv*T rows, D] for tile::gather4 (box = one row).
+static int make_row_map(CUtensorMap* map, const void* base, int64_t rows, int64_t D, int esz) {
+  static EncodeTiledFn encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q) != cudaSuccess ||
+        !encode)
+      return -3000;
+  }
+  cuuint64_t gdim[2] = {(cuuint64_t)D, (cuuint64_t)rows};
+  cuuint64_t gstr[1] = {(cuuint64_t)(D * esz)};
+  cuuint32_t box[2] = {(cuuint32_t)D, 1};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode(map, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                      const_cast<void*>(base), gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -3001;
+}
+
 template <typename T, int D, int G>
-static int launch_decode_t(const DecodeArgs& a, cudaStream_t s) {
+static int launch_decode_t(const DecodeArgs& a_in, cudaStream_t s) {
   using C = DecodeCfg<T, D, G>;
+  DecodeArgs a = a_in;
+  if (C::TMA) {
+    // cached per K buffer: encoding is host work only
+    static const void* cached_base = nullptr;
+    static int64_t cached_rows = -1;
+    static CUtensorMap cached;
+    const int64_t rows = a.B * a.Hkv * a.T;
+    if (cached_base != a.K || cached_rows != rows) {
+      const int rc = make_row_map(&cached, a.K, rows, D, C::ESZ);
+      if (rc) return rc;
+      cached_base = a.K;
+      cached_rows = rows;
+    }
+    a.kmap = cached;
+  }
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(decode_partial_kernel<T, D, G>,

@@ -1,5 +1,6 @@
 // Internal argument blocks and launchers (not part of the C ABI).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -43,6 +44,7 @@ struct MergeArgs {
 
 // Fused decode partial pass: dense window tiles + sparse union chunks.
 struct DecodeArgs {
+  CUtensorMap kmap;       // row map over K [B*Hkv*T, D] for TMA gather4 (bf16), set by the launcher
   const void* K;          // [B*Hkv, T, D] storage dtype
   const void* V;
   const void* q;          // [B*Hq, D] storage dtype (decode: one query row)
