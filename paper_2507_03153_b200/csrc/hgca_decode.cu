@@ -44,7 +44,7 @@ struct DecodeCfg {
   static constexpr bool PIECE32 = ESZ == 2;
   static constexpr bool V_SMEM = ESZ == 4;
   static constexpr int DPL = D / 32;                    // dims per lane in P.V
-  static constexpr int S = TMA ? 3 : 2;                 // stages per warp
+  static constexpr int S = 2;                           // stages per warp
   static constexpr int OFF_V = SUB * ROWB;
   static constexpr int OFF_POS = OFF_V + (V_SMEM ? SUB * ROWB : 0);
   static constexpr int OFF_QM = OFF_POS + SUB * 4;
@@ -271,6 +271,7 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial
   // ---------------------------------------------------------- compute
   for (int k = 0;; ++k) {
     const int s = k % C::S;
+    __syncwarp();
     if constexpr (C::TMA) {
       if (desc[s].item >= 0) mbar_wait(&bar[s], (k / C::S) & 1);
     } else {
@@ -417,6 +418,7 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial
 #pragma unroll
       for (int r = 0; r < C::SUB; ++r) {
         const float pr = __shfl_sync(FULL, pf, r);
+        if (C::V_SMEM && r >= d.n) break;  // staged V rows past the end are not loaded
         float vv[C::DPL];
         if constexpr (C::V_SMEM) {
           load_v_f32<T, C::DPL>(st + C::OFF_V + r * C::ROWB + lane * C::DPL * C::ESZ, vv);
