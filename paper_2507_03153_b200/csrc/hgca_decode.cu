@@ -58,8 +58,13 @@ struct DecodeCfg {
   static constexpr int OFF_ACC = OFF_SC + G * SUB * 8;  // P.V accumulators [G][D] fp32
   static constexpr int OFF_MZ = OFF_ACC + G * D * 4;    // running (m, z) [G][2] fp64
   static constexpr int OFF_BAR = OFF_MZ + G * 16;       // mbarriers [S]
-  static constexpr int OFF_DESC = OFF_BAR + S * 8;
-  static constexpr int WARP_SMEM = ((OFF_DESC + S * 32) + 127) / 128 * 128;
+  static constexpr int OFF_DESC = OFF_BAR + S * 8;       // stage descriptors [S]
+  // metadata ring: descriptor + union entries (pos, mask) of the next
+  // sub-chunks, fetched with cp.async one issue ahead
+  static constexpr int MR = 2;
+  static constexpr int MSLOT = 32 + SUB * 4 + SUB;       // desc, pos[32], qm[32]
+  static constexpr int OFF_META = ((OFF_DESC + S * 32) + 15) / 16 * 16;
+  static constexpr int WARP_SMEM = ((OFF_META + MR * MSLOT) + 127) / 128 * 128;
   static constexpr int NC0 = (232448 - 2048) / WARP_SMEM;
   // <= 8 warps: at most 2 per SM sub-partition, so 255 registers per thread
   static constexpr int NC = NC0 > 8 ? 8 : NC0;
@@ -151,15 +156,18 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial
   int next_item = 0;  // lane 0: id of the item after the current one
   if (lane == 0) next_item = atomicAdd(a.counter, 1);
   int L_item = -1, L_bk = 0, L_hi = 0, L_row = 0, L_lo = 0, L_dense = 0, L_qbuf = C::NQB - 1;
-  StageDesc pd1, pd2;
-  int32_t pd1_pos = 0, pd2_pos = 0;
-  uint32_t pd1_qm = 0, pd2_qm = 0;
+  int meta_slot = 0;  // slot holding the next sub-chunk to issue
 
-  auto advance = [&]() {  // form pd2 for the next sub-chunk and start its metadata loads
+  // Form the descriptor of the next sub-chunk into metadata slot ms; its union
+  // entries arrive by cp.async (sparse) or are computed (dense).
+  auto advance = [&](int ms) {
+    unsigned char* slot = wsm + C::OFF_META + ms * C::MSLOT;
+    StageDesc d;
     if (L_item < 0 || L_row >= L_hi) {
       const int item = __shfl_sync(FULL, next_item, 0);
       if (item >= total) {
-        pd2.item = -1;
+        d.item = -1;
+        if (lane == 0) *reinterpret_cast<StageDesc*>(slot) = d;
         return;
       }
       L_item = item;
@@ -178,93 +186,98 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial
       }
       L_row = L_lo;
     }
-    pd2.item = L_item;
-    pd2.bk = L_bk;
-    pd2.r0 = L_row;
-    pd2.n = min(C::SUB, L_hi - L_row);
-    pd2.first = L_row == L_lo;
-    pd2.last = L_row + C::SUB >= L_hi;
-    pd2.dense = L_dense;
-    pd2.qbuf = 0;
-    pd2_pos = 0;  // rows past the end read position 0 (valid memory, masked by qm = 0)
-    pd2_qm = 0;
-    if (lane < pd2.n) {
-      if (L_dense) {
-        pd2_pos = (int32_t)(a.dlo + L_row + lane);
-        pd2_qm = (1u << G) - 1u;
-      } else {
-        pd2_pos = __ldg(a.u_pos + (int64_t)L_bk * a.T + L_row + lane);
-        pd2_qm = __ldg(a.u_qm + (int64_t)L_bk * a.T + L_row + lane);
-      }
+    d.item = L_item;
+    d.bk = L_bk;
+    d.r0 = L_row;
+    d.n = min(C::SUB, L_hi - L_row);
+    d.first = L_row == L_lo;
+    d.last = L_row + C::SUB >= L_hi;
+    d.dense = L_dense;
+    d.qbuf = 0;
+    if (lane == 0) *reinterpret_cast<StageDesc*>(slot) = d;
+    int32_t* mpos = reinterpret_cast<int32_t*>(slot + 32);
+    uint8_t* mqm = slot + 32 + C::SUB * 4;
+    if (L_dense) {
+      mpos[lane] = lane < d.n ? (int32_t)(a.dlo + L_row + lane) : 0;
+      mqm[lane] = lane < d.n ? (uint8_t)((1u << G) - 1u) : (uint8_t)0;
+    } else {
+      // entries past the item end are masked at use (lane >= n); they are
+      // stale-but-valid positions of the [B*Hkv, T] union buffer
+      if (lane < 8) cp_async16(mpos + lane * 4, a.u_pos + (int64_t)L_bk * a.T + L_row + lane * 4);
+      else if (lane < 10) cp_async16(mqm + (lane - 8) * 16, a.u_qm + (int64_t)L_bk * a.T + L_row + (lane - 8) * 16);
     }
     L_row += C::SUB;
   };
 
-  auto shift = [&]() {  // pd1 <- pd2; warm L2 with pd1's V rows (bf16); advance pd2
-    pd1 = pd2;
-    pd1_pos = pd2_pos;
-    pd1_qm = pd2_qm;
-    if (pd1.item >= 0) {
-      if constexpr (!C::V_SMEM) {
-        if (lane < pd1.n) {
-          const int64_t off = ((int64_t)pd1.bk * a.T + pd1_pos) * C::ROWB;
-#pragma unroll
-          for (int l = 0; l < C::ROWB; l += 128) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(Vg + off + l));
-        }
-      }
-      advance();
-    }
-  };
-
   auto issue = [&](int s) {
     unsigned char* st = wsm + s * C::STAGE;
-    if (pd1.item >= 0 && pd1.first) {
-      L_qbuf = (L_qbuf + 1) % C::NQB;
-      pd1.qbuf = L_qbuf;
+    // this sub-chunk's metadata was fetched one issue ago
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncwarp();
+    const unsigned char* slot = wsm + C::OFF_META + meta_slot * C::MSLOT;
+    StageDesc d = *reinterpret_cast<const StageDesc*>(slot);
+    int32_t pos = 0;
+    uint32_t qm = 0;
+    if (d.item >= 0 && lane < d.n) {
+      pos = reinterpret_cast<const int32_t*>(slot + 32)[lane];
+      qm = slot[32 + C::SUB * 4 + lane];
     }
-    if (lane == 0) desc[s] = pd1;
-    if (pd1.item >= 0) {
-      reinterpret_cast<int32_t*>(st + C::OFF_POS)[lane] = pd1_pos;
-      st[C::OFF_QM + lane] = (uint8_t)pd1_qm;
-      const int64_t b = pd1.bk / a.Hkv, kvh = pd1.bk % a.Hkv;
+    if (d.item >= 0 && d.first) {
+      L_qbuf = (L_qbuf + 1) % C::NQB;
+      d.qbuf = L_qbuf;
+    }
+    if (lane == 0) desc[s] = d;
+    if (d.item >= 0) {
+      reinterpret_cast<int32_t*>(st + C::OFF_POS)[lane] = pos;
+      st[C::OFF_QM + lane] = (uint8_t)qm;
+      const int64_t b = d.bk / a.Hkv, kvh = d.bk % a.Hkv;
       const unsigned char* qsrc = Qg + (b * a.Hq + kvh * G) * (int64_t)C::ROWB;
-      unsigned char* qdst = wsm + C::OFF_QRAW + pd1.qbuf * C::QRAW;
+      unsigned char* qdst = wsm + C::OFF_QRAW + d.qbuf * C::QRAW;
       if constexpr (C::TMA) {
         // 8 gather4 ops (4 rows each) + the item's queries on this stage's mbarrier
-        const int rowbase = pd1.bk * (int)a.T;
-        const int q0 = __shfl_sync(FULL, pd1_pos, (lane & 7) * 4 + 0);
-        const int q1 = __shfl_sync(FULL, pd1_pos, (lane & 7) * 4 + 1);
-        const int q2 = __shfl_sync(FULL, pd1_pos, (lane & 7) * 4 + 2);
-        const int q3 = __shfl_sync(FULL, pd1_pos, (lane & 7) * 4 + 3);
-        if (lane == 0) mbar_expect_tx(&bar[s], C::SUB * C::ROWB + (pd1.first ? C::QRAW : 0));
+        const int rowbase = d.bk * (int)a.T;
+        const int q0 = __shfl_sync(FULL, pos, (lane & 7) * 4 + 0);
+        const int q1 = __shfl_sync(FULL, pos, (lane & 7) * 4 + 1);
+        const int q2 = __shfl_sync(FULL, pos, (lane & 7) * 4 + 2);
+        const int q3 = __shfl_sync(FULL, pos, (lane & 7) * 4 + 3);
+        if (lane == 0) mbar_expect_tx(&bar[s], C::SUB * C::ROWB + (d.first ? C::QRAW : 0));
         __syncwarp();
         if (lane < 8)
           tma_gather4(st + lane * 4 * C::ROWB, &a.kmap, 0, rowbase + q0, rowbase + q1, rowbase + q2,
                       rowbase + q3, &bar[s]);
-        if (lane == 8 && pd1.first) bulk_g2s(qdst, qsrc, C::QRAW, &bar[s]);
+        if (lane == 8 && d.first) bulk_g2s(qdst, qsrc, C::QRAW, &bar[s]);
+        if constexpr (!C::V_SMEM) {  // warm L2 with this sub-chunk's V rows
+          if (lane < d.n) {
+            const int64_t off = ((int64_t)d.bk * a.T + pos) * C::ROWB;
+#pragma unroll
+            for (int l = 0; l < C::ROWB; l += 128) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(Vg + off + l));
+          }
+        }
       } else {
-        if (pd1.first)
+        if (d.first)
           for (int t = lane; t < C::QRAW / 16; t += 32) cp_async16(qdst + t * 16, qsrc + t * 16);
-        const unsigned char* kbase = Kg + (int64_t)pd1.bk * a.T * C::ROWB;
-        const unsigned char* vbase = Vg + (int64_t)pd1.bk * a.T * C::ROWB;
+        const unsigned char* kbase = Kg + (int64_t)d.bk * a.T * C::ROWB;
+        const unsigned char* vbase = Vg + (int64_t)d.bk * a.T * C::ROWB;
 #pragma unroll 4
         for (int t = lane; t < C::SUB * C::PIECES; t += 32) {
           const int r = t / C::PIECES, p = t % C::PIECES;
-          const int32_t pr = __shfl_sync(FULL, pd1_pos, r);
-          if (r < pd1.n) {
+          const int32_t pr = __shfl_sync(FULL, pos, r);
+          if (r < d.n) {
             cp_async16(st + r * C::ROWB + swz(r, p) * 16, kbase + (int64_t)pr * C::ROWB + p * 16);
             if (C::V_SMEM) cp_async16(st + C::OFF_V + r * C::ROWB + p * 16, vbase + (int64_t)pr * C::ROWB + p * 16);
           }
         }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
       }
+      // fetch the following sub-chunk's metadata into the other slot
+      meta_slot ^= 1;
+      advance(meta_slot);
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
-    if constexpr (!C::TMA) asm volatile("cp.async.commit_group;\n" ::: "memory");
-    shift();
   };
 
-  pd2.item = 0;
-  advance();
-  shift();
+  advance(0);
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
 #pragma unroll
   for (int s = 0; s < C::S; ++s) issue(s);
 
@@ -275,7 +288,8 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial
     if constexpr (C::TMA) {
       if (desc[s].item >= 0) mbar_wait(&bar[s], (k / C::S) & 1);
     } else {
-      asm volatile("cp.async.wait_group %0;\n" ::"n"(C::S - 1) : "memory");
+      // outstanding groups, oldest first: data(k), meta(k+1)+..., data(k+1), meta(k+2)
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(2 * (C::S - 1)) : "memory");
     }
     __syncwarp();
     const StageDesc d = desc[s];
@@ -301,8 +315,13 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial
     if (d.first) {
       const T* qr = reinterpret_cast<const T*>(wsm + C::OFF_QRAW + d.qbuf * C::QRAW);
       if constexpr (C::PIECE32) {
+        // piece p's first 4 floats at [p*4], last 4 at [D/2 + p*4]: rotated
+        // per-lane piece reads then hit distinct banks
         float* qk = reinterpret_cast<float*>(wsm + C::OFF_QK);
-        for (int t = lane; t < G * D; t += 32) qk[t] = to_f32(qr[t]);
+        for (int t = lane; t < G * D; t += 32) {
+          const int g = t / D, e = t % D, p = e / 8, j = e % 8;
+          qk[g * D + (j < 4 ? p * 4 + j : D / 2 + p * 4 + (j - 4))] = to_f32(qr[t]);
+        }
       } else {
         double* qk = reinterpret_cast<double*>(wsm + C::OFF_QK);
         for (int t = lane; t < G * D; t += 32) qk[t] = to_f64(qr[t]);
@@ -330,8 +349,8 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial
             const int p = (i + lane) & (C::PIECES - 1);  // rotation: conflict-free dense rows
             float kf[8];
             unpack8<T>(*reinterpret_cast<const uint4*>(krow + p * 16), kf);
-            const float4 qa = *reinterpret_cast<const float4*>(qk + g * D + p * 8);
-            const float4 qb = *reinterpret_cast<const float4*>(qk + g * D + p * 8 + 4);
+            const float4 qa = *reinterpret_cast<const float4*>(qk + g * D + p * 4);
+            const float4 qb = *reinterpret_cast<const float4*>(qk + g * D + D / 2 + p * 4);
             float part = qa.x * kf[0];
             part = fmaf(qa.y, kf[1], part);
             part = fmaf(qa.z, kf[2], part);
@@ -353,8 +372,8 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial
 #pragma unroll
             for (int g = 0; g < G; ++g) {
               if ((wq >> g) & 1u) {
-                const float4 qa = *reinterpret_cast<const float4*>(qk + g * D + p * 8);
-                const float4 qb = *reinterpret_cast<const float4*>(qk + g * D + p * 8 + 4);
+                const float4 qa = *reinterpret_cast<const float4*>(qk + g * D + p * 4);
+                const float4 qb = *reinterpret_cast<const float4*>(qk + g * D + D / 2 + p * 4);
                 float part = qa.x * kf[0];
                 part = fmaf(qa.y, kf[1], part);
                 part = fmaf(qa.z, kf[2], part);
