@@ -151,7 +151,7 @@ typedef struct hgca_decode_desc {
   double* part_z;           /* [max_items*G] */
   float* part_acc;          /* [max_items*G*D] */
   int64_t max_items;
-  int32_t* counter;         /* 1 int scratch */
+  int32_t* counter;         /* (1 + B*Hkv) int32 scratch */
   double* maw;              /* [B*Hq, T] or NULL */
   double alpha;
   float* out;               /* [B*Hq, D] */
@@ -161,12 +161,10 @@ typedef struct hgca_decode_desc {
   double* lse_sparse;       /* optional [B*Hq] */
 } hgca_decode_desc;
 
-/* One decode step = hgca_decode_partial (dense window items + sparse union
- * items -> per-item (m, z, acc) partials) then hgca_decode_merge (fixed-order
- * fold, merge_states, MAW EMA). The halves are exported for per-kernel timing. */
+/* One decode step = one kernel: dense window items + sparse union items ->
+ * per-item (m, z, acc) partials; the warp finishing a (batch, kv-head)'s last
+ * item folds them in a fixed order, applies merge_states and the MAW EMA. */
 int hgca_decode_step(const hgca_decode_desc* desc, hgca_stream_t stream);
-int hgca_decode_partial(const hgca_decode_desc* desc, hgca_stream_t stream);
-int hgca_decode_merge(const hgca_decode_desc* desc, hgca_stream_t stream);
 
 #ifdef __cplusplus
 }

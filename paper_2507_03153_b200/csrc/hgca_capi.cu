@@ -301,30 +301,14 @@ static int decode_prepare(const hgca_decode_desc* d, DecodeArgs& a, DecodeMergeA
   return HGCA_OK;
 }
 
-int hgca_decode_partial(const hgca_decode_desc* d, hgca_stream_t stream) {
-  DecodeArgs a;
-  DecodeMergeArgs m;
-  int rc = decode_prepare(d, a, m);
-  if (rc) return rc;
-  return cuda_status(launch_decode_partial(d->dtype, a, S(stream)), "decode_partial");
-}
-
-int hgca_decode_merge(const hgca_decode_desc* d, hgca_stream_t stream) {
-  DecodeArgs a;
-  DecodeMergeArgs m;
-  int rc = decode_prepare(d, a, m);
-  if (rc) return rc;
-  return cuda_status(launch_decode_merge(m, S(stream)), "decode_merge");
-}
-
 int hgca_decode_step(const hgca_decode_desc* d, hgca_stream_t stream) {
   DecodeArgs a;
   DecodeMergeArgs m;
   int rc = decode_prepare(d, a, m);
   if (rc) return rc;
-  rc = cuda_status(launch_decode_partial(d->dtype, a, S(stream)), "decode_partial");
-  if (rc) return rc;
-  return cuda_status(launch_decode_merge(m, S(stream)), "decode_merge");
+  a.m = m;
+  a.bk_done = d->counter + 1;
+  return cuda_status(launch_decode_partial(d->dtype, a, S(stream)), "decode_step");
 }
 
 }  // extern "C"

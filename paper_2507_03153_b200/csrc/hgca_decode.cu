@@ -18,9 +18,10 @@
 //   * fp32 P.V accumulation, one warp per query head, lanes over dims.
 // Each item emits (m, z, acc) per query head into a fixed slot, so the result
 // is independent of which CTA ran which item (deterministic, no float atomics).
-// decode_merge_kernel then folds the partials in a fixed order, applies the
-// reference merge_states (attention.py:153-188) and the fp64 MAW EMA
-// (kv_cache.py:171-187, engine.py:177-191) from the stored dense scores.
+// The warp finishing the last item of a (batch, kv-head) then folds its
+// partials in a fixed order, applies the reference merge_states
+// (attention.py:153-188) and the fp64 MAW EMA (kv_cache.py:171-187,
+// engine.py:177-191) from the stored dense scores -- no second kernel.
 #include "hgca_common.cuh"
 #include "hgca_internal.h"
 
@@ -122,6 +123,101 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
   asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
                ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+}
+
+// ------------------------------------------------------------ in-kernel merge
+// Run by the warp that finishes the last work item of (b, kv-head) bk: folds
+// the dense and sparse partials of each of the G query heads in a fixed order
+// (so the result does not depend on which warp runs it), applies
+// merge_states(sparse, dense) (attention.py:153-188, engine.py:166-169) and
+// the fp64 MAW maintenance of the attended window from the stored scores:
+//   w   = float32(exp(s - m) / z)                     (_core.pyx:81-82)
+//   maw = (1-alpha)*maw + alpha*w   (3 roundings)     (kv_cache.py:186)
+//   new entries: maw = w                              (engine.py:191)
+template <int D, int G>
+__device__ __forceinline__ void warp_fold(const DecodeArgs& a, int64_t i0, int64_t i1, int g, int lane,
+                                          double& M, double& Z, double* acc) {
+  constexpr int DPL = D / 32;
+  const uint32_t FULL = 0xffffffffu;
+  double mx = -INFINITY;
+  for (int64_t i = i0 + lane; i < i1; i += 32) mx = fmax(mx, __ldcg(a.m.part_m + i * G + g));
+  M = warp_max_f64(mx);
+  double z = 0.0;
+#pragma unroll
+  for (int k = 0; k < DPL; ++k) acc[k] = 0.0;
+  for (int64_t c0 = i0; c0 < i1; c0 += 32) {
+    const int64_t i = c0 + lane;
+    double w = 0.0;
+    if (i < i1) {
+      const double mi = __ldcg(a.m.part_m + i * G + g);
+      if (mi != -INFINITY) {
+        w = exp(mi - M);
+        z += __ldcg(a.m.part_z + i * G + g) * w;
+      }
+    }
+    const int n = (int)min((int64_t)32, i1 - c0);
+    const float* pa = a.m.part_acc + (c0 * G + g) * D + lane * DPL;
+#pragma unroll 8
+    for (int jj = 0; jj < n; ++jj) {
+      const double wj = __shfl_sync(FULL, w, jj);
+      if constexpr (DPL == 4) {
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(pa + (int64_t)jj * G * D));
+        acc[0] += wj * v.x; acc[1] += wj * v.y; acc[2] += wj * v.z; acc[3] += wj * v.w;
+      } else {
+        const float2 v = __ldcg(reinterpret_cast<const float2*>(pa + (int64_t)jj * G * D));
+        acc[0] += wj * v.x; acc[1] += wj * v.y;
+      }
+    }
+  }
+  Z = warp_sum_f64(z);
+}
+
+template <int D, int G>
+__device__ void warp_merge_bk(const DecodeArgs& a, int64_t bk, int lane) {
+  constexpr int DPL = D / 32;
+  const DecodeMergeArgs& m = a.m;
+  const int64_t b = bk / a.Hkv, kvh = bk % a.Hkv;
+  const int64_t d0 = bk * a.Sd, d1 = d0 + a.Sd;
+  const int64_t s0 = a.n_dense_items + __ldcg(a.item_off + bk), s1 = a.n_dense_items + __ldcg(a.item_off + bk + 1);
+  for (int g = 0; g < G; ++g) {
+    const int64_t bq = b * a.Hq + kvh * G + g;
+    double Md, Zd, Ms, Zs, ad[DPL], as[DPL];
+    warp_fold<D, G>(a, d0, d1, g, lane, Md, Zd, ad);
+    warp_fold<D, G>(a, s0, s1, g, lane, Ms, Zs, as);
+    const bool s_empty = !(Zs > 0.0);
+    const bool d_empty = !(Zd > 0.0);
+    const double lse_s = s_empty ? -INFINITY : Ms + log(Zs);
+    const double lse_d = d_empty ? -INFINITY : Md + log(Zd);
+    const double mm = fmax(lse_s, lse_d);
+    const bool both_empty = mm == -INFINITY;
+    const double ms = both_empty ? 0.0 : mm;
+    const double wa = exp(lse_s - ms), wb = exp(lse_d - ms);
+    const double zs = both_empty ? 1.0 : wa + wb;
+    const float ca = (float)(wa / zs), cb = (float)(wb / zs);
+#pragma unroll
+    for (int k = 0; k < DPL; ++k) {
+      const int c = lane * DPL + k;
+      const float od = d_empty ? 0.f : (float)(ad[k] / Zd);
+      const float os = s_empty ? 0.f : (float)(as[k] / Zs);
+      m.out[bq * D + c] = __fadd_rn(__fmul_rn(ca, os), __fmul_rn(cb, od));
+      if (m.out_sparse) m.out_sparse[bq * D + c] = os;
+    }
+    if (lane == 0) {
+      m.lse[bq] = both_empty ? -INFINITY : ms + log(zs);
+      if (m.lse_sparse) m.lse_sparse[bq] = lse_s;
+    }
+    if (m.maw == nullptr && m.wts_out == nullptr) continue;
+#pragma unroll 4
+    for (int64_t j = lane; j < m.W; j += 32) {
+      const float w32 = d_empty ? 0.f : (float)(exp(__ldcg(m.dsc + bq * m.dsc_ld + j) - Md) / Zd);
+      if (m.wts_out) m.wts_out[bq * m.W + j] = w32;
+      if (m.maw) {
+        double* mp = m.maw + bq * m.T + m.dlo + j;
+        const double aw = (double)w32;
+        *mp = j < m.w_old ? __dadd_rn(__dmul_rn(m.one_minus_alpha, *mp), __dmul_rn(m.alpha, aw)) : aw;
+      }
+    }
+  }
 }
 
 template <typename T, int D, int G>
@@ -467,6 +563,17 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial
         a.part_m[(int64_t)d.item * G + lane] = mz[2 * lane];
         a.part_z[(int64_t)d.item * G + lane] = mz[2 * lane + 1];
       }
+      // the last finished item of this (b, kv-head) merges it
+      __threadfence();
+      __syncwarp();
+      int old = 0;
+      if (lane == 0) old = atomicAdd(a.bk_done + d.bk, 1);
+      old = __shfl_sync(FULL, old, 0);
+      const int n_items = (int)a.Sd + (__ldcg(a.item_off + d.bk + 1) - __ldcg(a.item_off + d.bk));
+      if (old == n_items - 1) {
+        __threadfence();
+        warp_merge_bk<D, G>(a, d.bk, lane);
+      }
     }
     __syncwarp();
     issue(s);
@@ -481,115 +588,6 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial
 //   w   = float32(exp(s - m) / z)                     (_core.pyx:81-82)
 //   maw = (1-alpha)*maw + alpha*w   (3 roundings)     (kv_cache.py:186)
 //   new entries: maw = w                              (engine.py:191)
-constexpr int MERGE_THREADS = 512;
-
-__device__ __forceinline__ double block_reduce_max(double v, double* red) {
-  v = warp_max_f64(v);
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  __syncthreads();
-  if (lane == 0) red[w] = v;
-  __syncthreads();
-  double r = -INFINITY;
-  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) r = fmax(r, red[i]);
-  return r;
-}
-
-__device__ __forceinline__ double block_reduce_sum(double v, double* red) {
-  v = warp_sum_f64(v);
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  __syncthreads();
-  if (lane == 0) red[w] = v;
-  __syncthreads();
-  double r = 0.0;
-  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) r += red[i];  // fixed order
-  return r;
-}
-
-// One CTA (512 threads) per (batch, query head).
-__global__ void __launch_bounds__(MERGE_THREADS) decode_merge_kernel(const DecodeMergeArgs a) {
-  __shared__ double wgt[MERGE_THREADS];
-  __shared__ double red[32];
-  __shared__ double part[MERGE_THREADS];
-  const int64_t bq = blockIdx.x;
-  const int64_t b = bq / a.Hq, h = bq % a.Hq;
-  const int64_t kvh = h / a.G, g = h % a.G;
-  const int64_t bk = b * a.Hkv + kvh;
-  const int tid = threadIdx.x;
-  const int64_t D = a.D;
-  const int P = (int)(MERGE_THREADS / D);  // item lanes per dim
-  const int c = tid % (int)D, pl = tid / (int)D;
-  const int64_t d0 = bk * a.Sd, d1 = d0 + a.Sd;
-  const int64_t s0 = a.n_dense_items + a.item_off[bk], s1 = a.n_dense_items + a.item_off[bk + 1];
-  // fold items [i0, i1): M = max m_i, w_i = exp(m_i - M), Z = sum z_i w_i, acc_c = sum w_i acc_i[c]
-  auto fold = [&](int64_t i0, int64_t i1, double& M, double& Z) -> double {
-    double mx = -INFINITY;
-    for (int64_t i = i0 + tid; i < i1; i += MERGE_THREADS) mx = fmax(mx, a.part_m[i * a.G + g]);
-    M = block_reduce_max(mx, red);
-    double zl = 0.0, acc = 0.0;
-    for (int64_t c0 = i0; c0 < i1; c0 += MERGE_THREADS) {
-      const int64_t n = min((int64_t)MERGE_THREADS, i1 - c0);
-      __syncthreads();
-      if (tid < n) {
-        const double mi = a.part_m[(c0 + tid) * a.G + g];
-        const double w = (mi == -INFINITY) ? 0.0 : exp(mi - M);
-        wgt[tid] = w;
-        zl += w == 0.0 ? 0.0 : a.part_z[(c0 + tid) * a.G + g] * w;
-      }
-      __syncthreads();
-      if (pl < P) {
-        const float* pa = a.part_acc + (c0 * a.G + g) * D + c;
-#pragma unroll 8
-        for (int64_t j = pl; j < n; j += P) {
-          const double w = wgt[j];
-          if (w != 0.0) acc += w * (double)pa[j * a.G * D];
-        }
-      }
-    }
-    Z = block_reduce_sum(zl, red);
-    __syncthreads();
-    part[tid] = acc;
-    __syncthreads();
-    double t = 0.0;
-    if (tid < D)
-      for (int q = 0; q < P; ++q) t += part[q * D + tid];  // fixed order over item lanes
-    return t;
-  };
-  double Md, Zd, Ms, Zs;
-  const double acc_d = fold(d0, d1, Md, Zd);
-  const double acc_s = fold(s0, s1, Ms, Zs);
-  const bool s_empty = !(Zs > 0.0);
-  const bool d_empty = !(Zd > 0.0);
-  const double lse_s = s_empty ? -INFINITY : Ms + log(Zs);
-  const double lse_d = d_empty ? -INFINITY : Md + log(Zd);
-  // merge_states coefficients (attention.py:170-182)
-  const double m = fmax(lse_s, lse_d);
-  const bool both_empty = m == -INFINITY;
-  const double ms = both_empty ? 0.0 : m;
-  const double wa = exp(lse_s - ms), wb = exp(lse_d - ms);
-  const double zs = both_empty ? 1.0 : wa + wb;
-  const float ca = (float)(wa / zs), cb = (float)(wb / zs);
-  if (tid < D) {
-    const float od = d_empty ? 0.f : (float)(acc_d / Zd);
-    const float os = s_empty ? 0.f : (float)(acc_s / Zs);
-    a.out[bq * D + tid] = __fadd_rn(__fmul_rn(ca, os), __fmul_rn(cb, od));
-    if (a.out_sparse) a.out_sparse[bq * D + tid] = os;
-  }
-  if (tid == 0) {
-    a.lse[bq] = both_empty ? -INFINITY : ms + log(zs);
-    if (a.lse_sparse) a.lse_sparse[bq] = lse_s;
-  }
-  if (a.maw == nullptr && a.wts_out == nullptr) return;
-  for (int64_t j = tid; j < a.W; j += MERGE_THREADS) {
-    const float w32 = d_empty ? 0.f : (float)(exp(a.dsc[bq * a.dsc_ld + j] - Md) / Zd);
-    if (a.wts_out) a.wts_out[bq * a.W + j] = w32;
-    if (a.maw) {
-      double* mp = a.maw + bq * a.T + a.dlo + j;
-      const double aw = (double)w32;
-      *mp = j < a.w_old ? __dadd_rn(__dmul_rn(a.one_minus_alpha, *mp), __dmul_rn(a.alpha, aw)) : aw;
-    }
-  }
-}
-
 // -------------------------------------------------------------- union build
 // Per (batch, kv-head): union of the G query heads' selection masks over the
 // archive [0, n_arch), emitted grouped by query-head mask value (ascending
@@ -824,7 +822,8 @@ int decode_chunk_rows(int dtype, int64_t D) {
 }
 
 int launch_decode_partial(int dtype, const DecodeArgs& a, cudaStream_t s) {
-  cudaError_t e = cudaMemsetAsync(a.counter, 0, sizeof(int32_t), s);
+  // work counter + per-(b, kv-head) finished-item counters
+  cudaError_t e = cudaMemsetAsync(a.counter, 0, sizeof(int32_t) * (1 + a.B * a.Hkv), s);
   if (e != cudaSuccess) return (int)e;
   if (dtype == kBF16) {
     if (a.D == 128) return launch_decode_g<__nv_bfloat16, 128>(a, s);
@@ -836,10 +835,6 @@ int launch_decode_partial(int dtype, const DecodeArgs& a, cudaStream_t s) {
   return -1001;
 }
 
-int launch_decode_merge(const DecodeMergeArgs& a, cudaStream_t s) {
-  decode_merge_kernel<<<(unsigned)(a.B * a.Hq), MERGE_THREADS, 0, s>>>(a);
-  return (int)cudaGetLastError();
-}
 
 int launch_union_build(const uint32_t* sel, int64_t B, int64_t Hq, int64_t Hkv, int64_t words,
                        int64_t n_arch, int64_t T, int32_t* u_pos, uint8_t* u_qm, int32_t* u_cnt,

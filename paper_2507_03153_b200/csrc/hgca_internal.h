@@ -42,8 +42,32 @@ struct MergeArgs {
   void* w_out;      // [rows, na + nb]
 };
 
-// Fused decode partial pass: dense window tiles + sparse union chunks.
+struct DecodeMergeArgs {
+  int64_t B, Hq, Hkv, G, D;
+  int64_t Sd, n_dense_items;
+  const int32_t* item_off;
+  const double* part_m;
+  const double* part_z;
+  const float* part_acc;
+  const double* dsc;
+  int64_t dsc_ld;
+  int64_t W;              // dense positions attended = dhi - dlo
+  int64_t w_old;          // window entries before this step (EMA'd); the rest are new
+  double* maw;            // [B*Hq, T] or nullptr (no MAW maintenance)
+  int64_t T;
+  int64_t dlo;
+  double one_minus_alpha, alpha;
+  float* wts_out;         // optional dense weights [B*Hq, W]
+  float* out;             // [B*Hq, D]
+  double* lse;            // [B*Hq]
+  float* out_sparse;      // optional sparse partial out [B*Hq, D] (for sharded merges)
+  double* lse_sparse;
+};
+
+// Fused decode step: dense window tiles + sparse union chunks, merged in-kernel.
 struct DecodeArgs {
+  DecodeMergeArgs m;      // fold / merge_states / MAW parameters (run by the last warp per (b, kv-head))
+  int32_t* bk_done;       // [B*Hkv] finished-item counters (zeroed before launch)
   CUtensorMap kmap;       // row map over K [B*Hkv*T, D] for TMA gather4 (bf16), set by the launcher
   const void* K;          // [B*Hkv, T, D] storage dtype
   const void* V;
@@ -68,27 +92,7 @@ struct DecodeArgs {
   int64_t n_dense_items;  // B*Hkv*Sd
 };
 
-struct DecodeMergeArgs {
-  int64_t B, Hq, Hkv, G, D;
-  int64_t Sd, n_dense_items;
-  const int32_t* item_off;
-  const double* part_m;
-  const double* part_z;
-  const float* part_acc;
-  const double* dsc;
-  int64_t dsc_ld;
-  int64_t W;              // dense positions attended = dhi - dlo
-  int64_t w_old;          // window entries before this step (EMA'd); the rest are new
-  double* maw;            // [B*Hq, T] or nullptr (no MAW maintenance)
-  int64_t T;
-  int64_t dlo;
-  double one_minus_alpha, alpha;
-  float* wts_out;         // optional dense weights [B*Hq, W]
-  float* out;             // [B*Hq, D]
-  double* lse;            // [B*Hq]
-  float* out_sparse;      // optional sparse partial out [B*Hq, D] (for sharded merges)
-  double* lse_sparse;
-};
+
 
 int launch_attend(int dtype, const AttendArgs& a, int64_t BH, cudaStream_t s);
 int launch_merge(int dtype, const MergeArgs& a, cudaStream_t s);
@@ -105,7 +109,6 @@ int launch_topk_mask(const double* maw, int64_t rows, int64_t ld, int64_t n, con
                      const uint32_t* exclude, uint32_t* out, int64_t words, cudaStream_t s);
 
 int launch_decode_partial(int dtype, const DecodeArgs& a, cudaStream_t s);
-int launch_decode_merge(const DecodeMergeArgs& a, cudaStream_t s);
 int launch_union_build(const uint32_t* sel, int64_t B, int64_t Hq, int64_t Hkv, int64_t words,
                        int64_t n_arch, int64_t T, int32_t* u_pos, uint8_t* u_qm, int32_t* u_cnt,
                        int32_t* item_off, int4* item_tab, int64_t sparse_rows, cudaStream_t s);

@@ -210,10 +210,10 @@ class HybridEngine:
         self.part_m = torch.empty(self.max_items * self.G, dtype=torch.float64, device=self.dev)
         self.part_z = torch.empty(self.max_items * self.G, dtype=torch.float64, device=self.dev)
         self.part_acc = torch.empty(self.max_items * self.G * self.D, dtype=torch.float32, device=self.dev)
-        self.counter = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.counter = torch.zeros(1 + self.B * self.Hkv, dtype=torch.int32, device=self.dev)
         self._desc = _lib.DecodeDesc()
         self.launches = 0          # kernels of libhgca_b200 launched by this engine
-        self.partial_events = None  # list -> (start, end) CUDA events around the partial kernel
+        self.step_events = None     # list -> (start, end) CUDA events around the decode kernel
 
     # ------------------------------------------------------------ helpers
     def _stream(self):
@@ -379,17 +379,16 @@ class HybridEngine:
         d.wts_out = wts.data_ptr() if wts is not None else None
         d.out_sparse = None
         d.lse_sparse = None
-        if self.partial_events is None:
+        if self.step_events is None:
             _lib.call("hgca_decode_step", d, s)
         else:
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
-            _lib.call("hgca_decode_partial", d, s)
+            _lib.call("hgca_decode_step", d, s)
             e1.record()
-            _lib.call("hgca_decode_merge", d, s)
-            self.partial_events.append((e0, e1))
-        self.launches += 3  # write_rows, decode_partial, decode_merge
+            self.step_events.append((e0, e1))
+        self.launches += 2  # write_rows, decode kernel (merge fused)
         self._last_dense_positions = np.arange(ls.lo, ls.nxt + 1, dtype=np.int64)
         # maintenance after the merge (engine.py:175-191): EMA + init done in
         # the merge kernel; eviction/offload here; append_kv = the position move.
