@@ -23,6 +23,7 @@
  *   hgca_union_build           (device layout of the context cache for the decode kernel)
  *   hgca_decode_step           HybridEngine._run_step, decode mode engine.py:151-195
  *   hgca_merge_partials        P-way merge of sharded (out, lse) partials
+ *   hgca_merge_packed          P-way merge of the allgathered packed partials
  */
 #ifndef HGCA_B200_H
 #define HGCA_B200_H
@@ -91,11 +92,19 @@ int hgca_merge_states(int dtype, const void* out_a, const double* lse_a, const v
 int hgca_merge_partials(const float* outs, const double* lses, int64_t P, int64_t rows, int64_t d,
                         float* out, double* lse, hgca_stream_t stream);
 
+/* P-way merge of packed partials: partial p = out [rows, d] f32 at
+ * parts + p*stride_bytes followed by lse [rows] f64 (the receive buffer of the
+ * sequence-sharded (out, lse) allgather; rank order fold). */
+int hgca_merge_packed(const void* parts, int64_t P, int64_t rows, int64_t d, int64_t stride_bytes,
+                      float* out, double* lse, hgca_stream_t stream);
+
 /* ---- selection ----------------------------------------------------------
  * Bit masks are [rows, words] uint32, bit p of row r = position p. */
+/* keep: optional [words] position mask (NULL = every position); under
+ * sequence sharding it holds the archive blocks this rank owns. */
 int hgca_select_threshold(const double* maw, int64_t rows, int64_t ld, int64_t p0, int64_t p1,
                           double beta, int64_t divisor, uint32_t* mask, int64_t words,
-                          int assign, hgca_stream_t stream);
+                          int assign, const uint32_t* keep, hgca_stream_t stream);
 int hgca_mask_to_indices(const uint32_t* mask_a, const uint32_t* mask_b, int64_t rows,
                          int64_t words, int64_t n, int64_t* idx, int64_t ld, uint8_t* flags,
                          int64_t* counts, hgca_stream_t stream);

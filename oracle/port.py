@@ -226,6 +226,8 @@ class OracleStep:
     a_gpu: np.ndarray        # [H, nq, w + nq] f32
     store_entries: list      # per head attended archive indices
     a_cpu: list              # per head [nq, n_h] f32 weights
+    s_out: np.ndarray = None  # sparse partial [H, nq, d] f32
+    s_lse: np.ndarray = None  # sparse partial lse [H, nq] f64
 
 
 class OracleEngine:
@@ -237,7 +239,7 @@ class OracleEngine:
 
     def __init__(self, heads, head_dim, blk_num, blk_size, alpha=0.5, beta=1.0,
                  core_count=8, batch=1, scale=None, max_len=4096, kernels="port",
-                 threads=1, selection="threshold", topk=0):
+                 threads=1, selection="threshold", topk=0, shard=(0, 1)):
         if blk_num < 2 or blk_size < 1:
             raise OracleError("bad cache geometry")
         self.H, self.d = heads, head_dim
@@ -248,6 +250,9 @@ class OracleEngine:
         self.scale = 1.0 / math.sqrt(head_dim) if scale is None else float(scale)
         self.kernels, self.threads = kernels, threads
         self.selection, self.topk = selection, topk
+        # sequence sharding (not in the reference): this
+        # engine selects only archive blocks j with j % world == rank
+        self.shard_rank, self.shard_world = shard
         self.keys = np.zeros((heads, max_len, head_dim), np.float32)
         self.values = np.zeros((heads, max_len, head_dim), np.float32)
         self.maw = np.zeros((heads, max_len), np.float64)
@@ -271,8 +276,14 @@ class OracleEngine:
             return
         picked = select_salient(self.maw[:, lo:hi], self.beta, divisor)
         for h in range(self.H):
-            if picked[h].size:
-                self.context[h] = np.sort(np.concatenate([self.context[h], picked[h] + lo]))
+            p = self._owned(picked[h] + lo)
+            if p.size:
+                self.context[h] = np.sort(np.concatenate([self.context[h], p]))
+
+    def _owned(self, pos):
+        if self.shard_world == 1:
+            return pos
+        return pos[(pos // self.blk_size) % self.shard_world == self.shard_rank]
 
     def _select_topk_all(self, n):
         self.context = select_topk(self.maw[:, :n], min(self.topk, n))
@@ -286,7 +297,7 @@ class OracleEngine:
         if self.selection == "topk":
             self._select_topk_all(n)
             return
-        self.context = select_salient(self.maw[:, :n], self.beta, n)
+        self.context = [self._owned(c) for c in select_salient(self.maw[:, :n], self.beta, n)]
 
     def bulk_ingest(self, keys, values, maw, divisor):
         """Archive positions [nxt, nxt+n) directly (one ingest_evicted call
@@ -368,7 +379,7 @@ class OracleEngine:
         self.values[:, self.nxt:self.nxt + nq] = v
         self.maw[:, self.nxt:self.nxt + nq] = a_mean[:, w_size:]
         self.nxt += nq
-        return OracleStep(out, lse, a_gpu, entries, a_cpu)
+        return OracleStep(out, lse, a_gpu, entries, a_cpu, s_out, s_lse)
 
     def _evict_if_full(self, incoming):
         """kv_cache.py:189-221 -> evicted position range [lo, lo + freed)."""
@@ -404,6 +415,29 @@ class OracleEngine:
         for h in range(H):
             a_cpu[h] = wts[w_off[h]:w_off[h + 1]].reshape(nq, sizes[h])
         del lo
+
+
+def merge_packed(outs, lses):
+    """P-way fold of sharded partials in rank order, restating the product's
+    hgca_merge_packed arithmetic (max, sum of exp(lse - M), weighted mean in
+    fp64, fp32 output). outs [P, rows, d] f32, lses [P, rows] f64."""
+    outs = np.asarray(outs, np.float32)
+    lses = np.asarray(lses, np.float64)
+    P, rows, d = outs.shape
+    M = lses.max(axis=0)
+    empty = M == -np.inf
+    Ms = np.where(empty, 0.0, M)
+    w = np.exp(lses - Ms[None])
+    w[:, empty] = 0.0
+    Z = np.zeros(rows)
+    acc = np.zeros((rows, d))
+    for p in range(P):
+        Z = Z + w[p]
+        acc = acc + w[p][:, None] * outs[p].astype(np.float64)
+    Zs = np.where(empty, 1.0, Z)
+    out = np.where(empty[:, None], 0.0, acc / Zs[:, None]).astype(np.float32)
+    lse = np.where(empty, -np.inf, Ms + np.log(Zs))
+    return out, lse
 
 
 def expand_gqa(x, q_heads):

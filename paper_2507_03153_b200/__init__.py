@@ -12,6 +12,7 @@ from .attention import AttentionResult, HeadShape, attend, attend_indexed, logsu
 from .backends import CUDA, install
 from .sparsifier import HeadGroupTask, pack_head_groups, select_salient, select_topk
 from .engine import CacheConfig, EngineConfig, HybridEngine, LayerState, StepInput, StepOutput
+from .sharded import ShardedHybridEngine, packed_stride, shard_owner
 from . import _lib
 
 __version__ = "0.1.0"

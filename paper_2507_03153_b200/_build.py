@@ -42,12 +42,15 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = False, defines=(), lib=LIB) -> str:
+    """defines: extra -D macros for instrumented variants (e.g. HGCA_TIMELINE
+    into _lib/libhgca_b200_tl.so, loaded by tools via HGCA_LIB)."""
     deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS]
     deps.append(os.path.join(ROOT, "include", "hgca_b200.h"))
+    LIB = lib
     if force or _stale(LIB, deps):
         os.makedirs(LIBDIR, exist_ok=True)
-        cmd = [_nvcc(), *NVCC_FLAGS]
+        cmd = [_nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines]]
         if ptxas_verbose:
             cmd += ["-Xptxas", "-v"]
         cmd += ["-I", CSRC, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp"]
@@ -65,5 +68,9 @@ def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = Fals
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True, ptxas_verbose="-v" in sys.argv)
-    print(LIB)
+    if "--timeline" in sys.argv:
+        print(build(force=True, verbose=True, defines=("HGCA_TIMELINE",),
+                    lib=os.path.join(LIBDIR, "libhgca_b200_tl.so")))
+    else:
+        build(force="--force" in sys.argv, verbose=True, ptxas_verbose="-v" in sys.argv)
+        print(LIB)

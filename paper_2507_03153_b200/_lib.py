@@ -12,7 +12,8 @@ import os
 from .errors import ContractError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libhgca_b200.so")
+# HGCA_LIB: load an instrumented build of the same library (tools/ only)
+LIB_PATH = os.environ.get("HGCA_LIB") or os.path.join(_HERE, "_lib", "libhgca_b200.so")
 
 DTYPE_F32, DTYPE_F64, DTYPE_BF16 = 0, 1, 2
 HGCA_OK, HGCA_EINVAL, HGCA_ECUDA = 0, 1, 2
@@ -53,7 +54,8 @@ _SIGS = {
     "hgca_attend_gqa": [I32, P, P, P, I64, I64, I64, I64, I64, I64, I64, I64, D, P, P, P, I64, P, P],
     "hgca_merge_states": [I32, P, P, P, P, I64, I64, P, P, P, P, I64, I64, P, P],
     "hgca_merge_partials": [P, P, I64, I64, I64, P, P, P],
-    "hgca_select_threshold": [P, I64, I64, I64, I64, D, I64, P, I64, I32, P],
+    "hgca_merge_packed": [P, I64, I64, I64, I64, P, P, P],
+    "hgca_select_threshold": [P, I64, I64, I64, I64, D, I64, P, I64, I32, P, P],
     "hgca_mask_to_indices": [P, P, I64, I64, I64, P, I64, P, P, P],
     "hgca_popcount_rows": [P, I64, I64, I64, P, P],
     "hgca_group_need": [P, I64, I64, I64, P, P],

@@ -50,6 +50,35 @@ __global__ void merge_partials_kernel(const float* outs, const double* lses, int
   if (threadIdx.x == 0) lse[r] = M + log(Z);
 }
 
+// P-way merge of packed per-rank partials (the receive buffer of the
+// sequence-sharded allgather): partial p holds out [rows, d] f32 at
+// parts + p*stride and lse [rows] f64 right after it. Same fold as
+// merge_partials_kernel, in rank order, so every rank computes identical bits.
+__global__ void merge_packed_kernel(const unsigned char* parts, int64_t P, int64_t rows, int64_t d,
+                                    int64_t stride, float* out, double* lse) {
+  const int64_t r = blockIdx.x;
+  const int64_t lse_off = rows * d * 4;
+  auto L = [&](int64_t p) { return reinterpret_cast<const double*>(parts + p * stride + lse_off)[r]; };
+  double M = -INFINITY;
+  for (int64_t p = 0; p < P; ++p) M = fmax(M, L(p));
+  if (M == -INFINITY) {
+    for (int64_t c = threadIdx.x; c < d; c += blockDim.x) out[r * d + c] = 0.f;
+    if (threadIdx.x == 0) lse[r] = -INFINITY;
+    return;
+  }
+  double Z = 0.0;
+  for (int64_t p = 0; p < P; ++p) Z += exp(L(p) - M);
+  for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
+    double acc = 0.0;
+    for (int64_t p = 0; p < P; ++p) {
+      const double w = exp(L(p) - M);
+      if (w != 0.0) acc += w * (double)reinterpret_cast<const float*>(parts + p * stride)[r * d + c];
+    }
+    out[r * d + c] = (float)(acc / Z);
+  }
+  if (threadIdx.x == 0) lse[r] = M + log(Z);
+}
+
 }  // namespace hgca
 
 using namespace hgca;
@@ -173,9 +202,20 @@ int hgca_merge_partials(const float* outs, const double* lses, int64_t P, int64_
   return cuda_status((int)cudaGetLastError(), "merge_partials");
 }
 
+int hgca_merge_packed(const void* parts, int64_t P, int64_t rows, int64_t d, int64_t stride_bytes, float* out,
+                      double* lse, hgca_stream_t stream) {
+  if (P < 1 || rows < 0 || d < 1 || stride_bytes < rows * d * 4 + rows * 8 || (rows * d * 4) % 8 ||
+      stride_bytes % 8)
+    return fail(HGCA_EINVAL, "merge_packed: bad shape");
+  if (rows == 0) return HGCA_OK;
+  merge_packed_kernel<<<(unsigned)rows, 128, 0, S(stream)>>>(reinterpret_cast<const unsigned char*>(parts), P,
+                                                            rows, d, stride_bytes, out, lse);
+  return cuda_status((int)cudaGetLastError(), "merge_packed");
+}
+
 int hgca_select_threshold(const double* maw, int64_t rows, int64_t ld, int64_t p0, int64_t p1,
                           double beta, int64_t divisor, uint32_t* mask, int64_t words, int assign,
-                          hgca_stream_t stream) {
+                          const uint32_t* keep, hgca_stream_t stream) {
   if (divisor < 1) return fail(HGCA_EINVAL, "divisor must be >= 1, got %lld", (long long)divisor);
   if (p0 < 0 || p1 < p0 || p1 > ld || words * 32 < p1 || rows < 0)
     return fail(HGCA_EINVAL, "select_threshold: bad range");
@@ -184,7 +224,7 @@ int hgca_select_threshold(const double* maw, int64_t rows, int64_t ld, int64_t p
   const int64_t nw = ((p1 + 31) >> 5) - (p0 >> 5);
   const int64_t total = nw * rows;
   (void)total;
-  return cuda_status(launch_threshold_mask(maw, rows, ld, p0, p1, thr, mask, words, assign, S(stream)),
+  return cuda_status(launch_threshold_mask(maw, rows, ld, p0, p1, thr, mask, words, assign, keep, S(stream)),
                      "select_threshold");
 }
 

@@ -29,6 +29,21 @@
 
 namespace hgca {
 
+// Debug build only (-DHGCA_TIMELINE): per-warp timeline of the decode kernel,
+// read back with hgca_debug_timeline (tools/timeline.py).
+#ifdef HGCA_TIMELINE
+#define TL_SLOTS 12
+__device__ unsigned long long g_tl[148 * 16 * TL_SLOTS];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TL(...) __VA_ARGS__
+#else
+#define TL(...)
+#endif
+
 template <typename T, int D, int G>
 struct DecodeCfg {
   static constexpr int ESZ = (int)sizeof(T);
@@ -242,6 +257,10 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial
     fence_mbar_init();
     __syncwarp();
   }
+  TL(unsigned long long* tl = g_tl + ((int64_t)blockIdx.x * C::NC + warp) * TL_SLOTS;
+     unsigned long long tl_merge = 0, tl_wait = 0, tl_sub = 0, tl_items = 0, tl_qk = 0, tl_pv = 0, tl_v = 0,
+                        tl_issue = 0;
+     if (lane == 0) tl[0] = gtimer(););
 
   // ---------------------------------------------------------- load cursor
   // Each warp streams whole work items (dynamic, global counter) through its
@@ -381,6 +400,7 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial
   for (int k = 0;; ++k) {
     const int s = k % C::S;
     __syncwarp();
+    TL(long long c0 = clock64();)
     if constexpr (C::TMA) {
       if (desc[s].item >= 0) mbar_wait(&bar[s], (k / C::S) & 1);
     } else {
@@ -390,6 +410,7 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial
     __syncwarp();
     const StageDesc d = desc[s];
     if (d.item < 0) break;
+    TL(long long c1 = clock64(); tl_wait += c1 - c0; ++tl_sub;)
     const unsigned char* st = wsm + s * C::STAGE;
     const int32_t mypos = reinterpret_cast<const int32_t*>(st + C::OFF_POS)[lane];
     const uint32_t qm = st[C::OFF_QM + lane];
@@ -408,6 +429,7 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial
         }
       }
     }
+    TL(long long c2 = clock64(); tl_v += c2 - c1;)
     if (d.first) {
       const T* qr = reinterpret_cast<const T*>(wsm + C::OFF_QRAW + d.qbuf * C::QRAW);
       if constexpr (C::PIECE32) {
@@ -513,6 +535,7 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial
       if (d.dense && lane < d.n) a.dsc[(b * a.Hq + kvh * G + g) * a.dsc_ld + (mypos - a.dlo)] = sv;
     }
     __syncwarp();
+    TL(long long c3 = clock64(); tl_qk += c3 - c2;)
     // ---- per active head (rolled loop): online softmax (fp64) + P.V (fp32)
     for (uint32_t hm = wq; hm; hm &= hm - 1) {
       const int g = __ffs(hm) - 1;
@@ -557,7 +580,9 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial
       }
       __syncwarp();
     }
+    TL(long long c4 = clock64(); tl_pv += c4 - c3;)
     if (d.last) {
+      TL(++tl_items;)
       for (int t = lane; t < G * D; t += 32) a.part_acc[(int64_t)d.item * G * D + t] = accs[t];
       if (lane < G) {
         a.part_m[(int64_t)d.item * G + lane] = mz[2 * lane];
@@ -572,13 +597,22 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial
       const int n_items = (int)a.Sd + (__ldcg(a.item_off + d.bk + 1) - __ldcg(a.item_off + d.bk));
       if (old == n_items - 1) {
         __threadfence();
+        TL(long long m0 = clock64();)
         warp_merge_bk<D, G>(a, d.bk, lane);
+        TL(tl_merge += clock64() - m0;)
       }
     }
     __syncwarp();
+    TL(long long c5 = clock64();)
     issue(s);
+    TL(tl_issue += clock64() - c5;)
   }
   if constexpr (!C::TMA) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  TL(if (lane == 0) {
+    tl[1] = gtimer();
+    tl[2] = tl_merge; tl[3] = tl_wait; tl[4] = tl_sub; tl[5] = tl_items; tl[6] = tl_qk; tl[7] = tl_pv;
+    tl[8] = tl_v; tl[9] = tl_issue; tl[10] = blockIdx.x; tl[11] = clock64();
+  })
 }
 
 // --------------------------------------------------------------------- merge
@@ -866,6 +900,18 @@ int launch_write_rows(int dtype, void* K, void* V, int64_t BH, int64_t T, int64_
 }
 
 }  // namespace hgca
+
+#ifdef HGCA_TIMELINE
+extern "C" int hgca_debug_timeline(void* host, int64_t n) {
+  const int64_t cap = (int64_t)sizeof(hgca::g_tl) / 8;
+  if (n > cap) n = cap;
+  if (!host) {
+    static unsigned long long zero[148 * 16 * TL_SLOTS];
+    return (int)cudaMemcpyToSymbol(hgca::g_tl, zero, sizeof(zero));
+  }
+  return (int)cudaMemcpyFromSymbol(host, hgca::g_tl, n * 8);
+}
+#endif
 
 namespace hgca {
 template <typename T, int D, int G>

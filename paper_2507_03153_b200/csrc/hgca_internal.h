@@ -97,7 +97,8 @@ struct DecodeArgs {
 int launch_attend(int dtype, const AttendArgs& a, int64_t BH, cudaStream_t s);
 int launch_merge(int dtype, const MergeArgs& a, cudaStream_t s);
 int launch_threshold_mask(const double* maw, int64_t rows, int64_t ld, int64_t p0, int64_t p1,
-                          double thr, uint32_t* mask, int64_t words, int assign, cudaStream_t s);
+                          double thr, uint32_t* mask, int64_t words, int assign, const uint32_t* keep,
+                          cudaStream_t s);
 int launch_mask_to_indices(const uint32_t* a, const uint32_t* b, int64_t rows, int64_t words,
                            int64_t n, int64_t* idx, int64_t ld, uint8_t* flags, int64_t* counts,
                            cudaStream_t s);

@@ -212,9 +212,11 @@ __global__ void merge_states_kernel<double>(MergeArgs a) {
 // (select_salient, sparsifier.py:32-42). One thread per 32-position word; the
 // word is read-modify-written by a single thread (no atomics). assign=1 clears
 // the row's bits in [p0, p1) first (re-evaluation), assign=0 ORs (ingest).
+// keep (optional, [words]) restricts selection to the positions this rank
+// owns under sequence sharding (block-cyclic archive shards).
 __global__ void threshold_mask_kernel(const double* __restrict__ maw, int64_t rows, int64_t ld,
                                       int64_t p0, int64_t p1, double thr, uint32_t* mask,
-                                      int64_t words, int assign) {
+                                      int64_t words, int assign, const uint32_t* __restrict__ keep) {
   const int64_t w0 = p0 >> 5, w1 = (p1 + 31) >> 5;
   const int64_t nw = w1 - w0;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -230,6 +232,7 @@ __global__ void threshold_mask_kernel(const double* __restrict__ maw, int64_t ro
       if (row[p] > thr) bits |= 1u << b;
     }
   }
+  if (keep) bits &= keep[w];
   uint32_t* mw = mask + r * words + w;
   const uint32_t old = *mw;
   *mw = assign ? ((old & ~inrange) | bits) : (old | bits);
@@ -487,12 +490,13 @@ int launch_merge(int dtype, const MergeArgs& a, cudaStream_t s) {
 
 
 int launch_threshold_mask(const double* maw, int64_t rows, int64_t ld, int64_t p0, int64_t p1,
-                          double thr, uint32_t* mask, int64_t words, int assign, cudaStream_t s) {
+                          double thr, uint32_t* mask, int64_t words, int assign, const uint32_t* keep,
+                          cudaStream_t s) {
   const int64_t nw = ((p1 + 31) >> 5) - (p0 >> 5);
   const int64_t total = nw * rows;
   if (total == 0) return 0;
   threshold_mask_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(maw, rows, ld, p0, p1, thr,
-                                                                         mask, words, assign);
+                                                                         mask, words, assign, keep);
   return (int)cudaGetLastError();
 }
 

@@ -33,7 +33,7 @@ from . import _lib
 from ._dev import DTYPE_CODE, device, stream_handle
 from .attention import HeadShape
 from .errors import ContractError
-from .sparsifier import group_size, mask_to_lists, topk_mask, words_for
+from .sparsifier import group_size, mask_to_lists, ownership_words, topk_mask, words_for
 
 __all__ = ["CacheConfig", "EngineConfig", "StepInput", "StepOutput", "LayerState", "HybridEngine"]
 
@@ -85,6 +85,8 @@ class EngineConfig:
     selection: str = "threshold"      # "threshold" (reference) | "topk" (F1 extension)
     topk: int = 0                     # entries per head for selection="topk"
     keep_weights: bool = False        # materialize a_gpu in StepOutput
+    shard_rank: int = 0               # sequence sharding: this rank ...
+    shard_world: int = 1              # ... of shard_world owns archive blocks j with j % world == rank
 
     def __post_init__(self):
         if self.layers < 1:
@@ -100,6 +102,15 @@ class EngineConfig:
             raise ContractError(f"dtype must be float32 or bfloat16, got {self.dtype}")
         if self.selection not in ("threshold", "topk"):
             raise ContractError(f"selection must be threshold or topk, got {self.selection}")
+        if self.shard_world < 1 or not 0 <= self.shard_rank < self.shard_world:
+            raise ContractError(f"bad shard {self.shard_rank}/{self.shard_world}")
+        if self.shard_world > 1:
+            # threshold selection is per entry, so it shards locally; padding and
+            # top-k need a global order (an allreduce at ingest) -- not built yet
+            if self.selection != "threshold":
+                raise ContractError("sequence sharding supports threshold selection only")
+            if group_size(self.batch, self.heads, self.core_count) != 1:
+                raise ContractError("sequence sharding needs padding group size 1 (raise core_count)")
 
     @property
     def head_shape(self) -> HeadShape:
@@ -172,6 +183,11 @@ class LayerState:
         self.item_tab = torch.zeros((B * Hkv * (T // 32 + 1), 4), dtype=torch.int32, device=dev)
         self.lo = 0    # archive size
         self.nxt = 0   # next position
+        self.keep = None
+        if cfg.shard_world > 1:
+            # ownership bits: archive block j (positions [j*blk, (j+1)*blk)) lives on rank j % world
+            bits = ownership_words(words, cfg.cache.blk_size, cfg.shard_rank, cfg.shard_world)
+            self.keep = torch.from_numpy(bits.view(np.int32)).to(dev)
 
     @property
     def window_size(self):
@@ -219,6 +235,10 @@ class HybridEngine:
     def _stream(self):
         return stream_handle(self.dev)
 
+    @staticmethod
+    def _keep_ptr(ls: LayerState):
+        return ls.keep.data_ptr() if ls.keep is not None else None
+
     def _as_dev(self, x, heads):
         """[B, heads, n, D] (or [heads, n, D] when B == 1) -> contiguous device tensor."""
         t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))
@@ -262,7 +282,7 @@ class HybridEngine:
             self.launches += 1
             _lib.call("hgca_select_threshold", ls.maw.data_ptr(), self.B * self.Hq, self.T, lo, hi,
                       float(self.config.cache.beta), int(divisor), ls.ctx.data_ptr(), ls.ctx.shape[1], 0,
-                      self._stream())
+                      self._keep_ptr(ls), self._stream())
         ls.lo = hi
         self._refresh_selection(ls)
 
@@ -340,10 +360,12 @@ class HybridEngine:
             w = w[0] if w is not None else None
         return StepOutput(o, l, w, None, self._last_dense_positions)
 
-    def decode_device(self, layer_idx, q, k, v, out=None, lse=None, wts=None):
+    def decode_device(self, layer_idx, q, k, v, out=None, lse=None, wts=None, out_sparse=None, lse_sparse=None):
         """The decode hot path on device tensors: q [B, Hq, 1, D], k/v
         [B, Hkv, 1, D] (storage dtype). Returns (out [B*Hq, D] f32,
-        lse [B*Hq] f64, a_gpu or None). Launches only; no host sync."""
+        lse [B*Hq] f64, a_gpu or None). Launches only; no host sync.
+        out_sparse / lse_sparse (optional) receive the sparse-only partial
+        (the per-rank contribution under sequence sharding)."""
         ls = self.layers[layer_idx]
         s = self._stream()
         if ls.nxt + 1 > self.T:
@@ -377,8 +399,8 @@ class HybridEngine:
         d.maw, d.alpha = ls.maw.data_ptr(), float(self.config.cache.alpha)
         d.out, d.lse = out.data_ptr(), lse.data_ptr()
         d.wts_out = wts.data_ptr() if wts is not None else None
-        d.out_sparse = None
-        d.lse_sparse = None
+        d.out_sparse = out_sparse.data_ptr() if out_sparse is not None else None
+        d.lse_sparse = lse_sparse.data_ptr() if lse_sparse is not None else None
         if self.step_events is None:
             _lib.call("hgca_decode_step", d, s)
         else:
@@ -469,7 +491,8 @@ class HybridEngine:
                       float(self.config.cache.alpha), 1, s)
             if self.config.selection == "threshold":
                 _lib.call("hgca_select_threshold", ls.maw.data_ptr(), BHq, self.T, 0, lo,
-                          float(self.config.cache.beta), int(lo), ls.ctx.data_ptr(), ls.ctx.shape[1], 1, s)
+                          float(self.config.cache.beta), int(lo), ls.ctx.data_ptr(), ls.ctx.shape[1], 1,
+                          self._keep_ptr(ls), s)
         if ev_hi > ev_lo:
             self._ingest(ls, ev_lo, ev_hi, w_size + nq)
         elif lo:

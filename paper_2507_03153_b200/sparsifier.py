@@ -48,6 +48,15 @@ def _maw_dev(maw):
     return t.contiguous(), is_np
 
 
+def ownership_words(words, blk_size, rank, world):
+    """Position mask [words] uint32 of the archive blocks rank owns under
+    block-cyclic sequence sharding: block j = positions [j*blk, (j+1)*blk)
+    belongs to rank j % world."""
+    pos = np.arange(words * 32, dtype=np.int64)
+    own = ((pos // blk_size) % world == rank).astype(np.uint64)
+    return (own.reshape(words, 32) << np.arange(32, dtype=np.uint64)).sum(axis=1).astype(np.uint32)
+
+
 def threshold_mask(maw_t, beta, divisor, p0=0, p1=None, mask=None, assign=True):
     """Device mask of maw > beta/divisor over [p0, p1) (sparsifier.py:41-42)."""
     rows, n = maw_t.shape
@@ -56,7 +65,7 @@ def threshold_mask(maw_t, beta, divisor, p0=0, p1=None, mask=None, assign=True):
     if mask is None:
         mask = torch.zeros((rows, words), dtype=torch.int32, device=maw_t.device)
     _lib.call("hgca_select_threshold", maw_t.data_ptr(), rows, maw_t.stride(0), p0, p1, float(beta),
-              int(divisor), mask.data_ptr(), mask.shape[1], int(assign), stream_handle(maw_t.device))
+              int(divisor), mask.data_ptr(), mask.shape[1], int(assign), None, stream_handle(maw_t.device))
     return mask
 
 
