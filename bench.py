@@ -133,17 +133,18 @@ def stage_engine(hg, torch, cfgd, max_positions, seed=0):
 
 def partial_bytes(eng, W_avg, U_avg):
     """Algorithmic HBM bytes of one decode kernel launch:
-    dense K+V rows of the window, unique union K+V rows + their (pos, mask)
-    entries, the queries, the dense fp64 scores (written, re-read by the
-    in-kernel merge), the per-item partials (written + re-read), the MAW of
-    the window (read + written, fp64) and out/lse."""
+    dense K|V rows of the window, unique union K|V rows + their 4-byte union
+    entries, the queries, the dense scores (written, re-read by the dense
+    epilogue), the per-item partials (written + re-read by the fold), the MAW
+    of the window (read + written, fp64) and out/lse."""
     B, Hq, Hkv, D, G = eng.B, eng.Hq, eng.Hkv, eng.D, eng.G
     e = 2 if eng.tdtype.itemsize == 2 else 4
+    sc = 4 if e == 2 else 8
     dense = B * Hkv * W_avg * D * 2 * e
-    sparse = U_avg * (D * 2 * e + 5)
+    sparse = U_avg * (D * 2 * e + 4)
     q = B * Hq * D * e
-    dsc = B * Hq * W_avg * 8 * 2
-    items = B * Hkv * (math.ceil(W_avg / 256) + U_avg / (B * Hkv) / 256)
+    dsc = B * Hq * W_avg * sc * 2
+    items = B * Hkv + U_avg / 256
     partials = items * G * (D * 4 + 16) * 2
     maw = B * Hq * W_avg * 8 * 2
     out = B * Hq * (D * 4 + 8)

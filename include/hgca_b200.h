@@ -72,13 +72,14 @@ int hgca_attend_indexed_heads(int dtype, const void* q, const void* k, const voi
                               double scale, void* out, double* lse, void* weights, void* ws,
                               hgca_stream_t stream);
 
-/* Grouped-query attention over rows [row0, row0+n) of a position buffer:
- * q [B*Hq, nq, d]; K/V [B*Hkv, T, d]; q-head h of batch b reads kv-head
- * b*Hkv + h/(Hq/Hkv). weights [B*Hq, nq, wts_ld] or NULL. */
-int hgca_attend_gqa(int dtype, const void* q, const void* K, const void* V, int64_t B, int64_t Hq,
-                    int64_t Hkv, int64_t T, int64_t row0, int64_t n, int64_t nq, int64_t d,
-                    double scale, void* out, double* lse, void* weights, int64_t wts_ld, void* ws,
-                    hgca_stream_t stream);
+/* Grouped-query attention over rows [row0, row0+n) of the interleaved
+ * position buffer KV [B*Hkv, T, 2, d] (F32 or BF16 storage; BF16 rows in the
+ * position-rotated layout hgca_write_rows produces): q [B*Hq, nq, d];
+ * q-head h of batch b reads kv-head b*Hkv + h/(Hq/Hkv). out float32,
+ * weights [B*Hq, nq, wts_ld] float32 or NULL. */
+int hgca_attend_gqa(int dtype, const void* q, const void* KV, int64_t B, int64_t Hq, int64_t Hkv,
+                    int64_t T, int64_t row0, int64_t n, int64_t nq, int64_t d, double scale, void* out,
+                    double* lse, void* weights, int64_t wts_ld, void* ws, hgca_stream_t stream);
 
 /* merge_states over `rows` rows of d: outputs in dtype, lse fp64. Optional
  * weight rows (w_a [rows,na], w_b [rows,nb] -> w_out [rows,na+nb]). */
@@ -118,7 +119,11 @@ int hgca_select_topk(const double* maw, int64_t rows, int64_t ld, int64_t n, con
                      const uint32_t* exclude, uint32_t* out, int64_t words, hgca_stream_t stream);
 
 /* ---- device-resident decode engine --------------------------------------- */
-int hgca_write_rows(int dtype, void* K, void* V, int64_t BH, int64_t T, int64_t d, int64_t pos,
+/* KV[bh, pos+i] = (k_new[bh, i], v_new[bh, i]) for the interleaved position
+ * buffer KV [BH, T, 2, d] (WindowCache.append_kv, kv_cache.py:122-169).
+ * BF16 rows are stored position-rotated: 16-byte chunk c of the 2d-element
+ * row pair of position p lands at chunk (c & ~7) | ((c ^ p) & 7). */
+int hgca_write_rows(int dtype, void* KV, int64_t BH, int64_t T, int64_t d, int64_t pos,
                     const void* k_new, const void* v_new, int64_t n, hgca_stream_t stream);
 int hgca_decode_chunk_rows(int dtype, int64_t d);
 /* Launch configuration of the decode kernel for (dtype, head_dim, Hq/Hkv):
@@ -130,37 +135,38 @@ int hgca_decode_config(int dtype, int64_t d, int64_t group, int64_t* out5);
  * engine.py:177-191); mode 1 = replace (StoreTier.reevaluate, sparsifier.py:158-177). */
 int hgca_maw_update(const float* w, int64_t BH, int64_t nq, int64_t W, int64_t w_ld, double* maw,
                     int64_t T, int64_t p0, int64_t w_old, double alpha, int mode, hgca_stream_t stream);
-/* Union of the Hq/Hkv query heads' selection masks per (batch, kv-head),
- * grouped by query-head mask; also the sparse work-item prefix item_off
- * [B*Hkv+1] and table item_tab [max items][4] = (bk, lo, hi, 0). */
+/* Union of the Hq/Hkv query heads' selection masks per (batch, kv-head) as
+ * entries u_ent [B*Hkv, T] = position | (query-head mask << 24), grouped by
+ * mask value (grouped = 1), in position order (0), or position-class
+ * interleaved (2: every aligned group of 8 entries has distinct p & 7, as far
+ * as the class counts allow; the bfloat16 decode layout); u_cnt [B*Hkv]; also the
+ * sparse work-item prefix item_off [B*Hkv+1] and table item_tab
+ * [max items][4] = (bk, lo, hi, 0). */
 int hgca_union_build(const uint32_t* sel_mask, int64_t B, int64_t Hq, int64_t Hkv, int64_t words,
-                     int64_t n_arch, int64_t T, int32_t* u_pos, uint8_t* u_qm, int32_t* u_cnt,
-                     int32_t* item_off, int32_t* item_tab, int64_t sparse_rows, hgca_stream_t stream);
+                     int64_t n_arch, int64_t T, int32_t* u_ent, int32_t* u_cnt, int32_t* item_off,
+                     int32_t* item_tab, int64_t sparse_rows, int grouped, hgca_stream_t stream);
 
 typedef struct hgca_decode_desc {
   int32_t dtype;            /* HGCA_DTYPE_F32 or HGCA_DTYPE_BF16 (storage) */
   int32_t pad0;
-  int64_t B, Hq, Hkv, D, T; /* batch, query heads, kv heads, head_dim, positions */
-  const void* K;            /* [B*Hkv, T, D] */
-  const void* V;
+  int64_t B, Hq, Hkv, D, T; /* batch, query heads, kv heads, head_dim, positions (T < 2^24) */
+  const void* KV;           /* [B*Hkv, T, 2, D]: K row then V row per position */
   const void* q;            /* [B*Hq, D] this step's queries (storage dtype) */
   double scale;
   int64_t dlo, dhi;         /* dense positions [dlo, dhi): window + kv_in */
   int64_t w_old;            /* window entries before this step (EMA'd) */
-  int64_t dense_rows;       /* rows per dense work item */
   int64_t sparse_rows;      /* rows per sparse work item (as in hgca_union_build) */
-  const int32_t* u_pos;     /* union lists from hgca_union_build */
-  const uint8_t* u_qm;
+  const int32_t* u_ent;     /* union entries from hgca_union_build */
   const int32_t* u_cnt;
   const int32_t* item_off;
   const int32_t* item_tab;  /* [items][4] from hgca_union_build */
-  double* dsc;              /* [B*Hq, dsc_ld] fp64 scratch, dsc_ld >= dhi-dlo */
+  void* dsc;                /* [B*Hq, dsc_ld] dense-score scratch: fp64 (F32) or fp32 (BF16), dsc_ld >= dhi-dlo */
   int64_t dsc_ld;
   double* part_m;           /* [max_items*G] */
   double* part_z;           /* [max_items*G] */
   float* part_acc;          /* [max_items*G*D] */
-  int64_t max_items;
-  int32_t* counter;         /* (1 + B*Hkv) int32 scratch */
+  int64_t max_items;        /* >= B*Hkv*(1 + ceil(T / sparse_rows)) */
+  int32_t* counter;         /* int32 work counter scratch (>= 1 element) */
   double* maw;              /* [B*Hq, T] or NULL */
   double alpha;
   float* out;               /* [B*Hq, D] */
@@ -170,9 +176,11 @@ typedef struct hgca_decode_desc {
   double* lse_sparse;       /* optional [B*Hq] */
 } hgca_decode_desc;
 
-/* One decode step = one kernel: dense window items + sparse union items ->
- * per-item (m, z, acc) partials; the warp finishing a (batch, kv-head)'s last
- * item folds them in a fixed order, applies merge_states and the MAW EMA. */
+/* One decode step = two kernels on `stream`: the decode kernel (one dense
+ * item per (batch, kv-head) over the window, which also applies the MAW EMA,
+ * + sparse union items -> per-item (m, z, acc) partials) and the merge kernel
+ * (programmatic dependent launch; folds the partials in item order and
+ * applies merge_states). */
 int hgca_decode_step(const hgca_decode_desc* desc, hgca_stream_t stream);
 
 #ifdef __cplusplus

@@ -71,6 +71,11 @@ if __name__ == "__main__":
     if "--timeline" in sys.argv:
         print(build(force=True, verbose=True, defines=("HGCA_TIMELINE",),
                     lib=os.path.join(LIBDIR, "libhgca_b200_tl.so")))
+    elif "--variant" in sys.argv:
+        # python _build.py --variant NAME MACRO[=V] ...  -> _lib/libhgca_b200_NAME.so
+        i = sys.argv.index("--variant")
+        name, defs = sys.argv[i + 1], tuple(sys.argv[i + 2:])
+        print(build(force=True, verbose=False, defines=defs, lib=os.path.join(LIBDIR, f"libhgca_b200_{name}.so")))
     else:
         build(force="--force" in sys.argv, verbose=True, ptxas_verbose="-v" in sys.argv)
         print(LIB)

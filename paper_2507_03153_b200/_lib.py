@@ -30,11 +30,11 @@ class DecodeDesc(ctypes.Structure):
     _fields_ = [
         ("dtype", ctypes.c_int32), ("pad0", ctypes.c_int32),
         ("B", I64), ("Hq", I64), ("Hkv", I64), ("D", I64), ("T", I64),
-        ("K", P), ("V", P), ("q", P),
+        ("KV", P), ("q", P),
         ("scale", D),
         ("dlo", I64), ("dhi", I64), ("w_old", I64),
-        ("dense_rows", I64), ("sparse_rows", I64),
-        ("u_pos", P), ("u_qm", P), ("u_cnt", P), ("item_off", P), ("item_tab", P),
+        ("sparse_rows", I64),
+        ("u_ent", P), ("u_cnt", P), ("item_off", P), ("item_tab", P),
         ("dsc", P), ("dsc_ld", I64),
         ("part_m", P), ("part_z", P), ("part_acc", P), ("max_items", I64),
         ("counter", P),
@@ -51,7 +51,7 @@ _SIGS = {
     "hgca_attend_dense": [I32, P, P, P, I64, I64, I64, I64, D, I32, P, P, P, P, P],
     "hgca_attend_indexed": [I32, P, P, P, P, I64, I64, I64, I64, D, I32, P, P, P, P, P],
     "hgca_attend_indexed_heads": [I32, P, P, P, I64, I64, P, P, P, I64, I64, I64, D, P, P, P, P, P],
-    "hgca_attend_gqa": [I32, P, P, P, I64, I64, I64, I64, I64, I64, I64, I64, D, P, P, P, I64, P, P],
+    "hgca_attend_gqa": [I32, P, P, I64, I64, I64, I64, I64, I64, I64, I64, D, P, P, P, I64, P, P],
     "hgca_merge_states": [I32, P, P, P, P, I64, I64, P, P, P, P, I64, I64, P, P],
     "hgca_merge_partials": [P, P, I64, I64, I64, P, P, P],
     "hgca_merge_packed": [P, I64, I64, I64, I64, P, P, P],
@@ -60,11 +60,11 @@ _SIGS = {
     "hgca_popcount_rows": [P, I64, I64, I64, P, P],
     "hgca_group_need": [P, I64, I64, I64, P, P],
     "hgca_select_topk": [P, I64, I64, I64, P, P, P, I64, P],
-    "hgca_write_rows": [I32, P, P, I64, I64, I64, I64, P, P, I64, P],
+    "hgca_write_rows": [I32, P, I64, I64, I64, I64, P, P, I64, P],
     "hgca_decode_chunk_rows": [I32, I64],
     "hgca_decode_config": [I32, I64, I64, P],
     "hgca_maw_update": [P, I64, I64, I64, I64, P, I64, I64, I64, D, I32, P],
-    "hgca_union_build": [P, I64, I64, I64, I64, I64, I64, P, P, P, P, P, I64, P],
+    "hgca_union_build": [P, I64, I64, I64, I64, I64, I64, P, P, P, P, I64, I32, P],
     "hgca_decode_step": [ctypes.POINTER(DecodeDesc), P],
 }
 _RESTYPES = {"hgca_last_error": ctypes.c_char_p, "hgca_attend_ws_bytes": I64}

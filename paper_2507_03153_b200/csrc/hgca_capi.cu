@@ -106,7 +106,7 @@ int hgca_attend_dense(int dtype, const void* q, const void* k, const void* v, in
   AttendArgs a{};
   a.q = q; a.k = k; a.v = v;
   a.Hq = H; a.Hkv = H; a.G = 1;
-  a.nq = nq; a.d = d; a.ld_head = nkv * d; a.row0 = 0; a.n = nkv;
+  a.nq = nq; a.d = d; a.ld_head = nkv * d; a.ld_row = d; a.row0 = 0; a.n = nkv;
   a.scale = scale;
   a.out = out; a.lse = lse;
   a.wts = keep_weights ? weights : nullptr; a.wts_ld = nkv;
@@ -126,7 +126,7 @@ int hgca_attend_indexed(int dtype, const void* q, const void* k, const void* v, 
   AttendArgs a{};
   a.q = q; a.k = k; a.v = v;
   a.Hq = 1; a.Hkv = 1; a.G = 1;
-  a.nq = nq; a.d = d; a.ld_head = M * d; a.row0 = 0; a.n = n;
+  a.nq = nq; a.d = d; a.ld_head = M * d; a.ld_row = d; a.row0 = 0; a.n = n;
   a.idx = idx;
   a.scale = scale;
   a.out = out; a.lse = lse;
@@ -149,7 +149,7 @@ int hgca_attend_indexed_heads(int dtype, const void* q, const void* k, const voi
   AttendArgs a{};
   a.q = q; a.k = k; a.v = v;
   a.Hq = H; a.Hkv = H; a.G = 1;
-  a.nq = nq; a.d = d; a.ld_head = M * d; a.row0 = 0; a.n = 0;
+  a.nq = nq; a.d = d; a.ld_head = M * d; a.ld_row = d; a.row0 = 0; a.n = 0;
   a.idx = idx; a.idx_off = idx_off; a.idx_cnt = idx_cnt;
   a.scale = scale;
   a.out = out; a.lse = lse;
@@ -158,19 +158,22 @@ int hgca_attend_indexed_heads(int dtype, const void* q, const void* k, const voi
   return cuda_status(launch_attend(dtype, a, H, S(stream)), "attend_indexed_heads");
 }
 
-int hgca_attend_gqa(int dtype, const void* q, const void* K, const void* V, int64_t B, int64_t Hq,
-                    int64_t Hkv, int64_t T, int64_t row0, int64_t n, int64_t nq, int64_t d,
-                    double scale, void* out, double* lse, void* weights, int64_t wts_ld, void* ws,
-                    hgca_stream_t stream) {
+int hgca_attend_gqa(int dtype, const void* q, const void* KV, int64_t B, int64_t Hq, int64_t Hkv, int64_t T,
+                    int64_t row0, int64_t n, int64_t nq, int64_t d, double scale, void* out, double* lse,
+                    void* weights, int64_t wts_ld, void* ws, hgca_stream_t stream) {
   if (B < 1 || Hq < 1 || Hkv < 1 || Hq % Hkv || d < 1 || n < 0 || row0 < 0 || row0 + n > T)
     return fail(HGCA_EINVAL, "attend_gqa: bad shape (B=%lld Hq=%lld Hkv=%lld row0=%lld n=%lld T=%lld)",
                 (long long)B, (long long)Hq, (long long)Hkv, (long long)row0, (long long)n,
                 (long long)T);
   if (weights && wts_ld < n) return fail(HGCA_EINVAL, "attend_gqa: wts_ld < n");
   AttendArgs a{};
-  a.q = q; a.k = K; a.v = V;
+  if (dtype != HGCA_DTYPE_F32 && dtype != HGCA_DTYPE_BF16)
+    return fail(HGCA_EINVAL, "attend_gqa: storage dtype must be float32 or bfloat16");
+  const int64_t esz = dtype == HGCA_DTYPE_BF16 ? 2 : 4;
+  a.q = q; a.k = KV; a.v = reinterpret_cast<const unsigned char*>(KV) + d * esz;
   a.Hq = Hq; a.Hkv = Hkv; a.G = Hq / Hkv;
-  a.nq = nq; a.d = d; a.ld_head = T * d; a.row0 = row0; a.n = n;
+  a.nq = nq; a.d = d; a.ld_head = T * 2 * d; a.ld_row = 2 * d; a.row0 = row0; a.n = n;
+  a.rot = dtype == HGCA_DTYPE_BF16 ? 1 : 0;  // the engine stores bf16 K|V rows position-rotated
   a.scale = scale;
   a.out = out; a.lse = lse;
   a.wts = weights; a.wts_ld = wts_ld;
@@ -258,10 +261,10 @@ int hgca_select_topk(const double* maw, int64_t rows, int64_t ld, int64_t n, con
   return cuda_status(launch_topk_mask(maw, rows, ld, n, k, exclude, out, words, S(stream)), "select_topk");
 }
 
-int hgca_write_rows(int dtype, void* K, void* V, int64_t BH, int64_t T, int64_t d, int64_t pos,
-                    const void* k_new, const void* v_new, int64_t n, hgca_stream_t stream) {
+int hgca_write_rows(int dtype, void* KV, int64_t BH, int64_t T, int64_t d, int64_t pos, const void* k_new,
+                    const void* v_new, int64_t n, hgca_stream_t stream) {
   if (pos < 0 || n < 0 || pos + n > T) return fail(HGCA_EINVAL, "write_rows: position range exceeds buffer");
-  return cuda_status(launch_write_rows(dtype, K, V, BH, T, d, pos, k_new, v_new, n, S(stream)), "write_rows");
+  return cuda_status(launch_write_rows(dtype, KV, BH, T, d, pos, k_new, v_new, n, S(stream)), "write_rows");
 }
 
 int hgca_decode_chunk_rows(int dtype, int64_t d) { return decode_chunk_rows(dtype, d); }
@@ -281,14 +284,16 @@ int hgca_maw_update(const float* w, int64_t BH, int64_t nq, int64_t W, int64_t w
 }
 
 int hgca_union_build(const uint32_t* sel_mask, int64_t B, int64_t Hq, int64_t Hkv, int64_t words,
-                     int64_t n_arch, int64_t T, int32_t* u_pos, uint8_t* u_qm, int32_t* u_cnt,
-                     int32_t* item_off, int32_t* item_tab, int64_t sparse_rows, hgca_stream_t stream) {
+                     int64_t n_arch, int64_t T, int32_t* u_ent, int32_t* u_cnt, int32_t* item_off,
+                     int32_t* item_tab, int64_t sparse_rows, int grouped, hgca_stream_t stream) {
   if (B < 1 || Hkv < 1 || Hq % Hkv || Hq / Hkv > 8 || n_arch < 0 || n_arch > T || words * 32 < n_arch ||
-      sparse_rows < 1)
+      sparse_rows < 1 || T >= (1 << 24))
     return fail(HGCA_EINVAL, "union_build: bad shape");
-  if (!item_tab) return fail(HGCA_EINVAL, "union_build: null item table");
-  return cuda_status(launch_union_build(sel_mask, B, Hq, Hkv, words, n_arch, T, u_pos, u_qm, u_cnt,
-                                        item_off, reinterpret_cast<int4*>(item_tab), sparse_rows, S(stream)),
+  if (!item_tab || !u_ent || !u_cnt || !item_off) return fail(HGCA_EINVAL, "union_build: null output");
+  return cuda_status(launch_union_build(sel_mask, B, Hq, Hkv, words, n_arch, T, u_ent, u_cnt, item_off,
+                                        reinterpret_cast<int4*>(item_tab), sparse_rows,
+                                        grouped == 2 ? 2 : (grouped ? 1 : 0),
+                                        S(stream)),
                      "union_build");
 }
 
@@ -300,43 +305,41 @@ static int decode_prepare(const hgca_decode_desc* d, DecodeArgs& a, DecodeMergeA
   const int64_t G = d->Hq / d->Hkv;
   if (G != 1 && G != 2 && G != 4 && G != 8) return fail(HGCA_EINVAL, "decode_step: Hq/Hkv must be 1, 2, 4 or 8");
   if (d->D != 64 && d->D != 128) return fail(HGCA_EINVAL, "decode_step: head_dim must be 64 or 128");
+  if (d->T < 1 || d->T >= (1 << 24)) return fail(HGCA_EINVAL, "decode_step: T must be in [1, 2^24)");
   const int64_t W = d->dhi - d->dlo;
   if (d->dlo < 0 || W < 1 || d->dhi > d->T || d->w_old < 0 || d->w_old > W || d->dsc_ld < W)
     return fail(HGCA_EINVAL, "decode_step: bad dense range");
-  const int ch = decode_chunk_rows(d->dtype, d->D);
-  if (d->dense_rows < 1 || d->dense_rows % ch || d->sparse_rows < 1)
-    return fail(HGCA_EINVAL, "decode_step: dense_rows must be a positive multiple of %d", ch);
-  const int64_t Sd = (W + d->dense_rows - 1) / d->dense_rows;
-  const int64_t n_dense = d->B * d->Hkv * Sd;
+  if (d->sparse_rows < 1) return fail(HGCA_EINVAL, "decode_step: sparse_rows must be >= 1");
+  const int64_t n_dense = d->B * d->Hkv;
   const int64_t max_sparse = d->B * d->Hkv * ((d->T + d->sparse_rows - 1) / d->sparse_rows);
   if (d->max_items < n_dense + max_sparse)
     return fail(HGCA_EINVAL, "decode_step: partial buffers hold %lld items, need %lld",
                 (long long)d->max_items, (long long)(n_dense + max_sparse));
-  if (!d->K || !d->V || !d->q || !d->u_pos || !d->u_qm || !d->u_cnt || !d->item_off || !d->item_tab || !d->dsc ||
-      !d->part_m || !d->part_z || !d->part_acc || !d->counter || !d->out || !d->lse)
+  if (!d->KV || !d->q || !d->u_ent || !d->u_cnt || !d->item_off || !d->item_tab || !d->dsc || !d->part_m ||
+      !d->part_z || !d->part_acc || !d->counter || !d->out || !d->lse)
     return fail(HGCA_EINVAL, "decode_step: null pointer");
+  if (!(d->alpha >= 0.0 && d->alpha <= 1.0)) return fail(HGCA_EINVAL, "alpha must be in [0, 1], got %g", d->alpha);
   a = DecodeArgs{};
-  a.K = d->K; a.V = d->V; a.q = d->q;
+  a.KV = d->KV; a.q = d->q;
   a.B = d->B; a.Hq = d->Hq; a.Hkv = d->Hkv; a.G = G; a.D = d->D; a.T = d->T;
   a.scale = d->scale;
   a.dlo = d->dlo; a.dhi = d->dhi;
-  a.Sd = Sd; a.dense_rows = d->dense_rows;
-  a.u_pos = d->u_pos; a.u_qm = d->u_qm; a.u_cnt = d->u_cnt; a.item_off = d->item_off;
+  a.u_ent = d->u_ent; a.u_cnt = d->u_cnt; a.item_off = d->item_off;
   a.item_tab = reinterpret_cast<const int4*>(d->item_tab);
   a.sparse_rows = d->sparse_rows;
   a.dsc = d->dsc; a.dsc_ld = d->dsc_ld;
   a.part_m = d->part_m; a.part_z = d->part_z; a.part_acc = d->part_acc;
   a.counter = d->counter;
   a.n_dense_items = n_dense;
+  a.w_old = d->w_old;
+  a.maw = d->maw;
+  a.one_minus_alpha = 1.0 - d->alpha; a.alpha = d->alpha;
+  a.wts_out = d->wts_out;
   m = DecodeMergeArgs{};
   m.B = d->B; m.Hq = d->Hq; m.Hkv = d->Hkv; m.G = G; m.D = d->D;
-  m.Sd = Sd; m.n_dense_items = n_dense; m.item_off = d->item_off;
+  m.n_dense_items = n_dense; m.item_off = d->item_off;
   m.part_m = d->part_m; m.part_z = d->part_z; m.part_acc = d->part_acc;
-  m.dsc = d->dsc; m.dsc_ld = d->dsc_ld;
-  m.W = W; m.w_old = d->w_old;
-  m.maw = d->maw; m.T = d->T; m.dlo = d->dlo;
-  m.one_minus_alpha = 1.0 - d->alpha; m.alpha = d->alpha;
-  m.wts_out = d->wts_out; m.out = d->out; m.lse = d->lse;
+  m.out = d->out; m.lse = d->lse;
   m.out_sparse = d->out_sparse; m.lse_sparse = d->lse_sparse;
   return HGCA_OK;
 }
@@ -347,7 +350,6 @@ int hgca_decode_step(const hgca_decode_desc* d, hgca_stream_t stream) {
   int rc = decode_prepare(d, a, m);
   if (rc) return rc;
   a.m = m;
-  a.bk_done = d->counter + 1;
   return cuda_status(launch_decode_partial(d->dtype, a, S(stream)), "decode_step");
 }
 

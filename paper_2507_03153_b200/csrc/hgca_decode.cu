@@ -1,27 +1,38 @@
 // Decode hot path of the hybrid two-tier attention step (engine.py:151-195,
 // decode mode) for B200 (sm_100a).
 //
-// One persistent kernel (decode_partial_kernel) streams two kinds of work
-// items through the same warp-specialized pipeline:
-//   * dense items  : contiguous window rows [dlo, dhi) of one (batch, kv-head)
-//                    -- all G query heads of the GQA group attend every row
-//                    (engine.py:161-164);
-//   * sparse items : a slice of the (batch, kv-head) union list of selected
-//                    archive rows; each entry carries a G-bit mask of the query
-//                    heads whose context/padding contains it (engine.py:134-149,
-//                    union-deduplicated so every archived row is read once).
-// A producer warp gathers K/V rows with 16-byte cp.async into padded shared
-// memory stages (mbarrier full/empty ring); four consumer warps compute
-//   * fp64 scores, one row per thread, sequential over the head dimension
-//     (exact products, reference summation order: _core.pyx:59-65),
-//   * an fp64 online softmax per query head,
-//   * fp32 P.V accumulation, one warp per query head, lanes over dims.
-// Each item emits (m, z, acc) per query head into a fixed slot, so the result
-// is independent of which CTA ran which item (deterministic, no float atomics).
-// The warp finishing the last item of a (batch, kv-head) then folds its
-// partials in a fixed order, applies the reference merge_states
-// (attention.py:153-188) and the fp64 MAW EMA (kv_cache.py:171-187,
-// engine.py:177-191) from the stored dense scores -- no second kernel.
+// HBM layout: K and V of one position are adjacent (KV [B*Hkv, T, 2, D]), so
+// every selected archive entry is ONE contiguous 2*D*esz-byte row; the TMA
+// unit gathers 4 such rows per tile::gather4 op straight into shared memory.
+//
+// One persistent kernel per step streams two kinds of work items through
+// warp-private TMA pipelines (S stages of SUB=32 rows, mbarrier per stage):
+//   * dense items  : the whole attended window [dlo, dhi) of one (batch,
+//                    kv-head); all G query heads attend every row
+//                    (engine.py:161-164). Item id == bk = b*Hkv + kv-head, so
+//                    they are dispatched first; the warp that finishes one
+//                    also computes the window weights and the fp64 MAW EMA
+//                    (kv_cache.py:171-187, engine.py:177-191) from the dense
+//                    scores it stored -- off the tail of the step.
+//   * sparse items : SPARSE_ROWS-row slices of the (batch, kv-head) union list
+//                    of selected archive rows; each entry carries a G-bit mask
+//                    of the query heads whose context/padding contains it
+//                    (engine.py:134-149), so every archived row is read once.
+// Each item writes (m, z, acc) per query head to a fixed slot; the warp that
+// finishes the last item of a (batch, kv-head) folds them in a fixed order
+// and applies merge_states(sparse, dense) (attention.py:153-188). Results do
+// not depend on which warp ran which item (no float atomics).
+//
+// Two compute variants:
+//   decode_f32_kernel  (float32 storage, the reference-exact path): one key
+//       row per lane, fp64 dot products in the reference's sequential order
+//       (_core.pyx:59-65), fp64 online softmax, fp32 P.V.
+//   decode_bf16_kernel (bfloat16 storage): QK^T and P.V on the tensor cores
+//       with mma.sync m16n8k16 (K rows x 8 query heads; V^T x P^T, P split
+//       into bf16 hi + lo so P keeps ~16 significant bits), fp32 softmax in
+//       the mma fragment layout. The tensor cores are used to cut issue slots
+//       of the 8-head GEMV, not for FLOPs: the kernel stays HBM-bound. K|V rows
+//       land in 128B-swizzled 32x128-byte tiles so ldmatrix is conflict-free.
 #include "hgca_common.cuh"
 #include "hgca_internal.h"
 
@@ -32,7 +43,7 @@ namespace hgca {
 // Debug build only (-DHGCA_TIMELINE): per-warp timeline of the decode kernel,
 // read back with hgca_debug_timeline (tools/timeline.py).
 #ifdef HGCA_TIMELINE
-#define TL_SLOTS 12
+#define TL_SLOTS 16
 __device__ unsigned long long g_tl[148 * 16 * TL_SLOTS];
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -44,93 +55,30 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define TL(...)
 #endif
 
-template <typename T, int D, int G>
-struct DecodeCfg {
-  static constexpr int ESZ = (int)sizeof(T);
-  static constexpr int ROWB = D * ESZ;
-  static constexpr int SUB = 32;                        // rows per sub-chunk (one per lane)
-  static constexpr int PIECES = ROWB / 16;
-  static constexpr int E = 16 / ESZ;                    // elements per 16-byte piece
-  // bf16: K rows gathered by TMA (tile::gather4, 4 rows per op) into dense
-  // rows, read with a per-lane piece rotation; QK in fp32 per 16-byte piece
-  // (8 exact products) accumulated in fp64; V rows gathered into registers.
-  // fp32 (reference-exact path): cp.async into XOR-swizzled rows, per-element
-  // fp64 DFMA in the reference's sequential order, V staged in smem.
-  static constexpr bool TMA = ESZ == 2;
-  static constexpr bool PIECE32 = ESZ == 2;
-  static constexpr bool V_SMEM = ESZ == 4;
-  static constexpr int DPL = D / 32;                    // dims per lane in P.V
-  static constexpr int S = 2;                           // stages per warp
-  static constexpr int OFF_V = SUB * ROWB;
-  static constexpr int OFF_POS = OFF_V + (V_SMEM ? SUB * ROWB : 0);
-  static constexpr int OFF_QM = OFF_POS + SUB * 4;
-  static constexpr int STAGE = ((OFF_QM + SUB) + 127) / 128 * 128;
-  static constexpr int QRAW = G * ROWB;                 // raw query block of one item
-  static constexpr int NQB = S;                         // raw query buffers
-  static constexpr int QK_ESZ = PIECE32 ? 4 : 8;
-  static constexpr int OFF_QRAW = S * STAGE;
-  static constexpr int OFF_QK = OFF_QRAW + NQB * QRAW;  // queries [G][D] (fp32 or fp64)
-  static constexpr int OFF_SC = OFF_QK + G * D * QK_ESZ;// scores [G][32] fp64
-  static constexpr int OFF_ACC = OFF_SC + G * SUB * 8;  // P.V accumulators [G][D] fp32
-  static constexpr int OFF_MZ = OFF_ACC + G * D * 4;    // running (m, z) [G][2] fp64
-  static constexpr int OFF_BAR = OFF_MZ + G * 16;       // mbarriers [S]
-  static constexpr int OFF_DESC = OFF_BAR + S * 8;       // stage descriptors [S]
-  // metadata ring: descriptor + union entries (pos, mask) of the next
-  // sub-chunks, fetched with cp.async one issue ahead
-  static constexpr int MR = 2;
-  static constexpr int MSLOT = 32 + SUB * 4 + SUB;       // desc, pos[32], qm[32]
-  static constexpr int OFF_META = ((OFF_DESC + S * 32) + 15) / 16 * 16;
-  static constexpr int WARP_SMEM = ((OFF_META + MR * MSLOT) + 127) / 128 * 128;
-  static constexpr int NC0 = (232448 - 2048) / WARP_SMEM;
-  // <= 8 warps: at most 2 per SM sub-partition, so 255 registers per thread
-  static constexpr int NC = NC0 > 8 ? 8 : NC0;
-  static constexpr int SMEM = NC * WARP_SMEM;
-  static_assert(NC >= 1, "decode warp pipeline does not fit shared memory");
-  static_assert(D % 32 == 0, "head_dim must be a multiple of 32");
-};
+#ifndef HGCA_BF16_STAGES
+#define HGCA_BF16_STAGES 2
+#endif
+
+constexpr int SUB = 32;  // rows per pipeline stage (one per lane)
+constexpr uint32_t FULL = 0xffffffffu;
+constexpr int SMEM_MAX = 232448;  // dynamic shared memory per CTA on sm_100
 
 // Per-stage descriptor (smem, written by the warp that issued the stage).
 struct StageDesc {
   int item, bk, r0, n;
-  int first, last, dense, qbuf;
+  int first, last, dense, pad;
 };
 
-__device__ __forceinline__ int swz(int r, int p) { return (p & ~7) | ((p ^ r) & 7); }
-
-template <typename T>
-__device__ __forceinline__ void unpack8(const uint4 v, float* f);
-template <>
-__device__ __forceinline__ void unpack8<__nv_bfloat16>(const uint4 v, float* f) {
-  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    f[2 * i] = __uint_as_float(w[i] << 16);
-    f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
-  }
-}
-
-template <typename T, int DPL>
-__device__ __forceinline__ void load_v_f32(const unsigned char* p, float* out);
-template <>
-__device__ __forceinline__ void load_v_f32<float, 4>(const unsigned char* p, float* out) {
-  const float4 v = *reinterpret_cast<const float4*>(p);
-  out[0] = v.x; out[1] = v.y; out[2] = v.z; out[3] = v.w;
-}
-template <>
-__device__ __forceinline__ void load_v_f32<float, 2>(const unsigned char* p, float* out) {
-  const float2 v = *reinterpret_cast<const float2*>(p);
-  out[0] = v.x; out[1] = v.y;
-}
-
+// ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, int col, int r0, int r1, int r2,
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map, int col, int r0, int r1, int r2,
                                             int r3, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(smem_u32(dst)),
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(dst),
       "l"(map), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
       : "memory");
 }
@@ -139,311 +87,614 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+// D = A(16x16 bf16, row) * B(16x8 bf16, col) + D, fp32 accumulate
+__device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);  // .x (low 16 bits) = lo
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ float bf16_lo_f(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16_hi_f(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
 
-// ------------------------------------------------------------ in-kernel merge
-// Run by the warp that finishes the last work item of (b, kv-head) bk: folds
-// the dense and sparse partials of each of the G query heads in a fixed order
-// (so the result does not depend on which warp runs it), applies
-// merge_states(sparse, dense) (attention.py:153-188, engine.py:166-169) and
-// the fp64 MAW maintenance of the attended window from the stored scores:
+// ------------------------------------------------------------------ work items
+// Item ids: [0, B*Hkv) dense (item == bk; window rows [0, W)), then the
+// sparse items of item_tab. The cursor walks a warp through items in
+// sub-chunks of SUB rows; lane 0 holds the prefetched id of the next item.
+struct Cursor {
+  int nxt;  // lane 0
+  int item, bk, lo, hi, row, dense;
+};
+
+__device__ __forceinline__ StageDesc cursor_next(Cursor& c, const DecodeArgs& a, int total, int W, int lane) {
+  StageDesc d;
+  if (c.item < 0 || c.row >= c.hi) {
+    const int it = __shfl_sync(FULL, c.nxt, 0);
+    if (it >= total) {
+      d.item = -1;
+      d.bk = d.r0 = d.n = d.first = d.last = d.dense = d.pad = 0;
+      return d;
+    }
+    c.item = it;
+    if (lane == 0) c.nxt = atomicAdd(a.counter, 1);
+    if (it < (int)a.n_dense_items) {
+      c.dense = 1;
+      c.bk = it;
+      c.lo = 0;
+      c.hi = W;
+    } else {
+      c.dense = 0;
+      const int4 e = __ldg(a.item_tab + (it - (int)a.n_dense_items));  // (bk, lo, hi, -)
+      c.bk = e.x;
+      c.lo = e.y;
+      c.hi = e.z;
+    }
+    c.row = c.lo;
+  }
+  d.item = c.item;
+  d.bk = c.bk;
+  d.r0 = c.row;
+  d.n = min(SUB, c.hi - c.row);
+  d.first = c.row == c.lo;
+  d.last = c.row + SUB >= c.hi;
+  d.dense = c.dense;
+  d.pad = 0;
+  c.row += SUB;
+  return d;
+}
+
+// Union entry of lane's row of sub-chunk d: position | (query-head mask << 24).
+// Rows past the sub-chunk end get position 0 and an empty mask.
+template <int G>
+__device__ __forceinline__ int32_t sub_entry(const StageDesc& d, const DecodeArgs& a, int lane) {
+  if (d.item < 0 || lane >= d.n) return 0;
+  if (d.dense) return (int32_t)(a.dlo + d.r0 + lane) | (int32_t)(((1u << G) - 1u) << 24);
+  return __ldg(a.u_ent + (int64_t)d.bk * a.T + d.r0 + lane);
+}
+
+// ------------------------------------------------------------------ epilogues
+// Dense-item epilogue: weights of the attended window from the stored scores
+// and the item's final (m, z), and the fp64 MAW maintenance:
 //   w   = float32(exp(s - m) / z)                     (_core.pyx:81-82)
 //   maw = (1-alpha)*maw + alpha*w   (3 roundings)     (kv_cache.py:186)
 //   new entries: maw = w                              (engine.py:191)
-template <int D, int G>
-__device__ __forceinline__ void warp_fold(const DecodeArgs& a, int64_t i0, int64_t i1, int g, int lane,
-                                          double& M, double& Z, double* acc) {
-  constexpr int DPL = D / 32;
-  const uint32_t FULL = 0xffffffffu;
-  double mx = -INFINITY;
-  for (int64_t i = i0 + lane; i < i1; i += 32) mx = fmax(mx, __ldcg(a.m.part_m + i * G + g));
-  M = warp_max_f64(mx);
-  double z = 0.0;
-#pragma unroll
-  for (int k = 0; k < DPL; ++k) acc[k] = 0.0;
-  for (int64_t c0 = i0; c0 < i1; c0 += 32) {
-    const int64_t i = c0 + lane;
-    double w = 0.0;
-    if (i < i1) {
-      const double mi = __ldcg(a.m.part_m + i * G + g);
-      if (mi != -INFINITY) {
-        w = exp(mi - M);
-        z += __ldcg(a.m.part_z + i * G + g) * w;
-      }
-    }
-    const int n = (int)min((int64_t)32, i1 - c0);
-    const float* pa = a.m.part_acc + (c0 * G + g) * D + lane * DPL;
-#pragma unroll 8
-    for (int jj = 0; jj < n; ++jj) {
-      const double wj = __shfl_sync(FULL, w, jj);
-      if constexpr (DPL == 4) {
-        const float4 v = __ldcg(reinterpret_cast<const float4*>(pa + (int64_t)jj * G * D));
-        acc[0] += wj * v.x; acc[1] += wj * v.y; acc[2] += wj * v.z; acc[3] += wj * v.w;
-      } else {
-        const float2 v = __ldcg(reinterpret_cast<const float2*>(pa + (int64_t)jj * G * D));
-        acc[0] += wj * v.x; acc[1] += wj * v.y;
-      }
-    }
-  }
-  Z = warp_sum_f64(z);
-}
-
-template <int D, int G>
-__device__ void warp_merge_bk(const DecodeArgs& a, int64_t bk, int lane) {
-  constexpr int DPL = D / 32;
-  const DecodeMergeArgs& m = a.m;
+// The scores were written by this warp (__syncwarp orders them).
+template <typename SC, int G>
+__device__ void dense_epilogue(const DecodeArgs& a, int bk, const double* m, const double* z, int lane) {
+  if (a.maw == nullptr && a.wts_out == nullptr) return;
+  constexpr int JB = G >= 4 ? 2 : 8 / G;  // window rows per lane per batch: JB*G loads of each kind in flight
+  const int64_t W = a.dhi - a.dlo;
   const int64_t b = bk / a.Hkv, kvh = bk % a.Hkv;
-  const int64_t d0 = bk * a.Sd, d1 = d0 + a.Sd;
-  const int64_t s0 = a.n_dense_items + __ldcg(a.item_off + bk), s1 = a.n_dense_items + __ldcg(a.item_off + bk + 1);
-  for (int g = 0; g < G; ++g) {
-    const int64_t bq = b * a.Hq + kvh * G + g;
-    double Md, Zd, Ms, Zs, ad[DPL], as[DPL];
-    warp_fold<D, G>(a, d0, d1, g, lane, Md, Zd, ad);
-    warp_fold<D, G>(a, s0, s1, g, lane, Ms, Zs, as);
-    const bool s_empty = !(Zs > 0.0);
-    const bool d_empty = !(Zd > 0.0);
-    const double lse_s = s_empty ? -INFINITY : Ms + log(Zs);
-    const double lse_d = d_empty ? -INFINITY : Md + log(Zd);
-    const double mm = fmax(lse_s, lse_d);
-    const bool both_empty = mm == -INFINITY;
-    const double ms = both_empty ? 0.0 : mm;
-    const double wa = exp(lse_s - ms), wb = exp(lse_d - ms);
-    const double zs = both_empty ? 1.0 : wa + wb;
-    const float ca = (float)(wa / zs), cb = (float)(wb / zs);
+  const int64_t bq0 = b * a.Hq + kvh * G;
+  const SC* dsc = reinterpret_cast<const SC*>(a.dsc);
+  for (int64_t j0 = 0; j0 < W; j0 += 32 * JB) {
+    SC sv[JB][G];
+    double mo[JB][G];
 #pragma unroll
-    for (int k = 0; k < DPL; ++k) {
-      const int c = lane * DPL + k;
-      const float od = d_empty ? 0.f : (float)(ad[k] / Zd);
-      const float os = s_empty ? 0.f : (float)(as[k] / Zs);
-      m.out[bq * D + c] = __fadd_rn(__fmul_rn(ca, os), __fmul_rn(cb, od));
-      if (m.out_sparse) m.out_sparse[bq * D + c] = os;
+    for (int u = 0; u < JB; ++u) {
+      const int64_t j = j0 + u * 32 + lane;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        sv[u][g] = j < W ? __ldcg(dsc + (bq0 + g) * a.dsc_ld + j) : (SC)0;
+        mo[u][g] = (a.maw && j < a.w_old) ? a.maw[(bq0 + g) * a.T + a.dlo + j] : 0.0;
+      }
     }
-    if (lane == 0) {
-      m.lse[bq] = both_empty ? -INFINITY : ms + log(zs);
-      if (m.lse_sparse) m.lse_sparse[bq] = lse_s;
-    }
-    if (m.maw == nullptr && m.wts_out == nullptr) continue;
-#pragma unroll 4
-    for (int64_t j = lane; j < m.W; j += 32) {
-      const float w32 = d_empty ? 0.f : (float)(exp(__ldcg(m.dsc + bq * m.dsc_ld + j) - Md) / Zd);
-      if (m.wts_out) m.wts_out[bq * m.W + j] = w32;
-      if (m.maw) {
-        double* mp = m.maw + bq * m.T + m.dlo + j;
-        const double aw = (double)w32;
-        *mp = j < m.w_old ? __dadd_rn(__dmul_rn(m.one_minus_alpha, *mp), __dmul_rn(m.alpha, aw)) : aw;
+#pragma unroll
+    for (int u = 0; u < JB; ++u) {
+      const int64_t j = j0 + u * 32 + lane;
+      if (j >= W) continue;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const int64_t bq = bq0 + g;
+        const float w32 = !(z[g] > 0.0) ? 0.f : (float)(exp((double)sv[u][g] - m[g]) / z[g]);
+        if (a.wts_out) a.wts_out[bq * W + j] = w32;
+        if (a.maw) {
+          const double aw = (double)w32;
+          a.maw[bq * a.T + a.dlo + j] =
+              j < a.w_old ? __dadd_rn(__dmul_rn(a.one_minus_alpha, mo[u][g]), __dmul_rn(a.alpha, aw)) : aw;
+        }
       }
     }
   }
 }
 
-template <typename T, int D, int G>
-__global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial_kernel(const __grid_constant__ DecodeArgs a) {
-  using C = DecodeCfg<T, D, G>;
-  extern __shared__ __align__(128) unsigned char sm[];
+// ------------------------------------------------------------------ merge kernel
+// One CTA per (batch, query head), one thread per head dimension. Folds the
+// per-item partials of its (batch, kv-head) in item order -- sparse items into
+// the context partial, the dense item into the window partial -- then applies
+// merge_states(sparse, dense) (attention.py:153-188, engine.py:166-169).
+// Launched right behind the decode kernel with programmatic dependent launch:
+// its CTAs become resident early and wait in griddepcontrol.wait until the
+// decode grid has finished and its writes are visible.
+template <int D, int G>
+__global__ void __launch_bounds__(D) decode_merge_kernel(const DecodeMergeArgs m) {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  __shared__ double wsh[1024];
+  __shared__ double red[D / 32];
+  __shared__ double stat[2];
+  const int64_t bq = blockIdx.x;
+  const int64_t b = bq / m.Hq, h = bq % m.Hq;
+  const int64_t kvh = h / G, g = h % G, bk = b * m.Hkv + kvh;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  auto block_max = [&](double x) {
+    x = warp_max_f64(x);
+    if (lane == 0) red[wid] = x;
+    __syncthreads();
+    if (tid == 0) {
+      double y = red[0];
+      for (int i = 1; i < D / 32; ++i) y = fmax(y, red[i]);
+      stat[0] = y;
+    }
+    __syncthreads();
+    const double r = stat[0];
+    __syncthreads();
+    return r;
+  };
+  auto block_sum = [&](double x) {
+    x = warp_sum_f64(x);
+    if (lane == 0) red[wid] = x;
+    __syncthreads();
+    if (tid == 0) {
+      double y = 0.0;
+      for (int i = 0; i < D / 32; ++i) y += red[i];  // fixed order
+      stat[1] = y;
+    }
+    __syncthreads();
+    const double r = stat[1];
+    __syncthreads();
+    return r;
+  };
+  // fold items [i0, i1) of head g: returns (out, lse) of the partial union
+  auto fold = [&](int64_t i0, int64_t i1, float& o, double& lse) {
+    o = 0.f;
+    lse = -INFINITY;
+    if (i1 <= i0) return;
+    double mx = -INFINITY;
+    for (int64_t i = i0 + tid; i < i1; i += D) mx = fmax(mx, m.part_m[i * G + g]);
+    const double M = block_max(mx);
+    if (M == -INFINITY) return;
+    double zl = 0.0, acc = 0.0;
+    for (int64_t c0 = i0; c0 < i1; c0 += 1024) {
+      const int64_t c1 = min(i1, c0 + 1024);
+      for (int64_t i = c0 + tid; i < c1; i += D) {
+        const double mi = m.part_m[i * G + g];
+        const double w = mi == -INFINITY ? 0.0 : exp(mi - M);
+        wsh[i - c0] = w;
+        zl += m.part_z[i * G + g] * w;
+      }
+      __syncthreads();
+      const float* pa = m.part_acc + (c0 * G + g) * D + tid;
+      const int n = (int)(c1 - c0);
+      int j = 0;
+      for (; j + 8 <= n; j += 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = pa[(int64_t)(j + u) * G * D];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += wsh[j + u] * (double)v[u];
+      }
+      for (; j < n; ++j) acc += wsh[j] * (double)pa[(int64_t)j * G * D];
+      __syncthreads();
+    }
+    const double Z = block_sum(zl);
+    if (!(Z > 0.0)) return;
+    o = (float)(acc / Z);
+    lse = M + log(Z);
+  };
+  const int64_t s0 = m.n_dense_items + m.item_off[bk], s1 = m.n_dense_items + m.item_off[bk + 1];
+  float os, od;
+  double lse_s, lse_d;
+  fold(s0, s1, os, lse_s);
+  fold(bk, bk + 1, od, lse_d);
+  const double mm = fmax(lse_s, lse_d);
+  const bool both_empty = mm == -INFINITY;
+  const double ms = both_empty ? 0.0 : mm;
+  const double wa = exp(lse_s - ms), wb = exp(lse_d - ms);
+  const double zs = both_empty ? 1.0 : wa + wb;
+  const float ca = (float)(wa / zs), cb = (float)(wb / zs);
+  m.out[bq * D + tid] = __fadd_rn(__fmul_rn(ca, os), __fmul_rn(cb, od));
+  if (m.out_sparse) m.out_sparse[bq * D + tid] = os;
+  if (tid == 0) {
+    m.lse[bq] = both_empty ? -INFINITY : ms + log(zs);
+    if (m.lse_sparse) m.lse_sparse[bq] = lse_s;
+  }
+}
+
+// =========================================================== bf16 (tensor-core) kernel
+template <int D, int G, int S>
+struct Bf16Cfg {
+  static constexpr int ROWB = D * 2;                    // bytes of one K (or V) row
+  static constexpr int STAGE = SUB * 2 * ROWB;          // 32 rotated K|V row pairs
+  static constexpr int NOPS = SUB / 4;                  // gather4 ops per stage (whole row pairs)
+  static constexpr int QB = G * ROWB;                   // raw query block of one item
+  static constexpr int QSLOT = (QB + 127) / 128 * 128;
+  static constexpr int PT_LD = 40;                      // P^T staging row (floats), conflict-free
+  static constexpr int OFF_Q = S * STAGE;
+  static constexpr int OFF_PT = OFF_Q + S * QSLOT;
+  static constexpr int OFF_META = OFF_PT + 8 * PT_LD * 4;
+  static constexpr int OFF_DESC = OFF_META + S * SUB * 4;
+  static constexpr int OFF_BAR = OFF_DESC + S * 32;
+  static constexpr int OFF_ST = OFF_BAR + S * 8;        // final (m, z) per head, fp64
+  static constexpr int WARP_SMEM = (OFF_ST + 16 * 8 + 1023) / 1024 * 1024;
+  static constexpr int NC0 = (SMEM_MAX - 1024) / WARP_SMEM;
+  static constexpr int NC = NC0 > 16 ? 16 : NC0;
+  static constexpr int SMEM = NC * WARP_SMEM + 1024;    // + alignment slack
+  static_assert(NC >= 1, "bf16 decode pipeline does not fit shared memory");
+  static_assert(G <= 8, "at most 8 query heads per kv head");
+};
+
+// swizzled byte offset of 16-byte chunk `ch` of row `r` inside a 32x128 B tile
+__device__ __forceinline__ uint32_t swz128(int r, int ch) { return (uint32_t)(r * 128 + ((ch ^ (r & 7)) << 4)); }
+
+// bf16 K|V rows are stored rotated by position (write_rows_kernel): 16-byte
+// chunk c of the row pair of position p sits at chunk (c & ~7) | ((c ^ p) & 7),
+// a permutation inside each 128-byte segment. Byte offset of logical chunk c
+// of stage row r holding a position with p & 7 == rot:
+template <int D>
+__device__ __forceinline__ uint32_t rotoff(int r, int c, int rot) {
+  return (uint32_t)(r * 4 * D + (((c & ~7) | ((c ^ rot) & 7)) << 4));
+}
+
+template <int D, int G, int S>
+__global__ void __launch_bounds__(Bf16Cfg<D, G, S>::NC * 32, 1) decode_bf16_kernel(const __grid_constant__ DecodeArgs a) {
+  using C = Bf16Cfg<D, G, S>;
+  constexpr int KC = D / 16;  // k16 chunks of the head dim (QK) == m16 tiles of the head dim (PV)
+  extern __shared__ unsigned char sm_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t FULL = 0xffffffffu;
   unsigned char* wsm = sm + warp * C::WARP_SMEM;
+  const uint32_t wsm_u = smem_u32(wsm);
   StageDesc* desc = reinterpret_cast<StageDesc*>(wsm + C::OFF_DESC);
   uint64_t* bar = reinterpret_cast<uint64_t*>(wsm + C::OFF_BAR);
+  int32_t* meta = reinterpret_cast<int32_t*>(wsm + C::OFF_META);
+  float* pt = reinterpret_cast<float*>(wsm + C::OFF_PT);
+  double* st = reinterpret_cast<double*>(wsm + C::OFF_ST);
+  const int W = (int)(a.dhi - a.dlo);
+  const int total = (int)(a.n_dense_items + (int64_t)a.item_off[a.B * a.Hkv]);
+  const unsigned char* Qg = reinterpret_cast<const unsigned char*>(a.q);
+  const int g4 = lane >> 2, t4 = lane & 3;      // mma groupID / thread-in-group
+  const int hA = 2 * t4, hB = 2 * t4 + 1;       // query heads of this lane's fragment columns
+  const float scale = (float)a.scale;
+  if (lane < S) mbar_init(&bar[lane], 1);
+  fence_mbar_init();
+  __syncwarp();
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // let the merge grid get resident
+  TL(unsigned long long* tl = g_tl + ((int64_t)blockIdx.x * C::NC + warp) * TL_SLOTS;
+     unsigned long long tl_merge = 0, tl_wait = 0, tl_sub = 0, tl_items = 0, tl_qk = 0, tl_pv = 0, tl_v = 0,
+                        tl_issue = 0, tl_tma = 0, tl_nmerge = 0, tl_sm = 0, tl_epi = 0;
+     if (lane == 0) tl[0] = gtimer(););
+
+  Cursor cur;
+  cur.nxt = 0;
+  if (lane == 0) cur.nxt = atomicAdd(a.counter, 1);
+  cur.item = -1;
+  cur.row = cur.hi = cur.lo = cur.bk = cur.dense = 0;
+  StageDesc pend = cursor_next(cur, a, total, W, lane);
+  int32_t pend_ent = sub_entry<G>(pend, a, lane);
+
+  // Place the pending sub-chunk into stage slot s (TMA gathers of its K|V
+  // rows, plus the item's queries on its first sub-chunk) and advance.
+  auto issue = [&](int s) {
+    const StageDesc d = pend;
+    const int32_t ent = pend_ent;
+    if (lane == 0) desc[s] = d;
+    meta[s * SUB + lane] = ent;
+    if (d.item >= 0) {
+      const int pos = ent & 0xffffff;
+      const int rg = lane & 7;  // 4-row group of this lane's gather4 op
+      const int rowbase = d.bk * (int)a.T;
+      const int q0 = __shfl_sync(FULL, pos, rg * 4 + 0);
+      const int q1 = __shfl_sync(FULL, pos, rg * 4 + 1);
+      const int q2 = __shfl_sync(FULL, pos, rg * 4 + 2);
+      const int q3 = __shfl_sync(FULL, pos, rg * 4 + 3);
+      if (lane == 0) mbar_expect_tx(&bar[s], C::STAGE + (d.first ? C::QB : 0));
+      __syncwarp();
+      TL(long long i0 = clock64();)
+      if (lane < C::NOPS)
+        tma_gather4(wsm_u + s * C::STAGE + rg * 4 * 2 * C::ROWB, &a.kmap, 0, rowbase + q0, rowbase + q1,
+                    rowbase + q2, rowbase + q3, &bar[s]);
+      TL(tl_tma += clock64() - i0;)
+      if (lane == 0 && d.first) {
+        const int64_t b = d.bk / a.Hkv, kvh = d.bk % a.Hkv;
+        bulk_g2s(wsm + C::OFF_Q + s * C::QSLOT, Qg + (b * a.Hq + kvh * G) * (int64_t)C::ROWB, C::QB, &bar[s]);
+      }
+    }
+    pend = cursor_next(cur, a, total, W, lane);
+    pend_ent = sub_entry<G>(pend, a, lane);
+  };
+
+#pragma unroll
+  for (int s = 0; s < S; ++s) issue(s);
+
+  // per-item state (fragment layout: this lane owns heads hA, hB)
+  uint32_t qf[KC][2];
+  float acc[KC][4];
+  float mA = -INFINITY, mB = -INFINITY, zA = 0.f, zB = 0.f;
+
+  for (int k = 0;; ++k) {
+    const int s = k % S;
+    __syncwarp();
+    TL(long long c0 = clock64();)
+    const StageDesc d = desc[s];
+    if (d.item < 0) break;
+    mbar_wait(&bar[s], (k / S) & 1);
+    TL(long long c1 = clock64(); tl_wait += c1 - c0; ++tl_sub;)
+    const uint32_t stg = wsm_u + s * C::STAGE;
+    if (d.first) {
+      const uint32_t* qw = reinterpret_cast<const uint32_t*>(wsm + C::OFF_Q + s * C::QSLOT);
+#pragma unroll
+      for (int kc = 0; kc < KC; ++kc) {
+        qf[kc][0] = g4 < G ? qw[g4 * (D / 2) + kc * 8 + t4] : 0u;
+        qf[kc][1] = g4 < G ? qw[g4 * (D / 2) + kc * 8 + 4 + t4] : 0u;
+      }
+#pragma unroll
+      for (int mt = 0; mt < KC; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
+      mA = mB = -INFINITY;
+      zA = zB = 0.f;
+    }
+    TL(long long c2 = clock64(); tl_v += c2 - c1;)
+    // ---- S = K Q^T: rows x heads, fp32 accumulate on the tensor cores.
+    // ldmatrix row of this lane: K rows h*16 + (mi&1)*8 + (lane&7), k-half mi>>1
+    const int mi = lane >> 3;
+    float c[2][4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      c[h][0] = c[h][1] = c[h][2] = c[h][3] = 0.f;
+      const int r = h * 16 + (mi & 1) * 8 + (lane & 7);
+      const int rot = meta[s * SUB + r] & 7;
+#pragma unroll
+      for (int kc = 0; kc < KC; ++kc) {
+        uint32_t af[4];
+        ldsm_x4(stg + rotoff<D>(r, 2 * kc + (mi >> 1), rot), af);
+        mma_bf16(c[h], af, qf[kc][0], qf[kc][1]);
+      }
+    }
+    // ---- scale + mask: value j of this lane is row j*8 + g4, heads hA / hB
+    float sA[4], sB[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int row = j * 8 + g4;
+      const uint32_t qm = (uint32_t)meta[s * SUB + row] >> 24;
+      const bool ok = row < d.n;
+      const float va = c[j >> 1][(j & 1) * 2 + 0] * scale;
+      const float vb = c[j >> 1][(j & 1) * 2 + 1] * scale;
+      sA[j] = (ok && hA < G && ((qm >> hA) & 1u)) ? va : -INFINITY;
+      sB[j] = (ok && hB < G && ((qm >> hB) & 1u)) ? vb : -INFINITY;
+      if (d.dense && ok) {
+        float* dsc = reinterpret_cast<float*>(a.dsc);
+        const int64_t bq0 = (int64_t)(d.bk / a.Hkv) * a.Hq + (d.bk % a.Hkv) * G;
+        if (hA < G) dsc[(bq0 + hA) * a.dsc_ld + d.r0 + row] = va;
+        if (hB < G) dsc[(bq0 + hB) * a.dsc_ld + d.r0 + row] = vb;
+      }
+    }
+    // ---- online softmax (fp32) per head, reduced over the 8 lanes sharing t4
+    float xA = fmaxf(fmaxf(sA[0], sA[1]), fmaxf(sA[2], sA[3]));
+    float xB = fmaxf(fmaxf(sB[0], sB[1]), fmaxf(sB[2], sB[3]));
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      xA = fmaxf(xA, __shfl_xor_sync(FULL, xA, o));
+      xB = fmaxf(xB, __shfl_xor_sync(FULL, xB, o));
+    }
+    const float nA = fmaxf(mA, xA), nB = fmaxf(mB, xB);
+    const float alA = nA == -INFINITY ? 1.f : __expf(mA - nA);
+    const float alB = nB == -INFINITY ? 1.f : __expf(mB - nB);
+    float pA[4], pB[4], sumA = 0.f, sumB = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      pA[j] = sA[j] == -INFINITY ? 0.f : __expf(sA[j] - nA);
+      pB[j] = sB[j] == -INFINITY ? 0.f : __expf(sB[j] - nB);
+      sumA += pA[j];
+      sumB += pB[j];
+    }
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      sumA += __shfl_xor_sync(FULL, sumA, o);
+      sumB += __shfl_xor_sync(FULL, sumB, o);
+    }
+    zA = zA * alA + sumA;
+    zB = zB * alB + sumB;
+    mA = nA;
+    mB = nB;
+    if (__any_sync(FULL, alA != 1.f || alB != 1.f)) {
+#pragma unroll
+      for (int mt = 0; mt < KC; ++mt) {
+        acc[mt][0] *= alA; acc[mt][1] *= alB; acc[mt][2] *= alA; acc[mt][3] *= alB;
+      }
+    }
+    // ---- P^T to shared memory (rows x heads -> heads x rows)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int row = j * 8 + g4;
+      if (hA < G) pt[hA * C::PT_LD + row] = pA[j];
+      if (hB < G) pt[hB * C::PT_LD + row] = pB[j];
+    }
+    __syncwarp();
+    TL(long long c3 = clock64(); tl_qk += c3 - c2;)
+    // ---- O^T += V^T P^T: dims x heads; P = hi + lo in bf16
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      uint32_t bh0 = 0, bh1 = 0, bl0 = 0, bl1 = 0;
+      if (g4 < G) {
+        const float2 p01 = *reinterpret_cast<const float2*>(pt + g4 * C::PT_LD + kk * 16 + 2 * t4);
+        const float2 p89 = *reinterpret_cast<const float2*>(pt + g4 * C::PT_LD + kk * 16 + 8 + 2 * t4);
+        bh0 = pack_bf16(p01.x, p01.y);
+        bh1 = pack_bf16(p89.x, p89.y);
+        bl0 = pack_bf16(p01.x - bf16_lo_f(bh0), p01.y - bf16_hi_f(bh0));
+        bl1 = pack_bf16(p89.x - bf16_lo_f(bh1), p89.y - bf16_hi_f(bh1));
+      }
+      // ldmatrix.trans row of this lane: V rows kk*16 + (mi>>1)*8 + (lane&7), dim-half mi&1
+      const int r = kk * 16 + (mi >> 1) * 8 + (lane & 7);
+      const int rot = meta[s * SUB + r] & 7;
+#pragma unroll
+      for (int mt = 0; mt < KC; ++mt) {
+        uint32_t af[4];
+        ldsm_x4_t(stg + rotoff<D>(r, D / 8 + mt * 2 + (mi & 1), rot), af);
+        mma_bf16(acc[mt], af, bh0, bh1);
+        mma_bf16(acc[mt], af, bl0, bl1);
+      }
+    }
+    TL(long long c4 = clock64(); tl_pv += c4 - c3;)
+    if (d.last) {
+      TL(++tl_items;)
+      // partial (m, z, acc) of this item; acc[mt][j] = O[head hA|hB][dim mt*16 + g4 (+8)]
+      if (lane < 4) {
+        if (hA < G) { a.part_m[(int64_t)d.item * G + hA] = mA; a.part_z[(int64_t)d.item * G + hA] = zA; }
+        if (hB < G) { a.part_m[(int64_t)d.item * G + hB] = mB; a.part_z[(int64_t)d.item * G + hB] = zB; }
+      }
+      float* pa = a.part_acc + (int64_t)d.item * G * D;
+#pragma unroll
+      for (int mt = 0; mt < KC; ++mt) {
+        if (hA < G) { pa[hA * D + mt * 16 + g4] = acc[mt][0]; pa[hA * D + mt * 16 + 8 + g4] = acc[mt][2]; }
+        if (hB < G) { pa[hB * D + mt * 16 + g4] = acc[mt][1]; pa[hB * D + mt * 16 + 8 + g4] = acc[mt][3]; }
+      }
+      if (d.dense) {
+        if (lane < 4) {
+          if (hA < G) { st[hA] = mA; st[8 + hA] = zA; }
+          if (hB < G) { st[hB] = mB; st[8 + hB] = zB; }
+        }
+        __syncwarp();
+        double mm[G], zz[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) { mm[g] = st[g]; zz[g] = st[8 + g]; }
+        TL(long long e0 = clock64();)
+        dense_epilogue<float, G>(a, d.bk, mm, zz, lane);
+        TL(tl_epi += clock64() - e0;)
+      }
+
+    }
+    __syncwarp();
+    TL(long long c5 = clock64();)
+    issue(s);
+    TL(tl_issue += clock64() - c5;)
+  }
+  TL(if (lane == 0) {
+    tl[1] = gtimer();
+    tl[2] = tl_merge; tl[3] = tl_wait; tl[4] = tl_sub; tl[5] = tl_items; tl[6] = tl_qk; tl[7] = tl_pv;
+    tl[8] = tl_v; tl[9] = tl_issue; tl[10] = tl_tma; tl[11] = tl_nmerge; tl[12] = tl_sm; tl[13] = tl_epi;
+  })
+}
+
+// =========================================================== fp32 (reference-exact) kernel
+template <int D, int G>
+struct F32Cfg {
+  static constexpr int ROWB = D * 4;
+  static constexpr int NKC = ROWB / 128;                // 128-byte tiles per K (or V) row
+  static constexpr int TILE = SUB * 128;                // 32 rows x 128 B, 128B-swizzled
+  static constexpr int PIECES = ROWB / 16;
+  static constexpr int DPL = D / 32;
+  static constexpr int S = 2;
+  static constexpr int STAGE = 2 * NKC * TILE;
+  static constexpr int NOPS = SUB / 4 * 2 * NKC;        // gather4 ops per stage
+  static_assert(NOPS % 32 == 0, "whole gather4 ops per lane");
+  static constexpr int QB = G * ROWB;
+  static constexpr int OFF_Q = S * STAGE;                   // raw queries [S][G][D] f32
+  static constexpr int OFF_QK = OFF_Q + S * QB;             // queries [G][D] fp64
+  static constexpr int OFF_SC = OFF_QK + G * D * 8;         // scores [G][32] fp64
+  static constexpr int OFF_ACC = OFF_SC + G * SUB * 8;      // P.V accumulators [G][D] fp32
+  static constexpr int OFF_MZ = OFF_ACC + G * D * 4;        // running (m, z) [G][2] fp64
+  static constexpr int OFF_META = OFF_MZ + G * 16;          // entries [S][32]
+  static constexpr int OFF_DESC = OFF_META + S * SUB * 4;
+  static constexpr int OFF_BAR = OFF_DESC + S * 32;
+  static constexpr int WARP_SMEM = (OFF_BAR + S * 8 + 1023) / 1024 * 1024;
+  static constexpr int NC0 = (SMEM_MAX - 1024) / WARP_SMEM;
+  static constexpr int NC = NC0 > 8 ? 8 : NC0;
+  static constexpr int SMEM = NC * WARP_SMEM + 1024;
+  static_assert(NC >= 1, "fp32 decode pipeline does not fit shared memory");
+};
+
+template <int D, int G>
+__global__ void __launch_bounds__(F32Cfg<D, G>::NC * 32, 1) decode_f32_kernel(const __grid_constant__ DecodeArgs a) {
+  using C = F32Cfg<D, G>;
+  extern __shared__ unsigned char sm_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* wsm = sm + warp * C::WARP_SMEM;
+  const uint32_t wsm_u = smem_u32(wsm);
+  StageDesc* desc = reinterpret_cast<StageDesc*>(wsm + C::OFF_DESC);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wsm + C::OFF_BAR);
+  int32_t* meta = reinterpret_cast<int32_t*>(wsm + C::OFF_META);
+  double* qk = reinterpret_cast<double*>(wsm + C::OFF_QK);
   double* sc = reinterpret_cast<double*>(wsm + C::OFF_SC);
   float* accs = reinterpret_cast<float*>(wsm + C::OFF_ACC);
   double* mz = reinterpret_cast<double*>(wsm + C::OFF_MZ);
-  const int64_t W = a.dhi - a.dlo;
+  const int W = (int)(a.dhi - a.dlo);
   const int total = (int)(a.n_dense_items + (int64_t)a.item_off[a.B * a.Hkv]);
-  const unsigned char* Kg = reinterpret_cast<const unsigned char*>(a.K);
-  const unsigned char* Vg = reinterpret_cast<const unsigned char*>(a.V);
   const unsigned char* Qg = reinterpret_cast<const unsigned char*>(a.q);
-  if constexpr (C::TMA) {
-    if (lane < C::S) mbar_init(&bar[lane], 1);
-    fence_mbar_init();
-    __syncwarp();
-  }
-  TL(unsigned long long* tl = g_tl + ((int64_t)blockIdx.x * C::NC + warp) * TL_SLOTS;
-     unsigned long long tl_merge = 0, tl_wait = 0, tl_sub = 0, tl_items = 0, tl_qk = 0, tl_pv = 0, tl_v = 0,
-                        tl_issue = 0;
-     if (lane == 0) tl[0] = gtimer(););
+  if (lane < C::S) mbar_init(&bar[lane], 1);
+  fence_mbar_init();
+  __syncwarp();
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // let the merge grid get resident
 
-  // ---------------------------------------------------------- load cursor
-  // Each warp streams whole work items (dynamic, global counter) through its
-  // own S-stage ring. The cursor runs ahead across item boundaries; the union
-  // entries (position, query-head mask) of a sub-chunk are loaded one issue
-  // ahead (pd2) and its rows are prefetched into L2 (bf16: V) when it becomes
-  // pd1, the next sub-chunk to issue.
-  int next_item = 0;  // lane 0: id of the item after the current one
-  if (lane == 0) next_item = atomicAdd(a.counter, 1);
-  int L_item = -1, L_bk = 0, L_hi = 0, L_row = 0, L_lo = 0, L_dense = 0, L_qbuf = C::NQB - 1;
-  int meta_slot = 0;  // slot holding the next sub-chunk to issue
-
-  // Form the descriptor of the next sub-chunk into metadata slot ms; its union
-  // entries arrive by cp.async (sparse) or are computed (dense).
-  auto advance = [&](int ms) {
-    unsigned char* slot = wsm + C::OFF_META + ms * C::MSLOT;
-    StageDesc d;
-    if (L_item < 0 || L_row >= L_hi) {
-      const int item = __shfl_sync(FULL, next_item, 0);
-      if (item >= total) {
-        d.item = -1;
-        if (lane == 0) *reinterpret_cast<StageDesc*>(slot) = d;
-        return;
-      }
-      L_item = item;
-      if (lane == 0) next_item = atomicAdd(a.counter, 1);
-      if (L_item < a.n_dense_items) {
-        L_dense = 1;
-        L_bk = (int)(L_item / a.Sd);
-        L_lo = (int)((L_item % a.Sd) * a.dense_rows);
-        L_hi = (int)min(W, (int64_t)L_lo + a.dense_rows);
-      } else {
-        L_dense = 0;
-        const int4 e = __ldg(a.item_tab + (L_item - (int)a.n_dense_items));  // (bk, lo, hi, -)
-        L_bk = e.x;
-        L_lo = e.y;
-        L_hi = e.z;
-      }
-      L_row = L_lo;
-    }
-    d.item = L_item;
-    d.bk = L_bk;
-    d.r0 = L_row;
-    d.n = min(C::SUB, L_hi - L_row);
-    d.first = L_row == L_lo;
-    d.last = L_row + C::SUB >= L_hi;
-    d.dense = L_dense;
-    d.qbuf = 0;
-    if (lane == 0) *reinterpret_cast<StageDesc*>(slot) = d;
-    int32_t* mpos = reinterpret_cast<int32_t*>(slot + 32);
-    uint8_t* mqm = slot + 32 + C::SUB * 4;
-    if (L_dense) {
-      mpos[lane] = lane < d.n ? (int32_t)(a.dlo + L_row + lane) : 0;
-      mqm[lane] = lane < d.n ? (uint8_t)((1u << G) - 1u) : (uint8_t)0;
-    } else {
-      // entries past the item end are masked at use (lane >= n); they are
-      // stale-but-valid positions of the [B*Hkv, T] union buffer
-      if (lane < 8) cp_async16(mpos + lane * 4, a.u_pos + (int64_t)L_bk * a.T + L_row + lane * 4);
-      else if (lane < 10) cp_async16(mqm + (lane - 8) * 16, a.u_qm + (int64_t)L_bk * a.T + L_row + (lane - 8) * 16);
-    }
-    L_row += C::SUB;
-  };
+  Cursor cur;
+  cur.nxt = 0;
+  if (lane == 0) cur.nxt = atomicAdd(a.counter, 1);
+  cur.item = -1;
+  cur.row = cur.hi = cur.lo = cur.bk = cur.dense = 0;
+  StageDesc pend = cursor_next(cur, a, total, W, lane);
+  int32_t pend_ent = sub_entry<G>(pend, a, lane);
 
   auto issue = [&](int s) {
-    unsigned char* st = wsm + s * C::STAGE;
-    // this sub-chunk's metadata was fetched one issue ago
-    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    __syncwarp();
-    const unsigned char* slot = wsm + C::OFF_META + meta_slot * C::MSLOT;
-    StageDesc d = *reinterpret_cast<const StageDesc*>(slot);
-    int32_t pos = 0;
-    uint32_t qm = 0;
-    if (d.item >= 0 && lane < d.n) {
-      pos = reinterpret_cast<const int32_t*>(slot + 32)[lane];
-      qm = slot[32 + C::SUB * 4 + lane];
-    }
-    if (d.item >= 0 && d.first) {
-      L_qbuf = (L_qbuf + 1) % C::NQB;
-      d.qbuf = L_qbuf;
-    }
+    const StageDesc d = pend;
+    const int32_t ent = pend_ent;
     if (lane == 0) desc[s] = d;
+    meta[s * SUB + lane] = ent;
     if (d.item >= 0) {
-      reinterpret_cast<int32_t*>(st + C::OFF_POS)[lane] = pos;
-      st[C::OFF_QM + lane] = (uint8_t)qm;
-      const int64_t b = d.bk / a.Hkv, kvh = d.bk % a.Hkv;
-      const unsigned char* qsrc = Qg + (b * a.Hq + kvh * G) * (int64_t)C::ROWB;
-      unsigned char* qdst = wsm + C::OFF_QRAW + d.qbuf * C::QRAW;
-      if constexpr (C::TMA) {
-        // 8 gather4 ops (4 rows each) + the item's queries on this stage's mbarrier
-        const int rowbase = d.bk * (int)a.T;
-        const int q0 = __shfl_sync(FULL, pos, (lane & 7) * 4 + 0);
-        const int q1 = __shfl_sync(FULL, pos, (lane & 7) * 4 + 1);
-        const int q2 = __shfl_sync(FULL, pos, (lane & 7) * 4 + 2);
-        const int q3 = __shfl_sync(FULL, pos, (lane & 7) * 4 + 3);
-        if (lane == 0) mbar_expect_tx(&bar[s], C::SUB * C::ROWB + (d.first ? C::QRAW : 0));
-        __syncwarp();
-        if (lane < 8)
-          tma_gather4(st + lane * 4 * C::ROWB, &a.kmap, 0, rowbase + q0, rowbase + q1, rowbase + q2,
-                      rowbase + q3, &bar[s]);
-        if (lane == 8 && d.first) bulk_g2s(qdst, qsrc, C::QRAW, &bar[s]);
-        if constexpr (!C::V_SMEM) {  // warm L2 with this sub-chunk's V rows
-          if (lane < d.n) {
-            const int64_t off = ((int64_t)d.bk * a.T + pos) * C::ROWB;
+      const int pos = ent & 0xffffff;
+      const int rg = lane & 7;
+      const int rowbase = d.bk * (int)a.T;
+      const int q0 = __shfl_sync(FULL, pos, rg * 4 + 0);
+      const int q1 = __shfl_sync(FULL, pos, rg * 4 + 1);
+      const int q2 = __shfl_sync(FULL, pos, rg * 4 + 2);
+      const int q3 = __shfl_sync(FULL, pos, rg * 4 + 3);
+      if (lane == 0) mbar_expect_tx(&bar[s], C::STAGE + (d.first ? C::QB : 0));
+      __syncwarp();
 #pragma unroll
-            for (int l = 0; l < C::ROWB; l += 128) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(Vg + off + l));
-          }
-        }
-      } else {
-        if (d.first)
-          for (int t = lane; t < C::QRAW / 16; t += 32) cp_async16(qdst + t * 16, qsrc + t * 16);
-        const unsigned char* kbase = Kg + (int64_t)d.bk * a.T * C::ROWB;
-        const unsigned char* vbase = Vg + (int64_t)d.bk * a.T * C::ROWB;
-#pragma unroll 4
-        for (int t = lane; t < C::SUB * C::PIECES; t += 32) {
-          const int r = t / C::PIECES, p = t % C::PIECES;
-          const int32_t pr = __shfl_sync(FULL, pos, r);
-          if (r < d.n) {
-            cp_async16(st + r * C::ROWB + swz(r, p) * 16, kbase + (int64_t)pr * C::ROWB + p * 16);
-            if (C::V_SMEM) cp_async16(st + C::OFF_V + r * C::ROWB + p * 16, vbase + (int64_t)pr * C::ROWB + p * 16);
-          }
-        }
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
+      for (int op = lane; op < C::NOPS; op += 32) {
+        const int tile = op >> 3;  // 128-byte column tile: K tiles then V tiles
+        const int col = tile < C::NKC ? tile * 32 : D + (tile - C::NKC) * 32;
+        tma_gather4(wsm_u + s * C::STAGE + tile * C::TILE + rg * 512, &a.kmap, col, rowbase + q0, rowbase + q1,
+                    rowbase + q2, rowbase + q3, &bar[s]);
       }
-      // fetch the following sub-chunk's metadata into the other slot
-      meta_slot ^= 1;
-      advance(meta_slot);
-      asm volatile("cp.async.commit_group;\n" ::: "memory");
+      if (lane == 8 && d.first) {
+        const int64_t b = d.bk / a.Hkv, kvh = d.bk % a.Hkv;
+        bulk_g2s(wsm + C::OFF_Q + s * C::QB, Qg + (b * a.Hq + kvh * G) * (int64_t)C::ROWB, C::QB, &bar[s]);
+      }
     }
+    pend = cursor_next(cur, a, total, W, lane);
+    pend_ent = sub_entry<G>(pend, a, lane);
   };
 
-  advance(0);
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
 #pragma unroll
   for (int s = 0; s < C::S; ++s) issue(s);
 
-  // ---------------------------------------------------------- compute
   for (int k = 0;; ++k) {
     const int s = k % C::S;
     __syncwarp();
-    TL(long long c0 = clock64();)
-    if constexpr (C::TMA) {
-      if (desc[s].item >= 0) mbar_wait(&bar[s], (k / C::S) & 1);
-    } else {
-      // outstanding groups, oldest first: data(k), meta(k+1)+..., data(k+1), meta(k+2)
-      asm volatile("cp.async.wait_group %0;\n" ::"n"(2 * (C::S - 1)) : "memory");
-    }
-    __syncwarp();
     const StageDesc d = desc[s];
     if (d.item < 0) break;
-    TL(long long c1 = clock64(); tl_wait += c1 - c0; ++tl_sub;)
-    const unsigned char* st = wsm + s * C::STAGE;
-    const int32_t mypos = reinterpret_cast<const int32_t*>(st + C::OFF_POS)[lane];
-    const uint32_t qm = st[C::OFF_QM + lane];
+    mbar_wait(&bar[s], (k / C::S) & 1);
+    const unsigned char* st = wsm + s * C::STAGE;  // tiles: K[NKC] then V[NKC], rows swizzled
+    const int32_t myent = meta[s * SUB + lane];
+    const uint32_t qm = (uint32_t)myent >> 24;
     const uint32_t wq = __reduce_or_sync(FULL, qm);
-    // ---- V rows of this sub-chunk into registers (bf16), unconditional
-    uint2 vreg[C::V_SMEM ? 1 : C::SUB];
-    if constexpr (!C::V_SMEM) {
-      const unsigned char* vbase = Vg + (int64_t)d.bk * a.T * C::ROWB + lane * C::DPL * C::ESZ;
-#pragma unroll
-      for (int r = 0; r < C::SUB; ++r) {
-        const int32_t pr = __shfl_sync(FULL, mypos, r);
-        if constexpr (C::DPL * C::ESZ == 8) {
-          vreg[r] = __ldg(reinterpret_cast<const uint2*>(vbase + (int64_t)pr * C::ROWB));
-        } else {
-          vreg[r].x = __ldg(reinterpret_cast<const uint32_t*>(vbase + (int64_t)pr * C::ROWB));
-        }
-      }
-    }
-    TL(long long c2 = clock64(); tl_v += c2 - c1;)
     if (d.first) {
-      const T* qr = reinterpret_cast<const T*>(wsm + C::OFF_QRAW + d.qbuf * C::QRAW);
-      if constexpr (C::PIECE32) {
-        // piece p's first 4 floats at [p*4], last 4 at [D/2 + p*4]: rotated
-        // per-lane piece reads then hit distinct banks
-        float* qk = reinterpret_cast<float*>(wsm + C::OFF_QK);
-        for (int t = lane; t < G * D; t += 32) {
-          const int g = t / D, e = t % D, p = e / 8, j = e % 8;
-          qk[g * D + (j < 4 ? p * 4 + j : D / 2 + p * 4 + (j - 4))] = to_f32(qr[t]);
-        }
-      } else {
-        double* qk = reinterpret_cast<double*>(wsm + C::OFF_QK);
-        for (int t = lane; t < G * D; t += 32) qk[t] = to_f64(qr[t]);
-      }
+      const float* qr = reinterpret_cast<const float*>(wsm + C::OFF_Q + s * C::QB);
+      for (int t = lane; t < G * D; t += 32) qk[t] = (double)qr[t];
       for (int t = lane; t < G * D; t += 32) accs[t] = 0.f;
       if (lane < G) {
         mz[2 * lane] = -INFINITY;
@@ -451,77 +702,25 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial
       }
       __syncwarp();
     }
-    // ---- scores: lane = row
+    // ---- scores: lane = row, exact fp64 products summed in the reference's
+    // sequential order over the head dimension (_core.pyx:59-65); the swizzle
+    // spreads one piece index over 8 banks groups, so lane = row is conflict-free
     double sacc[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) sacc[g] = 0.0;
     {
-      const unsigned char* krow = st + lane * C::ROWB;
-      if constexpr (C::PIECE32) {
-        const float* qk = reinterpret_cast<const float*>(wsm + C::OFF_QK);
-        if (__popc(wq) == 1) {  // single query head (most union chunks): no per-piece branching
-          const int g = __ffs(wq) - 1;
-          double s1 = 0.0;
 #pragma unroll 4
-          for (int i = 0; i < C::PIECES; ++i) {
-            const int p = (i + lane) & (C::PIECES - 1);  // rotation: conflict-free dense rows
-            float kf[8];
-            unpack8<T>(*reinterpret_cast<const uint4*>(krow + p * 16), kf);
-            const float4 qa = *reinterpret_cast<const float4*>(qk + g * D + p * 4);
-            const float4 qb = *reinterpret_cast<const float4*>(qk + g * D + D / 2 + p * 4);
-            float part = qa.x * kf[0];
-            part = fmaf(qa.y, kf[1], part);
-            part = fmaf(qa.z, kf[2], part);
-            part = fmaf(qa.w, kf[3], part);
-            part = fmaf(qb.x, kf[4], part);
-            part = fmaf(qb.y, kf[5], part);
-            part = fmaf(qb.z, kf[6], part);
-            part = fmaf(qb.w, kf[7], part);
-            s1 += (double)part;
-          }
+      for (int p = 0; p < C::PIECES; ++p) {
+        const float4 kv = *reinterpret_cast<const float4*>(st + (p >> 3) * C::TILE + swz128(lane, p & 7));
 #pragma unroll
-          for (int gg = 0; gg < G; ++gg) sacc[gg] = (gg == g) ? s1 : 0.0;
-        } else {
-#pragma unroll 2
-          for (int i = 0; i < C::PIECES; ++i) {
-            const int p = (i + lane) & (C::PIECES - 1);
-            float kf[8];
-            unpack8<T>(*reinterpret_cast<const uint4*>(krow + p * 16), kf);
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-              if ((wq >> g) & 1u) {
-                const float4 qa = *reinterpret_cast<const float4*>(qk + g * D + p * 4);
-                const float4 qb = *reinterpret_cast<const float4*>(qk + g * D + D / 2 + p * 4);
-                float part = qa.x * kf[0];
-                part = fmaf(qa.y, kf[1], part);
-                part = fmaf(qa.z, kf[2], part);
-                part = fmaf(qa.w, kf[3], part);
-                part = fmaf(qb.x, kf[4], part);
-                part = fmaf(qb.y, kf[5], part);
-                part = fmaf(qb.z, kf[6], part);
-                part = fmaf(qb.w, kf[7], part);
-                sacc[g] += (double)part;
-              }
-            }
-          }
-        }
-      } else {
-        const double* qk = reinterpret_cast<const double*>(wsm + C::OFF_QK);
-#pragma unroll 4
-        for (int p = 0; p < C::PIECES; ++p) {
-          const uint4 raw = *reinterpret_cast<const uint4*>(krow + swz(lane, p) * 16);
-          const double kd[4] = {(double)__uint_as_float(raw.x), (double)__uint_as_float(raw.y),
-                                (double)__uint_as_float(raw.z), (double)__uint_as_float(raw.w)};
-#pragma unroll
-          for (int g = 0; g < G; ++g) {
-            if ((wq >> g) & 1u) {
-              const double2 qa = *reinterpret_cast<const double2*>(qk + g * D + p * 4);
-              const double2 qb = *reinterpret_cast<const double2*>(qk + g * D + p * 4 + 2);
-              sacc[g] = fma(qa.x, kd[0], sacc[g]);  // exact products: reference order
-              sacc[g] = fma(qa.y, kd[1], sacc[g]);
-              sacc[g] = fma(qb.x, kd[2], sacc[g]);
-              sacc[g] = fma(qb.y, kd[3], sacc[g]);
-            }
+        for (int g = 0; g < G; ++g) {
+          if ((wq >> g) & 1u) {
+            const double2 qa = *reinterpret_cast<const double2*>(qk + g * D + p * 4);
+            const double2 qb = *reinterpret_cast<const double2*>(qk + g * D + p * 4 + 2);
+            sacc[g] = fma(qa.x, (double)kv.x, sacc[g]);  // exact products: one rounding per add
+            sacc[g] = fma(qa.y, (double)kv.y, sacc[g]);
+            sacc[g] = fma(qb.x, (double)kv.z, sacc[g]);
+            sacc[g] = fma(qb.y, (double)kv.w, sacc[g]);
           }
         }
       }
@@ -530,16 +729,16 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       if (!((wq >> g) & 1u)) continue;
-      const double sv = ((qm >> g) & 1u) ? sacc[g] * a.scale : -INFINITY;
-      sc[g * C::SUB + lane] = sv;
-      if (d.dense && lane < d.n) a.dsc[(b * a.Hq + kvh * G + g) * a.dsc_ld + (mypos - a.dlo)] = sv;
+      const double sv = (lane < d.n && ((qm >> g) & 1u)) ? sacc[g] * a.scale : -INFINITY;
+      sc[g * SUB + lane] = sv;
+      if (d.dense && lane < d.n)
+        reinterpret_cast<double*>(a.dsc)[(b * a.Hq + kvh * G + g) * a.dsc_ld + d.r0 + lane] = sv;
     }
     __syncwarp();
-    TL(long long c3 = clock64(); tl_qk += c3 - c2;)
-    // ---- per active head (rolled loop): online softmax (fp64) + P.V (fp32)
+    // ---- per active head: online softmax (fp64) + P.V (fp32, lanes over dims)
     for (uint32_t hm = wq; hm; hm &= hm - 1) {
       const int g = __ffs(hm) - 1;
-      const double sv = sc[g * C::SUB + lane];
+      const double sv = sc[g * SUB + lane];
       const double cm = warp_max_f64(sv);
       const double m_old = mz[2 * g];
       const double mnew = fmax(m_old, cm);
@@ -553,23 +752,21 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial
       float* ag = accs + g * D + lane * C::DPL;
 #pragma unroll
       for (int i = 0; i < C::DPL; ++i) acc[i] = ag[i] * sf;
-#pragma unroll
-      for (int r = 0; r < C::SUB; ++r) {
+#pragma unroll 8
+      for (int r = 0; r < SUB; ++r) {
         const float pr = __shfl_sync(FULL, pf, r);
-        if (C::V_SMEM && r >= d.n) break;  // staged V rows past the end are not loaded
-        float vv[C::DPL];
-        if constexpr (C::V_SMEM) {
-          load_v_f32<T, C::DPL>(st + C::OFF_V + r * C::ROWB + lane * C::DPL * C::ESZ, vv);
+        if (r >= d.n) break;
+        const int pc = lane * C::DPL / 4;  // 16-byte piece of the V row holding this lane's dims
+        const float* vr = reinterpret_cast<const float*>(st + (C::NKC + (pc >> 3)) * C::TILE + swz128(r, pc & 7)) +
+                          (lane * C::DPL) % 4;
+        if constexpr (C::DPL == 4) {
+          const float4 v = *reinterpret_cast<const float4*>(vr);
+          acc[0] = fmaf(pr, v.x, acc[0]); acc[1] = fmaf(pr, v.y, acc[1]);
+          acc[2] = fmaf(pr, v.z, acc[2]); acc[3] = fmaf(pr, v.w, acc[3]);
         } else {
-          vv[0] = __uint_as_float(vreg[r].x << 16);
-          vv[1] = __uint_as_float(vreg[r].x & 0xffff0000u);
-          if constexpr (C::DPL == 4) {
-            vv[C::DPL > 2 ? 2 : 0] = __uint_as_float(vreg[r].y << 16);
-            vv[C::DPL > 3 ? 3 : 0] = __uint_as_float(vreg[r].y & 0xffff0000u);
-          }
+          const float2 v = *reinterpret_cast<const float2*>(vr);
+          acc[0] = fmaf(pr, v.x, acc[0]); acc[1] = fmaf(pr, v.y, acc[1]);
         }
-#pragma unroll
-        for (int i = 0; i < C::DPL; ++i) acc[i] = fmaf(pr, vv[i], acc[i]);
       }
 #pragma unroll
       for (int i = 0; i < C::DPL; ++i) ag[i] = acc[i];
@@ -580,58 +777,35 @@ __global__ void __launch_bounds__(DecodeCfg<T, D, G>::NC * 32, 1) decode_partial
       }
       __syncwarp();
     }
-    TL(long long c4 = clock64(); tl_pv += c4 - c3;)
     if (d.last) {
-      TL(++tl_items;)
       for (int t = lane; t < G * D; t += 32) a.part_acc[(int64_t)d.item * G * D + t] = accs[t];
       if (lane < G) {
         a.part_m[(int64_t)d.item * G + lane] = mz[2 * lane];
         a.part_z[(int64_t)d.item * G + lane] = mz[2 * lane + 1];
       }
-      // the last finished item of this (b, kv-head) merges it
-      __threadfence();
-      __syncwarp();
-      int old = 0;
-      if (lane == 0) old = atomicAdd(a.bk_done + d.bk, 1);
-      old = __shfl_sync(FULL, old, 0);
-      const int n_items = (int)a.Sd + (__ldcg(a.item_off + d.bk + 1) - __ldcg(a.item_off + d.bk));
-      if (old == n_items - 1) {
-        __threadfence();
-        TL(long long m0 = clock64();)
-        warp_merge_bk<D, G>(a, d.bk, lane);
-        TL(tl_merge += clock64() - m0;)
+      if (d.dense) {
+        __syncwarp();
+        double mm[G], zz[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) { mm[g] = mz[2 * g]; zz[g] = mz[2 * g + 1]; }
+        dense_epilogue<double, G>(a, d.bk, mm, zz, lane);
       }
     }
     __syncwarp();
-    TL(long long c5 = clock64();)
     issue(s);
-    TL(tl_issue += clock64() - c5;)
   }
-  if constexpr (!C::TMA) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-  TL(if (lane == 0) {
-    tl[1] = gtimer();
-    tl[2] = tl_merge; tl[3] = tl_wait; tl[4] = tl_sub; tl[5] = tl_items; tl[6] = tl_qk; tl[7] = tl_pv;
-    tl[8] = tl_v; tl[9] = tl_issue; tl[10] = blockIdx.x; tl[11] = clock64();
-  })
 }
 
-// --------------------------------------------------------------------- merge
-// One CTA per (batch, query head). Folds dense and sparse partials in a fixed
-// order, applies merge_states(sparse, dense) (engine.py:166-169), and updates
-// the MAW of the attended window positions from the stored fp64 scores:
-//   w   = float32(exp(s - m) / z)                     (_core.pyx:81-82)
-//   maw = (1-alpha)*maw + alpha*w   (3 roundings)     (kv_cache.py:186)
-//   new entries: maw = w                              (engine.py:191)
 // -------------------------------------------------------------- union build
 // Per (batch, kv-head): union of the G query heads' selection masks over the
-// archive [0, n_arch), emitted grouped by query-head mask value (ascending
-// mask, then ascending position) so consecutive rows of a chunk share their
-// mask and the consumer warps skip inactive heads uniformly.
-__global__ void __launch_bounds__(1024) union_build_kernel(const uint32_t* __restrict__ sel,
-                                                           int64_t Hq, int64_t Hkv, int64_t G,
-                                                           int64_t words, int64_t n_arch, int64_t T,
-                                                           int32_t* u_pos, uint8_t* u_qm,
-                                                           int32_t* u_cnt) {
+// archive [0, n_arch) as packed entries pos | (query-head mask << 24).
+// grouped = 1 orders them by mask value, then position (the fp32 kernel then
+// sees mostly single-head sub-chunks); grouped = 0 keeps position order (the
+// bf16 kernel computes every head of a row anyway, and position order keeps
+// neighbouring rows close in HBM).
+__global__ void __launch_bounds__(1024) union_build_kernel(const uint32_t* __restrict__ sel, int64_t Hq, int64_t Hkv,
+                                                           int64_t G, int64_t words, int64_t n_arch, int64_t T,
+                                                           int32_t* u_ent, int32_t* u_cnt, int grouped) {
   __shared__ unsigned int hist[256];
   __shared__ int wsum[32];
   __shared__ int base_s;
@@ -652,35 +826,41 @@ __global__ void __launch_bounds__(1024) union_build_kernel(const uint32_t* __res
     }
     return any;
   };
-  for (int64_t w = tid; w < nw; w += blockDim.x) {
-    uint32_t mg[8];
-    uint32_t any = word_masks(w, mg);
-    while (any) {
-      const int bit = __ffs(any) - 1;
-      any &= any - 1;
-      uint32_t qm = 0;
-      for (int g = 0; g < G; ++g) qm |= ((mg[g] >> bit) & 1u) << g;
-      atomicAdd(&hist[qm], 1u);
+  if (grouped) {
+    for (int64_t w = tid; w < nw; w += blockDim.x) {
+      uint32_t mg[8];
+      uint32_t any = word_masks(w, mg);
+      while (any) {
+        const int bit = __ffs(any) - 1;
+        any &= any - 1;
+        uint32_t qm = 0;
+        for (int g = 0; g < G; ++g) qm |= ((mg[g] >> bit) & 1u) << g;
+        atomicAdd(&hist[qm], 1u);
+      }
     }
   }
   __syncthreads();
   if (tid == 0) base_s = 0;
   __syncthreads();
-  const int nbins = 1 << G;
+  const int nbins = grouped ? (1 << G) : 2;
   for (int v = 1; v < nbins; ++v) {
-    if (hist[v] == 0) continue;  // uniform: hist is stable after the barrier
+    if (grouped && hist[v] == 0) continue;  // uniform: hist is stable after the barrier
     for (int64_t w0 = 0; w0 < nw; w0 += blockDim.x) {
       const int64_t w = w0 + tid;
       uint32_t hit = 0;
+      uint32_t mg[8];
       if (w < nw) {
-        uint32_t mg[8];
         uint32_t any = word_masks(w, mg);
-        while (any) {
-          const int bit = __ffs(any) - 1;
-          any &= any - 1;
-          uint32_t qm = 0;
-          for (int g = 0; g < G; ++g) qm |= ((mg[g] >> bit) & 1u) << g;
-          if (qm == (uint32_t)v) hit |= 1u << bit;
+        if (!grouped) {
+          hit = any;
+        } else {
+          while (any) {
+            const int bit = __ffs(any) - 1;
+            any &= any - 1;
+            uint32_t qm = 0;
+            for (int g = 0; g < G; ++g) qm |= ((mg[g] >> bit) & 1u) << g;
+            if (qm == (uint32_t)v) hit |= 1u << bit;
+          }
         }
       }
       const int c = __popc(hit);
@@ -706,8 +886,9 @@ __global__ void __launch_bounds__(1024) union_build_kernel(const uint32_t* __res
       while (hit) {
         const int bit = __ffs(hit) - 1;
         hit &= hit - 1;
-        u_pos[bk * T + pos] = (int32_t)((w << 5) + bit);
-        u_qm[bk * T + pos] = (uint8_t)v;
+        uint32_t qm = 0;
+        for (int g = 0; g < G; ++g) qm |= ((mg[g] >> bit) & 1u) << g;
+        u_ent[bk * T + pos] = (int32_t)((uint32_t)((w << 5) + bit) | (qm << 24));
         ++pos;
       }
       __syncthreads();
@@ -716,6 +897,132 @@ __global__ void __launch_bounds__(1024) union_build_kernel(const uint32_t* __res
     }
   }
   if (tid == 0) u_cnt[bk] = base_s;
+}
+
+// Union for the bf16 kernel (mode 2): entries ordered so that every aligned
+// group of 8 consecutive entries has 8 distinct position classes p & 7 (the
+// bf16 K|V rows are stored rotated by p & 7, so the 8 rows one ldmatrix
+// reads then sit in 8 different bank groups). Class c's j-th entry (ascending
+// position) goes to 8*j + c while j < n_min = min_c count_c; the surplus
+// entries follow class by class.
+__global__ void __launch_bounds__(1024) union_classes_kernel(const uint32_t* __restrict__ sel, int64_t Hq,
+                                                             int64_t Hkv, int64_t G, int64_t words, int64_t n_arch,
+                                                             int64_t T, int32_t* u_ent, int32_t* u_cnt) {
+  __shared__ int cnt[8], base[8], tail[8];
+  __shared__ unsigned long long wsum[2][32];
+  const int64_t bk = blockIdx.x;
+  const int64_t b = bk / Hkv, kvh = bk % Hkv;
+  const uint32_t* m0 = sel + (b * Hq + kvh * G) * words;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarp = blockDim.x >> 5;
+  const int64_t nw = (n_arch + 31) >> 5;
+  if (tid < 8) cnt[tid] = 0, base[tid] = 0;
+  __syncthreads();
+  auto word_masks = [&](int64_t w, uint32_t* mg) -> uint32_t {
+    uint32_t any = 0;
+    const int64_t rem = n_arch - (w << 5);
+    const uint32_t keep = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
+    for (int g = 0; g < G; ++g) {
+      mg[g] = m0[g * words + w] & keep;
+      any |= mg[g];
+    }
+    return any;
+  };
+  // pass 1: entries per class
+  int loc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int64_t w = tid; w < nw; w += blockDim.x) {
+    uint32_t mg[8];
+    const uint32_t any = word_masks(w, mg);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) loc[c] += __popc(any & (0x01010101u << c));
+  }
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int v = warp_sum_i32(loc[c]);
+    if (lane == 0 && v) atomicAdd(&cnt[c], v);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int nmin = cnt[0];
+    for (int c = 1; c < 8; ++c) nmin = min(nmin, cnt[c]);
+    int t = 8 * nmin;
+    for (int c = 0; c < 8; ++c) {
+      tail[c] = t - nmin;  // index of class c's j-th entry (j >= nmin) = tail[c] + j
+      t += cnt[c] - nmin;
+    }
+    base[0] = nmin;  // stash n_min in base[] slot 0 until pass 2 starts
+  }
+  __syncthreads();
+  const int nmin = base[0];
+  __syncthreads();
+  if (tid == 0) base[0] = 0;
+  __syncthreads();
+  // pass 2: per class running index j, block-wide exclusive scans of the
+  // per-word class counts, packed 4 classes x 16 bits per 64-bit lane value
+  for (int64_t w0 = 0; w0 < nw; w0 += blockDim.x) {
+    const int64_t w = w0 + tid;
+    uint32_t mg[8];
+    const uint32_t any = w < nw ? word_masks(w, mg) : 0u;
+    unsigned long long pk[2] = {0ull, 0ull};
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      pk[c >> 2] |= (unsigned long long)__popc(any & (0x01010101u << c)) << (16 * (c & 3));
+    unsigned long long incl[2] = {pk[0], pk[1]};
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, incl[h], o);
+        if (lane >= o) incl[h] += y;
+      }
+    }
+    if (lane == 31) wsum[0][wid] = incl[0], wsum[1][wid] = incl[1];
+    __syncthreads();
+    if (wid == 0) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        unsigned long long x = lane < nwarp ? wsum[h][lane] : 0ull;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        if (lane < nwarp) wsum[h][lane] = x;
+      }
+    }
+    __syncthreads();
+    int j[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int h = c >> 2, sh = 16 * (c & 3);
+      const unsigned long long ex = (wid ? wsum[h][wid - 1] : 0ull) + (incl[h] - pk[h]);
+      j[c] = base[c] + (int)((ex >> sh) & 0xffffu);
+    }
+    uint32_t hit = any;
+    while (hit) {
+      const int bit = __ffs(hit) - 1;
+      hit &= hit - 1;
+      const int c = bit & 7;
+      uint32_t qm = 0;
+      for (int g = 0; g < G; ++g) qm |= ((mg[g] >> bit) & 1u) << g;
+      int jc = 0;
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc)
+        if (cc == c) jc = j[cc]++;
+      const int idx = jc < nmin ? 8 * jc + c : tail[c] + jc;
+      u_ent[bk * T + idx] = (int32_t)((uint32_t)((w << 5) + bit) | (qm << 24));
+    }
+    __syncthreads();
+    if (tid < 8) {
+      const int h = tid >> 2, sh = 16 * (tid & 3);
+      base[tid] += (int)((wsum[h][nwarp - 1] >> sh) & 0xffffu);
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    int t = 0;
+    for (int c = 0; c < 8; ++c) t += cnt[c];
+    u_cnt[bk] = t;
+  }
 }
 
 // item_off[bk] = sum_{x<bk} ceil(u_cnt[x] / rows)  (single CTA, sequential chunks)
@@ -753,8 +1060,7 @@ __global__ void item_offsets_kernel(const int32_t* u_cnt, int64_t BK, int64_t ro
 }
 
 // item_tab[item_off[bk] + i] = (bk, i*rows, min(u_cnt[bk], (i+1)*rows), 0)
-__global__ void item_table_kernel(const int32_t* u_cnt, const int32_t* off, int64_t BK, int64_t rows,
-                                  int4* tab) {
+__global__ void item_table_kernel(const int32_t* u_cnt, const int32_t* off, int64_t BK, int64_t rows, int4* tab) {
   const int64_t bk = blockIdx.x;
   if (bk >= BK) return;
   const int n = off[bk + 1] - off[bk];
@@ -764,20 +1070,24 @@ __global__ void item_table_kernel(const int32_t* u_cnt, const int32_t* off, int6
   }
 }
 
-// K/V[bh, pos + i, :] = new[bh, i, :]  (append_kv into the position buffer)
-__global__ void write_rows_kernel(unsigned char* K, unsigned char* V, int64_t BH, int64_t T,
-                                  int64_t rowb, int64_t pos, const unsigned char* kn,
-                                  const unsigned char* vn, int64_t n) {
+// KV[bh, pos + i, 0, :] = k_new[bh, i, :], KV[bh, pos + i, 1, :] = v_new[bh, i, :];
+// rot = 1 (bf16 storage) stores 16-byte chunk c of the row pair at
+// (c & ~7) | ((c ^ position) & 7) -- see rotoff().
+__global__ void write_rows_kernel(unsigned char* KV, int64_t BH, int64_t T, int64_t rowb, int64_t pos,
+                                  const unsigned char* kn, const unsigned char* vn, int64_t n, int rot) {
   const int64_t pieces = rowb / 16;
   const int64_t total = BH * n * pieces;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t p = t % pieces, row = t / pieces;
     const int64_t bh = row / n, i = row % n;
-    const int64_t dst = (bh * T + pos + i) * rowb + p * 16;
+    const int64_t position = pos + i;
+    const int64_t kc = p, vc = pieces + p;
+    const int64_t kp = rot ? ((kc & ~7) | ((kc ^ position) & 7)) : kc;
+    const int64_t vp = rot ? ((vc & ~7) | ((vc ^ position) & 7)) : vc;
+    const int64_t base = (bh * T + position) * 2 * rowb;
     const int64_t src = (bh * n + i) * rowb + p * 16;
-    *reinterpret_cast<uint4*>(K + dst) = *reinterpret_cast<const uint4*>(kn + src);
-    *reinterpret_cast<uint4*>(V + dst) = *reinterpret_cast<const uint4*>(vn + src);
+    *reinterpret_cast<uint4*>(KV + base + kp * 16) = *reinterpret_cast<const uint4*>(kn + src);
+    *reinterpret_cast<uint4*>(KV + base + vp * 16) = *reinterpret_cast<const uint4*>(vn + src);
   }
 }
 
@@ -786,8 +1096,11 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-// 2-D tensor map over the K buffer [B*Hkv*T rows, D] for tile::gather4 (box = one row).
-static int make_row_map(CUtensorMap* map, const void* base, int64_t rows, int64_t D, int esz) {
+// 2-D tensor map over KV viewed as [rows = B*Hkv*T, 2*D elements] for
+// tile::gather4. bf16: box = one whole (rotated) K|V row pair, no swizzle --
+// TMA gather cost is per gathered row, so whole rows keep it at 8 ops per
+// 32-row stage. fp32: box = one 128-byte column tile, 128B swizzle.
+static int make_row_map(CUtensorMap* map, const void* base, int64_t rows, int64_t D, bool bf16) {
   static EncodeTiledFn encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -795,56 +1108,86 @@ static int make_row_map(CUtensorMap* map, const void* base, int64_t rows, int64_
         !encode)
       return -3000;
   }
-  cuuint64_t gdim[2] = {(cuuint64_t)D, (cuuint64_t)rows};
-  cuuint64_t gstr[1] = {(cuuint64_t)(D * esz)};
-  cuuint32_t box[2] = {(cuuint32_t)D, 1};
+  const int esz = bf16 ? 2 : 4;
+  cuuint64_t gdim[2] = {(cuuint64_t)(2 * D), (cuuint64_t)rows};
+  cuuint64_t gstr[1] = {(cuuint64_t)(2 * D * esz)};
+  cuuint32_t box[2] = {bf16 ? (cuuint32_t)(2 * D) : 32u, 1};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = encode(map, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+  CUresult r = encode(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                       const_cast<void*>(base), gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                      bf16 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : -3001;
 }
 
-template <typename T, int D, int G>
+template <typename K>
+static int set_smem(K kernel, int bytes, bool& done) {
+  if (done) return 0;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return (int)e;
+  done = true;
+  return 0;
+}
+
+template <int D, int G>
+static int launch_merge_t(const DecodeMergeArgs& m, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(m.B * m.Hq));
+  cfg.blockDim = dim3(D);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return (int)cudaLaunchKernelEx(&cfg, decode_merge_kernel<D, G>, m);
+}
+
+template <bool BF16, int D, int G>
 static int launch_decode_t(const DecodeArgs& a_in, cudaStream_t s) {
-  using C = DecodeCfg<T, D, G>;
   DecodeArgs a = a_in;
-  if (C::TMA) {
-    // cached per K buffer: encoding is host work only
+  {
+    // cached per KV buffer: encoding is host work only
     static const void* cached_base = nullptr;
     static int64_t cached_rows = -1;
     static CUtensorMap cached;
     const int64_t rows = a.B * a.Hkv * a.T;
-    if (cached_base != a.K || cached_rows != rows) {
-      const int rc = make_row_map(&cached, a.K, rows, D, C::ESZ);
+    if (cached_base != a.KV || cached_rows != rows) {
+      const int rc = make_row_map(&cached, a.KV, rows, D, BF16);
       if (rc) return rc;
-      cached_base = a.K;
+      cached_base = a.KV;
       cached_rows = rows;
     }
     a.kmap = cached;
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(decode_partial_kernel<T, D, G>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    if (e != cudaSuccess) return -(int)e;
-    attr = true;
-  }
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  decode_partial_kernel<T, D, G><<<nsm, C::NC * 32, C::SMEM, s>>>(a);
-  return (int)cudaGetLastError();
+  static bool attr = false;
+  if constexpr (BF16) {
+    using C = Bf16Cfg<D, G, HGCA_BF16_STAGES>;
+    const int rc = set_smem(decode_bf16_kernel<D, G, HGCA_BF16_STAGES>, C::SMEM, attr);
+    if (rc) return rc;
+    decode_bf16_kernel<D, G, HGCA_BF16_STAGES><<<nsm, C::NC * 32, C::SMEM, s>>>(a);
+  } else {
+    using C = F32Cfg<D, G>;
+    const int rc = set_smem(decode_f32_kernel<D, G>, C::SMEM, attr);
+    if (rc) return rc;
+    decode_f32_kernel<D, G><<<nsm, C::NC * 32, C::SMEM, s>>>(a);
+  }
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return (int)e;
+  return launch_merge_t<D, G>(a.m, s);
 }
 
-template <typename T, int D>
+template <bool BF16, int D>
 static int launch_decode_g(const DecodeArgs& a, cudaStream_t s) {
   switch (a.G) {
-    case 1: return launch_decode_t<T, D, 1>(a, s);
-    case 2: return launch_decode_t<T, D, 2>(a, s);
-    case 4: return launch_decode_t<T, D, 4>(a, s);
-    case 8: return launch_decode_t<T, D, 8>(a, s);
+    case 1: return launch_decode_t<BF16, D, 1>(a, s);
+    case 2: return launch_decode_t<BF16, D, 2>(a, s);
+    case 4: return launch_decode_t<BF16, D, 4>(a, s);
+    case 8: return launch_decode_t<BF16, D, 8>(a, s);
   }
   return -1000;
 }
@@ -852,30 +1195,32 @@ static int launch_decode_g(const DecodeArgs& a, cudaStream_t s) {
 int decode_chunk_rows(int dtype, int64_t D) {
   (void)dtype;
   (void)D;
-  return 32;
+  return SUB;
 }
 
 int launch_decode_partial(int dtype, const DecodeArgs& a, cudaStream_t s) {
-  // work counter + per-(b, kv-head) finished-item counters
-  cudaError_t e = cudaMemsetAsync(a.counter, 0, sizeof(int32_t) * (1 + a.B * a.Hkv), s);
+  // work counter
+  cudaError_t e = cudaMemsetAsync(a.counter, 0, sizeof(int32_t), s);
   if (e != cudaSuccess) return (int)e;
   if (dtype == kBF16) {
-    if (a.D == 128) return launch_decode_g<__nv_bfloat16, 128>(a, s);
-    if (a.D == 64) return launch_decode_g<__nv_bfloat16, 64>(a, s);
+    if (a.D == 128) return launch_decode_g<true, 128>(a, s);
+    if (a.D == 64) return launch_decode_g<true, 64>(a, s);
   } else if (dtype == kF32) {
-    if (a.D == 128) return launch_decode_g<float, 128>(a, s);
-    if (a.D == 64) return launch_decode_g<float, 64>(a, s);
+    if (a.D == 128) return launch_decode_g<false, 128>(a, s);
+    if (a.D == 64) return launch_decode_g<false, 64>(a, s);
   }
   return -1001;
 }
 
-
-int launch_union_build(const uint32_t* sel, int64_t B, int64_t Hq, int64_t Hkv, int64_t words,
-                       int64_t n_arch, int64_t T, int32_t* u_pos, uint8_t* u_qm, int32_t* u_cnt,
-                       int32_t* item_off, int4* item_tab, int64_t sparse_rows, cudaStream_t s) {
+int launch_union_build(const uint32_t* sel, int64_t B, int64_t Hq, int64_t Hkv, int64_t words, int64_t n_arch,
+                       int64_t T, int32_t* u_ent, int32_t* u_cnt, int32_t* item_off, int4* item_tab,
+                       int64_t sparse_rows, int grouped, cudaStream_t s) {
   const int64_t G = Hq / Hkv;
-  union_build_kernel<<<(unsigned)(B * Hkv), 1024, 0, s>>>(sel, Hq, Hkv, G, words, n_arch, T, u_pos,
-                                                          u_qm, u_cnt);
+  if (grouped == 2)
+    union_classes_kernel<<<(unsigned)(B * Hkv), 1024, 0, s>>>(sel, Hq, Hkv, G, words, n_arch, T, u_ent, u_cnt);
+  else
+    union_build_kernel<<<(unsigned)(B * Hkv), 1024, 0, s>>>(sel, Hq, Hkv, G, words, n_arch, T, u_ent, u_cnt,
+                                                            grouped);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
   item_offsets_kernel<<<1, 1024, 0, s>>>(u_cnt, B * Hkv, sparse_rows, item_off);
@@ -885,8 +1230,8 @@ int launch_union_build(const uint32_t* sel, int64_t B, int64_t Hq, int64_t Hkv, 
   return (int)cudaGetLastError();
 }
 
-int launch_write_rows(int dtype, void* K, void* V, int64_t BH, int64_t T, int64_t D, int64_t pos,
-                      const void* k_new, const void* v_new, int64_t n, cudaStream_t s) {
+int launch_write_rows(int dtype, void* KV, int64_t BH, int64_t T, int64_t D, int64_t pos, const void* k_new,
+                      const void* v_new, int64_t n, cudaStream_t s) {
   const int64_t esz = dtype == kBF16 ? 2 : (dtype == kF64 ? 8 : 4);
   const int64_t rowb = D * esz;
   if (rowb % 16) return -1002;
@@ -894,9 +1239,37 @@ int launch_write_rows(int dtype, void* K, void* V, int64_t BH, int64_t T, int64_
   if (total == 0) return 0;
   const int64_t nb = (total + 255) / 256;
   const int blocks = (int)(nb < 148 * 8 ? nb : 148 * 8);
-  write_rows_kernel<<<blocks, 256, 0, s>>>((unsigned char*)K, (unsigned char*)V, BH, T, rowb, pos,
-                                           (const unsigned char*)k_new, (const unsigned char*)v_new, n);
+  write_rows_kernel<<<blocks, 256, 0, s>>>((unsigned char*)KV, BH, T, rowb, pos, (const unsigned char*)k_new,
+                                           (const unsigned char*)v_new, n, dtype == kBF16 ? 1 : 0);
   return (int)cudaGetLastError();
+}
+
+template <bool BF16, int D, int G>
+static void cfg_of(int64_t* o) {
+  if constexpr (BF16) {
+    using C = Bf16Cfg<D, G, HGCA_BF16_STAGES>;
+    o[0] = C::NC; o[1] = C::WARP_SMEM; o[2] = HGCA_BF16_STAGES; o[3] = SUB; o[4] = C::SMEM;
+  } else {
+    using C = F32Cfg<D, G>;
+    o[0] = C::NC; o[1] = C::WARP_SMEM; o[2] = C::S; o[3] = SUB; o[4] = C::SMEM;
+  }
+}
+
+int decode_config(int dtype, int64_t D, int64_t G, int64_t* o) {
+#define HG_CFG(BB, DD)                        \
+  switch (G) {                                \
+    case 1: cfg_of<BB, DD, 1>(o); return 0;   \
+    case 2: cfg_of<BB, DD, 2>(o); return 0;   \
+    case 4: cfg_of<BB, DD, 4>(o); return 0;   \
+    case 8: cfg_of<BB, DD, 8>(o); return 0;   \
+  }                                           \
+  return -1;
+  if (dtype == kBF16 && D == 128) { HG_CFG(true, 128) }
+  if (dtype == kBF16 && D == 64) { HG_CFG(true, 64) }
+  if (dtype == kF32 && D == 128) { HG_CFG(false, 128) }
+  if (dtype == kF32 && D == 64) { HG_CFG(false, 64) }
+#undef HG_CFG
+  return -1;
 }
 
 }  // namespace hgca
@@ -912,27 +1285,3 @@ extern "C" int hgca_debug_timeline(void* host, int64_t n) {
   return (int)cudaMemcpyFromSymbol(host, hgca::g_tl, n * 8);
 }
 #endif
-
-namespace hgca {
-template <typename T, int D, int G>
-static void cfg_of(int64_t* o) {
-  using C = DecodeCfg<T, D, G>;
-  o[0] = C::NC; o[1] = C::WARP_SMEM; o[2] = C::S; o[3] = C::SUB; o[4] = C::SMEM;
-}
-int decode_config(int dtype, int64_t D, int64_t G, int64_t* o) {
-#define HG_CFG(TT, DD)                                       \
-  switch (G) {                                               \
-    case 1: cfg_of<TT, DD, 1>(o); return 0;                  \
-    case 2: cfg_of<TT, DD, 2>(o); return 0;                  \
-    case 4: cfg_of<TT, DD, 4>(o); return 0;                  \
-    case 8: cfg_of<TT, DD, 8>(o); return 0;                  \
-  }                                                          \
-  return -1;
-  if (dtype == kBF16 && D == 128) { HG_CFG(__nv_bfloat16, 128) }
-  if (dtype == kBF16 && D == 64) { HG_CFG(__nv_bfloat16, 64) }
-  if (dtype == kF32 && D == 128) { HG_CFG(float, 128) }
-  if (dtype == kF32 && D == 64) { HG_CFG(float, 64) }
-#undef HG_CFG
-  return -1;
-}
-}  // namespace hgca

@@ -14,6 +14,8 @@ struct AttendArgs {
   int64_t Hq, Hkv, G;   // bh = b*Hq + h; kvh = b*Hkv + h/G
   int64_t nq, d;
   int64_t ld_head;      // elements between consecutive kv heads
+  int64_t ld_row;       // elements between consecutive kv rows (d, or 2d for interleaved K|V rows)
+  int rot;              // 1: rows are the engine's position-rotated bf16 K|V pairs (see write_rows_kernel)
   int64_t row0;         // first row (dense) / base for idx
   int64_t n;            // dense key count (when idx == nullptr and idx_cnt == nullptr)
   const int64_t* idx;      // optional gathered rows (concatenated per head)
@@ -44,52 +46,43 @@ struct MergeArgs {
 
 struct DecodeMergeArgs {
   int64_t B, Hq, Hkv, G, D;
-  int64_t Sd, n_dense_items;
+  int64_t n_dense_items;  // = B*Hkv: one dense item per (batch, kv-head), item id = bk
   const int32_t* item_off;
   const double* part_m;
   const double* part_z;
   const float* part_acc;
-  const double* dsc;
-  int64_t dsc_ld;
-  int64_t W;              // dense positions attended = dhi - dlo
-  int64_t w_old;          // window entries before this step (EMA'd); the rest are new
-  double* maw;            // [B*Hq, T] or nullptr (no MAW maintenance)
-  int64_t T;
-  int64_t dlo;
-  double one_minus_alpha, alpha;
-  float* wts_out;         // optional dense weights [B*Hq, W]
   float* out;             // [B*Hq, D]
   double* lse;            // [B*Hq]
   float* out_sparse;      // optional sparse partial out [B*Hq, D] (for sharded merges)
   double* lse_sparse;
 };
 
-// Fused decode step: dense window tiles + sparse union chunks, merged in-kernel.
+// Fused decode step: dense window items + sparse union chunks, merged in-kernel.
 struct DecodeArgs {
-  DecodeMergeArgs m;      // fold / merge_states / MAW parameters (run by the last warp per (b, kv-head))
-  int32_t* bk_done;       // [B*Hkv] finished-item counters (zeroed before launch)
-  CUtensorMap kmap;       // row map over K [B*Hkv*T, D] for TMA gather4 (bf16), set by the launcher
-  const void* K;          // [B*Hkv, T, D] storage dtype
-  const void* V;
+  DecodeMergeArgs m;      // fold / merge_states parameters (decode_merge_kernel)
+  CUtensorMap kmap;       // row map over KV [B*Hkv*T rows, 2D] for TMA gather4, set by the launcher
+  const void* KV;         // [B*Hkv, T, 2, D] storage dtype: K row then V row per position
   const void* q;          // [B*Hq, D] storage dtype (decode: one query row)
   int64_t B, Hq, Hkv, G, D, T;
   double scale;
   int64_t dlo, dhi;       // dense positions [dlo, dhi)
-  int64_t Sd;             // dense items per (b, kvh)
-  int64_t dense_rows;     // rows per dense item (multiple of the chunk)
-  const int32_t* u_pos;   // [B*Hkv, T] union positions (grouped by query-head mask)
-  const uint8_t* u_qm;    // [B*Hkv, T] query-head masks
+  const int32_t* u_ent;   // [B*Hkv, T] union entries pos | (query-head mask << 24)
   const int32_t* u_cnt;   // [B*Hkv]
   const int32_t* item_off;// [B*Hkv + 1] sparse item prefix
   const int4* item_tab;   // [sparse items] (bk, lo, hi, 0)
   int64_t sparse_rows;    // rows per sparse item
-  double* dsc;            // [B*Hq, dsc_ld] dense scores (fp64) for the MAW update
+  void* dsc;              // [B*Hq, dsc_ld] dense scores (fp64 for fp32 storage, fp32 for bf16)
   int64_t dsc_ld;
   double* part_m;         // [items, G]
   double* part_z;         // [items, G]
   float* part_acc;        // [items, G, D]
   int32_t* counter;       // work counter (zeroed before launch)
-  int64_t n_dense_items;  // B*Hkv*Sd
+  int64_t n_dense_items;  // B*Hkv
+  // dense-item epilogue: weights + MAW maintenance of the attended window
+  int64_t w_old;          // window entries before this step (EMA'd); the rest are new
+  double* maw;            // [B*Hq, T] or nullptr (no MAW maintenance)
+  double one_minus_alpha, alpha;
+  float* wts_out;         // optional dense weights [B*Hq, dhi - dlo]
 };
 
 
@@ -111,9 +104,9 @@ int launch_topk_mask(const double* maw, int64_t rows, int64_t ld, int64_t n, con
 
 int launch_decode_partial(int dtype, const DecodeArgs& a, cudaStream_t s);
 int launch_union_build(const uint32_t* sel, int64_t B, int64_t Hq, int64_t Hkv, int64_t words,
-                       int64_t n_arch, int64_t T, int32_t* u_pos, uint8_t* u_qm, int32_t* u_cnt,
-                       int32_t* item_off, int4* item_tab, int64_t sparse_rows, cudaStream_t s);
-int launch_write_rows(int dtype, void* K, void* V, int64_t BH, int64_t T, int64_t D, int64_t pos,
+                       int64_t n_arch, int64_t T, int32_t* u_ent, int32_t* u_cnt, int32_t* item_off,
+                       int4* item_tab, int64_t sparse_rows, int grouped, cudaStream_t s);
+int launch_write_rows(int dtype, void* KV, int64_t BH, int64_t T, int64_t D, int64_t pos,
                       const void* k_new, const void* v_new, int64_t n, cudaStream_t s);
 int decode_chunk_rows(int dtype, int64_t D);
 int decode_config(int dtype, int64_t D, int64_t G, int64_t* out);

@@ -30,9 +30,18 @@ __device__ __forceinline__ double dot_step<double>(double s, double q, double k)
 template <typename T> struct OutT { using type = T; };
 template <> struct OutT<__nv_bfloat16> { using type = float; };
 
+// Element c of a rotated row (position p): 16-byte chunk (c / epc) sits at
+// (chunk & ~7) | ((chunk ^ p) & 7) -- the engine's bf16 K|V layout.
+__device__ __forceinline__ int64_t rot_elem(int64_t c, int64_t p, int64_t epc) {
+  const int64_t ch = c / epc;
+  return (((ch & ~7) | ((ch ^ p) & 7)) * epc) + c % epc;
+}
+
 // One CTA per (query row i, head bh). K/V rows for head bh start at
-//   kv + kv_head_index(bh) * ld_head + row0 * d
-// and are either the first n rows (dense) or the rows listed in idx.
+//   kv + kv_head_index(bh) * ld_head + row0 * ld_row
+// (row stride ld_row: d for plain [.., n, d] buffers, 2d for the engine's
+// interleaved K|V rows) and are either the first n rows (dense) or the rows
+// listed in idx.
 template <typename T>
 __global__ void __launch_bounds__(256) attend_rows_kernel(AttendArgs a) {
   using O = typename OutT<T>::type;
@@ -46,8 +55,9 @@ __global__ void __launch_bounds__(256) attend_rows_kernel(AttendArgs a) {
   const int64_t b = bh / a.Hq, h = bh % a.Hq;
   const int64_t kvh = b * a.Hkv + h / a.G;
   const T* q = reinterpret_cast<const T*>(a.q) + (bh * a.nq + i) * d;
-  const T* k = reinterpret_cast<const T*>(a.k) + kvh * a.ld_head + a.row0 * d;
-  const T* v = reinterpret_cast<const T*>(a.v) + kvh * a.ld_head + a.row0 * d;
+  const int64_t ldr = a.ld_row;
+  const T* k = reinterpret_cast<const T*>(a.k) + kvh * a.ld_head + a.row0 * ldr;
+  const T* v = reinterpret_cast<const T*>(a.v) + kvh * a.ld_head + a.row0 * ldr;
   const int64_t* idx = a.idx ? a.idx + (a.idx_off ? a.idx_off[bh] : 0) : nullptr;
   const int64_t n = a.idx_cnt ? a.idx_cnt[bh] : a.n;
   O* out = reinterpret_cast<O*>(a.out) + (bh * a.nq + i) * d;
@@ -66,9 +76,14 @@ __global__ void __launch_bounds__(256) attend_rows_kernel(AttendArgs a) {
   double m = -INFINITY;
   for (int64_t j = tid; j < n; j += nt) {
     const int64_t r = idx ? idx[j] : j;
-    const T* kr = k + r * d;
+    const T* kr = k + r * ldr;
     double s = 0.0;
-    for (int64_t c = 0; c < d; ++c) s = dot_step<T>(s, qs[c], kr[c]);
+    if (a.rot) {
+      const int64_t p = a.row0 + r, epc = 16 / (int64_t)sizeof(T);
+      for (int64_t c = 0; c < d; ++c) s = dot_step<T>(s, qs[c], kr[rot_elem(c, p, epc)]);
+    } else {
+      for (int64_t c = 0; c < d; ++c) s = dot_step<T>(s, qs[c], kr[c]);
+    }
     s = s * a.scale;
     sc[j] = s;
     m = fmax(m, s);
@@ -109,7 +124,8 @@ __global__ void __launch_bounds__(256) attend_rows_kernel(AttendArgs a) {
     double acc = 0.0;
     for (int64_t j = j0; j < j1; ++j) {
       const int64_t r = idx ? idx[j] : j;
-      acc = __dadd_rn(acc, __dmul_rn(sc[j], to_f64(v[r * d + c])));
+      const int64_t cc = a.rot ? rot_elem(c, a.row0 + r, 16 / (int64_t)sizeof(T)) : c;
+      acc = __dadd_rn(acc, __dmul_rn(sc[j], to_f64(v[r * ldr + cc])));
     }
     if (nseg == 1) {
       out[c] = from_f64<O>(acc / z);

@@ -11,11 +11,13 @@ maintenance order, extended the way SURVEY.md F8 describes:
 
 HBM layout per layer (positions are absolute, so the window tier and the
 store tier share one buffer and eviction is a pointer move, not a copy):
-  K, V       [B*Hkv, T, D]    storage dtype; archive = [0, lo), window = [lo, nxt)
+  KV         [B*Hkv, T, 2, D] storage dtype, K row then V row of each position
+                              (one contiguous gather per selected entry);
+                              archive = [0, lo), window = [lo, nxt)
   maw        [B*Hq, T]        float64 per (query head, position)     kv_cache.py:73-75
   ctx        [B*Hq, T/32]     context-cache membership bits          sparsifier.py:58-87
   sel        [B*Hq, T/32]     attended set = ctx | padding           sparsifier.py:198-235
-  u_pos/u_qm [B*Hkv, T]       per-KV-head union of `sel` with query-head masks
+  u_ent      [B*Hkv, T]       per-KV-head union of `sel`: position | query-head mask << 24
 The decode step is one call of hgca_decode_step (dense window + sparse union
 + merge + MAW EMA); selection changes (ingest / re-evaluation) rebuild the
 masks and the union with the selection kernels.
@@ -38,8 +40,7 @@ from .sparsifier import group_size, mask_to_lists, ownership_words, topk_mask, w
 __all__ = ["CacheConfig", "EngineConfig", "StepInput", "StepOutput", "LayerState", "HybridEngine"]
 
 MODES = ("decode", "append")
-DENSE_ROWS = 256
-SPARSE_ROWS = 256
+SPARSE_ROWS = 256   # union rows per sparse work item of the decode kernel
 
 
 @dataclass(frozen=True)
@@ -170,14 +171,12 @@ class LayerState:
     def __init__(self, cfg: EngineConfig, T: int, dev):
         B, Hq, Hkv, D = cfg.batch, cfg.heads, cfg.n_kv_heads, cfg.head_dim
         tdt = torch.bfloat16 if cfg.dtype == "bfloat16" else torch.float32
-        self.K = torch.zeros((B * Hkv, T, D), dtype=tdt, device=dev)
-        self.V = torch.zeros((B * Hkv, T, D), dtype=tdt, device=dev)
+        self.KV = torch.zeros((B * Hkv, T, 2, D), dtype=tdt, device=dev)
         self.maw = torch.zeros((B * Hq, T), dtype=torch.float64, device=dev)
         words = T // 32
         self.ctx = torch.zeros((B * Hq, words), dtype=torch.int32, device=dev)
         self.sel = torch.zeros((B * Hq, words), dtype=torch.int32, device=dev)
-        self.u_pos = torch.zeros((B * Hkv, T), dtype=torch.int32, device=dev)
-        self.u_qm = torch.zeros((B * Hkv, T), dtype=torch.uint8, device=dev)
+        self.u_ent = torch.zeros((B * Hkv, T), dtype=torch.int32, device=dev)
         self.u_cnt = torch.zeros(B * Hkv, dtype=torch.int32, device=dev)
         self.item_off = torch.zeros(B * Hkv + 1, dtype=torch.int32, device=dev)
         self.item_tab = torch.zeros((B * Hkv * (T // 32 + 1), 4), dtype=torch.int32, device=dev)
@@ -188,6 +187,29 @@ class LayerState:
             # ownership bits: archive block j (positions [j*blk, (j+1)*blk)) lives on rank j % world
             bits = ownership_words(words, cfg.cache.blk_size, cfg.shard_rank, cfg.shard_world)
             self.keep = torch.from_numpy(bits.view(np.int32)).to(dev)
+
+    def rows(self):
+        """Logical [B*Hkv, T, 2, D] view of KV (a copy for bfloat16 storage,
+        whose rows are stored position-rotated: 16-byte chunk c of the row pair
+        of position p at chunk (c & ~7) | ((c ^ p) & 7), hgca_write_rows)."""
+        if self.KV.dtype != torch.bfloat16:
+            return self.KV
+        BH, T, _, D = self.KV.shape
+        ch = 2 * D // 8
+        c = torch.arange(ch, device=self.KV.device)
+        p = torch.arange(T, device=self.KV.device)
+        phys = (c[None, :] & ~7) | ((c[None, :] ^ p[:, None]) & 7)          # [T, ch]
+        flat = self.KV.view(BH, T, ch, 8)
+        idx = phys[None, :, :, None].expand(BH, T, ch, 8)
+        return torch.gather(flat, 2, idx).view(BH, T, 2, D)
+
+    @property
+    def K(self):
+        return self.rows()[:, :, 0]
+
+    @property
+    def V(self):
+        return self.rows()[:, :, 1]
 
     @property
     def window_size(self):
@@ -211,6 +233,8 @@ class HybridEngine:
         if self.D not in (64, 128):
             raise ContractError("the device engine supports head_dim 64 or 128")
         self.T = int(math.ceil(c.max_positions / 32) * 32)
+        if self.T >= 1 << 24:
+            raise ContractError("max_positions must be below 2^24 (union entries pack 24-bit positions)")
         self.cap = c.cache.capacity
         self.tdtype = torch.bfloat16 if c.dtype == "bfloat16" else torch.float32
         self.dcode = DTYPE_CODE[self.tdtype]
@@ -220,7 +244,7 @@ class HybridEngine:
         BHq = self.B * self.Hq
         self.dsc_ld = self.cap + 1
         self.dsc = torch.zeros((BHq, self.dsc_ld), dtype=torch.float64, device=self.dev)
-        n_dense = self.B * self.Hkv * math.ceil(self.dsc_ld / DENSE_ROWS)
+        n_dense = self.B * self.Hkv
         n_sparse = self.B * self.Hkv * math.ceil(self.T / SPARSE_ROWS)
         self.max_items = n_dense + n_sparse
         self.part_m = torch.empty(self.max_items * self.G, dtype=torch.float64, device=self.dev)
@@ -272,9 +296,13 @@ class HybridEngine:
         else:
             ls.sel.copy_(ls.ctx)
         self.launches += 2 + (3 if (self.g_pad > 1 and n) else 0) + (1 if self.config.selection == "topk" and n else 0)
+        # fp32 kernel: group union rows by query-head mask (single-head
+        # sub-chunks); bf16 kernel: position-class interleaved (conflict-free
+        # ldmatrix over the position-rotated rows; it scores every head)
+        grouped = 1 if self.tdtype == torch.float32 else 2
         _lib.call("hgca_union_build", ls.sel.data_ptr(), self.B, self.Hq, self.Hkv, words, n, self.T,
-                  ls.u_pos.data_ptr(), ls.u_qm.data_ptr(), ls.u_cnt.data_ptr(), ls.item_off.data_ptr(),
-                  ls.item_tab.data_ptr(), SPARSE_ROWS, s)
+                  ls.u_ent.data_ptr(), ls.u_cnt.data_ptr(), ls.item_off.data_ptr(), ls.item_tab.data_ptr(),
+                  SPARSE_ROWS, grouped, s)
 
     def _ingest(self, ls: LayerState, lo, hi, divisor):
         """StoreTier.ingest_evicted of positions [lo, hi) (sparsifier.py:127-156)."""
@@ -322,7 +350,7 @@ class HybridEngine:
         m = maw if isinstance(maw, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(maw))
         m = m.to(device=self.dev, dtype=torch.float64).reshape(self.B * self.Hq, n)
         p0 = ls.nxt
-        _lib.call("hgca_write_rows", self.dcode, ls.K.data_ptr(), ls.V.data_ptr(), self.B * self.Hkv,
+        _lib.call("hgca_write_rows", self.dcode, ls.KV.data_ptr(), self.B * self.Hkv,
                   self.T, self.D, p0, k.data_ptr(), v.data_ptr(), n, self._stream())
         ls.maw[:, p0:p0 + n].copy_(m)
         ls.nxt = p0 + n
@@ -371,7 +399,7 @@ class HybridEngine:
         if ls.nxt + 1 > self.T:
             raise ContractError("max_positions exceeded")
         # kv_in lands at position nxt before the dense pass (append_kv's slot)
-        _lib.call("hgca_write_rows", self.dcode, ls.K.data_ptr(), ls.V.data_ptr(), self.B * self.Hkv,
+        _lib.call("hgca_write_rows", self.dcode, ls.KV.data_ptr(), self.B * self.Hkv,
                   self.T, self.D, ls.nxt, k.data_ptr(), v.data_ptr(), 1, s)
         w_size = ls.window_size
         W = w_size + 1
@@ -385,12 +413,11 @@ class HybridEngine:
         d = self._desc
         d.dtype = self.dcode
         d.B, d.Hq, d.Hkv, d.D, d.T = self.B, self.Hq, self.Hkv, self.D, self.T
-        d.K, d.V, d.q = ls.K.data_ptr(), ls.V.data_ptr(), q.data_ptr()
+        d.KV, d.q = ls.KV.data_ptr(), q.data_ptr()
         d.scale = float(self.shape.scale)
         d.dlo, d.dhi, d.w_old = ls.lo, ls.nxt + 1, w_size
-        d.dense_rows, d.sparse_rows = DENSE_ROWS, SPARSE_ROWS
-        d.u_pos, d.u_qm, d.u_cnt, d.item_off = (ls.u_pos.data_ptr(), ls.u_qm.data_ptr(),
-                                                ls.u_cnt.data_ptr(), ls.item_off.data_ptr())
+        d.sparse_rows = SPARSE_ROWS
+        d.u_ent, d.u_cnt, d.item_off = ls.u_ent.data_ptr(), ls.u_cnt.data_ptr(), ls.item_off.data_ptr()
         d.item_tab = ls.item_tab.data_ptr()
         d.dsc, d.dsc_ld = self.dsc.data_ptr(), self.dsc_ld
         d.part_m, d.part_z, d.part_acc = self.part_m.data_ptr(), self.part_z.data_ptr(), self.part_acc.data_ptr()
@@ -410,7 +437,7 @@ class HybridEngine:
             _lib.call("hgca_decode_step", d, s)
             e1.record()
             self.step_events.append((e0, e1))
-        self.launches += 2  # write_rows, decode kernel (merge fused)
+        self.launches += 3  # write_rows, decode kernel, merge kernel
         self._last_dense_positions = np.arange(ls.lo, ls.nxt + 1, dtype=np.int64)
         # maintenance after the merge (engine.py:175-191): EMA + init done in
         # the merge kernel; eviction/offload here; append_kv = the position move.
@@ -450,7 +477,7 @@ class HybridEngine:
         s = self._stream()
         if ls.nxt + nq > self.T:
             raise ContractError("max_positions exceeded")
-        _lib.call("hgca_write_rows", self.dcode, ls.K.data_ptr(), ls.V.data_ptr(), self.B * self.Hkv,
+        _lib.call("hgca_write_rows", self.dcode, ls.KV.data_ptr(), self.B * self.Hkv,
                   self.T, self.D, ls.nxt, k.data_ptr(), v.data_ptr(), nq, s)
         BHq = self.B * self.Hq
         lo, nxt = ls.lo, ls.nxt
@@ -464,7 +491,7 @@ class HybridEngine:
         if lo:
             a_cpu = torch.empty((BHq, nq, lo), dtype=odt, device=self.dev)
             ws = torch.empty(BHq * nq * lo, dtype=torch.float64, device=self.dev)
-            _lib.call("hgca_attend_gqa", self.dcode, q.data_ptr(), ls.K.data_ptr(), ls.V.data_ptr(),
+            _lib.call("hgca_attend_gqa", self.dcode, q.data_ptr(), ls.KV.data_ptr(),
                       self.B, self.Hq, self.Hkv, self.T, 0, lo, nq, self.D, float(self.shape.scale),
                       s_out.data_ptr(), s_lse.data_ptr(), a_cpu.data_ptr(), lo, ws.data_ptr(), s)
         # dense over window + kv_in (engine.py:161-164)
@@ -472,7 +499,7 @@ class HybridEngine:
         d_lse = torch.empty((BHq, nq), dtype=torch.float64, device=self.dev)
         a_gpu = torch.empty((BHq, nq, W), dtype=odt, device=self.dev)
         ws = torch.empty(BHq * nq * W, dtype=torch.float64, device=self.dev)
-        _lib.call("hgca_attend_gqa", self.dcode, q.data_ptr(), ls.K.data_ptr(), ls.V.data_ptr(),
+        _lib.call("hgca_attend_gqa", self.dcode, q.data_ptr(), ls.KV.data_ptr(),
                   self.B, self.Hq, self.Hkv, self.T, lo, W, nq, self.D, float(self.shape.scale),
                   d_out.data_ptr(), d_lse.data_ptr(), a_gpu.data_ptr(), W, ws.data_ptr(), s)
         # merge (engine.py:166-169)

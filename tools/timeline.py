@@ -17,7 +17,7 @@ os.environ.setdefault("HGCA_LIB", os.path.join(ROOT, "paper_2507_03153_b200", "_
 import bench  # noqa: E402
 import paper_2507_03153_b200 as hg  # noqa: E402
 
-SLOTS = 12
+SLOTS = 16
 
 
 def main():
@@ -32,7 +32,7 @@ def main():
     hg._lib.call("hgca_decode_config", eng.dcode, D, Hq // Hkv, cfg)
     nc = cfg[0]
     tdt = eng.tdtype
-    for it in range(4):
+    for it in range(2):
         q = torch.randn((B, Hq, 1, D), generator=g, device="cuda").to(tdt)
         k = torch.randn((B, Hkv, 1, D), generator=g, device="cuda").to(tdt)
         torch.cuda.synchronize()
@@ -50,8 +50,8 @@ def main():
         t = buf.reshape(n, SLOTS).astype(np.float64)
         t0 = t[:, 0].min()
         start, end = (t[:, 0] - t0) / 1e3, (t[:, 1] - t0) / 1e3
-        cyc = {k: t[:, i] for i, k in enumerate(["", "", "merge", "wait", "sub", "items", "qk", "pv", "v", "issue"])
-               if k}
+        names = ["", "", "merge", "wait", "sub", "items", "qk", "pv", "v", "issue", "tma", "nmerge", "smma", "epi"]
+        cyc = {k: t[:, i] for i, k in enumerate(names) if k}
         span = end.max()
         print(f"--- step {it}: kernel {ms*1e3:.1f} us (events), warps {n} ({nc}/SM), span {span:.1f} us")
         print("warp end us: p0 %.1f p10 %.1f p50 %.1f p90 %.1f p99 %.1f max %.1f" %
@@ -61,6 +61,11 @@ def main():
         clk_mhz = 1965.0
         for k in ("wait", "v", "qk", "pv", "issue", "merge"):
             print(f"  {k:6s} {cyc[k].sum()/tot:6.1%}  per sub-chunk {cyc[k].sum()/max(cyc['sub'].sum(),1):8.0f} cyc")
+        sub = max(cyc['sub'].sum(), 1)
+        print(f"  of which: qk-mma {cyc['smma'].sum()/sub:.0f} cyc/sub, tma-issue {cyc['tma'].sum()/sub:.0f} cyc/sub; "
+              f"merges {cyc['nmerge'].sum():.0f} (max/warp {cyc['nmerge'].max():.0f}), "
+              f"cyc/merge {cyc['merge'].sum()/max(cyc['nmerge'].sum(),1):.0f}, dense epilogue cyc/item "
+              f"{cyc['epi'].sum()/max(len(np.nonzero(cyc['epi'])[0]),1):.0f}")
         print(f"  sub-chunks {cyc['sub'].sum():.0f} items {cyc['items'].sum():.0f} "
               f"merge cyc max/warp {cyc['merge'].max():.0f} ({cyc['merge'].max()/clk_mhz:.1f} us)")
         print(f"  busy cycles per warp mean {tot/n:.0f} = {tot/n/clk_mhz:.1f} us at {clk_mhz} MHz")
