@@ -139,9 +139,13 @@ int hgca_maw_update(const float* w, int64_t BH, int64_t nq, int64_t W, int64_t w
  * entries u_ent [B*Hkv, T] = position | (query-head mask << 24), grouped by
  * mask value (grouped = 1), in position order (0), or position-class
  * interleaved (2: every aligned group of 8 entries has distinct p & 7, as far
- * as the class counts allow; the bfloat16 decode layout); u_cnt [B*Hkv]; also the
- * sparse work-item prefix item_off [B*Hkv+1] and table item_tab
- * [max items][4] = (bk, lo, hi, 0). */
+ * as the class counts allow; the bfloat16 decode layout); u_cnt [B*Hkv]; and
+ * the sparse work items: each list is cut into items of sparse_rows entries
+ * followed by tail items of sparse_rows/4 entries covering its last sixth or
+ * more (all full items first, then all tail items, so the step ends on small
+ * items). item_off
+ * [2, B*Hkv+1] holds the full-item and tail-item prefixes, item_tab
+ * [items][4] = (bk, lo, hi, 0). */
 int hgca_union_build(const uint32_t* sel_mask, int64_t B, int64_t Hq, int64_t Hkv, int64_t words,
                      int64_t n_arch, int64_t T, int32_t* u_ent, int32_t* u_cnt, int32_t* item_off,
                      int32_t* item_tab, int64_t sparse_rows, int grouped, hgca_stream_t stream);
@@ -165,8 +169,9 @@ typedef struct hgca_decode_desc {
   double* part_m;           /* [max_items*G] */
   double* part_z;           /* [max_items*G] */
   float* part_acc;          /* [max_items*G*D] */
-  int64_t max_items;        /* >= B*Hkv*(1 + ceil(T / sparse_rows)) */
-  int32_t* counter;         /* int32 work counter scratch (>= 1 element) */
+  int64_t max_items;        /* >= B*Hkv*(3 + ceil(4T / sparse_rows)) */
+  int32_t* counter;         /* int32 work counter (>= 1 element): zero it once before the first step;
+                               every step leaves it 0 again */
   double* maw;              /* [B*Hq, T] or NULL */
   double alpha;
   float* out;               /* [B*Hq, D] */

@@ -287,7 +287,7 @@ int hgca_union_build(const uint32_t* sel_mask, int64_t B, int64_t Hq, int64_t Hk
                      int64_t n_arch, int64_t T, int32_t* u_ent, int32_t* u_cnt, int32_t* item_off,
                      int32_t* item_tab, int64_t sparse_rows, int grouped, hgca_stream_t stream) {
   if (B < 1 || Hkv < 1 || Hq % Hkv || Hq / Hkv > 8 || n_arch < 0 || n_arch > T || words * 32 < n_arch ||
-      sparse_rows < 1 || T >= (1 << 24))
+      sparse_rows < 4 || sparse_rows % 4 || T >= (1 << 24))
     return fail(HGCA_EINVAL, "union_build: bad shape");
   if (!item_tab || !u_ent || !u_cnt || !item_off) return fail(HGCA_EINVAL, "union_build: null output");
   return cuda_status(launch_union_build(sel_mask, B, Hq, Hkv, words, n_arch, T, u_ent, u_cnt, item_off,
@@ -309,9 +309,10 @@ static int decode_prepare(const hgca_decode_desc* d, DecodeArgs& a, DecodeMergeA
   const int64_t W = d->dhi - d->dlo;
   if (d->dlo < 0 || W < 1 || d->dhi > d->T || d->w_old < 0 || d->w_old > W || d->dsc_ld < W)
     return fail(HGCA_EINVAL, "decode_step: bad dense range");
-  if (d->sparse_rows < 1) return fail(HGCA_EINVAL, "decode_step: sparse_rows must be >= 1");
+  if (d->sparse_rows < 4 || d->sparse_rows % 4) return fail(HGCA_EINVAL, "decode_step: sparse_rows must be a positive multiple of 4");
   const int64_t n_dense = d->B * d->Hkv;
-  const int64_t max_sparse = d->B * d->Hkv * ((d->T + d->sparse_rows - 1) / d->sparse_rows);
+  // every item but the last full and last tail item of a list holds >= sparse_rows/4 rows
+  const int64_t max_sparse = d->B * d->Hkv * ((4 * d->T + d->sparse_rows - 1) / d->sparse_rows + 2);
   if (d->max_items < n_dense + max_sparse)
     return fail(HGCA_EINVAL, "decode_step: partial buffers hold %lld items, need %lld",
                 (long long)d->max_items, (long long)(n_dense + max_sparse));

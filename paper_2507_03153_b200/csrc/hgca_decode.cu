@@ -43,7 +43,7 @@ namespace hgca {
 // Debug build only (-DHGCA_TIMELINE): per-warp timeline of the decode kernel,
 // read back with hgca_debug_timeline (tools/timeline.py).
 #ifdef HGCA_TIMELINE
-#define TL_SLOTS 16
+#define TL_SLOTS 20
 __device__ unsigned long long g_tl[148 * 16 * TL_SLOTS];
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -214,104 +214,152 @@ __device__ void dense_epilogue(const DecodeArgs& a, int bk, const double* m, con
 }
 
 // ------------------------------------------------------------------ merge kernel
-// One CTA per (batch, query head), one thread per head dimension. Folds the
-// per-item partials of its (batch, kv-head) in item order -- sparse items into
-// the context partial, the dense item into the window partial -- then applies
-// merge_states(sparse, dense) (attention.py:153-188, engine.py:166-169).
-// Launched right behind the decode kernel with programmatic dependent launch:
-// its CTAs become resident early and wait in griddepcontrol.wait until the
-// decode grid has finished and its writes are visible.
+// One CTA per (batch, kv-head), launched behind the decode kernel with
+// programmatic dependent launch. Its sparse partials are two contiguous item
+// ranges (full items, tail items); they are streamed into shared memory with
+// 1-D TMA bulk copies (chunks of up to MERGE_CHUNK_BYTES, so the fold is not
+// limited by per-SM outstanding L1 misses), then folded per query head in
+// item order: max, one exp per (item, head), weighted sums with threads over
+// (head, dim). Chunks of long lists are combined with an online rescale. Then
+// merge_states(sparse, dense) with the dense item's partial
+// (attention.py:153-188, engine.py:166-169). Fixed order: deterministic.
+constexpr int MERGE_CHUNK_BYTES = 192 * 1024;
+
 template <int D, int G>
-__global__ void __launch_bounds__(D) decode_merge_kernel(const DecodeMergeArgs m) {
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  __shared__ double wsh[1024];
-  __shared__ double red[D / 32];
-  __shared__ double stat[2];
-  const int64_t bq = blockIdx.x;
-  const int64_t b = bq / m.Hq, h = bq % m.Hq;
-  const int64_t kvh = h / G, g = h % G, bk = b * m.Hkv + kvh;
+struct MergeCfg {
+  static constexpr int NT = G * D >= 256 ? 256 : G * D;         // threads
+  static constexpr int ROW = G * D * 4;                          // accumulator bytes per item
+  static constexpr int NI = MERGE_CHUNK_BYTES / (ROW + 16 * G);  // items per chunk
+  static constexpr int OFF_M = NI * ROW;                         // part_m [NI][G] fp64
+  static constexpr int OFF_Z = OFF_M + NI * G * 8;               // part_z [NI][G] fp64
+  static constexpr int OFF_W = OFF_Z + NI * G * 8;               // weights [G][NI] fp64
+  static constexpr int OFF_BAR = OFF_W + NI * G * 8;
+  static constexpr int SMEM = OFF_BAR + 64;
+  static constexpr int OPT = G * D / NT;                         // outputs (head, dim) per thread
+  static_assert(G * D % NT == 0, "merge thread mapping");
+};
+
+template <int D, int G>
+__global__ void __launch_bounds__(MergeCfg<D, G>::NT) decode_merge_kernel(const DecodeMergeArgs m, int32_t* counter) {
+  using C = MergeCfg<D, G>;
+  extern __shared__ __align__(128) unsigned char msm[];
+  float* sacc = reinterpret_cast<float*>(msm);
+  double* sm_m = reinterpret_cast<double*>(msm + C::OFF_M);
+  double* sm_z = reinterpret_cast<double*>(msm + C::OFF_Z);
+  double* sw = reinterpret_cast<double*>(msm + C::OFF_W);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(msm + C::OFF_BAR);
+  __shared__ double hM[G], hZ[G], hS[G];
+  const int64_t bk = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  auto block_max = [&](double x) {
-    x = warp_max_f64(x);
-    if (lane == 0) red[wid] = x;
-    __syncthreads();
-    if (tid == 0) {
-      double y = red[0];
-      for (int i = 1; i < D / 32; ++i) y = fmax(y, red[i]);
-      stat[0] = y;
-    }
-    __syncthreads();
-    const double r = stat[0];
-    __syncthreads();
-    return r;
-  };
-  auto block_sum = [&](double x) {
-    x = warp_sum_f64(x);
-    if (lane == 0) red[wid] = x;
-    __syncthreads();
-    if (tid == 0) {
-      double y = 0.0;
-      for (int i = 0; i < D / 32; ++i) y += red[i];  // fixed order
-      stat[1] = y;
-    }
-    __syncthreads();
-    const double r = stat[1];
-    __syncthreads();
-    return r;
-  };
-  // fold items [i0, i1) of head g: returns (out, lse) of the partial union
-  auto fold = [&](int64_t i0, int64_t i1, float& o, double& lse) {
-    o = 0.f;
-    lse = -INFINITY;
-    if (i1 <= i0) return;
-    double mx = -INFINITY;
-    for (int64_t i = i0 + tid; i < i1; i += D) mx = fmax(mx, m.part_m[i * G + g]);
-    const double M = block_max(mx);
-    if (M == -INFINITY) return;
-    double zl = 0.0, acc = 0.0;
-    for (int64_t c0 = i0; c0 < i1; c0 += 1024) {
-      const int64_t c1 = min(i1, c0 + 1024);
-      for (int64_t i = c0 + tid; i < c1; i += D) {
-        const double mi = m.part_m[i * G + g];
-        const double w = mi == -INFINITY ? 0.0 : exp(mi - M);
-        wsh[i - c0] = w;
-        zl += m.part_z[i * G + g] * w;
-      }
-      __syncthreads();
-      const float* pa = m.part_acc + (c0 * G + g) * D + tid;
-      const int n = (int)(c1 - c0);
-      int j = 0;
-      for (; j + 8 <= n; j += 8) {
-        float v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = pa[(int64_t)(j + u) * G * D];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) acc += wsh[j + u] * (double)v[u];
-      }
-      for (; j < n; ++j) acc += wsh[j] * (double)pa[(int64_t)j * G * D];
-      __syncthreads();
-    }
-    const double Z = block_sum(zl);
-    if (!(Z > 0.0)) return;
-    o = (float)(acc / Z);
-    lse = M + log(Z);
-  };
-  const int64_t s0 = m.n_dense_items + m.item_off[bk], s1 = m.n_dense_items + m.item_off[bk + 1];
-  float os, od;
-  double lse_s, lse_d;
-  fold(s0, s1, os, lse_s);
-  fold(bk, bk + 1, od, lse_d);
-  const double mm = fmax(lse_s, lse_d);
-  const bool both_empty = mm == -INFINITY;
-  const double ms = both_empty ? 0.0 : mm;
-  const double wa = exp(lse_s - ms), wb = exp(lse_d - ms);
-  const double zs = both_empty ? 1.0 : wa + wb;
-  const float ca = (float)(wa / zs), cb = (float)(wb / zs);
-  m.out[bq * D + tid] = __fadd_rn(__fmul_rn(ca, os), __fmul_rn(cb, od));
-  if (m.out_sparse) m.out_sparse[bq * D + tid] = os;
   if (tid == 0) {
-    m.lse[bq] = both_empty ? -INFINITY : ms + log(zs);
-    if (m.lse_sparse) m.lse_sparse[bq] = lse_s;
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  // the decode grid is complete: re-arm its work counter for the next step
+  if (blockIdx.x == 0 && tid == 0) *counter = 0;
+  const int64_t BK = m.B * m.Hkv, nd = m.n_dense_items;
+  const int64_t o0 = m.item_off[bk], o1 = m.item_off[bk + 1];
+  const int64_t t0 = m.item_off[BK + 1 + bk], t1 = m.item_off[BK + 1 + bk + 1];
+  const int64_t na = o1 - o0, n = na + (t1 - t0);
+  if (tid < G) {
+    hM[tid] = -INFINITY;
+    hZ[tid] = 0.0;
+  }
+  // this thread's outputs: (head, dim) = idx / D, idx % D for idx = tid + k*256
+  double acc[C::OPT];
+#pragma unroll
+  for (int k = 0; k < C::OPT; ++k) acc[k] = 0.0;
+  __syncthreads();
+  uint32_t phase = 0;
+  for (int64_t c0 = 0; c0 < n; c0 += C::NI) {
+    const int64_t c1 = min(n, c0 + C::NI), cn = c1 - c0;
+    // items [c0, c1) of the concatenated (full, tail) list: at most two contiguous ranges
+    if (tid == 0) {
+      const int64_t a_lo = c0, a_hi = min(c1, na);              // full-item part
+      const int64_t b_lo = max(c0, na), b_hi = c1;              // tail-item part
+      uint32_t bytes = 0;
+      if (a_hi > a_lo) bytes += (uint32_t)((a_hi - a_lo) * C::ROW);
+      if (b_hi > b_lo) bytes += (uint32_t)((b_hi - b_lo) * C::ROW);
+      mbar_expect_tx(bar, bytes);
+      if (a_hi > a_lo) {
+        const int64_t it = nd + o0 + a_lo, k = a_hi - a_lo, dst = a_lo - c0;
+        bulk_g2s(sacc + dst * G * D, m.part_acc + it * G * D, (uint32_t)(k * C::ROW), bar);
+      }
+      if (b_hi > b_lo) {
+        const int64_t it = nd + t0 + (b_lo - na), k = b_hi - b_lo, dst = b_lo - c0;
+        bulk_g2s(sacc + dst * G * D, m.part_acc + it * G * D, (uint32_t)(k * C::ROW), bar);
+      }
+    }
+    // (m, z) of the chunk's items: plain loads while the bulk copies land
+    for (int64_t x = tid; x < cn * G; x += C::NT) {
+      const int64_t i = c0 + x / G, g = x % G;
+      const int64_t it = i < na ? nd + o0 + i : nd + t0 + (i - na);
+      sm_m[x] = m.part_m[it * G + g];
+      sm_z[x] = m.part_z[it * G + g];
+    }
+    __syncthreads();
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    // per head: chunk max (warp g over items), new running max, weights, z
+    for (int g = wid; g < G; g += C::NT / 32) {
+      double mx = -INFINITY;
+      for (int64_t i = lane; i < cn; i += 32) mx = fmax(mx, sm_m[i * G + g]);
+      mx = warp_max_f64(mx);
+      const double mo = hM[g], mn = fmax(mo, mx);
+      double zl = 0.0;
+      for (int64_t i = lane; i < cn; i += 32) {
+        const double mi = sm_m[i * G + g];
+        const double w = (mi == -INFINITY || mn == -INFINITY) ? 0.0 : exp(mi - mn);
+        sw[g * C::NI + i] = w;
+        zl += sm_z[i * G + g] * w;
+      }
+      zl = warp_sum_f64(zl);
+      if (lane == 0) {
+        const double so = (mo == -INFINITY || mn == -INFINITY) ? 0.0 : exp(mo - mn);
+        hS[g] = so;
+        hZ[g] = hZ[g] * so + zl;
+        hM[g] = mn;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < C::OPT; ++k) {
+      const int idx = tid + k * C::NT, g = idx / D;
+      double a = acc[k] * hS[g];
+      const double* w = sw + g * C::NI;
+      const float* src = sacc + idx;
+      for (int64_t i = 0; i < cn; ++i) a += w[i] * (double)src[i * G * D];
+      acc[k] = a;
+    }
+    __syncthreads();  // the next chunk's copies overwrite sacc / sw
+  }
+  // merge_states(sparse, dense) per output (head, dim)
+  const int64_t b = bk / m.Hkv, kvh = bk % m.Hkv;
+#pragma unroll
+  for (int k = 0; k < C::OPT; ++k) {
+    const int idx = tid + k * C::NT, g = idx / D, c = idx % D;
+    const int64_t bq = b * m.Hq + kvh * G + g;
+    const double Ms = hM[g], Zs = hZ[g];
+    const bool s_empty = !(Zs > 0.0) || Ms == -INFINITY;
+    const double lse_s = s_empty ? -INFINITY : Ms + log(Zs);
+    const double md = m.part_m[bk * G + g], zd = m.part_z[bk * G + g];
+    const bool d_empty = !(zd > 0.0) || md == -INFINITY;
+    const double lse_d = d_empty ? -INFINITY : md + log(zd);
+    const double mm = fmax(lse_s, lse_d);
+    const bool both_empty = mm == -INFINITY;
+    const double ms = both_empty ? 0.0 : mm;
+    const double wa = exp(lse_s - ms), wb = exp(lse_d - ms);
+    const double zs = both_empty ? 1.0 : wa + wb;
+    const float ca = (float)(wa / zs), cb = (float)(wb / zs);
+    const float os = s_empty ? 0.f : (float)(acc[k] / Zs);
+    const float od = d_empty ? 0.f : (float)((double)m.part_acc[(bk * G + g) * D + c] / zd);
+    m.out[bq * D + c] = __fadd_rn(__fmul_rn(ca, os), __fmul_rn(cb, od));
+    if (m.out_sparse) m.out_sparse[bq * D + c] = os;
+    if (c == 0) {
+      m.lse[bq] = both_empty ? -INFINITY : ms + log(zs);
+      if (m.lse_sparse) m.lse_sparse[bq] = lse_s;
+    }
   }
 }
 
@@ -365,7 +413,7 @@ __global__ void __launch_bounds__(Bf16Cfg<D, G, S>::NC * 32, 1) decode_bf16_kern
   float* pt = reinterpret_cast<float*>(wsm + C::OFF_PT);
   double* st = reinterpret_cast<double*>(wsm + C::OFF_ST);
   const int W = (int)(a.dhi - a.dlo);
-  const int total = (int)(a.n_dense_items + (int64_t)a.item_off[a.B * a.Hkv]);
+  const int total = (int)(a.n_dense_items + (int64_t)a.item_off[2 * a.B * a.Hkv + 1]);
   const unsigned char* Qg = reinterpret_cast<const unsigned char*>(a.q);
   const int g4 = lane >> 2, t4 = lane & 3;      // mma groupID / thread-in-group
   const int hA = 2 * t4, hB = 2 * t4 + 1;       // query heads of this lane's fragment columns
@@ -373,10 +421,10 @@ __global__ void __launch_bounds__(Bf16Cfg<D, G, S>::NC * 32, 1) decode_bf16_kern
   if (lane < S) mbar_init(&bar[lane], 1);
   fence_mbar_init();
   __syncwarp();
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // let the merge grid get resident
   TL(unsigned long long* tl = g_tl + ((int64_t)blockIdx.x * C::NC + warp) * TL_SLOTS;
      unsigned long long tl_merge = 0, tl_wait = 0, tl_sub = 0, tl_items = 0, tl_qk = 0, tl_pv = 0, tl_v = 0,
-                        tl_issue = 0, tl_tma = 0, tl_nmerge = 0, tl_sm = 0, tl_epi = 0;
+                        tl_issue = 0, tl_tma = 0, tl_nmerge = 0, tl_sm = 0, tl_epi = 0, tl_mask = 0,
+                        tl_smax = 0, tl_end = 0;
      if (lane == 0) tl[0] = gtimer(););
 
   Cursor cur;
@@ -405,9 +453,20 @@ __global__ void __launch_bounds__(Bf16Cfg<D, G, S>::NC * 32, 1) decode_bf16_kern
       if (lane == 0) mbar_expect_tx(&bar[s], C::STAGE + (d.first ? C::QB : 0));
       __syncwarp();
       TL(long long i0 = clock64();)
+#ifdef HGCA_BULK_ROWS
+      // experiment: one 1-D bulk copy per row pair (no tensor map)
+      {
+        const unsigned char* src = reinterpret_cast<const unsigned char*>(a.KV) +
+                                   ((int64_t)d.bk * a.T + pos) * (int64_t)(2 * C::ROWB);
+        asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                     ::"r"(wsm_u + s * C::STAGE + lane * 2 * C::ROWB), "l"(src), "r"(2 * C::ROWB),
+                     "r"(smem_u32(&bar[s])) : "memory");
+      }
+#else
       if (lane < C::NOPS)
         tma_gather4(wsm_u + s * C::STAGE + rg * 4 * 2 * C::ROWB, &a.kmap, 0, rowbase + q0, rowbase + q1,
                     rowbase + q2, rowbase + q3, &bar[s]);
+#endif
       TL(tl_tma += clock64() - i0;)
       if (lane == 0 && d.first) {
         const int64_t b = d.bk / a.Hkv, kvh = d.bk % a.Hkv;
@@ -434,6 +493,12 @@ __global__ void __launch_bounds__(Bf16Cfg<D, G, S>::NC * 32, 1) decode_bf16_kern
     if (d.item < 0) break;
     mbar_wait(&bar[s], (k / S) & 1);
     TL(long long c1 = clock64(); tl_wait += c1 - c0; ++tl_sub;)
+#ifdef HGCA_NOCOMPUTE
+    // experiment: data movement only (results are garbage)
+    __syncwarp();
+    issue(s);
+    continue;
+#endif
     const uint32_t stg = wsm_u + s * C::STAGE;
     if (d.first) {
       const uint32_t* qw = reinterpret_cast<const uint32_t*>(wsm + C::OFF_Q + s * C::QSLOT);
@@ -464,6 +529,7 @@ __global__ void __launch_bounds__(Bf16Cfg<D, G, S>::NC * 32, 1) decode_bf16_kern
         mma_bf16(c[h], af, qf[kc][0], qf[kc][1]);
       }
     }
+    TL(long long c2a = clock64(); tl_sm += c2a - c2;)
     // ---- scale + mask: value j of this lane is row j*8 + g4, heads hA / hB
     float sA[4], sB[4];
 #pragma unroll
@@ -482,6 +548,7 @@ __global__ void __launch_bounds__(Bf16Cfg<D, G, S>::NC * 32, 1) decode_bf16_kern
         if (hB < G) dsc[(bq0 + hB) * a.dsc_ld + d.r0 + row] = vb;
       }
     }
+    TL(long long c2b = clock64(); tl_mask += c2b - c2a;)
     // ---- online softmax (fp32) per head, reduced over the 8 lanes sharing t4
     float xA = fmaxf(fmaxf(sA[0], sA[1]), fmaxf(sA[2], sA[3]));
     float xB = fmaxf(fmaxf(sB[0], sB[1]), fmaxf(sB[2], sB[3]));
@@ -516,6 +583,7 @@ __global__ void __launch_bounds__(Bf16Cfg<D, G, S>::NC * 32, 1) decode_bf16_kern
         acc[mt][0] *= alA; acc[mt][1] *= alB; acc[mt][2] *= alA; acc[mt][3] *= alB;
       }
     }
+    TL(long long c2c = clock64(); tl_smax += c2c - c2b;)
     // ---- P^T to shared memory (rows x heads -> heads x rows)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -549,6 +617,7 @@ __global__ void __launch_bounds__(Bf16Cfg<D, G, S>::NC * 32, 1) decode_bf16_kern
       }
     }
     TL(long long c4 = clock64(); tl_pv += c4 - c3;)
+    TL(long long c4b = clock64();)
     if (d.last) {
       TL(++tl_items;)
       // partial (m, z, acc) of this item; acc[mt][j] = O[head hA|hB][dim mt*16 + g4 (+8)]
@@ -578,14 +647,16 @@ __global__ void __launch_bounds__(Bf16Cfg<D, G, S>::NC * 32, 1) decode_bf16_kern
 
     }
     __syncwarp();
-    TL(long long c5 = clock64();)
+    TL(long long c5 = clock64(); tl_end += c5 - c4b;)
     issue(s);
     TL(tl_issue += clock64() - c5;)
   }
+  TL(if (lane == 0) tl[17] = gtimer();)
   TL(if (lane == 0) {
     tl[1] = gtimer();
     tl[2] = tl_merge; tl[3] = tl_wait; tl[4] = tl_sub; tl[5] = tl_items; tl[6] = tl_qk; tl[7] = tl_pv;
-    tl[8] = tl_v; tl[9] = tl_issue; tl[10] = tl_tma; tl[11] = tl_nmerge; tl[12] = tl_sm; tl[13] = tl_epi;
+    tl[8] = tl_v; tl[9] = tl_issue; tl[10] = tl_tma; tl[11] = tl_mask; tl[12] = tl_sm; tl[13] = tl_epi;
+    tl[14] = tl_smax; tl[15] = tl_end; tl[16] = blockIdx.x;
   })
 }
 
@@ -633,12 +704,11 @@ __global__ void __launch_bounds__(F32Cfg<D, G>::NC * 32, 1) decode_f32_kernel(co
   float* accs = reinterpret_cast<float*>(wsm + C::OFF_ACC);
   double* mz = reinterpret_cast<double*>(wsm + C::OFF_MZ);
   const int W = (int)(a.dhi - a.dlo);
-  const int total = (int)(a.n_dense_items + (int64_t)a.item_off[a.B * a.Hkv]);
+  const int total = (int)(a.n_dense_items + (int64_t)a.item_off[2 * a.B * a.Hkv + 1]);
   const unsigned char* Qg = reinterpret_cast<const unsigned char*>(a.q);
   if (lane < C::S) mbar_init(&bar[lane], 1);
   fence_mbar_init();
   __syncwarp();
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // let the merge grid get resident
 
   Cursor cur;
   cur.nxt = 0;
@@ -1025,49 +1095,75 @@ __global__ void __launch_bounds__(1024) union_classes_kernel(const uint32_t* __r
   }
 }
 
-// item_off[bk] = sum_{x<bk} ceil(u_cnt[x] / rows)  (single CTA, sequential chunks)
-__global__ void item_offsets_kernel(const int32_t* u_cnt, int64_t BK, int64_t rows, int32_t* off) {
-  __shared__ int32_t carry;
-  __shared__ int wsum[32];
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarp = blockDim.x >> 5;
-  if (tid == 0) carry = 0;
-  __syncthreads();
-  for (int64_t x0 = 0; x0 < BK; x0 += blockDim.x) {
-    const int64_t x = x0 + tid;
-    const int c = x < BK ? (int)((u_cnt[x] + rows - 1) / rows) : 0;
-    int incl = c;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane == 31) wsum[wid] = incl;
-    __syncthreads();
-    if (wid == 0) {
-      int v = lane < nwarp ? wsum[lane] : 0;
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += y;
-      }
-      if (lane < nwarp) wsum[lane] = v;
-    }
-    __syncthreads();
-    if (x < BK) off[x] = carry + (wid ? wsum[wid - 1] : 0) + (incl - c);
-    __syncthreads();
-    if (tid == 0) carry += wsum[nwarp - 1];
-    __syncthreads();
-  }
-  if (tid == 0) off[BK] = carry;
+// Sparse work items. Each (b, kv-head) union list [0, u_cnt) is cut into
+// full items of `rows` entries over [0, big) and tail items of rows/4 entries
+// over [big, u_cnt), big = rows * floor((u_cnt - u_cnt/TAIL_DIV) / rows): the
+// last >= 1/TAIL_DIV of every list is small items. Item ids: all full items
+// (bk order), then all tail items (bk order), so once the queue reaches the
+// tail every warp picks up short items and the warps finish together (the
+// tail must hold more work than one full item per warp).
+// item_off [2][BK+1]: row 0 = full-item prefix (row 0 [BK] = number of full
+// items), row 1 = absolute start of each bk's tail items (row 1 [BK] = total).
+constexpr int TAIL_DIV = 6;
+__device__ __forceinline__ void item_counts(int64_t cnt, int64_t rows, int& nbig, int& nsmall) {
+  const int64_t big = (cnt - cnt / TAIL_DIV) / rows * rows;
+  const int64_t small = rows / 4;
+  nbig = (int)(big / rows);
+  nsmall = (int)((cnt - big + small - 1) / small);
 }
 
-// item_tab[item_off[bk] + i] = (bk, i*rows, min(u_cnt[bk], (i+1)*rows), 0)
+__global__ void item_offsets_kernel(const int32_t* u_cnt, int64_t BK, int64_t rows, int32_t* off) {
+  __shared__ int32_t carry[2];
+  __shared__ int wsum[2][32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarp = blockDim.x >> 5;
+  if (tid < 2) carry[tid] = 0;
+  __syncthreads();
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int64_t x0 = 0; x0 < BK; x0 += blockDim.x) {
+      const int64_t x = x0 + tid;
+      int nb = 0, ns = 0;
+      if (x < BK) item_counts(u_cnt[x], rows, nb, ns);
+      const int c = pass == 0 ? nb : ns;
+      int incl = c;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) wsum[pass][wid] = incl;
+      __syncthreads();
+      if (wid == 0) {
+        int v = lane < nwarp ? wsum[pass][lane] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, v, o);
+          if (lane >= o) v += y;
+        }
+        if (lane < nwarp) wsum[pass][lane] = v;
+      }
+      __syncthreads();
+      if (x < BK) off[pass * (BK + 1) + x] = carry[pass] + (wid ? wsum[pass][wid - 1] : 0) + (incl - c);
+      __syncthreads();
+      if (tid == 0) carry[pass] += wsum[pass][nwarp - 1];
+      __syncthreads();
+    }
+    if (tid == 0) {
+      off[pass * (BK + 1) + BK] = carry[pass];
+      if (pass == 0) carry[1] = carry[0];  // tail items follow all full items
+    }
+    __syncthreads();
+  }
+}
+
+// item_tab[id] = (bk, lo, hi, 0) for the full and tail items of bk
 __global__ void item_table_kernel(const int32_t* u_cnt, const int32_t* off, int64_t BK, int64_t rows, int4* tab) {
   const int64_t bk = blockIdx.x;
   if (bk >= BK) return;
-  const int n = off[bk + 1] - off[bk];
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int lo = (int)(i * rows);
-    tab[off[bk] + i] = make_int4((int)bk, lo, (int)min((int64_t)u_cnt[bk], (int64_t)lo + rows), 0);
-  }
+  int nb = 0, ns = 0;
+  item_counts(u_cnt[bk], rows, nb, ns);
+  const int cnt = u_cnt[bk], small = (int)(rows / 4), big = nb * (int)rows;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x)
+    tab[off[bk] + i] = make_int4((int)bk, i * (int)rows, (i + 1) * (int)rows, 0);
+  for (int i = threadIdx.x; i < ns; i += blockDim.x)
+    tab[off[BK + 1 + bk] + i] = make_int4((int)bk, big + i * small, min(cnt, big + (i + 1) * small), 0);
 }
 
 // KV[bh, pos + i, 0, :] = k_new[bh, i, :], KV[bh, pos + i, 1, :] = v_new[bh, i, :];
@@ -1129,21 +1225,6 @@ static int set_smem(K kernel, int bytes, bool& done) {
   return 0;
 }
 
-template <int D, int G>
-static int launch_merge_t(const DecodeMergeArgs& m, cudaStream_t s) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(m.B * m.Hq));
-  cfg.blockDim = dim3(D);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return (int)cudaLaunchKernelEx(&cfg, decode_merge_kernel<D, G>, m);
-}
-
 template <bool BF16, int D, int G>
 static int launch_decode_t(const DecodeArgs& a_in, cudaStream_t s) {
   DecodeArgs a = a_in;
@@ -1178,7 +1259,23 @@ static int launch_decode_t(const DecodeArgs& a_in, cudaStream_t s) {
   }
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
-  return launch_merge_t<D, G>(a.m, s);
+  // merge kernel: programmatic dependent launch (its launch overlaps the decode tail)
+  cudaLaunchConfig_t cfg = {};
+  static bool mattr = false;
+  {
+    const int rc = set_smem(decode_merge_kernel<D, G>, MergeCfg<D, G>::SMEM, mattr);
+    if (rc) return rc;
+  }
+  cfg.gridDim = dim3((unsigned)(a.B * a.Hkv));
+  cfg.blockDim = dim3(MergeCfg<D, G>::NT);
+  cfg.dynamicSmemBytes = MergeCfg<D, G>::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return (int)cudaLaunchKernelEx(&cfg, decode_merge_kernel<D, G>, a.m, a.counter);
 }
 
 template <bool BF16, int D>
@@ -1199,9 +1296,8 @@ int decode_chunk_rows(int dtype, int64_t D) {
 }
 
 int launch_decode_partial(int dtype, const DecodeArgs& a, cudaStream_t s) {
-  // work counter
-  cudaError_t e = cudaMemsetAsync(a.counter, 0, sizeof(int32_t), s);
-  if (e != cudaSuccess) return (int)e;
+  // the work counter must be 0 on entry: zeroed by the caller once, then re-armed
+  // by every merge kernel (no per-step memset launch)
   if (dtype == kBF16) {
     if (a.D == 128) return launch_decode_g<true, 128>(a, s);
     if (a.D == 64) return launch_decode_g<true, 64>(a, s);

@@ -76,7 +76,7 @@ struct DecodeArgs {
   double* part_m;         // [items, G]
   double* part_z;         // [items, G]
   float* part_acc;        // [items, G, D]
-  int32_t* counter;       // work counter (zeroed before launch)
+  int32_t* counter;       // work counter (0 on entry; re-armed by the merge kernel)
   int64_t n_dense_items;  // B*Hkv
   // dense-item epilogue: weights + MAW maintenance of the attended window
   int64_t w_old;          // window entries before this step (EMA'd); the rest are new

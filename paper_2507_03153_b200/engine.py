@@ -178,8 +178,8 @@ class LayerState:
         self.sel = torch.zeros((B * Hq, words), dtype=torch.int32, device=dev)
         self.u_ent = torch.zeros((B * Hkv, T), dtype=torch.int32, device=dev)
         self.u_cnt = torch.zeros(B * Hkv, dtype=torch.int32, device=dev)
-        self.item_off = torch.zeros(B * Hkv + 1, dtype=torch.int32, device=dev)
-        self.item_tab = torch.zeros((B * Hkv * (T // 32 + 1), 4), dtype=torch.int32, device=dev)
+        self.item_off = torch.zeros(2 * (B * Hkv + 1), dtype=torch.int32, device=dev)
+        self.item_tab = torch.zeros((B * Hkv * (-(-4 * T // SPARSE_ROWS) + 2), 4), dtype=torch.int32, device=dev)
         self.lo = 0    # archive size
         self.nxt = 0   # next position
         self.keep = None
@@ -245,12 +245,12 @@ class HybridEngine:
         self.dsc_ld = self.cap + 1
         self.dsc = torch.zeros((BHq, self.dsc_ld), dtype=torch.float64, device=self.dev)
         n_dense = self.B * self.Hkv
-        n_sparse = self.B * self.Hkv * math.ceil(self.T / SPARSE_ROWS)
+        n_sparse = self.B * self.Hkv * (math.ceil(4 * self.T / SPARSE_ROWS) + 2)
         self.max_items = n_dense + n_sparse
         self.part_m = torch.empty(self.max_items * self.G, dtype=torch.float64, device=self.dev)
         self.part_z = torch.empty(self.max_items * self.G, dtype=torch.float64, device=self.dev)
         self.part_acc = torch.empty(self.max_items * self.G * self.D, dtype=torch.float32, device=self.dev)
-        self.counter = torch.zeros(1 + self.B * self.Hkv, dtype=torch.int32, device=self.dev)
+        self.counter = torch.zeros(4, dtype=torch.int32, device=self.dev)  # decode work counter
         self._desc = _lib.DecodeDesc()
         self.launches = 0          # kernels of libhgca_b200 launched by this engine
         self.step_events = None     # list -> (start, end) CUDA events around the decode kernel

@@ -1,11 +1,11 @@
 #!/bin/bash
-# A/B of library variants (run under gpurun): timeline + bench for each
+# A/B of library variants (run under gpurun): timeline + bench for each. usage: gpu_ab.sh v1 v2 ...
 L=paper_2507_03153_b200/_lib
-echo "=== base"; HGCA_LIB=$L/libhgca_b200_tl.so timeout 300 python tools/timeline.py 2>&1 | tail -10
-echo "=== rowbox"; HGCA_LIB=$L/libhgca_b200_tlrow.so timeout 300 python tools/timeline.py 2>&1 | tail -10
-for v in "" row; do
+for v in "$@"; do
+  tl=$L/libhgca_b200_tl${v:+$v}.so; [ "$v" = "" ] && tl=$L/libhgca_b200_tl.so
+  echo "=== timeline [$v]"; HGCA_LIB=$tl timeout 300 python tools/timeline.py 2>&1 | tail -8
   lib=$L/libhgca_b200${v:+_$v}.so
-  echo "=== bench $v"; HGCA_LIB=$lib timeout 300 python bench.py --no-cpu-baseline --steps 200 --e2e-steps 20 2>&1 | tail -1 | python -c "
+  echo "=== bench [$v]"; HGCA_LIB=$lib timeout 300 python bench.py --no-cpu-baseline --steps 200 --e2e-steps 20 2>&1 | tail -1 | python -c "
 import json,sys
 d=json.loads(sys.stdin.read()); r=d['roofline']
 print('step_ms', d['ms_per_step'], 'kernel_ms', r['kernel_ms'], 'GB/s', r['achieved'], 'frac', r['frac'])"

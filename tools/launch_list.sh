@@ -1,6 +1,7 @@
 #!/bin/bash
-# per-launch device times of the bench's steady-state steps (run under gpurun)
+# per-launch device times of the bench's timed steps only (NVTX range "timed"); run under gpurun
 tag=${1:-launches}
-timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none -s 3700 -c ${2:-200} --csv \
-  --log-file gpurun_out/${tag}.csv python bench.py --steps 60 --warmup 3 --no-cpu-baseline --e2e-steps 2 > /dev/null 2>&1
-python tools/launch_summary.py gpurun_out/${tag}.csv
+timeout 600 ncu --nvtx --nvtx-include "timed/" --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/${tag}.csv python bench.py --steps ${2:-20} --warmup 3 --no-cpu-baseline --e2e-steps 2 \
+  > gpurun_out/${tag}_bench.log 2>&1
+python tools/launch_summary.py gpurun_out/${tag}.csv | tee gpurun_out/${tag}_summary.txt

@@ -17,7 +17,7 @@ os.environ.setdefault("HGCA_LIB", os.path.join(ROOT, "paper_2507_03153_b200", "_
 import bench  # noqa: E402
 import paper_2507_03153_b200 as hg  # noqa: E402
 
-SLOTS = 16
+SLOTS = 20
 
 
 def main():
@@ -50,25 +50,34 @@ def main():
         t = buf.reshape(n, SLOTS).astype(np.float64)
         t0 = t[:, 0].min()
         start, end = (t[:, 0] - t0) / 1e3, (t[:, 1] - t0) / 1e3
-        names = ["", "", "merge", "wait", "sub", "items", "qk", "pv", "v", "issue", "tma", "nmerge", "smma", "epi"]
+        names = ["", "", "merge", "wait", "sub", "items", "qk", "pv", "v", "issue", "tma", "mask", "smma", "epi",
+                 "smax", "end", "sm"]
         cyc = {k: t[:, i] for i, k in enumerate(names) if k}
         span = end.max()
-        print(f"--- step {it}: kernel {ms*1e3:.1f} us (events), warps {n} ({nc}/SM), span {span:.1f} us")
+        print(f"--- step {it}: decode+merge {ms*1e3:.1f} us (events), warps {n} ({nc}/SM), decode span {span:.1f} us")
         print("warp end us: p0 %.1f p10 %.1f p50 %.1f p90 %.1f p99 %.1f max %.1f" %
               tuple(np.percentile(end, [0, 10, 50, 90, 99, 100])))
-        print("warp start us: max %.1f" % start.max())
-        tot = sum(cyc[k].sum() for k in ("merge", "wait", "qk", "pv", "v", "issue"))
-        clk_mhz = 1965.0
-        for k in ("wait", "v", "qk", "pv", "issue", "merge"):
-            print(f"  {k:6s} {cyc[k].sum()/tot:6.1%}  per sub-chunk {cyc[k].sum()/max(cyc['sub'].sum(),1):8.0f} cyc")
-        sub = max(cyc['sub'].sum(), 1)
-        print(f"  of which: qk-mma {cyc['smma'].sum()/sub:.0f} cyc/sub, tma-issue {cyc['tma'].sum()/sub:.0f} cyc/sub; "
-              f"merges {cyc['nmerge'].sum():.0f} (max/warp {cyc['nmerge'].max():.0f}), "
-              f"cyc/merge {cyc['merge'].sum()/max(cyc['nmerge'].sum(),1):.0f}, dense epilogue cyc/item "
-              f"{cyc['epi'].sum()/max(len(np.nonzero(cyc['epi'])[0]),1):.0f}")
-        print(f"  sub-chunks {cyc['sub'].sum():.0f} items {cyc['items'].sum():.0f} "
-              f"merge cyc max/warp {cyc['merge'].max():.0f} ({cyc['merge'].max()/clk_mhz:.1f} us)")
-        print(f"  busy cycles per warp mean {tot/n:.0f} = {tot/n/clk_mhz:.1f} us at {clk_mhz} MHz")
+        sub = max(cyc["sub"].sum(), 1)
+        parts = ["wait", "v", "smma", "mask", "smax", "qk", "pv", "end", "issue", "tma"]
+        print("  cycles per sub-chunk: " + ", ".join(f"{k} {cyc[k].sum()/sub:.0f}" for k in parts))
+        print("  (qk = smma + mask + smax + P^T store; issue includes tma)")
+        tot = sum(cyc[k].sum() for k in ("wait", "v", "qk", "pv", "end", "issue"))
+        print(f"  busy cycles per warp mean {tot/n:.0f} = {tot/n/1965:.1f} us; sub-chunks/warp "
+              f"min {cyc['sub'].min():.0f} mean {cyc['sub'].mean():.1f} max {cyc['sub'].max():.0f}; "
+              f"dense epilogue {cyc['epi'].sum()/max(np.count_nonzero(cyc['epi']),1):.0f} cyc/item")
+        smid = cyc["sm"].astype(int)
+        sm_end = np.array([end[smid == k].max() for k in range(148)])
+        sm_sub = np.array([cyc["sub"][smid == k].sum() for k in range(148)])
+        print(f"  per-SM: last warp end p0 {sm_end.min():.1f} p50 {np.median(sm_end):.1f} max {sm_end.max():.1f} us; "
+              f"sub-chunks per SM min {sm_sub.min():.0f} max {sm_sub.max():.0f}; corr(end, sub) "
+              f"{np.corrcoef(sm_end, sm_sub)[0, 1]:.2f}")
+        items_end = (t[:, 17] - t0) / 1e3
+        print(f"  items done: p0 {items_end.min():.1f} p50 {np.median(items_end):.1f} max {items_end.max():.1f} us; "
+              f"after merge phase: p50 {np.median(end):.1f} max {end.max():.1f} us")
+        # early finishers: what were they doing?
+        order = np.argsort(end)
+        print(f"  first 5 finishers: end {np.round(end[order[:5]], 1)} subs {cyc['sub'][order[:5]]}; "
+              f"last 5: end {np.round(end[order[-5:]], 1)} subs {cyc['sub'][order[-5:]]}")
 
 
 if __name__ == "__main__":
