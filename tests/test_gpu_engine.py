@@ -219,3 +219,57 @@ def test_engine_decode_is_deterministic(cuda):
         outs.append((r.output.cpu().numpy(), r.lse.cpu().numpy(), eng.maw_host()))
     for a, b in zip(*outs):
         np.testing.assert_array_equal(a, b)
+
+
+# every (storage dtype, head_dim, GQA group) instantiation of the decode kernels
+@pytest.mark.parametrize("dtype", ["bfloat16", "float32"])
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("Hq,Hkv", [(4, 4), (8, 4), (8, 2), (8, 1)])
+def test_engine_kernel_instantiations(cuda, dtype, d, Hq, Hkv):
+    eng, oracles, worst = _run_batched(cuda, B=2, Hq=Hq, Hkv=Hkv, d=d, dtype=dtype, beta=1.0,
+                                       cores=64, steps_n=90, seed=d + Hq + Hkv)
+    assert eng.layers[0].archive_size > 0
+    assert worst <= (REL_BF16 if dtype == "bfloat16" else REL_FP32), worst
+    if dtype == "float32":  # reference-exact path: selections bit-exact per query head
+        ctx = eng.context_indices()
+        for b, o in enumerate(oracles):
+            for h in range(Hq):
+                np.testing.assert_array_equal(ctx[b * Hq + h], o.context[h])
+
+
+def test_bf16_rows_rotated_and_union_classes(cuda):
+    """bf16 K|V rows are stored position-rotated (hgca_write_rows) and the
+    union lists are class-interleaved: the logical K/V views give back exactly
+    what was written, every selected archive row appears once in its
+    (batch, kv-head) union with the right query-head mask, and aligned groups
+    of 8 entries have distinct p & 7 outside the per-list surplus tail."""
+    B, Hq, Hkv = 2, 8, 2
+    eng, g, tdt = _big_engine(cuda, "bfloat16", B=B, Hq=Hq, Hkv=Hkv, ctx=2048, seed=9)
+    ls = eng.layers[0]
+    kv = ls.rows()
+    # rows written by the staged decode steps round-trip through the rotation
+    src = torch.randn((B, Hkv, 1, 128), generator=g, device="cuda").to(tdt)
+    pos = ls.nxt
+    eng.step(0, cuda.StepInput("decode", torch.randn((B, Hq, 1, 128), generator=g, device="cuda").to(tdt),
+                               src, -src))
+    kv = ls.rows()
+    torch.testing.assert_close(kv[:, pos, 0].view(B, Hkv, 128), src[:, :, 0], rtol=0, atol=0)
+    torch.testing.assert_close(kv[:, pos, 1].view(B, Hkv, 128), -src[:, :, 0], rtol=0, atol=0)
+    G = Hq // Hkv
+    sel = eng.store_entries()[0]
+    ent = ls.u_ent.cpu().numpy().view(np.uint32)
+    cnt = ls.u_cnt.cpu().numpy()
+    for bk in range(B * Hkv):
+        e = ent[bk, :cnt[bk]]
+        p, qm = e & 0xFFFFFF, e >> 24
+        b, kvh = divmod(bk, Hkv)
+        want = {}
+        for gi in range(G):
+            for x in sel[b * Hq + kvh * G + gi]:
+                want[int(x)] = want.get(int(x), 0) | (1 << gi)
+        assert len(p) == len(set(p.tolist())) == len(want)
+        assert all(want[int(x)] == int(m) for x, m in zip(p, qm))
+        classes = np.bincount(p % 8, minlength=8)
+        n_min = classes.min()
+        groups = (p[: 8 * n_min] % 8).reshape(-1, 8)
+        assert (np.sort(groups, axis=1) == np.arange(8)).all()
