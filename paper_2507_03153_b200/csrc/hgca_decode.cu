@@ -58,6 +58,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #ifndef HGCA_BF16_STAGES
 #define HGCA_BF16_STAGES 2
 #endif
+#ifndef HGCA_BF16_PAIRS
+#define HGCA_BF16_PAIRS 6  // consumer warps per CTA, each paired with its own producer warp
+#endif
 
 constexpr int SUB = 32;  // rows per pipeline stage (one per lane)
 constexpr uint32_t FULL = 0xffffffffu;
@@ -177,7 +180,7 @@ __device__ __forceinline__ int32_t sub_entry(const StageDesc& d, const DecodeArg
 template <typename SC, int G>
 __device__ void dense_epilogue(const DecodeArgs& a, int bk, const double* m, const double* z, int lane) {
   if (a.maw == nullptr && a.wts_out == nullptr) return;
-  constexpr int JB = G >= 4 ? 2 : 8 / G;  // window rows per lane per batch: JB*G loads of each kind in flight
+  constexpr int JB = G >= 8 ? 1 : (G >= 4 ? 2 : 8 / G);  // window rows per lane per batch: JB*G loads in flight
   const int64_t W = a.dhi - a.dlo;
   const int64_t b = bk / a.Hkv, kvh = bk % a.Hkv;
   const int64_t bq0 = b * a.Hq + kvh * G;
@@ -364,7 +367,13 @@ __global__ void __launch_bounds__(MergeCfg<D, G>::NT) decode_merge_kernel(const 
 }
 
 // =========================================================== bf16 (tensor-core) kernel
-template <int D, int G, int S>
+// Warp-specialized CTA: NC consumer warps, each with its own S-stage ring in
+// shared memory, and NC producer warps, one per consumer, that run that
+// consumer's work cursor and issue its TMA gathers, so the consumers only
+// compute. (A producer costs ~1.1K cycles per stage -- 8 gather4 ops at ~70
+// cycles each plus the cursor -- so sharing producers between consumers makes
+// the producers the bottleneck; measured on B200.)
+template <int D, int G, int S, int NPAIR>
 struct Bf16Cfg {
   static constexpr int ROWB = D * 2;                    // bytes of one K (or V) row
   static constexpr int STAGE = SUB * 2 * ROWB;          // 32 rotated K|V row pairs
@@ -376,11 +385,13 @@ struct Bf16Cfg {
   static constexpr int OFF_PT = OFF_Q + S * QSLOT;
   static constexpr int OFF_META = OFF_PT + 8 * PT_LD * 4;
   static constexpr int OFF_DESC = OFF_META + S * SUB * 4;
-  static constexpr int OFF_BAR = OFF_DESC + S * 32;
-  static constexpr int OFF_ST = OFF_BAR + S * 8;        // final (m, z) per head, fp64
+  static constexpr int OFF_FULL = OFF_DESC + S * 32;    // mbarriers: stage landed (TMA tx)
+  static constexpr int OFF_EMPTY = OFF_FULL + S * 8;    // mbarriers: stage consumed
+  static constexpr int OFF_ST = OFF_EMPTY + S * 8;      // final (m, z) per head, fp64
   static constexpr int WARP_SMEM = (OFF_ST + 16 * 8 + 1023) / 1024 * 1024;
   static constexpr int NC0 = (SMEM_MAX - 1024) / WARP_SMEM;
-  static constexpr int NC = NC0 > 16 ? 16 : NC0;
+  static constexpr int NC = NC0 > NPAIR ? NPAIR : NC0;  // consumer warps
+  static constexpr int NW = 2 * NC;                     // + one producer warp per consumer
   static constexpr int SMEM = NC * WARP_SMEM + 1024;    // + alignment slack
   static_assert(NC >= 1, "bf16 decode pipeline does not fit shared memory");
   static_assert(G <= 8, "at most 8 query heads per kv head");
@@ -398,51 +409,55 @@ __device__ __forceinline__ uint32_t rotoff(int r, int c, int rot) {
   return (uint32_t)(r * 4 * D + (((c & ~7) | ((c ^ rot) & 7)) << 4));
 }
 
-template <int D, int G, int S>
-__global__ void __launch_bounds__(Bf16Cfg<D, G, S>::NC * 32, 1) decode_bf16_kernel(const __grid_constant__ DecodeArgs a) {
-  using C = Bf16Cfg<D, G, S>;
+template <int D, int G, int S, int NPAIR>
+__global__ void __launch_bounds__(Bf16Cfg<D, G, S, NPAIR>::NW * 32, 1)
+    decode_bf16_kernel(const __grid_constant__ DecodeArgs a) {
+  using C = Bf16Cfg<D, G, S, NPAIR>;
   constexpr int KC = D / 16;  // k16 chunks of the head dim (QK) == m16 tiles of the head dim (PV)
   extern __shared__ unsigned char sm_raw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* wsm = sm + warp * C::WARP_SMEM;
-  const uint32_t wsm_u = smem_u32(wsm);
-  StageDesc* desc = reinterpret_cast<StageDesc*>(wsm + C::OFF_DESC);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(wsm + C::OFF_BAR);
-  int32_t* meta = reinterpret_cast<int32_t*>(wsm + C::OFF_META);
-  float* pt = reinterpret_cast<float*>(wsm + C::OFF_PT);
-  double* st = reinterpret_cast<double*>(wsm + C::OFF_ST);
   const int W = (int)(a.dhi - a.dlo);
   const int total = (int)(a.n_dense_items + (int64_t)a.item_off[2 * a.B * a.Hkv + 1]);
-  const unsigned char* Qg = reinterpret_cast<const unsigned char*>(a.q);
-  const int g4 = lane >> 2, t4 = lane & 3;      // mma groupID / thread-in-group
-  const int hA = 2 * t4, hB = 2 * t4 + 1;       // query heads of this lane's fragment columns
-  const float scale = (float)a.scale;
-  if (lane < S) mbar_init(&bar[lane], 1);
-  fence_mbar_init();
-  __syncwarp();
-  TL(unsigned long long* tl = g_tl + ((int64_t)blockIdx.x * C::NC + warp) * TL_SLOTS;
-     unsigned long long tl_merge = 0, tl_wait = 0, tl_sub = 0, tl_items = 0, tl_qk = 0, tl_pv = 0, tl_v = 0,
-                        tl_issue = 0, tl_tma = 0, tl_nmerge = 0, tl_sm = 0, tl_epi = 0, tl_mask = 0,
-                        tl_smax = 0, tl_end = 0;
-     if (lane == 0) tl[0] = gtimer(););
+  if (warp < C::NC) {  // each consumer warp initialises its own ring's barriers
+    unsigned char* wsm = sm + warp * C::WARP_SMEM;
+    if (lane < S) {
+      mbar_init(reinterpret_cast<uint64_t*>(wsm + C::OFF_FULL) + lane, 1);
+      mbar_init(reinterpret_cast<uint64_t*>(wsm + C::OFF_EMPTY) + lane, 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
 
-  Cursor cur;
-  cur.nxt = 0;
-  if (lane == 0) cur.nxt = atomicAdd(a.counter, 1);
-  cur.item = -1;
-  cur.row = cur.hi = cur.lo = cur.bk = cur.dense = 0;
-  StageDesc pend = cursor_next(cur, a, total, W, lane);
-  int32_t pend_ent = sub_entry<G>(pend, a, lane);
-
-  // Place the pending sub-chunk into stage slot s (TMA gathers of its K|V
-  // rows, plus the item's queries on its first sub-chunk) and advance.
-  auto issue = [&](int s) {
-    const StageDesc d = pend;
-    const int32_t ent = pend_ent;
-    if (lane == 0) desc[s] = d;
-    meta[s * SUB + lane] = ent;
-    if (d.item >= 0) {
+  if (warp >= C::NC) {
+    // ================================================================ producer
+    // serves consumer warp (warp - NC): its work cursor, its ring's stages
+    unsigned char* cw = sm + (warp - C::NC) * C::WARP_SMEM;
+    const uint32_t cw_u = smem_u32(cw);
+    const unsigned char* Qg = reinterpret_cast<const unsigned char*>(a.q);
+    StageDesc* cdesc = reinterpret_cast<StageDesc*>(cw + C::OFF_DESC);
+    int32_t* cmeta = reinterpret_cast<int32_t*>(cw + C::OFF_META);
+    uint64_t* cfull = reinterpret_cast<uint64_t*>(cw + C::OFF_FULL);
+    uint64_t* cempty = reinterpret_cast<uint64_t*>(cw + C::OFF_EMPTY);
+    Cursor cur;
+    cur.nxt = 0;
+    if (lane == 0) cur.nxt = atomicAdd(a.counter, 1);
+    cur.item = -1;
+    cur.row = cur.hi = cur.lo = cur.bk = cur.dense = 0;
+    StageDesc pend = cursor_next(cur, a, total, W, lane);
+    int32_t pend_ent = sub_entry<G>(pend, a, lane);
+    for (int k = 0;; ++k) {
+      const int s = k % S;
+      if (k >= S) mbar_wait(&cempty[s], ((k / S) - 1) & 1);
+      const StageDesc d = pend;
+      const int32_t ent = pend_ent;
+      if (lane == 0) cdesc[s] = d;
+      cmeta[s * SUB + lane] = ent;
+      __syncwarp();  // desc/meta stores before lane 0's (release) arrive
+      if (d.item < 0) {
+        if (lane == 0) mbar_arrive(&cfull[s]);  // wake the consumer: no more work
+        break;
+      }
       const int pos = ent & 0xffffff;
       const int rg = lane & 7;  // 4-row group of this lane's gather4 op
       const int rowbase = d.bk * (int)a.T;
@@ -450,35 +465,38 @@ __global__ void __launch_bounds__(Bf16Cfg<D, G, S>::NC * 32, 1) decode_bf16_kern
       const int q1 = __shfl_sync(FULL, pos, rg * 4 + 1);
       const int q2 = __shfl_sync(FULL, pos, rg * 4 + 2);
       const int q3 = __shfl_sync(FULL, pos, rg * 4 + 3);
-      if (lane == 0) mbar_expect_tx(&bar[s], C::STAGE + (d.first ? C::QB : 0));
+      if (lane == 0) mbar_expect_tx(&cfull[s], C::STAGE + (d.first ? C::QB : 0));
       __syncwarp();
-      TL(long long i0 = clock64();)
-#ifdef HGCA_BULK_ROWS
-      // experiment: one 1-D bulk copy per row pair (no tensor map)
-      {
-        const unsigned char* src = reinterpret_cast<const unsigned char*>(a.KV) +
-                                   ((int64_t)d.bk * a.T + pos) * (int64_t)(2 * C::ROWB);
-        asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-                     ::"r"(wsm_u + s * C::STAGE + lane * 2 * C::ROWB), "l"(src), "r"(2 * C::ROWB),
-                     "r"(smem_u32(&bar[s])) : "memory");
-      }
-#else
       if (lane < C::NOPS)
-        tma_gather4(wsm_u + s * C::STAGE + rg * 4 * 2 * C::ROWB, &a.kmap, 0, rowbase + q0, rowbase + q1,
-                    rowbase + q2, rowbase + q3, &bar[s]);
-#endif
-      TL(tl_tma += clock64() - i0;)
+        tma_gather4(cw_u + s * C::STAGE + rg * 4 * 2 * C::ROWB, &a.kmap, 0, rowbase + q0, rowbase + q1,
+                    rowbase + q2, rowbase + q3, &cfull[s]);
       if (lane == 0 && d.first) {
         const int64_t b = d.bk / a.Hkv, kvh = d.bk % a.Hkv;
-        bulk_g2s(wsm + C::OFF_Q + s * C::QSLOT, Qg + (b * a.Hq + kvh * G) * (int64_t)C::ROWB, C::QB, &bar[s]);
+        bulk_g2s(cw + C::OFF_Q + s * C::QSLOT, Qg + (b * a.Hq + kvh * G) * (int64_t)C::ROWB, C::QB, &cfull[s]);
       }
+      pend = cursor_next(cur, a, total, W, lane);
+      pend_ent = sub_entry<G>(pend, a, lane);
     }
-    pend = cursor_next(cur, a, total, W, lane);
-    pend_ent = sub_entry<G>(pend, a, lane);
-  };
+    return;
+  }
 
-#pragma unroll
-  for (int s = 0; s < S; ++s) issue(s);
+  // ================================================================== consumer
+  unsigned char* wsm = sm + warp * C::WARP_SMEM;
+  const uint32_t wsm_u = smem_u32(wsm);
+  StageDesc* desc = reinterpret_cast<StageDesc*>(wsm + C::OFF_DESC);
+  uint64_t* full = reinterpret_cast<uint64_t*>(wsm + C::OFF_FULL);
+  uint64_t* empty = reinterpret_cast<uint64_t*>(wsm + C::OFF_EMPTY);
+  int32_t* meta = reinterpret_cast<int32_t*>(wsm + C::OFF_META);
+  float* pt = reinterpret_cast<float*>(wsm + C::OFF_PT);
+  double* st = reinterpret_cast<double*>(wsm + C::OFF_ST);
+  const int g4 = lane >> 2, t4 = lane & 3;      // mma groupID / thread-in-group
+  const int hA = 2 * t4, hB = 2 * t4 + 1;       // query heads of this lane's fragment columns
+  const float scale = (float)a.scale;
+  TL(unsigned long long* tl = g_tl + ((int64_t)blockIdx.x * C::NC + warp) * TL_SLOTS;
+     unsigned long long tl_merge = 0, tl_wait = 0, tl_sub = 0, tl_items = 0, tl_qk = 0, tl_pv = 0, tl_v = 0,
+                        tl_issue = 0, tl_tma = 0, tl_nmerge = 0, tl_sm = 0, tl_epi = 0, tl_mask = 0,
+                        tl_smax = 0, tl_end = 0;
+     if (lane == 0) tl[0] = gtimer(););
 
   // per-item state (fragment layout: this lane owns heads hA, hB)
   uint32_t qf[KC][2];
@@ -487,16 +505,15 @@ __global__ void __launch_bounds__(Bf16Cfg<D, G, S>::NC * 32, 1) decode_bf16_kern
 
   for (int k = 0;; ++k) {
     const int s = k % S;
-    __syncwarp();
     TL(long long c0 = clock64();)
+    mbar_wait(&full[s], (k / S) & 1);
     const StageDesc d = desc[s];
     if (d.item < 0) break;
-    mbar_wait(&bar[s], (k / S) & 1);
     TL(long long c1 = clock64(); tl_wait += c1 - c0; ++tl_sub;)
 #ifdef HGCA_NOCOMPUTE
     // experiment: data movement only (results are garbage)
     __syncwarp();
-    issue(s);
+    if (lane == 0) mbar_arrive(&empty[s]);
     continue;
 #endif
     const uint32_t stg = wsm_u + s * C::STAGE;
@@ -648,12 +665,10 @@ __global__ void __launch_bounds__(Bf16Cfg<D, G, S>::NC * 32, 1) decode_bf16_kern
     }
     __syncwarp();
     TL(long long c5 = clock64(); tl_end += c5 - c4b;)
-    issue(s);
-    TL(tl_issue += clock64() - c5;)
+    if (lane == 0) mbar_arrive(&empty[s]);  // stage consumed: the producer may refill it
   }
-  TL(if (lane == 0) tl[17] = gtimer();)
   TL(if (lane == 0) {
-    tl[1] = gtimer();
+    tl[1] = gtimer(); tl[17] = tl[1];
     tl[2] = tl_merge; tl[3] = tl_wait; tl[4] = tl_sub; tl[5] = tl_items; tl[6] = tl_qk; tl[7] = tl_pv;
     tl[8] = tl_v; tl[9] = tl_issue; tl[10] = tl_tma; tl[11] = tl_mask; tl[12] = tl_sm; tl[13] = tl_epi;
     tl[14] = tl_smax; tl[15] = tl_end; tl[16] = blockIdx.x;
@@ -1247,10 +1262,10 @@ static int launch_decode_t(const DecodeArgs& a_in, cudaStream_t s) {
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   static bool attr = false;
   if constexpr (BF16) {
-    using C = Bf16Cfg<D, G, HGCA_BF16_STAGES>;
-    const int rc = set_smem(decode_bf16_kernel<D, G, HGCA_BF16_STAGES>, C::SMEM, attr);
+    using C = Bf16Cfg<D, G, HGCA_BF16_STAGES, HGCA_BF16_PAIRS>;
+    const int rc = set_smem(decode_bf16_kernel<D, G, HGCA_BF16_STAGES, HGCA_BF16_PAIRS>, C::SMEM, attr);
     if (rc) return rc;
-    decode_bf16_kernel<D, G, HGCA_BF16_STAGES><<<nsm, C::NC * 32, C::SMEM, s>>>(a);
+    decode_bf16_kernel<D, G, HGCA_BF16_STAGES, HGCA_BF16_PAIRS><<<nsm, C::NW * 32, C::SMEM, s>>>(a);
   } else {
     using C = F32Cfg<D, G>;
     const int rc = set_smem(decode_f32_kernel<D, G>, C::SMEM, attr);
@@ -1343,7 +1358,7 @@ int launch_write_rows(int dtype, void* KV, int64_t BH, int64_t T, int64_t D, int
 template <bool BF16, int D, int G>
 static void cfg_of(int64_t* o) {
   if constexpr (BF16) {
-    using C = Bf16Cfg<D, G, HGCA_BF16_STAGES>;
+    using C = Bf16Cfg<D, G, HGCA_BF16_STAGES, HGCA_BF16_PAIRS>;
     o[0] = C::NC; o[1] = C::WARP_SMEM; o[2] = HGCA_BF16_STAGES; o[3] = SUB; o[4] = C::SMEM;
   } else {
     using C = F32Cfg<D, G>;
