@@ -156,6 +156,9 @@ typedef struct hgca_decode_desc {
   int64_t B, Hq, Hkv, D, T; /* batch, query heads, kv heads, head_dim, positions (T < 2^24) */
   const void* KV;           /* [B*Hkv, T, 2, D]: K row then V row per position */
   const void* q;            /* [B*Hq, D] this step's queries (storage dtype) */
+  const void* k_new;        /* optional [B*Hkv, D] kv_in keys: written into KV at position dhi-1
+                               by the kernel itself (else the caller stored them, hgca_write_rows) */
+  const void* v_new;        /* optional [B*Hkv, D] kv_in values (with k_new) */
   double scale;
   int64_t dlo, dhi;         /* dense positions [dlo, dhi): window + kv_in */
   int64_t w_old;            /* window entries before this step (EMA'd) */

@@ -30,7 +30,7 @@ class DecodeDesc(ctypes.Structure):
     _fields_ = [
         ("dtype", ctypes.c_int32), ("pad0", ctypes.c_int32),
         ("B", I64), ("Hq", I64), ("Hkv", I64), ("D", I64), ("T", I64),
-        ("KV", P), ("q", P),
+        ("KV", P), ("q", P), ("k_new", P), ("v_new", P),
         ("scale", D),
         ("dlo", I64), ("dhi", I64), ("w_old", I64),
         ("sparse_rows", I64),

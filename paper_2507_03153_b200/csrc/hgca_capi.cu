@@ -321,7 +321,9 @@ static int decode_prepare(const hgca_decode_desc* d, DecodeArgs& a, DecodeMergeA
     return fail(HGCA_EINVAL, "decode_step: null pointer");
   if (!(d->alpha >= 0.0 && d->alpha <= 1.0)) return fail(HGCA_EINVAL, "alpha must be in [0, 1], got %g", d->alpha);
   a = DecodeArgs{};
+  if ((d->k_new == nullptr) != (d->v_new == nullptr)) return fail(HGCA_EINVAL, "decode_step: k_new and v_new go together");
   a.KV = d->KV; a.q = d->q;
+  a.k_new = d->k_new; a.v_new = d->v_new;
   a.B = d->B; a.Hq = d->Hq; a.Hkv = d->Hkv; a.G = G; a.D = d->D; a.T = d->T;
   a.scale = d->scale;
   a.dlo = d->dlo; a.dhi = d->dhi;

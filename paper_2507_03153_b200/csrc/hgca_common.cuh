@@ -37,6 +37,11 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 }
+// Order this thread's prior generic-proxy global writes before its later
+// async-proxy (TMA) accesses.
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+}
 // Arrive-on triggered when all prior cp.async of this thread have landed; the
 // barrier's expected count includes this arrival (.noinc).
 __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {

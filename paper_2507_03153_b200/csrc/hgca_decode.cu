@@ -161,6 +161,26 @@ __device__ __forceinline__ StageDesc cursor_next(Cursor& c, const DecodeArgs& a,
   return d;
 }
 
+// kv_in (engine.py:161-163, append_kv kv_cache.py:122-169): the step's new K
+// and V rows of (batch, kv-head) bk are written at position dhi-1 by the warp
+// that issues the dense sub-chunk holding that row, right before its gather
+// (generic-proxy stores fenced before the async-proxy TMA read). bf16 rows are
+// stored position-rotated (see rotoff). Every lane writes 16-byte chunks.
+template <int D, bool BF16>
+__device__ __forceinline__ void write_new_row(const DecodeArgs& a, const StageDesc& d, int lane) {
+  if (!a.k_new || !d.dense || d.r0 + d.n != (int)(a.dhi - a.dlo)) return;
+  constexpr int ROWB = D * (BF16 ? 2 : 4), CH = 2 * ROWB / 16;  // 16-byte chunks of the K|V row pair
+  const int64_t pos = a.dhi - 1;
+  unsigned char* dst = reinterpret_cast<unsigned char*>(const_cast<void*>(a.KV)) + ((int64_t)d.bk * a.T + pos) * 2 * ROWB;
+  for (int c = lane; c < CH; c += 32) {
+    const unsigned char* src = reinterpret_cast<const unsigned char*>(c < CH / 2 ? a.k_new : a.v_new) +
+                               (int64_t)d.bk * ROWB + (c % (CH / 2)) * 16;
+    const int pc = BF16 ? ((c & ~7) | ((c ^ (int)pos) & 7)) : c;
+    *reinterpret_cast<uint4*>(dst + pc * 16) = *reinterpret_cast<const uint4*>(src);
+  }
+  fence_proxy_async_global();
+}
+
 // Union entry of lane's row of sub-chunk d: position | (query-head mask << 24).
 // Rows past the sub-chunk end get position 0 and an empty mask.
 template <int G>
@@ -458,6 +478,7 @@ __global__ void __launch_bounds__(Bf16Cfg<D, G, S, NPAIR>::NW * 32, 1)
         if (lane == 0) mbar_arrive(&cfull[s]);  // wake the consumer: no more work
         break;
       }
+      write_new_row<D, true>(a, d, lane);
       const int pos = ent & 0xffffff;
       const int rg = lane & 7;  // 4-row group of this lane's gather4 op
       const int rowbase = d.bk * (int)a.T;
@@ -739,6 +760,7 @@ __global__ void __launch_bounds__(F32Cfg<D, G>::NC * 32, 1) decode_f32_kernel(co
     if (lane == 0) desc[s] = d;
     meta[s * SUB + lane] = ent;
     if (d.item >= 0) {
+      write_new_row<D, false>(a, d, lane);
       const int pos = ent & 0xffffff;
       const int rg = lane & 7;
       const int rowbase = d.bk * (int)a.T;

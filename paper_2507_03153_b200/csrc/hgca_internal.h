@@ -63,6 +63,8 @@ struct DecodeArgs {
   CUtensorMap kmap;       // row map over KV [B*Hkv*T rows, 2D] for TMA gather4, set by the launcher
   const void* KV;         // [B*Hkv, T, 2, D] storage dtype: K row then V row per position
   const void* q;          // [B*Hq, D] storage dtype (decode: one query row)
+  const void* k_new;      // optional [B*Hkv, D] kv_in rows written at position dhi-1 by the kernel
+  const void* v_new;
   int64_t B, Hq, Hkv, G, D, T;
   double scale;
   int64_t dlo, dhi;       // dense positions [dlo, dhi)

@@ -182,6 +182,7 @@ class LayerState:
         self.item_tab = torch.zeros((B * Hkv * (-(-4 * T // SPARSE_ROWS) + 2), 4), dtype=torch.int32, device=dev)
         self.lo = 0    # archive size
         self.nxt = 0   # next position
+        self.desc = None  # cached hgca_decode_desc (engine-owned)
         self.keep = None
         if cfg.shard_world > 1:
             # ownership bits: archive block j (positions [j*blk, (j+1)*blk)) lives on rank j % world
@@ -251,7 +252,6 @@ class HybridEngine:
         self.part_z = torch.empty(self.max_items * self.G, dtype=torch.float64, device=self.dev)
         self.part_acc = torch.empty(self.max_items * self.G * self.D, dtype=torch.float32, device=self.dev)
         self.counter = torch.zeros(4, dtype=torch.int32, device=self.dev)  # decode work counter
-        self._desc = _lib.DecodeDesc()
         self.launches = 0          # kernels of libhgca_b200 launched by this engine
         self.step_events = None     # list -> (start, end) CUDA events around the decode kernel
 
@@ -398,9 +398,8 @@ class HybridEngine:
         s = self._stream()
         if ls.nxt + 1 > self.T:
             raise ContractError("max_positions exceeded")
-        # kv_in lands at position nxt before the dense pass (append_kv's slot)
-        _lib.call("hgca_write_rows", self.dcode, ls.KV.data_ptr(), self.B * self.Hkv,
-                  self.T, self.D, ls.nxt, k.data_ptr(), v.data_ptr(), 1, s)
+        if not (q.is_contiguous() and k.is_contiguous() and v.is_contiguous()) or k.dtype != self.tdtype:
+            raise ContractError("decode_device takes contiguous device tensors in the storage dtype")
         w_size = ls.window_size
         W = w_size + 1
         BHq = self.B * self.Hq
@@ -410,20 +409,25 @@ class HybridEngine:
             lse = torch.empty(BHq, dtype=torch.float64, device=self.dev)
         if wts is None and self.config.keep_weights:
             wts = torch.empty((BHq, W), dtype=torch.float32, device=self.dev)
-        d = self._desc
-        d.dtype = self.dcode
-        d.B, d.Hq, d.Hkv, d.D, d.T = self.B, self.Hq, self.Hkv, self.D, self.T
-        d.KV, d.q = ls.KV.data_ptr(), q.data_ptr()
-        d.scale = float(self.shape.scale)
+        d = ls.desc
+        if d is None:  # per-layer descriptor: the static fields once
+            d = ls.desc = _lib.DecodeDesc()
+            d.dtype = self.dcode
+            d.B, d.Hq, d.Hkv, d.D, d.T = self.B, self.Hq, self.Hkv, self.D, self.T
+            d.KV = ls.KV.data_ptr()
+            d.scale = float(self.shape.scale)
+            d.sparse_rows = SPARSE_ROWS
+            d.u_ent, d.u_cnt, d.item_off = ls.u_ent.data_ptr(), ls.u_cnt.data_ptr(), ls.item_off.data_ptr()
+            d.item_tab = ls.item_tab.data_ptr()
+            d.dsc, d.dsc_ld = self.dsc.data_ptr(), self.dsc_ld
+            d.part_m, d.part_z, d.part_acc = self.part_m.data_ptr(), self.part_z.data_ptr(), self.part_acc.data_ptr()
+            d.max_items = self.max_items
+            d.counter = self.counter.data_ptr()
+            d.maw, d.alpha = ls.maw.data_ptr(), float(self.config.cache.alpha)
+        # per step: the queries, kv_in (the kernel writes it at position nxt, append_kv's slot,
+        # before the dense pass), the window range and the outputs
+        d.q, d.k_new, d.v_new = q.data_ptr(), k.data_ptr(), v.data_ptr()
         d.dlo, d.dhi, d.w_old = ls.lo, ls.nxt + 1, w_size
-        d.sparse_rows = SPARSE_ROWS
-        d.u_ent, d.u_cnt, d.item_off = ls.u_ent.data_ptr(), ls.u_cnt.data_ptr(), ls.item_off.data_ptr()
-        d.item_tab = ls.item_tab.data_ptr()
-        d.dsc, d.dsc_ld = self.dsc.data_ptr(), self.dsc_ld
-        d.part_m, d.part_z, d.part_acc = self.part_m.data_ptr(), self.part_z.data_ptr(), self.part_acc.data_ptr()
-        d.max_items = self.max_items
-        d.counter = self.counter.data_ptr()
-        d.maw, d.alpha = ls.maw.data_ptr(), float(self.config.cache.alpha)
         d.out, d.lse = out.data_ptr(), lse.data_ptr()
         d.wts_out = wts.data_ptr() if wts is not None else None
         d.out_sparse = out_sparse.data_ptr() if out_sparse is not None else None
@@ -437,7 +441,7 @@ class HybridEngine:
             _lib.call("hgca_decode_step", d, s)
             e1.record()
             self.step_events.append((e0, e1))
-        self.launches += 3  # write_rows, decode kernel, merge kernel
+        self.launches += 2  # decode kernel (writes kv_in), merge kernel
         self._last_dense_positions = np.arange(ls.lo, ls.nxt + 1, dtype=np.int64)
         # maintenance after the merge (engine.py:175-191): EMA + init done in
         # the merge kernel; eviction/offload here; append_kv = the position move.
