@@ -22,6 +22,7 @@
  *   hgca_maw_update            WindowCache.update_maw / StoreTier.reevaluate kv_cache.py:171-187, sparsifier.py:158-177
  *   hgca_union_build           (device layout of the context cache for the decode kernel)
  *   hgca_decode_step           HybridEngine._run_step, decode mode engine.py:151-195
+ *   hgca_decode_step_host      the same step with host q|k|v in / out|lse back (one call)
  *   hgca_merge_partials        P-way merge of sharded (out, lse) partials
  *   hgca_merge_packed          P-way merge of the allgathered packed partials
  */
@@ -190,6 +191,13 @@ typedef struct hgca_decode_desc {
  * (programmatic dependent launch; folds the partials in item order and
  * applies merge_states). */
 int hgca_decode_step(const hgca_decode_desc* desc, hgca_stream_t stream);
+
+/* End-to-end step from HOST buffers (pinned): copy in_bytes of in_host to
+ * in_dev (the caller points desc->q / k_new / v_new into in_dev), run the
+ * step, copy out_bytes of out_dev (desc->out / lse point into it) back to
+ * out_host, and synchronize the stream. One call per decode step. */
+int hgca_decode_step_host(const hgca_decode_desc* desc, const void* in_host, void* in_dev, int64_t in_bytes,
+                          void* out_host, const void* out_dev, int64_t out_bytes, hgca_stream_t stream);
 
 #ifdef __cplusplus
 }

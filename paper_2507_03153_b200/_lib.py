@@ -66,6 +66,7 @@ _SIGS = {
     "hgca_maw_update": [P, I64, I64, I64, I64, P, I64, I64, I64, D, I32, P],
     "hgca_union_build": [P, I64, I64, I64, I64, I64, I64, P, P, P, P, I64, I32, P],
     "hgca_decode_step": [ctypes.POINTER(DecodeDesc), P],
+    "hgca_decode_step_host": [ctypes.POINTER(DecodeDesc), P, P, I64, P, P, I64, P],
 }
 _RESTYPES = {"hgca_last_error": ctypes.c_char_p, "hgca_attend_ws_bytes": I64}
 

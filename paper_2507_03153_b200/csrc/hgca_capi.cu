@@ -347,6 +347,31 @@ static int decode_prepare(const hgca_decode_desc* d, DecodeArgs& a, DecodeMergeA
   return HGCA_OK;
 }
 
+int hgca_decode_step_host(const hgca_decode_desc* d, const void* in_host, void* in_dev, int64_t in_bytes,
+                          void* out_host, const void* out_dev, int64_t out_bytes, hgca_stream_t stream) {
+  if (in_bytes < 0 || out_bytes < 0 || (in_bytes && (!in_host || !in_dev)) || (out_bytes && (!out_host || !out_dev)))
+    return fail(HGCA_EINVAL, "decode_step_host: bad staging buffers");
+  DecodeArgs a;
+  DecodeMergeArgs m;
+  int rc = decode_prepare(d, a, m);
+  if (rc) return rc;
+  a.m = m;
+  cudaStream_t s = S(stream);
+  if (in_bytes) {
+    rc = cuda_status((int)cudaMemcpyAsync(in_dev, in_host, (size_t)in_bytes, cudaMemcpyHostToDevice, s),
+                     "decode_step_host: H2D");
+    if (rc) return rc;
+  }
+  rc = cuda_status(launch_decode_partial(d->dtype, a, s), "decode_step_host");
+  if (rc) return rc;
+  if (out_bytes) {
+    rc = cuda_status((int)cudaMemcpyAsync(out_host, out_dev, (size_t)out_bytes, cudaMemcpyDeviceToHost, s),
+                     "decode_step_host: D2H");
+    if (rc) return rc;
+  }
+  return cuda_status((int)cudaStreamSynchronize(s), "decode_step_host: sync");
+}
+
 int hgca_decode_step(const hgca_decode_desc* d, hgca_stream_t stream) {
   DecodeArgs a;
   DecodeMergeArgs m;

@@ -386,7 +386,7 @@ class HybridEngine:
         if squeeze:
             o, l = o[0], l[0]
             w = w[0] if w is not None else None
-        return StepOutput(o, l, w, None, self._last_dense_positions)
+        return StepOutput(o, l, w, None, np.arange(*self._last_dense_range, dtype=np.int64))
 
     def decode_device(self, layer_idx, q, k, v, out=None, lse=None, wts=None, out_sparse=None, lse_sparse=None):
         """The decode hot path on device tensors: q [B, Hq, 1, D], k/v
@@ -395,20 +395,36 @@ class HybridEngine:
         out_sparse / lse_sparse (optional) receive the sparse-only partial
         (the per-rank contribution under sequence sharding)."""
         ls = self.layers[layer_idx]
-        s = self._stream()
-        if ls.nxt + 1 > self.T:
-            raise ContractError("max_positions exceeded")
         if not (q.is_contiguous() and k.is_contiguous() and v.is_contiguous()) or k.dtype != self.tdtype:
             raise ContractError("decode_device takes contiguous device tensors in the storage dtype")
-        w_size = ls.window_size
-        W = w_size + 1
         BHq = self.B * self.Hq
         if out is None:
             out = torch.empty((BHq, self.D), dtype=torch.float32, device=self.dev)
         if lse is None:
             lse = torch.empty(BHq, dtype=torch.float64, device=self.dev)
         if wts is None and self.config.keep_weights:
-            wts = torch.empty((BHq, W), dtype=torch.float32, device=self.dev)
+            wts = torch.empty((BHq, ls.window_size + 1), dtype=torch.float32, device=self.dev)
+        d = self._step_desc(ls, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), lse.data_ptr(),
+                            wts.data_ptr() if wts is not None else None,
+                            out_sparse.data_ptr() if out_sparse is not None else None,
+                            lse_sparse.data_ptr() if lse_sparse is not None else None)
+        s = self._stream()
+        if self.step_events is None:
+            _lib.call("hgca_decode_step", d, s)
+        else:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            _lib.call("hgca_decode_step", d, s)
+            e1.record()
+            self.step_events.append((e0, e1))
+        self._step_done(ls)
+        return out, lse, wts
+
+    def _step_desc(self, ls, q, k, v, out, lse, wts=None, out_sparse=None, lse_sparse=None):
+        """Fill the layer's cached hgca_decode_desc for this step (raw device pointers)."""
+        if ls.nxt + 1 > self.T:
+            raise ContractError("max_positions exceeded")
         d = ls.desc
         if d is None:  # per-layer descriptor: the static fields once
             d = ls.desc = _lib.DecodeDesc()
@@ -426,30 +442,50 @@ class HybridEngine:
             d.maw, d.alpha = ls.maw.data_ptr(), float(self.config.cache.alpha)
         # per step: the queries, kv_in (the kernel writes it at position nxt, append_kv's slot,
         # before the dense pass), the window range and the outputs
-        d.q, d.k_new, d.v_new = q.data_ptr(), k.data_ptr(), v.data_ptr()
-        d.dlo, d.dhi, d.w_old = ls.lo, ls.nxt + 1, w_size
-        d.out, d.lse = out.data_ptr(), lse.data_ptr()
-        d.wts_out = wts.data_ptr() if wts is not None else None
-        d.out_sparse = out_sparse.data_ptr() if out_sparse is not None else None
-        d.lse_sparse = lse_sparse.data_ptr() if lse_sparse is not None else None
-        if self.step_events is None:
-            _lib.call("hgca_decode_step", d, s)
-        else:
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record()
-            _lib.call("hgca_decode_step", d, s)
-            e1.record()
-            self.step_events.append((e0, e1))
+        d.q, d.k_new, d.v_new = q, k, v
+        d.dlo, d.dhi, d.w_old = ls.lo, ls.nxt + 1, ls.nxt - ls.lo
+        d.out, d.lse, d.wts_out = out, lse, wts
+        d.out_sparse, d.lse_sparse = out_sparse, lse_sparse
+        return d
+
+    def _step_done(self, ls):
+        """Host bookkeeping after a launched decode step (engine.py:175-191): the
+        MAW EMA / init ran in the kernel; eviction -> ingest here; append_kv is
+        the position move."""
         self.launches += 2  # decode kernel (writes kv_in), merge kernel
-        self._last_dense_positions = np.arange(ls.lo, ls.nxt + 1, dtype=np.int64)
-        # maintenance after the merge (engine.py:175-191): EMA + init done in
-        # the merge kernel; eviction/offload here; append_kv = the position move.
+        self._last_dense_range = (ls.lo, ls.nxt + 1)
+        w_size = ls.window_size
         ev_lo, ev_hi = self._evict_range(ls, 1)
         ls.nxt += 1
         if ev_hi > ev_lo:
             self._ingest(ls, ev_lo, ev_hi, w_size + 1)
-        return out, lse, wts
+
+    def decode_host_packed(self, layer_idx, in_host, out_host, staging=None):
+        """End-to-end decode in ONE library call: in_host is a pinned buffer
+        holding q [B,Hq,D] | k [B,Hkv,D] | v [B,Hkv,D] in the storage dtype back
+        to back; out_host a pinned uint8 buffer of B*Hq*(4*D + 8) bytes that
+        receives out f32 [B*Hq, D] followed by lse f64 [B*Hq].
+        hgca_decode_step_host copies in, runs the step, copies out and
+        synchronizes (the host owns the result on return)."""
+        B, Hq, Hkv, D = self.B, self.Hq, self.Hkv, self.D
+        nq, nk = B * Hq * D, B * Hkv * D
+        if in_host.numel() != nq + 2 * nk or in_host.dtype != self.tdtype:
+            raise ContractError("in_host must hold q | k | v in the storage dtype")
+        nout = B * Hq * (4 * D + 8)
+        if out_host.numel() != nout or out_host.dtype != torch.uint8:
+            raise ContractError(f"out_host must be a uint8 buffer of {nout} bytes")
+        if staging is None:
+            staging = (torch.empty(nq + 2 * nk, dtype=self.tdtype, device=self.dev),
+                       torch.empty(nout, dtype=torch.uint8, device=self.dev))
+        dev_in, dev_out = staging
+        ls = self.layers[layer_idx]
+        e = self.tdtype.itemsize
+        pi, po = dev_in.data_ptr(), dev_out.data_ptr()
+        d = self._step_desc(ls, pi, pi + nq * e, pi + (nq + nk) * e, po, po + B * Hq * D * 4)
+        _lib.call("hgca_decode_step_host", d, in_host.data_ptr(), pi, (nq + 2 * nk) * e, out_host.data_ptr(), po,
+                  nout, self._stream())
+        self._step_done(ls)
+        return out_host
 
     def decode_host(self, layer_idx, q_host, k_host, v_host, out_host, lse_host, staging=None):
         """End-to-end decode through the C ABI with HOST buffers: pinned

@@ -95,6 +95,23 @@ class ShardedHybridEngine(HybridEngine):
         self.launches += 1
         return out, lse
 
+    def decode_host_packed(self, layer_idx, in_host, out_host, staging=None):
+        """End-to-end decode with host buffers (as HybridEngine.decode_host_packed),
+        through the sharded step: H2D, this rank's partial, all-gather, merge, D2H."""
+        B, Hq, Hkv, D = self.B, self.Hq, self.Hkv, self.D
+        nq, nk = B * Hq * D, B * Hkv * D
+        if staging is None:
+            staging = (torch.empty(nq + 2 * nk, dtype=self.tdtype, device=self.dev),
+                       torch.empty(B * Hq * (4 * D + 8), dtype=torch.uint8, device=self.dev))
+        dev_in, dev_out = staging
+        dev_in.copy_(in_host, non_blocking=True)
+        out = dev_out[: B * Hq * D * 4].view(torch.float32).view(B * Hq, D)
+        lse = dev_out[B * Hq * D * 4:].view(torch.float64)
+        self.decode_device(layer_idx, dev_in[:nq], dev_in[nq:nq + nk], dev_in[nq + nk:], out=out, lse=lse)
+        out_host.copy_(dev_out, non_blocking=True)
+        torch.cuda.current_stream(self.dev).synchronize()
+        return out_host
+
     def decode_device(self, layer_idx, q, k, v, out=None, lse=None, wts=None, out_sparse=None, lse_sparse=None):
         if out_sparse is not None or lse_sparse is not None:
             raise ContractError("the sharded engine owns the sparse partial buffers")

@@ -273,3 +273,31 @@ def test_bf16_rows_rotated_and_union_classes(cuda):
         n_min = classes.min()
         groups = (p[: 8 * n_min] % 8).reshape(-1, 8)
         assert (np.sort(groups, axis=1) == np.arange(8)).all()
+
+
+def test_decode_host_packed_matches_device_path(cuda):
+    """The end-to-end host-buffer entry point (one H2D of q|k|v, one D2H of
+    out|lse) computes exactly what the device-tensor path computes."""
+    outs = []
+    for packed in (False, True):
+        eng, g, tdt = _big_engine(cuda, "bfloat16", B=2, ctx=2048, seed=21)
+        B, Hq, Hkv, D = eng.B, eng.Hq, eng.Hkv, eng.D
+        res = []
+        for _ in range(40):  # crosses an eviction + re-selection
+            q = torch.randn((B, Hq, 1, D), generator=g, device="cuda").to(tdt)
+            k = torch.randn((B, Hkv, 1, D), generator=g, device="cuda").to(tdt)
+            v = torch.randn((B, Hkv, 1, D), generator=g, device="cuda").to(tdt)
+            if packed:
+                in_h = torch.cat([q.reshape(-1), k.reshape(-1), v.reshape(-1)]).cpu().pin_memory()
+                out_h = torch.empty(B * Hq * (4 * D + 8), dtype=torch.uint8).pin_memory()
+                eng.decode_host_packed(0, in_h, out_h)
+                o = out_h[: B * Hq * D * 4].view(torch.float32).numpy().copy()
+                l = out_h[B * Hq * D * 4:].view(torch.float64).numpy().copy()
+            else:
+                ot, lt, _ = eng.decode_device(0, q, k, v)
+                o, l = ot.cpu().numpy().ravel(), lt.cpu().numpy()
+            res.append((o, l))
+        outs.append(res)
+    for (o1, l1), (o2, l2) in zip(*outs):
+        np.testing.assert_array_equal(o1, o2)
+        np.testing.assert_array_equal(l1, l2)
