@@ -173,7 +173,7 @@ typedef struct hgca_decode_desc {
   double* part_m;           /* [max_items*G] */
   double* part_z;           /* [max_items*G] */
   float* part_acc;          /* [max_items*G*D] */
-  int64_t max_items;        /* >= B*Hkv*(3 + ceil(4T / sparse_rows)) */
+  int64_t max_items;        /* >= B*Hkv*(ceil((dhi-dlo)/256) + 2 + ceil(4T / sparse_rows)) */
   int32_t* counter;         /* int32 work counter (>= 1 element): zero it once before the first step;
                                every step leaves it 0 again */
   double* maw;              /* [B*Hq, T] or NULL */
@@ -185,11 +185,11 @@ typedef struct hgca_decode_desc {
   double* lse_sparse;       /* optional [B*Hq] */
 } hgca_decode_desc;
 
-/* One decode step = two kernels on `stream`: the decode kernel (one dense
- * item per (batch, kv-head) over the window, which also applies the MAW EMA,
- * + sparse union items -> per-item (m, z, acc) partials) and the merge kernel
- * (programmatic dependent launch; folds the partials in item order and
- * applies merge_states). */
+/* One decode step = two kernels on `stream`: the decode kernel (dense items =
+ * 256-row parts of the window, sparse items = union slices -> per-item
+ * (m, z, acc) partials; it also writes k_new/v_new) and the merge kernel
+ * (programmatic dependent launch; folds the partials in item order, applies
+ * merge_states, the window weights and the MAW EMA). */
 int hgca_decode_step(const hgca_decode_desc* desc, hgca_stream_t stream);
 
 /* End-to-end step from HOST buffers (pinned): copy in_bytes of in_host to

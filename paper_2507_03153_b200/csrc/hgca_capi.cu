@@ -310,7 +310,8 @@ static int decode_prepare(const hgca_decode_desc* d, DecodeArgs& a, DecodeMergeA
   if (d->dlo < 0 || W < 1 || d->dhi > d->T || d->w_old < 0 || d->w_old > W || d->dsc_ld < W)
     return fail(HGCA_EINVAL, "decode_step: bad dense range");
   if (d->sparse_rows < 4 || d->sparse_rows % 4) return fail(HGCA_EINVAL, "decode_step: sparse_rows must be a positive multiple of 4");
-  const int64_t n_dense = d->B * d->Hkv;
+  const int64_t Sd = (W + 255) / 256;  // dense items (window parts of 256 rows) per (batch, kv-head)
+  const int64_t n_dense = d->B * d->Hkv * Sd;
   // every item but the last full and last tail item of a list holds >= sparse_rows/4 rows
   const int64_t max_sparse = d->B * d->Hkv * ((4 * d->T + d->sparse_rows - 1) / d->sparse_rows + 2);
   if (d->max_items < n_dense + max_sparse)
@@ -334,6 +335,7 @@ static int decode_prepare(const hgca_decode_desc* d, DecodeArgs& a, DecodeMergeA
   a.part_m = d->part_m; a.part_z = d->part_z; a.part_acc = d->part_acc;
   a.counter = d->counter;
   a.n_dense_items = n_dense;
+  a.Sd = Sd;
   a.w_old = d->w_old;
   a.maw = d->maw;
   a.one_minus_alpha = 1.0 - d->alpha; a.alpha = d->alpha;

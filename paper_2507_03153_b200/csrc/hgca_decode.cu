@@ -38,6 +38,8 @@
 
 #include <cuda.h>
 
+#include <type_traits>
+
 namespace hgca {
 
 // Debug build only (-DHGCA_TIMELINE): per-warp timeline of the decode kernel,
@@ -51,6 +53,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 #define TL(...) __VA_ARGS__
+__device__ unsigned long long g_tlm[4096 * 8];  // merge kernel: per CTA phase stamps
 #else
 #define TL(...)
 #endif
@@ -63,6 +66,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #endif
 
 constexpr int SUB = 32;  // rows per pipeline stage (one per lane)
+constexpr int DENSE_ROWS = 256;  // window rows per dense work item
 constexpr uint32_t FULL = 0xffffffffu;
 constexpr int SMEM_MAX = 232448;  // dynamic shared memory per CTA on sm_100
 
@@ -84,6 +88,22 @@ __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map
       " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(dst),
       "l"(map), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
       : "memory");
+}
+// Same with an L2 cache policy (the K|V gathers stream through L2 once per
+// step: evict-first keeps the step's small working set -- partials, dense
+// scores, MAW -- resident for the merge kernel).
+__device__ __forceinline__ void tma_gather4_hint(uint32_t dst, const CUtensorMap* map, int col, int r0, int r1,
+                                                 int r2, int r3, uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;\n" ::"r"(dst),
+      "l"(map), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
@@ -116,8 +136,8 @@ __device__ __forceinline__ float bf16_lo_f(uint32_t w) { return __uint_as_float(
 __device__ __forceinline__ float bf16_hi_f(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
 
 // ------------------------------------------------------------------ work items
-// Item ids: [0, B*Hkv) dense (item == bk; window rows [0, W)), then the
-// sparse items of item_tab. The cursor walks a warp through items in
+// Item ids: [0, B*Hkv*Sd) dense (bk = id / Sd; window rows of part id % Sd,
+// DENSE_ROWS each), then the sparse items of item_tab. The cursor walks a warp through items in
 // sub-chunks of SUB rows; lane 0 holds the prefetched id of the next item.
 struct Cursor {
   int nxt;  // lane 0
@@ -135,11 +155,11 @@ __device__ __forceinline__ StageDesc cursor_next(Cursor& c, const DecodeArgs& a,
     }
     c.item = it;
     if (lane == 0) c.nxt = atomicAdd(a.counter, 1);
-    if (it < (int)a.n_dense_items) {
+    if (it < (int)a.n_dense_items) {  // dense item: window rows [part*DR, (part+1)*DR) of bk
       c.dense = 1;
-      c.bk = it;
-      c.lo = 0;
-      c.hi = W;
+      c.bk = it / (int)a.Sd;
+      c.lo = (it % (int)a.Sd) * DENSE_ROWS;
+      c.hi = min(W, c.lo + DENSE_ROWS);
     } else {
       c.dense = 0;
       const int4 e = __ldg(a.item_tab + (it - (int)a.n_dense_items));  // (bk, lo, hi, -)
@@ -190,69 +210,28 @@ __device__ __forceinline__ int32_t sub_entry(const StageDesc& d, const DecodeArg
   return __ldg(a.u_ent + (int64_t)d.bk * a.T + d.r0 + lane);
 }
 
-// ------------------------------------------------------------------ epilogues
-// Dense-item epilogue: weights of the attended window from the stored scores
-// and the item's final (m, z), and the fp64 MAW maintenance:
-//   w   = float32(exp(s - m) / z)                     (_core.pyx:81-82)
-//   maw = (1-alpha)*maw + alpha*w   (3 roundings)     (kv_cache.py:186)
-//   new entries: maw = w                              (engine.py:191)
-// The scores were written by this warp (__syncwarp orders them).
-template <typename SC, int G>
-__device__ void dense_epilogue(const DecodeArgs& a, int bk, const double* m, const double* z, int lane) {
-  if (a.maw == nullptr && a.wts_out == nullptr) return;
-  constexpr int JB = G >= 8 ? 1 : (G >= 4 ? 2 : 8 / G);  // window rows per lane per batch: JB*G loads in flight
-  const int64_t W = a.dhi - a.dlo;
-  const int64_t b = bk / a.Hkv, kvh = bk % a.Hkv;
-  const int64_t bq0 = b * a.Hq + kvh * G;
-  const SC* dsc = reinterpret_cast<const SC*>(a.dsc);
-  for (int64_t j0 = 0; j0 < W; j0 += 32 * JB) {
-    SC sv[JB][G];
-    double mo[JB][G];
-#pragma unroll
-    for (int u = 0; u < JB; ++u) {
-      const int64_t j = j0 + u * 32 + lane;
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        sv[u][g] = j < W ? __ldcg(dsc + (bq0 + g) * a.dsc_ld + j) : (SC)0;
-        mo[u][g] = (a.maw && j < a.w_old) ? a.maw[(bq0 + g) * a.T + a.dlo + j] : 0.0;
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < JB; ++u) {
-      const int64_t j = j0 + u * 32 + lane;
-      if (j >= W) continue;
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const int64_t bq = bq0 + g;
-        const float w32 = !(z[g] > 0.0) ? 0.f : (float)(exp((double)sv[u][g] - m[g]) / z[g]);
-        if (a.wts_out) a.wts_out[bq * W + j] = w32;
-        if (a.maw) {
-          const double aw = (double)w32;
-          a.maw[bq * a.T + a.dlo + j] =
-              j < a.w_old ? __dadd_rn(__dmul_rn(a.one_minus_alpha, mo[u][g]), __dmul_rn(a.alpha, aw)) : aw;
-        }
-      }
-    }
-  }
-}
-
 // ------------------------------------------------------------------ merge kernel
 // One CTA per (batch, kv-head), launched behind the decode kernel with
-// programmatic dependent launch. Its sparse partials are two contiguous item
-// ranges (full items, tail items); they are streamed into shared memory with
-// 1-D TMA bulk copies (chunks of up to MERGE_CHUNK_BYTES, so the fold is not
-// limited by per-SM outstanding L1 misses), then folded per query head in
-// item order: max, one exp per (item, head), weighted sums with threads over
-// (head, dim). Chunks of long lists are combined with an online rescale. Then
-// merge_states(sparse, dense) with the dense item's partial
-// (attention.py:153-188, engine.py:166-169). Fixed order: deterministic.
+// programmatic dependent launch. Its partials are contiguous item ranges
+// (sparse: full items, tail items; dense: the window parts); they are streamed
+// into shared memory with 1-D TMA bulk copies (chunks of up to
+// MERGE_CHUNK_BYTES, so the fold is not limited by per-SM outstanding L1
+// misses) and folded per query head in item order: max, one exp per
+// (item, head), weighted sums with threads over (head, dim); chunks of long
+// lists combine with an online rescale. Then:
+//   * merge_states(sparse, dense)            attention.py:153-188, engine.py:166-169
+//   * window weights w = float32(exp(s - m) / z) from the stored dense
+//     scores and the dense (m, z)            _core.pyx:81-82
+//   * MAW maintenance, 3 separately rounded fp64 ops (kv_cache.py:186), new
+//     entries maw = w (engine.py:177-191).
+// Fixed order throughout: deterministic.
 constexpr int MERGE_CHUNK_BYTES = 192 * 1024;
 
 template <int D, int G>
 struct MergeCfg {
   static constexpr int NT = G * D >= 256 ? 256 : G * D;         // threads
   static constexpr int ROW = G * D * 4;                          // accumulator bytes per item
-  static constexpr int NI = MERGE_CHUNK_BYTES / (ROW + 16 * G);  // items per chunk
+  static constexpr int NI = MERGE_CHUNK_BYTES / (ROW + 24 * G);  // items per chunk
   static constexpr int OFF_M = NI * ROW;                         // part_m [NI][G] fp64
   static constexpr int OFF_Z = OFF_M + NI * G * 8;               // part_z [NI][G] fp64
   static constexpr int OFF_W = OFF_Z + NI * G * 8;               // weights [G][NI] fp64
@@ -262,9 +241,10 @@ struct MergeCfg {
   static_assert(G * D % NT == 0, "merge thread mapping");
 };
 
-template <int D, int G>
-__global__ void __launch_bounds__(MergeCfg<D, G>::NT) decode_merge_kernel(const DecodeMergeArgs m, int32_t* counter) {
+template <int D, int G, typename SC>
+__global__ void __launch_bounds__(MergeCfg<D, G>::NT) decode_merge_kernel(const __grid_constant__ DecodeArgs a) {
   using C = MergeCfg<D, G>;
+  const DecodeMergeArgs& m = a.m;
   extern __shared__ __align__(128) unsigned char msm[];
   float* sacc = reinterpret_cast<float*>(msm);
   double* sm_m = reinterpret_cast<double*>(msm + C::OFF_M);
@@ -274,99 +254,131 @@ __global__ void __launch_bounds__(MergeCfg<D, G>::NT) decode_merge_kernel(const 
   __shared__ double hM[G], hZ[G], hS[G];
   const int64_t bk = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  TL(if (tid == 0) g_tlm[blockIdx.x * 8 + 0] = gtimer();)
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
   }
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  TL(if (tid == 0) g_tlm[blockIdx.x * 8 + 1] = gtimer();)
   // the decode grid is complete: re-arm its work counter for the next step
-  if (blockIdx.x == 0 && tid == 0) *counter = 0;
+  if (blockIdx.x == 0 && tid == 0) *a.counter = 0;
   const int64_t BK = m.B * m.Hkv, nd = m.n_dense_items;
-  const int64_t o0 = m.item_off[bk], o1 = m.item_off[bk + 1];
-  const int64_t t0 = m.item_off[BK + 1 + bk], t1 = m.item_off[BK + 1 + bk + 1];
-  const int64_t na = o1 - o0, n = na + (t1 - t0);
-  if (tid < G) {
-    hM[tid] = -INFINITY;
-    hZ[tid] = 0.0;
-  }
-  // this thread's outputs: (head, dim) = idx / D, idx % D for idx = tid + k*256
-  double acc[C::OPT];
-#pragma unroll
-  for (int k = 0; k < C::OPT; ++k) acc[k] = 0.0;
-  __syncthreads();
-  uint32_t phase = 0;
-  for (int64_t c0 = 0; c0 < n; c0 += C::NI) {
-    const int64_t c1 = min(n, c0 + C::NI), cn = c1 - c0;
-    // items [c0, c1) of the concatenated (full, tail) list: at most two contiguous ranges
-    if (tid == 0) {
-      const int64_t a_lo = c0, a_hi = min(c1, na);              // full-item part
-      const int64_t b_lo = max(c0, na), b_hi = c1;              // tail-item part
-      uint32_t bytes = 0;
-      if (a_hi > a_lo) bytes += (uint32_t)((a_hi - a_lo) * C::ROW);
-      if (b_hi > b_lo) bytes += (uint32_t)((b_hi - b_lo) * C::ROW);
-      mbar_expect_tx(bar, bytes);
-      if (a_hi > a_lo) {
-        const int64_t it = nd + o0 + a_lo, k = a_hi - a_lo, dst = a_lo - c0;
-        bulk_g2s(sacc + dst * G * D, m.part_acc + it * G * D, (uint32_t)(k * C::ROW), bar);
-      }
-      if (b_hi > b_lo) {
-        const int64_t it = nd + t0 + (b_lo - na), k = b_hi - b_lo, dst = b_lo - c0;
-        bulk_g2s(sacc + dst * G * D, m.part_acc + it * G * D, (uint32_t)(k * C::ROW), bar);
-      }
-    }
-    // (m, z) of the chunk's items: plain loads while the bulk copies land
-    for (int64_t x = tid; x < cn * G; x += C::NT) {
-      const int64_t i = c0 + x / G, g = x % G;
-      const int64_t it = i < na ? nd + o0 + i : nd + t0 + (i - na);
-      sm_m[x] = m.part_m[it * G + g];
-      sm_z[x] = m.part_z[it * G + g];
-    }
-    __syncthreads();
-    mbar_wait(bar, phase);
-    phase ^= 1;
-    // per head: chunk max (warp g over items), new running max, weights, z
-    for (int g = wid; g < G; g += C::NT / 32) {
-      double mx = -INFINITY;
-      for (int64_t i = lane; i < cn; i += 32) mx = fmax(mx, sm_m[i * G + g]);
-      mx = warp_max_f64(mx);
-      const double mo = hM[g], mn = fmax(mo, mx);
-      double zl = 0.0;
-      for (int64_t i = lane; i < cn; i += 32) {
-        const double mi = sm_m[i * G + g];
-        const double w = (mi == -INFINITY || mn == -INFINITY) ? 0.0 : exp(mi - mn);
-        sw[g * C::NI + i] = w;
-        zl += sm_z[i * G + g] * w;
-      }
-      zl = warp_sum_f64(zl);
-      if (lane == 0) {
-        const double so = (mo == -INFINITY || mn == -INFINITY) ? 0.0 : exp(mo - mn);
-        hS[g] = so;
-        hZ[g] = hZ[g] * so + zl;
-        hM[g] = mn;
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < C::OPT; ++k) {
-      const int idx = tid + k * C::NT, g = idx / D;
-      double a = acc[k] * hS[g];
-      const double* w = sw + g * C::NI;
-      const float* src = sacc + idx;
-      for (int64_t i = 0; i < cn; ++i) a += w[i] * (double)src[i * G * D];
-      acc[k] = a;
-    }
-    __syncthreads();  // the next chunk's copies overwrite sacc / sw
-  }
-  // merge_states(sparse, dense) per output (head, dim)
   const int64_t b = bk / m.Hkv, kvh = bk % m.Hkv;
+  // window-epilogue operands of the first batch: loaded now, consumed after the folds
+  constexpr int EB = 8;
+  const bool epi = a.maw != nullptr || a.wts_out != nullptr;
+  const int64_t W = a.dhi - a.dlo, n_el = epi ? (int64_t)G * W : 0;
+  const SC* dsc = reinterpret_cast<const SC*>(a.dsc);
+  SC sv[EB];
+  double mo[EB];
+  auto epi_load = [&](int64_t x0) {
+#pragma unroll
+    for (int u = 0; u < EB; ++u) {
+      const int64_t x = x0 + (int64_t)u * C::NT + tid;
+      sv[u] = 0;
+      mo[u] = 0.0;
+      if (x < n_el) {
+        const int g = (int)(x / W);
+        const int64_t j = x - g * W, bq = b * m.Hq + kvh * G + g;
+        sv[u] = dsc[bq * a.dsc_ld + j];
+        if (a.maw && j < a.w_old) mo[u] = a.maw[bq * a.T + a.dlo + j];
+      }
+    }
+  };
+  epi_load(0);
+  uint32_t phase = 0;
+  // fold the items of up to two contiguous ranges [r0, r0+n0), [r1, r1+n1)
+  // (in that order) for every head: fills hM/hZ and this thread's acc
+  auto fold = [&](int64_t r0, int64_t n0, int64_t r1, int64_t n1, double (&acc)[C::OPT]) {
+    const int64_t n = n0 + n1;
+    if (tid < G) {
+      hM[tid] = -INFINITY;
+      hZ[tid] = 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < C::OPT; ++k) acc[k] = 0.0;
+    __syncthreads();
+    for (int64_t c0 = 0; c0 < n; c0 += C::NI) {
+      const int64_t c1 = min(n, c0 + C::NI), cn = c1 - c0;
+      if (tid == 0) {
+        const int64_t a_lo = c0, a_hi = min(c1, n0), b_lo = max(c0, n0), b_hi = c1;
+        uint32_t bytes = 0;
+        if (a_hi > a_lo) bytes += (uint32_t)((a_hi - a_lo) * C::ROW);
+        if (b_hi > b_lo) bytes += (uint32_t)((b_hi - b_lo) * C::ROW);
+        mbar_expect_tx(bar, bytes);
+        if (a_hi > a_lo)
+          bulk_g2s(sacc + (a_lo - c0) * G * D, m.part_acc + (r0 + a_lo) * G * D, (uint32_t)((a_hi - a_lo) * C::ROW),
+                   bar);
+        if (b_hi > b_lo)
+          bulk_g2s(sacc + (b_lo - c0) * G * D, m.part_acc + (r1 + b_lo - n0) * G * D,
+                   (uint32_t)((b_hi - b_lo) * C::ROW), bar);
+      }
+      // (m, z) of the chunk's items: plain loads while the bulk copies land
+      for (int64_t x = tid; x < cn * G; x += C::NT) {
+        const int64_t i = c0 + x / G, g = x % G;
+        const int64_t it = i < n0 ? r0 + i : r1 + (i - n0);
+        sm_m[x] = m.part_m[it * G + g];
+        sm_z[x] = m.part_z[it * G + g];
+      }
+      __syncthreads();
+      mbar_wait(bar, phase);
+      phase ^= 1;
+      for (int g = wid; g < G; g += C::NT / 32) {
+        double mx = -INFINITY;
+        for (int64_t i = lane; i < cn; i += 32) mx = fmax(mx, sm_m[i * G + g]);
+        mx = warp_max_f64(mx);
+        const double mo = hM[g], mn = fmax(mo, mx);
+        double zl = 0.0;
+        for (int64_t i = lane; i < cn; i += 32) {
+          const double mi = sm_m[i * G + g];
+          const double w = (mi == -INFINITY || mn == -INFINITY) ? 0.0 : exp(mi - mn);
+          sw[g * C::NI + i] = w;
+          zl += sm_z[i * G + g] * w;
+        }
+        zl = warp_sum_f64(zl);
+        if (lane == 0) {
+          const double so = (mo == -INFINITY || mn == -INFINITY) ? 0.0 : exp(mo - mn);
+          hS[g] = so;
+          hZ[g] = hZ[g] * so + zl;
+          hM[g] = mn;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < C::OPT; ++k) {
+        const int idx = tid + k * C::NT, g = idx / D;
+        double acc_k = acc[k] * hS[g];
+        const double* w = sw + g * C::NI;
+        const float* src = sacc + idx;
+        for (int64_t i = 0; i < cn; ++i) acc_k += w[i] * (double)src[i * G * D];
+        acc[k] = acc_k;
+      }
+      __syncthreads();  // the next chunk's copies overwrite sacc / sw
+    }
+  };
+  // ---- sparse partials: bk's full items, then its tail items
+  double acc_s[C::OPT], Ms[G], Zs[G];
+  {
+    const int64_t o0 = m.item_off[bk], o1 = m.item_off[bk + 1];
+    const int64_t t0 = m.item_off[BK + 1 + bk], t1 = m.item_off[BK + 1 + bk + 1];
+    fold(nd + o0, o1 - o0, nd + t0, t1 - t0, acc_s);
+#pragma unroll
+    for (int g = 0; g < G; ++g) { Ms[g] = hM[g]; Zs[g] = hZ[g]; }
+    __syncthreads();
+  }
+  TL(if (tid == 0) g_tlm[blockIdx.x * 8 + 2] = gtimer();)
+  // ---- dense partials: the window parts of bk
+  double acc_d[C::OPT];
+  fold(bk * a.Sd, a.Sd, 0, 0, acc_d);
+  TL(if (tid == 0) g_tlm[blockIdx.x * 8 + 3] = gtimer();)
 #pragma unroll
   for (int k = 0; k < C::OPT; ++k) {
     const int idx = tid + k * C::NT, g = idx / D, c = idx % D;
     const int64_t bq = b * m.Hq + kvh * G + g;
-    const double Ms = hM[g], Zs = hZ[g];
-    const bool s_empty = !(Zs > 0.0) || Ms == -INFINITY;
-    const double lse_s = s_empty ? -INFINITY : Ms + log(Zs);
-    const double md = m.part_m[bk * G + g], zd = m.part_z[bk * G + g];
+    const bool s_empty = !(Zs[g] > 0.0) || Ms[g] == -INFINITY;
+    const double lse_s = s_empty ? -INFINITY : Ms[g] + log(Zs[g]);
+    const double md = hM[g], zd = hZ[g];
     const bool d_empty = !(zd > 0.0) || md == -INFINITY;
     const double lse_d = d_empty ? -INFINITY : md + log(zd);
     const double mm = fmax(lse_s, lse_d);
@@ -375,8 +387,8 @@ __global__ void __launch_bounds__(MergeCfg<D, G>::NT) decode_merge_kernel(const 
     const double wa = exp(lse_s - ms), wb = exp(lse_d - ms);
     const double zs = both_empty ? 1.0 : wa + wb;
     const float ca = (float)(wa / zs), cb = (float)(wb / zs);
-    const float os = s_empty ? 0.f : (float)(acc[k] / Zs);
-    const float od = d_empty ? 0.f : (float)((double)m.part_acc[(bk * G + g) * D + c] / zd);
+    const float os = s_empty ? 0.f : (float)(acc_s[k] / Zs[g]);
+    const float od = d_empty ? 0.f : (float)(acc_d[k] / zd);
     m.out[bq * D + c] = __fadd_rn(__fmul_rn(ca, os), __fmul_rn(cb, od));
     if (m.out_sparse) m.out_sparse[bq * D + c] = os;
     if (c == 0) {
@@ -384,6 +396,28 @@ __global__ void __launch_bounds__(MergeCfg<D, G>::NT) decode_merge_kernel(const 
       if (m.lse_sparse) m.lse_sparse[bq] = lse_s;
     }
   }
+  TL(if (tid == 0) g_tlm[blockIdx.x * 8 + 4] = gtimer();)
+  // ---- window weights + MAW maintenance from the stored dense scores
+  // (batches of EB elements per thread; batch 0 was loaded before the folds)
+  for (int64_t x0 = 0; x0 < n_el; x0 += (int64_t)EB * C::NT) {
+    if (x0) epi_load(x0);
+#pragma unroll
+    for (int u = 0; u < EB; ++u) {
+      const int64_t x = x0 + (int64_t)u * C::NT + tid;
+      if (x >= n_el) continue;
+      const int g = (int)(x / W);
+      const int64_t j = x - g * W, bq = b * m.Hq + kvh * G + g;
+      const double md = hM[g], zd = hZ[g];
+      const float w32 = (!(zd > 0.0) || md == -INFINITY) ? 0.f : (float)(exp((double)sv[u] - md) / zd);
+      if (a.wts_out) a.wts_out[bq * W + j] = w32;
+      if (a.maw) {
+        const double aw = (double)w32;
+        a.maw[bq * a.T + a.dlo + j] =
+            j < a.w_old ? __dadd_rn(__dmul_rn(a.one_minus_alpha, mo[u]), __dmul_rn(a.alpha, aw)) : aw;
+      }
+    }
+  }
+  TL(__syncthreads(); if (tid == 0) g_tlm[blockIdx.x * 8 + 5] = gtimer();)
 }
 
 // =========================================================== bf16 (tensor-core) kernel
@@ -448,6 +482,9 @@ __global__ void __launch_bounds__(Bf16Cfg<D, G, S, NPAIR>::NW * 32, 1)
     fence_mbar_init();
   }
   __syncthreads();
+  // let the merge grid launch now: its CTAs take SMs as decode CTAs exit and
+  // wait in griddepcontrol.wait until this whole grid has completed
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 
   if (warp >= C::NC) {
     // ================================================================ producer
@@ -466,6 +503,7 @@ __global__ void __launch_bounds__(Bf16Cfg<D, G, S, NPAIR>::NW * 32, 1)
     cur.row = cur.hi = cur.lo = cur.bk = cur.dense = 0;
     StageDesc pend = cursor_next(cur, a, total, W, lane);
     int32_t pend_ent = sub_entry<G>(pend, a, lane);
+    const uint64_t evict_first = l2_evict_first_policy();
     for (int k = 0;; ++k) {
       const int s = k % S;
       if (k >= S) mbar_wait(&cempty[s], ((k / S) - 1) & 1);
@@ -489,8 +527,8 @@ __global__ void __launch_bounds__(Bf16Cfg<D, G, S, NPAIR>::NW * 32, 1)
       if (lane == 0) mbar_expect_tx(&cfull[s], C::STAGE + (d.first ? C::QB : 0));
       __syncwarp();
       if (lane < C::NOPS)
-        tma_gather4(cw_u + s * C::STAGE + rg * 4 * 2 * C::ROWB, &a.kmap, 0, rowbase + q0, rowbase + q1,
-                    rowbase + q2, rowbase + q3, &cfull[s]);
+        tma_gather4_hint(cw_u + s * C::STAGE + rg * 4 * 2 * C::ROWB, &a.kmap, 0, rowbase + q0, rowbase + q1,
+                         rowbase + q2, rowbase + q3, &cfull[s], evict_first);
       if (lane == 0 && d.first) {
         const int64_t b = d.bk / a.Hkv, kvh = d.bk % a.Hkv;
         bulk_g2s(cw + C::OFF_Q + s * C::QSLOT, Qg + (b * a.Hq + kvh * G) * (int64_t)C::ROWB, C::QB, &cfull[s]);
@@ -669,20 +707,6 @@ __global__ void __launch_bounds__(Bf16Cfg<D, G, S, NPAIR>::NW * 32, 1)
         if (hA < G) { pa[hA * D + mt * 16 + g4] = acc[mt][0]; pa[hA * D + mt * 16 + 8 + g4] = acc[mt][2]; }
         if (hB < G) { pa[hB * D + mt * 16 + g4] = acc[mt][1]; pa[hB * D + mt * 16 + 8 + g4] = acc[mt][3]; }
       }
-      if (d.dense) {
-        if (lane < 4) {
-          if (hA < G) { st[hA] = mA; st[8 + hA] = zA; }
-          if (hB < G) { st[hB] = mB; st[8 + hB] = zB; }
-        }
-        __syncwarp();
-        double mm[G], zz[G];
-#pragma unroll
-        for (int g = 0; g < G; ++g) { mm[g] = st[g]; zz[g] = st[8 + g]; }
-        TL(long long e0 = clock64();)
-        dense_epilogue<float, G>(a, d.bk, mm, zz, lane);
-        TL(tl_epi += clock64() - e0;)
-      }
-
     }
     __syncwarp();
     TL(long long c5 = clock64(); tl_end += c5 - c4b;)
@@ -745,6 +769,7 @@ __global__ void __launch_bounds__(F32Cfg<D, G>::NC * 32, 1) decode_f32_kernel(co
   if (lane < C::S) mbar_init(&bar[lane], 1);
   fence_mbar_init();
   __syncwarp();
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // see decode_bf16_kernel
 
   Cursor cur;
   cur.nxt = 0;
@@ -889,13 +914,6 @@ __global__ void __launch_bounds__(F32Cfg<D, G>::NC * 32, 1) decode_f32_kernel(co
       if (lane < G) {
         a.part_m[(int64_t)d.item * G + lane] = mz[2 * lane];
         a.part_z[(int64_t)d.item * G + lane] = mz[2 * lane + 1];
-      }
-      if (d.dense) {
-        __syncwarp();
-        double mm[G], zz[G];
-#pragma unroll
-        for (int g = 0; g < G; ++g) { mm[g] = mz[2 * g]; zz[g] = mz[2 * g + 1]; }
-        dense_epilogue<double, G>(a, d.bk, mm, zz, lane);
       }
     }
     __syncwarp();
@@ -1298,9 +1316,10 @@ static int launch_decode_t(const DecodeArgs& a_in, cudaStream_t s) {
   if (e != cudaSuccess) return (int)e;
   // merge kernel: programmatic dependent launch (its launch overlaps the decode tail)
   cudaLaunchConfig_t cfg = {};
+  using SC = typename std::conditional<BF16, float, double>::type;  // dense score type
   static bool mattr = false;
   {
-    const int rc = set_smem(decode_merge_kernel<D, G>, MergeCfg<D, G>::SMEM, mattr);
+    const int rc = set_smem(decode_merge_kernel<D, G, SC>, MergeCfg<D, G>::SMEM, mattr);
     if (rc) return rc;
   }
   cfg.gridDim = dim3((unsigned)(a.B * a.Hkv));
@@ -1312,7 +1331,7 @@ static int launch_decode_t(const DecodeArgs& a_in, cudaStream_t s) {
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return (int)cudaLaunchKernelEx(&cfg, decode_merge_kernel<D, G>, a.m, a.counter);
+  return (int)cudaLaunchKernelEx(&cfg, decode_merge_kernel<D, G, SC>, a);
 }
 
 template <bool BF16, int D>
@@ -1408,6 +1427,9 @@ int decode_config(int dtype, int64_t D, int64_t G, int64_t* o) {
 }  // namespace hgca
 
 #ifdef HGCA_TIMELINE
+extern "C" int hgca_debug_timeline_merge(void* host) {
+  return (int)cudaMemcpyFromSymbol(host, hgca::g_tlm, sizeof(hgca::g_tlm));
+}
 extern "C" int hgca_debug_timeline(void* host, int64_t n) {
   const int64_t cap = (int64_t)sizeof(hgca::g_tl) / 8;
   if (n > cap) n = cap;

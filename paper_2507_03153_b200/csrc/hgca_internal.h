@@ -46,7 +46,7 @@ struct MergeArgs {
 
 struct DecodeMergeArgs {
   int64_t B, Hq, Hkv, G, D;
-  int64_t n_dense_items;  // = B*Hkv: one dense item per (batch, kv-head), item id = bk
+  int64_t n_dense_items;  // = B*Hkv*Sd dense items (window parts), ids first
   const int32_t* item_off;
   const double* part_m;
   const double* part_z;
@@ -79,8 +79,9 @@ struct DecodeArgs {
   double* part_z;         // [items, G]
   float* part_acc;        // [items, G, D]
   int32_t* counter;       // work counter (0 on entry; re-armed by the merge kernel)
-  int64_t n_dense_items;  // B*Hkv
-  // dense-item epilogue: weights + MAW maintenance of the attended window
+  int64_t n_dense_items;  // B*Hkv*Sd
+  int64_t Sd;             // dense items (window parts of DENSE_ROWS rows) per (batch, kv-head)
+  // merge-kernel epilogue: window weights + MAW maintenance
   int64_t w_old;          // window entries before this step (EMA'd); the rest are new
   double* maw;            // [B*Hq, T] or nullptr (no MAW maintenance)
   double one_minus_alpha, alpha;

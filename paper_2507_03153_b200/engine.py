@@ -245,7 +245,7 @@ class HybridEngine:
         BHq = self.B * self.Hq
         self.dsc_ld = self.cap + 1
         self.dsc = torch.zeros((BHq, self.dsc_ld), dtype=torch.float64, device=self.dev)
-        n_dense = self.B * self.Hkv
+        n_dense = self.B * self.Hkv * math.ceil(self.dsc_ld / 256)  # window parts of 256 rows
         n_sparse = self.B * self.Hkv * (math.ceil(4 * self.T / SPARSE_ROWS) + 2)
         self.max_items = n_dense + n_sparse
         self.part_m = torch.empty(self.max_items * self.G, dtype=torch.float64, device=self.dev)

@@ -74,6 +74,16 @@ def main():
         items_end = (t[:, 17] - t0) / 1e3
         print(f"  items done: p0 {items_end.min():.1f} p50 {np.median(items_end):.1f} max {items_end.max():.1f} us; "
               f"after merge phase: p50 {np.median(end):.1f} max {end.max():.1f} us")
+        fm = lib.hgca_debug_timeline_merge
+        fm.argtypes = [ctypes.c_void_p]
+        mb = np.zeros(4096 * 8, np.uint64)
+        fm(mb.ctypes.data)
+        tm = (mb.reshape(4096, 8)[: B * Hkv, :6].astype(np.float64) - t0) / 1e3
+        print("  merge CTAs (us): resident p0 %.1f max %.1f | after wait p0 %.1f max %.1f | sparse fold max %.1f "
+              "| dense fold max %.1f | epilogue end p50 %.1f max %.1f; per CTA: sparse %.1f dense %.1f epi %.1f" % (
+                  tm[:, 0].min(), tm[:, 0].max(), tm[:, 1].min(), tm[:, 1].max(), tm[:, 2].max(), tm[:, 3].max(),
+                  np.median(tm[:, 5]), tm[:, 5].max(), np.median(tm[:, 2] - tm[:, 1]), np.median(tm[:, 3] - tm[:, 2]),
+                  np.median(tm[:, 5] - tm[:, 4])))
         # early finishers: what were they doing?
         order = np.argsort(end)
         print(f"  first 5 finishers: end {np.round(end[order[:5]], 1)} subs {cyc['sub'][order[:5]]}; "
