@@ -105,7 +105,7 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------- ours
-def stage_engine(hg, torch, cfgd, max_positions, seed=0, sharded=False):
+def stage_engine(hg, torch, cfgd, max_positions, seed=0, sharded=False, layers=1):
     """Build the engine and stage a 32K context: bulk-ingest the archive with
     MAW drawn so that ~frac of entries per query head pass beta/divisor, then
     decode until the window reaches its steady state. sharded: every rank
@@ -113,7 +113,7 @@ def stage_engine(hg, torch, cfgd, max_positions, seed=0, sharded=False):
     keeps only its own archive blocks selectable."""
     B, Hq, Hkv, D = cfgd["batch"], cfgd["heads"], cfgd["kv_heads"], cfgd["head_dim"]
     cap = cfgd["blk_num"] * cfgd["blk_size"]
-    cfg = hg.EngineConfig(layers=1, heads=Hq, kv_heads=Hkv, head_dim=D, batch=B, dtype=cfgd["dtype"],
+    cfg = hg.EngineConfig(layers=layers, heads=Hq, kv_heads=Hkv, head_dim=D, batch=B, dtype=cfgd["dtype"],
                           cache=hg.CacheConfig(blk_num=cfgd["blk_num"], blk_size=cfgd["blk_size"],
                                                alpha=cfgd["alpha"], beta=cfgd["beta"]),
                           core_count=10 ** 6, max_positions=max_positions)
@@ -121,18 +121,20 @@ def stage_engine(hg, torch, cfgd, max_positions, seed=0, sharded=False):
     g = torch.Generator(device="cuda").manual_seed(seed)
     tdt = eng.tdtype
     n_arch = cfgd["context"] - cap
-    k = torch.randn((B, Hkv, n_arch, D), generator=g, device="cuda").to(tdt)
-    v = torch.randn((B, Hkv, n_arch, D), generator=g, device="cuda").to(tdt)
     divisor = cap
     thr = cfgd["beta"] / divisor
-    u = torch.rand((B, Hq, n_arch), generator=g, device="cuda", dtype=torch.float64)
-    maw = torch.where(u < cfgd["frac"], thr * (1.0 + u), thr * u)
-    eng.bulk_ingest(0, k, v, maw, divisor)
-    del k, v, u, maw
+    for layer in range(layers):
+        k = torch.randn((B, Hkv, n_arch, D), generator=g, device="cuda").to(tdt)
+        v = torch.randn((B, Hkv, n_arch, D), generator=g, device="cuda").to(tdt)
+        u = torch.rand((B, Hq, n_arch), generator=g, device="cuda", dtype=torch.float64)
+        maw = torch.where(u < cfgd["frac"], thr * (1.0 + u), thr * u)
+        eng.bulk_ingest(layer, k, v, maw, divisor)
+        del k, v, u, maw
     for _ in range(cap - 1):
         q = torch.randn((B, Hq, 1, D), generator=g, device="cuda").to(tdt)
         kk = torch.randn((B, Hkv, 1, D), generator=g, device="cuda").to(tdt)
-        eng.decode_device(0, q, kk, kk)
+        for layer in range(layers):
+            eng.decode_device(layer, q, kk, kk)
     torch.cuda.synchronize()
     return eng, g
 
