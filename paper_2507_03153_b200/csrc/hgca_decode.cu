@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(MergeCfg<D, G>::NT) decode_merge_kernel(const 
   double* sm_z = reinterpret_cast<double*>(msm + C::OFF_Z);
   double* sw = reinterpret_cast<double*>(msm + C::OFF_W);
   uint64_t* bar = reinterpret_cast<uint64_t*>(msm + C::OFF_BAR);
-  __shared__ double hM[G], hZ[G], hS[G];
+  __shared__ double hM[2][G], hZ[2][G], hS[2][G];  // [0] sparse, [1] dense running stats
   const int64_t bk = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   TL(if (tid == 0) g_tlm[blockIdx.x * 8 + 0] = gtimer();)
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(MergeCfg<D, G>::NT) decode_merge_kernel(const 
   const int64_t BK = m.B * m.Hkv, nd = m.n_dense_items;
   const int64_t b = bk / m.Hkv, kvh = bk % m.Hkv;
   // window-epilogue operands of the first batch: loaded now, consumed after the folds
-  constexpr int EB = 8;
+  constexpr int EB = 12;  // one batch covers G*W <= 12*NT window weights (the whole C2 window)
   const bool epi = a.maw != nullptr || a.wts_out != nullptr;
   const int64_t W = a.dhi - a.dlo, n_el = epi ? (int64_t)G * W : 0;
   const SC* dsc = reinterpret_cast<const SC*>(a.dsc);
@@ -288,97 +288,102 @@ __global__ void __launch_bounds__(MergeCfg<D, G>::NT) decode_merge_kernel(const 
   };
   epi_load(0);
   uint32_t phase = 0;
-  // fold the items of up to two contiguous ranges [r0, r0+n0), [r1, r1+n1)
-  // (in that order) for every head: fills hM/hZ and this thread's acc
-  auto fold = [&](int64_t r0, int64_t n0, int64_t r1, int64_t n1, double (&acc)[C::OPT]) {
-    const int64_t n = n0 + n1;
-    if (tid < G) {
-      hM[tid] = -INFINITY;
-      hZ[tid] = 0.0;
-    }
-#pragma unroll
-    for (int k = 0; k < C::OPT; ++k) acc[k] = 0.0;
-    __syncthreads();
-    for (int64_t c0 = 0; c0 < n; c0 += C::NI) {
-      const int64_t c1 = min(n, c0 + C::NI), cn = c1 - c0;
-      if (tid == 0) {
-        const int64_t a_lo = c0, a_hi = min(c1, n0), b_lo = max(c0, n0), b_hi = c1;
-        uint32_t bytes = 0;
-        if (a_hi > a_lo) bytes += (uint32_t)((a_hi - a_lo) * C::ROW);
-        if (b_hi > b_lo) bytes += (uint32_t)((b_hi - b_lo) * C::ROW);
-        mbar_expect_tx(bar, bytes);
-        if (a_hi > a_lo)
-          bulk_g2s(sacc + (a_lo - c0) * G * D, m.part_acc + (r0 + a_lo) * G * D, (uint32_t)((a_hi - a_lo) * C::ROW),
-                   bar);
-        if (b_hi > b_lo)
-          bulk_g2s(sacc + (b_lo - c0) * G * D, m.part_acc + (r1 + b_lo - n0) * G * D,
-                   (uint32_t)((b_hi - b_lo) * C::ROW), bar);
-      }
-      // (m, z) of the chunk's items: plain loads while the bulk copies land
-      for (int64_t x = tid; x < cn * G; x += C::NT) {
-        const int64_t i = c0 + x / G, g = x % G;
-        const int64_t it = i < n0 ? r0 + i : r1 + (i - n0);
-        sm_m[x] = m.part_m[it * G + g];
-        sm_z[x] = m.part_z[it * G + g];
-      }
-      __syncthreads();
-      mbar_wait(bar, phase);
-      phase ^= 1;
-      for (int g = wid; g < G; g += C::NT / 32) {
-        double mx = -INFINITY;
-        for (int64_t i = lane; i < cn; i += 32) mx = fmax(mx, sm_m[i * G + g]);
-        mx = warp_max_f64(mx);
-        const double mo = hM[g], mn = fmax(mo, mx);
-        double zl = 0.0;
-        for (int64_t i = lane; i < cn; i += 32) {
-          const double mi = sm_m[i * G + g];
-          const double w = (mi == -INFINITY || mn == -INFINITY) ? 0.0 : exp(mi - mn);
-          sw[g * C::NI + i] = w;
-          zl += sm_z[i * G + g] * w;
-        }
-        zl = warp_sum_f64(zl);
-        if (lane == 0) {
-          const double so = (mo == -INFINITY || mn == -INFINITY) ? 0.0 : exp(mo - mn);
-          hS[g] = so;
-          hZ[g] = hZ[g] * so + zl;
-          hM[g] = mn;
-        }
-      }
-      __syncthreads();
-#pragma unroll
-      for (int k = 0; k < C::OPT; ++k) {
-        const int idx = tid + k * C::NT, g = idx / D;
-        double acc_k = acc[k] * hS[g];
-        const double* w = sw + g * C::NI;
-        const float* src = sacc + idx;
-        for (int64_t i = 0; i < cn; ++i) acc_k += w[i] * (double)src[i * G * D];
-        acc[k] = acc_k;
-      }
-      __syncthreads();  // the next chunk's copies overwrite sacc / sw
-    }
+  // One fold pass over the concatenated item list [full items, tail items |
+  // dense parts]: the first ns items are sparse, the rest dense. Each chunk is
+  // bulk-copied (up to three contiguous ranges) and folded per head into the
+  // sparse (s = 0) or dense (s = 1) running statistics, in item order.
+  const int64_t o0 = m.item_off[bk], o1 = m.item_off[bk + 1];
+  const int64_t t0 = m.item_off[BK + 1 + bk], t1 = m.item_off[BK + 1 + bk + 1];
+  const int64_t nf = o1 - o0, ns = nf + (t1 - t0), n = ns + a.Sd;
+  auto item_id = [&](int64_t i) {
+    return i < nf ? nd + o0 + i : (i < ns ? nd + t0 + (i - nf) : bk * a.Sd + (i - ns));
   };
-  // ---- sparse partials: bk's full items, then its tail items
-  double acc_s[C::OPT], Ms[G], Zs[G];
-  {
-    const int64_t o0 = m.item_off[bk], o1 = m.item_off[bk + 1];
-    const int64_t t0 = m.item_off[BK + 1 + bk], t1 = m.item_off[BK + 1 + bk + 1];
-    fold(nd + o0, o1 - o0, nd + t0, t1 - t0, acc_s);
+  double acc_s[C::OPT], acc_d[C::OPT];
 #pragma unroll
-    for (int g = 0; g < G; ++g) { Ms[g] = hM[g]; Zs[g] = hZ[g]; }
-    __syncthreads();
+  for (int k = 0; k < C::OPT; ++k) acc_s[k] = acc_d[k] = 0.0;
+  if (tid < 2 * G) {
+    hM[tid / G][tid % G] = -INFINITY;
+    hZ[tid / G][tid % G] = 0.0;
   }
-  TL(if (tid == 0) g_tlm[blockIdx.x * 8 + 2] = gtimer();)
-  // ---- dense partials: the window parts of bk
-  double acc_d[C::OPT];
-  fold(bk * a.Sd, a.Sd, 0, 0, acc_d);
-  TL(if (tid == 0) g_tlm[blockIdx.x * 8 + 3] = gtimer();)
+  __syncthreads();
+  for (int64_t c0 = 0; c0 < n; c0 += C::NI) {
+    const int64_t c1 = min(n, c0 + C::NI), cn = c1 - c0;
+    if (tid == 0) {
+      const int64_t lo[3] = {0, nf, ns}, hi[3] = {nf, ns, n};
+      uint32_t bytes = 0;
+      for (int r = 0; r < 3; ++r) {
+        const int64_t x0 = max(c0, lo[r]), x1 = min(c1, hi[r]);
+        if (x1 > x0) bytes += (uint32_t)((x1 - x0) * C::ROW);
+      }
+      mbar_expect_tx(bar, bytes);
+      for (int r = 0; r < 3; ++r) {
+        const int64_t x0 = max(c0, lo[r]), x1 = min(c1, hi[r]);
+        if (x1 > x0)
+          bulk_g2s(sacc + (x0 - c0) * G * D, m.part_acc + item_id(x0) * G * D, (uint32_t)((x1 - x0) * C::ROW), bar);
+      }
+    }
+    // (m, z) of the chunk's items: plain loads while the bulk copies land
+    for (int64_t x = tid; x < cn * G; x += C::NT) {
+      const int64_t it = item_id(c0 + x / G), g = x % G;
+      sm_m[x] = m.part_m[it * G + g];
+      sm_z[x] = m.part_z[it * G + g];
+    }
+    __syncthreads();
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    // the chunk's sparse rows [0, ce) and dense rows [ce, cn)
+    const int64_t ce = min(cn, max((int64_t)0, ns - c0));
+    for (int task = wid; task < 2 * G; task += C::NT / 32) {
+      const int sd = task / G, g = task % G;
+      const int64_t i0 = sd ? ce : 0, i1 = sd ? cn : ce;
+      if (i1 <= i0) continue;  // warp-uniform
+      double mx = -INFINITY;
+      for (int64_t i = i0 + lane; i < i1; i += 32) mx = fmax(mx, sm_m[i * G + g]);
+      mx = warp_max_f64(mx);
+      const double mo = hM[sd][g], mn = fmax(mo, mx);
+      double zl = 0.0;
+      for (int64_t i = i0 + lane; i < i1; i += 32) {
+        const double mi = sm_m[i * G + g];
+        const double w = (mi == -INFINITY || mn == -INFINITY) ? 0.0 : exp(mi - mn);
+        sw[g * C::NI + i] = w;
+        zl += sm_z[i * G + g] * w;
+      }
+      zl = warp_sum_f64(zl);
+      if (lane == 0) {
+        const double so = (mo == -INFINITY || mn == -INFINITY) ? 0.0 : exp(mo - mn);
+        hS[sd][g] = so;
+        hZ[sd][g] = hZ[sd][g] * so + zl;
+        hM[sd][g] = mn;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < C::OPT; ++k) {
+      const int idx = tid + k * C::NT, g = idx / D;
+      const double* w = sw + g * C::NI;
+      const float* src = sacc + idx;
+      if (ce > 0) {
+        double as = acc_s[k] * hS[0][g];
+        for (int64_t i = 0; i < ce; ++i) as += w[i] * (double)src[i * G * D];
+        acc_s[k] = as;
+      }
+      if (cn > ce) {
+        double ad = acc_d[k] * hS[1][g];
+        for (int64_t i = ce; i < cn; ++i) ad += w[i] * (double)src[i * G * D];
+        acc_d[k] = ad;
+      }
+    }
+    __syncthreads();  // the next chunk's copies overwrite sacc / sw
+  }
+  TL(if (tid == 0) g_tlm[blockIdx.x * 8 + 2] = gtimer(); if (tid == 0) g_tlm[blockIdx.x * 8 + 3] = gtimer();)
 #pragma unroll
   for (int k = 0; k < C::OPT; ++k) {
     const int idx = tid + k * C::NT, g = idx / D, c = idx % D;
     const int64_t bq = b * m.Hq + kvh * G + g;
-    const bool s_empty = !(Zs[g] > 0.0) || Ms[g] == -INFINITY;
-    const double lse_s = s_empty ? -INFINITY : Ms[g] + log(Zs[g]);
-    const double md = hM[g], zd = hZ[g];
+    const double Msg = hM[0][g], Zsg = hZ[0][g];
+    const bool s_empty = !(Zsg > 0.0) || Msg == -INFINITY;
+    const double lse_s = s_empty ? -INFINITY : Msg + log(Zsg);
+    const double md = hM[1][g], zd = hZ[1][g];
     const bool d_empty = !(zd > 0.0) || md == -INFINITY;
     const double lse_d = d_empty ? -INFINITY : md + log(zd);
     const double mm = fmax(lse_s, lse_d);
@@ -387,7 +392,7 @@ __global__ void __launch_bounds__(MergeCfg<D, G>::NT) decode_merge_kernel(const 
     const double wa = exp(lse_s - ms), wb = exp(lse_d - ms);
     const double zs = both_empty ? 1.0 : wa + wb;
     const float ca = (float)(wa / zs), cb = (float)(wb / zs);
-    const float os = s_empty ? 0.f : (float)(acc_s[k] / Zs[g]);
+    const float os = s_empty ? 0.f : (float)(acc_s[k] / Zsg);
     const float od = d_empty ? 0.f : (float)(acc_d[k] / zd);
     m.out[bq * D + c] = __fadd_rn(__fmul_rn(ca, os), __fmul_rn(cb, od));
     if (m.out_sparse) m.out_sparse[bq * D + c] = os;
@@ -407,8 +412,13 @@ __global__ void __launch_bounds__(MergeCfg<D, G>::NT) decode_merge_kernel(const 
       if (x >= n_el) continue;
       const int g = (int)(x / W);
       const int64_t j = x - g * W, bq = b * m.Hq + kvh * G + g;
-      const double md = hM[g], zd = hZ[g];
-      const float w32 = (!(zd > 0.0) || md == -INFINITY) ? 0.f : (float)(exp((double)sv[u] - md) / zd);
+      const double md = hM[1][g], zd = hZ[1][g];
+      float w32;
+      if constexpr (sizeof(SC) == 8) {  // fp32 storage: reference-exact fp64 weights (_core.pyx:81-82)
+        w32 = (!(zd > 0.0) || md == -INFINITY) ? 0.f : (float)(exp((double)sv[u] - md) / zd);
+      } else {  // bf16 storage: fp32 math (no bit-exactness contract on this path)
+        w32 = (!(zd > 0.0) || md == -INFINITY) ? 0.f : __expf((float)sv[u] - (float)md) * (float)(1.0 / zd);
+      }
       if (a.wts_out) a.wts_out[bq * W + j] = w32;
       if (a.maw) {
         const double aw = (double)w32;
