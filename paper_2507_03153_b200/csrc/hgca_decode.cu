@@ -66,6 +66,9 @@ __device__ unsigned long long g_tlm[4096 * 8];  // merge kernel: per CTA phase s
 #endif
 
 constexpr int SUB = 32;  // rows per pipeline stage (one per lane)
+// per-item (m, z) rows are padded to 16 bytes so TMA bulk copies can move them
+template <int G>
+constexpr int mz_stride() { return G < 2 ? 2 : G; }
 constexpr int DENSE_ROWS = 256;  // window rows per dense work item
 constexpr uint32_t FULL = 0xffffffffu;
 constexpr int SMEM_MAX = 232448;  // dynamic shared memory per CTA on sm_100
@@ -231,10 +234,11 @@ template <int D, int G>
 struct MergeCfg {
   static constexpr int NT = G * D >= 256 ? 256 : G * D;         // threads
   static constexpr int ROW = G * D * 4;                          // accumulator bytes per item
-  static constexpr int NI = MERGE_CHUNK_BYTES / (ROW + 24 * G);  // items per chunk
-  static constexpr int OFF_M = NI * ROW;                         // part_m [NI][G] fp64
-  static constexpr int OFF_Z = OFF_M + NI * G * 8;               // part_z [NI][G] fp64
-  static constexpr int OFF_W = OFF_Z + NI * G * 8;               // weights [G][NI] fp64
+  static constexpr int GS = mz_stride<G>();                      // (m, z) row stride (16-byte rows)
+  static constexpr int NI = MERGE_CHUNK_BYTES / (ROW + 16 * GS + 8 * G);  // items per chunk
+  static constexpr int OFF_M = NI * ROW;                         // part_m [NI][GS] fp64
+  static constexpr int OFF_Z = OFF_M + NI * GS * 8;              // part_z [NI][GS] fp64
+  static constexpr int OFF_W = OFF_Z + NI * GS * 8;              // weights [G][NI] fp64
   static constexpr int OFF_BAR = OFF_W + NI * G * 8;
   static constexpr int SMEM = OFF_BAR + 64;
   static constexpr int OPT = G * D / NT;                         // outputs (head, dim) per thread
@@ -259,53 +263,65 @@ __global__ void __launch_bounds__(MergeCfg<D, G>::NT) decode_merge_kernel(const 
     mbar_init(bar, 1);
     fence_mbar_init();
   }
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  TL(if (tid == 0) g_tlm[blockIdx.x * 8 + 1] = gtimer();)
-  // the decode grid is complete: re-arm its work counter for the next step
-  if (blockIdx.x == 0 && tid == 0) *a.counter = 0;
+  // Everything that does not depend on this step's decode grid is read before
+  // griddepcontrol.wait: the item ranges (built at the last selection change)
+  // and the window MAW (only this kernel writes it).
   const int64_t BK = m.B * m.Hkv, nd = m.n_dense_items;
   const int64_t b = bk / m.Hkv, kvh = bk % m.Hkv;
-  // window-epilogue operands of the first batch: loaded now, consumed after the folds
-  constexpr int EB = 12;  // one batch covers G*W <= 12*NT window weights (the whole C2 window)
-  const bool epi = a.maw != nullptr || a.wts_out != nullptr;
-  const int64_t W = a.dhi - a.dlo, n_el = epi ? (int64_t)G * W : 0;
-  const SC* dsc = reinterpret_cast<const SC*>(a.dsc);
-  SC sv[EB];
-  double mo[EB];
-  auto epi_load = [&](int64_t x0) {
-#pragma unroll
-    for (int u = 0; u < EB; ++u) {
-      const int64_t x = x0 + (int64_t)u * C::NT + tid;
-      sv[u] = 0;
-      mo[u] = 0.0;
-      if (x < n_el) {
-        const int g = (int)(x / W);
-        const int64_t j = x - g * W, bq = b * m.Hq + kvh * G + g;
-        sv[u] = dsc[bq * a.dsc_ld + j];
-        if (a.maw && j < a.w_old) mo[u] = a.maw[bq * a.T + a.dlo + j];
-      }
-    }
-  };
-  epi_load(0);
-  uint32_t phase = 0;
-  // One fold pass over the concatenated item list [full items, tail items |
-  // dense parts]: the first ns items are sparse, the rest dense. Each chunk is
-  // bulk-copied (up to three contiguous ranges) and folded per head into the
-  // sparse (s = 0) or dense (s = 1) running statistics, in item order.
   const int64_t o0 = m.item_off[bk], o1 = m.item_off[bk + 1];
   const int64_t t0 = m.item_off[BK + 1 + bk], t1 = m.item_off[BK + 1 + bk + 1];
   const int64_t nf = o1 - o0, ns = nf + (t1 - t0), n = ns + a.Sd;
   auto item_id = [&](int64_t i) {
     return i < nf ? nd + o0 + i : (i < ns ? nd + t0 + (i - nf) : bk * a.Sd + (i - ns));
   };
-  double acc_s[C::OPT], acc_d[C::OPT];
+  constexpr int EB = 12;  // one batch covers G*W <= 12*NT window weights (the whole C2 window)
+  const bool epi = a.maw != nullptr || a.wts_out != nullptr;
+  const int64_t W = a.dhi - a.dlo, n_el = epi ? (int64_t)G * W : 0;
+  const SC* dsc = reinterpret_cast<const SC*>(a.dsc);
+  SC sv[EB];
+  double mo[EB];
+  auto maw_load = [&](int64_t x0) {
 #pragma unroll
-  for (int k = 0; k < C::OPT; ++k) acc_s[k] = acc_d[k] = 0.0;
+    for (int u = 0; u < EB; ++u) {
+      const int64_t x = x0 + (int64_t)u * C::NT + tid;
+      mo[u] = 0.0;
+      if (x < n_el && a.maw) {
+        const int g = (int)(x / W);
+        const int64_t j = x - g * W, bq = b * m.Hq + kvh * G + g;
+        if (j < a.w_old) mo[u] = a.maw[bq * a.T + a.dlo + j];
+      }
+    }
+  };
+  auto dsc_load = [&](int64_t x0) {
+#pragma unroll
+    for (int u = 0; u < EB; ++u) {
+      const int64_t x = x0 + (int64_t)u * C::NT + tid;
+      sv[u] = 0;
+      if (x < n_el) {
+        const int g = (int)(x / W);
+        const int64_t j = x - g * W, bq = b * m.Hq + kvh * G + g;
+        sv[u] = dsc[bq * a.dsc_ld + j];
+      }
+    }
+  };
+  maw_load(0);
   if (tid < 2 * G) {
     hM[tid / G][tid % G] = -INFINITY;
     hZ[tid / G][tid % G] = 0.0;
   }
-  __syncthreads();
+  double acc_s[C::OPT], acc_d[C::OPT];
+#pragma unroll
+  for (int k = 0; k < C::OPT; ++k) acc_s[k] = acc_d[k] = 0.0;
+  uint32_t phase = 0;
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  TL(if (tid == 0) g_tlm[blockIdx.x * 8 + 1] = gtimer();)
+  // the decode grid is complete: re-arm its work counter for the next step
+  if (blockIdx.x == 0 && tid == 0) *a.counter = 0;
+  // One fold pass over the concatenated item list [full items, tail items |
+  // dense parts]: the first ns items are sparse, the rest dense. Each chunk is
+  // bulk-copied (up to three contiguous ranges; accumulator and (m, z) rows)
+  // and folded per head into the sparse (s = 0) or dense (s = 1) running
+  // statistics, in item order.
   for (int64_t c0 = 0; c0 < n; c0 += C::NI) {
     const int64_t c1 = min(n, c0 + C::NI), cn = c1 - c0;
     if (tid == 0) {
@@ -315,22 +331,27 @@ __global__ void __launch_bounds__(MergeCfg<D, G>::NT) decode_merge_kernel(const 
         const int64_t x0 = max(c0, lo[r]), x1 = min(c1, hi[r]);
         if (x1 > x0) bytes += (uint32_t)((x1 - x0) * C::ROW);
       }
+      for (int r = 0; r < 3; ++r) {
+        const int64_t x0 = max(c0, lo[r]), x1 = min(c1, hi[r]);
+        if (x1 > x0) bytes += (uint32_t)((x1 - x0) * 16 * C::GS);  // + the (m, z) rows
+      }
       mbar_expect_tx(bar, bytes);
       for (int r = 0; r < 3; ++r) {
         const int64_t x0 = max(c0, lo[r]), x1 = min(c1, hi[r]);
-        if (x1 > x0)
-          bulk_g2s(sacc + (x0 - c0) * G * D, m.part_acc + item_id(x0) * G * D, (uint32_t)((x1 - x0) * C::ROW), bar);
+        if (x1 > x0) {
+          const int64_t it = item_id(x0), k = x1 - x0, dst = x0 - c0;
+          bulk_g2s(sacc + dst * G * D, m.part_acc + it * G * D, (uint32_t)(k * C::ROW), bar);
+          bulk_g2s(sm_m + dst * C::GS, m.part_m + it * C::GS, (uint32_t)(k * 8 * C::GS), bar);
+          bulk_g2s(sm_z + dst * C::GS, m.part_z + it * C::GS, (uint32_t)(k * 8 * C::GS), bar);
+        }
       }
     }
-    // (m, z) of the chunk's items: plain loads while the bulk copies land
-    for (int64_t x = tid; x < cn * G; x += C::NT) {
-      const int64_t it = item_id(c0 + x / G), g = x % G;
-      sm_m[x] = m.part_m[it * G + g];
-      sm_z[x] = m.part_z[it * G + g];
-    }
+    if (c0 == 0) dsc_load(0);  // the window scores of the epilogue: in flight during the fold
     __syncthreads();
+    TL(if (tid == 0 && c0 == 0) g_tlm[blockIdx.x * 8 + 6] = gtimer();)
     mbar_wait(bar, phase);
     phase ^= 1;
+    TL(if (tid == 0 && c0 == 0) g_tlm[blockIdx.x * 8 + 7] = gtimer();)
     // the chunk's sparse rows [0, ce) and dense rows [ce, cn)
     const int64_t ce = min(cn, max((int64_t)0, ns - c0));
     for (int task = wid; task < 2 * G; task += C::NT / 32) {
@@ -338,15 +359,15 @@ __global__ void __launch_bounds__(MergeCfg<D, G>::NT) decode_merge_kernel(const 
       const int64_t i0 = sd ? ce : 0, i1 = sd ? cn : ce;
       if (i1 <= i0) continue;  // warp-uniform
       double mx = -INFINITY;
-      for (int64_t i = i0 + lane; i < i1; i += 32) mx = fmax(mx, sm_m[i * G + g]);
+      for (int64_t i = i0 + lane; i < i1; i += 32) mx = fmax(mx, sm_m[i * C::GS + g]);
       mx = warp_max_f64(mx);
       const double mo = hM[sd][g], mn = fmax(mo, mx);
       double zl = 0.0;
       for (int64_t i = i0 + lane; i < i1; i += 32) {
-        const double mi = sm_m[i * G + g];
+        const double mi = sm_m[i * C::GS + g];
         const double w = (mi == -INFINITY || mn == -INFINITY) ? 0.0 : exp(mi - mn);
         sw[g * C::NI + i] = w;
-        zl += sm_z[i * G + g] * w;
+        zl += sm_z[i * C::GS + g] * w;
       }
       zl = warp_sum_f64(zl);
       if (lane == 0) {
@@ -362,16 +383,20 @@ __global__ void __launch_bounds__(MergeCfg<D, G>::NT) decode_merge_kernel(const 
       const int idx = tid + k * C::NT, g = idx / D;
       const double* w = sw + g * C::NI;
       const float* src = sacc + idx;
-      if (ce > 0) {
-        double as = acc_s[k] * hS[0][g];
-        for (int64_t i = 0; i < ce; ++i) as += w[i] * (double)src[i * G * D];
-        acc_s[k] = as;
-      }
-      if (cn > ce) {
-        double ad = acc_d[k] * hS[1][g];
-        for (int64_t i = ce; i < cn; ++i) ad += w[i] * (double)src[i * G * D];
-        acc_d[k] = ad;
-      }
+      auto dot = [&](int64_t i0, int64_t i1) {  // 4 interleaved partial sums, combined in a fixed order
+        double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+        int64_t i = i0;
+        for (; i + 4 <= i1; i += 4) {
+          p0 += w[i] * (double)src[i * G * D];
+          p1 += w[i + 1] * (double)src[(i + 1) * G * D];
+          p2 += w[i + 2] * (double)src[(i + 2) * G * D];
+          p3 += w[i + 3] * (double)src[(i + 3) * G * D];
+        }
+        for (; i < i1; ++i) p0 += w[i] * (double)src[i * G * D];
+        return (p0 + p1) + (p2 + p3);
+      };
+      if (ce > 0) acc_s[k] = acc_s[k] * hS[0][g] + dot(0, ce);
+      if (cn > ce) acc_d[k] = acc_d[k] * hS[1][g] + dot(ce, cn);
     }
     __syncthreads();  // the next chunk's copies overwrite sacc / sw
   }
@@ -404,8 +429,12 @@ __global__ void __launch_bounds__(MergeCfg<D, G>::NT) decode_merge_kernel(const 
   TL(if (tid == 0) g_tlm[blockIdx.x * 8 + 4] = gtimer();)
   // ---- window weights + MAW maintenance from the stored dense scores
   // (batches of EB elements per thread; batch 0 was loaded before the folds)
+  if (n == 0) dsc_load(0);  // (no fold chunk ran)
   for (int64_t x0 = 0; x0 < n_el; x0 += (int64_t)EB * C::NT) {
-    if (x0) epi_load(x0);
+    if (x0) {
+      maw_load(x0);
+      dsc_load(x0);
+    }
 #pragma unroll
     for (int u = 0; u < EB; ++u) {
       const int64_t x = x0 + (int64_t)u * C::NT + tid;
@@ -708,8 +737,9 @@ __global__ void __launch_bounds__(Bf16Cfg<D, G, S, NPAIR>::NW * 32, 1)
       TL(++tl_items;)
       // partial (m, z, acc) of this item; acc[mt][j] = O[head hA|hB][dim mt*16 + g4 (+8)]
       if (lane < 4) {
-        if (hA < G) { a.part_m[(int64_t)d.item * G + hA] = mA; a.part_z[(int64_t)d.item * G + hA] = zA; }
-        if (hB < G) { a.part_m[(int64_t)d.item * G + hB] = mB; a.part_z[(int64_t)d.item * G + hB] = zB; }
+        constexpr int GS = mz_stride<G>();
+        if (hA < G) { a.part_m[(int64_t)d.item * GS + hA] = mA; a.part_z[(int64_t)d.item * GS + hA] = zA; }
+        if (hB < G) { a.part_m[(int64_t)d.item * GS + hB] = mB; a.part_z[(int64_t)d.item * GS + hB] = zB; }
       }
       float* pa = a.part_acc + (int64_t)d.item * G * D;
 #pragma unroll
@@ -922,8 +952,8 @@ __global__ void __launch_bounds__(F32Cfg<D, G>::NC * 32, 1) decode_f32_kernel(co
     if (d.last) {
       for (int t = lane; t < G * D; t += 32) a.part_acc[(int64_t)d.item * G * D + t] = accs[t];
       if (lane < G) {
-        a.part_m[(int64_t)d.item * G + lane] = mz[2 * lane];
-        a.part_z[(int64_t)d.item * G + lane] = mz[2 * lane + 1];
+        a.part_m[(int64_t)d.item * mz_stride<G>() + lane] = mz[2 * lane];
+        a.part_z[(int64_t)d.item * mz_stride<G>() + lane] = mz[2 * lane + 1];
       }
     }
     __syncwarp();

@@ -78,12 +78,14 @@ def main():
         fm.argtypes = [ctypes.c_void_p]
         mb = np.zeros(4096 * 8, np.uint64)
         fm(mb.ctypes.data)
-        tm = (mb.reshape(4096, 8)[: B * Hkv, :6].astype(np.float64) - t0) / 1e3
+        tm = (mb.reshape(4096, 8)[: B * Hkv, :8].astype(np.float64) - t0) / 1e3
         print("  merge CTAs (us): resident p0 %.1f max %.1f | after wait p0 %.1f max %.1f | sparse fold max %.1f "
               "| dense fold max %.1f | epilogue end p50 %.1f max %.1f; per CTA: sparse %.1f dense %.1f epi %.1f" % (
                   tm[:, 0].min(), tm[:, 0].max(), tm[:, 1].min(), tm[:, 1].max(), tm[:, 2].max(), tm[:, 3].max(),
                   np.median(tm[:, 5]), tm[:, 5].max(), np.median(tm[:, 2] - tm[:, 1]), np.median(tm[:, 3] - tm[:, 2]),
                   np.median(tm[:, 5] - tm[:, 4])))
+        print("  merge fold detail (median per CTA, us): m/z loads + issue %.1f, bulk wait %.1f, stats+acc %.1f" % (
+            np.median(tm[:, 6] - tm[:, 1]), np.median(tm[:, 7] - tm[:, 6]), np.median(tm[:, 2] - tm[:, 7])))
         # early finishers: what were they doing?
         order = np.argsort(end)
         print(f"  first 5 finishers: end {np.round(end[order[:5]], 1)} subs {cyc['sub'][order[:5]]}; "
