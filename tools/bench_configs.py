@@ -1,5 +1,6 @@
 """The other BASELINE.json configs on one B200 (manual runs; bench.py's driver line is C2).
 
+  python tools/bench_configs.py C1      the reference's fp32 case (32 heads, 4K context, batch 1) vs its CPU path
   python tools/bench_configs.py C3      B=4, 128K context (the N=1 point of the sequence-sharded scaling run)
   python tools/bench_configs.py C4      Llama-3-70B shape (64 q / 8 kv heads), 16K context, 80 layers per
                                         decode step; the per-GPU batch shard (B=8 of 64) of the 8-GPU run
@@ -67,7 +68,17 @@ def measure(cfgd, layers=1, steps=50, warmup=5, name=""):
 def main():
     which = sys.argv[1] if len(sys.argv) > 1 else "C3"
     base = dict(bench.C2)
-    if which == "C3":
+    if which == "C1":
+        # the reference's own CPU-runnable case: 32 heads d=128 (MHA), batch 1, 4K context,
+        # 512-token window, fp32 -- the reference-exact kernel (fp64 dot products)
+        cfgd = dict(base, batch=1, heads=32, kv_heads=32, context=4096, dtype="float32")
+        r = measure(cfgd, steps=200, warmup=10, name="C1 (fp32, reference-exact path)")
+        from oracle import cpu_bench  # the reference's CPU path, timed beside it (baseline only)
+        cpu = cpu_bench.time_single(32, 32, 128, 4096 - 512, 512, cfgd["frac"], sequences=4, reps=10)
+        r["cpu_reference_tokens_per_s"] = round(cpu["value"], 2)
+        r["cpu_kind"] = cpu["kind"]
+        print(json.dumps(r), flush=True)
+    elif which == "C3":
         cfgd = dict(base, batch=4, context=131072)
         print(json.dumps(measure(cfgd, steps=50, name="C3 (1 GPU point)")), flush=True)
     elif which == "C4":
