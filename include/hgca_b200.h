@@ -12,6 +12,7 @@
  *   hgca_attend_indexed        backends.active.attend_indexed backends.py:8-20, _core.pyx:87-150
  *   hgca_attend_indexed_heads  per-head attend_indexed loop   engine.py:139-148
  *   hgca_attend_gqa            append-mode attend over window / archive  engine.py:127-132, 161-164
+ *   hgca_append_bf16           the same append step for BF16 storage on the tensor cores (+ row-mean weights)
  *   hgca_merge_states          merge_states                   attention.py:153-188
  *   hgca_select_threshold      select_salient                 sparsifier.py:32-42
  *   hgca_mask_to_indices       np.nonzero / context index lists sparsifier.py:42, 77-87
@@ -191,6 +192,19 @@ typedef struct hgca_decode_desc {
  * (programmatic dependent launch; folds the partials in item order, applies
  * merge_states, the window weights and the MAW EMA). */
 int hgca_decode_step(const hgca_decode_desc* desc, hgca_stream_t stream);
+
+/* Append / re-evaluation attention for BF16 storage on the tensor cores
+ * (engine.py:111-132, 161-169; sparsifier.py:158-177): q [B*Hq, nq, D]
+ * (nq <= 128) attends the archive [0, lo) and the window + kv_in [lo, hi) of
+ * the position buffer KV (kv_in already written); out [B*Hq, nq, D] f32 and
+ * lse [B*Hq, nq] f64 are merge_states(archive, window); mean_archive
+ * [B*Hq, lo] and mean_window [B*Hq, hi-lo] (optional) receive, per query head
+ * and position, the mean attention weight over the nq rows (a_cpu / a_gpu
+ * row means). ws: hgca_append_ws_bytes(...) bytes of device scratch. */
+int64_t hgca_append_ws_bytes(int64_t B, int64_t Hq, int64_t Hkv, int64_t D, int64_t nq, int64_t lo, int64_t hi);
+int hgca_append_bf16(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, int64_t T, int64_t D, const void* q,
+                     int64_t nq, double scale, int64_t lo, int64_t hi, float* out, double* lse, float* mean_archive,
+                     float* mean_window, void* ws, int64_t ws_bytes, hgca_stream_t stream);
 
 /* End-to-end step from HOST buffers (pinned): copy in_bytes of in_host to
  * in_dev (the caller points desc->q / k_new / v_new into in_dev), run the

@@ -67,8 +67,10 @@ _SIGS = {
     "hgca_union_build": [P, I64, I64, I64, I64, I64, I64, P, P, P, P, I64, I32, P],
     "hgca_decode_step": [ctypes.POINTER(DecodeDesc), P],
     "hgca_decode_step_host": [ctypes.POINTER(DecodeDesc), P, P, I64, P, P, I64, P],
+    "hgca_append_ws_bytes": [I64, I64, I64, I64, I64, I64, I64],
+    "hgca_append_bf16": [P, I64, I64, I64, I64, I64, P, I64, D, I64, I64, P, P, P, P, P, I64, P],
 }
-_RESTYPES = {"hgca_last_error": ctypes.c_char_p, "hgca_attend_ws_bytes": I64}
+_RESTYPES = {"hgca_last_error": ctypes.c_char_p, "hgca_attend_ws_bytes": I64, "hgca_append_ws_bytes": I64}
 
 _lib = None
 

@@ -1,0 +1,495 @@
+// Append / re-evaluation step for bfloat16 storage (engine.py:111-132,
+// 161-169; sparsifier.py:158-177) on the tensor cores.
+//
+// An append step attends n_q new queries per query head to (segment 0) the
+// whole archive [0, lo) and (segment 1) the window plus the new entries
+// [lo, hi), with the reference's merge_states(archive, window) on top, and it
+// needs, per query head and position, the mean attention weight over the n_q
+// rows (a_cpu -> StoreTier.reevaluate, a_gpu -> the window MAW). The keys are
+// consecutive positions, so this is GEMM-shaped: per (batch, kv-head) the
+// G * n_q query rows (head-major: row = g * n_q + i) form the M side.
+//
+//   append_attend_kernel<D, 1>  split-K over chunks of ACHUNK keys: one CTA per
+//       (batch x kv-head, row group, segment, chunk); a producer warp TMA-loads
+//       32-key stages (2-D tile box, one op per stage) into a ring, each
+//       consumer warp owns 16 query rows: S = Q K^T and O += P V on mma.sync
+//       m16n8k16 (P as bf16 hi + lo), fp32 online softmax -> (m, z, acc) per row.
+//   append_fold_kernel<D>       one warp per (batch x kv-head, row): folds the
+//       chunk partials of each segment in chunk order, merge_states, out/lse,
+//       and keeps each row's final (m, z) per segment.
+//   append_attend_kernel<D, 2>  same tiling, recomputes S with the final
+//       statistics: w = exp(s - m) / z, and writes per (query head, position)
+//       the mean of w over the head's n_q rows (fixed summation order).
+// Deterministic: fixed partition and fixed fold / summation orders.
+#include "hgca_common.cuh"
+#include "hgca_internal.h"
+#include "hgca_tc.cuh"
+
+#include <cuda.h>
+
+namespace hgca {
+
+constexpr uint32_t FULL_MASK = 0xffffffffu;
+constexpr int AK = 32;          // keys per stage
+constexpr int ACHUNK = 4096;    // keys per split-K item
+constexpr int AS = 4;           // stages in the ring
+constexpr int AMAXW = 8;        // consumer warps per CTA -> <= 128 query rows per row group
+
+struct AppendArgs {
+  CUtensorMap kmap;             // 2-D tile map over KV [B*Hkv*T rows, 2D], box {2D, 32}
+  const __nv_bfloat16* q;       // [B*Hq, nq, D]
+  int64_t B, Hq, Hkv, G, T, nq;
+  float scale;
+  int64_t seg_lo[2], seg_hi[2];  // 0 = archive [0, lo), 1 = window + kv_in [lo, hi)
+  int64_t nch[2];                // split-K chunks per segment
+  int64_t R, RG, n_rg;           // rows per (batch, kv-head), rows per row group, row groups
+  int64_t n_items;
+  float* part_acc;               // [n_items][RG][D]
+  float* part_m;                 // [n_items][RG]
+  float* part_z;
+  float* fin;                    // [B*Hkv][R][2 segments][m, z]
+  float* out;                    // [B*Hq, nq, D]
+  double* lse;                   // [B*Hq, nq]
+  float* mean[2];                // [B*Hq, mean_ld] mean weights per position, or null
+  int64_t mean_ld[2];
+};
+
+template <int D, int PASS>
+struct AppendCfg {
+  static constexpr int ROWB = 2 * D * 2;                 // bytes of one rotated K|V row pair
+  static constexpr int STAGE = AK * ROWB;
+  static constexpr int OFF_W = AS * STAGE;               // pass 2: weights [RG <= 128][AK] fp32
+  static constexpr int OFF_BAR = OFF_W + (PASS == 2 ? AMAXW * 16 * AK * 4 : 0);
+  static constexpr int SMEM = OFF_BAR + 2 * AS * 8 + 1024;  // + alignment slack
+};
+
+template <int D>
+__device__ __forceinline__ uint32_t arot(int r, int c, int rot) {
+  return (uint32_t)(r * 4 * D + (((c & ~7) | ((c ^ rot) & 7)) << 4));
+}
+
+// item id -> (bk, row group, segment, chunk)
+__device__ __forceinline__ void append_item(const AppendArgs& a, int64_t id, int64_t& bk, int64_t& rg, int& seg,
+                                            int64_t& chunk) {
+  const int64_t nc = a.nch[0] + a.nch[1];
+  const int64_t c = id % nc;
+  const int64_t t = id / nc;
+  rg = t % a.n_rg;
+  bk = t / a.n_rg;
+  seg = c < a.nch[0] ? 0 : 1;
+  chunk = seg ? c - a.nch[0] : c;
+}
+
+template <int D, int PASS>
+__global__ void __launch_bounds__((AMAXW + 1) * 32, 1) append_attend_kernel(const __grid_constant__ AppendArgs a) {
+  using C = AppendCfg<D, PASS>;
+  constexpr int KC = D / 16;
+  extern __shared__ unsigned char sm_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);
+  uint64_t* empty = full + AS;
+  float* wbuf = reinterpret_cast<float*>(sm + C::OFF_W);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int NW = (int)(blockDim.x >> 5) - 1;  // consumer warps
+  int64_t bk, rg, chunk;
+  int seg;
+  append_item(a, blockIdx.x, bk, rg, seg, chunk);
+  const int64_t p0 = a.seg_lo[seg] + chunk * ACHUNK;
+  const int64_t p1 = min(a.seg_hi[seg], p0 + ACHUNK);
+  const int nst = (int)((p1 - p0 + AK - 1) / AK);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < AS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == NW) {  // ----------------------------------------------- producer
+    if (lane == 0) {
+      const uint64_t policy = l2_evict_first_policy();
+      const int rowbase = (int)(bk * a.T + p0);
+      for (int st = 0; st < nst; ++st) {
+        const int s = st % AS;
+        if (st >= AS) mbar_wait(&empty[s], ((st / AS) - 1) & 1);
+        mbar_expect_tx(&full[s], C::STAGE);
+        tma_load_2d(smem_u32(sm + s * C::STAGE), &a.kmap, 0, rowbase + st * AK, &full[s], policy);
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------ consumer
+  const int g4 = lane >> 2, t4 = lane & 3, mi = lane >> 3;
+  const int r0 = warp * 16;                                   // first row of this warp in the group
+  const int64_t rowA = rg * a.RG + r0 + g4, rowB = rowA + 8;  // rows of this lane in the (b, kv-head)
+  const bool okA = r0 + g4 < a.RG && rowA < a.R, okB = r0 + g4 + 8 < a.RG && rowB < a.R;
+  const int64_t b = bk / a.Hkv, kvh = bk % a.Hkv;
+  const __nv_bfloat16* qbase = a.q + (b * a.Hq + kvh * a.G) * a.nq * D;  // rows of this (b, kv-head)
+  // Q A-fragments for all k16 chunks (rows r0..r0+15 of the group)
+  uint32_t qa[KC][4];
+  {
+    const uint32_t* qA = reinterpret_cast<const uint32_t*>(qbase + rowA * D);
+    const uint32_t* qB = reinterpret_cast<const uint32_t*>(qbase + rowB * D);
+#pragma unroll
+    for (int kc = 0; kc < KC; ++kc) {
+      qa[kc][0] = okA ? qA[kc * 8 + t4] : 0u;
+      qa[kc][1] = okB ? qB[kc * 8 + t4] : 0u;
+      qa[kc][2] = okA ? qA[kc * 8 + 4 + t4] : 0u;
+      qa[kc][3] = okB ? qB[kc * 8 + 4 + t4] : 0u;
+    }
+  }
+  // pass 2: the rows' final statistics of this segment
+  float fmA = 0.f, fzA = 1.f, fmB = 0.f, fzB = 1.f;
+  if (PASS == 2) {
+    if (okA) { fmA = a.fin[((bk * a.R + rowA) * 2 + seg) * 2]; fzA = a.fin[((bk * a.R + rowA) * 2 + seg) * 2 + 1]; }
+    if (okB) { fmB = a.fin[((bk * a.R + rowB) * 2 + seg) * 2]; fzB = a.fin[((bk * a.R + rowB) * 2 + seg) * 2 + 1]; }
+  }
+  const float rzA = 1.f / fzA, rzB = 1.f / fzB;
+  // pass 2: the (query head, key) mean targets of this thread, fixed for the item
+  // (at most G*AK / 32 = 8 per thread: heads*AK pairs over ceil(RG/16) warps, RG <= 128)
+  int64_t mdst[8];
+  int mrow[8], mkey[8];
+  int n_mt = 0;
+  if (PASS == 2 && a.mean[seg]) {
+    const int heads = (int)(a.RG / a.nq);  // row groups hold whole heads
+    const int64_t g0 = (rg * a.RG) / a.nq;
+    for (int t = threadIdx.x; t < heads * AK && n_mt < 8; t += NW * 32) {
+      const int hl = t / AK, k = t % AK;
+      if (g0 + hl >= a.G) break;
+      mrow[n_mt] = hl * (int)a.nq;
+      mkey[n_mt] = k;
+      mdst[n_mt] = (b * a.Hq + kvh * a.G + g0 + hl) * a.mean_ld[seg] - a.seg_lo[seg] + k;
+      ++n_mt;
+    }
+  }
+  const float inv_nq = 1.f / (float)a.nq;
+  float o[D / 8][4];
+#pragma unroll
+  for (int n = 0; n < D / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+  float mA = -INFINITY, mB = -INFINITY, zA = 0.f, zB = 0.f;
+
+  for (int st = 0; st < nst; ++st) {
+    const int s = st % AS;
+    mbar_wait(&full[s], (st / AS) & 1);
+    const uint32_t stg = smem_u32(sm + s * C::STAGE);
+    const int64_t kp0 = p0 + (int64_t)st * AK;  // position of key 0 of the stage
+    // ---- S = Q K^T for the 32 keys: 4 n-tiles of 8 keys
+    float sc[4][4];
+#pragma unroll
+    for (int n = 0; n < 4; ++n) sc[n][0] = sc[n][1] = sc[n][2] = sc[n][3] = 0.f;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int key = j * 16 + (mi >> 1) * 8 + (lane & 7);
+      const int rot = (int)((kp0 + key) & 7);
+#pragma unroll
+      for (int kc = 0; kc < KC; ++kc) {
+        uint32_t kb[4];
+        ldsm_x4(stg + arot<D>(key, 2 * kc + (mi & 1), rot), kb);
+        mma_bf16(sc[2 * j], qa[kc], kb[0], kb[1]);
+        mma_bf16(sc[2 * j + 1], qa[kc], kb[2], kb[3]);
+      }
+    }
+    // ---- scale + mask (keys past the segment end)
+#pragma unroll
+    for (int n = 0; n < 4; ++n) {
+      const int64_t kpos = kp0 + n * 8 + 2 * t4;
+      const bool v0 = kpos < p1, v1 = kpos + 1 < p1;
+      sc[n][0] = v0 ? sc[n][0] * a.scale : -INFINITY;
+      sc[n][1] = v1 ? sc[n][1] * a.scale : -INFINITY;
+      sc[n][2] = v0 ? sc[n][2] * a.scale : -INFINITY;
+      sc[n][3] = v1 ? sc[n][3] * a.scale : -INFINITY;
+    }
+    if constexpr (PASS == 1) {
+      // ---- online softmax per row (rows g4 | g4 + 8), reduced over the 4 lanes sharing g4
+      float xA = -INFINITY, xB = -INFINITY;
+#pragma unroll
+      for (int n = 0; n < 4; ++n) {
+        xA = fmaxf(xA, fmaxf(sc[n][0], sc[n][1]));
+        xB = fmaxf(xB, fmaxf(sc[n][2], sc[n][3]));
+      }
+#pragma unroll
+      for (int off = 1; off < 4; off <<= 1) {
+        xA = fmaxf(xA, __shfl_xor_sync(FULL_MASK, xA, off));
+        xB = fmaxf(xB, __shfl_xor_sync(FULL_MASK, xB, off));
+      }
+      const float nA = fmaxf(mA, xA), nB = fmaxf(mB, xB);
+      const float alA = nA == -INFINITY ? 1.f : __expf(mA - nA);
+      const float alB = nB == -INFINITY ? 1.f : __expf(mB - nB);
+      float sA = 0.f, sB = 0.f;
+#pragma unroll
+      for (int n = 0; n < 4; ++n) {
+        sc[n][0] = sc[n][0] == -INFINITY ? 0.f : __expf(sc[n][0] - nA);
+        sc[n][1] = sc[n][1] == -INFINITY ? 0.f : __expf(sc[n][1] - nA);
+        sc[n][2] = sc[n][2] == -INFINITY ? 0.f : __expf(sc[n][2] - nB);
+        sc[n][3] = sc[n][3] == -INFINITY ? 0.f : __expf(sc[n][3] - nB);
+        sA += sc[n][0] + sc[n][1];
+        sB += sc[n][2] + sc[n][3];
+      }
+#pragma unroll
+      for (int off = 1; off < 4; off <<= 1) {
+        sA += __shfl_xor_sync(FULL_MASK, sA, off);
+        sB += __shfl_xor_sync(FULL_MASK, sB, off);
+      }
+      zA = zA * alA + sA;
+      zB = zB * alB + sB;
+      mA = nA;
+      mB = nB;
+#pragma unroll
+      for (int n = 0; n < D / 8; ++n) {
+        o[n][0] *= alA; o[n][1] *= alA; o[n][2] *= alB; o[n][3] *= alB;
+      }
+      // ---- O += P V: P (rows x 16 keys) as A fragments straight from the S
+      // fragments (bf16 hi + lo), V as the B operand via ldmatrix.trans
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        uint32_t ph[4], pl[4];
+        ph[0] = pack_bf16(sc[2 * j][0], sc[2 * j][1]);
+        ph[1] = pack_bf16(sc[2 * j][2], sc[2 * j][3]);
+        ph[2] = pack_bf16(sc[2 * j + 1][0], sc[2 * j + 1][1]);
+        ph[3] = pack_bf16(sc[2 * j + 1][2], sc[2 * j + 1][3]);
+        pl[0] = pack_bf16(sc[2 * j][0] - bf16_lo_f(ph[0]), sc[2 * j][1] - bf16_hi_f(ph[0]));
+        pl[1] = pack_bf16(sc[2 * j][2] - bf16_lo_f(ph[1]), sc[2 * j][3] - bf16_hi_f(ph[1]));
+        pl[2] = pack_bf16(sc[2 * j + 1][0] - bf16_lo_f(ph[2]), sc[2 * j + 1][1] - bf16_hi_f(ph[2]));
+        pl[3] = pack_bf16(sc[2 * j + 1][2] - bf16_lo_f(ph[3]), sc[2 * j + 1][3] - bf16_hi_f(ph[3]));
+        const int key = j * 16 + (mi & 1) * 8 + (lane & 7);
+        const int rot = (int)((kp0 + key) & 7);
+#pragma unroll
+        for (int dp = 0; dp < D / 16; ++dp) {
+          uint32_t vb[4];
+          ldsm_x4_t(stg + arot<D>(key, D / 8 + 2 * dp + (mi >> 1), rot), vb);
+          mma_bf16(o[2 * dp], ph, vb[0], vb[1]);
+          mma_bf16(o[2 * dp], pl, vb[0], vb[1]);
+          mma_bf16(o[2 * dp + 1], ph, vb[2], vb[3]);
+          mma_bf16(o[2 * dp + 1], pl, vb[2], vb[3]);
+        }
+      }
+    } else {
+      // ---- pass 2: final weights of the rows, staged for the per-head means
+#pragma unroll
+      for (int n = 0; n < 4; ++n) {
+        const int k0 = n * 8 + 2 * t4;
+        wbuf[(r0 + g4) * AK + k0] = sc[n][0] == -INFINITY ? 0.f : __expf(sc[n][0] - fmA) * rzA;
+        wbuf[(r0 + g4) * AK + k0 + 1] = sc[n][1] == -INFINITY ? 0.f : __expf(sc[n][1] - fmA) * rzA;
+        wbuf[(r0 + g4 + 8) * AK + k0] = sc[n][2] == -INFINITY ? 0.f : __expf(sc[n][2] - fmB) * rzB;
+        wbuf[(r0 + g4 + 8) * AK + k0 + 1] = sc[n][3] == -INFINITY ? 0.f : __expf(sc[n][3] - fmB) * rzB;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // stage consumed
+    if constexpr (PASS == 2) {
+      // all consumers' weights of this stage are in wbuf: per (query head of
+      // this row group, key) the mean over the head's nq rows, in row order
+      asm volatile("bar.sync 1, %0;\n" ::"r"(NW * 32) : "memory");
+      for (int j = 0; j < n_mt; ++j) {
+        if (kp0 + mkey[j] >= p1) continue;
+        float acc = 0.f;
+        for (int i = 0; i < (int)a.nq; ++i) acc += wbuf[(mrow[j] + i) * AK + mkey[j]];
+        a.mean[seg][mdst[j] + kp0] = acc * inv_nq;
+      }
+      asm volatile("bar.sync 1, %0;\n" ::"r"(NW * 32) : "memory");
+    }
+  }
+  if constexpr (PASS == 1) {
+    // partial (m, z, acc) of this item's rows
+    const int64_t item = blockIdx.x;
+    if (t4 == 0) {
+      if (r0 + g4 < a.RG) {
+        a.part_m[item * a.RG + r0 + g4] = mA;
+        a.part_z[item * a.RG + r0 + g4] = zA;
+      }
+      if (r0 + g4 + 8 < a.RG) {
+        a.part_m[item * a.RG + r0 + g4 + 8] = mB;
+        a.part_z[item * a.RG + r0 + g4 + 8] = zB;
+      }
+    }
+    float* pa = a.part_acc + item * a.RG * D;
+#pragma unroll
+    for (int n = 0; n < D / 8; ++n) {
+      const int c = n * 8 + 2 * t4;
+      if (r0 + g4 < a.RG) { pa[(r0 + g4) * D + c] = o[n][0]; pa[(r0 + g4) * D + c + 1] = o[n][1]; }
+      if (r0 + g4 + 8 < a.RG) { pa[(r0 + g4 + 8) * D + c] = o[n][2]; pa[(r0 + g4 + 8) * D + c + 1] = o[n][3]; }
+    }
+  }
+}
+
+// One warp per (b, kv-head, row): fold the chunk partials of both segments,
+// merge_states(archive, window) (attention.py:153-188), out / lse, and the
+// row's final (m, z) per segment for pass 2.
+template <int D>
+__global__ void __launch_bounds__(256) append_fold_kernel(const __grid_constant__ AppendArgs a) {
+  constexpr int DPL = D / 32;
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t BK = a.B * a.Hkv;
+  if (wid >= BK * a.R) return;
+  const int64_t bk = wid / a.R, row = wid % a.R;
+  const int64_t rg = row / a.RG, rr = row % a.RG;
+  const int64_t nc = a.nch[0] + a.nch[1];
+  const int64_t base = (bk * a.n_rg + rg) * nc;
+  float so[2][DPL];
+  double lse_seg[2];
+  for (int seg = 0; seg < 2; ++seg) {
+    const int64_t c0 = seg ? a.nch[0] : 0, c1 = seg ? nc : a.nch[0];
+    float M = -INFINITY;
+    for (int64_t c = c0; c < c1; ++c) M = fmaxf(M, a.part_m[(base + c) * a.RG + rr]);
+    float Z = 0.f, acc[DPL];
+#pragma unroll
+    for (int k = 0; k < DPL; ++k) acc[k] = 0.f;
+    if (M != -INFINITY) {
+      for (int64_t c = c0; c < c1; ++c) {
+        const float mc = a.part_m[(base + c) * a.RG + rr];
+        if (mc == -INFINITY) continue;
+        const float w = __expf(mc - M);
+        Z += a.part_z[(base + c) * a.RG + rr] * w;
+        const float* pa = a.part_acc + ((base + c) * a.RG + rr) * D + lane * DPL;
+#pragma unroll
+        for (int k = 0; k < DPL; ++k) acc[k] += w * pa[k];
+      }
+    }
+    const bool empty = !(Z > 0.f);
+#pragma unroll
+    for (int k = 0; k < DPL; ++k) so[seg][k] = empty ? 0.f : acc[k] / Z;
+    lse_seg[seg] = empty ? -INFINITY : (double)M + log((double)Z);
+    if (lane == 0) {
+      a.fin[((bk * a.R + row) * 2 + seg) * 2] = M;
+      a.fin[((bk * a.R + row) * 2 + seg) * 2 + 1] = empty ? 1.f : Z;
+    }
+  }
+  const double mm = fmax(lse_seg[0], lse_seg[1]);
+  const bool both_empty = mm == -INFINITY;
+  const double ms = both_empty ? 0.0 : mm;
+  const double wa = exp(lse_seg[0] - ms), wb = exp(lse_seg[1] - ms);
+  const double zs = both_empty ? 1.0 : wa + wb;
+  const float ca = (float)(wa / zs), cb = (float)(wb / zs);
+  const int64_t b = bk / a.Hkv, kvh = bk % a.Hkv;
+  const int64_t g = row / a.nq, i = row % a.nq;
+  const int64_t orow = (b * a.Hq + kvh * a.G + g) * a.nq + i;
+#pragma unroll
+  for (int k = 0; k < DPL; ++k)
+    a.out[orow * D + lane * DPL + k] = __fadd_rn(__fmul_rn(ca, so[0][k]), __fmul_rn(cb, so[1][k]));
+  if (lane == 0) a.lse[orow] = both_empty ? -INFINITY : ms + log(zs);
+}
+
+// ------------------------------------------------------------------ launcher
+typedef CUresult (*EncodeTiledFnA)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static int make_tile_map(CUtensorMap* map, const void* base, int64_t rows, int64_t D) {
+  static EncodeTiledFnA encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q) != cudaSuccess ||
+        !encode)
+      return -3000;
+  }
+  cuuint64_t gdim[2] = {(cuuint64_t)(2 * D), (cuuint64_t)rows};
+  cuuint64_t gstr[1] = {(cuuint64_t)(2 * D * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)(2 * D), (cuuint32_t)AK};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), gdim, gstr, box, es,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -3001;
+}
+
+// Layout of the caller's workspace for one append step (all sizes in bytes).
+struct AppendPlan {
+  int64_t R, RG, n_rg, nch0, nch1, n_items;
+  int64_t off_acc, off_m, off_z, off_fin, bytes;
+};
+
+static AppendPlan append_plan(int64_t B, int64_t Hq, int64_t Hkv, int64_t D, int64_t nq, int64_t lo, int64_t hi) {
+  AppendPlan p{};
+  const int64_t G = Hq / Hkv;
+  p.R = G * nq;
+  // row groups of <= AMAXW*16 rows holding whole query heads (nq <= 128)
+  const int64_t heads_per_group = (AMAXW * 16) / nq;
+  p.RG = (heads_per_group >= G ? G : heads_per_group) * nq;
+  p.n_rg = (p.R + p.RG - 1) / p.RG;
+  p.nch0 = (lo + ACHUNK - 1) / ACHUNK;
+  p.nch1 = (hi - lo + ACHUNK - 1) / ACHUNK;
+  p.n_items = B * Hkv * p.n_rg * (p.nch0 + p.nch1);
+  auto al = [](int64_t x) { return (x + 255) / 256 * 256; };
+  p.off_acc = 0;
+  p.off_m = al(p.n_items * p.RG * D * 4);
+  p.off_z = p.off_m + al(p.n_items * p.RG * 4);
+  p.off_fin = p.off_z + al(p.n_items * p.RG * 4);
+  p.bytes = p.off_fin + al(B * Hkv * p.R * 4 * 4);
+  return p;
+}
+
+int64_t append_ws_bytes(int64_t B, int64_t Hq, int64_t Hkv, int64_t D, int64_t nq, int64_t lo, int64_t hi) {
+  if (nq < 1 || nq > AMAXW * 16 || Hkv < 1 || Hq % Hkv) return -1;
+  return append_plan(B, Hq, Hkv, D, nq, lo, hi).bytes;
+}
+
+template <int D>
+static int launch_append_d(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, int64_t T, const void* q, int64_t nq,
+                           double scale, int64_t lo, int64_t hi, float* out, double* lse, float* mean_archive,
+                           float* mean_window, void* ws, cudaStream_t s) {
+  using C1 = AppendCfg<D, 1>;
+  using C2 = AppendCfg<D, 2>;
+  const AppendPlan p = append_plan(B, Hq, Hkv, D, nq, lo, hi);
+  AppendArgs a{};
+  {
+    static const void* cached_base = nullptr;
+    static int64_t cached_rows = -1;
+    static CUtensorMap cached;
+    const int64_t rows = B * Hkv * T;
+    if (cached_base != KV || cached_rows != rows) {
+      const int rc = make_tile_map(&cached, KV, rows, D);
+      if (rc) return rc;
+      cached_base = KV;
+      cached_rows = rows;
+    }
+    a.kmap = cached;
+  }
+  a.q = reinterpret_cast<const __nv_bfloat16*>(q);
+  a.B = B; a.Hq = Hq; a.Hkv = Hkv; a.G = Hq / Hkv; a.T = T; a.nq = nq;
+  a.scale = (float)scale;
+  a.seg_lo[0] = 0; a.seg_hi[0] = lo; a.seg_lo[1] = lo; a.seg_hi[1] = hi;
+  a.nch[0] = p.nch0; a.nch[1] = p.nch1;
+  a.R = p.R; a.RG = p.RG; a.n_rg = p.n_rg; a.n_items = p.n_items;
+  unsigned char* w = reinterpret_cast<unsigned char*>(ws);
+  a.part_acc = reinterpret_cast<float*>(w + p.off_acc);
+  a.part_m = reinterpret_cast<float*>(w + p.off_m);
+  a.part_z = reinterpret_cast<float*>(w + p.off_z);
+  a.fin = reinterpret_cast<float*>(w + p.off_fin);
+  a.out = out; a.lse = lse;
+  a.mean[0] = mean_archive; a.mean_ld[0] = lo;
+  a.mean[1] = mean_window; a.mean_ld[1] = hi - lo;
+  static bool attr1 = false, attr2 = false;
+  if (!attr1) {
+    cudaError_t e = cudaFuncSetAttribute(append_attend_kernel<D, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, C1::SMEM);
+    if (e != cudaSuccess) return (int)e;
+    e = cudaFuncSetAttribute(append_attend_kernel<D, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, C2::SMEM);
+    if (e != cudaSuccess) return (int)e;
+    attr1 = attr2 = true;
+  }
+  const int nw = (int)((p.RG + 15) / 16);
+  if (p.n_items > 0) append_attend_kernel<D, 1><<<(unsigned)p.n_items, (nw + 1) * 32, C1::SMEM, s>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return (int)e;
+  const int64_t warps = B * Hkv * p.R;
+  append_fold_kernel<D><<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(a);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return (int)e;
+  if ((mean_archive || mean_window) && p.n_items > 0)
+    append_attend_kernel<D, 2><<<(unsigned)p.n_items, (nw + 1) * 32, C2::SMEM, s>>>(a);
+  return (int)cudaGetLastError();
+}
+
+int launch_append_bf16(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, int64_t T, int64_t D, const void* q,
+                       int64_t nq, double scale, int64_t lo, int64_t hi, float* out, double* lse, float* mean_archive,
+                       float* mean_window, void* ws, cudaStream_t s) {
+  if (D == 128)
+    return launch_append_d<128>(KV, B, Hq, Hkv, T, q, nq, scale, lo, hi, out, lse, mean_archive, mean_window, ws, s);
+  if (D == 64)
+    return launch_append_d<64>(KV, B, Hq, Hkv, T, q, nq, scale, lo, hi, out, lse, mean_archive, mean_window, ws, s);
+  return -1001;
+}
+
+}  // namespace hgca

@@ -349,6 +349,28 @@ static int decode_prepare(const hgca_decode_desc* d, DecodeArgs& a, DecodeMergeA
   return HGCA_OK;
 }
 
+int64_t hgca_append_ws_bytes(int64_t B, int64_t Hq, int64_t Hkv, int64_t D, int64_t nq, int64_t lo, int64_t hi) {
+  if (B < 1 || lo < 0 || hi <= lo) return -1;
+  return append_ws_bytes(B, Hq, Hkv, D, nq, lo, hi);
+}
+
+int hgca_append_bf16(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, int64_t T, int64_t D, const void* q,
+                     int64_t nq, double scale, int64_t lo, int64_t hi, float* out, double* lse, float* mean_archive,
+                     float* mean_window, void* ws, int64_t ws_bytes, hgca_stream_t stream) {
+  if (B < 1 || Hkv < 1 || Hq % Hkv || Hq / Hkv > 8 || (D != 64 && D != 128))
+    return fail(HGCA_EINVAL, "append_bf16: bad heads / head_dim");
+  if (nq < 1 || nq > 128) return fail(HGCA_EINVAL, "append_bf16: n_q must be in [1, 128], got %lld", (long long)nq);
+  if (lo < 0 || hi <= lo || hi > T) return fail(HGCA_EINVAL, "append_bf16: bad position range");
+  if (!KV || !q || !out || !lse || !ws) return fail(HGCA_EINVAL, "append_bf16: null pointer");
+  const int64_t need = append_ws_bytes(B, Hq, Hkv, D, nq, lo, hi);
+  if (need < 0 || ws_bytes < need)
+    return fail(HGCA_EINVAL, "append_bf16: workspace holds %lld bytes, needs %lld", (long long)ws_bytes,
+                (long long)need);
+  return cuda_status(launch_append_bf16(KV, B, Hq, Hkv, T, D, q, nq, scale, lo, hi, out, lse, mean_archive,
+                                        mean_window, ws, S(stream)),
+                     "append_bf16");
+}
+
 int hgca_decode_step_host(const hgca_decode_desc* d, const void* in_host, void* in_dev, int64_t in_bytes,
                           void* out_host, const void* out_dev, int64_t out_bytes, hgca_stream_t stream) {
   if (in_bytes < 0 || out_bytes < 0 || (in_bytes && (!in_host || !in_dev)) || (out_bytes && (!out_host || !out_dev)))

@@ -112,6 +112,10 @@ int launch_union_build(const uint32_t* sel, int64_t B, int64_t Hq, int64_t Hkv, 
 int launch_write_rows(int dtype, void* KV, int64_t BH, int64_t T, int64_t D, int64_t pos,
                       const void* k_new, const void* v_new, int64_t n, cudaStream_t s);
 int decode_chunk_rows(int dtype, int64_t D);
+int64_t append_ws_bytes(int64_t B, int64_t Hq, int64_t Hkv, int64_t D, int64_t nq, int64_t lo, int64_t hi);
+int launch_append_bf16(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, int64_t T, int64_t D, const void* q,
+                       int64_t nq, double scale, int64_t lo, int64_t hi, float* out, double* lse, float* mean_archive,
+                       float* mean_window, void* ws, cudaStream_t s);
 int decode_config(int dtype, int64_t D, int64_t G, int64_t* out);
 int launch_maw_update(const float* w, int64_t BH, int64_t nq, int64_t W, int64_t w_ld, double* maw,
                       int64_t T, int64_t p0, int64_t w_old, double alpha, int mode, cudaStream_t s);

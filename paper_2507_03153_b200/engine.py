@@ -525,6 +525,8 @@ class HybridEngine:
         w_size = nxt - lo
         W = w_size + nq
         odt = torch.float32
+        if self.tdtype == torch.bfloat16 and not self.config.keep_weights and nq <= 128:
+            return self._append_tc(ls, q, nq, squeeze)
         # sparse partial over the whole archive, with weights (engine.py:127-132)
         s_out = torch.zeros((BHq, nq, self.D), dtype=odt, device=self.dev)
         s_lse = torch.full((BHq, nq), -math.inf, dtype=torch.float64, device=self.dev)
@@ -574,6 +576,53 @@ class HybridEngine:
         if squeeze:
             o, l, ag = o[0], l[0], ag[0]
         return StepOutput(o, l, ag, a_cpu, np.arange(lo, nxt + nq, dtype=np.int64))
+
+    def _append_tc(self, ls, q, nq, squeeze):
+        """Append step for bf16 storage on the tensor cores (hgca_append_bf16):
+        archive + window attention, merge_states, and the per-head row-mean
+        weights a_cpu / a_gpu feed the reference maintenance directly
+        (engine.py:175-186): the window MAW EMA / init and
+        StoreTier.reevaluate + re-selection. The per-row weight matrices are
+        not materialised (StepOutput a_gpu / a_cpu are None; use
+        keep_weights=True for them)."""
+        s = self._stream()
+        BHq = self.B * self.Hq
+        lo, nxt = ls.lo, ls.nxt
+        w_size = nxt - lo
+        W, hi = w_size + nq, nxt + nq
+        out = torch.empty((BHq, nq, self.D), dtype=torch.float32, device=self.dev)
+        lse = torch.empty((BHq, nq), dtype=torch.float64, device=self.dev)
+        mean_a = torch.empty((BHq, max(lo, 1)), dtype=torch.float32, device=self.dev)
+        mean_w = torch.empty((BHq, W), dtype=torch.float32, device=self.dev)
+        nb = int(_lib.load().hgca_append_ws_bytes(self.B, self.Hq, self.Hkv, self.D, nq, lo, hi))
+        ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=self.dev)
+        _lib.call("hgca_append_bf16", ls.KV.data_ptr(), self.B, self.Hq, self.Hkv, self.T, self.D, q.data_ptr(), nq,
+                  float(self.shape.scale), lo, hi, out.data_ptr(), lse.data_ptr(),
+                  mean_a.data_ptr() if lo else None, mean_w.data_ptr(), ws.data_ptr(), nb, s)
+        # maintenance (engine.py:175-186): the kernel already took the row means
+        _lib.call("hgca_maw_update", mean_w.data_ptr(), BHq, 1, W, W, ls.maw.data_ptr(), self.T, lo, w_size,
+                  float(self.config.cache.alpha), 0, s)
+        ev_lo, ev_hi = self._evict_range(ls, nq)
+        if lo:
+            _lib.call("hgca_maw_update", mean_a.data_ptr(), BHq, 1, lo, lo, ls.maw.data_ptr(), self.T, 0, 0,
+                      float(self.config.cache.alpha), 1, s)
+            if self.config.selection == "threshold":
+                _lib.call("hgca_select_threshold", ls.maw.data_ptr(), BHq, self.T, 0, lo,
+                          float(self.config.cache.beta), int(lo), ls.ctx.data_ptr(), ls.ctx.shape[1], 1,
+                          self._keep_ptr(ls), s)
+        if ev_hi > ev_lo:
+            self._ingest(ls, ev_lo, ev_hi, w_size + nq)
+        elif lo:
+            self._refresh_selection(ls)
+        if ls.window_size + nq > self.cap:
+            raise ContractError(f"append of {nq} entries overflows window capacity {self.cap}")
+        ls.nxt += nq
+        self.launches += 5
+        o = out.view(self.B, self.Hq, nq, self.D)
+        l = lse.view(self.B, self.Hq, nq)
+        if squeeze:
+            o, l = o[0], l[0]
+        return StepOutput(o, l, None, None, np.arange(lo, nxt + nq, dtype=np.int64))
 
     # ------------------------------------------------------------ inspection
     def context_indices(self, layer_idx=0):

@@ -301,3 +301,39 @@ def test_decode_host_packed_matches_device_path(cuda):
     for (o1, l1), (o2, l2) in zip(*outs):
         np.testing.assert_array_equal(o1, o2)
         np.testing.assert_array_equal(l1, l2)
+
+
+@pytest.mark.parametrize("nq,Hq,Hkv,d", [(16, 8, 2, 128), (5, 8, 4, 128), (1, 4, 4, 64), (40, 8, 2, 64)])
+def test_bf16_append_tensor_core_path_matches_reference_path(cuda, nq, Hq, Hkv, d):
+    """hgca_append_bf16 (tensor cores, row-mean weights in-kernel) against the
+    reference-order fp64 path (keep_weights=True) on the same staged state: the
+    step output, lse, and the re-evaluated archive / EMA'd window MAW."""
+    res = []
+    for keep in (True, False):
+        cfg = cuda.EngineConfig(layers=1, heads=Hq, kv_heads=Hkv, head_dim=d, batch=2, dtype="bfloat16",
+                                cache=cuda.CacheConfig(blk_num=8, blk_size=32, beta=1.0),
+                                core_count=10 ** 6, max_positions=6000, keep_weights=keep)
+        eng = cuda.HybridEngine(cfg)
+        g = torch.Generator(device="cuda").manual_seed(77)
+        n = 4096 + 37  # archive not a multiple of the 4096-key chunk
+        k = torch.randn((2, Hkv, n, d), generator=g, device="cuda").to(torch.bfloat16)
+        v = torch.randn((2, Hkv, n, d), generator=g, device="cuda").to(torch.bfloat16)
+        maw = torch.rand((2, Hq, n), generator=g, device="cuda", dtype=torch.float64) / 256
+        eng.bulk_ingest(0, k, v, maw, 256)
+        for _ in range(100):
+            q = torch.randn((2, Hq, 1, d), generator=g, device="cuda").to(torch.bfloat16)
+            kk = torch.randn((2, Hkv, 1, d), generator=g, device="cuda").to(torch.bfloat16)
+            eng.step(0, cuda.StepInput("decode", q, kk, kk))
+        q = torch.randn((2, Hq, nq, d), generator=g, device="cuda").to(torch.bfloat16)
+        kk = torch.randn((2, Hkv, nq, d), generator=g, device="cuda").to(torch.bfloat16)
+        ls = eng.layers[0]
+        lo, nxt = ls.lo, ls.nxt
+        r = eng.step(0, cuda.StepInput("append", q, kk, -kk))
+        torch.cuda.synchronize()
+        res.append((r.output.cpu().numpy(), r.lse.cpu().numpy(), ls.maw[:, :nxt + nq].cpu().numpy(), lo, nxt))
+    (o1, l1, m1, lo, nxt), (o2, l2, m2, _, _) = res
+    assert rel_err(o2, o1) <= 1e-3
+    np.testing.assert_allclose(l2, l1, rtol=0, atol=1e-4)
+    # archive MAW = re-evaluated row means; window = EMA / init from the window weights
+    np.testing.assert_allclose(m2[:, :lo], m1[:, :lo], rtol=2e-3, atol=1e-9)
+    np.testing.assert_allclose(m2[:, lo:], m1[:, lo:], rtol=2e-3, atol=1e-9)
