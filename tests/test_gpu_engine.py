@@ -337,3 +337,33 @@ def test_bf16_append_tensor_core_path_matches_reference_path(cuda, nq, Hq, Hkv, 
     # archive MAW = re-evaluated row means; window = EMA / init from the window weights
     np.testing.assert_allclose(m2[:, :lo], m1[:, :lo], rtol=2e-3, atol=1e-9)
     np.testing.assert_allclose(m2[:, lo:], m1[:, lo:], rtol=2e-3, atol=1e-9)
+
+
+def test_accuracy_metrics_full_selection_and_top1(cuda, rng):
+    """accuracy.step_metrics (harness.py:147-160 on the GPU): with beta = 0 every
+    archived entry is selected, so the hybrid step equals full attention (eps ~ 0,
+    no bound violation); with a 1-entry top-k context the dropped mass is large
+    but the error stays within 2*eps*max|V| (the reference's guarantee)."""
+    from paper_2507_03153_b200 import accuracy
+
+    for kw in (dict(cache=cuda.CacheConfig(blk_num=4, blk_size=16, beta=0.0)),
+               dict(cache=cuda.CacheConfig(blk_num=4, blk_size=16, beta=1.0), selection="topk", topk=1)):
+        cfg = cuda.EngineConfig(layers=1, heads=4, kv_heads=2, head_dim=64, batch=2, core_count=64,
+                                max_positions=512, **kw)
+        eng = cuda.HybridEngine(cfg)
+        for _ in range(300):
+            q, k, v = (torch.from_numpy(rng.standard_normal(s).astype(np.float32)).cuda()
+                       for s in ((2, 4, 1, 64), (2, 2, 1, 64), (2, 2, 1, 64)))
+            eng.decode_device(0, q, k, v)
+        ls = eng.layers[0]
+        n = ls.nxt + 1
+        mask = accuracy.attended_mask(eng, 0, n)
+        q, k, v = (torch.from_numpy(rng.standard_normal(s).astype(np.float32)).cuda()
+                   for s in ((2, 4, 1, 64), (2, 2, 1, 64), (2, 2, 1, 64)))
+        out, _, _ = eng.decode_device(0, q, k, v)
+        m = accuracy.step_metrics(eng, 0, out, q, mask, n)
+        assert m["bound_violations"] == 0, m
+        if kw["cache"].beta == 0.0:
+            assert m["eps_max"] < 1e-6 and m["max_err"] < 1e-5, m
+        else:
+            assert m["eps_mean"] > 0.1, m
