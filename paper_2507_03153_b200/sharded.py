@@ -123,7 +123,12 @@ class ShardedHybridEngine(HybridEngine):
         if self.world > 1:
             if self.dist is None:
                 raise ContractError("world > 1 needs an initialised process group (or call decode_partial/merge)")
-            self.dist.all_gather_into_tensor(self.recv, self.send, group=self.group)
+            if self.dist.get_backend(self.group) == "nccl":
+                self.dist.all_gather_into_tensor(self.recv, self.send, group=self.group)
+            else:  # gloo (CPU tests of the multi-process path): gather through host copies
+                host = [torch.empty(self.stride, dtype=torch.uint8) for _ in range(self.world)]
+                self.dist.all_gather(host, self.send.cpu(), group=self.group)
+                self.recv.copy_(torch.cat(host))
             self.collectives += 1
             parts = self.recv
         else:

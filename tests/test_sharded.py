@@ -208,3 +208,64 @@ def test_gpu_sharded_shards_match_single_engine(cuda, world, dtype):
         allp = np.concatenate([c[row] for c in ctx_sh])
         assert len(np.unique(allp)) == len(allp)
         np.testing.assert_array_equal(np.sort(allp), ctx_single[row])
+
+
+def _gpu_worker(rank, world, port_no, q):
+    import torch.distributed as dist
+
+    import paper_2507_03153_b200 as hg
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port_no)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        cfg = hg.EngineConfig(layers=1, heads=8, kv_heads=2, head_dim=128, batch=2, dtype="bfloat16",
+                              cache=hg.CacheConfig(blk_num=4, blk_size=32, beta=1.0), core_count=64,
+                              max_positions=1024)
+        eng = hg.ShardedHybridEngine(cfg)  # rank / world from the process group
+        g = torch.Generator(device="cuda").manual_seed(5)
+        outs = []
+        for _ in range(400):
+            qq = torch.randn((2, 8, 1, 128), generator=g, device="cuda").to(torch.bfloat16)
+            kk = torch.randn((2, 2, 1, 128), generator=g, device="cuda").to(torch.bfloat16)
+            o, l, _ = eng.decode_device(0, qq, kk, -kk)
+            outs.append(o.cpu().numpy().copy())
+        q.put((rank, np.stack(outs), eng.collectives, eng.layers[0].archive_size))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_gpu_sharded_engine_two_processes(cuda):
+    """ShardedHybridEngine.decode_device end to end in two processes (gloo
+    process group, both on cuda:0): every rank returns the same output, equal
+    to the single-GPU engine's within bf16 tolerance."""
+    import torch.multiprocessing as mp
+
+    hg = cuda
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port_no = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port_no, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((r[0], r[1:]) for r in (q.get(timeout=600) for _ in range(2)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cfg = hg.EngineConfig(layers=1, heads=8, kv_heads=2, head_dim=128, batch=2, dtype="bfloat16",
+                          cache=hg.CacheConfig(blk_num=4, blk_size=32, beta=1.0), core_count=64, max_positions=1024)
+    single = hg.HybridEngine(cfg)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    ref = []
+    for _ in range(400):
+        qq = torch.randn((2, 8, 1, 128), generator=g, device="cuda").to(torch.bfloat16)
+        kk = torch.randn((2, 2, 1, 128), generator=g, device="cuda").to(torch.bfloat16)
+        o, _, _ = single.decode_device(0, qq, kk, -kk)
+        ref.append(o.cpu().numpy().copy())
+    ref = np.stack(ref)
+    assert res[0][1] == 400 and res[0][2] == single.layers[0].archive_size > 0
+    np.testing.assert_array_equal(res[0][0], res[1][0])
+    err = np.abs(res[0][0] - ref).max() / np.abs(ref).max()
+    assert err <= 1e-2, err
