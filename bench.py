@@ -164,12 +164,16 @@ def run_ours(args, rank, world):
 
     import paper_2507_03153_b200 as hg
 
-    local = int(os.environ.get("LOCAL_RANK", 0))
+    local = int(os.environ.get("LOCAL_RANK", 0)) % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist  # noqa: F811
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("HGCA_DIST_BACKEND", "nccl")  # gloo: multi-rank smoke runs on one GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     cfgd = dict(C2)
     K, Wm = args.steps, args.warmup
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else min(K, 200)
