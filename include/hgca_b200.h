@@ -171,9 +171,9 @@ typedef struct hgca_decode_desc {
   const int32_t* item_tab;  /* [items][4] from hgca_union_build */
   void* dsc;                /* [B*Hq, dsc_ld] dense-score scratch: fp64 (F32) or fp32 (BF16), dsc_ld >= dhi-dlo */
   int64_t dsc_ld;
-  double* part_m;           /* [max_items*max(G,2)] (rows padded to 16 bytes) */
-  double* part_z;           /* [max_items*max(G,2)] */
-  float* part_acc;          /* [max_items*G*D] */
+  double* part_m;           /* [G*max_items] head-major item partials */
+  double* part_z;           /* [G*max_items] */
+  float* part_acc;          /* [G*max_items*D] */
   int64_t max_items;        /* >= B*Hkv*(ceil((dhi-dlo)/256) + 2 + ceil(4T / sparse_rows)) */
   int32_t* counter;         /* int32 work counter (>= 1 element): zero it once before the first step;
                                every step leaves it 0 again */

@@ -343,7 +343,7 @@ static int decode_prepare(const hgca_decode_desc* d, DecodeArgs& a, DecodeMergeA
   m = DecodeMergeArgs{};
   m.B = d->B; m.Hq = d->Hq; m.Hkv = d->Hkv; m.G = G; m.D = d->D;
   m.n_dense_items = n_dense; m.item_off = d->item_off;
-  m.part_m = d->part_m; m.part_z = d->part_z; m.part_acc = d->part_acc;
+  m.part_m = d->part_m; m.part_z = d->part_z; m.part_acc = d->part_acc; m.MI = d->max_items;
   m.out = d->out; m.lse = d->lse;
   m.out_sparse = d->out_sparse; m.lse_sparse = d->lse_sparse;
   return HGCA_OK;

@@ -67,9 +67,6 @@ __device__ unsigned long long g_tlm[4096 * 8];  // merge kernel: per CTA phase s
 #endif
 
 constexpr int SUB = 32;  // rows per pipeline stage (one per lane)
-// per-item (m, z) rows are padded to 16 bytes so TMA bulk copies can move them
-template <int G>
-constexpr int mz_stride() { return G < 2 ? 2 : G; }
 constexpr int DENSE_ROWS = 256;  // window rows per dense work item
 constexpr uint32_t FULL = 0xffffffffu;
 constexpr int SMEM_MAX = 232448;  // dynamic shared memory per CTA on sm_100
@@ -156,49 +153,48 @@ __device__ __forceinline__ int32_t sub_entry(const StageDesc& d, const DecodeArg
 }
 
 // ------------------------------------------------------------------ merge kernel
-// One CTA per (batch, kv-head), launched behind the decode kernel with
-// programmatic dependent launch. Its partials are contiguous item ranges
-// (sparse: full items, tail items; dense: the window parts); they are streamed
-// into shared memory with 1-D TMA bulk copies (chunks of up to
-// MERGE_CHUNK_BYTES, so the fold is not limited by per-SM outstanding L1
-// misses) and folded per query head in item order: max, one exp per
-// (item, head), weighted sums with threads over (head, dim); chunks of long
-// lists combine with an online rescale. Then:
+// One CTA per query head (batch, kv-head, g) with D threads, one output dim
+// each, launched behind the decode kernel with programmatic dependent launch.
+// The partials are head-major, so this head's partials of the (batch,
+// kv-head)'s contiguous item ranges (sparse: full items, tail items; dense:
+// the window parts) are contiguous: up to three 1-D TMA bulk copies per chunk
+// of MERGE_NI items stream them into shared memory while two warps read the
+// items' (m, z) and form the fold weights. The fold runs in item order: max,
+// one exp per item, weighted sums over the chunk (4 interleaved partial sums,
+// combined in a fixed order); chunks of long lists combine with an online
+// rescale. Then:
 //   * merge_states(sparse, dense)            attention.py:153-188, engine.py:166-169
 //   * window weights w = float32(exp(s - m) / z) from the stored dense
 //     scores and the dense (m, z)            _core.pyx:81-82
 //   * MAW maintenance, 3 separately rounded fp64 ops (kv_cache.py:186), new
 //     entries maw = w (engine.py:177-191).
-// Fixed order throughout: deterministic.
-constexpr int MERGE_CHUNK_BYTES = 192 * 1024;
+// Fixed order throughout: deterministic. (B*Hq CTAs of ~50 KB: four per SM,
+// so the whole merge of a C2/C4 step is one wave.)
+constexpr int MERGE_NI = 96;  // items per fold chunk
 
-template <int D, int G>
+template <int D>
 struct MergeCfg {
-  static constexpr int NT = G * D >= 256 ? 256 : G * D;         // threads
-  static constexpr int ROW = G * D * 4;                          // accumulator bytes per item
-  static constexpr int GS = mz_stride<G>();                      // (m, z) row stride (16-byte rows)
-  static constexpr int NI = MERGE_CHUNK_BYTES / (ROW + 16 * GS + 8 * G);  // items per chunk
-  static constexpr int OFF_M = NI * ROW;                         // part_m [NI][GS] fp64
-  static constexpr int OFF_Z = OFF_M + NI * GS * 8;              // part_z [NI][GS] fp64
-  static constexpr int OFF_W = OFF_Z + NI * GS * 8;              // weights [G][NI] fp64
-  static constexpr int OFF_BAR = OFF_W + NI * G * 8;
-  static constexpr int SMEM = OFF_BAR + 64;
-  static constexpr int OPT = G * D / NT;                         // outputs (head, dim) per thread
-  static_assert(G * D % NT == 0, "merge thread mapping");
+  static constexpr int NT = D;                 // threads: one per output dim
+  static constexpr int NI = MERGE_NI;
+  static constexpr int IPL = NI / 32;          // items per lane in the (m, z) pass
+  static constexpr int OFF_W = NI * D * 4;     // accumulators [NI][D] f32, then weights [NI] f64
+  static constexpr int OFF_BAR = OFF_W + NI * 8;
+  static constexpr int SMEM = OFF_BAR + 16;
+  static_assert(NI % 32 == 0 && D % 64 == 0, "merge mapping");
 };
 
 template <int D, int G, typename SC>
-__global__ void __launch_bounds__(MergeCfg<D, G>::NT) decode_merge_kernel(const __grid_constant__ DecodeArgs a) {
-  using C = MergeCfg<D, G>;
+__global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __grid_constant__ DecodeArgs a) {
+  using C = MergeCfg<D>;
   const DecodeMergeArgs& m = a.m;
   extern __shared__ __align__(128) unsigned char msm[];
   float* sacc = reinterpret_cast<float*>(msm);
-  double* sm_m = reinterpret_cast<double*>(msm + C::OFF_M);
-  double* sm_z = reinterpret_cast<double*>(msm + C::OFF_Z);
   double* sw = reinterpret_cast<double*>(msm + C::OFF_W);
   uint64_t* bar = reinterpret_cast<uint64_t*>(msm + C::OFF_BAR);
-  __shared__ double hM[2][G], hZ[2][G], hS[2][G];  // [0] sparse, [1] dense running stats
-  const int64_t bk = blockIdx.x;
+  __shared__ double hM[2], hZ[2], hS[2];  // [0] sparse, [1] dense running stats
+  const int64_t bq = blockIdx.x;          // b * Hq + kv-head * G + g
+  const int64_t b = bq / m.Hq, kvh = (bq % m.Hq) / G, bk = b * m.Hkv + kvh;
+  const int g = (int)(bq % m.Hq) % G;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   TL(if (tid == 0) g_tlm[blockIdx.x * 8 + 0] = gtimer();)
   if (tid == 0) {
@@ -209,148 +205,134 @@ __global__ void __launch_bounds__(MergeCfg<D, G>::NT) decode_merge_kernel(const 
   // griddepcontrol.wait: the item ranges (built at the last selection change)
   // and the window MAW (only this kernel writes it).
   const int64_t BK = m.B * m.Hkv, nd = m.n_dense_items;
-  const int64_t b = bk / m.Hkv, kvh = bk % m.Hkv;
   const int64_t o0 = m.item_off[bk], o1 = m.item_off[bk + 1];
   const int64_t t0 = m.item_off[BK + 1 + bk], t1 = m.item_off[BK + 1 + bk + 1];
   const int64_t nf = o1 - o0, ns = nf + (t1 - t0), n = ns + a.Sd;
   auto item_id = [&](int64_t i) {
     return i < nf ? nd + o0 + i : (i < ns ? nd + t0 + (i - nf) : bk * a.Sd + (i - ns));
   };
-  constexpr int EB = 12;  // one batch covers G*W <= 12*NT window weights (the whole C2 window)
+  const double* pm = m.part_m + g * m.MI;
+  const double* pz = m.part_z + g * m.MI;
+  const float* pacc = m.part_acc + g * m.MI * D;
+  constexpr int EB = 8;  // window entries per thread per epilogue batch (one batch covers 8*D)
   const bool epi = a.maw != nullptr || a.wts_out != nullptr;
-  const int64_t W = a.dhi - a.dlo, n_el = epi ? (int64_t)G * W : 0;
-  const SC* dsc = reinterpret_cast<const SC*>(a.dsc);
+  const int64_t W = a.dhi - a.dlo, n_el = epi ? W : 0;
+  const SC* dsc = reinterpret_cast<const SC*>(a.dsc) + bq * a.dsc_ld;
+  double* maw = a.maw ? a.maw + bq * a.T + a.dlo : nullptr;
   SC sv[EB];
   double mo[EB];
   auto maw_load = [&](int64_t x0) {
 #pragma unroll
     for (int u = 0; u < EB; ++u) {
-      const int64_t x = x0 + (int64_t)u * C::NT + tid;
-      mo[u] = 0.0;
-      if (x < n_el && a.maw) {
-        const int g = (int)(x / W);
-        const int64_t j = x - g * W, bq = b * m.Hq + kvh * G + g;
-        if (j < a.w_old) mo[u] = a.maw[bq * a.T + a.dlo + j];
-      }
+      const int64_t j = x0 + u * C::NT + tid;
+      mo[u] = (maw && j < n_el && j < a.w_old) ? maw[j] : 0.0;
     }
   };
   auto dsc_load = [&](int64_t x0) {
 #pragma unroll
     for (int u = 0; u < EB; ++u) {
-      const int64_t x = x0 + (int64_t)u * C::NT + tid;
-      sv[u] = 0;
-      if (x < n_el) {
-        const int g = (int)(x / W);
-        const int64_t j = x - g * W, bq = b * m.Hq + kvh * G + g;
-        sv[u] = dsc[bq * a.dsc_ld + j];
-      }
+      const int64_t j = x0 + u * C::NT + tid;
+      sv[u] = j < n_el ? dsc[j] : (SC)0;
     }
   };
   maw_load(0);
-  if (tid < 2 * G) {
-    hM[tid / G][tid % G] = -INFINITY;
-    hZ[tid / G][tid % G] = 0.0;
+  if (tid < 2) {
+    hM[tid] = -INFINITY;
+    hZ[tid] = 0.0;
   }
-  double acc_s[C::OPT], acc_d[C::OPT];
-#pragma unroll
-  for (int k = 0; k < C::OPT; ++k) acc_s[k] = acc_d[k] = 0.0;
+  double acc_s = 0.0, acc_d = 0.0;
   uint32_t phase = 0;
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   TL(if (tid == 0) g_tlm[blockIdx.x * 8 + 1] = gtimer();)
   // the decode grid is complete: re-arm its work counter for the next step
   if (blockIdx.x == 0 && tid == 0) *a.counter = 0;
   // One fold pass over the concatenated item list [full items, tail items |
-  // dense parts]: the first ns items are sparse, the rest dense. Each chunk is
-  // bulk-copied (up to three contiguous ranges; accumulator and (m, z) rows)
-  // and folded per head into the sparse (s = 0) or dense (s = 1) running
-  // statistics, in item order.
+  // dense parts]: the first ns items are sparse, the rest dense.
   for (int64_t c0 = 0; c0 < n; c0 += C::NI) {
     const int64_t c1 = min(n, c0 + C::NI), cn = c1 - c0;
+    const int64_t lo[3] = {0, nf, ns}, hi[3] = {nf, ns, n};
     if (tid == 0) {
-      const int64_t lo[3] = {0, nf, ns}, hi[3] = {nf, ns, n};
       uint32_t bytes = 0;
       for (int r = 0; r < 3; ++r) {
         const int64_t x0 = max(c0, lo[r]), x1 = min(c1, hi[r]);
-        if (x1 > x0) bytes += (uint32_t)((x1 - x0) * C::ROW);
-      }
-      for (int r = 0; r < 3; ++r) {
-        const int64_t x0 = max(c0, lo[r]), x1 = min(c1, hi[r]);
-        if (x1 > x0) bytes += (uint32_t)((x1 - x0) * 16 * C::GS);  // + the (m, z) rows
+        if (x1 > x0) bytes += (uint32_t)((x1 - x0) * D * 4);
       }
       mbar_expect_tx(bar, bytes);
       for (int r = 0; r < 3; ++r) {
         const int64_t x0 = max(c0, lo[r]), x1 = min(c1, hi[r]);
-        if (x1 > x0) {
-          const int64_t it = item_id(x0), k = x1 - x0, dst = x0 - c0;
-          bulk_g2s(sacc + dst * G * D, m.part_acc + it * G * D, (uint32_t)(k * C::ROW), bar);
-          bulk_g2s(sm_m + dst * C::GS, m.part_m + it * C::GS, (uint32_t)(k * 8 * C::GS), bar);
-          bulk_g2s(sm_z + dst * C::GS, m.part_z + it * C::GS, (uint32_t)(k * 8 * C::GS), bar);
-        }
+        if (x1 > x0)
+          bulk_g2s(sacc + (x0 - c0) * D, pacc + item_id(x0) * D, (uint32_t)((x1 - x0) * D * 4), bar);
       }
     }
     if (c0 == 0) dsc_load(0);  // the window scores of the epilogue: in flight during the fold
-    __syncthreads();
     TL(if (tid == 0 && c0 == 0) g_tlm[blockIdx.x * 8 + 6] = gtimer();)
+    // the chunk's sparse items [0, ce) (warp 0) and dense items [ce, cn) (warp 1)
+    const int64_t ce = min(cn, max((int64_t)0, ns - c0));
+    if (wid < 2) {
+      const int64_t i0 = wid ? ce : 0, i1 = wid ? cn : ce;
+      if (i1 > i0) {  // warp-uniform
+        double mv[C::IPL], zv[C::IPL];
+#pragma unroll
+        for (int u = 0; u < C::IPL; ++u) {
+          const int64_t i = i0 + u * 32 + lane;
+          mv[u] = -INFINITY;
+          zv[u] = 0.0;
+          if (i < i1) {
+            const int64_t it = item_id(c0 + i);
+            mv[u] = pm[it];
+            zv[u] = pz[it];
+          }
+        }
+        double mx = -INFINITY;
+#pragma unroll
+        for (int u = 0; u < C::IPL; ++u) mx = fmax(mx, mv[u]);
+        mx = warp_max_f64(mx);
+        const double mold = hM[wid], mn = fmax(mold, mx);
+        double zl = 0.0;
+#pragma unroll
+        for (int u = 0; u < C::IPL; ++u) {
+          const int64_t i = i0 + u * 32 + lane;
+          if (i < i1) {
+            const double w = (mv[u] == -INFINITY || mn == -INFINITY) ? 0.0 : exp(mv[u] - mn);
+            sw[i] = w;
+            zl += zv[u] * w;
+          }
+        }
+        zl = warp_sum_f64(zl);
+        if (lane == 0) {
+          const double so = (mold == -INFINITY || mn == -INFINITY) ? 0.0 : exp(mold - mn);
+          hS[wid] = so;
+          hZ[wid] = hZ[wid] * so + zl;
+          hM[wid] = mn;
+        }
+      }
+    }
+    __syncthreads();
+    TL(if (tid == 0 && c0 == 0) g_tlm[blockIdx.x * 8 + 7] = gtimer();)
     mbar_wait(bar, phase);
     phase ^= 1;
-    TL(if (tid == 0 && c0 == 0) g_tlm[blockIdx.x * 8 + 7] = gtimer();)
-    // the chunk's sparse rows [0, ce) and dense rows [ce, cn)
-    const int64_t ce = min(cn, max((int64_t)0, ns - c0));
-    for (int task = wid; task < 2 * G; task += C::NT / 32) {
-      const int sd = task / G, g = task % G;
-      const int64_t i0 = sd ? ce : 0, i1 = sd ? cn : ce;
-      if (i1 <= i0) continue;  // warp-uniform
-      double mx = -INFINITY;
-      for (int64_t i = i0 + lane; i < i1; i += 32) mx = fmax(mx, sm_m[i * C::GS + g]);
-      mx = warp_max_f64(mx);
-      const double mo = hM[sd][g], mn = fmax(mo, mx);
-      double zl = 0.0;
-      for (int64_t i = i0 + lane; i < i1; i += 32) {
-        const double mi = sm_m[i * C::GS + g];
-        const double w = (mi == -INFINITY || mn == -INFINITY) ? 0.0 : exp(mi - mn);
-        sw[g * C::NI + i] = w;
-        zl += sm_z[i * C::GS + g] * w;
+    const float* src = sacc + tid;
+    auto dot = [&](int64_t i0, int64_t i1) {  // 4 interleaved partial sums, combined in a fixed order
+      double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+      int64_t i = i0;
+      for (; i + 4 <= i1; i += 4) {
+        p0 += sw[i] * (double)src[i * D];
+        p1 += sw[i + 1] * (double)src[(i + 1) * D];
+        p2 += sw[i + 2] * (double)src[(i + 2) * D];
+        p3 += sw[i + 3] * (double)src[(i + 3) * D];
       }
-      zl = warp_sum_f64(zl);
-      if (lane == 0) {
-        const double so = (mo == -INFINITY || mn == -INFINITY) ? 0.0 : exp(mo - mn);
-        hS[sd][g] = so;
-        hZ[sd][g] = hZ[sd][g] * so + zl;
-        hM[sd][g] = mn;
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < C::OPT; ++k) {
-      const int idx = tid + k * C::NT, g = idx / D;
-      const double* w = sw + g * C::NI;
-      const float* src = sacc + idx;
-      auto dot = [&](int64_t i0, int64_t i1) {  // 4 interleaved partial sums, combined in a fixed order
-        double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
-        int64_t i = i0;
-        for (; i + 4 <= i1; i += 4) {
-          p0 += w[i] * (double)src[i * G * D];
-          p1 += w[i + 1] * (double)src[(i + 1) * G * D];
-          p2 += w[i + 2] * (double)src[(i + 2) * G * D];
-          p3 += w[i + 3] * (double)src[(i + 3) * G * D];
-        }
-        for (; i < i1; ++i) p0 += w[i] * (double)src[i * G * D];
-        return (p0 + p1) + (p2 + p3);
-      };
-      if (ce > 0) acc_s[k] = acc_s[k] * hS[0][g] + dot(0, ce);
-      if (cn > ce) acc_d[k] = acc_d[k] * hS[1][g] + dot(ce, cn);
-    }
+      for (; i < i1; ++i) p0 += sw[i] * (double)src[i * D];
+      return (p0 + p1) + (p2 + p3);
+    };
+    if (ce > 0) acc_s = acc_s * hS[0] + dot(0, ce);
+    if (cn > ce) acc_d = acc_d * hS[1] + dot(ce, cn);
     __syncthreads();  // the next chunk's copies overwrite sacc / sw
   }
   TL(if (tid == 0) g_tlm[blockIdx.x * 8 + 2] = gtimer(); if (tid == 0) g_tlm[blockIdx.x * 8 + 3] = gtimer();)
-#pragma unroll
-  for (int k = 0; k < C::OPT; ++k) {
-    const int idx = tid + k * C::NT, g = idx / D, c = idx % D;
-    const int64_t bq = b * m.Hq + kvh * G + g;
-    const double Msg = hM[0][g], Zsg = hZ[0][g];
-    const bool s_empty = !(Zsg > 0.0) || Msg == -INFINITY;
-    const double lse_s = s_empty ? -INFINITY : Msg + log(Zsg);
-    const double md = hM[1][g], zd = hZ[1][g];
+  const double Ms = hM[0], Zs = hZ[0], md = hM[1], zd = hZ[1];
+  {
+    const bool s_empty = !(Zs > 0.0) || Ms == -INFINITY;
+    const double lse_s = s_empty ? -INFINITY : Ms + log(Zs);
     const bool d_empty = !(zd > 0.0) || md == -INFINITY;
     const double lse_d = d_empty ? -INFINITY : md + log(zd);
     const double mm = fmax(lse_s, lse_d);
@@ -359,19 +341,21 @@ __global__ void __launch_bounds__(MergeCfg<D, G>::NT) decode_merge_kernel(const 
     const double wa = exp(lse_s - ms), wb = exp(lse_d - ms);
     const double zs = both_empty ? 1.0 : wa + wb;
     const float ca = (float)(wa / zs), cb = (float)(wb / zs);
-    const float os = s_empty ? 0.f : (float)(acc_s[k] / Zsg);
-    const float od = d_empty ? 0.f : (float)(acc_d[k] / zd);
-    m.out[bq * D + c] = __fadd_rn(__fmul_rn(ca, os), __fmul_rn(cb, od));
-    if (m.out_sparse) m.out_sparse[bq * D + c] = os;
-    if (c == 0) {
+    const float os = s_empty ? 0.f : (float)(acc_s / Zs);
+    const float od = d_empty ? 0.f : (float)(acc_d / zd);
+    m.out[bq * D + tid] = __fadd_rn(__fmul_rn(ca, os), __fmul_rn(cb, od));
+    if (m.out_sparse) m.out_sparse[bq * D + tid] = os;
+    if (tid == 0) {
       m.lse[bq] = both_empty ? -INFINITY : ms + log(zs);
       if (m.lse_sparse) m.lse_sparse[bq] = lse_s;
     }
   }
   TL(if (tid == 0) g_tlm[blockIdx.x * 8 + 4] = gtimer();)
   // ---- window weights + MAW maintenance from the stored dense scores
-  // (batches of EB elements per thread; batch 0 was loaded before the folds)
+  // (batches of EB entries per thread; batch 0 was loaded before the folds)
   if (n == 0) dsc_load(0);  // (no fold chunk ran)
+  const bool d_ok = (zd > 0.0) && md != -INFINITY;
+  const double rz = 1.0 / zd;
   for (int64_t x0 = 0; x0 < n_el; x0 += (int64_t)EB * C::NT) {
     if (x0) {
       maw_load(x0);
@@ -379,22 +363,18 @@ __global__ void __launch_bounds__(MergeCfg<D, G>::NT) decode_merge_kernel(const 
     }
 #pragma unroll
     for (int u = 0; u < EB; ++u) {
-      const int64_t x = x0 + (int64_t)u * C::NT + tid;
-      if (x >= n_el) continue;
-      const int g = (int)(x / W);
-      const int64_t j = x - g * W, bq = b * m.Hq + kvh * G + g;
-      const double md = hM[1][g], zd = hZ[1][g];
+      const int64_t j = x0 + u * C::NT + tid;
+      if (j >= n_el) continue;
       float w32;
       if constexpr (sizeof(SC) == 8) {  // fp32 storage: reference-exact fp64 weights (_core.pyx:81-82)
-        w32 = (!(zd > 0.0) || md == -INFINITY) ? 0.f : (float)(exp((double)sv[u] - md) / zd);
+        w32 = d_ok ? (float)(exp((double)sv[u] - md) / zd) : 0.f;
       } else {  // bf16 storage: fp32 math (no bit-exactness contract on this path)
-        w32 = (!(zd > 0.0) || md == -INFINITY) ? 0.f : __expf((float)sv[u] - (float)md) * (float)(1.0 / zd);
+        w32 = d_ok ? __expf((float)sv[u] - (float)md) * (float)rz : 0.f;
       }
       if (a.wts_out) a.wts_out[bq * W + j] = w32;
-      if (a.maw) {
+      if (maw) {
         const double aw = (double)w32;
-        a.maw[bq * a.T + a.dlo + j] =
-            j < a.w_old ? __dadd_rn(__dmul_rn(a.one_minus_alpha, mo[u]), __dmul_rn(a.alpha, aw)) : aw;
+        maw[j] = j < a.w_old ? __dadd_rn(__dmul_rn(a.one_minus_alpha, mo[u]), __dmul_rn(a.alpha, aw)) : aw;
       }
     }
   }
@@ -678,16 +658,18 @@ __global__ void __launch_bounds__(Bf16Cfg<D, G, S, NPAIR>::NW * 32, 1)
     if (d.last) {
       TL(++tl_items;)
       // partial (m, z, acc) of this item; acc[mt][j] = O[head hA|hB][dim mt*16 + g4 (+8)]
+      // (head-major partials: head h of item i at h * MI + i)
+      const int64_t iA = hA * a.m.MI + d.item, iB = hB * a.m.MI + d.item;
       if (lane < 4) {
-        constexpr int GS = mz_stride<G>();
-        if (hA < G) { a.part_m[(int64_t)d.item * GS + hA] = mA; a.part_z[(int64_t)d.item * GS + hA] = zA; }
-        if (hB < G) { a.part_m[(int64_t)d.item * GS + hB] = mB; a.part_z[(int64_t)d.item * GS + hB] = zB; }
+        if (hA < G) { a.part_m[iA] = mA; a.part_z[iA] = zA; }
+        if (hB < G) { a.part_m[iB] = mB; a.part_z[iB] = zB; }
       }
-      float* pa = a.part_acc + (int64_t)d.item * G * D;
+      float* paA = a.part_acc + iA * D;
+      float* paB = a.part_acc + iB * D;
 #pragma unroll
       for (int mt = 0; mt < KC; ++mt) {
-        if (hA < G) { pa[hA * D + mt * 16 + g4] = acc[mt][0]; pa[hA * D + mt * 16 + 8 + g4] = acc[mt][2]; }
-        if (hB < G) { pa[hB * D + mt * 16 + g4] = acc[mt][1]; pa[hB * D + mt * 16 + 8 + g4] = acc[mt][3]; }
+        if (hA < G) { paA[mt * 16 + g4] = acc[mt][0]; paA[mt * 16 + 8 + g4] = acc[mt][2]; }
+        if (hB < G) { paB[mt * 16 + g4] = acc[mt][1]; paB[mt * 16 + 8 + g4] = acc[mt][3]; }
       }
     }
     __syncwarp();
@@ -892,10 +874,10 @@ __global__ void __launch_bounds__(F32Cfg<D, G>::NC * 32, 1) decode_f32_kernel(co
       __syncwarp();
     }
     if (d.last) {
-      for (int t = lane; t < G * D; t += 32) a.part_acc[(int64_t)d.item * G * D + t] = accs[t];
+      for (int t = lane; t < G * D; t += 32) a.part_acc[((t / D) * a.m.MI + d.item) * D + t % D] = accs[t];
       if (lane < G) {
-        a.part_m[(int64_t)d.item * mz_stride<G>() + lane] = mz[2 * lane];
-        a.part_z[(int64_t)d.item * mz_stride<G>() + lane] = mz[2 * lane + 1];
+        a.part_m[lane * a.m.MI + d.item] = mz[2 * lane];
+        a.part_z[lane * a.m.MI + d.item] = mz[2 * lane + 1];
       }
     }
     __syncwarp();
@@ -1301,12 +1283,12 @@ static int launch_decode_t(const DecodeArgs& a_in, cudaStream_t s) {
   using SC = typename std::conditional<BF16, float, double>::type;  // dense score type
   static bool mattr = false;
   {
-    const int rc = set_smem(decode_merge_kernel<D, G, SC>, MergeCfg<D, G>::SMEM, mattr);
+    const int rc = set_smem(decode_merge_kernel<D, G, SC>, MergeCfg<D>::SMEM, mattr);
     if (rc) return rc;
   }
-  cfg.gridDim = dim3((unsigned)(a.B * a.Hkv));
-  cfg.blockDim = dim3(MergeCfg<D, G>::NT);
-  cfg.dynamicSmemBytes = MergeCfg<D, G>::SMEM;
+  cfg.gridDim = dim3((unsigned)(a.B * a.Hq));
+  cfg.blockDim = dim3(MergeCfg<D>::NT);
+  cfg.dynamicSmemBytes = MergeCfg<D>::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -48,9 +48,10 @@ struct DecodeMergeArgs {
   int64_t B, Hq, Hkv, G, D;
   int64_t n_dense_items;  // = B*Hkv*Sd dense items (window parts), ids first
   const int32_t* item_off;
-  const double* part_m;
-  const double* part_z;
-  const float* part_acc;
+  const double* part_m;   // [G, MI] head-major item partials
+  const double* part_z;   // [G, MI]
+  const float* part_acc;  // [G, MI, D]
+  int64_t MI;             // item stride of the partials (descriptor max_items)
   float* out;             // [B*Hq, D]
   double* lse;            // [B*Hq]
   float* out_sparse;      // optional sparse partial out [B*Hq, D] (for sharded merges)
@@ -75,9 +76,9 @@ struct DecodeArgs {
   int64_t sparse_rows;    // rows per sparse item
   void* dsc;              // [B*Hq, dsc_ld] dense scores (fp64 for fp32 storage, fp32 for bf16)
   int64_t dsc_ld;
-  double* part_m;         // [items, G]
-  double* part_z;         // [items, G]
-  float* part_acc;        // [items, G, D]
+  double* part_m;         // [G, m.MI] head-major: one head's items are contiguous
+  double* part_z;         // [G, m.MI]
+  float* part_acc;        // [G, m.MI, D]
   int32_t* counter;       // work counter (0 on entry; re-armed by the merge kernel)
   int64_t n_dense_items;  // B*Hkv*Sd
   int64_t Sd;             // dense items (window parts of DENSE_ROWS rows) per (batch, kv-head)

@@ -248,9 +248,9 @@ class HybridEngine:
         n_dense = self.B * self.Hkv * math.ceil(self.dsc_ld / 256)  # window parts of 256 rows
         n_sparse = self.B * self.Hkv * (math.ceil(4 * self.T / SPARSE_ROWS) + 2)
         self.max_items = n_dense + n_sparse
-        gs = max(self.G, 2)  # (m, z) rows padded to 16 bytes (TMA bulk copies in the merge)
-        self.part_m = torch.empty(self.max_items * gs, dtype=torch.float64, device=self.dev)
-        self.part_z = torch.empty(self.max_items * gs, dtype=torch.float64, device=self.dev)
+        # per-item partials, head-major ([G, max_items] / [G, max_items, D])
+        self.part_m = torch.empty(self.G * self.max_items, dtype=torch.float64, device=self.dev)
+        self.part_z = torch.empty(self.G * self.max_items, dtype=torch.float64, device=self.dev)
         self.part_acc = torch.empty(self.max_items * self.G * self.D, dtype=torch.float32, device=self.dev)
         self.counter = torch.zeros(4, dtype=torch.int32, device=self.dev)  # decode work counter
         self.launches = 0          # kernels of libhgca_b200 launched by this engine

@@ -46,11 +46,13 @@ def measure(cfgd, layers=1, steps=50, warmup=5, name=""):
     n_items = BK * -(-Wavg // 256) + int(ls.item_off[2 * BK + 1])
     eng.step_events = []
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.nvtx.range_push("timed")
     e0.record()
     for i in range(warmup, warmup + steps):
         for layer in range(layers):
             eng.decode_device(layer, qs[i], ks[i], ks[i], out=out, lse=lse)
     e1.record()
+    torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
     kern_ms = statistics.mean(a.elapsed_time(b) for a, b in eng.step_events)  # per layer-step
@@ -86,6 +88,10 @@ def main():
         r = measure(cfgd, layers=80, steps=10, warmup=2, name="C4 per-GPU batch shard (B=8 of 64), 80 layers")
         r["projected_8gpu_tokens_per_s"] = round(8 * r["tokens_per_s"], 1)
         print(json.dumps(r), flush=True)
+    elif which == "C4L":  # one layer of the C4 shape: the per-layer-step kernels in isolation
+        cfgd = dict(base, batch=8, heads=64, kv_heads=8, context=16384)
+        print(json.dumps(measure(cfgd, layers=1, steps=int(os.environ.get("HGCA_STEPS", "100")), warmup=5,
+                                 name="C4 shape, one layer")), flush=True)
     elif which == "C5":
         for win_blocks in (8, 32, 128, 256):          # window 256 .. 8192 tokens (blocks of 32)
             for frac in (0.01, 0.05, 0.10, 0.20):

@@ -1,4 +1,4 @@
-"""Per-warp timeline of one C2 decode step (debug build, -DHGCA_TIMELINE).
+"""Per-warp timeline of one C2 decode step (debug build, -DHGCA_TIMELINE; HGCA_TL_CFG=C4L: the C4 shape).
 
 usage (GPU box): python paper_2507_03153_b200/_build.py --timeline
                  HGCA_LIB=paper_2507_03153_b200/_lib/libhgca_b200_tl.so python tools/timeline.py
@@ -23,6 +23,8 @@ SLOTS = 20
 def main():
     torch.cuda.set_device(0)
     cfgd = dict(bench.C2)
+    if os.environ.get("HGCA_TL_CFG") == "C4L":  # one layer of the C4 shape
+        cfgd.update(batch=8, heads=64, kv_heads=8, context=16384)
     eng, g = bench.stage_engine(hg, torch, cfgd, cfgd["context"] + 64)
     lib = hg._lib.load()
     fn = lib.hgca_debug_timeline
@@ -78,7 +80,7 @@ def main():
         fm.argtypes = [ctypes.c_void_p]
         mb = np.zeros(4096 * 8, np.uint64)
         fm(mb.ctypes.data)
-        tm = (mb.reshape(4096, 8)[: B * Hkv, :8].astype(np.float64) - t0) / 1e3
+        tm = (mb.reshape(4096, 8)[: B * Hq, :8].astype(np.float64) - t0) / 1e3
         print("  merge CTAs (us): resident p0 %.1f max %.1f | after wait p0 %.1f max %.1f | sparse fold max %.1f "
               "| dense fold max %.1f | epilogue end p50 %.1f max %.1f; per CTA: sparse %.1f dense %.1f epi %.1f" % (
                   tm[:, 0].min(), tm[:, 0].max(), tm[:, 1].min(), tm[:, 1].max(), tm[:, 2].max(), tm[:, 3].max(),
