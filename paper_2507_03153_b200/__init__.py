@@ -13,6 +13,7 @@ from .backends import CUDA, install
 from .sparsifier import HeadGroupTask, pack_head_groups, select_salient, select_topk
 from .engine import CacheConfig, EngineConfig, HybridEngine, LayerState, StepInput, StepOutput
 from .sharded import ShardedHybridEngine, packed_stride, shard_owner
+from .workload import Workload, WorkloadSpec, gen_workload_device, load_workload, save_workload
 from . import _lib
 
 __version__ = "0.1.0"

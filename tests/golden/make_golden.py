@@ -155,9 +155,17 @@ def workload(tk, out):
     np.savez_compressed(out, **rec)
 
 
+def workload_file(tk, out):
+    """A small file written by the reference's own save_workload (workload.py:189-210):
+    pins paper_2507_03153_b200.workload's reader and writer to the format."""
+    spec = tk.WorkloadSpec(seed=3, steps=12, prefill_len=4, append_events=((5, 3),))
+    tk.save_workload(tk.gen_workload(spec, tk.HeadShape(2, 16), 2), out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref-src", default="/tmp/refbuild/pkg/src")
+    ap.add_argument("--only", default=None, help="regenerate one fixture (e.g. workload_file)")
     args = ap.parse_args()
     src = ensure_ref(args.ref_src)
     sys.path.insert(0, src)
@@ -166,6 +174,10 @@ def main():
     import tierkv as tk
 
     assert tk.backends.active.name == "compiled"
+    if args.only == "workload_file":
+        workload_file(tk, os.path.join(HERE, "workload_small.tkv"))
+        return
+    workload_file(tk, os.path.join(HERE, "workload_small.tkv"))
     kernels(tk, os.path.join(HERE, "kernels.npz"))
     selection(tk, os.path.join(HERE, "selection.npz"))
     engine(tk, os.path.join(HERE, "engine.npz"))
