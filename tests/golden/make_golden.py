@@ -162,6 +162,25 @@ def workload_file(tk, out):
     tk.save_workload(tk.gen_workload(spec, tk.HeadShape(2, 16), 2), out)
 
 
+def perf_model(tk, out):
+    """Reference perf_model.py values at a few cells: pins costmodel's reference layer."""
+    import json
+    from tierkv import perf_model as pm
+    shape = pm.WorkloadShape(batch=1, heads=32, head_dim=128, n_q=1, bytes_per_elem=2)
+    rec = {"merge_bytes": pm.merge_bytes(shape), "kv_bytes_1000": pm.kv_bytes(1000, shape),
+           "cost_gpu_1025": pm.attention_cost(1025, shape.with_(n_window=1024), pm.DEFAULT_GPU),
+           "cost_cpu_8192_q64": pm.attention_cost(8192, shape.with_(n_q=64, batch=3), pm.DEFAULT_CPU)}
+    cell = shape.with_(n_window=256, n_store=4096, n_selected=819)
+    b = pm.time_offload_baseline(cell, pm.DEFAULT_GPU, pm.DEFAULT_LINK)
+    h = pm.time_hybrid(cell, pm.DEFAULT_GPU, pm.DEFAULT_CPU, pm.DEFAULT_LINK, 0.7)
+    rec.update(baseline=[b.transfer, b.compute], hybrid=[h.gpu_part, h.cpu_part, h.merge])
+    rec["heatmap"] = pm.speedup_heatmap([256, 512, 1024], [0, 1024, 16384], shape).tolist()
+    rec["rows"] = pm.heatmap_rows([256, 1024], [0, 4096], [1, 4], shape, core_efficiency=0.25,
+                                  retention_fraction=0.1)
+    with open(out, "w") as f:
+        json.dump(rec, f, indent=1)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref-src", default="/tmp/refbuild/pkg/src")
@@ -177,7 +196,11 @@ def main():
     if args.only == "workload_file":
         workload_file(tk, os.path.join(HERE, "workload_small.tkv"))
         return
+    if args.only == "perf_model":
+        perf_model(tk, os.path.join(HERE, "perf_model.json"))
+        return
     workload_file(tk, os.path.join(HERE, "workload_small.tkv"))
+    perf_model(tk, os.path.join(HERE, "perf_model.json"))
     kernels(tk, os.path.join(HERE, "kernels.npz"))
     selection(tk, os.path.join(HERE, "selection.npz"))
     engine(tk, os.path.join(HERE, "engine.npz"))
