@@ -132,6 +132,13 @@ int hgca_decode_chunk_rows(int dtype, int64_t d);
  * out5 = {warps per CTA, smem bytes per warp, cp.async stages, rows per
  * sub-chunk, smem bytes per CTA}. */
 int hgca_decode_config(int dtype, int64_t d, int64_t group, int64_t* out5);
+/* Work-item granularity of hgca_decode_step for a storage dtype: out2 =
+ * {window rows per dense item, union rows per sparse item (the sparse_rows to
+ * pass to hgca_union_build and the descriptor)}. float32: {64, 64} -- the fp64
+ * dot-product kernel's step is set by its longest item; bfloat16: {256, 256} --
+ * per-item costs (q load, partial write, merge fold) dominate below that
+ * (measured on B200). */
+int hgca_item_rows(int dtype, int64_t* out2);
 /* MAW maintenance from float32 weight rows w [BH, nq, w_ld] (row mean in fp64):
  * mode 0 = window EMA for j < w_old and init for j >= w_old (kv_cache.py:171-187,
  * engine.py:177-191); mode 1 = replace (StoreTier.reevaluate, sparsifier.py:158-177). */
@@ -174,7 +181,7 @@ typedef struct hgca_decode_desc {
   double* part_m;           /* [G*max_items] head-major item partials */
   double* part_z;           /* [G*max_items] */
   float* part_acc;          /* [G*max_items*D] */
-  int64_t max_items;        /* >= B*Hkv*(ceil((dhi-dlo)/256) + 2 + ceil(4T / sparse_rows)) */
+  int64_t max_items;        /* >= B*Hkv*(ceil((dhi-dlo)/dense_rows) + 2 + ceil(4T / sparse_rows)), dense_rows from hgca_item_rows */
   int32_t* counter;         /* int32 work counter (>= 1 element): zero it once before the first step;
                                every step leaves it 0 again */
   double* maw;              /* [B*Hq, T] or NULL */

@@ -63,6 +63,7 @@ _SIGS = {
     "hgca_write_rows": [I32, P, I64, I64, I64, I64, P, P, I64, P],
     "hgca_decode_chunk_rows": [I32, I64],
     "hgca_decode_config": [I32, I64, I64, P],
+    "hgca_item_rows": [I32, P],
     "hgca_maw_update": [P, I64, I64, I64, I64, P, I64, I64, I64, D, I32, P],
     "hgca_union_build": [P, I64, I64, I64, I64, I64, I64, P, P, P, P, I64, I32, P],
     "hgca_decode_step": [ctypes.POINTER(DecodeDesc), P],

@@ -269,6 +269,15 @@ int hgca_write_rows(int dtype, void* KV, int64_t BH, int64_t T, int64_t d, int64
 
 int hgca_decode_chunk_rows(int dtype, int64_t d) { return decode_chunk_rows(dtype, d); }
 
+static int64_t dense_rows_of(int dtype) { return dtype == HGCA_DTYPE_F32 ? 64 : 256; }
+
+int hgca_item_rows(int dtype, int64_t* out2) {
+  if (!out2 || (dtype != HGCA_DTYPE_F32 && dtype != HGCA_DTYPE_BF16))
+    return fail(HGCA_EINVAL, "item_rows: storage dtype must be float32 or bfloat16");
+  out2[0] = out2[1] = dense_rows_of(dtype);
+  return HGCA_OK;
+}
+
 int hgca_decode_config(int dtype, int64_t d, int64_t group, int64_t* out5) {
   if (!out5 || decode_config(dtype, d, group, out5)) return fail(HGCA_EINVAL, "decode_config: unsupported");
   return HGCA_OK;
@@ -310,7 +319,8 @@ static int decode_prepare(const hgca_decode_desc* d, DecodeArgs& a, DecodeMergeA
   if (d->dlo < 0 || W < 1 || d->dhi > d->T || d->w_old < 0 || d->w_old > W || d->dsc_ld < W)
     return fail(HGCA_EINVAL, "decode_step: bad dense range");
   if (d->sparse_rows < 4 || d->sparse_rows % 4) return fail(HGCA_EINVAL, "decode_step: sparse_rows must be a positive multiple of 4");
-  const int64_t Sd = (W + 255) / 256;  // dense items (window parts of 256 rows) per (batch, kv-head)
+  const int64_t DR = dense_rows_of(d->dtype);
+  const int64_t Sd = (W + DR - 1) / DR;  // dense items (window parts) per (batch, kv-head)
   const int64_t n_dense = d->B * d->Hkv * Sd;
   // every item but the last full and last tail item of a list holds >= sparse_rows/4 rows
   const int64_t max_sparse = d->B * d->Hkv * ((4 * d->T + d->sparse_rows - 1) / d->sparse_rows + 2);
@@ -336,6 +346,7 @@ static int decode_prepare(const hgca_decode_desc* d, DecodeArgs& a, DecodeMergeA
   a.counter = d->counter;
   a.n_dense_items = n_dense;
   a.Sd = Sd;
+  a.dense_rows = DR;
   a.w_old = d->w_old;
   a.maw = d->maw;
   a.one_minus_alpha = 1.0 - d->alpha; a.alpha = d->alpha;

@@ -67,7 +67,6 @@ __device__ unsigned long long g_tlm[4096 * 8];  // merge kernel: per CTA phase s
 #endif
 
 constexpr int SUB = 32;  // rows per pipeline stage (one per lane)
-constexpr int DENSE_ROWS = 256;  // window rows per dense work item
 constexpr uint32_t FULL = 0xffffffffu;
 constexpr int SMEM_MAX = 232448;  // dynamic shared memory per CTA on sm_100
 
@@ -79,7 +78,7 @@ struct StageDesc {
 
 // ------------------------------------------------------------------ work items
 // Item ids: [0, B*Hkv*Sd) dense (bk = id / Sd; window rows of part id % Sd,
-// DENSE_ROWS each), then the sparse items of item_tab. The cursor walks a warp through items in
+// a.dense_rows each), then the sparse items of item_tab. The cursor walks a warp through items in
 // sub-chunks of SUB rows; lane 0 holds the prefetched id of the next item.
 struct Cursor {
   int nxt;  // lane 0
@@ -100,8 +99,8 @@ __device__ __forceinline__ StageDesc cursor_next(Cursor& c, const DecodeArgs& a,
     if (it < (int)a.n_dense_items) {  // dense item: window rows [part*DR, (part+1)*DR) of bk
       c.dense = 1;
       c.bk = it / (int)a.Sd;
-      c.lo = (it % (int)a.Sd) * DENSE_ROWS;
-      c.hi = min(W, c.lo + DENSE_ROWS);
+      c.lo = (it % (int)a.Sd) * (int)a.dense_rows;
+      c.hi = min(W, c.lo + (int)a.dense_rows);
     } else {
       c.dense = 0;
       const int4 e = __ldg(a.item_tab + (it - (int)a.n_dense_items));  // (bk, lo, hi, -)

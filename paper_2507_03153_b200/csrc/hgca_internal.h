@@ -81,7 +81,8 @@ struct DecodeArgs {
   float* part_acc;        // [G, m.MI, D]
   int32_t* counter;       // work counter (0 on entry; re-armed by the merge kernel)
   int64_t n_dense_items;  // B*Hkv*Sd
-  int64_t Sd;             // dense items (window parts of DENSE_ROWS rows) per (batch, kv-head)
+  int64_t Sd;             // dense items (window parts of dense_rows rows) per (batch, kv-head)
+  int64_t dense_rows;     // window rows per dense item (hgca_item_rows)
   // merge-kernel epilogue: window weights + MAW maintenance
   int64_t w_old;          // window entries before this step (EMA'd); the rest are new
   double* maw;            // [B*Hq, T] or nullptr (no MAW maintenance)

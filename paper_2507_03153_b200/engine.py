@@ -25,6 +25,7 @@ masks and the union with the selection kernels.
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass, field, replace
 
@@ -40,7 +41,14 @@ from .sparsifier import group_size, mask_to_lists, ownership_words, topk_mask, w
 __all__ = ["CacheConfig", "EngineConfig", "StepInput", "StepOutput", "LayerState", "HybridEngine"]
 
 MODES = ("decode", "append")
-SPARSE_ROWS = 256   # union rows per sparse work item of the decode kernel
+
+
+def item_rows(dtype: str) -> tuple[int, int]:
+    """(window rows per dense item, union rows per sparse item) of the decode
+    kernel for a storage dtype (hgca_item_rows)."""
+    out = (ctypes.c_int64 * 2)()
+    _lib.call("hgca_item_rows", DTYPE_CODE[torch.bfloat16 if dtype == "bfloat16" else torch.float32], out)
+    return int(out[0]), int(out[1])
 
 
 @dataclass(frozen=True)
@@ -179,7 +187,9 @@ class LayerState:
         self.u_ent = torch.zeros((B * Hkv, T), dtype=torch.int32, device=dev)
         self.u_cnt = torch.zeros(B * Hkv, dtype=torch.int32, device=dev)
         self.item_off = torch.zeros(2 * (B * Hkv + 1), dtype=torch.int32, device=dev)
-        self.item_tab = torch.zeros((B * Hkv * (-(-4 * T // SPARSE_ROWS) + 2), 4), dtype=torch.int32, device=dev)
+        self.sparse_rows = item_rows(cfg.dtype)[1]
+        self.item_tab = torch.zeros((B * Hkv * (-(-4 * T // self.sparse_rows) + 2), 4), dtype=torch.int32,
+                                    device=dev)
         self.lo = 0    # archive size
         self.nxt = 0   # next position
         self.desc = None  # cached hgca_decode_desc (engine-owned)
@@ -245,8 +255,9 @@ class HybridEngine:
         BHq = self.B * self.Hq
         self.dsc_ld = self.cap + 1
         self.dsc = torch.zeros((BHq, self.dsc_ld), dtype=torch.float64, device=self.dev)
-        n_dense = self.B * self.Hkv * math.ceil(self.dsc_ld / 256)  # window parts of 256 rows
-        n_sparse = self.B * self.Hkv * (math.ceil(4 * self.T / SPARSE_ROWS) + 2)
+        dense_rows, sparse_rows = item_rows(c.dtype)
+        n_dense = self.B * self.Hkv * math.ceil(self.dsc_ld / dense_rows)
+        n_sparse = self.B * self.Hkv * (math.ceil(4 * self.T / sparse_rows) + 2)
         self.max_items = n_dense + n_sparse
         # per-item partials, head-major ([G, max_items] / [G, max_items, D])
         self.part_m = torch.empty(self.G * self.max_items, dtype=torch.float64, device=self.dev)
@@ -303,7 +314,7 @@ class HybridEngine:
         grouped = 1 if self.tdtype == torch.float32 else 2
         _lib.call("hgca_union_build", ls.sel.data_ptr(), self.B, self.Hq, self.Hkv, words, n, self.T,
                   ls.u_ent.data_ptr(), ls.u_cnt.data_ptr(), ls.item_off.data_ptr(), ls.item_tab.data_ptr(),
-                  SPARSE_ROWS, grouped, s)
+                  ls.sparse_rows, grouped, s)
 
     def _ingest(self, ls: LayerState, lo, hi, divisor):
         """StoreTier.ingest_evicted of positions [lo, hi) (sparsifier.py:127-156)."""
@@ -433,7 +444,7 @@ class HybridEngine:
             d.B, d.Hq, d.Hkv, d.D, d.T = self.B, self.Hq, self.Hkv, self.D, self.T
             d.KV = ls.KV.data_ptr()
             d.scale = float(self.shape.scale)
-            d.sparse_rows = SPARSE_ROWS
+            d.sparse_rows = ls.sparse_rows
             d.u_ent, d.u_cnt, d.item_off = ls.u_ent.data_ptr(), ls.u_cnt.data_ptr(), ls.item_off.data_ptr()
             d.item_tab = ls.item_tab.data_ptr()
             d.dsc, d.dsc_ld = self.dsc.data_ptr(), self.dsc_ld

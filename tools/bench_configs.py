@@ -92,6 +92,11 @@ def main():
         cfgd = dict(base, batch=8, heads=64, kv_heads=8, context=16384)
         print(json.dumps(measure(cfgd, layers=1, steps=int(os.environ.get("HGCA_STEPS", "100")), warmup=5,
                                  name="C4 shape, one layer")), flush=True)
+    elif which == "C5S":  # the small-step corner of C5
+        for win_blocks, frac in ((8, 0.01), (8, 0.05), (256, 0.01)):
+            cfgd = dict(base, batch=4, context=65536, blk_num=win_blocks, frac=frac)
+            print(json.dumps(measure(cfgd, steps=30, warmup=3, name="C5 small")), flush=True)
+            torch.cuda.empty_cache()
     elif which == "C5":
         for win_blocks in (8, 32, 128, 256):          # window 256 .. 8192 tokens (blocks of 32)
             for frac in (0.01, 0.05, 0.10, 0.20):

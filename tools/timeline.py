@@ -25,6 +25,8 @@ def main():
     cfgd = dict(bench.C2)
     if os.environ.get("HGCA_TL_CFG") == "C4L":  # one layer of the C4 shape
         cfgd.update(batch=8, heads=64, kv_heads=8, context=16384)
+    elif os.environ.get("HGCA_TL_CFG") == "C5S":  # a small step: C5 at 64K, window 256, 1% selected
+        cfgd.update(batch=4, context=65536, blk_num=8, frac=0.01)
     eng, g = bench.stage_engine(hg, torch, cfgd, cfgd["context"] + 64)
     lib = hg._lib.load()
     fn = lib.hgca_debug_timeline
