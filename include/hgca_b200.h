@@ -215,8 +215,12 @@ int hgca_append_bf16(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, int64_t
 
 /* End-to-end step from HOST buffers (pinned): copy in_bytes of in_host to
  * in_dev (the caller points desc->q / k_new / v_new into in_dev), run the
- * step, copy out_bytes of out_dev (desc->out / lse point into it) back to
- * out_host, and synchronize the stream. One call per decode step. */
+ * step, deliver out_bytes of out_dev (desc->out / lse point into it) to
+ * out_host, and synchronize the stream. One call per decode step. When
+ * out_host is pinned and mapped (cudaHostGetDevicePointer succeeds, as for
+ * cudaHostAlloc memory under UVA) the merge kernel writes out / lse straight to
+ * their mirror offsets in out_host and no D2H copy is issued; otherwise
+ * out_dev is copied back. */
 int hgca_decode_step_host(const hgca_decode_desc* desc, const void* in_host, void* in_dev, int64_t in_bytes,
                           void* out_host, const void* out_dev, int64_t out_bytes, hgca_stream_t stream);
 

@@ -397,9 +397,29 @@ int hgca_decode_step_host(const hgca_decode_desc* d, const void* in_host, void* 
                      "decode_step_host: H2D");
     if (rc) return rc;
   }
+  // Results straight to the host: when out_host is pinned and mapped (UVA), the
+  // merge kernel writes out / lse (which the descriptor places inside
+  // out_dev) into their mirror locations in out_host over the bus, so no D2H
+  // copy sits on the step's critical path. Otherwise: staged + copied.
+  bool direct = false;
+  if (out_bytes) {
+    void* mapped = nullptr;
+    const char* od = static_cast<const char*>(out_dev);
+    const char* po = reinterpret_cast<const char*>(m.out);
+    const char* pl = reinterpret_cast<const char*>(m.lse);
+    const int64_t nb_out = m.B * m.Hq * m.D * 4, nb_lse = m.B * m.Hq * 8;
+    const bool inside = po >= od && po + nb_out <= od + out_bytes && pl >= od && pl + nb_lse <= od + out_bytes;
+    if (inside && cudaHostGetDevicePointer(&mapped, out_host, 0) == cudaSuccess && mapped) {
+      a.m.out = reinterpret_cast<float*>(static_cast<char*>(mapped) + (po - od));
+      a.m.lse = reinterpret_cast<double*>(static_cast<char*>(mapped) + (pl - od));
+      direct = true;
+    } else {
+      (void)cudaGetLastError();  // not mapped: clear the lookup error, use the staged copy
+    }
+  }
   rc = cuda_status(launch_decode_partial(d->dtype, a, s), "decode_step_host");
   if (rc) return rc;
-  if (out_bytes) {
+  if (out_bytes && !direct) {
     rc = cuda_status((int)cudaMemcpyAsync(out_host, out_dev, (size_t)out_bytes, cudaMemcpyDeviceToHost, s),
                      "decode_step_host: D2H");
     if (rc) return rc;

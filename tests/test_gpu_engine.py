@@ -276,10 +276,12 @@ def test_bf16_rows_rotated_and_union_classes(cuda):
 
 
 def test_decode_host_packed_matches_device_path(cuda):
-    """The end-to-end host-buffer entry point (one H2D of q|k|v, one D2H of
-    out|lse) computes exactly what the device-tensor path computes."""
+    """The end-to-end host-buffer entry point (one H2D of q|k|v; out|lse written
+    by the merge kernel straight into the pinned, mapped host buffer -- or, for a
+    pageable buffer, staged and copied) computes exactly what the device-tensor
+    path computes."""
     outs = []
-    for packed in (False, True):
+    for packed in (False, "pinned", "pageable"):
         eng, g, tdt = _big_engine(cuda, "bfloat16", B=2, ctx=2048, seed=21)
         B, Hq, Hkv, D = eng.B, eng.Hq, eng.Hkv, eng.D
         res = []
@@ -289,7 +291,9 @@ def test_decode_host_packed_matches_device_path(cuda):
             v = torch.randn((B, Hkv, 1, D), generator=g, device="cuda").to(tdt)
             if packed:
                 in_h = torch.cat([q.reshape(-1), k.reshape(-1), v.reshape(-1)]).cpu().pin_memory()
-                out_h = torch.empty(B * Hq * (4 * D + 8), dtype=torch.uint8).pin_memory()
+                out_h = torch.empty(B * Hq * (4 * D + 8), dtype=torch.uint8)
+                if packed == "pinned":
+                    out_h = out_h.pin_memory()
                 eng.decode_host_packed(0, in_h, out_h)
                 o = out_h[: B * Hq * D * 4].view(torch.float32).numpy().copy()
                 l = out_h[B * Hq * D * 4:].view(torch.float64).numpy().copy()
@@ -298,9 +302,10 @@ def test_decode_host_packed_matches_device_path(cuda):
                 o, l = ot.cpu().numpy().ravel(), lt.cpu().numpy()
             res.append((o, l))
         outs.append(res)
-    for (o1, l1), (o2, l2) in zip(*outs):
-        np.testing.assert_array_equal(o1, o2)
-        np.testing.assert_array_equal(l1, l2)
+    for other in outs[1:]:
+        for (o1, l1), (o2, l2) in zip(outs[0], other):
+            np.testing.assert_array_equal(o1, o2)
+            np.testing.assert_array_equal(l1, l2)
 
 
 @pytest.mark.parametrize("nq,Hq,Hkv,d", [(16, 8, 2, 128), (5, 8, 4, 128), (1, 4, 4, 64), (40, 8, 2, 64)])
