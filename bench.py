@@ -53,6 +53,10 @@ def parse():
                     help="N>1: 'seq' shards the KV sequence of the C2 batch over the ranks (one NCCL "
                          "all-gather of (out, lse) partials per step; strong scaling, the north star's "
                          "mode); 'batch' runs one independent C2 batch per rank (weak scaling)")
+    ap.add_argument("--exchange", default="push", choices=["push", "allgather"],
+                    help="--shard seq: 'push' = the merge kernel stores each rank's (out, lse) partial into "
+                         "every peer's HBM box over NVLink (CUDA IPC) and the P-way merge waits on device "
+                         "flags; 'allgather' = one NCCL all_gather_into_tensor per step")
     return ap.parse_args()
 
 
@@ -105,7 +109,7 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------- ours
-def stage_engine(hg, torch, cfgd, max_positions, seed=0, sharded=False, layers=1):
+def stage_engine(hg, torch, cfgd, max_positions, seed=0, sharded=False, layers=1, exchange="allgather"):
     """Build the engine and stage a 32K context: bulk-ingest the archive with
     MAW drawn so that ~frac of entries per query head pass beta/divisor, then
     decode until the window reaches its steady state. sharded: every rank
@@ -117,7 +121,14 @@ def stage_engine(hg, torch, cfgd, max_positions, seed=0, sharded=False, layers=1
                           cache=hg.CacheConfig(blk_num=cfgd["blk_num"], blk_size=cfgd["blk_size"],
                                                alpha=cfgd["alpha"], beta=cfgd["beta"]),
                           core_count=10 ** 6, max_positions=max_positions)
-    eng = hg.ShardedHybridEngine(cfg) if sharded else hg.HybridEngine(cfg)
+    if sharded:
+        try:
+            eng = hg.ShardedHybridEngine(cfg, exchange=exchange)
+        except RuntimeError as e:  # e.g. no CUDA IPC between these GPUs: keep the run, use NCCL
+            print(f"[bench] push exchange unavailable ({e}); falling back to the NCCL all-gather", file=sys.stderr)
+            eng = hg.ShardedHybridEngine(cfg, exchange="allgather")
+    else:
+        eng = hg.HybridEngine(cfg)
     g = torch.Generator(device="cuda").manual_seed(seed)
     tdt = eng.tdtype
     n_arch = cfgd["context"] - cap
@@ -182,7 +193,8 @@ def run_ours(args, rank, world):
     seq = world > 1 and args.shard == "seq"
     clocks = ClockSampler(local)
     clocks.start()
-    eng, g = stage_engine(hg, torch, cfgd, max_positions, seed=1234 if seq else 1234 + rank, sharded=seq)
+    eng, g = stage_engine(hg, torch, cfgd, max_positions, seed=1234 if seq else 1234 + rank, sharded=seq,
+                          exchange=args.exchange)
     B, Hq, Hkv, D = eng.B, eng.Hq, eng.Hkv, eng.D
     tdt = eng.tdtype
     qs = torch.randn((Wm + K, B, Hq, 1, D), generator=g, device="cuda").to(tdt)
@@ -288,8 +300,12 @@ def run_ours(args, rank, world):
                        "context": cfgd["context"], "window_blocks": f"{cfgd['blk_num']}x{cfgd['blk_size']}",
                        "selected_frac": cfgd["frac"],
                        "parallelism": ("1 GPU" if world == 1 else
-                                       f"KV-sequence sharded x{world} (block-cyclic archive, NCCL all-gather of "
-                                       f"packed (out, lse) partials + P-way merge)" if seq else
+                                       f"KV-sequence sharded x{world} (block-cyclic archive; "
+                                       + ("one-shot push of packed (out, lse) partials from the merge kernel into "
+                                          "the peers' HBM (CUDA IPC / NVLink) + flag-waiting P-way merge"
+                                          if getattr(eng, "xchg", None) is not None else
+                                          "NCCL all-gather of packed (out, lse) partials + P-way merge") + ")"
+                                       if seq else
                                        f"batch replicas x{world} (one C2 batch per GPU, no collective)"),
                        "l2": "inputs larger than L2 (K/V 2.1 GB per GPU), no flush"},
             "hbm_gbs_step": round(pbytes / (ms_max * 1e-3) / 1e9, 1),

@@ -26,6 +26,7 @@
  *   hgca_decode_step_host      the same step with host q|k|v in / out|lse back (one call)
  *   hgca_merge_partials        P-way merge of sharded (out, lse) partials
  *   hgca_merge_packed          P-way merge of the allgathered packed partials
+ *   hgca_merge_packed_wait     the same merge behind the one-shot NVLink push (flags), hgca_peer_*
  */
 #ifndef HGCA_B200_H
 #define HGCA_B200_H
@@ -98,6 +99,20 @@ int hgca_merge_partials(const float* outs, const double* lses, int64_t P, int64_
 /* P-way merge of packed partials: partial p = out [rows, d] f32 at
  * parts + p*stride_bytes followed by lse [rows] f64 (the receive buffer of the
  * sequence-sharded (out, lse) allgather; rank order fold). */
+/* Peer buffers for the one-shot exchange: device memory that other processes
+ * map (CUDA IPC). hgca_peer_alloc returns the pointer and a 64-byte handle for
+ * the peers; hgca_peer_open maps a peer's handle (hgca_peer_close unmaps it). */
+int hgca_peer_alloc(int64_t bytes, void** ptr, void* handle64);
+int hgca_peer_open(const void* handle64, void** ptr);
+int hgca_peer_close(void* ptr);
+int hgca_peer_free(void* ptr);
+/* In stream order: wait on the device until flags[i] >= epoch for all i < P
+ * (acquire loads at system scope; the peers' merge kernels publish them), then
+ * hgca_merge_packed over parts. A wait longer than timeout_ms stores 1 to *err
+ * (device int32, optional) and merges what is there instead of hanging. */
+int hgca_merge_packed_wait(const void* parts, int64_t P, int64_t rows, int64_t d, int64_t stride_bytes,
+                           const uint64_t* flags, uint64_t epoch, int64_t timeout_ms, int32_t* err, float* out,
+                           double* lse, hgca_stream_t stream);
 int hgca_merge_packed(const void* parts, int64_t P, int64_t rows, int64_t d, int64_t stride_bytes,
                       float* out, double* lse, hgca_stream_t stream);
 
@@ -191,6 +206,21 @@ typedef struct hgca_decode_desc {
   float* wts_out;           /* optional [B*Hq, dhi-dlo] dense weights (a_gpu) */
   float* out_sparse;        /* optional sparse-only partial [B*Hq, D] */
   double* lse_sparse;       /* optional [B*Hq] */
+  /* Sequence-sharded one-shot exchange; push_n = 0 disables.
+   * The merge kernel stores this rank's packed partial -- out / lse
+   * (push_sparse 0: the rank whose partial includes the window) or the
+   * sparse-only out / lse (push_sparse 1) -- straight into each push_dst[p]
+   * (f32 [B*Hq, D] then f64 [B*Hq], the hgca_merge_packed slot layout; peer
+   * memory from hgca_peer_open, so the stores go over NVLink while the merge
+   * runs), fences at system scope, and its last CTA publishes `epoch` to each
+   * *push_flag[p] with a release store. push_cnt: a uint32 counter, zero
+   * before the first step (every step leaves it 0). */
+  int32_t push_n;
+  int32_t push_sparse;
+  void* push_dst[8];
+  uint64_t* push_flag[8];
+  uint64_t epoch;
+  uint32_t* push_cnt;
 } hgca_decode_desc;
 
 /* One decode step = two kernels on `stream`: the decode kernel (dense items =

@@ -40,6 +40,8 @@ class DecodeDesc(ctypes.Structure):
         ("counter", P),
         ("maw", P), ("alpha", D),
         ("out", P), ("lse", P), ("wts_out", P), ("out_sparse", P), ("lse_sparse", P),
+        ("push_n", ctypes.c_int32), ("push_sparse", ctypes.c_int32),
+        ("push_dst", P * 8), ("push_flag", P * 8), ("epoch", ctypes.c_uint64), ("push_cnt", P),
     ]
 
 
@@ -55,6 +57,11 @@ _SIGS = {
     "hgca_merge_states": [I32, P, P, P, P, I64, I64, P, P, P, P, I64, I64, P, P],
     "hgca_merge_partials": [P, P, I64, I64, I64, P, P, P],
     "hgca_merge_packed": [P, I64, I64, I64, I64, P, P, P],
+    "hgca_merge_packed_wait": [P, I64, I64, I64, I64, P, ctypes.c_uint64, I64, P, P, P, P],
+    "hgca_peer_alloc": [I64, ctypes.POINTER(P), P],
+    "hgca_peer_open": [P, ctypes.POINTER(P)],
+    "hgca_peer_close": [P],
+    "hgca_peer_free": [P],
     "hgca_select_threshold": [P, I64, I64, I64, I64, D, I64, P, I64, I32, P, P],
     "hgca_mask_to_indices": [P, P, I64, I64, I64, P, I64, P, P, P],
     "hgca_popcount_rows": [P, I64, I64, I64, P, P],

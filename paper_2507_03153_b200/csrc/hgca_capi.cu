@@ -79,6 +79,28 @@ __global__ void merge_packed_kernel(const unsigned char* parts, int64_t P, int64
   if (threadIdx.x == 0) lse[r] = M + log(Z);
 }
 
+// One CTA, one thread per flag: spin (acquire, system scope) until every
+// peer has published this step's epoch, or the timeout passes.
+__global__ void wait_flags_kernel(const unsigned long long* flags, int64_t n, unsigned long long epoch,
+                                  long long timeout_ns, int32_t* err) {
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + i) : "memory");
+      if (v >= epoch) break;
+      long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > timeout_ns) {
+        if (err) atomicExch(err, 1);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+}
+
 }  // namespace hgca
 
 using namespace hgca;
@@ -214,6 +236,42 @@ int hgca_merge_packed(const void* parts, int64_t P, int64_t rows, int64_t d, int
   merge_packed_kernel<<<(unsigned)rows, 128, 0, S(stream)>>>(reinterpret_cast<const unsigned char*>(parts), P,
                                                             rows, d, stride_bytes, out, lse);
   return cuda_status((int)cudaGetLastError(), "merge_packed");
+}
+
+int hgca_peer_alloc(int64_t bytes, void** ptr, void* handle64) {
+  if (bytes < 1 || !ptr || !handle64) return fail(HGCA_EINVAL, "peer_alloc: bad arguments");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  int rc = cuda_status((int)cudaMalloc(ptr, (size_t)bytes), "peer_alloc: cudaMalloc");
+  if (rc) return rc;
+  rc = cuda_status((int)cudaMemset(*ptr, 0, (size_t)bytes), "peer_alloc: memset");
+  if (rc) return rc;
+  cudaIpcMemHandle_t h;
+  rc = cuda_status((int)cudaIpcGetMemHandle(&h, *ptr), "peer_alloc: cudaIpcGetMemHandle");
+  if (rc) return rc;
+  memcpy(handle64, &h, 64);
+  return HGCA_OK;
+}
+
+int hgca_peer_open(const void* handle64, void** ptr) {
+  if (!handle64 || !ptr) return fail(HGCA_EINVAL, "peer_open: bad arguments");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, 64);
+  return cuda_status((int)cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess), "peer_open");
+}
+
+int hgca_peer_close(void* ptr) { return cuda_status((int)cudaIpcCloseMemHandle(ptr), "peer_close"); }
+
+int hgca_peer_free(void* ptr) { return cuda_status((int)cudaFree(ptr), "peer_free"); }
+
+int hgca_merge_packed_wait(const void* parts, int64_t P, int64_t rows, int64_t d, int64_t stride_bytes,
+                           const uint64_t* flags, uint64_t epoch, int64_t timeout_ms, int32_t* err, float* out,
+                           double* lse, hgca_stream_t stream) {
+  if (!flags || P < 1 || timeout_ms < 0) return fail(HGCA_EINVAL, "merge_packed_wait: bad arguments");
+  wait_flags_kernel<<<1, 32, 0, S(stream)>>>(reinterpret_cast<const unsigned long long*>(flags), P,
+                                             (unsigned long long)epoch, (long long)timeout_ms * 1000000LL, err);
+  const int rc = cuda_status((int)cudaGetLastError(), "merge_packed_wait");
+  if (rc) return rc;
+  return hgca_merge_packed(parts, P, rows, d, stride_bytes, out, lse, stream);
 }
 
 int hgca_select_threshold(const double* maw, int64_t rows, int64_t ld, int64_t p0, int64_t p1,
@@ -357,6 +415,17 @@ static int decode_prepare(const hgca_decode_desc* d, DecodeArgs& a, DecodeMergeA
   m.part_m = d->part_m; m.part_z = d->part_z; m.part_acc = d->part_acc; m.MI = d->max_items;
   m.out = d->out; m.lse = d->lse;
   m.out_sparse = d->out_sparse; m.lse_sparse = d->lse_sparse;
+  if (d->push_n < 0 || d->push_n > 8 || (d->push_n && !d->push_cnt))
+    return fail(HGCA_EINVAL, "decode_step: push_n must be in [0, 8] with a push counter");
+  m.push_n = d->push_n;
+  m.push_sparse = d->push_sparse ? 1 : 0;
+  for (int p = 0; p < d->push_n; ++p) {
+    if (!d->push_dst[p] || !d->push_flag[p]) return fail(HGCA_EINVAL, "decode_step: null push slot %d", p);
+    m.push_dst[p] = static_cast<unsigned char*>(d->push_dst[p]);
+    m.push_flag[p] = reinterpret_cast<unsigned long long*>(d->push_flag[p]);
+  }
+  m.epoch = d->epoch;
+  m.push_cnt = d->push_cnt;
   return HGCA_OK;
 }
 

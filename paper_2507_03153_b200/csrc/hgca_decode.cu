@@ -342,11 +342,36 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
     const float ca = (float)(wa / zs), cb = (float)(wb / zs);
     const float os = s_empty ? 0.f : (float)(acc_s / Zs);
     const float od = d_empty ? 0.f : (float)(acc_d / zd);
-    m.out[bq * D + tid] = __fadd_rn(__fmul_rn(ca, os), __fmul_rn(cb, od));
+    const float ov = __fadd_rn(__fmul_rn(ca, os), __fmul_rn(cb, od));
+    const double lv = both_empty ? -INFINITY : ms + log(zs);
+    m.out[bq * D + tid] = ov;
     if (m.out_sparse) m.out_sparse[bq * D + tid] = os;
     if (tid == 0) {
-      m.lse[bq] = both_empty ? -INFINITY : ms + log(zs);
+      m.lse[bq] = lv;
       if (m.lse_sparse) m.lse_sparse[bq] = lse_s;
+    }
+    if (m.push_n) {
+      // one-shot exchange: this head's row of the rank's packed partial goes
+      // straight into every destination slot (peer HBM over NVLink); the last
+      // CTA to finish publishes the step's epoch once all rows are fenced
+      const float pv = m.push_sparse ? os : ov;
+      const double pl = m.push_sparse ? lse_s : lv;
+      const int64_t lse_off = m.B * m.Hq * D * 4;
+      for (int p = 0; p < m.push_n; ++p) {
+        reinterpret_cast<float*>(m.push_dst[p])[bq * D + tid] = pv;
+        if (tid == 0) reinterpret_cast<double*>(m.push_dst[p] + lse_off)[bq] = pl;
+      }
+      __threadfence_system();
+      __syncthreads();
+      if (tid == 0) {
+        const unsigned prev = atomicAdd(m.push_cnt, 1u);
+        if (prev == gridDim.x - 1) {
+          *m.push_cnt = 0;  // re-armed for the next step (stream order)
+          __threadfence_system();
+          for (int p = 0; p < m.push_n; ++p)
+            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(m.push_flag[p]), "l"(m.epoch) : "memory");
+        }
+      }
     }
   }
   TL(if (tid == 0) g_tlm[blockIdx.x * 8 + 4] = gtimer();)

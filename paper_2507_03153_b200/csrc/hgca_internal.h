@@ -56,6 +56,12 @@ struct DecodeMergeArgs {
   double* lse;            // [B*Hq]
   float* out_sparse;      // optional sparse partial out [B*Hq, D] (for sharded merges)
   double* lse_sparse;
+  // one-shot exchange: this rank's packed partial pushed into push_n slots
+  int push_n, push_sparse;
+  unsigned char* push_dst[8];
+  unsigned long long* push_flag[8];
+  unsigned long long epoch;
+  unsigned int* push_cnt;
 };
 
 // Fused decode step: dense window items + sparse union chunks, merged in-kernel.

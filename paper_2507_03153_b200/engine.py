@@ -266,6 +266,7 @@ class HybridEngine:
         self.counter = torch.zeros(4, dtype=torch.int32, device=self.dev)  # decode work counter
         self.launches = 0          # kernels of libhgca_b200 launched by this engine
         self.step_events = None     # list -> (start, end) CUDA events around the decode kernel
+        self._push = None           # per-step push descriptor (ShardedHybridEngine, exchange="push")
 
     # ------------------------------------------------------------ helpers
     def _stream(self):
@@ -458,6 +459,14 @@ class HybridEngine:
         d.dlo, d.dhi, d.w_old = ls.lo, ls.nxt + 1, ls.nxt - ls.lo
         d.out, d.lse, d.wts_out = out, lse, wts
         d.out_sparse, d.lse_sparse = out_sparse, lse_sparse
+        push = self._push  # one-shot exchange of the sharded engine (sharded.PeerExchange), else off
+        d.push_n = 0
+        if push is not None:
+            d.push_sparse = push["sparse"]
+            for i, (dst, flag) in enumerate(zip(push["dst"], push["flag"])):
+                d.push_dst[i], d.push_flag[i] = dst, flag
+            d.epoch, d.push_cnt = push["epoch"], push["cnt"]
+            d.push_n = len(push["dst"])
         return d
 
     def _step_done(self, ls):

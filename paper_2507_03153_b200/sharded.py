@@ -20,12 +20,27 @@ sets, which is what makes the archive shardable:
 
 Per-rank HBM traffic of the step is the window plus 1/world of the selected
 archive rows; the collective moves (D*4 + 8) bytes per (batch, query head)
-per rank. Only decode steps are sharded; append steps run replicated (every
+per rank.
+
+exchange="push" replaces the all-gather with a one-shot push fused into the
+merge kernel (PeerExchange): every rank owns a receive box in HBM that all
+ranks map (CUDA IPC), [2 parities][world slots][packed partial] plus one
+epoch flag per (parity, slot); the merge kernel stores each finished head's
+row straight into its slot of every peer's box over NVLink while the rest of
+the merge runs, and its last CTA publishes the step's epoch to the peers'
+flags (system-scope release). hgca_merge_packed_wait then waits for the
+world flags on the device and folds the box in rank order -- no NCCL call and
+no host synchronisation on the step. Parity double-buffering makes slot reuse
+safe: a rank can only write parity p again after it has waited for every
+peer's flag of the step in between, which each peer publishes after its own
+merge of parity p. Only decode steps are sharded; append steps run replicated (every
 rank holds every K/V row), and their re-evaluation re-selects within the
 rank's shard.
 """
 
 from __future__ import annotations
+
+import ctypes
 
 import torch
 
@@ -45,6 +60,65 @@ def packed_stride(rows: int, d: int) -> int:
     return rows * d * 4 + rows * 8
 
 
+class PeerExchange:
+    """Receive boxes + epoch flags of the one-shot push (hgca_peer_alloc / hgca_peer_open)."""
+
+    FLAG_ALIGN = 256
+
+    def __init__(self, world: int, rank: int, stride: int, dev, timeout_ms: int = 10000):
+        if not 1 <= world <= 8:
+            raise ContractError("the one-shot push supports 1..8 ranks")
+        self.world, self.rank, self.stride, self.timeout_ms = world, rank, stride, timeout_ms
+        self.box_bytes = 2 * world * stride
+        self.flags_off = -(-self.box_bytes // self.FLAG_ALIGN) * self.FLAG_ALIGN
+        ptr, handle = ctypes.c_void_p(), (ctypes.c_uint8 * 64)()
+        _lib.call("hgca_peer_alloc", self.flags_off + 2 * world * 8, ctypes.byref(ptr), handle)
+        self.base, self.handle = ptr.value, bytes(handle)
+        self.peers = None
+        self._opened = []
+        self.cnt = torch.zeros(1, dtype=torch.int32, device=dev)   # merge-kernel CTA counter
+        self.err = torch.zeros(1, dtype=torch.int32, device=dev)   # set by a timed-out wait
+        self.epoch = 0
+
+    def connect_ipc(self, handles):
+        """Map every peer's box from its 64-byte handle (one per rank, rank order)."""
+        peers = []
+        for p, h in enumerate(handles):
+            if p == self.rank:
+                peers.append(self.base)
+                continue
+            ptr = ctypes.c_void_p()
+            _lib.call("hgca_peer_open", (ctypes.c_uint8 * 64).from_buffer_copy(h), ctypes.byref(ptr))
+            self._opened.append(ptr.value)
+            peers.append(ptr.value)
+        self.peers = peers
+
+    def connect_local(self, bases):
+        """Single-process ranks (tests): the peers' boxes are plain device pointers."""
+        self.peers = list(bases)
+
+    def next_step(self, sparse: bool):
+        """The push descriptor of the next step (engine._push) and this rank's
+        (box half, flags) for hgca_merge_packed_wait."""
+        if self.peers is None:
+            raise ContractError("PeerExchange is not connected")
+        self.epoch += 1
+        par = self.epoch & 1
+        half = par * self.world * self.stride
+        push = {"sparse": int(sparse), "epoch": self.epoch, "cnt": self.cnt.data_ptr(),
+                "dst": [b + half + self.rank * self.stride for b in self.peers],
+                "flag": [b + self.flags_off + (par * self.world + self.rank) * 8 for b in self.peers]}
+        return push, self.base + half, self.base + self.flags_off + par * self.world * 8
+
+    def close(self):
+        for p in self._opened:
+            _lib.call("hgca_peer_close", p)
+        self._opened = []
+        if self.base:
+            _lib.call("hgca_peer_free", self.base)
+            self.base = None
+
+
 class ShardedHybridEngine(HybridEngine):
     """HybridEngine whose decode step is sequence-sharded over a process group.
 
@@ -54,8 +128,12 @@ class ShardedHybridEngine(HybridEngine):
     themselves. With world == 1 it is an ordinary HybridEngine.
     """
 
-    def __init__(self, config: EngineConfig, group=None, dev=None, rank=None, world=None):
+    def __init__(self, config: EngineConfig, group=None, dev=None, rank=None, world=None, exchange="allgather",
+                 push_timeout_ms: int = 10000):
         import torch.distributed as dist
+
+        if exchange not in ("allgather", "push"):
+            raise ContractError(f"exchange must be 'allgather' or 'push', got {exchange!r}")
 
         self.group = group
         self.dist = dist if dist.is_available() and dist.is_initialized() else None
@@ -76,6 +154,14 @@ class ShardedHybridEngine(HybridEngine):
         self._loc_out = torch.empty((rows, D), dtype=torch.float32, device=self.dev)
         self._loc_lse = torch.empty(rows, dtype=torch.float64, device=self.dev)
         self.collectives = 0
+        self.exchange = exchange
+        self.xchg = None
+        if exchange == "push" and world > 1:
+            self.xchg = PeerExchange(world, rank, self.stride, self.dev, timeout_ms=push_timeout_ms)
+            if self.dist is not None:  # exchange the IPC handles once
+                handles = [None] * world
+                self.dist.all_gather_object(handles, self.xchg.handle, group=group)
+                self.xchg.connect_ipc(handles)
 
     def decode_partial(self, layer_idx, q, k, v, wts=None):
         """This rank's decode step, leaving its packed partial in self.send."""
@@ -119,6 +205,8 @@ class ShardedHybridEngine(HybridEngine):
             out = torch.empty((self.rows, self.D), dtype=torch.float32, device=self.dev)
         if lse is None:
             lse = torch.empty(self.rows, dtype=torch.float64, device=self.dev)
+        if self.xchg is not None:
+            return self._decode_push(layer_idx, q, k, v, out, lse, wts)
         w = self.decode_partial(layer_idx, q, k, v, wts=wts)
         if self.world > 1:
             if self.dist is None:
@@ -135,3 +223,32 @@ class ShardedHybridEngine(HybridEngine):
             parts = self.send
         self.merge(parts, out, lse)
         return out, lse, w
+
+    def _decode_push(self, layer_idx, q, k, v, out, lse, wts):
+        """exchange="push": the merge kernel pushes this rank's packed partial
+        into every peer's box; the P-way merge waits for the peers' flags on
+        the device (see the module docstring)."""
+        push, box, flags = self.xchg.next_step(sparse=self.rank > 0)
+        self._push = push
+        try:
+            _, _, w = HybridEngine.decode_device(self, layer_idx, q, k, v, out=self._loc_out, lse=self._loc_lse,
+                                                 wts=wts)
+        finally:
+            self._push = None
+        _lib.call("hgca_merge_packed_wait", box, self.world, self.rows, self.D, self.stride, flags,
+                  self.xchg.epoch, self.xchg.timeout_ms, self.xchg.err.data_ptr(), out.data_ptr(), lse.data_ptr(),
+                  self._stream())
+        self.launches += 2  # wait + merge
+        self.collectives += 1
+        return out, lse, w
+
+    def check_exchange(self):
+        """Raise if a push-exchange wait timed out (host sync)."""
+        if self.xchg is not None and int(self.xchg.err.item()):
+            raise RuntimeError("one-shot exchange: a peer's flag did not arrive before the timeout")
+
+    def close(self):
+        if self.xchg is not None:
+            torch.cuda.synchronize(self.dev)
+            self.xchg.close()
+            self.xchg = None

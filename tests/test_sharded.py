@@ -210,7 +210,56 @@ def test_gpu_sharded_shards_match_single_engine(cuda, world, dtype):
         np.testing.assert_array_equal(np.sort(allp), ctx_single[row])
 
 
-def _gpu_worker(rank, world, port_no, q):
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,dtype", [(2, "bfloat16"), (3, "float32")])
+def test_gpu_push_exchange_matches_allgather(cuda, world, dtype):
+    """exchange="push" with `world` ranks in one process (one stream each, the
+    peers' boxes as plain device pointers): the merge kernels push their packed
+    partials into every box and the flag-waiting merge folds them -- bit-equal
+    to the all-gather exchange of the same partials, on every rank."""
+    hg = cuda
+    H, Hkv, d, B = 8, 2, 128, 2
+    cfg = hg.EngineConfig(layers=1, heads=H, kv_heads=Hkv, head_dim=d, batch=B, dtype=dtype,
+                          cache=hg.CacheConfig(blk_num=4, blk_size=32, beta=1.0),
+                          core_count=64, max_positions=1024)
+    push = [hg.ShardedHybridEngine(cfg, rank=r, world=world, exchange="push") for r in range(world)]
+    bases = [e.xchg.base for e in push]
+    for e in push:
+        e.xchg.connect_local(bases)
+    ref = [hg.ShardedHybridEngine(cfg, rank=r, world=world) for r in range(world)]
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    outs = [(torch.empty((B * H, d), dtype=torch.float32, device="cuda"),
+             torch.empty(B * H, dtype=torch.float64, device="cuda")) for _ in range(world)]
+    rout = torch.empty((B * H, d), dtype=torch.float32, device="cuda")
+    rlse = torch.empty(B * H, dtype=torch.float64, device="cuda")
+    g = torch.Generator(device="cuda").manual_seed(3)
+    tdt = push[0].tdtype
+    for t in range(300):
+        qq = torch.randn((B, H, 1, d), generator=g, device="cuda").to(tdt)
+        kk = torch.randn((B, Hkv, 1, d), generator=g, device="cuda").to(tdt)
+        vv = torch.randn((B, Hkv, 1, d), generator=g, device="cuda").to(tdt)
+        main = torch.cuda.current_stream()
+        for r, e in enumerate(push):
+            streams[r].wait_stream(main)
+            with torch.cuda.stream(streams[r]):
+                e.decode_device(0, qq, kk, vv, out=outs[r][0], lse=outs[r][1])
+        for s_ in streams:
+            main.wait_stream(s_)
+        for e in ref:
+            e.decode_partial(0, qq, kk, vv)
+        ref[0].merge(torch.cat([e.send for e in ref]), rout, rlse)
+        for r in range(world):
+            assert torch.equal(outs[r][0], rout) and torch.equal(outs[r][1], rlse), (t, r)
+    torch.cuda.synchronize()
+    for e in push:
+        e.check_exchange()
+        assert e.collectives == 300
+    assert push[0].layers[0].archive_size > 100
+    for e in push:
+        e.close()
+
+
+def _gpu_worker(rank, world, port_no, q, exchange="allgather", steps=400):
     import torch.distributed as dist
 
     import paper_2507_03153_b200 as hg
@@ -223,31 +272,40 @@ def _gpu_worker(rank, world, port_no, q):
         cfg = hg.EngineConfig(layers=1, heads=8, kv_heads=2, head_dim=128, batch=2, dtype="bfloat16",
                               cache=hg.CacheConfig(blk_num=4, blk_size=32, beta=1.0), core_count=64,
                               max_positions=1024)
-        eng = hg.ShardedHybridEngine(cfg)  # rank / world from the process group
+        # rank / world from the process group (push: IPC handles exchanged through it)
+        eng = hg.ShardedHybridEngine(cfg, exchange=exchange, push_timeout_ms=20000)
         g = torch.Generator(device="cuda").manual_seed(5)
         outs = []
-        for _ in range(400):
+        for _ in range(steps):
             qq = torch.randn((2, 8, 1, 128), generator=g, device="cuda").to(torch.bfloat16)
             kk = torch.randn((2, 2, 1, 128), generator=g, device="cuda").to(torch.bfloat16)
             o, l, _ = eng.decode_device(0, qq, kk, -kk)
             outs.append(o.cpu().numpy().copy())
+        eng.check_exchange()
+        torch.cuda.synchronize()
+        dist.barrier()
+        eng.close()
         q.put((rank, np.stack(outs), eng.collectives, eng.layers[0].archive_size))
     finally:
         dist.destroy_process_group()
 
 
 @pytest.mark.gpu
-def test_gpu_sharded_engine_two_processes(cuda):
+@pytest.mark.parametrize("exchange,steps", [("allgather", 400), ("push", 200)])
+def test_gpu_sharded_engine_two_processes(cuda, exchange, steps):
     """ShardedHybridEngine.decode_device end to end in two processes (gloo
     process group, both on cuda:0): every rank returns the same output, equal
-    to the single-GPU engine's within bf16 tolerance."""
+    to the single-GPU engine's within bf16 tolerance. exchange="push": the
+    receive boxes are mapped across the processes with CUDA IPC and the merge
+    kernels push into them (the two contexts time-slice one GPU here, so the
+    flag waits are slow but bounded)."""
     import torch.multiprocessing as mp
 
     hg = cuda
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port_no = _free_port()
-    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port_no, q)) for r in range(2)]
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port_no, q, exchange, steps)) for r in range(2)]
     for p in procs:
         p.start()
     res = dict((r[0], r[1:]) for r in (q.get(timeout=600) for _ in range(2)))
@@ -259,13 +317,13 @@ def test_gpu_sharded_engine_two_processes(cuda):
     single = hg.HybridEngine(cfg)
     g = torch.Generator(device="cuda").manual_seed(5)
     ref = []
-    for _ in range(400):
+    for _ in range(steps):
         qq = torch.randn((2, 8, 1, 128), generator=g, device="cuda").to(torch.bfloat16)
         kk = torch.randn((2, 2, 1, 128), generator=g, device="cuda").to(torch.bfloat16)
         o, _, _ = single.decode_device(0, qq, kk, -kk)
         ref.append(o.cpu().numpy().copy())
     ref = np.stack(ref)
-    assert res[0][1] == 400 and res[0][2] == single.layers[0].archive_size > 0
+    assert res[0][1] == steps and res[0][2] == single.layers[0].archive_size > 0
     np.testing.assert_array_equal(res[0][0], res[1][0])
     err = np.abs(res[0][0] - ref).max() / np.abs(ref).max()
     assert err <= 1e-2, err
