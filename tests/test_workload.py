@@ -152,6 +152,7 @@ class TestPlantedStructure:
 def test_device_generation_at_128k_context():
     """One layer of the C3 shape (32 heads, d=128, 128K tokens) generated on the device."""
     spec = wk.WorkloadSpec(seed=7, steps=131072 - 128, prefill_len=128)
+    wk.gen_workload_device(wk.WorkloadSpec(seed=1, steps=64), heads=2, head_dim=128, layers=1, device="cuda")
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
