@@ -224,10 +224,11 @@ typedef struct hgca_decode_desc {
 } hgca_decode_desc;
 
 /* One decode step = two kernels on `stream`: the decode kernel (dense items =
- * 256-row parts of the window, sparse items = union slices -> per-item
- * (m, z, acc) partials; it also writes k_new/v_new) and the merge kernel
- * (programmatic dependent launch; folds the partials in item order, applies
- * merge_states, the window weights and the MAW EMA). */
+ * window parts of hgca_item_rows(dtype)[0] rows, sparse items = union slices
+ * -> per-item (m, z, acc) partials, head-major; it also writes k_new/v_new)
+ * and the merge kernel (one CTA per query head, programmatic dependent launch;
+ * folds the partials in item order, applies merge_states, the window weights
+ * and the MAW EMA, and with push_n > 0 pushes the rank's packed partial). */
 int hgca_decode_step(const hgca_decode_desc* desc, hgca_stream_t stream);
 
 /* Append / re-evaluation attention for BF16 storage on the tensor cores
