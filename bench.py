@@ -206,6 +206,17 @@ def run_ours(args, rank, world):
     for i in range(Wm):
         eng.decode_device(0, qs[i], ks[i], vs[i], out=out, lse=lse)
     torch.cuda.synchronize()
+    exchange_note = None
+    if getattr(eng, "xchg", None) is not None:  # push exchange: did every peer flag arrive in time?
+        bad = torch.tensor([int(eng.xchg.err.item())])
+        if world > 1:
+            if dist.get_backend() == "nccl":
+                bad = bad.cuda()
+            dist.all_reduce(bad)
+        if int(bad.item()):
+            exchange_note = "push exchange timed out during warm-up; measured with the NCCL all-gather"
+            print(f"[bench] {exchange_note}", file=sys.stderr)
+            eng.xchg = None
     U0 = int(ls.u_cnt.sum())
     Ws = []
     eng.step_events = []
@@ -304,6 +315,7 @@ def run_ours(args, rank, world):
                                        + ("one-shot push of packed (out, lse) partials from the merge kernel into "
                                           "the peers' HBM (CUDA IPC / NVLink) + flag-waiting P-way merge"
                                           if getattr(eng, "xchg", None) is not None else
+                                          ((exchange_note + "; ") if exchange_note else "") +
                                           "NCCL all-gather of packed (out, lse) partials + P-way merge") + ")"
                                        if seq else
                                        f"batch replicas x{world} (one C2 batch per GPU, no collective)"),
