@@ -24,8 +24,10 @@
 #include "hgca_common.cuh"
 #include "hgca_internal.h"
 #include "hgca_tc.cuh"
+#include "hgca_umma.cuh"
 
 #include <cuda.h>
+#include <cstdlib>
 
 namespace hgca {
 
@@ -37,6 +39,8 @@ constexpr int AMAXW = 8;        // consumer warps per CTA -> <= 128 query rows p
 
 struct AppendArgs {
   CUtensorMap kmap;             // 2-D tile map over KV [B*Hkv*T rows, 2D], box {2D, 32}
+  CUtensorMap kvmap5;           // tcgen05 pass: over KV [B*Hkv*T rows, 2D], box {64, 64}, no swizzle
+  CUtensorMap qmap5;            // tcgen05 pass: over q [B*Hq*nq rows, D], box {64, 128}, 128-byte swizzle
   const __nv_bfloat16* q;       // [B*Hq, nq, D]
   int64_t B, Hq, Hkv, G, T, nq;
   float scale;
@@ -314,6 +318,263 @@ __global__ void __launch_bounds__((AMAXW + 1) * 32, 1) append_attend_kernel(cons
   }
 }
 
+// ------------------------------------------------------------------ tcgen05 pass 1
+// Same work items and partial outputs as append_attend_kernel<D, 1>, with
+// both GEMMs on the 5th-generation tensor cores (D = 128, row groups of 128):
+//   warp 0  TMA: the row group's Q once (two 64-column 128-byte-swizzled
+//           atoms, 128 rows), then per stage of 64 keys four 64x64 boxes
+//           K0 K1 V0 V1 into a 3-stage ring. bf16 rows are stored rotated by
+//           position (16-byte chunk c at c ^ (p & 7) inside each 128-byte
+//           segment), which IS the 128-byte swizzle of an 8-row-aligned box:
+//           stages start at positions rounded down to 8 (the extra keys are
+//           masked), so the tiles are canonical SW128 operands as loaded.
+//   warp 1  one thread issues tcgen05.mma: S = Q K^T (M 128, N 64, K-major
+//           operands) into a double-buffered TMEM tile, then O += P V (V as
+//           the MN-major B operand; P = bf16 hi + lo) into the TMEM
+//           accumulator; tcgen05.commit drives the mbarriers.
+//   warps 2-5  one thread per row (its TMEM lane): tcgen05.ld the S row,
+//           scale + mask, fp32 softmax against a per-row reference max that
+//           is only raised when a score exceeds it by more than 8 (p <= e^8,
+//           so P and O stay in range); raising it rescales the row's O in
+//           TMEM (ld, scale, st -- warp-collective, after the previous P V
+//           completed), which happens a few times per row, not per stage.
+//           P rows (hi, lo) go to shared memory in the SW128 layout.
+// (m, z, acc) per row as the mma.sync kernel writes them (m is the reference
+// max: z and acc are relative to it, which is all the fold needs).
+constexpr int T5_KEYS = 64;  // keys per stage
+#ifndef HGCA_T5_STAGES
+#define HGCA_T5_STAGES 4
+#endif
+constexpr int T5_S = HGCA_T5_STAGES;  // K|V stages in the ring
+constexpr float T5_HEADROOM = 8.f;
+
+struct Tc5Cfg {               // D = 128
+  static constexpr int QATOM = 128 * 128;               // 128 rows x 64 bf16 (16 KB)
+  static constexpr int KVQ = T5_KEYS * 128;             // 64 keys x 64 bf16 (8 KB)
+  static constexpr int STAGE = 4 * KVQ;                 // K0 K1 V0 V1
+  static constexpr int PBUF = 128 * 128;                // 128 rows x 64 keys bf16
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_KV = OFF_Q + 2 * QATOM;
+  static constexpr int OFF_P = OFF_KV + T5_S * STAGE;   // [2 buffers][hi, lo]
+  static constexpr int OFF_BAR = OFF_P + 4 * PBUF;
+  static constexpr int NBAR = 1 + 2 * T5_S + 6;         // qfull, full[S], empty[S], sfull[2], pfull[2], pvdone[2]
+  static constexpr int OFF_TM = OFF_BAR + NBAR * 8;
+  static constexpr int SMEM = OFF_TM + 16 + 1024;       // + alignment slack
+  static constexpr int TMEM_COLS = 256;                 // S[2] x 64 | O 128
+  static constexpr int THREADS = 6 * 32;
+};
+
+__global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __grid_constant__ AppendArgs a) {
+  using C = Tc5Cfg;
+  constexpr int D = 128;
+  constexpr uint32_t O_COL = 2 * T5_KEYS;
+  extern __shared__ unsigned char sm_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);
+  uint64_t* qfull = bars;
+  uint64_t* full = bars + 1;
+  uint64_t* empty = full + T5_S;
+  uint64_t* sfull = empty + T5_S;
+  uint64_t* pfull = sfull + 2;
+  uint64_t* pvdone = pfull + 2;
+  uint32_t* tm_holder = reinterpret_cast<uint32_t*>(sm + C::OFF_TM);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int64_t bk, rg, chunk;
+  int seg;
+  append_item(a, blockIdx.x, bk, rg, seg, chunk);
+  const int64_t p0 = a.seg_lo[seg] + chunk * ACHUNK;
+  const int64_t p1 = min(a.seg_hi[seg], p0 + ACHUNK);
+  const int64_t p0a = p0 & ~(int64_t)7;  // 8-aligned stage base: rotation == swizzle phase
+  const int nst = (int)((p1 - p0a + T5_KEYS - 1) / T5_KEYS);
+  if (threadIdx.x == 0) {
+    mbar_init(qfull, 1);
+    for (int s = 0; s < T5_S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sfull[b], 1);
+      mbar_init(&pfull[b], 4);  // one arrive per softmax warp
+    }
+    mbar_init(&pvdone[0], 1);
+    mbar_init(&pvdone[1], 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) umma::tmem_alloc<C::TMEM_COLS>(smem_u32(tm_holder));
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+  const uint32_t tmem = *tm_holder;
+  const uint32_t sQ = smem_u32(sm + C::OFF_Q), sKV = smem_u32(sm + C::OFF_KV), sP = smem_u32(sm + C::OFF_P);
+
+  if (warp == 0) {  // ------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const uint64_t policy = l2_evict_first_policy();
+      const int64_t b = bk / a.Hkv, kvh = bk % a.Hkv;
+      const int qrow = (int)((b * a.Hq + kvh * a.G) * a.nq + rg * a.RG);
+      mbar_expect_tx(qfull, 2 * C::QATOM);
+      tma_load_2d(sQ, &a.qmap5, 0, qrow, qfull, policy);
+      tma_load_2d(sQ + C::QATOM, &a.qmap5, 64, qrow, qfull, policy);
+      const int rowbase = (int)(bk * a.T + p0a);
+      for (int st = 0; st < nst; ++st) {
+        const int s = st % T5_S;
+        if (st >= T5_S) mbar_wait(&empty[s], ((st / T5_S) - 1) & 1);
+        mbar_expect_tx(&full[s], C::STAGE);
+#pragma unroll
+        for (int qd = 0; qd < 4; ++qd)
+          tma_load_2d(sKV + s * C::STAGE + qd * C::KVQ, &a.kvmap5, qd * 64, rowbase + st * T5_KEYS, &full[s], policy);
+      }
+    }
+  } else if (warp == 1) {  // ------------------------------------------ MMA issuer
+    if (lane == 0) {
+      mbar_wait(qfull, 0);
+      umma::fence_after_sync();
+      constexpr uint32_t IDESC_QK = umma::idesc_bf16_f32(128, T5_KEYS, false, false);
+      constexpr uint32_t IDESC_PV = umma::idesc_bf16_f32(128, D, false, true);
+      auto qk = [&](int st) {
+        const int s = st % T5_S, b = st & 1;
+        mbar_wait(&full[s], (st / T5_S) & 1);
+        umma::fence_after_sync();
+        const uint32_t kb = sKV + s * C::STAGE;
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint64_t ad = umma::smem_desc(sQ + (k / 4) * C::QATOM + (k % 4) * 32, 16, 1024);
+          const uint64_t bd = umma::smem_desc(kb + (k / 4) * C::KVQ + (k % 4) * 32, 16, 1024);
+          umma::mma_bf16(tmem + b * T5_KEYS, ad, bd, IDESC_QK, k > 0);
+        }
+        umma::commit(smem_u32(&sfull[b]));
+      };
+      auto pv = [&](int st) {
+        const int s = st % T5_S, b = st & 1;
+        mbar_wait(&pfull[b], (st >> 1) & 1);
+        umma::fence_after_sync();
+        const uint32_t vb = sKV + s * C::STAGE + 2 * C::KVQ;  // V0 then V1: the two 64-column atoms
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // P hi, P lo
+          const uint32_t pb = sP + (b * 2 + h) * C::PBUF;
+#pragma unroll
+          for (int j = 0; j < T5_KEYS / 16; ++j) {
+            const uint64_t ad = umma::smem_desc(pb + j * 32, 16, 1024);
+            const uint64_t bd = umma::smem_desc(vb + j * 16 * 128, C::KVQ, 1024);
+            umma::mma_bf16(tmem + O_COL, ad, bd, IDESC_PV, st > 0 || h > 0 || j > 0);
+          }
+        }
+        umma::commit(smem_u32(&pvdone[b]));  // PV(st) -- and every earlier MMA -- complete
+        umma::commit(smem_u32(&empty[s]));
+      };
+      qk(0);
+      for (int st = 1; st <= nst; ++st) {
+        if (st < nst) qk(st);
+        pv(st - 1);
+      }
+    }
+    __syncwarp();
+  } else {  // ------------------------------------------------------- softmax warps
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;          // row of the group == TMEM lane
+    const uint32_t tl = (uint32_t)(quarter * 32) << 16;
+    float mu = -INFINITY, z = 0.f;              // reference max, sum of exp(s - mu)
+    const uint32_t prow = (uint32_t)((r >> 3) * 1024 + (r & 7) * 128);
+    for (int st = 0; st < nst; ++st) {
+      const int b = st & 1;
+      mbar_wait(&sfull[b], (st >> 1) & 1);
+      umma::fence_after_sync();
+      float x[T5_KEYS];
+#pragma unroll
+      for (int c0 = 0; c0 < T5_KEYS; c0 += 16) {
+        uint32_t v[16];
+        umma::ld_32x32b_x16(tmem + tl + b * T5_KEYS + c0, v);
+        umma::ld_wait();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) x[c0 + j] = __uint_as_float(v[j]);
+      }
+      const int64_t kp0 = p0a + (int64_t)st * T5_KEYS;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < T5_KEYS; ++j) {
+        const bool ok = kp0 + j >= p0 && kp0 + j < p1;
+        x[j] = ok ? x[j] * a.scale : -INFINITY;
+        mx = fmaxf(mx, x[j]);
+      }
+      float alpha = 1.f;
+      if (mx > mu + T5_HEADROOM) {  // raise the reference max (also the first finite score)
+        alpha = mu == -INFINITY ? 0.f : __expf(mu - mx);
+        mu = mx;
+      }
+      float sum = 0.f;
+#pragma unroll
+      for (int j = 0; j < T5_KEYS; ++j) {
+        x[j] = x[j] == -INFINITY ? 0.f : __expf(x[j] - mu);
+        sum += x[j];
+      }
+      z = z * alpha + sum;
+      // P buffer b was last read by PV(st-2)
+      if (st >= 2) mbar_wait(&pvdone[b], ((st - 2) >> 1) & 1);
+      if (st >= 1 && __any_sync(FULL_MASK, alpha != 1.f)) {
+        // rescale the rows' O once PV(st-1) has completed (PV(st) waits for this
+        // stage's P, released below); warp-collective TMEM ld / st
+        mbar_wait(&pvdone[b ^ 1], ((st - 1) >> 1) & 1);
+        umma::fence_after_sync();
+        {
+#pragma unroll
+          for (int c0 = 0; c0 < D; c0 += 16) {
+            uint32_t v[16];
+            umma::ld_32x32b_x16(tmem + tl + O_COL + c0, v);
+            umma::ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * alpha);
+            umma::st_32x32b_x16(tmem + tl + O_COL + c0, v);
+          }
+          umma::st_wait();
+        }
+      }
+      unsigned char* ph = sm + C::OFF_P + (b * 2) * C::PBUF + prow;
+      unsigned char* pl = ph + C::PBUF;
+#pragma unroll
+      for (int c = 0; c < T5_KEYS / 8; ++c) {
+        uint32_t hi[4], lo[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          hi[e] = pack_bf16(x[c * 8 + 2 * e], x[c * 8 + 2 * e + 1]);
+          lo[e] = pack_bf16(x[c * 8 + 2 * e] - bf16_lo_f(hi[e]), x[c * 8 + 2 * e + 1] - bf16_hi_f(hi[e]));
+        }
+        const uint32_t off = (uint32_t)((c ^ (r & 7)) << 4);
+        *reinterpret_cast<uint4*>(ph + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<uint4*>(pl + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      }
+      umma::fence_smem_async();  // P (generic stores) -> visible to the tensor core
+      umma::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pfull[b]);
+    }
+    mbar_wait(&pvdone[(nst - 1) & 1], ((nst - 1) >> 1) & 1);  // the last PV (and all before it)
+    umma::fence_after_sync();
+    // this row's partial (m, z, acc), as append_attend_kernel<D, 1> writes it
+    const bool mine = r < a.RG && rg * a.RG + r < a.R;
+    const int64_t item = blockIdx.x;
+    float4* pa = reinterpret_cast<float4*>(a.part_acc + (item * a.RG + r) * D);
+#pragma unroll
+    for (int c0 = 0; c0 < D; c0 += 16) {
+      uint32_t v[16];
+      umma::ld_32x32b_x16(tmem + tl + O_COL + c0, v);
+      umma::ld_wait();
+      if (mine) {
+#pragma unroll
+        for (int j = 0; j < 16; j += 4)
+          pa[(c0 + j) / 4] = make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
+                                         __uint_as_float(v[j + 3]));
+      }
+    }
+    if (mine) {
+      a.part_m[item * a.RG + r] = mu;
+      a.part_z[item * a.RG + r] = z;
+    }
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  if (warp == 1) umma::tmem_dealloc<C::TMEM_COLS>(tmem);
+}
+
 // One warp per (b, kv-head, row): fold the chunk partials of both segments,
 // merge_states(archive, window) (attention.py:153-188), out / lse, and the
 // row's final (m, z) per segment for pass 2.
@@ -395,6 +656,26 @@ static int make_tile_map(CUtensorMap* map, const void* base, int64_t rows, int64
   return r == CUDA_SUCCESS ? 0 : -3001;
 }
 
+// 2-D bf16 map [rows, cols] with a (box_cols x box_rows) box
+static int make_map2d(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_cols, int box_rows,
+                      CUtensorMapSwizzle swz) {
+  static EncodeTiledFnA encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q) != cudaSuccess ||
+        !encode)
+      return -3000;
+  }
+  cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t gstr[1] = {(cuuint64_t)(cols * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), gdim, gstr, box, es,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -3001;
+}
+
 // Layout of the caller's workspace for one append step (all sizes in bytes).
 struct AppendPlan {
   int64_t R, RG, n_rg, nch0, nch1, n_items;
@@ -470,7 +751,37 @@ static int launch_append_d(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, i
     attr1 = attr2 = true;
   }
   const int nw = (int)((p.RG + 15) / 16);
-  if (p.n_items > 0) append_attend_kernel<D, 1><<<(unsigned)p.n_items, (nw + 1) * 32, C1::SMEM, s>>>(a);
+  if constexpr (D == 128) {  // pass 1 on tcgen05
+    {
+      static const void* kv_base = nullptr;
+      static int64_t kv_rows = -1;
+      static CUtensorMap kv_map;
+      const int64_t rows = B * Hkv * T;
+      if (kv_base != KV || kv_rows != rows) {
+        const int rc = make_map2d(&kv_map, KV, rows, 2 * D, 64, T5_KEYS, CU_TENSOR_MAP_SWIZZLE_NONE);
+        if (rc) return rc;
+        kv_base = KV;
+        kv_rows = rows;
+      }
+      a.kvmap5 = kv_map;
+      const int rc = make_map2d(&a.qmap5, q, B * Hq * nq, D, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+      if (rc) return rc;
+    }
+    static bool attr5 = false;
+    if (!attr5) {
+      const cudaError_t e5 =
+          cudaFuncSetAttribute(append_tc5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Tc5Cfg::SMEM);
+      if (e5 != cudaSuccess) return (int)e5;
+      attr5 = true;
+    }
+    // full 128-row groups only: smaller groups would leave most of the M = 128 tile idle
+    if (p.n_items > 0 && p.RG == 128 && !getenv("HGCA_APPEND_MMA_SYNC"))
+      append_tc5_kernel<<<(unsigned)p.n_items, Tc5Cfg::THREADS, Tc5Cfg::SMEM, s>>>(a);
+    else if (p.n_items > 0)
+      append_attend_kernel<D, 1><<<(unsigned)p.n_items, (nw + 1) * 32, C1::SMEM, s>>>(a);
+  } else {
+    if (p.n_items > 0) append_attend_kernel<D, 1><<<(unsigned)p.n_items, (nw + 1) * 32, C1::SMEM, s>>>(a);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
   const int64_t warps = B * Hkv * p.R;

@@ -308,7 +308,8 @@ def test_decode_host_packed_matches_device_path(cuda):
             np.testing.assert_array_equal(l1, l2)
 
 
-@pytest.mark.parametrize("nq,Hq,Hkv,d", [(16, 8, 2, 128), (5, 8, 4, 128), (1, 4, 4, 64), (40, 8, 2, 64)])
+@pytest.mark.parametrize("nq,Hq,Hkv,d", [(16, 8, 2, 128), (5, 8, 4, 128), (1, 4, 4, 64), (40, 8, 2, 64),
+                                         (32, 8, 2, 128), (64, 8, 2, 128)])  # last two: tcgen05 pass 1
 def test_bf16_append_tensor_core_path_matches_reference_path(cuda, nq, Hq, Hkv, d):
     """hgca_append_bf16 (tensor cores, row-mean weights in-kernel) against the
     reference-order fp64 path (keep_weights=True) on the same staged state: the
