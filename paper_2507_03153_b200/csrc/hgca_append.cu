@@ -346,7 +346,13 @@ constexpr int T5_KEYS = 64;  // keys per stage
 #define HGCA_T5_STAGES 4
 #endif
 constexpr int T5_S = HGCA_T5_STAGES;  // K|V stages in the ring
-constexpr float T5_HEADROOM = 8.f;
+constexpr float T5_HEADROOM2 = 8.f * 1.4426950408889634f;  // e^8 of headroom, in log2 units
+
+__device__ __forceinline__ float ex2_approx(float x) {  // 2^x; 2^-inf = +0
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 struct Tc5Cfg {               // D = 128
   static constexpr int QATOM = 128 * 128;               // 128 rows x 64 bf16 (16 KB)
@@ -364,6 +370,14 @@ struct Tc5Cfg {               // D = 128
   static constexpr int THREADS = 6 * 32;
 };
 
+#ifdef HGCA_TC5_PROF
+// debug build: per-CTA cycle counters [0] MMA wait full, [1] MMA wait pfull, [2] MMA total,
+// [3] softmax (warp 2) wait sfull, [4] softmax wait pvdone, [5] softmax total, [6] stages
+__device__ unsigned long long g_tc5prof[8];
+#define P5(...) __VA_ARGS__
+#else
+#define P5(...)
+#endif
 __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __grid_constant__ AppendArgs a) {
   using C = Tc5Cfg;
   constexpr int D = 128;
@@ -431,9 +445,12 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
       umma::fence_after_sync();
       constexpr uint32_t IDESC_QK = umma::idesc_bf16_f32(128, T5_KEYS, false, false);
       constexpr uint32_t IDESC_PV = umma::idesc_bf16_f32(128, D, false, true);
+      P5(long long w_full = 0, w_pfull = 0, t_start = clock64();)
       auto qk = [&](int st) {
         const int s = st % T5_S, b = st & 1;
+        P5(long long c0 = clock64();)
         mbar_wait(&full[s], (st / T5_S) & 1);
+        P5(w_full += clock64() - c0;)
         umma::fence_after_sync();
         const uint32_t kb = sKV + s * C::STAGE;
 #pragma unroll
@@ -446,7 +463,9 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
       };
       auto pv = [&](int st) {
         const int s = st % T5_S, b = st & 1;
+        P5(long long c0 = clock64();)
         mbar_wait(&pfull[b], (st >> 1) & 1);
+        P5(w_pfull += clock64() - c0;)
         umma::fence_after_sync();
         const uint32_t vb = sKV + s * C::STAGE + 2 * C::KVQ;  // V0 then V1: the two 64-column atoms
 #pragma unroll
@@ -467,49 +486,68 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
         if (st < nst) qk(st);
         pv(st - 1);
       }
+      P5(atomicAdd(&g_tc5prof[0], (unsigned long long)w_full); atomicAdd(&g_tc5prof[1], (unsigned long long)w_pfull);
+         atomicAdd(&g_tc5prof[2], (unsigned long long)(clock64() - t_start)); atomicAdd(&g_tc5prof[6], (unsigned long long)nst);)
     }
     __syncwarp();
   } else {  // ------------------------------------------------------- softmax warps
     const int quarter = warp & 3;
     const int r = quarter * 32 + lane;          // row of the group == TMEM lane
     const uint32_t tl = (uint32_t)(quarter * 32) << 16;
-    float mu = -INFINITY, z = 0.f;              // reference max, sum of exp(s - mu)
+    // softmax in log2 units: x = s * log2(e), p = 2^(x - mu2) == exp(s - mu2 * ln 2)
+    const float sl2 = a.scale * 1.4426950408889634f;
+    float mu2 = -INFINITY, z = 0.f;             // reference max (log2 units), sum of p
     const uint32_t prow = (uint32_t)((r >> 3) * 1024 + (r & 7) * 128);
+    P5(long long w_s = 0, w_pv = 0, t_s0 = clock64();)
     for (int st = 0; st < nst; ++st) {
       const int b = st & 1;
+      P5(long long c0 = clock64();)
       mbar_wait(&sfull[b], (st >> 1) & 1);
+      P5(w_s += clock64() - c0;)
       umma::fence_after_sync();
       float x[T5_KEYS];
+      {
+        uint32_t v[4][16];  // all four loads in flight, one wait
 #pragma unroll
-      for (int c0 = 0; c0 < T5_KEYS; c0 += 16) {
-        uint32_t v[16];
-        umma::ld_32x32b_x16(tmem + tl + b * T5_KEYS + c0, v);
+        for (int c = 0; c < 4; ++c) umma::ld_32x32b_x16(tmem + tl + b * T5_KEYS + c * 16, v[c]);
         umma::ld_wait();
 #pragma unroll
-        for (int j = 0; j < 16; ++j) x[c0 + j] = __uint_as_float(v[j]);
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int j = 0; j < 16; ++j) x[c * 16 + j] = __uint_as_float(v[c][j]);
       }
       const int64_t kp0 = p0a + (int64_t)st * T5_KEYS;
       float mx = -INFINITY;
+      if (kp0 >= p0 && kp0 + T5_KEYS <= p1) {  // every key of the stage is in range (warp-uniform)
 #pragma unroll
-      for (int j = 0; j < T5_KEYS; ++j) {
-        const bool ok = kp0 + j >= p0 && kp0 + j < p1;
-        x[j] = ok ? x[j] * a.scale : -INFINITY;
-        mx = fmaxf(mx, x[j]);
+        for (int j = 0; j < T5_KEYS; ++j) {
+          x[j] *= sl2;
+          mx = fmaxf(mx, x[j]);
+        }
+      } else {
+        const int jlo = (int)max(p0 - kp0, (int64_t)0), jhi = (int)min(p1 - kp0, (int64_t)T5_KEYS);
+#pragma unroll
+        for (int j = 0; j < T5_KEYS; ++j) {
+          x[j] = (j >= jlo && j < jhi) ? x[j] * sl2 : -INFINITY;
+          mx = fmaxf(mx, x[j]);
+        }
       }
       float alpha = 1.f;
-      if (mx > mu + T5_HEADROOM) {  // raise the reference max (also the first finite score)
-        alpha = mu == -INFINITY ? 0.f : __expf(mu - mx);
-        mu = mx;
+      if (mx > mu2 + T5_HEADROOM2) {  // raise the reference max (also the first finite score)
+        alpha = mu2 == -INFINITY ? 0.f : ex2_approx(mu2 - mx);
+        mu2 = mx;
       }
       float sum = 0.f;
 #pragma unroll
       for (int j = 0; j < T5_KEYS; ++j) {
-        x[j] = x[j] == -INFINITY ? 0.f : __expf(x[j] - mu);
+        x[j] = ex2_approx(x[j] - mu2);  // masked keys: 2^-inf = 0
         sum += x[j];
       }
       z = z * alpha + sum;
       // P buffer b was last read by PV(st-2)
+      P5(long long c1 = clock64();)
       if (st >= 2) mbar_wait(&pvdone[b], ((st - 2) >> 1) & 1);
+      P5(w_pv += clock64() - c1;)
       if (st >= 1 && __any_sync(FULL_MASK, alpha != 1.f)) {
         // rescale the rows' O once PV(st-1) has completed (PV(st) waits for this
         // stage's P, released below); warp-collective TMEM ld / st
@@ -548,6 +586,8 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
       if (lane == 0) mbar_arrive(&pfull[b]);
     }
     mbar_wait(&pvdone[(nst - 1) & 1], ((nst - 1) >> 1) & 1);  // the last PV (and all before it)
+    P5(if (warp == 2 && lane == 0) { atomicAdd(&g_tc5prof[3], (unsigned long long)w_s);
+       atomicAdd(&g_tc5prof[4], (unsigned long long)w_pv); atomicAdd(&g_tc5prof[5], (unsigned long long)(clock64() - t_s0)); })
     umma::fence_after_sync();
     // this row's partial (m, z, acc), as append_attend_kernel<D, 1> writes it
     const bool mine = r < a.RG && rg * a.RG + r < a.R;
@@ -566,7 +606,7 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
       }
     }
     if (mine) {
-      a.part_m[item * a.RG + r] = mu;
+      a.part_m[item * a.RG + r] = mu2 == -INFINITY ? -INFINITY : mu2 * 0.6931471805599453f;  // natural-log units
       a.part_z[item * a.RG + r] = z;
     }
   }
@@ -775,7 +815,9 @@ static int launch_append_d(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, i
       attr5 = true;
     }
     // full 128-row groups only: smaller groups would leave most of the M = 128 tile idle
-    if (p.n_items > 0 && p.RG == 128 && !getenv("HGCA_APPEND_MMA_SYNC"))
+    const char* force_mma = getenv("HGCA_APPEND_MMA_SYNC");  // A/B switch: 1 = the mma.sync pass for every group
+    const bool tc5 = p.RG == 128 && !(force_mma && *force_mma && *force_mma != '0');
+    if (p.n_items > 0 && tc5)
       append_tc5_kernel<<<(unsigned)p.n_items, Tc5Cfg::THREADS, Tc5Cfg::SMEM, s>>>(a);
     else if (p.n_items > 0)
       append_attend_kernel<D, 1><<<(unsigned)p.n_items, (nw + 1) * 32, C1::SMEM, s>>>(a);
@@ -802,5 +844,12 @@ int launch_append_bf16(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, int64
     return launch_append_d<64>(KV, B, Hq, Hkv, T, q, nq, scale, lo, hi, out, lse, mean_archive, mean_window, ws, s);
   return -1001;
 }
+
+#ifdef HGCA_TC5_PROF
+extern "C" int hgca_debug_tc5prof(unsigned long long* out8) {
+  cudaDeviceSynchronize();
+  return (int)cudaMemcpyFromSymbol(out8, g_tc5prof, sizeof(unsigned long long) * 8);
+}
+#endif
 
 }  // namespace hgca
