@@ -1061,9 +1061,9 @@ static int launch_append_d(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, i
       if (e5 != cudaSuccess) return (int)e5;
       attr5 = true;
     }
-    // full 128-row groups only: smaller groups would leave most of the M = 128 tile idle
+    // row groups of >= 64 rows (the M = 128 tile's cost is per item; tiny groups stay on mma.sync)
     const char* force_mma = getenv("HGCA_APPEND_MMA_SYNC");  // A/B switch: 1 = the mma.sync pass for every group
-    const bool tc5 = p.RG == 128 && !(force_mma && *force_mma && *force_mma != '0');
+    const bool tc5 = p.RG >= 64 && !(force_mma && *force_mma && *force_mma != '0');
     if (p.n_items > 0 && tc5)
       append_tc5_kernel<<<(unsigned)p.n_items, Tc5Cfg::THREADS, Tc5Cfg::SMEM, s>>>(a);
     else if (p.n_items > 0)
@@ -1081,7 +1081,7 @@ static int launch_append_d(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, i
     bool tc5_mean = false;
     if constexpr (D == 128) {
       const char* force_mma = getenv("HGCA_APPEND_MMA_SYNC");
-      tc5_mean = p.RG == 128 && !(force_mma && *force_mma && *force_mma != '0');
+      tc5_mean = p.RG >= 64 && !(force_mma && *force_mma && *force_mma != '0');
       static bool attr_m = false;
       if (tc5_mean && !attr_m) {
         const cudaError_t em =
