@@ -12,7 +12,7 @@ sys.path.insert(0, ROOT)
 import paper_2507_03153_b200 as hg  # noqa: E402
 
 
-def run(dtype, steps=150, append_at=60):
+def run(dtype, steps=150, append_at=60, append_nq=8):
     cfg = hg.EngineConfig(layers=1, heads=8, kv_heads=2, head_dim=128, batch=2, dtype=dtype,
                           cache=hg.CacheConfig(blk_num=4, blk_size=32, beta=1.0), core_count=4,
                           max_positions=1024)
@@ -25,8 +25,8 @@ def run(dtype, steps=150, append_at=60):
                     torch.rand((2, 8, n), generator=g, device="cuda", dtype=torch.float64) / 128, 128)
     for t in range(steps):
         if t == append_at:
-            q = torch.randn((2, 8, 8, 128), generator=g, device="cuda").to(tdt)
-            k = torch.randn((2, 2, 8, 128), generator=g, device="cuda").to(tdt)
+            q = torch.randn((2, 8, append_nq, 128), generator=g, device="cuda").to(tdt)
+            k = torch.randn((2, 2, append_nq, 128), generator=g, device="cuda").to(tdt)
             eng.step(0, hg.StepInput("append", q, k, k))
             continue
         q = torch.randn((2, 8, 1, 128), generator=g, device="cuda").to(tdt)
@@ -42,5 +42,7 @@ if __name__ == "__main__":
         run("bfloat16", append_at=-1)
     if mode in ("all", "bf16-append"):
         run("bfloat16", steps=3, append_at=0)
+    if mode in ("all", "bf16-append-tc5"):  # G*n_q = 64 rows: the tcgen05 append passes
+        run("bfloat16", steps=3, append_at=0, append_nq=16)
     if mode in ("all", "f32"):
         run("float32", steps=80)
