@@ -14,7 +14,9 @@ of largest MAW, ties by position -- the padding order of sparsifier.py:219-226):
   4. one measured decode step, compared with paper_2507_03153_b200.accuracy:
      err, eps (dropped oracle mass), the 2*eps*max|V| bound (harness.py:147-160).
 
-Prints one JSON line per point. float32 storage: the reference-exact kernels.
+Prints one JSON line per point. float32 storage (default): the reference-exact kernels;
+HGCA_ACC_DTYPE=bfloat16: the bf16 path (tensor-core decode, tcgen05 append), the same
+history rounded to bf16, so err includes the bf16 arithmetic on top of the dropped mass.
 """
 import json
 import os
@@ -48,6 +50,7 @@ def queries(g, u, nq):
 
 
 BOOST = float(os.environ.get("HGCA_ACC_BOOST", "0.5"))  # heavy-hitter key boost along u
+DTYPE = os.environ.get("HGCA_ACC_DTYPE", "float32")
 
 
 def point(win_blocks, frac, seed=0):
@@ -55,29 +58,30 @@ def point(win_blocks, frac, seed=0):
     u = torch.nn.functional.normalize(torch.randn((B, HKV, D), generator=g, device="cuda"), dim=-1)
     cap = win_blocks * 32
     n_arch = CTX - cap
-    cfg = hg.EngineConfig(layers=1, heads=HQ, kv_heads=HKV, head_dim=D, batch=B, dtype="float32",
+    cfg = hg.EngineConfig(layers=1, heads=HQ, kv_heads=HKV, head_dim=D, batch=B, dtype=DTYPE,
                           cache=hg.CacheConfig(blk_num=win_blocks, blk_size=32, alpha=0.5, beta=1.0),
                           core_count=10 ** 6, max_positions=CTX + 64, selection="topk",
                           topk=max(1, int(round(frac * n_arch))))
     eng = hg.HybridEngine(cfg)
-    k = structured(g, u, n_arch)
-    v = torch.randn((B, HKV, n_arch, D), generator=g, device="cuda")
+    tdt = eng.tdtype
+    k = structured(g, u, n_arch).to(tdt)
+    v = torch.randn((B, HKV, n_arch, D), generator=g, device="cuda").to(tdt)
     eng.bulk_ingest(0, k, v, torch.zeros((B, HQ, n_arch), dtype=torch.float64, device="cuda"), cap)
     nq = 16
-    eng.step(0, hg.StepInput("append", queries(g, u, nq), structured(g, u, nq, sinks=0),
-                             torch.randn((B, HKV, nq, D), generator=g, device="cuda")))
+    eng.step(0, hg.StepInput("append", queries(g, u, nq).to(tdt), structured(g, u, nq, sinks=0).to(tdt),
+                             torch.randn((B, HKV, nq, D), generator=g, device="cuda").to(tdt)))
     while eng.layers[0].window_size < cap - 1:
-        eng.decode_device(0, queries(g, u, 1).contiguous(), structured(g, u, 1, sinks=0).contiguous(),
-                          torch.randn((B, HKV, 1, D), generator=g, device="cuda"))
+        eng.decode_device(0, queries(g, u, 1).to(tdt).contiguous(), structured(g, u, 1, sinks=0).to(tdt).contiguous(),
+                          torch.randn((B, HKV, 1, D), generator=g, device="cuda").to(tdt))
     ls = eng.layers[0]
     n = ls.nxt + 1
     mask = accuracy.attended_mask(eng, 0, n)
-    q = queries(g, u, 1).contiguous()
-    out, lse, _ = eng.decode_device(0, q, structured(g, u, 1, sinks=0).contiguous(),
-                                    torch.randn((B, HKV, 1, D), generator=g, device="cuda"))
+    q = queries(g, u, 1).to(tdt).contiguous()
+    out, lse, _ = eng.decode_device(0, q, structured(g, u, 1, sinks=0).to(tdt).contiguous(),
+                                    torch.randn((B, HKV, 1, D), generator=g, device="cuda").to(tdt))
     m = accuracy.step_metrics(eng, 0, out, q, mask, n)
     m.update({"config": "C5 accuracy", "context": n, "window_cap": cap, "topk_frac": frac, "archive": ls.lo,
-              "dtype": "float32", "heavy_boost": BOOST})
+              "dtype": DTYPE, "heavy_boost": BOOST})
     return m
 
 
