@@ -304,8 +304,9 @@ def run_ours(args, rank, world):
             "higher_is_better": True,
             "scaling": "strong" if seq else "weak",
             "vs_baseline": None,
-            "dtype": "bf16 storage; QK^T and P.V on mma.sync (fp32 accumulate, P as bf16 hi+lo), "
-                     "fp32 softmax, fp64 MAW/merge",
+            "dtype": "bf16",
+            "numerics": "bf16 storage; QK^T and P.V on mma.sync (fp32 accumulate, P as bf16 hi+lo), "
+                        "fp32 softmax, fp64 MAW/merge",
             "data": "synthetic (torch.randn K/V/q, MAW drawn for 10% threshold selection per query head)",
             "config": {"workload": WORKLOAD, "batch": B, "q_heads": Hq, "kv_heads": Hkv, "head_dim": D,
                        "context": cfgd["context"], "window_blocks": f"{cfgd['blk_num']}x{cfgd['blk_size']}",
@@ -366,7 +367,8 @@ def run_reference(args, rank, world):
         "metric": "hybrid-attn decode tokens/s (1 layer, C2)",
         "value": round(tok, 3), "unit": "tokens/s", "n_gpus": world, "steps": steps, "warmup": warm,
         "ms_per_step": round(ms, 2), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "fp32 (bf16-rounded values upcast), fp64 accumulation (reference _core)",
+        "dtype": "f32",
+        "numerics": "fp32 (bf16-rounded values upcast), fp64 accumulation (reference _core)",
         "data": "synthetic", "config": {"workload": WORKLOAD, "batch": cfgd["batch"]},
         "cpu_baseline": {"value": round(tok, 3), "unit": "tokens/s", "cores": r["workers"], "kind": r["kind"],
                          "sample": f"{steps} step(s) x full batch of {cfgd['batch']} sequences, one process "
