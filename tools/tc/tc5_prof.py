@@ -1,3 +1,11 @@
+"""Per-stage cycle profile of the tcgen05 append pass 1 (C2 scale, n_q = 64).
+
+  python paper_2507_03153_b200/_build.py --variant p5 HGCA_TC5_PROF   # builds libhgca_b200_p5.so
+  python tools/tc/tc5_prof.py                                          # on the GPU box
+
+Prints, per 64-key stage, the MMA thread's cycles waiting for K (TMA) and for P
+(the softmax warps), and the softmax warp's cycles waiting for S and for P.V.
+"""
 import ctypes, os, sys, torch
 sys.path.insert(0, ".")
 os.environ["HGCA_LIB"] = "paper_2507_03153_b200/_lib/libhgca_b200_p5.so"
