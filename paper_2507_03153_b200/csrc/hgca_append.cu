@@ -367,12 +367,12 @@ struct Tc5Cfg {               // D = 128
   static constexpr int OFF_TM = OFF_BAR + NBAR * 8;
   static constexpr int SMEM = OFF_TM + 16 + 1024;       // + alignment slack
   static constexpr int TMEM_COLS = 256;                 // S[2] x 64 | O 128
-  static constexpr int THREADS = 6 * 32;
+  static constexpr int THREADS = 7 * 32;               // TMA, QK issuer, 4 softmax warps, PV issuer
 };
 
 #ifdef HGCA_TC5_PROF
-// debug build: per-CTA cycle counters [0] MMA wait full, [1] MMA wait pfull, [2] MMA total,
-// [3] softmax (warp 2) wait sfull, [4] softmax wait pvdone, [5] softmax total, [6] stages
+// debug build: cycle counters summed over CTAs (softmax warp 2): [3] wait sfull,
+// [4] wait pvdone, [5] total, [6] stages
 __device__ unsigned long long g_tc5prof[8];
 #define P5(...) __VA_ARGS__
 #else
@@ -439,55 +439,51 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
           tma_load_2d(sKV + s * C::STAGE + qd * C::KVQ, &a.kvmap5, qd * 64, rowbase + st * T5_KEYS, &full[s], policy);
       }
     }
-  } else if (warp == 1) {  // ------------------------------------------ MMA issuer
+  } else if (warp == 1 || warp == 6) {  // ----------------------------- MMA issuers
+    // two issuing threads (tcgen05.mma issue costs tens of cycles each):
+    // warp 1 issues S = Q K^T, warp 6 issues O += P V
     if (lane == 0) {
-      mbar_wait(qfull, 0);
-      umma::fence_after_sync();
       constexpr uint32_t IDESC_QK = umma::idesc_bf16_f32(128, T5_KEYS, false, false);
       constexpr uint32_t IDESC_PV = umma::idesc_bf16_f32(128, D, false, true);
-      P5(long long w_full = 0, w_pfull = 0, t_start = clock64();)
-      auto qk = [&](int st) {
-        const int s = st % T5_S, b = st & 1;
-        P5(long long c0 = clock64();)
-        mbar_wait(&full[s], (st / T5_S) & 1);
-        P5(w_full += clock64() - c0;)
+      if (warp == 1) {
+        mbar_wait(qfull, 0);
         umma::fence_after_sync();
-        const uint32_t kb = sKV + s * C::STAGE;
+        for (int st = 0; st < nst; ++st) {
+          const int s = st % T5_S, b = st & 1;
+          mbar_wait(&full[s], (st / T5_S) & 1);
+          // S buffer b was read by softmax(st-2): its P of stage st-2 is out
+          if (st >= 2) mbar_wait(&pfull[b], ((st - 2) >> 1) & 1);
+          umma::fence_after_sync();
+          const uint32_t kb = sKV + s * C::STAGE;
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint64_t ad = umma::smem_desc(sQ + (k / 4) * C::QATOM + (k % 4) * 32, 16, 1024);
-          const uint64_t bd = umma::smem_desc(kb + (k / 4) * C::KVQ + (k % 4) * 32, 16, 1024);
-          umma::mma_bf16(tmem + b * T5_KEYS, ad, bd, IDESC_QK, k > 0);
-        }
-        umma::commit(smem_u32(&sfull[b]));
-      };
-      auto pv = [&](int st) {
-        const int s = st % T5_S, b = st & 1;
-        P5(long long c0 = clock64();)
-        mbar_wait(&pfull[b], (st >> 1) & 1);
-        P5(w_pfull += clock64() - c0;)
-        umma::fence_after_sync();
-        const uint32_t vb = sKV + s * C::STAGE + 2 * C::KVQ;  // V0 then V1: the two 64-column atoms
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {  // P hi, P lo
-          const uint32_t pb = sP + (b * 2 + h) * C::PBUF;
-#pragma unroll
-          for (int j = 0; j < T5_KEYS / 16; ++j) {
-            const uint64_t ad = umma::smem_desc(pb + j * 32, 16, 1024);
-            const uint64_t bd = umma::smem_desc(vb + j * 16 * 128, C::KVQ, 1024);
-            umma::mma_bf16(tmem + O_COL, ad, bd, IDESC_PV, st > 0 || h > 0 || j > 0);
+          for (int k = 0; k < D / 16; ++k) {
+            const uint64_t ad = umma::smem_desc(sQ + (k / 4) * C::QATOM + (k % 4) * 32, 16, 1024);
+            const uint64_t bd = umma::smem_desc(kb + (k / 4) * C::KVQ + (k % 4) * 32, 16, 1024);
+            umma::mma_bf16(tmem + b * T5_KEYS, ad, bd, IDESC_QK, k > 0);
           }
+          umma::commit(smem_u32(&sfull[b]));
         }
-        umma::commit(smem_u32(&pvdone[b]));  // PV(st) -- and every earlier MMA -- complete
-        umma::commit(smem_u32(&empty[s]));
-      };
-      qk(0);
-      for (int st = 1; st <= nst; ++st) {
-        if (st < nst) qk(st);
-        pv(st - 1);
+      } else {
+        for (int st = 0; st < nst; ++st) {
+          const int s = st % T5_S, b = st & 1;
+          // P of stage st written (and so S = Q K^T of stage st complete)
+          mbar_wait(&pfull[b], (st >> 1) & 1);
+          umma::fence_after_sync();
+          const uint32_t vb = sKV + s * C::STAGE + 2 * C::KVQ;  // V0 then V1: the two 64-column atoms
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {  // P hi, P lo
+            const uint32_t pb = sP + (b * 2 + h) * C::PBUF;
+#pragma unroll
+            for (int j = 0; j < T5_KEYS / 16; ++j) {
+              const uint64_t ad = umma::smem_desc(pb + j * 32, 16, 1024);
+              const uint64_t bd = umma::smem_desc(vb + j * 16 * 128, C::KVQ, 1024);
+              umma::mma_bf16(tmem + O_COL, ad, bd, IDESC_PV, st > 0 || h > 0 || j > 0);
+            }
+          }
+          umma::commit(smem_u32(&pvdone[b]));  // PV(st) -- and every earlier PV -- complete
+          umma::commit(smem_u32(&empty[s]));   // K (read by QK(st), complete) and V free
+        }
       }
-      P5(atomicAdd(&g_tc5prof[0], (unsigned long long)w_full); atomicAdd(&g_tc5prof[1], (unsigned long long)w_pfull);
-         atomicAdd(&g_tc5prof[2], (unsigned long long)(clock64() - t_start)); atomicAdd(&g_tc5prof[6], (unsigned long long)nst);)
     }
     __syncwarp();
   } else {  // ------------------------------------------------------- softmax warps
@@ -587,6 +583,7 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
     }
     mbar_wait(&pvdone[(nst - 1) & 1], ((nst - 1) >> 1) & 1);  // the last PV (and all before it)
     P5(if (warp == 2 && lane == 0) { atomicAdd(&g_tc5prof[3], (unsigned long long)w_s);
+       atomicAdd(&g_tc5prof[6], (unsigned long long)nst);
        atomicAdd(&g_tc5prof[4], (unsigned long long)w_pv); atomicAdd(&g_tc5prof[5], (unsigned long long)(clock64() - t_s0)); })
     umma::fence_after_sync();
     // this row's partial (m, z, acc), as append_attend_kernel<D, 1> writes it

@@ -3,8 +3,8 @@
   python paper_2507_03153_b200/_build.py --variant p5 HGCA_TC5_PROF   # builds libhgca_b200_p5.so
   python tools/tc/tc5_prof.py                                          # on the GPU box
 
-Prints, per 64-key stage, the MMA thread's cycles waiting for K (TMA) and for P
-(the softmax warps), and the softmax warp's cycles waiting for S and for P.V.
+Prints, per 64-key stage, a softmax warp's cycles waiting for S = Q K^T, waiting
+for the P.V that frees its P buffer, and in total.
 """
 import ctypes, os, sys, torch
 sys.path.insert(0, ".")
@@ -22,5 +22,5 @@ for nq in (64,):
     buf = (ctypes.c_ulonglong * 8)()
     f(buf)
     st = buf[6]
-    print("stages", st, "per stage cycles: MMA wait full %.0f, wait pfull %.0f, total %.0f | softmax wait S %.0f, wait pvdone %.0f, total %.0f" % (
-        buf[0]/st, buf[1]/st, buf[2]/st, buf[3]/st, buf[4]/st, buf[5]/st))
+    print("stages", st, "per stage cycles (softmax warp): wait S %.0f, wait P.V %.0f, total %.0f" % (
+        buf[3]/st, buf[4]/st, buf[5]/st))
