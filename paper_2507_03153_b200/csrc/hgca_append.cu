@@ -636,7 +636,7 @@ struct Tc5MCfg {               // D = 128
   static constexpr int OFF_TM = OFF_BAR + NBAR * 8;
   static constexpr int SMEM = OFF_TM + 16 + 1024;
   static constexpr int TMEM_COLS = 256;                 // S[2] x 64 | MEAN[2] x 64
-  static constexpr int THREADS = 6 * 32;
+  static constexpr int THREADS = 7 * 32;               // TMA, QK issuer, 4 row warps, GEMM issuer
 };
 
 __global__ void __launch_bounds__(Tc5MCfg::THREADS, 1) append_tc5_mean_kernel(const __grid_constant__ AppendArgs a) {
@@ -677,7 +677,7 @@ __global__ void __launch_bounds__(Tc5MCfg::THREADS, 1) append_tc5_mean_kernel(co
     }
     fence_mbar_init();
   }
-  if (warp >= 2) {  // head-membership matrix A [128 heads][128 rows], K-major SW128
+  if (warp >= 2 && warp < 6) {  // head-membership matrix A [128 heads][128 rows], K-major SW128 (row warps)
     const int h = threadIdx.x - 64;
     unsigned char* arow = sm + C::OFF_A + (h >> 3) * 1024 + (h & 7) * 128;
 #pragma unroll
@@ -718,46 +718,46 @@ __global__ void __launch_bounds__(Tc5MCfg::THREADS, 1) append_tc5_mean_kernel(co
         tma_load_2d(sK + s * C::STAGE + C::KQ, &a.kvmap5, 64, rowbase + st * T5_KEYS, &full[s], policy);
       }
     }
-  } else if (warp == 1) {  // ------------------------------------------ MMA issuer
+  } else if (warp == 1 || warp == 6) {  // ----------------------------- MMA issuers
+    // warp 1 issues S = Q K^T, warp 6 the head-sum GEMM MEAN = A . W
     if (lane == 0) {
-      mbar_wait(qfull, 0);
-      umma::fence_after_sync();
       constexpr uint32_t IDESC_QK = umma::idesc_bf16_f32(128, T5_KEYS, false, false);
       constexpr uint32_t IDESC_M = umma::idesc_bf16_f32(128, T5_KEYS, false, true);
-      auto qk = [&](int st) {
-        const int s = st % C::S, b = st & 1;
-        mbar_wait(&full[s], (st / C::S) & 1);
+      if (warp == 1) {
+        mbar_wait(qfull, 0);
         umma::fence_after_sync();
-        const uint32_t kb = sK + s * C::STAGE;
+        for (int st = 0; st < nst; ++st) {
+          const int s = st % C::S, b = st & 1;
+          mbar_wait(&full[s], (st / C::S) & 1);
+          if (st >= 2) mbar_wait(&wfull[b], ((st - 2) >> 1) & 1);  // S buffer b read by the rows of stage st-2
+          umma::fence_after_sync();
+          const uint32_t kb = sK + s * C::STAGE;
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint64_t ad = umma::smem_desc(sQ + (k / 4) * C::QATOM + (k % 4) * 32, 16, 1024);
-          const uint64_t bd = umma::smem_desc(kb + (k / 4) * C::KQ + (k % 4) * 32, 16, 1024);
-          umma::mma_bf16(tmem + b * T5_KEYS, ad, bd, IDESC_QK, k > 0);
-        }
-        umma::commit(smem_u32(&sfull[b]));
-        umma::commit(smem_u32(&empty[s]));  // K is read by this GEMM only
-      };
-      auto mm = [&](int st) {
-        const int b = st & 1;
-        mbar_wait(&wfull[b], (st >> 1) & 1);
-        umma::fence_after_sync();
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {  // W hi, W lo
-          const uint32_t wb = sW + (b * 2 + h) * C::WBUF;
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {  // 16 rows per step
-            const uint64_t ad = umma::smem_desc(sA + (k / 4) * C::QATOM + (k % 4) * 32, 16, 1024);
-            const uint64_t bd = umma::smem_desc(wb + k * 16 * 128, C::WBUF, 1024);
-            umma::mma_bf16(tmem + M_COL + b * T5_KEYS, ad, bd, IDESC_M, h > 0 || k > 0);
+          for (int k = 0; k < D / 16; ++k) {
+            const uint64_t ad = umma::smem_desc(sQ + (k / 4) * C::QATOM + (k % 4) * 32, 16, 1024);
+            const uint64_t bd = umma::smem_desc(kb + (k / 4) * C::KQ + (k % 4) * 32, 16, 1024);
+            umma::mma_bf16(tmem + b * T5_KEYS, ad, bd, IDESC_QK, k > 0);
           }
+          umma::commit(smem_u32(&sfull[b]));
+          umma::commit(smem_u32(&empty[s]));  // K is read by this GEMM only
         }
-        umma::commit(smem_u32(&mdone[b]));
-      };
-      qk(0);
-      for (int st = 1; st <= nst; ++st) {
-        if (st < nst) qk(st);
-        mm(st - 1);
+      } else {
+        for (int st = 0; st < nst; ++st) {
+          const int b = st & 1;
+          mbar_wait(&wfull[b], (st >> 1) & 1);
+          umma::fence_after_sync();
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {  // W hi, W lo
+            const uint32_t wb = sW + (b * 2 + h) * C::WBUF;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {  // 16 rows per step
+              const uint64_t ad = umma::smem_desc(sA + (k / 4) * C::QATOM + (k % 4) * 32, 16, 1024);
+              const uint64_t bd = umma::smem_desc(wb + k * 16 * 128, C::WBUF, 1024);
+              umma::mma_bf16(tmem + M_COL + b * T5_KEYS, ad, bd, IDESC_M, h > 0 || k > 0);
+            }
+          }
+          umma::commit(smem_u32(&mdone[b]));
+        }
       }
     }
     __syncwarp();
