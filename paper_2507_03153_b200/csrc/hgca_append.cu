@@ -612,6 +612,265 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
   if (warp == 1) umma::tmem_dealloc<C::TMEM_COLS>(tmem);
 }
 
+// ------------------------------------------------------------------ tcgen05 pass 1, two tiles
+// For (batch, kv-head)s with >= 2 row groups of 128 (G * n_q >= 256): one CTA
+// takes two row groups (tiles) against the same keys, so each K|V stage is
+// loaded once for both, and the tiles' softmax warps (4 each) run side by side
+// while the tensor core works on the other tile (as FA4 ping-pongs two Q tiles).
+// Per tile: S double-buffered in TMEM, P (hi, lo) single-buffered in shared
+// memory (rewritten after the tile's previous P V completed), O in TMEM.
+struct Tc5x2Cfg {              // D = 128
+  static constexpr int QATOM = 128 * 128;
+  static constexpr int KVQ = T5_KEYS * 128;
+  static constexpr int S = 3;
+  static constexpr int STAGE = 4 * KVQ;                 // K0 K1 V0 V1
+  static constexpr int PBUF = 128 * 128;
+  static constexpr int OFF_Q = 0;                       // [tile][2 atoms]
+  static constexpr int OFF_KV = OFF_Q + 4 * QATOM;
+  static constexpr int OFF_P = OFF_KV + S * STAGE;      // [tile][hi, lo]
+  static constexpr int OFF_BAR = OFF_P + 4 * PBUF;
+  static constexpr int NBAR = 1 + 2 * S + 2 + 8;        // qfull, full[S], empty[S], sfull[2], pfull[2][2], pvdone[2][2]
+  static constexpr int OFF_TM = OFF_BAR + NBAR * 8;
+  static constexpr int SMEM = OFF_TM + 16 + 1024;
+  static constexpr int TMEM_COLS = 512;                 // S[2 tiles][2] x 64 | O[2 tiles] x 128
+  static constexpr int THREADS = 11 * 32;               // TMA, QK, softmax 2-5 (tile 0), PV, softmax 7-10 (tile 1)
+};
+
+__global__ void __launch_bounds__(Tc5x2Cfg::THREADS, 1) append_tc5x2_kernel(const __grid_constant__ AppendArgs a) {
+  using C = Tc5x2Cfg;
+  constexpr int D = 128;
+  constexpr uint32_t O_COL = 4 * T5_KEYS;
+  extern __shared__ unsigned char sm_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);
+  uint64_t* qfull = bars;
+  uint64_t* full = bars + 1;
+  uint64_t* empty = full + C::S;
+  uint64_t* sfull = empty + C::S;
+  uint64_t* pfull = sfull + 2;   // [tile][parity]
+  uint64_t* pvdone = pfull + 4;  // [tile][parity]
+  uint32_t* tm_holder = reinterpret_cast<uint32_t*>(sm + C::OFF_TM);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // item -> (bk, tile pair, segment, chunk)
+  const int64_t nc = a.nch[0] + a.nch[1], npair = (a.n_rg + 1) / 2;
+  const int64_t cidx = blockIdx.x % nc, t_ = blockIdx.x / nc;
+  const int64_t pair = t_ % npair, bk = t_ / npair;
+  const int seg = cidx < a.nch[0] ? 0 : 1;
+  const int64_t chunk = seg ? cidx - a.nch[0] : cidx;
+  bool valid[2];
+  valid[0] = true;
+  valid[1] = 2 * pair + 1 < a.n_rg;
+  const int64_t p0 = a.seg_lo[seg] + chunk * ACHUNK;
+  const int64_t p1 = min(a.seg_hi[seg], p0 + ACHUNK);
+  const int64_t p0a = p0 & ~(int64_t)7;
+  const int nst = (int)((p1 - p0a + T5_KEYS - 1) / T5_KEYS);
+  if (threadIdx.x == 0) {
+    mbar_init(qfull, 1);
+    for (int s = 0; s < C::S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) mbar_init(&sfull[i], 1);
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&pfull[i], 4);
+      mbar_init(&pvdone[i], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) umma::tmem_alloc<C::TMEM_COLS>(smem_u32(tm_holder));
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+  const uint32_t tmem = *tm_holder;
+  const uint32_t sQ = smem_u32(sm + C::OFF_Q), sKV = smem_u32(sm + C::OFF_KV), sP = smem_u32(sm + C::OFF_P);
+
+  if (warp == 0) {  // ------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const uint64_t policy = l2_evict_first_policy();
+      const int64_t b = bk / a.Hkv, kvh = bk % a.Hkv;
+      const int nt = valid[1] ? 2 : 1;
+      mbar_expect_tx(qfull, nt * 2 * C::QATOM);
+      for (int t = 0; t < nt; ++t) {
+        const int qrow = (int)((b * a.Hq + kvh * a.G) * a.nq + (2 * pair + t) * a.RG);
+        tma_load_2d(sQ + t * 2 * C::QATOM, &a.qmap5, 0, qrow, qfull, policy);
+        tma_load_2d(sQ + t * 2 * C::QATOM + C::QATOM, &a.qmap5, 64, qrow, qfull, policy);
+      }
+      const int rowbase = (int)(bk * a.T + p0a);
+      for (int st = 0; st < nst; ++st) {
+        const int s = st % C::S;
+        if (st >= C::S) mbar_wait(&empty[s], ((st / C::S) - 1) & 1);
+        mbar_expect_tx(&full[s], C::STAGE);
+#pragma unroll
+        for (int qd = 0; qd < 4; ++qd)
+          tma_load_2d(sKV + s * C::STAGE + qd * C::KVQ, &a.kvmap5, qd * 64, rowbase + st * T5_KEYS, &full[s], policy);
+      }
+    }
+  } else if (warp == 1 || warp == 6) {  // ----------------------------- MMA issuers
+    if (lane == 0) {
+      constexpr uint32_t IDESC_QK = umma::idesc_bf16_f32(128, T5_KEYS, false, false);
+      constexpr uint32_t IDESC_PV = umma::idesc_bf16_f32(128, D, false, true);
+      if (warp == 1) {  // S = Q K^T for both tiles
+        mbar_wait(qfull, 0);
+        umma::fence_after_sync();
+        for (int st = 0; st < nst; ++st) {
+          const int s = st % C::S, b = st & 1;
+          mbar_wait(&full[s], (st / C::S) & 1);
+          for (int t = 0; t < 2; ++t)  // S[t][b] was read by the tile's softmax of stage st-2
+            if (valid[t] && st >= 2) mbar_wait(&pfull[t * 2 + b], ((st - 2) >> 1) & 1);
+          umma::fence_after_sync();
+          const uint32_t kb = sKV + s * C::STAGE;
+          for (int t = 0; t < 2; ++t) {
+            if (!valid[t]) continue;
+#pragma unroll
+            for (int k = 0; k < D / 16; ++k) {
+              const uint64_t ad = umma::smem_desc(sQ + t * 2 * C::QATOM + (k / 4) * C::QATOM + (k % 4) * 32, 16, 1024);
+              const uint64_t bd = umma::smem_desc(kb + (k / 4) * C::KVQ + (k % 4) * 32, 16, 1024);
+              umma::mma_bf16(tmem + (t * 2 + b) * T5_KEYS, ad, bd, IDESC_QK, k > 0);
+            }
+          }
+          umma::commit(smem_u32(&sfull[b]));
+        }
+      } else {  // O[t] += P[t] V
+        for (int st = 0; st < nst; ++st) {
+          const int s = st % C::S, b = st & 1;
+          const uint32_t vb = sKV + s * C::STAGE + 2 * C::KVQ;
+          for (int t = 0; t < 2; ++t) {
+            if (!valid[t]) continue;
+            mbar_wait(&pfull[t * 2 + b], (st >> 1) & 1);
+            umma::fence_after_sync();
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const uint32_t pb = sP + (t * 2 + h) * C::PBUF;
+#pragma unroll
+              for (int j = 0; j < T5_KEYS / 16; ++j) {
+                const uint64_t ad = umma::smem_desc(pb + j * 32, 16, 1024);
+                const uint64_t bd = umma::smem_desc(vb + j * 16 * 128, C::KVQ, 1024);
+                umma::mma_bf16(tmem + O_COL + t * D, ad, bd, IDESC_PV, st > 0 || h > 0 || j > 0);
+              }
+            }
+            umma::commit(smem_u32(&pvdone[t * 2 + b]));
+          }
+          umma::commit(smem_u32(&empty[s]));  // both tiles' QK (complete) and PV of this stage
+        }
+      }
+    }
+    __syncwarp();
+  } else {  // ------------------------------------------------------- softmax warps
+    const int t = warp >= 7 ? 1 : 0;
+    if (valid[t]) {
+      const int quarter = warp & 3;
+      const int r = quarter * 32 + lane;
+      const uint32_t tl = (uint32_t)(quarter * 32) << 16;
+      const float sl2 = a.scale * 1.4426950408889634f;
+      float mu2 = -INFINITY, z = 0.f;
+      const uint32_t prow = (uint32_t)((r >> 3) * 1024 + (r & 7) * 128);
+      for (int st = 0; st < nst; ++st) {
+        const int b = st & 1;
+        mbar_wait(&sfull[b], (st >> 1) & 1);
+        umma::fence_after_sync();
+        float x[T5_KEYS];
+        {
+          uint32_t v[4][16];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) umma::ld_32x32b_x16(tmem + tl + (t * 2 + b) * T5_KEYS + c * 16, v[c]);
+          umma::ld_wait();
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int j = 0; j < 16; ++j) x[c * 16 + j] = __uint_as_float(v[c][j]);
+        }
+        const int64_t kp0 = p0a + (int64_t)st * T5_KEYS;
+        float mx = -INFINITY;
+        if (kp0 >= p0 && kp0 + T5_KEYS <= p1) {
+#pragma unroll
+          for (int j = 0; j < T5_KEYS; ++j) {
+            x[j] *= sl2;
+            mx = fmaxf(mx, x[j]);
+          }
+        } else {
+          const int jlo = (int)max(p0 - kp0, (int64_t)0), jhi = (int)min(p1 - kp0, (int64_t)T5_KEYS);
+#pragma unroll
+          for (int j = 0; j < T5_KEYS; ++j) {
+            x[j] = (j >= jlo && j < jhi) ? x[j] * sl2 : -INFINITY;
+            mx = fmaxf(mx, x[j]);
+          }
+        }
+        float alpha = 1.f;
+        if (mx > mu2 + T5_HEADROOM2) {
+          alpha = mu2 == -INFINITY ? 0.f : ex2_approx(mu2 - mx);
+          mu2 = mx;
+        }
+        float sum = 0.f;
+#pragma unroll
+        for (int j = 0; j < T5_KEYS; ++j) {
+          x[j] = ex2_approx(x[j] - mu2);
+          sum += x[j];
+        }
+        z = z * alpha + sum;
+        if (st >= 1) {  // the tile's PV(st-1): P free again, O stable for a rescale
+          mbar_wait(&pvdone[t * 2 + (b ^ 1)], ((st - 1) >> 1) & 1);
+          umma::fence_after_sync();
+          if (__any_sync(FULL_MASK, alpha != 1.f)) {
+#pragma unroll
+            for (int c0 = 0; c0 < D; c0 += 16) {
+              uint32_t v[16];
+              umma::ld_32x32b_x16(tmem + tl + O_COL + t * D + c0, v);
+              umma::ld_wait();
+#pragma unroll
+              for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * alpha);
+              umma::st_32x32b_x16(tmem + tl + O_COL + t * D + c0, v);
+            }
+            umma::st_wait();
+          }
+        }
+        unsigned char* ph = sm + C::OFF_P + (t * 2) * C::PBUF + prow;
+        unsigned char* pl = ph + C::PBUF;
+#pragma unroll
+        for (int c = 0; c < T5_KEYS / 8; ++c) {
+          uint32_t hi[4], lo[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            hi[e] = pack_bf16(x[c * 8 + 2 * e], x[c * 8 + 2 * e + 1]);
+            lo[e] = pack_bf16(x[c * 8 + 2 * e] - bf16_lo_f(hi[e]), x[c * 8 + 2 * e + 1] - bf16_hi_f(hi[e]));
+          }
+          const uint32_t off = (uint32_t)((c ^ (r & 7)) << 4);
+          *reinterpret_cast<uint4*>(ph + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+          *reinterpret_cast<uint4*>(pl + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        }
+        umma::fence_smem_async();
+        umma::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pfull[t * 2 + b]);
+      }
+      mbar_wait(&pvdone[t * 2 + ((nst - 1) & 1)], ((nst - 1) >> 1) & 1);
+      umma::fence_after_sync();
+      const int64_t rg = 2 * pair + t;
+      const bool mine = r < a.RG && rg * a.RG + r < a.R;
+      const int64_t item = (bk * a.n_rg + rg) * nc + cidx;  // the (bk, row group, segment, chunk) item
+      float4* pa = reinterpret_cast<float4*>(a.part_acc + (item * a.RG + r) * D);
+#pragma unroll
+      for (int c0 = 0; c0 < D; c0 += 16) {
+        uint32_t v[16];
+        umma::ld_32x32b_x16(tmem + tl + O_COL + t * D + c0, v);
+        umma::ld_wait();
+        if (mine) {
+#pragma unroll
+          for (int j = 0; j < 16; j += 4)
+            pa[(c0 + j) / 4] = make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
+                                           __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
+        }
+      }
+      if (mine) {
+        a.part_m[item * a.RG + r] = mu2 == -INFINITY ? -INFINITY : mu2 * 0.6931471805599453f;
+        a.part_z[item * a.RG + r] = z;
+      }
+    }
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  if (warp == 1) umma::tmem_dealloc<C::TMEM_COLS>(tmem);
+}
+
 // ------------------------------------------------------------------ tcgen05 pass 2
 // The per-(query head, position) mean weights for a 128-row group on the
 // tensor cores: S = Q K^T as in pass 1, the rows' final weights
@@ -1061,7 +1320,18 @@ static int launch_append_d(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, i
     // row groups of >= 64 rows (the M = 128 tile's cost is per item; tiny groups stay on mma.sync)
     const char* force_mma = getenv("HGCA_APPEND_MMA_SYNC");  // A/B switch: 1 = the mma.sync pass for every group
     const bool tc5 = p.RG >= 64 && !(force_mma && *force_mma && *force_mma != '0');
-    if (p.n_items > 0 && tc5)
+    static bool attr52 = false;
+    if (!attr52) {
+      const cudaError_t e52 =
+          cudaFuncSetAttribute(append_tc5x2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Tc5x2Cfg::SMEM);
+      if (e52 != cudaSuccess) return (int)e52;
+      attr52 = true;
+    }
+    const bool two_tiles = tc5 && p.RG == 128 && p.n_rg >= 2;  // pairs of 128-row groups share the K|V stream
+    if (p.n_items > 0 && two_tiles)
+      append_tc5x2_kernel<<<(unsigned)(B * Hkv * ((p.n_rg + 1) / 2) * (p.nch0 + p.nch1)), Tc5x2Cfg::THREADS,
+                            Tc5x2Cfg::SMEM, s>>>(a);
+    else if (p.n_items > 0 && tc5)
       append_tc5_kernel<<<(unsigned)p.n_items, Tc5Cfg::THREADS, Tc5Cfg::SMEM, s>>>(a);
     else if (p.n_items > 0)
       append_attend_kernel<D, 1><<<(unsigned)p.n_items, (nw + 1) * 32, C1::SMEM, s>>>(a);
