@@ -1118,6 +1118,267 @@ __global__ void __launch_bounds__(Tc5MCfg::THREADS, 1) append_tc5_mean_kernel(co
   if (warp == 1) umma::tmem_dealloc<C::TMEM_COLS>(tmem);
 }
 
+// ------------------------------------------------------------------ tcgen05 pass 2, two tiles
+// The mean-weight pass for two 128-row groups of a (batch, kv-head) per CTA:
+// one K stream, one head-membership matrix (the tiles have the same head
+// layout), per tile: S double-buffered, W (hi, lo) single-buffered, MEAN
+// double-buffered in TMEM, its own row warps and readout warp.
+struct Tc5Mx2Cfg {             // D = 128
+  static constexpr int QATOM = 128 * 128;
+  static constexpr int KQ = T5_KEYS * 128;
+  static constexpr int S = 4;
+  static constexpr int STAGE = 2 * KQ;                  // K0 K1
+  static constexpr int WBUF = 128 * 128;
+  static constexpr int OFF_Q = 0;                       // [tile][2 atoms]
+  static constexpr int OFF_K = OFF_Q + 4 * QATOM;
+  static constexpr int OFF_W = OFF_K + S * STAGE;       // [tile][hi, lo]
+  static constexpr int OFF_A = OFF_W + 4 * WBUF;
+  static constexpr int OFF_BAR = OFF_A + 2 * QATOM;
+  static constexpr int NBAR = 1 + 2 * S + 2 + 8;        // qfull, full[S], empty[S], sfull[2], wfull[2][2], mdone[2][2]
+  static constexpr int OFF_TM = OFF_BAR + NBAR * 8;
+  static constexpr int SMEM = OFF_TM + 16 + 1024;
+  static constexpr int TMEM_COLS = 512;                 // S[2][2] x 64 | MEAN[2][2] x 64
+  static constexpr int THREADS = 11 * 32;
+};
+
+__global__ void __launch_bounds__(Tc5Mx2Cfg::THREADS, 1) append_tc5_mean_x2_kernel(const __grid_constant__ AppendArgs a) {
+  using C = Tc5Mx2Cfg;
+  constexpr int D = 128;
+  constexpr uint32_t M_COL = 4 * T5_KEYS;
+  extern __shared__ unsigned char sm_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  const int64_t nc = a.nch[0] + a.nch[1], npair = (a.n_rg + 1) / 2;
+  const int64_t cidx = blockIdx.x % nc, t_ = blockIdx.x / nc;
+  const int64_t pair = t_ % npair, bk = t_ / npair;
+  const int seg = cidx < a.nch[0] ? 0 : 1;
+  const int64_t chunk = seg ? cidx - a.nch[0] : cidx;
+  if (!a.mean[seg]) return;
+  bool valid[2];
+  valid[0] = true;
+  valid[1] = 2 * pair + 1 < a.n_rg;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);
+  uint64_t* qfull = bars;
+  uint64_t* full = bars + 1;
+  uint64_t* empty = full + C::S;
+  uint64_t* sfull = empty + C::S;
+  uint64_t* wfull = sfull + 2;   // [tile][parity]
+  uint64_t* mdone = wfull + 4;   // [tile][parity]
+  uint32_t* tm_holder = reinterpret_cast<uint32_t*>(sm + C::OFF_TM);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t p0 = a.seg_lo[seg] + chunk * ACHUNK;
+  const int64_t p1 = min(a.seg_hi[seg], p0 + ACHUNK);
+  const int64_t p0a = p0 & ~(int64_t)7;
+  const int nst = (int)((p1 - p0a + T5_KEYS - 1) / T5_KEYS);
+  const int nq = (int)a.nq, heads = (int)(a.RG / a.nq);
+  const int64_t b_ = bk / a.Hkv, kvh = bk % a.Hkv;
+  if (threadIdx.x == 0) {
+    mbar_init(qfull, 1);
+    for (int s = 0; s < C::S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) mbar_init(&sfull[i], 1);
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&wfull[i], 4);
+      mbar_init(&mdone[i], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp >= 2 && warp < 6) {  // head-membership matrix A [128 heads][128 rows], K-major SW128
+    const int h = threadIdx.x - 64;
+    unsigned char* arow = sm + C::OFF_A + (h >> 3) * 1024 + (h & 7) * 128;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      uint32_t v[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r0 = c * 8 + 2 * e;
+        const float x0 = (h < heads && r0 / nq == h) ? 1.f : 0.f;
+        const float x1 = (h < heads && (r0 + 1) / nq == h) ? 1.f : 0.f;
+        v[e] = pack_bf16(x0, x1);
+      }
+      *reinterpret_cast<uint4*>(arow + (c >> 3) * C::QATOM + (((c & 7) ^ (h & 7)) << 4)) = make_uint4(v[0], v[1], v[2], v[3]);
+    }
+    umma::fence_smem_async();
+  }
+  if (warp == 1) umma::tmem_alloc<C::TMEM_COLS>(smem_u32(tm_holder));
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+  const uint32_t tmem = *tm_holder;
+  const uint32_t sQ = smem_u32(sm + C::OFF_Q), sK = smem_u32(sm + C::OFF_K), sW = smem_u32(sm + C::OFF_W),
+                 sA = smem_u32(sm + C::OFF_A);
+
+  if (warp == 0) {  // ------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const uint64_t policy = l2_evict_first_policy();
+      const int nt = valid[1] ? 2 : 1;
+      mbar_expect_tx(qfull, nt * 2 * C::QATOM);
+      for (int t = 0; t < nt; ++t) {
+        const int qrow = (int)((b_ * a.Hq + kvh * a.G) * a.nq + (2 * pair + t) * a.RG);
+        tma_load_2d(sQ + t * 2 * C::QATOM, &a.qmap5, 0, qrow, qfull, policy);
+        tma_load_2d(sQ + t * 2 * C::QATOM + C::QATOM, &a.qmap5, 64, qrow, qfull, policy);
+      }
+      const int rowbase = (int)(bk * a.T + p0a);
+      for (int st = 0; st < nst; ++st) {
+        const int s = st % C::S;
+        if (st >= C::S) mbar_wait(&empty[s], ((st / C::S) - 1) & 1);
+        mbar_expect_tx(&full[s], C::STAGE);
+        tma_load_2d(sK + s * C::STAGE, &a.kvmap5, 0, rowbase + st * T5_KEYS, &full[s], policy);
+        tma_load_2d(sK + s * C::STAGE + C::KQ, &a.kvmap5, 64, rowbase + st * T5_KEYS, &full[s], policy);
+      }
+    }
+  } else if (warp == 1 || warp == 6) {  // ----------------------------- MMA issuers
+    if (lane == 0) {
+      constexpr uint32_t IDESC_QK = umma::idesc_bf16_f32(128, T5_KEYS, false, false);
+      constexpr uint32_t IDESC_M = umma::idesc_bf16_f32(128, T5_KEYS, false, true);
+      if (warp == 1) {
+        mbar_wait(qfull, 0);
+        umma::fence_after_sync();
+        for (int st = 0; st < nst; ++st) {
+          const int s = st % C::S, b = st & 1;
+          mbar_wait(&full[s], (st / C::S) & 1);
+          for (int t = 0; t < 2; ++t)  // S[t][b] was read by the tile's rows of stage st-2
+            if (valid[t] && st >= 2) mbar_wait(&wfull[t * 2 + b], ((st - 2) >> 1) & 1);
+          umma::fence_after_sync();
+          const uint32_t kb = sK + s * C::STAGE;
+          for (int t = 0; t < 2; ++t) {
+            if (!valid[t]) continue;
+#pragma unroll
+            for (int k = 0; k < D / 16; ++k) {
+              const uint64_t ad = umma::smem_desc(sQ + t * 2 * C::QATOM + (k / 4) * C::QATOM + (k % 4) * 32, 16, 1024);
+              const uint64_t bd = umma::smem_desc(kb + (k / 4) * C::KQ + (k % 4) * 32, 16, 1024);
+              umma::mma_bf16(tmem + (t * 2 + b) * T5_KEYS, ad, bd, IDESC_QK, k > 0);
+            }
+          }
+          umma::commit(smem_u32(&sfull[b]));
+          umma::commit(smem_u32(&empty[s]));  // K is read by these GEMMs only
+        }
+      } else {
+        for (int st = 0; st < nst; ++st) {
+          const int b = st & 1;
+          for (int t = 0; t < 2; ++t) {
+            if (!valid[t]) continue;
+            mbar_wait(&wfull[t * 2 + b], (st >> 1) & 1);
+            umma::fence_after_sync();
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const uint32_t wb = sW + (t * 2 + h) * C::WBUF;
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const uint64_t ad = umma::smem_desc(sA + (k / 4) * C::QATOM + (k % 4) * 32, 16, 1024);
+                const uint64_t bd = umma::smem_desc(wb + k * 16 * 128, C::WBUF, 1024);
+                umma::mma_bf16(tmem + M_COL + (t * 2 + b) * T5_KEYS, ad, bd, IDESC_M, h > 0 || k > 0);
+              }
+            }
+            umma::commit(smem_u32(&mdone[t * 2 + b]));
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else {  // ------------------------------------------------------- row warps
+    const int t = warp >= 7 ? 1 : 0;
+    if (valid[t]) {
+      const int quarter = warp & 3;
+      const int r = quarter * 32 + lane;
+      const uint32_t tl = (uint32_t)(quarter * 32) << 16;
+      const float sl2 = a.scale * 1.4426950408889634f;
+      const int64_t rg = 2 * pair + t, g0 = rg * a.RG / a.nq;
+      float m2 = INFINITY, rz = 0.f;
+      if (r < a.RG && rg * a.RG + r < a.R) {
+        const float* f = a.fin + ((bk * a.R + rg * a.RG + r) * 2 + seg) * 2;
+        m2 = f[0] * 1.4426950408889634f;
+        rz = 1.f / f[1];
+      }
+      const float inv_nq = 1.f / (float)nq;
+      auto readout = [&](int j) {  // the warp whose TMEM lanes 0-31 hold the heads
+        const int b = j & 1;
+        mbar_wait(&mdone[t * 2 + b], (j >> 1) & 1);
+        umma::fence_after_sync();
+        uint32_t v[4][16];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) umma::ld_32x32b_x16(tmem + tl + M_COL + (t * 2 + b) * T5_KEYS + c * 16, v[c]);
+        umma::ld_wait();
+        if (lane < heads && g0 + lane < a.G) {
+          const int64_t kp0 = p0a + (int64_t)j * T5_KEYS;
+          float* dst = a.mean[seg] + (b_ * a.Hq + kvh * a.G + g0 + lane) * a.mean_ld[seg] - a.seg_lo[seg] + kp0;
+          const bool aligned = ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
+          if (kp0 >= p0 && kp0 + T5_KEYS <= p1 && aligned) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+              for (int e = 0; e < 16; e += 4)
+                *reinterpret_cast<float4*>(dst + c * 16 + e) =
+                    make_float4(__uint_as_float(v[c][e]) * inv_nq, __uint_as_float(v[c][e + 1]) * inv_nq,
+                                __uint_as_float(v[c][e + 2]) * inv_nq, __uint_as_float(v[c][e + 3]) * inv_nq);
+          } else {
+            const int jlo = (int)max(p0 - kp0, (int64_t)0), jhi = (int)min(p1 - kp0, (int64_t)T5_KEYS);
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+              for (int e = 0; e < 16; ++e)
+                if (c * 16 + e >= jlo && c * 16 + e < jhi) dst[c * 16 + e] = __uint_as_float(v[c][e]) * inv_nq;
+          }
+        }
+      };
+      const uint32_t prow = (uint32_t)((r >> 3) * 1024 + (r & 7) * 128);
+      for (int st = 0; st < nst; ++st) {
+        const int b = st & 1;
+        mbar_wait(&sfull[b], (st >> 1) & 1);
+        umma::fence_after_sync();
+        float x[T5_KEYS];
+        {
+          uint32_t v[4][16];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) umma::ld_32x32b_x16(tmem + tl + (t * 2 + b) * T5_KEYS + c * 16, v[c]);
+          umma::ld_wait();
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int j = 0; j < 16; ++j) x[c * 16 + j] = __uint_as_float(v[c][j]);
+        }
+        const int64_t kp0 = p0a + (int64_t)st * T5_KEYS;
+        if (kp0 >= p0 && kp0 + T5_KEYS <= p1) {
+#pragma unroll
+          for (int j = 0; j < T5_KEYS; ++j) x[j] = ex2_approx(fmaf(x[j], sl2, -m2)) * rz;
+        } else {
+          const int jlo = (int)max(p0 - kp0, (int64_t)0), jhi = (int)min(p1 - kp0, (int64_t)T5_KEYS);
+#pragma unroll
+          for (int j = 0; j < T5_KEYS; ++j) {
+            const float w = ex2_approx(fmaf(x[j], sl2, -m2)) * rz;
+            x[j] = (j >= jlo && j < jhi) ? w : 0.f;
+          }
+        }
+        if (st >= 1) mbar_wait(&mdone[t * 2 + (b ^ 1)], ((st - 1) >> 1) & 1);  // W (single buffer) read by MEAN(st-1)
+        unsigned char* wh = sm + C::OFF_W + (t * 2) * C::WBUF + prow;
+        unsigned char* wl = wh + C::WBUF;
+#pragma unroll
+        for (int c = 0; c < T5_KEYS / 8; ++c) {
+          uint32_t hi[4], lo[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            hi[e] = pack_bf16(x[c * 8 + 2 * e], x[c * 8 + 2 * e + 1]);
+            lo[e] = pack_bf16(x[c * 8 + 2 * e] - bf16_lo_f(hi[e]), x[c * 8 + 2 * e + 1] - bf16_hi_f(hi[e]));
+          }
+          const uint32_t off = (uint32_t)((c ^ (r & 7)) << 4);
+          *reinterpret_cast<uint4*>(wh + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+          *reinterpret_cast<uint4*>(wl + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        }
+        umma::fence_smem_async();
+        umma::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&wfull[t * 2 + b]);
+        if (quarter == 0 && st >= 1) readout(st - 1);
+      }
+      if (quarter == 0) readout(nst - 1);
+    }
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  if (warp == 1) umma::tmem_dealloc<C::TMEM_COLS>(tmem);
+}
+
 // One warp per (b, kv-head, row): fold the chunk partials of both segments,
 // merge_states(archive, window) (attention.py:153-188), out / lse, and the
 // row's final (m, z) per segment for pass 2.
@@ -1356,7 +1617,18 @@ static int launch_append_d(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, i
         if (em != cudaSuccess) return (int)em;
         attr_m = true;
       }
-      if (tc5_mean) append_tc5_mean_kernel<<<(unsigned)p.n_items, Tc5MCfg::THREADS, Tc5MCfg::SMEM, s>>>(a);
+      static bool attr_m2 = false;
+      if (tc5_mean && !attr_m2) {
+        const cudaError_t em2 = cudaFuncSetAttribute(append_tc5_mean_x2_kernel,
+                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, Tc5Mx2Cfg::SMEM);
+        if (em2 != cudaSuccess) return (int)em2;
+        attr_m2 = true;
+      }
+      if (tc5_mean && p.RG == 128 && p.n_rg >= 2)  // pairs of 128-row groups share the K stream
+        append_tc5_mean_x2_kernel<<<(unsigned)(B * Hkv * ((p.n_rg + 1) / 2) * (p.nch0 + p.nch1)), Tc5Mx2Cfg::THREADS,
+                                    Tc5Mx2Cfg::SMEM, s>>>(a);
+      else if (tc5_mean)
+        append_tc5_mean_kernel<<<(unsigned)p.n_items, Tc5MCfg::THREADS, Tc5MCfg::SMEM, s>>>(a);
     }
     if (!tc5_mean) append_attend_kernel<D, 2><<<(unsigned)p.n_items, (nw + 1) * 32, C2::SMEM, s>>>(a);
   }

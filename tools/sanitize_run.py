@@ -44,5 +44,7 @@ if __name__ == "__main__":
         run("bfloat16", steps=3, append_at=0)
     if mode in ("all", "bf16-append-tc5"):  # G*n_q = 64 rows: the tcgen05 append passes
         run("bfloat16", steps=3, append_at=0, append_nq=16)
+    if mode in ("all", "bf16-append-tc5x2"):  # G*n_q = 256 rows: the two-tile tcgen05 passes
+        run("bfloat16", steps=3, append_at=0, append_nq=64)
     if mode in ("all", "f32"):
         run("float32", steps=80)
