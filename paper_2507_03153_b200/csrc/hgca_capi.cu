@@ -245,6 +245,10 @@ int hgca_peer_alloc(int64_t bytes, void** ptr, void* handle64) {
   if (rc) return rc;
   rc = cuda_status((int)cudaMemset(*ptr, 0, (size_t)bytes), "peer_alloc: memset");
   if (rc) return rc;
+  // the zeroed boxes and flags must be in place before any rank's kernels (on
+  // other, non-blocking streams -- or in other processes) write into them
+  rc = cuda_status((int)cudaDeviceSynchronize(), "peer_alloc: sync");
+  if (rc) return rc;
   cudaIpcMemHandle_t h;
   rc = cuda_status((int)cudaIpcGetMemHandle(&h, *ptr), "peer_alloc: cudaIpcGetMemHandle");
   if (rc) return rc;

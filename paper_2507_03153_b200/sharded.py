@@ -228,19 +228,33 @@ class ShardedHybridEngine(HybridEngine):
         """exchange="push": the merge kernel pushes this rank's packed partial
         into every peer's box; the P-way merge waits for the peers' flags on
         the device (see the module docstring)."""
-        push, box, flags = self.xchg.next_step(sparse=self.rank > 0)
+        w = self.push_partial(layer_idx, q, k, v, wts=wts)
+        self.push_merge(out, lse)
+        return out, lse, w
+
+    def push_partial(self, layer_idx, q, k, v, wts=None):
+        """exchange="push", first half of a step: this rank's decode step, whose
+        merge kernel pushes the packed partial into every peer's box (no wait)."""
+        push, self._box, self._flags = self.xchg.next_step(sparse=self.rank > 0)
         self._push = push
         try:
             _, _, w = HybridEngine.decode_device(self, layer_idx, q, k, v, out=self._loc_out, lse=self._loc_lse,
                                                  wts=wts)
         finally:
             self._push = None
-        _lib.call("hgca_merge_packed_wait", box, self.world, self.rows, self.D, self.stride, flags,
+        return w
+
+    def push_merge(self, out, lse):
+        """Second half: wait on the device for every peer's flag of this step,
+        then the P-way merge. Ranks sharing one process (tests) enqueue every
+        rank's push_partial before any push_merge, so no spinning wait sits on
+        the GPU while the host still launches a peer's step."""
+        _lib.call("hgca_merge_packed_wait", self._box, self.world, self.rows, self.D, self.stride, self._flags,
                   self.xchg.epoch, self.xchg.timeout_ms, self.xchg.err.data_ptr(), out.data_ptr(), lse.data_ptr(),
                   self._stream())
         self.launches += 2  # wait + merge
         self.collectives += 1
-        return out, lse, w
+        return out, lse
 
     def check_exchange(self):
         """Raise if a push-exchange wait timed out (host sync)."""

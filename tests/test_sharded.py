@@ -239,10 +239,13 @@ def test_gpu_push_exchange_matches_allgather(cuda, world, dtype):
         kk = torch.randn((B, Hkv, 1, d), generator=g, device="cuda").to(tdt)
         vv = torch.randn((B, Hkv, 1, d), generator=g, device="cuda").to(tdt)
         main = torch.cuda.current_stream()
-        for r, e in enumerate(push):
+        for r, e in enumerate(push):  # every rank's partial (and push) first ...
             streams[r].wait_stream(main)
             with torch.cuda.stream(streams[r]):
-                e.decode_device(0, qq, kk, vv, out=outs[r][0], lse=outs[r][1])
+                e.push_partial(0, qq, kk, vv)
+        for r, e in enumerate(push):  # ... then the flag-waiting merges
+            with torch.cuda.stream(streams[r]):
+                e.push_merge(outs[r][0], outs[r][1])
         for s_ in streams:
             main.wait_stream(s_)
         for e in ref:
