@@ -89,3 +89,10 @@ def cuda():
     import paper_2507_03153_b200 as pkg
     pkg._lib.load()
     return pkg
+
+
+def pytest_collection_modifyitems(config, items):
+    """HGCA_TEST_REVERSE=1 runs the collected tests in reverse order (a check
+    that no test depends on state an earlier test left behind)."""
+    if os.environ.get("HGCA_TEST_REVERSE"):
+        items.reverse()
