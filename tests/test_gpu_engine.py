@@ -119,6 +119,38 @@ def test_engine_soak_vs_oracle(cuda, dtype):
                 np.testing.assert_array_equal(ctx[b * 8 + h], o.context[h])
 
 
+def test_engine_append_events_soak_bf16(cuda):
+    """bf16, G = 4, D = 128: 16-query appends every 150 steps (the tcgen05 append
+    passes: MAW re-evaluation and re-selection) interleaved with decode steps,
+    every step's output against the oracle."""
+    B, Hq, Hkv, d = 2, 8, 2, 128
+    rng = np.random.default_rng(12)
+    bn, bs, prefill, steps_n, nq = 4, 16, 24, 900, 16
+    total = prefill + steps_n + (steps_n // 150) * nq + nq
+    eng = make_engine(cuda, Hq, d, bn, bs, 0.5, 1.0, 64, total, kv_heads=Hkv, batch=B, dtype="bfloat16")
+    oracles = [port.OracleEngine(Hq, d, bn, bs, 0.5, 1.0, core_count=64, batch=B, max_len=total) for _ in range(B)]
+    worst, appends = 0.0, 0
+    for t in range(-1, steps_n):
+        if t < 0:
+            mode, n = "append", prefill
+        elif t % 150 == 149:
+            mode, n = "append", nq
+            appends += 1
+        else:
+            mode, n = "decode", 1
+        q = port.bf16_round(rng.standard_normal((B, Hq, n, d)).astype(np.float32))
+        k = port.bf16_round(rng.standard_normal((B, Hkv, n, d)).astype(np.float32))
+        v = port.bf16_round(rng.standard_normal((B, Hkv, n, d)).astype(np.float32))
+        r = eng.step(0, cuda.StepInput(mode, q, k, v))
+        got = r.output.cpu().numpy()
+        for b in range(B):
+            o = oracles[b].step(mode, q[b], port.expand_gqa(k[b], Hq), port.expand_gqa(v[b], Hq))
+            for i in range(n):
+                worst = max(worst, rel_err(got[b, :, i], o.output[:, i]))
+    assert appends == steps_n // 150 and eng.layers[0].archive_size > 800
+    assert worst <= REL_BF16, worst
+
+
 def test_engine_gqa_batch_bf16(cuda):
     eng, oracles, worst = _run_batched(cuda, B=2, Hq=32, Hkv=8, d=128, dtype="bfloat16", beta=1.0,
                                        cores=64, steps_n=120, seed=2)
