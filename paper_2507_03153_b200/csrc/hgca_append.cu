@@ -328,10 +328,10 @@ __global__ void __launch_bounds__((AMAXW + 1) * 32, 1) append_attend_kernel(cons
 //           segment), which IS the 128-byte swizzle of an 8-row-aligned box:
 //           stages start at positions rounded down to 8 (the extra keys are
 //           masked), so the tiles are canonical SW128 operands as loaded.
-//   warp 1  one thread issues tcgen05.mma: S = Q K^T (M 128, N 64, K-major
-//           operands) into a double-buffered TMEM tile, then O += P V (V as
-//           the MN-major B operand; P = bf16 hi + lo) into the TMEM
-//           accumulator; tcgen05.commit drives the mbarriers.
+//   warp 1  one thread issues S = Q K^T on tcgen05 (M 128, N 64, K-major
+//           operands) into a double-buffered TMEM tile; warp 6 one thread
+//           issues O += P V (V as the MN-major B operand; P = bf16 hi + lo)
+//           into the TMEM accumulator; tcgen05.commit drives the mbarriers.
 //   warps 2-5  one thread per row (its TMEM lane): tcgen05.ld the S row,
 //           scale + mask, fp32 softmax against a per-row reference max that
 //           is only raised when a score exceeds it by more than 8 (p <= e^8,
