@@ -36,7 +36,7 @@ from . import _lib
 from ._dev import DTYPE_CODE, device, stream_handle
 from .attention import HeadShape
 from .errors import ContractError
-from .sparsifier import group_size, mask_to_lists, ownership_words, topk_mask, words_for
+from .sparsifier import group_size, mask_to_lists, ownership_words, topk_mask
 
 __all__ = ["CacheConfig", "EngineConfig", "StepInput", "StepOutput", "LayerState", "HybridEngine"]
 

@@ -6,7 +6,6 @@ check here is bitwise unless a tolerance is written next to it.
 """
 
 import math
-import os
 
 import numpy as np
 import pytest
