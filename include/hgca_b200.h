@@ -162,8 +162,9 @@ int hgca_maw_update(const float* w, int64_t BH, int64_t nq, int64_t W, int64_t w
 /* Union of the Hq/Hkv query heads' selection masks per (batch, kv-head) as
  * entries u_ent [B*Hkv, T] = position | (query-head mask << 24), grouped by
  * mask value (grouped = 1), in position order (0), or position-class
- * interleaved (2: every aligned group of 8 entries has distinct p & 7, as far
- * as the class counts allow; the bfloat16 decode layout); u_cnt [B*Hkv]; and
+ * interleaved (2: position order, each aligned window of 32 entries permuted
+ * to (rank within class p & 7, class) order so groups of 8 have distinct p & 7
+ * where the window's classes allow; the bfloat16 decode layout); u_cnt [B*Hkv]; and
  * the sparse work items: each list is cut into items of sparse_rows entries
  * followed by tail items of sparse_rows/4 entries covering its last sixth or
  * more (all full items first, then all tail items, so the step ends on small
