@@ -276,10 +276,10 @@ class DecodeBreakdown:
 
 
 # fit_decode over the 18 bf16 round-1 points (profiles/r01_configs_timing.jsonl; C3, C4, C5):
-# t = 24.7 us + bytes / 7.31 TB/s (the marginal rate is read-dominated: the pure-read probe
-# reaches 7.19 TB/s, the copy peak counts reads and writes). Median |error| 5%.
-FIXED_S = 24.7e-6   # per layer-step: launch, pipeline fill, merge tail
-B200_DECODE = DeviceSpec("b200-decode-fit", peak_flops=2.25e15, mem_bw=7.31e12)
+# t = 24.5 us + bytes / 7.35 TB/s (the marginal rate is read-dominated: the pure-read probe
+# reaches 7.19 TB/s, the copy peak counts reads and writes). Median |error| 6%.
+FIXED_S = 24.5e-6   # per layer-step: launch, pipeline fill, merge tail
+B200_DECODE = DeviceSpec("b200-decode-fit", peak_flops=2.25e15, mem_bw=7.35e12)
 
 
 def _decode_bytes(s: DecodeShape, union: float):
