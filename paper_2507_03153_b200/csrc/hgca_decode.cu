@@ -1055,10 +1055,17 @@ __global__ void __launch_bounds__(1024) union_window_classes_kernel(int32_t* u_e
 // tail must hold more work than one full item per warp).
 // item_off [2][BK+1]: row 0 = full-item prefix (row 0 [BK] = number of full
 // items), row 1 = absolute start of each bk's tail items (row 1 [BK] = total).
-constexpr int TAIL_DIV = 6;
+#ifndef HGCA_TAIL_DIV
+#define HGCA_TAIL_DIV 6
+#endif
+#ifndef HGCA_TAIL_SPLIT
+#define HGCA_TAIL_SPLIT 4
+#endif
+constexpr int TAIL_DIV = HGCA_TAIL_DIV;      // the last >= 1/TAIL_DIV of each list is tail items
+constexpr int TAIL_SPLIT = HGCA_TAIL_SPLIT;  // of rows / TAIL_SPLIT entries each
 __device__ __forceinline__ void item_counts(int64_t cnt, int64_t rows, int& nbig, int& nsmall) {
   const int64_t big = (cnt - cnt / TAIL_DIV) / rows * rows;
-  const int64_t small = rows / 4;
+  const int64_t small = rows / TAIL_SPLIT;
   nbig = (int)(big / rows);
   nsmall = (int)((cnt - big + small - 1) / small);
 }
@@ -1110,7 +1117,7 @@ __global__ void item_table_kernel(const int32_t* u_cnt, const int32_t* off, int6
   if (bk >= BK) return;
   int nb = 0, ns = 0;
   item_counts(u_cnt[bk], rows, nb, ns);
-  const int cnt = u_cnt[bk], small = (int)(rows / 4), big = nb * (int)rows;
+  const int cnt = u_cnt[bk], small = (int)(rows / TAIL_SPLIT), big = nb * (int)rows;
   for (int i = threadIdx.x; i < nb; i += blockDim.x)
     tab[off[bk] + i] = make_int4((int)bk, i * (int)rows, (i + 1) * (int)rows, 0);
   for (int i = threadIdx.x; i < ns; i += blockDim.x)
