@@ -241,6 +241,9 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
   }
   double acc_s = 0.0, acc_d = 0.0;
   uint32_t phase = 0;
+  // the mbarrier init and the running stats are visible to every warp before
+  // any of them folds (griddepcontrol.wait is not a CTA barrier)
+  __syncthreads();
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   TL(if (tid == 0) g_tlm[blockIdx.x * 8 + 1] = gtimer();)
   // the decode grid is complete: re-arm its work counter for the next step

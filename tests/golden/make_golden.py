@@ -181,6 +181,102 @@ def perf_model(tk, out):
         json.dump(rec, f, indent=1)
 
 
+C1_BETAS = (0.0, 0.5, 1.0, 2.0)
+C1_CORES = (32, 8)          # g = 1 and g = 4 (padding) at batch 1, 32 heads
+C1_FULL = "c1_b1.0_c32"     # the run whose final MAW is stored in full (the rest: sha256)
+C1_OUT_EVERY, C1_LSE_EVERY = 128, 8
+
+
+def c1_name(beta, cores):
+    return f"c1_b{beta}_c{cores}"
+
+
+def _c1_run(args):
+    """One BASELINE config-1 run of the reference (SURVEY.md §8(d) Config 1):
+    gen_workload(seed=7, steps=3968, prefill_len=128), HeadShape(32, 128),
+    CacheConfig(16, 32, 0.5, beta), core_count `cores`, compiled backend."""
+    src, beta, cores = args
+    sys.path.insert(0, src)
+    os.environ["TIERKV_BACKEND"] = "compiled"
+    import tierkv as tk
+
+    cfg = tk.EngineConfig(layers=1, heads=32, head_dim=128,
+                          cache=tk.CacheConfig(blk_num=16, blk_size=32, alpha=0.5, beta=beta),
+                          core_count=cores)
+    wl = tk.gen_workload(tk.WorkloadSpec(seed=7, steps=3968, prefill_len=128), cfg.head_shape, 1)
+    eng = tk.HybridEngine(cfg)
+    ck_out, outs, ck_lse, lses, ctx_sizes, attended = [], [], [], [], [], []
+    n_steps = len(wl)
+    for i, s in enumerate(wl):
+        r = eng.step(0, tk.StepInput(s.mode, s.q[0], s.keys[0], s.values[0]))
+        last = i == n_steps - 1
+        if i % C1_LSE_EVERY == 0 or last:
+            ck_lse.append(i)
+            lses.append(r.lse[:, -1].copy())
+            ctx_sizes.append(eng.layers[0].store.context.sizes())
+            attended.append([p.size for p in r.store_positions])
+        if i % C1_OUT_EVERY == 0 or last:
+            ck_out.append(i)
+            outs.append(np.ascontiguousarray(r.output[:, -1, :]))
+    st, win = eng.layers[0].store, eng.layers[0].window
+    n = st.archive_size
+    ctx = np.stack([np.isin(np.arange(n), st.context.indices[h]) for h in range(32)])
+    name = c1_name(beta, cores)
+    rec = {f"{name}_out_steps": np.array(ck_out), f"{name}_out": np.stack(outs).astype(np.float32),
+           f"{name}_lse_steps": np.array(ck_lse), f"{name}_lse": np.stack(lses),
+           f"{name}_ctx_sizes": np.array(ctx_sizes, np.int32), f"{name}_attended": np.array(attended, np.int32),
+           f"{name}_ctx_bits": np.packbits(ctx, axis=1), f"{name}_sizes": np.array([win.size, n]),
+           f"{name}_store_maw_sha": np.frombuffer(hashlib.sha256(np.ascontiguousarray(st.maw).tobytes()).digest(), np.uint8),
+           f"{name}_window_maw_sha": np.frombuffer(hashlib.sha256(np.ascontiguousarray(win.maw_matrix()).tobytes()).digest(), np.uint8)}
+    if name == C1_FULL:
+        rec[f"{name}_store_maw"] = st.maw
+        rec[f"{name}_window_maw"] = win.maw_matrix()
+    return rec
+
+
+def c1(src, out):
+    """BASELINE config 1 at full size, every beta x {g=1, g=4}: outputs every 128
+    steps, lse / context sizes / attended counts every 8 steps, the final context
+    bitmasks and MAW (sha256; full arrays for one run). 8 processes."""
+    import multiprocessing as mp
+
+    jobs = [(src, b, c) for b in C1_BETAS for c in C1_CORES]
+    with mp.get_context("spawn").Pool(min(len(jobs), os.cpu_count() or 1)) as pool:
+        recs = pool.map(_c1_run, jobs)
+    rec = {}
+    for r in recs:
+        rec.update(r)
+    np.savez_compressed(out, **rec)
+
+
+HARNESS_CASES = {
+    # name: (layers, heads, head_dim, blk_num, blk_size, alpha, beta, core_count, spec kwargs)
+    "h1": (1, 4, 64, 4, 16, 0.5, 1.0, 8, dict(seed=5, steps=300, prefill_len=16,
+                                              append_events=((150, 8),))),
+    "h2": (2, 4, 32, 3, 8, 0.7, 0.5, 2, dict(seed=6, steps=200, prefill_len=8, heavy_hitter_boost=0.6,
+                                             append_events=((90, 4),))),
+}
+
+
+def harness(tk, out):
+    """tierkv.harness.run_experiment (harness.py:123-192) per-head metric rows
+    and summary: pins accuracy.step_metrics and the harness restatement."""
+    from tierkv.harness import run_experiment
+
+    rec = {}
+    for name, (L, H, d, bn, bs, alpha, beta, cores, spec_kw) in HARNESS_CASES.items():
+        cfg = tk.EngineConfig(layers=L, heads=H, head_dim=d,
+                              cache=tk.CacheConfig(blk_num=bn, blk_size=bs, alpha=alpha, beta=beta),
+                              core_count=cores)
+        wl = tk.gen_workload(tk.WorkloadSpec(**spec_kw), cfg.head_shape, cfg.layers)
+        rep = run_experiment(cfg, tk.PerfConfig(), wl)
+        rows = np.array([[float(x) for x in r] for r in rep.per_head_rows], np.float64)
+        rec[f"{name}_rows"] = rows
+        rec[f"{name}_summary_keys"] = np.array(list(rep.summary.keys()))
+        rec[f"{name}_summary"] = np.array([float(v) for v in rep.summary.values()])
+    np.savez_compressed(out, **rec)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref-src", default="/tmp/refbuild/pkg/src")
@@ -199,12 +295,20 @@ def main():
     if args.only == "perf_model":
         perf_model(tk, os.path.join(HERE, "perf_model.json"))
         return
+    if args.only == "c1":
+        c1(src, os.path.join(HERE, "c1.npz"))
+        return
+    if args.only == "harness":
+        harness(tk, os.path.join(HERE, "harness.npz"))
+        return
     workload_file(tk, os.path.join(HERE, "workload_small.tkv"))
     perf_model(tk, os.path.join(HERE, "perf_model.json"))
     kernels(tk, os.path.join(HERE, "kernels.npz"))
     selection(tk, os.path.join(HERE, "selection.npz"))
     engine(tk, os.path.join(HERE, "engine.npz"))
     workload(tk, os.path.join(HERE, "workload.npz"))
+    harness(tk, os.path.join(HERE, "harness.npz"))
+    c1(src, os.path.join(HERE, "c1.npz"))
     for f in sorted(glob.glob(os.path.join(HERE, "*.npz"))):
         print(f, os.path.getsize(f))
 

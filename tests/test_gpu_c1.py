@@ -1,0 +1,114 @@
+"""GPU parity at BASELINE config 1 (SURVEY.md §8(d) Config 1), full size.
+
+The reference's own CPU-runnable case: gen_workload(seed=7, steps=3968,
+prefill_len=128) (workload.py:124-182), HeadShape(32, 128),
+CacheConfig(blk_num=16, blk_size=32, alpha=0.5, beta), every beta in
+{0, 0.5, 1, 2}, core_count 32 (g = 1) and 8 (g = 4, padding). Key norms grow
+with position, so this is the regime where fp32 accumulation
+of q.k fails and bit-exact selection depends on bit-exact fp64 MAW.
+
+Goldens (tests/golden/c1.npz) are outputs of the reference itself
+(make_golden.py --only c1, compiled backend). Checked per run:
+  * outputs every 128 steps: per element |a - b| <= 1e-4 |b| + 1e-4 max|b_head|
+    (the north star's 1e-4 relative on the fp32 path);
+  * lse every 8 steps: within 1e-9 relative;
+  * context sizes after every 8th step and the attended store entries
+    (context + padding, store_positions sizes) of every 8th step: exact;
+  * the final context sets: bit-exact; the final store and window MAW:
+    bit-exact (sha256; full arrays for one run).
+"""
+
+import hashlib
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import workload as owl
+
+pytestmark = pytest.mark.gpu
+
+BETAS = (0.0, 0.5, 1.0, 2.0)
+CORES = (32, 8)
+FULL = "c1_b1.0_c32"
+REL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def c1_workload(golden):
+    steps = owl.gen_workload(owl.WorkloadSpec(seed=7, steps=3968, prefill_len=128), 32, 128,
+                             1 / math.sqrt(128), 1)
+    h = hashlib.sha256()
+    for s in steps:
+        h.update(s.q.tobytes())
+        h.update(s.keys.tobytes())
+        h.update(s.values.tobytes())
+    assert h.digest() == golden("workload.npz")["c1_sha256"].tobytes(), "C1 workload differs from the reference's"
+    return steps
+
+
+def _popcounts(mask, n):
+    """[rows, words] int32 bitmask -> per-row count of set bits below n."""
+    words = (n + 31) // 32
+    if words == 0:
+        return np.zeros(mask.shape[0], np.int64)
+    m = mask[:, :words].to(torch.int64) & 0xFFFFFFFF
+    rem = n - 32 * (words - 1)
+    if rem < 32:
+        m[:, -1] &= (1 << rem) - 1
+    bits = torch.arange(32, device=mask.device, dtype=torch.int64)
+    return ((m[:, :, None] >> bits) & 1).sum(dim=(1, 2)).cpu().numpy()
+
+
+@pytest.mark.parametrize("cores", CORES)
+@pytest.mark.parametrize("beta", BETAS)
+def test_c1_vs_reference(cuda, golden, c1_workload, beta, cores):
+    g = golden("c1.npz")
+    name = f"c1_b{beta}_c{cores}"
+    cfg = cuda.EngineConfig(layers=1, heads=32, head_dim=128,
+                            cache=cuda.CacheConfig(blk_num=16, blk_size=32, alpha=0.5, beta=beta),
+                            core_count=cores, max_positions=4096)
+    eng = cuda.HybridEngine(cfg)
+    ls = eng.layers[0]
+    out_steps = set(g[f"{name}_out_steps"].tolist())
+    lse_steps = set(g[f"{name}_lse_steps"].tolist())
+    outs, lses, ctx_sizes, attended = {}, {}, [], []
+    for i, s in enumerate(c1_workload):
+        if i in lse_steps:
+            attended.append(_popcounts(ls.sel, ls.lo) if s.mode == "decode" else
+                            np.full(32, ls.lo, np.int64))
+        r = eng.step(0, cuda.StepInput(s.mode, s.q[0], s.keys[0], s.values[0]))
+        if i in lse_steps:
+            lses[i] = r.lse[:, -1].cpu().numpy()
+            ctx_sizes.append(_popcounts(ls.ctx, ls.lo))
+        if i in out_steps:
+            outs[i] = r.output[:, -1, :].cpu().numpy()
+    go, gl = g[f"{name}_out"], g[f"{name}_lse"]
+    worst = 0.0
+    for j, i in enumerate(g[f"{name}_out_steps"]):
+        ref = go[j].astype(np.float64)
+        tol = REL * np.abs(ref) + REL * np.abs(ref).max(axis=1, keepdims=True)
+        err = np.abs(outs[i] - ref)
+        assert (err <= tol).all(), f"step {i}: output error {float((err / tol).max()):.3g} x tolerance"
+        worst = max(worst, float((err / np.maximum(np.abs(ref), 1e-30)).max()))
+    got_l = np.stack([lses[i] for i in g[f"{name}_lse_steps"]])
+    np.testing.assert_allclose(got_l, gl, rtol=1e-9, atol=0)
+    np.testing.assert_array_equal(np.stack(ctx_sizes), g[f"{name}_ctx_sizes"])
+    np.testing.assert_array_equal(np.stack(attended), g[f"{name}_attended"])
+    w_size, n = g[f"{name}_sizes"]
+    assert (ls.window_size, ls.archive_size) == (w_size, n)
+    ctx = np.zeros((32, n), bool)
+    for h, idx in enumerate(eng.context_indices()):
+        ctx[h, idx] = True
+    np.testing.assert_array_equal(np.packbits(ctx, axis=1), g[f"{name}_ctx_bits"])
+    maw = eng.maw_host()
+    store_maw = np.ascontiguousarray(maw[:, :n])
+    window_maw = np.ascontiguousarray(maw[:, n:n + w_size])
+    if name == FULL:
+        np.testing.assert_array_equal(store_maw, g[f"{name}_store_maw"])
+        np.testing.assert_array_equal(window_maw, g[f"{name}_window_maw"])
+    assert hashlib.sha256(store_maw.tobytes()).digest() == g[f"{name}_store_maw_sha"].tobytes(), \
+        "final store MAW differs bitwise"
+    assert hashlib.sha256(window_maw.tobytes()).digest() == g[f"{name}_window_maw_sha"].tobytes(), \
+        "final window MAW differs bitwise"

@@ -177,3 +177,29 @@ def test_c_restatement_equals_reference_core(rng):
         b = port.attend_dense(q, k, v, 0.125, True, kernels="reference")
         for x, y in zip(a, b):
             np.testing.assert_array_equal(x, y)
+
+
+@pytest.mark.parametrize("beta,cores", [(1.0, 8), (0.0, 32)])
+def test_engine_port_matches_reference_c1_prefix(beta, cores, golden):
+    """BASELINE config 1 (32 heads d128, gen_workload seed 7, window 16x32): the
+    first 640 steps of the reference's own run (tests/golden/c1.npz), bitwise --
+    outputs, lse, context sizes and attended (context + padding) counts."""
+    g = golden("c1.npz")
+    name = f"c1_b{beta}_c{cores}"
+    spec = owl.WorkloadSpec(seed=7, steps=3968, prefill_len=128)
+    steps = owl.gen_workload(spec, 32, 128, 1 / math.sqrt(128), 1)[:641]
+    eng = port.OracleEngine(32, 128, 16, 32, 0.5, beta, core_count=cores, batch=1, max_len=4096, threads=4)
+    out_idx = {int(s): j for j, s in enumerate(g[f"{name}_out_steps"])}
+    lse_idx = {int(s): j for j, s in enumerate(g[f"{name}_lse_steps"])}
+    checked = 0
+    for i, s in enumerate(steps):
+        r = eng.step(s.mode, s.q[0], s.keys[0], s.values[0])
+        if i in lse_idx:
+            j = lse_idx[i]
+            np.testing.assert_array_equal(r.lse[:, -1], g[f"{name}_lse"][j])
+            np.testing.assert_array_equal([c.size for c in eng.context], g[f"{name}_ctx_sizes"][j])
+            np.testing.assert_array_equal([e.size for e in r.store_entries], g[f"{name}_attended"][j])
+        if i in out_idx:
+            np.testing.assert_array_equal(r.output[:, -1, :], g[f"{name}_out"][out_idx[i]])
+            checked += 1
+    assert checked == 6 and eng.archive_size > 0
