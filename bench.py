@@ -268,6 +268,8 @@ def run_ours(args, rank, world):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t)
     clocks.stop()
+    if getattr(eng, "xchg", None) is not None:
+        eng.check_exchange()  # a push timeout in the timed or e2e steps poisons (NaN) and raises here
     oh = out_h[: B * Hq * D * 4].view(torch.float32)
     if not np.isfinite(oh.numpy()).all() and not os.environ.get("HGCA_LIB"):  # HGCA_LIB: experimental builds
         raise RuntimeError("non-finite decode output")

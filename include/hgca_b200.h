@@ -12,6 +12,7 @@
  *   hgca_attend_indexed        backends.active.attend_indexed backends.py:8-20, _core.pyx:87-150
  *   hgca_attend_indexed_heads  per-head attend_indexed loop   engine.py:139-148
  *   hgca_attend_gqa            append-mode attend over window / archive  engine.py:127-132, 161-164
+ *   hgca_attend_gqa_indexed    decode a_cpu: per-head attend_indexed over the engine's KV  engine.py:139-148
  *   hgca_append_bf16           the same append step for BF16 storage on the tensor cores (+ row-mean weights)
  *   hgca_merge_states          merge_states                   attention.py:153-188
  *   hgca_select_threshold      select_salient                 sparsifier.py:32-42
@@ -21,6 +22,7 @@
  *   hgca_select_topk           pack_head_groups padding order sparsifier.py:219-226
  *   hgca_write_rows            WindowCache.append_kv          kv_cache.py:122-169
  *   hgca_maw_update            WindowCache.update_maw / StoreTier.reevaluate kv_cache.py:171-187, sparsifier.py:158-177
+ *   hgca_maw_ema               WindowCache.update_maw on fp64 weights   kv_cache.py:171-187
  *   hgca_union_build           (device layout of the context cache for the decode kernel)
  *   hgca_decode_step           HybridEngine._run_step, decode mode engine.py:151-195
  *   hgca_decode_step_host      the same step with host q|k|v in / out|lse back (one call)
@@ -83,6 +85,15 @@ int hgca_attend_indexed_heads(int dtype, const void* q, const void* k, const voi
 int hgca_attend_gqa(int dtype, const void* q, const void* KV, int64_t B, int64_t Hq, int64_t Hkv,
                     int64_t T, int64_t row0, int64_t n, int64_t nq, int64_t d, double scale, void* out,
                     double* lse, void* weights, int64_t wts_ld, void* ws, hgca_stream_t stream);
+/* attend_indexed per query head over the engine's HBM layout (KV [B*Hkv, T, 2, d],
+ * bf16 rows position-rotated): head bh = b*Hq + h attends rows idx[idx_off[bh] ..
+ * + idx_cnt[bh]) of kv head b*Hkv + h/(Hq/Hkv); weights [B*Hq, nq, max_n] in the
+ * output dtype (float32). The decode step's store-tier weight rows a_cpu
+ * (engine.py:139-148) when the engine keeps weights. ws: [B*Hq*nq*max_n] fp64. */
+int hgca_attend_gqa_indexed(int dtype, const void* q, const void* KV, int64_t B, int64_t Hq, int64_t Hkv,
+                            int64_t T, const int64_t* idx, const int64_t* idx_off, const int64_t* idx_cnt,
+                            int64_t max_n, int64_t nq, int64_t d, double scale, void* out, double* lse,
+                            void* weights, void* ws, hgca_stream_t stream);
 
 /* merge_states over `rows` rows of d: outputs in dtype, lse fp64. Optional
  * weight rows (w_a [rows,na], w_b [rows,nb] -> w_out [rows,na+nb]). */
@@ -109,7 +120,8 @@ int hgca_peer_free(void* ptr);
 /* In stream order: wait on the device until flags[i] >= epoch for all i < P
  * (acquire loads at system scope; the peers' merge kernels publish them), then
  * hgca_merge_packed over parts. A wait longer than timeout_ms stores 1 to *err
- * (device int32, optional) and merges what is there instead of hanging. */
+ * (device int32, optional) instead of hanging, and the merge then writes NaN
+ * to out / lse rather than folding stale slots (check *err at a sync point). */
 int hgca_merge_packed_wait(const void* parts, int64_t P, int64_t rows, int64_t d, int64_t stride_bytes,
                            const uint64_t* flags, uint64_t epoch, int64_t timeout_ms, int32_t* err, float* out,
                            double* lse, hgca_stream_t stream);
@@ -159,6 +171,10 @@ int hgca_item_rows(int dtype, int64_t* out2);
  * engine.py:177-191); mode 1 = replace (StoreTier.reevaluate, sparsifier.py:158-177). */
 int hgca_maw_update(const float* w, int64_t BH, int64_t nq, int64_t W, int64_t w_ld, double* maw,
                     int64_t T, int64_t p0, int64_t w_old, double alpha, int mode, hgca_stream_t stream);
+/* WindowCache.update_maw (kv_cache.py:171-187): maw[r, j] = (1 - alpha) * maw[r, j]
+ * + alpha * a[r, j] for j < n, three separately rounded fp64 ops (kv_cache.py:186). */
+int hgca_maw_ema(double* maw, int64_t rows, int64_t ld, int64_t n, const double* a, int64_t lda, double alpha,
+                 hgca_stream_t stream);
 /* Union of the Hq/Hkv query heads' selection masks per (batch, kv-head) as
  * entries u_ent [B*Hkv, T] = position | (query-head mask << 24), grouped by
  * mask value (grouped = 1), in position order (0), or position-class

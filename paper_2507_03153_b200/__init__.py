@@ -10,8 +10,10 @@ include/hgca_b200.h). There is no CPU fallback.
 from .errors import ContractError
 from .attention import AttentionResult, HeadShape, attend, attend_indexed, logsumexp, merge_states
 from .backends import CUDA, install
-from .sparsifier import HeadGroupTask, pack_head_groups, select_salient, select_topk
-from .engine import CacheConfig, EngineConfig, HybridEngine, LayerState, StepInput, StepOutput
+from .kv_cache import CacheConfig, KvBlock, WindowCache, offload
+from .sparsifier import (ContextCache, HeadGroupTask, StoreTier, pack_head_groups, renormalize, select_salient,
+                         select_topk)
+from .engine import EngineConfig, HybridEngine, LayerState, StepInput, StepOutput, run_sequence
 from .sharded import ShardedHybridEngine, packed_stride, shard_owner
 from .workload import Workload, WorkloadSpec, gen_workload_device, load_workload, save_workload
 from . import _lib

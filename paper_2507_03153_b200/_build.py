@@ -17,7 +17,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libhgca_b200.so")
 SOURCES = ["hgca_plugin.cu", "hgca_decode.cu", "hgca_append.cu", "hgca_capi.cu"]
-HEADERS = ["hgca_common.cuh", "hgca_internal.h", "hgca_tc.cuh", "hgca_umma.cuh"]
+HEADERS = ["hgca_common.cuh", "hgca_internal.h", "hgca_tc.cuh", "hgca_umma.cuh", "hgca_host.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

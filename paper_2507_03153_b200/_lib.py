@@ -54,6 +54,7 @@ _SIGS = {
     "hgca_attend_indexed": [I32, P, P, P, P, I64, I64, I64, I64, D, I32, P, P, P, P, P],
     "hgca_attend_indexed_heads": [I32, P, P, P, I64, I64, P, P, P, I64, I64, I64, D, P, P, P, P, P],
     "hgca_attend_gqa": [I32, P, P, I64, I64, I64, I64, I64, I64, I64, I64, D, P, P, P, I64, P, P],
+    "hgca_attend_gqa_indexed": [I32, P, P, I64, I64, I64, I64, P, P, P, I64, I64, I64, D, P, P, P, P, P],
     "hgca_merge_states": [I32, P, P, P, P, I64, I64, P, P, P, P, I64, I64, P, P],
     "hgca_merge_partials": [P, P, I64, I64, I64, P, P, P],
     "hgca_merge_packed": [P, I64, I64, I64, I64, P, P, P],
@@ -72,6 +73,7 @@ _SIGS = {
     "hgca_decode_config": [I32, I64, I64, P],
     "hgca_item_rows": [I32, P],
     "hgca_maw_update": [P, I64, I64, I64, I64, P, I64, I64, I64, D, I32, P],
+    "hgca_maw_ema": [P, I64, I64, I64, P, I64, D, P],
     "hgca_union_build": [P, I64, I64, I64, I64, I64, I64, P, P, P, P, I64, I32, P],
     "hgca_decode_step": [ctypes.POINTER(DecodeDesc), P],
     "hgca_decode_step_host": [ctypes.POINTER(DecodeDesc), P, P, I64, P, P, I64, P],

@@ -28,7 +28,7 @@ __all__ = ["full_attention", "attended_mask", "step_metrics"]
 def full_attention(eng, layer_idx, q, n):
     """fp64 attention of q [B, Hq, 1, D] (storage dtype, on the device) over
     positions [0, n) of the layer -> (out [B*Hq, D] f32, lse [B*Hq] f64,
-    weights [B*Hq, n] f32)."""
+    weights [B*Hq, n] f64)."""
     ls = eng.layers[layer_idx]
     BHq = eng.B * eng.Hq
     if not 0 < n <= ls.nxt:
@@ -41,7 +41,9 @@ def full_attention(eng, layer_idx, q, n):
     _lib.call("hgca_attend_gqa", eng.dcode, q.data_ptr(), ls.KV.data_ptr(), eng.B, eng.Hq, eng.Hkv, eng.T, 0, n, 1,
               eng.D, float(eng.shape.scale), out.data_ptr(), lse.data_ptr(), w.data_ptr(), n, ws.data_ptr(),
               eng._stream())
-    return out[:, 0], lse[:, 0], w[:, 0]
+    # fp64 weights for the mass accounting: ws holds exp(s - m) per key (fp64)
+    e = ws.view(BHq, n)
+    return out[:, 0], lse[:, 0], e / e.sum(dim=1, keepdim=True)
 
 
 def attended_mask(eng, layer_idx, n):
@@ -64,7 +66,7 @@ def step_metrics(eng, layer_idx, out_hybrid, q, mask, n, slack=1e-5):
     (attended_mask taken before the step)."""
     out_f, _, w = full_attention(eng, layer_idx, q, n)
     err = (out_hybrid.double() - out_f.double()).abs()                     # [BHq, D]
-    retained = (w.double() * mask.double()).sum(dim=1)
+    retained = (w * mask.double()).sum(dim=1)
     eps = (1.0 - retained).clamp(min=0.0)
     ls = eng.layers[layer_idx]
     vabs = ls.rows()[:, :n, 1].double().abs().amax(dim=1)                 # [B*Hkv, D]

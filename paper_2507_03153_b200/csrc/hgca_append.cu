@@ -23,6 +23,7 @@
 // Deterministic: fixed partition and fixed fold / summation orders.
 #include "hgca_common.cuh"
 #include "hgca_internal.h"
+#include "hgca_host.h"
 #include "hgca_tc.cuh"
 #include "hgca_umma.cuh"
 
@@ -1520,17 +1521,10 @@ static int launch_append_d(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, i
   const AppendPlan p = append_plan(B, Hq, Hkv, D, nq, lo, hi);
   AppendArgs a{};
   {
-    static const void* cached_base = nullptr;
-    static int64_t cached_rows = -1;
-    static CUtensorMap cached;
     const int64_t rows = B * Hkv * T;
-    if (cached_base != KV || cached_rows != rows) {
-      const int rc = make_tile_map(&cached, KV, rows, D);
-      if (rc) return rc;
-      cached_base = KV;
-      cached_rows = rows;
-    }
-    a.kmap = cached;
+    const int rc = map_cache().get(map_key(10 + (int)D, KV, rows, 2 * D, 0, 0), &a.kmap,
+                                   [&](CUtensorMap* m) { return make_tile_map(m, KV, rows, D); });
+    if (rc) return rc;
   }
   a.q = reinterpret_cast<const __nv_bfloat16*>(q);
   a.B = B; a.Hq = Hq; a.Hkv = Hkv; a.G = Hq / Hkv; a.T = T; a.nq = nq;
@@ -1546,48 +1540,31 @@ static int launch_append_d(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, i
   a.out = out; a.lse = lse;
   a.mean[0] = mean_archive; a.mean_ld[0] = lo;
   a.mean[1] = mean_window; a.mean_ld[1] = hi - lo;
-  static bool attr1 = false, attr2 = false;
-  if (!attr1) {
-    cudaError_t e = cudaFuncSetAttribute(append_attend_kernel<D, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, C1::SMEM);
-    if (e != cudaSuccess) return (int)e;
-    e = cudaFuncSetAttribute(append_attend_kernel<D, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, C2::SMEM);
-    if (e != cudaSuccess) return (int)e;
-    attr1 = attr2 = true;
+  static DevFlags attr1, attr2;
+  {
+    int e = set_smem_dev(append_attend_kernel<D, 1>, C1::SMEM, attr1);
+    if (e) return e;
+    e = set_smem_dev(append_attend_kernel<D, 2>, C2::SMEM, attr2);
+    if (e) return e;
   }
   const int nw = (int)((p.RG + 15) / 16);
   if constexpr (D == 128) {  // pass 1 on tcgen05
     {
-      static const void* kv_base = nullptr;
-      static int64_t kv_rows = -1;
-      static CUtensorMap kv_map;
       const int64_t rows = B * Hkv * T;
-      if (kv_base != KV || kv_rows != rows) {
-        const int rc = make_map2d(&kv_map, KV, rows, 2 * D, 64, T5_KEYS, CU_TENSOR_MAP_SWIZZLE_NONE);
-        if (rc) return rc;
-        kv_base = KV;
-        kv_rows = rows;
-      }
-      a.kvmap5 = kv_map;
+      const int rc5 = map_cache().get(map_key(20, KV, rows, 2 * D, 64, T5_KEYS), &a.kvmap5, [&](CUtensorMap* m) {
+        return make_map2d(m, KV, rows, 2 * D, 64, T5_KEYS, CU_TENSOR_MAP_SWIZZLE_NONE);
+      });
+      if (rc5) return rc5;
       const int rc = make_map2d(&a.qmap5, q, B * Hq * nq, D, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
       if (rc) return rc;
     }
-    static bool attr5 = false;
-    if (!attr5) {
-      const cudaError_t e5 =
-          cudaFuncSetAttribute(append_tc5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Tc5Cfg::SMEM);
-      if (e5 != cudaSuccess) return (int)e5;
-      attr5 = true;
-    }
+    static DevFlags attr5;
+    if (const int e5 = set_smem_dev(append_tc5_kernel, Tc5Cfg::SMEM, attr5)) return e5;
     // row groups of >= 64 rows (the M = 128 tile's cost is per item; tiny groups stay on mma.sync)
     const char* force_mma = getenv("HGCA_APPEND_MMA_SYNC");  // A/B switch: 1 = the mma.sync pass for every group
     const bool tc5 = p.RG >= 64 && !(force_mma && *force_mma && *force_mma != '0');
-    static bool attr52 = false;
-    if (!attr52) {
-      const cudaError_t e52 =
-          cudaFuncSetAttribute(append_tc5x2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Tc5x2Cfg::SMEM);
-      if (e52 != cudaSuccess) return (int)e52;
-      attr52 = true;
-    }
+    static DevFlags attr52;
+    if (const int e52 = set_smem_dev(append_tc5x2_kernel, Tc5x2Cfg::SMEM, attr52)) return e52;
     const bool two_tiles = tc5 && p.RG == 128 && p.n_rg >= 2;  // pairs of 128-row groups share the K|V stream
     if (p.n_items > 0 && two_tiles)
       append_tc5x2_kernel<<<(unsigned)(B * Hkv * ((p.n_rg + 1) / 2) * (p.nch0 + p.nch1)), Tc5x2Cfg::THREADS,
@@ -1610,19 +1587,10 @@ static int launch_append_d(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, i
     if constexpr (D == 128) {
       const char* force_mma = getenv("HGCA_APPEND_MMA_SYNC");
       tc5_mean = p.RG >= 64 && !(force_mma && *force_mma && *force_mma != '0');
-      static bool attr_m = false;
-      if (tc5_mean && !attr_m) {
-        const cudaError_t em =
-            cudaFuncSetAttribute(append_tc5_mean_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Tc5MCfg::SMEM);
-        if (em != cudaSuccess) return (int)em;
-        attr_m = true;
-      }
-      static bool attr_m2 = false;
-      if (tc5_mean && !attr_m2) {
-        const cudaError_t em2 = cudaFuncSetAttribute(append_tc5_mean_x2_kernel,
-                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, Tc5Mx2Cfg::SMEM);
-        if (em2 != cudaSuccess) return (int)em2;
-        attr_m2 = true;
+      static DevFlags attr_m, attr_m2;
+      if (tc5_mean) {
+        if (const int em = set_smem_dev(append_tc5_mean_kernel, Tc5MCfg::SMEM, attr_m)) return em;
+        if (const int em2 = set_smem_dev(append_tc5_mean_x2_kernel, Tc5Mx2Cfg::SMEM, attr_m2)) return em2;
       }
       if (tc5_mean && p.RG == 128 && p.n_rg >= 2)  // pairs of 128-row groups share the K stream
         append_tc5_mean_x2_kernel<<<(unsigned)(B * Hkv * ((p.n_rg + 1) / 2) * (p.nch0 + p.nch1)), Tc5Mx2Cfg::THREADS,

@@ -55,8 +55,13 @@ __global__ void merge_partials_kernel(const float* outs, const double* lses, int
 // parts + p*stride and lse [rows] f64 right after it. Same fold as
 // merge_partials_kernel, in rank order, so every rank computes identical bits.
 __global__ void merge_packed_kernel(const unsigned char* parts, int64_t P, int64_t rows, int64_t d,
-                                    int64_t stride, float* out, double* lse) {
+                                    int64_t stride, float* out, double* lse, const int32_t* err) {
   const int64_t r = blockIdx.x;
+  if (err && *(volatile const int32_t*)err) {  // a peer's partial never arrived: poison, never merge stale data
+    for (int64_t c = threadIdx.x; c < d; c += blockDim.x) out[r * d + c] = __int_as_float(0x7fc00000);
+    if (threadIdx.x == 0) lse[r] = __longlong_as_double(0x7ff8000000000000LL);
+    return;
+  }
   const int64_t lse_off = rows * d * 4;
   auto L = [&](int64_t p) { return reinterpret_cast<const double*>(parts + p * stride + lse_off)[r]; };
   double M = -INFINITY;
@@ -203,6 +208,30 @@ int hgca_attend_gqa(int dtype, const void* q, const void* KV, int64_t B, int64_t
   return cuda_status(launch_attend(dtype, a, B * Hq, S(stream)), "attend_gqa");
 }
 
+int hgca_attend_gqa_indexed(int dtype, const void* q, const void* KV, int64_t B, int64_t Hq, int64_t Hkv,
+                            int64_t T, const int64_t* idx, const int64_t* idx_off, const int64_t* idx_cnt,
+                            int64_t max_n, int64_t nq, int64_t d, double scale, void* out, double* lse,
+                            void* weights, void* ws, hgca_stream_t stream) {
+  if (B < 1 || Hq < 1 || Hkv < 1 || Hq % Hkv || d < 1 || nq < 0 || max_n < 0 || max_n > T)
+    return fail(HGCA_EINVAL, "attend_gqa_indexed: bad shape");
+  if (dtype != HGCA_DTYPE_F32 && dtype != HGCA_DTYPE_BF16)
+    return fail(HGCA_EINVAL, "attend_gqa_indexed: storage dtype must be float32 or bfloat16");
+  if (!q || !KV || !out || !lse || !idx_off || !idx_cnt || (max_n > 0 && (!idx || !ws)))
+    return fail(HGCA_EINVAL, "attend_gqa_indexed: null pointer");
+  const int64_t esz = dtype == HGCA_DTYPE_BF16 ? 2 : 4;
+  AttendArgs a{};
+  a.q = q; a.k = KV; a.v = reinterpret_cast<const unsigned char*>(KV) + d * esz;
+  a.Hq = Hq; a.Hkv = Hkv; a.G = Hq / Hkv;
+  a.nq = nq; a.d = d; a.ld_head = T * 2 * d; a.ld_row = 2 * d; a.row0 = 0; a.n = 0;
+  a.rot = dtype == HGCA_DTYPE_BF16 ? 1 : 0;
+  a.idx = idx; a.idx_off = idx_off; a.idx_cnt = idx_cnt;
+  a.scale = scale;
+  a.out = out; a.lse = lse;
+  a.wts = weights; a.wts_ld = max_n;
+  a.ws = reinterpret_cast<double*>(ws); a.ws_ld = max_n > 0 ? max_n : 1;
+  return cuda_status(launch_attend(dtype, a, B * Hq, S(stream)), "attend_gqa_indexed");
+}
+
 int hgca_merge_states(int dtype, const void* out_a, const double* lse_a, const void* out_b,
                       const double* lse_b, int64_t rows, int64_t d, void* out, double* lse,
                       const void* w_a, const void* w_b, int64_t na, int64_t nb, void* w_out,
@@ -234,7 +263,7 @@ int hgca_merge_packed(const void* parts, int64_t P, int64_t rows, int64_t d, int
     return fail(HGCA_EINVAL, "merge_packed: bad shape");
   if (rows == 0) return HGCA_OK;
   merge_packed_kernel<<<(unsigned)rows, 128, 0, S(stream)>>>(reinterpret_cast<const unsigned char*>(parts), P,
-                                                            rows, d, stride_bytes, out, lse);
+                                                            rows, d, stride_bytes, out, lse, nullptr);
   return cuda_status((int)cudaGetLastError(), "merge_packed");
 }
 
@@ -275,7 +304,13 @@ int hgca_merge_packed_wait(const void* parts, int64_t P, int64_t rows, int64_t d
                                              (unsigned long long)epoch, (long long)timeout_ms * 1000000LL, err);
   const int rc = cuda_status((int)cudaGetLastError(), "merge_packed_wait");
   if (rc) return rc;
-  return hgca_merge_packed(parts, P, rows, d, stride_bytes, out, lse, stream);
+  if (rows < 0 || d < 1 || stride_bytes < rows * d * 4 + rows * 8 || (rows * d * 4) % 8 || stride_bytes % 8)
+    return fail(HGCA_EINVAL, "merge_packed_wait: bad shape");
+  if (rows == 0) return HGCA_OK;
+  // on a timeout the wait kernel raised *err: the merge then writes NaN instead of folding stale slots
+  merge_packed_kernel<<<(unsigned)rows, 128, 0, S(stream)>>>(reinterpret_cast<const unsigned char*>(parts), P,
+                                                            rows, d, stride_bytes, out, lse, err);
+  return cuda_status((int)cudaGetLastError(), "merge_packed_wait");
 }
 
 int hgca_select_threshold(const double* maw, int64_t rows, int64_t ld, int64_t p0, int64_t p1,
@@ -352,6 +387,14 @@ int hgca_maw_update(const float* w, int64_t BH, int64_t nq, int64_t W, int64_t w
   if (!(alpha >= 0.0 && alpha <= 1.0)) return fail(HGCA_EINVAL, "alpha must be in [0, 1], got %g", alpha);
   return cuda_status(launch_maw_update(w, BH, nq, W, w_ld, maw, T, p0, w_old, alpha, mode, S(stream)),
                      "maw_update");
+}
+
+int hgca_maw_ema(double* maw, int64_t rows, int64_t ld, int64_t n, const double* a, int64_t lda, double alpha,
+                 hgca_stream_t stream) {
+  if (rows < 0 || n < 0 || ld < n || lda < n || (rows * n > 0 && (!maw || !a)))
+    return fail(HGCA_EINVAL, "maw_ema: bad shape");
+  if (!(alpha >= 0.0 && alpha <= 1.0)) return fail(HGCA_EINVAL, "alpha must be in [0, 1], got %g", alpha);
+  return cuda_status(launch_maw_ema(maw, rows, ld, n, a, lda, alpha, S(stream)), "maw_ema");
 }
 
 int hgca_union_build(const uint32_t* sel_mask, int64_t B, int64_t Hq, int64_t Hkv, int64_t words,

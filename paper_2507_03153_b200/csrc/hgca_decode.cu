@@ -36,6 +36,7 @@
 #include "hgca_common.cuh"
 #include "hgca_internal.h"
 #include "hgca_tc.cuh"
+#include "hgca_host.h"
 
 #include <cuda.h>
 
@@ -757,6 +758,10 @@ __global__ void __launch_bounds__(F32Cfg<D, G>::NC * 32, 1) decode_f32_kernel(co
   const int W = (int)(a.dhi - a.dlo);
   const int total = (int)(a.n_dense_items + (int64_t)a.item_off[2 * a.B * a.Hkv + 1]);
   const unsigned char* Qg = reinterpret_cast<const unsigned char*>(a.q);
+  TL(unsigned long long* tl = g_tl + ((int64_t)blockIdx.x * C::NC + warp) * TL_SLOTS;
+     unsigned long long tl_wait = 0, tl_score = 0, tl_pv = 0, tl_issue = 0, tl_part = 0, tl_sub = 0, tl_items = 0,
+                        tl_first = 0;
+     if (lane == 0) tl[0] = gtimer(););
   if (lane < C::S) mbar_init(&bar[lane], 1);
   fence_mbar_init();
   __syncwarp();
@@ -802,15 +807,19 @@ __global__ void __launch_bounds__(F32Cfg<D, G>::NC * 32, 1) decode_f32_kernel(co
     pend_ent = sub_entry<G>(pend, a, lane);
   };
 
+  TL(long long ci0 = clock64();)
 #pragma unroll
   for (int s = 0; s < C::S; ++s) issue(s);
+  TL(tl_issue += clock64() - ci0;)
 
   for (int k = 0;; ++k) {
     const int s = k % C::S;
     __syncwarp();
     const StageDesc d = desc[s];
     if (d.item < 0) break;
+    TL(long long c0 = clock64();)
     mbar_wait(&bar[s], (k / C::S) & 1);
+    TL(long long c1 = clock64(); tl_wait += c1 - c0; ++tl_sub; if (!tl_first) tl_first = gtimer();)
     const unsigned char* st = wsm + s * C::STAGE;  // tiles: K[NKC] then V[NKC], rows swizzled
     const int32_t myent = meta[s * SUB + lane];
     const uint32_t qm = (uint32_t)myent >> 24;
@@ -849,6 +858,7 @@ __global__ void __launch_bounds__(F32Cfg<D, G>::NC * 32, 1) decode_f32_kernel(co
       }
     }
     const int64_t b = d.bk / a.Hkv, kvh = d.bk % a.Hkv;
+    TL(long long c2 = clock64(); tl_score += c2 - c1;)
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       if (!((wq >> g) & 1u)) continue;
@@ -900,7 +910,9 @@ __global__ void __launch_bounds__(F32Cfg<D, G>::NC * 32, 1) decode_f32_kernel(co
       }
       __syncwarp();
     }
+    TL(long long c3 = clock64(); tl_pv += c3 - c2;)
     if (d.last) {
+      TL(++tl_items;)
       for (int t = lane; t < G * D; t += 32) a.part_acc[((t / D) * a.m.MI + d.item) * D + t % D] = accs[t];
       if (lane < G) {
         a.part_m[lane * a.m.MI + d.item] = mz[2 * lane];
@@ -908,8 +920,14 @@ __global__ void __launch_bounds__(F32Cfg<D, G>::NC * 32, 1) decode_f32_kernel(co
       }
     }
     __syncwarp();
+    TL(long long c4 = clock64(); tl_part += c4 - c3;)
     issue(s);
+    TL(tl_issue += clock64() - c4;)
   }
+  TL(if (lane == 0) {
+    tl[1] = gtimer(); tl[2] = tl_sub; tl[3] = tl_wait; tl[4] = tl_score; tl[5] = tl_pv; tl[6] = tl_issue;
+    tl[7] = tl_part; tl[8] = tl_first; tl[9] = tl_items; tl[16] = blockIdx.x;
+  })
 }
 
 // -------------------------------------------------------------- union build
@@ -1177,44 +1195,33 @@ static int make_row_map(CUtensorMap* map, const void* base, int64_t rows, int64_
   return r == CUDA_SUCCESS ? 0 : -3001;
 }
 
-template <typename K>
-static int set_smem(K kernel, int bytes, bool& done) {
-  if (done) return 0;
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e != cudaSuccess) return (int)e;
-  done = true;
-  return 0;
+MapCache& map_cache() {
+  static MapCache c;
+  return c;
 }
 
 template <bool BF16, int D, int G>
 static int launch_decode_t(const DecodeArgs& a_in, cudaStream_t s) {
   DecodeArgs a = a_in;
   {
-    // cached per KV buffer: encoding is host work only
-    static const void* cached_base = nullptr;
-    static int64_t cached_rows = -1;
-    static CUtensorMap cached;
+    // encoded once per (device, KV buffer): host work only
     const int64_t rows = a.B * a.Hkv * a.T;
-    if (cached_base != a.KV || cached_rows != rows) {
-      const int rc = make_row_map(&cached, a.KV, rows, D, BF16);
-      if (rc) return rc;
-      cached_base = a.KV;
-      cached_rows = rows;
-    }
-    a.kmap = cached;
+    const int rc = map_cache().get(map_key(BF16 ? 1 : 2, a.KV, rows, 2 * D, 0, 0), &a.kmap,
+                                   [&](CUtensorMap* m) { return make_row_map(m, a.KV, rows, D, BF16); });
+    if (rc) return rc;
   }
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  static bool attr = false;
+  static DevFlags attr;
   if constexpr (BF16) {
     using C = Bf16Cfg<D, G, HGCA_BF16_STAGES, HGCA_BF16_PAIRS>;
-    const int rc = set_smem(decode_bf16_kernel<D, G, HGCA_BF16_STAGES, HGCA_BF16_PAIRS>, C::SMEM, attr);
+    const int rc = set_smem_dev(decode_bf16_kernel<D, G, HGCA_BF16_STAGES, HGCA_BF16_PAIRS>, C::SMEM, attr);
     if (rc) return rc;
     decode_bf16_kernel<D, G, HGCA_BF16_STAGES, HGCA_BF16_PAIRS><<<nsm, C::NW * 32, C::SMEM, s>>>(a);
   } else {
     using C = F32Cfg<D, G>;
-    const int rc = set_smem(decode_f32_kernel<D, G>, C::SMEM, attr);
+    const int rc = set_smem_dev(decode_f32_kernel<D, G>, C::SMEM, attr);
     if (rc) return rc;
     decode_f32_kernel<D, G><<<nsm, C::NC * 32, C::SMEM, s>>>(a);
   }
@@ -1223,9 +1230,9 @@ static int launch_decode_t(const DecodeArgs& a_in, cudaStream_t s) {
   // merge kernel: programmatic dependent launch (its launch overlaps the decode tail)
   cudaLaunchConfig_t cfg = {};
   using SC = typename std::conditional<BF16, float, double>::type;  // dense score type
-  static bool mattr = false;
+  static DevFlags mattr;
   {
-    const int rc = set_smem(decode_merge_kernel<D, G, SC>, MergeCfg<D>::SMEM, mattr);
+    const int rc = set_smem_dev(decode_merge_kernel<D, G, SC>, MergeCfg<D>::SMEM, mattr);
     if (rc) return rc;
   }
   cfg.gridDim = dim3((unsigned)(a.B * a.Hq));

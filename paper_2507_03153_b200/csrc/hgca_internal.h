@@ -125,6 +125,8 @@ int launch_append_bf16(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, int64
                        int64_t nq, double scale, int64_t lo, int64_t hi, float* out, double* lse, float* mean_archive,
                        float* mean_window, void* ws, cudaStream_t s);
 int decode_config(int dtype, int64_t D, int64_t G, int64_t* out);
+int launch_maw_ema(double* maw, int64_t rows, int64_t ld, int64_t n, const double* a, int64_t lda, double alpha,
+                   cudaStream_t s);
 int launch_maw_update(const float* w, int64_t BH, int64_t nq, int64_t W, int64_t w_ld, double* maw,
                       int64_t T, int64_t p0, int64_t w_old, double alpha, int mode, cudaStream_t s);
 

@@ -564,6 +564,29 @@ __global__ void maw_update_kernel(const float* __restrict__ w, int64_t BH, int64
     *mp = a;
 }
 
+// f64 EMA of fp64 weights a [rows, lda] into maw [rows, ld] over [0, n):
+// (1 - alpha) * maw + alpha * a with three separately rounded ops
+// (kv_cache.py:186) -- WindowCache.update_maw.
+__global__ void maw_ema_kernel(double* maw, int64_t rows, int64_t ld, int64_t n, const double* __restrict__ a,
+                               int64_t lda, double one_minus_alpha, double alpha) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < rows * n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / n, j = t % n;
+    double* mp = maw + r * ld + j;
+    *mp = __dadd_rn(__dmul_rn(one_minus_alpha, *mp), __dmul_rn(alpha, a[r * lda + j]));
+  }
+}
+
+int launch_maw_ema(double* maw, int64_t rows, int64_t ld, int64_t n, const double* a, int64_t lda, double alpha,
+                   cudaStream_t s) {
+  const int64_t total = rows * n;
+  if (total == 0) return 0;
+  const int64_t nb = (total + 255) / 256;
+  maw_ema_kernel<<<(unsigned)(nb < 148 * 16 ? nb : 148 * 16), 256, 0, s>>>(maw, rows, ld, n, a, lda, 1.0 - alpha,
+                                                                           alpha);
+  return (int)cudaGetLastError();
+}
+
 int launch_maw_update(const float* w, int64_t BH, int64_t nq, int64_t W, int64_t w_ld, double* maw,
                       int64_t T, int64_t p0, int64_t w_old, double alpha, int mode, cudaStream_t s) {
   const int64_t total = BH * W;

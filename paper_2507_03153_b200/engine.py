@@ -36,9 +36,11 @@ from . import _lib
 from ._dev import DTYPE_CODE, device, stream_handle
 from .attention import HeadShape
 from .errors import ContractError
-from .sparsifier import group_size, mask_to_lists, ownership_words, topk_mask
+from .kv_cache import CacheConfig, KvBlock
+from .sparsifier import HeadGroupTask, group_size, mask_to_lists, ownership_words, topk_mask
 
-__all__ = ["CacheConfig", "EngineConfig", "StepInput", "StepOutput", "LayerState", "HybridEngine"]
+__all__ = ["CacheConfig", "EngineConfig", "StepInput", "StepOutput", "LayerState", "HybridEngine", "WindowView",
+           "StoreView", "run_sequence"]
 
 MODES = ("decode", "append")
 
@@ -49,30 +51,6 @@ def item_rows(dtype: str) -> tuple[int, int]:
     out = (ctypes.c_int64 * 2)()
     _lib.call("hgca_item_rows", DTYPE_CODE[torch.bfloat16 if dtype == "bfloat16" else torch.float32], out)
     return int(out[0]), int(out[1])
-
-
-@dataclass(frozen=True)
-class CacheConfig:
-    """kv_cache.py:26-52."""
-
-    blk_num: int
-    blk_size: int
-    alpha: float = 0.5
-    beta: float = 1.0
-
-    def __post_init__(self):
-        if self.blk_num < 2:
-            raise ContractError(f"blk_num must be >= 2, got {self.blk_num}")
-        if self.blk_size < 1:
-            raise ContractError(f"blk_size must be >= 1, got {self.blk_size}")
-        if not 0.0 <= self.alpha <= 1.0:
-            raise ContractError(f"alpha must be in [0, 1], got {self.alpha}")
-        if self.beta < 0.0:
-            raise ContractError(f"beta must be >= 0, got {self.beta}")
-
-    @property
-    def capacity(self) -> int:
-        return self.blk_num * self.blk_size
 
 
 @dataclass(frozen=True)
@@ -161,22 +139,48 @@ class StepInput:
         return int(self.q.shape[-2])
 
 
-@dataclass
 class StepOutput:
-    """engine.py:61-78 (device tensors). store_positions is computed on demand
-    through HybridEngine.store_entries()."""
+    """engine.py:61-78. Arrays come back in the caller's kind: numpy when the
+    StepInput held numpy arrays (the reference's contract), device tensors
+    otherwise.
 
-    output: torch.Tensor          # [B, Hq, n_q, D] float32 (or [Hq, n_q, D])
-    lse: torch.Tensor             # [B, Hq, n_q] float64
-    a_gpu: torch.Tensor | None    # [B, Hq, n_q, W] float32 when keep_weights
-    a_cpu: list | None            # append mode: per (b, h) archive weights
-    dense_positions: np.ndarray
+      output  [B, Hq, n_q, D] float32 (or [Hq, n_q, D] when batch == 1)
+      lse     [B, Hq, n_q] float64
+      a_gpu   window-tier weights [B, Hq, n_q, W] (append steps, or decode
+              with keep_weights), else None
+      a_cpu   per (b*Hq + h) store-tier weight rows [n_q, n_h] over the
+              attended entries (append: the whole archive; decode: context +
+              padding, keep_weights only), else None
+      dense_positions   window-tier positions attended (int64)
+      store_positions   per (b*Hq + h) attended store positions (int64),
+                        computed on first access from the selection the step
+                        attended
+    """
+
+    __slots__ = ("output", "lse", "a_gpu", "a_cpu", "dense_positions", "_store", "_store_fn")
+
+    def __init__(self, output, lse, a_gpu, a_cpu, dense_positions, store_positions=None, store_fn=None):
+        self.output, self.lse, self.a_gpu, self.a_cpu = output, lse, a_gpu, a_cpu
+        self.dense_positions = dense_positions
+        self._store, self._store_fn = store_positions, store_fn
+
+    @property
+    def store_positions(self):
+        if self._store is None and self._store_fn is not None:
+            self._store = self._store_fn()
+            self._store_fn = None
+        return self._store
+
+
+def _np(x):
+    return x.detach().cpu().numpy() if isinstance(x, torch.Tensor) else x
 
 
 class LayerState:
     """HBM-resident window + store tiers of one layer (see module docstring)."""
 
-    def __init__(self, cfg: EngineConfig, T: int, dev):
+    def __init__(self, cfg: EngineConfig, T: int, dev, layer_id: int = 0):
+        self.cfg, self.layer_id = cfg, layer_id
         B, Hq, Hkv, D = cfg.batch, cfg.heads, cfg.n_kv_heads, cfg.head_dim
         tdt = torch.bfloat16 if cfg.dtype == "bfloat16" else torch.float32
         self.KV = torch.zeros((B * Hkv, T, 2, D), dtype=tdt, device=dev)
@@ -230,6 +234,193 @@ class LayerState:
     def archive_size(self):
         return self.lo
 
+    @property
+    def window(self) -> "WindowView":
+        """The reference's LayerState.window (engine.py:81-84): WindowCache read API."""
+        return WindowView(self)
+
+    @property
+    def store(self) -> "StoreView":
+        """The reference's LayerState.store (engine.py:81-84): StoreTier read API."""
+        return StoreView(self)
+
+
+class WindowView:
+    """WindowCache's read API (kv_cache.py:102-255) over one layer's window
+    tier, positions [lo, nxt) of the engine's HBM buffer. K/V rows are
+    (b*Hkv + kv-head), MAW rows (b*Hq + h); with batch 1 and kv_heads == heads
+    the shapes are the reference's [num_heads, ...]. Mutation goes through
+    HybridEngine.step, which keeps the tiers consistent."""
+
+    def __init__(self, ls: LayerState):
+        self._ls = ls
+        self.layer_id = ls.layer_id
+        self.config = ls.cfg.cache
+
+    @property
+    def shape(self):
+        return self._ls.cfg.head_shape
+
+    @property
+    def capacity(self) -> int:
+        return self.config.capacity
+
+    @property
+    def size(self) -> int:
+        return self._ls.window_size
+
+    @property
+    def next_position(self) -> int:
+        return self._ls.nxt
+
+    @property
+    def blocks(self) -> list:
+        """KvBlocks (float32 device copies) of the window, oldest first."""
+        ls, blk = self._ls, self.config.blk_size
+        rows = ls.rows()
+        out = []
+        for start in range(ls.lo, ls.nxt, blk):
+            occ = min(blk, ls.nxt - start)
+            kv = rows[:, start:start + blk].float()
+            if kv.shape[1] < blk:
+                kv = torch.cat([kv, kv.new_zeros((kv.shape[0], blk - kv.shape[1]) + tuple(kv.shape[2:]))], dim=1)
+            maw = ls.maw[:, start:start + blk]
+            if maw.shape[1] < blk:
+                maw = torch.cat([maw, maw.new_zeros((maw.shape[0], blk - maw.shape[1]))], dim=1)
+            out.append(KvBlock(keys=kv[:, :, 0].contiguous(), values=kv[:, :, 1].contiguous(), maw=maw.clone(),
+                               start=start, occupancy=occ))
+        return out
+
+    def gather(self):
+        """kv_cache.py:223-230: ([rows, size, D], [rows, size, D]) float32 device copies."""
+        ls = self._ls
+        kv = ls.rows()[:, ls.lo:ls.nxt].float()
+        return kv[:, :, 0].contiguous(), kv[:, :, 1].contiguous()
+
+    def maw_matrix(self) -> np.ndarray:
+        ls = self._ls
+        return ls.maw[:, ls.lo:ls.nxt].cpu().numpy()
+
+    def positions(self) -> np.ndarray:
+        return np.arange(self._ls.lo, self._ls.nxt, dtype=np.int64)
+
+    def dump(self) -> str:
+        """kv_cache.py:243-255."""
+        ls, blk = self._ls, self.config.blk_size
+        maw = self.maw_matrix()
+        lines = []
+        for i, start in enumerate(range(ls.lo, ls.nxt, blk)):
+            occ = min(blk, ls.nxt - start)
+            col = start - ls.lo
+            mm = " ".join(f"{m:.6f}" for m in maw[:, col:col + occ].mean(axis=1))
+            lines.append(f"layer={self.layer_id} block={i} pos={start}..{start + occ - 1} "
+                         f"occ={occ}/{blk} maw_mean=[{mm}]")
+        return "\n".join(lines)
+
+
+class ContextView:
+    """ContextCache's read API (sparsifier.py:58-87) over the engine's
+    context-cache bitmask of one layer (rows b*Hq + h)."""
+
+    def __init__(self, ls: LayerState):
+        self._ls = ls
+        self.num_heads = ls.ctx.shape[0]
+        self.head_dim = ls.cfg.head_dim
+
+    @property
+    def indices(self) -> list:
+        return mask_to_lists(self._ls.ctx, self._ls.lo)
+
+    def sizes(self) -> list:
+        ls = self._ls
+        counts = torch.zeros(ls.ctx.shape[0], dtype=torch.int64, device=ls.ctx.device)
+        if ls.lo:
+            _lib.call("hgca_popcount_rows", ls.ctx.data_ptr(), ls.ctx.shape[0], ls.ctx.shape[1], ls.lo,
+                      counts.data_ptr(), stream_handle(ls.ctx.device))
+        return counts.cpu().tolist()
+
+    @property
+    def weights(self) -> list:
+        """Renormalized MAW over each head's context (metadata, sparsifier.py:83-87)."""
+        maw = self._ls.maw[:, : self._ls.lo].cpu().numpy()
+        out = []
+        for r, idx in enumerate(self.indices):
+            sel = maw[r, idx]
+            out.append(sel / sel.sum() if idx.size and sel.sum() > 0.0 else np.zeros(idx.size, np.float64))
+        return out
+
+    def _rows(self, which):
+        ls = self._ls
+        G = ls.cfg.heads // ls.cfg.n_kv_heads
+        rows = ls.rows()
+        out = []
+        for r, idx in enumerate(self.indices):
+            bk = (r // ls.cfg.heads) * ls.cfg.n_kv_heads + (r % ls.cfg.heads) // G
+            out.append(rows[bk, torch.from_numpy(idx).to(rows.device), which].float())
+        return out
+
+    @property
+    def keys(self) -> list:
+        return self._rows(0)
+
+    @property
+    def values(self) -> list:
+        return self._rows(1)
+
+
+class StoreView:
+    """StoreTier's read API (sparsifier.py:105-195) over the engine's archive
+    tier of one layer: positions [0, lo) of the HBM buffer."""
+
+    def __init__(self, ls: LayerState):
+        self._ls = ls
+        self.layer_id = ls.layer_id
+        self.context = ContextView(ls)
+
+    @property
+    def shape(self):
+        return self._ls.cfg.head_shape
+
+    @property
+    def archive_size(self) -> int:
+        return self._ls.lo
+
+    @property
+    def positions(self) -> np.ndarray:
+        return np.arange(self._ls.lo, dtype=np.int64)
+
+    @property
+    def maw(self):
+        """[rows, archive_size] float64 device view."""
+        return self._ls.maw[:, : self._ls.lo]
+
+    @property
+    def keys(self):
+        return self._ls.rows()[:, : self._ls.lo, 0].float()
+
+    @property
+    def values(self):
+        return self._ls.rows()[:, : self._ls.lo, 1].float()
+
+    def context_dump(self, tasks=None) -> str:
+        """sparsifier.py:179-195."""
+        ls = self._ls
+        rows = ls.ctx.shape[0]
+        padded = [set() for _ in range(rows)]
+        if tasks:
+            for task in tasks:
+                for h, entries, pad in zip(task.heads, task.entries, task.padding):
+                    padded[h].update(np.asarray(entries)[np.asarray(pad, bool)].tolist())
+        maw = self.maw.cpu().numpy()
+        idx = self.context.indices
+        lines = []
+        for h in range(rows):
+            selected = set(idx[h].tolist())
+            for i in range(ls.lo):
+                lines.append(f"layer={self.layer_id} head={h} pos={i} maw={maw[h, i]:.6e} "
+                             f"selected={int(i in selected)} padding={int(i in padded[h])}")
+        return "\n".join(lines)
+
 
 class HybridEngine:
     """engine.py:87-195 on the B200, for `layers` layers."""
@@ -250,7 +441,7 @@ class HybridEngine:
         self.tdtype = torch.bfloat16 if c.dtype == "bfloat16" else torch.float32
         self.dcode = DTYPE_CODE[self.tdtype]
         self.g_pad = group_size(c.batch, c.heads, c.core_count)
-        self.layers = [LayerState(c, self.T, self.dev) for _ in range(c.layers)]
+        self.layers = [LayerState(c, self.T, self.dev, i) for i in range(c.layers)]
         # shared per-step scratch (steps run in stream order)
         BHq = self.B * self.Hq
         self.dsc_ld = self.cap + 1
@@ -304,10 +495,10 @@ class HybridEngine:
             need = torch.zeros_like(counts)
             _lib.call("hgca_group_need", counts.data_ptr(), self.B, self.Hq, self.g_pad,
                       need.data_ptr(), s)
-            ls.sel.copy_(ls.ctx)
+            ls.sel = ls.ctx.clone()  # a fresh tensor: a StepOutput may hold the old one
             topk_mask(ls.maw, need, n=n, exclude=ls.ctx, out=ls.sel)
         else:
-            ls.sel.copy_(ls.ctx)
+            ls.sel = ls.ctx.clone()  # a fresh tensor: a StepOutput may hold the old one
         self.launches += 2 + (3 if (self.g_pad > 1 and n) else 0) + (1 if self.config.selection == "topk" and n else 0)
         # fp32 kernel: group union rows by query-head mask (single-head
         # sub-chunks); bf16 kernel: position-class interleaved (conflict-free
@@ -387,10 +578,13 @@ class HybridEngine:
 
     def _decode(self, layer_idx, inp, out=None, lse=None):
         ls = self.layers[layer_idx]
+        to_np = not isinstance(inp.q, torch.Tensor)
         squeeze = inp.q.ndim == 3
         q = self._as_dev(inp.q, self.Hq)
         k = self._as_dev(inp.keys, self.Hkv)
         v = self._as_dev(inp.values, self.Hkv)
+        lo, sel = ls.lo, ls.sel  # the selection this step attends (refreshes replace ls.sel)
+        a_cpu = self._store_weights(ls, q, sel, lo, 1) if (self.config.keep_weights and lo) else None
         o, l, w = self.decode_device(layer_idx, q, k, v, out=out, lse=lse)
         o = o.view(self.B, self.Hq, 1, self.D)
         l = l.view(self.B, self.Hq, 1)
@@ -399,7 +593,43 @@ class HybridEngine:
         if squeeze:
             o, l = o[0], l[0]
             w = w[0] if w is not None else None
-        return StepOutput(o, l, w, None, np.arange(*self._last_dense_range, dtype=np.int64))
+        rows = self.B * self.Hq
+
+        def store_positions():
+            if lo == 0:
+                return [np.zeros(0, np.int64) for _ in range(rows)]
+            return mask_to_lists(sel, lo)
+
+        return self._output(to_np, o, l, w, a_cpu, np.arange(*self._last_dense_range, dtype=np.int64),
+                            store_fn=store_positions)
+
+    @staticmethod
+    def _output(to_np, o, l, w, a_cpu, dense, store=None, store_fn=None):
+        if to_np:
+            o, l, w = _np(o), _np(l), _np(w)
+            a_cpu = [_np(x) for x in a_cpu] if a_cpu is not None else None
+        return StepOutput(o, l, w, a_cpu, dense, store_positions=store, store_fn=store_fn)
+
+    def _store_weights(self, ls, q, sel, lo, nq):
+        """Decode a_cpu (engine.py:139-148, keep_weights only): per query head the
+        softmax weights [nq, n_h] over its attended store entries (context +
+        padding), through hgca_attend_gqa_indexed on the engine's KV."""
+        rows, dev, s = self.B * self.Hq, self.dev, self._stream()
+        idx = torch.empty((rows, lo), dtype=torch.int64, device=dev)
+        cnt = torch.zeros(rows, dtype=torch.int64, device=dev)
+        _lib.call("hgca_mask_to_indices", sel.data_ptr(), None, rows, sel.shape[1], lo, idx.data_ptr(), lo, None,
+                  cnt.data_ptr(), s)
+        off = torch.arange(rows, dtype=torch.int64, device=dev) * lo
+        o = torch.empty((rows, nq, self.D), dtype=torch.float32, device=dev)
+        l = torch.empty((rows, nq), dtype=torch.float64, device=dev)
+        w = torch.zeros((rows, nq, lo), dtype=torch.float32, device=dev)
+        ws = torch.empty(rows * nq * lo, dtype=torch.float64, device=dev)
+        _lib.call("hgca_attend_gqa_indexed", self.dcode, q.data_ptr(), ls.KV.data_ptr(), self.B, self.Hq, self.Hkv,
+                  self.T, idx.data_ptr(), off.data_ptr(), cnt.data_ptr(), lo, nq, self.D, float(self.shape.scale),
+                  o.data_ptr(), l.data_ptr(), w.data_ptr(), ws.data_ptr(), s)
+        self.launches += 2
+        cnt_h = cnt.cpu().tolist()
+        return [w[r, :, : cnt_h[r]] for r in range(rows)]
 
     def decode_device(self, layer_idx, q, k, v, out=None, lse=None, wts=None, out_sparse=None, lse_sparse=None):
         """The decode hot path on device tensors: q [B, Hq, 1, D], k/v
@@ -546,7 +776,7 @@ class HybridEngine:
         W = w_size + nq
         odt = torch.float32
         if self.tdtype == torch.bfloat16 and not self.config.keep_weights and nq <= 128:
-            return self._append_tc(ls, q, nq, squeeze)
+            return self._append_tc(ls, q, nq, squeeze, not isinstance(inp.q, torch.Tensor))
         # sparse partial over the whole archive, with weights (engine.py:127-132)
         s_out = torch.zeros((BHq, nq, self.D), dtype=odt, device=self.dev)
         s_lse = torch.full((BHq, nq), -math.inf, dtype=torch.float64, device=self.dev)
@@ -595,9 +825,16 @@ class HybridEngine:
         ag = a_gpu.view(self.B, self.Hq, nq, W)
         if squeeze:
             o, l, ag = o[0], l[0], ag[0]
-        return StepOutput(o, l, ag, a_cpu, np.arange(lo, nxt + nq, dtype=np.int64))
+        a_list = [a_cpu[r] for r in range(BHq)] if a_cpu is not None else [
+            torch.zeros((nq, 0), dtype=odt, device=self.dev) for _ in range(BHq)]
+        return self._output(not isinstance(inp.q, torch.Tensor), o, l, ag, a_list,
+                            np.arange(lo, nxt + nq, dtype=np.int64), store=self._archive_positions(lo))
 
-    def _append_tc(self, ls, q, nq, squeeze):
+    def _archive_positions(self, lo):
+        """Append-mode store_positions: every head attends the whole archive (engine.py:131)."""
+        return [np.arange(lo, dtype=np.int64) for _ in range(self.B * self.Hq)]
+
+    def _append_tc(self, ls, q, nq, squeeze, to_np=False):
         """Append step for bf16 storage on the tensor cores (hgca_append_bf16):
         archive + window attention, merge_states, and the per-head row-mean
         weights a_cpu / a_gpu feed the reference maintenance directly
@@ -642,7 +879,8 @@ class HybridEngine:
         l = lse.view(self.B, self.Hq, nq)
         if squeeze:
             o, l = o[0], l[0]
-        return StepOutput(o, l, None, None, np.arange(lo, nxt + nq, dtype=np.int64))
+        return self._output(to_np, o, l, None, None, np.arange(lo, nxt + nq, dtype=np.int64),
+                            store=self._archive_positions(lo))
 
     # ------------------------------------------------------------ inspection
     def context_indices(self, layer_idx=0):
@@ -659,3 +897,37 @@ class HybridEngine:
         ls = self.layers[layer_idx]
         return ls.maw[:, : ls.nxt].cpu().numpy()
 
+
+
+def run_sequence(config: EngineConfig, workload, on_step=None, collect: bool = False):
+    """engine.py:198-224: drive every layer through a workload's steps in order.
+
+    `workload` yields steps with `mode` and per-layer q / keys / values stacked
+    as [layers, heads, n_q, head_dim] (tierkv.Workload, workload.Workload).
+    on_step(step_idx, layer_idx, inp, out, layer_state) runs after each layer
+    step; layer_state.window / .store give the reference's read API. Returns
+    (engine, outputs): per step, per layer StepOutputs when collect, else None.
+    When the workload's length is known, max_positions is raised to hold it.
+    """
+    steps = workload.steps if hasattr(workload, "steps") else workload
+    if hasattr(steps, "__len__"):
+        total = sum(int(s.q.shape[2]) for s in steps)
+        if total > config.max_positions:
+            config = config.with_(max_positions=total)
+    engine = HybridEngine(config)
+    outputs = [] if collect else None
+    for step_idx, step in enumerate(steps):
+        if step.q.shape[0] < config.layers:
+            raise ContractError(f"workload exhausted mid-layer at step {step_idx}: "
+                                f"{step.q.shape[0]} layers provided, {config.layers} required")
+        per_layer = [] if collect else None
+        for li in range(config.layers):
+            inp = StepInput(step.mode, step.q[li], step.keys[li], step.values[li])
+            out = engine.step(li, inp)
+            if on_step is not None:
+                on_step(step_idx, li, inp, out, engine.layers[li])
+            if collect:
+                per_layer.append(out)
+        if collect:
+            outputs.append(per_layer)
+    return engine, outputs

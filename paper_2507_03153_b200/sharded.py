@@ -196,6 +196,7 @@ class ShardedHybridEngine(HybridEngine):
         self.decode_device(layer_idx, dev_in[:nq], dev_in[nq:nq + nk], dev_in[nq + nk:], out=out, lse=lse)
         out_host.copy_(dev_out, non_blocking=True)
         torch.cuda.current_stream(self.dev).synchronize()
+        self.check_exchange()  # host sync point: a timed-out push poisoned this result
         return out_host
 
     def decode_device(self, layer_idx, q, k, v, out=None, lse=None, wts=None, out_sparse=None, lse_sparse=None):

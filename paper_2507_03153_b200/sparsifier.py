@@ -18,8 +18,8 @@ from . import _lib
 from ._dev import as_device, device, stream_handle
 from .errors import ContractError
 
-__all__ = ["HeadGroupTask", "select_salient", "select_topk", "pack_head_groups", "group_size",
-           "indices_to_mask", "mask_to_lists", "words_for"]
+__all__ = ["HeadGroupTask", "ContextCache", "StoreTier", "select_salient", "select_topk", "renormalize",
+           "pack_head_groups", "group_size", "indices_to_mask", "mask_to_lists", "words_for"]
 
 
 def words_for(n: int) -> int:
@@ -178,3 +178,130 @@ def pack_head_groups(store, batch: int, core_count: int) -> list:
         tasks.append(HeadGroupTask(heads=heads, entries=[lists[x] for x in heads],
                                    padding=[flags[x] for x in heads]))
     return tasks
+
+
+def renormalize(weights):
+    """sparsifier.py:45-55: weights / sum (float64); ValueError for an empty or
+    all-zero set."""
+    w, is_np = as_device(weights)
+    w = w.to(torch.float64)
+    total = float(w.sum()) if w.numel() else 0.0
+    if w.numel() == 0 or total <= 0.0:
+        raise ValueError("cannot renormalize an empty or all-zero weight set")
+    out = w / total
+    return out.cpu().numpy() if is_np else out
+
+
+class ContextCache:
+    """sparsifier.py:58-87: per-head salient subset of the archive -- sorted
+    archive indices (host int64 arrays, the reference's type), their
+    renormalized MAW (metadata only) and contiguous device copies of the
+    selected keys / values."""
+
+    def __init__(self, num_heads: int, head_dim: int):
+        dev = device()
+        self.num_heads = num_heads
+        self.head_dim = head_dim
+        self.indices = [np.zeros(0, np.int64) for _ in range(num_heads)]
+        self.weights = [np.zeros(0, np.float64) for _ in range(num_heads)]
+        self.keys = [torch.zeros((0, head_dim), dtype=torch.float32, device=dev) for _ in range(num_heads)]
+        self.values = [torch.zeros((0, head_dim), dtype=torch.float32, device=dev) for _ in range(num_heads)]
+
+    def sizes(self) -> list:
+        return [int(idx.size) for idx in self.indices]
+
+    def set_head(self, head: int, idx, archive_keys, archive_values, maw_source):
+        """Replace one head's selection; renormalizes maw_source over idx."""
+        idx = np.sort(np.asarray(idx.cpu() if isinstance(idx, torch.Tensor) else idx, dtype=np.int64))
+        self.indices[head] = idx
+        ti = torch.from_numpy(idx).to(archive_keys.device)
+        self.keys[head] = archive_keys[head].index_select(0, ti).contiguous()
+        self.values[head] = archive_values[head].index_select(0, ti).contiguous()
+        sel = maw_source[head].index_select(0, ti.to(maw_source.device))
+        if idx.size and float(sel.sum()) > 0.0:
+            self.weights[head] = renormalize(sel.cpu().numpy())
+        else:
+            self.weights[head] = np.zeros(idx.size, np.float64)
+
+
+class StoreTier:
+    """sparsifier.py:105-195: per-layer archive of evicted KV blocks (device
+    tensors keys / values [H, N, d] float32, maw [H, N] float64, host
+    positions) plus the context cache. Selection runs on the device
+    (hgca_select_threshold: strict maw > beta / divisor with an IEEE fp64
+    divide)."""
+
+    def __init__(self, shape, layer_id: int = 0):
+        dev = device()
+        self.shape = shape
+        self.layer_id = layer_id
+        h, d = shape.num_heads, shape.head_dim
+        self.keys = torch.zeros((h, 0, d), dtype=torch.float32, device=dev)
+        self.values = torch.zeros((h, 0, d), dtype=torch.float32, device=dev)
+        self.maw = torch.zeros((h, 0), dtype=torch.float64, device=dev)
+        self.positions = np.zeros(0, np.int64)
+        self.context = ContextCache(h, d)
+
+    @property
+    def archive_size(self) -> int:
+        return int(self.positions.size)
+
+    def _picked(self, maw_t, beta, divisor):
+        n = maw_t.shape[1]
+        mask = threshold_mask(maw_t.contiguous(), beta, divisor)
+        return mask_to_lists(mask, n)
+
+    def ingest_evicted(self, blocks, beta: float, window_size: int) -> None:
+        """sparsifier.py:127-156: archive the blocks (eviction order) and admit
+        per head the entries with maw > beta / window_size."""
+        if not blocks:
+            return
+        new_keys = torch.cat([b.keys[:, : b.occupancy] for b in blocks], dim=1)
+        new_values = torch.cat([b.values[:, : b.occupancy] for b in blocks], dim=1)
+        new_maw = torch.cat([b.maw[:, : b.occupancy] for b in blocks], dim=1)
+        new_pos = np.concatenate([b.positions for b in blocks])
+        if self.positions.size and new_pos[0] <= self.positions[-1]:
+            raise ContractError(f"blocks out of eviction order: position {new_pos[0]} after {self.positions[-1]}")
+        if window_size < 1:
+            raise ContractError(f"divisor must be >= 1, got {window_size}")
+        base = self.archive_size
+        self.keys = torch.cat([self.keys, new_keys], dim=1)
+        self.values = torch.cat([self.values, new_values], dim=1)
+        self.maw = torch.cat([self.maw, new_maw], dim=1)
+        self.positions = np.concatenate([self.positions, new_pos])
+        picked = self._picked(new_maw, beta, window_size)
+        for h in range(self.shape.num_heads):
+            if picked[h].size == 0:
+                continue
+            merged = np.concatenate([self.context.indices[h], picked[h] + base])
+            self.context.set_head(h, merged, self.keys, self.values, self.maw)
+
+    def reevaluate(self, a_cpu, beta: float) -> None:
+        """sparsifier.py:158-177: MAW := a_cpu [num_heads, archive_size]; the
+        context becomes the entries passing beta / archive_size."""
+        a, _ = as_device(a_cpu)
+        a = a.to(torch.float64)
+        if tuple(a.shape) != (self.shape.num_heads, self.archive_size):
+            raise ContractError(f"a_cpu shape {tuple(a.shape)} != ({self.shape.num_heads}, {self.archive_size})")
+        if self.archive_size == 0:
+            return
+        self.maw = a.clone().contiguous()
+        picked = self._picked(self.maw, beta, self.archive_size)
+        for h in range(self.shape.num_heads):
+            self.context.set_head(h, picked[h], self.keys, self.values, self.maw)
+
+    def context_dump(self, tasks=None) -> str:
+        """sparsifier.py:179-195: per head, one line per archive entry."""
+        padded = [set() for _ in range(self.shape.num_heads)]
+        if tasks:
+            for task in tasks:
+                for h, entries, pad in zip(task.heads, task.entries, task.padding):
+                    padded[h].update(np.asarray(entries)[np.asarray(pad, bool)].tolist())
+        maw = self.maw.cpu().numpy()
+        lines = []
+        for h in range(self.shape.num_heads):
+            selected = set(self.context.indices[h].tolist())
+            for i in range(self.archive_size):
+                lines.append(f"layer={self.layer_id} head={h} pos={self.positions[i]} maw={maw[h, i]:.6e} "
+                             f"selected={int(i in selected)} padding={int(i in padded[h])}")
+        return "\n".join(lines)

@@ -62,6 +62,11 @@ def reference_attention(q, k, v, scale):
     return out, lse, weights
 
 
+def host(x):
+    """numpy view of a step result (numpy already when the step got numpy inputs)."""
+    return x.detach().cpu().numpy() if hasattr(x, "detach") else np.asarray(x)
+
+
 @pytest.fixture
 def rng():
     return np.random.default_rng(0xC0FFEE)

@@ -253,7 +253,7 @@ HARNESS_CASES = {
     # name: (layers, heads, head_dim, blk_num, blk_size, alpha, beta, core_count, spec kwargs)
     "h1": (1, 4, 64, 4, 16, 0.5, 1.0, 8, dict(seed=5, steps=300, prefill_len=16,
                                               append_events=((150, 8),))),
-    "h2": (2, 4, 32, 3, 8, 0.7, 0.5, 2, dict(seed=6, steps=200, prefill_len=8, heavy_hitter_boost=0.6,
+    "h2": (2, 4, 64, 3, 8, 0.7, 0.5, 2, dict(seed=6, steps=200, prefill_len=8, heavy_hitter_boost=0.6,
                                              append_events=((90, 4),))),
 }
 

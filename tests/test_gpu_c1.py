@@ -27,6 +27,8 @@ import torch
 
 from oracle import workload as owl
 
+from conftest import host  # noqa: E402
+
 pytestmark = pytest.mark.gpu
 
 BETAS = (0.0, 0.5, 1.0, 2.0)
@@ -75,15 +77,15 @@ def test_c1_vs_reference(cuda, golden, c1_workload, beta, cores):
     lse_steps = set(g[f"{name}_lse_steps"].tolist())
     outs, lses, ctx_sizes, attended = {}, {}, [], []
     for i, s in enumerate(c1_workload):
-        if i in lse_steps:
-            attended.append(_popcounts(ls.sel, ls.lo) if s.mode == "decode" else
-                            np.full(32, ls.lo, np.int64))
         r = eng.step(0, cuda.StepInput(s.mode, s.q[0], s.keys[0], s.values[0]))
         if i in lse_steps:
-            lses[i] = r.lse[:, -1].cpu().numpy()
-            ctx_sizes.append(_popcounts(ls.ctx, ls.lo))
+            lses[i] = host(r.lse[:, -1])
+            # the reference's reads: StepOutput.store_positions, store.context.sizes()
+            attended.append([p.size for p in r.store_positions])
+            ctx_sizes.append(ls.store.context.sizes())
+            assert ctx_sizes[-1] == _popcounts(ls.ctx, ls.lo).tolist()
         if i in out_steps:
-            outs[i] = r.output[:, -1, :].cpu().numpy()
+            outs[i] = host(r.output[:, -1, :])
     go, gl = g[f"{name}_out"], g[f"{name}_lse"]
     worst = 0.0
     for j, i in enumerate(g[f"{name}_out_steps"]):

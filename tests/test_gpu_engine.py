@@ -20,6 +20,8 @@ from oracle import port
 from oracle import workload as owl
 from test_oracle import ENGINE_CASES
 
+from conftest import host  # noqa: E402
+
 pytestmark = pytest.mark.gpu
 
 REL_FP32 = 1e-4   # north star: outputs within 1e-4 relative on the fp32 path
@@ -47,8 +49,8 @@ def test_engine_vs_reference_golden(cuda, name, golden):
     outs, lses = [], []
     for s in steps:
         r = eng.step(0, cuda.StepInput(s.mode, s.q[0], s.keys[0], s.values[0]))
-        outs.append(r.output[:, -1, :].cpu().numpy())
-        lses.append(r.lse[:, -1].cpu().numpy())
+        outs.append(host(r.output[:, -1, :]))
+        lses.append(host(r.lse[:, -1]))
     sel = g[f"{name}_steps"]
     go, gl = g[f"{name}_out"], g[f"{name}_lse"]
     worst = max(rel_err(outs[i], go[j]) for j, i in enumerate(sel))
@@ -85,7 +87,7 @@ def _run_batched(cuda, B, Hq, Hkv, d, dtype, beta, cores, steps_n, seed):
         k = rnd(rng.standard_normal((B, Hkv, n, d)).astype(np.float32))
         v = rnd(rng.standard_normal((B, Hkv, n, d)).astype(np.float32))
         r = eng.step(0, cuda.StepInput(mode, q, k, v))
-        got = r.output.cpu().numpy()
+        got = host(r.output)
         for b in range(B):
             o = oracles[b].step(mode, q[b], port.expand_gqa(k[b], Hq), port.expand_gqa(v[b], Hq))
             worst = max(worst, rel_err(got[b, :, -1], o.output[:, -1]))
@@ -142,7 +144,7 @@ def test_engine_append_events_soak_bf16(cuda):
         k = port.bf16_round(rng.standard_normal((B, Hkv, n, d)).astype(np.float32))
         v = port.bf16_round(rng.standard_normal((B, Hkv, n, d)).astype(np.float32))
         r = eng.step(0, cuda.StepInput(mode, q, k, v))
-        got = r.output.cpu().numpy()
+        got = host(r.output)
         for b in range(B):
             o = oracles[b].step(mode, q[b], port.expand_gqa(k[b], Hq), port.expand_gqa(v[b], Hq))
             for i in range(n):
@@ -179,8 +181,8 @@ def test_engine_empty_store_equals_dense(cuda, rng):
         hv.append(v)
         r = eng.step(0, cuda.StepInput("decode", q, k, v))
         dense = cuda.attend(q, np.concatenate(hk, 1), np.concatenate(hv, 1), cuda.HeadShape(4, 64))
-        np.testing.assert_allclose(r.output.cpu().numpy(), dense.output, rtol=0, atol=2e-6)
-        np.testing.assert_allclose(r.lse.cpu().numpy(), dense.lse, rtol=0, atol=1e-9)
+        np.testing.assert_allclose(host(r.output), dense.output, rtol=0, atol=2e-6)
+        np.testing.assert_allclose(host(r.lse), dense.lse, rtol=0, atol=1e-9)
     assert eng.layers[0].archive_size == 0
 
 
@@ -240,7 +242,7 @@ def test_engine_long_context_vs_oracle(cuda, dtype):
     K = ls.K.float().cpu().numpy()
     V = ls.V.float().cpu().numpy()
     r = eng.step(0, cuda.StepInput("decode", q, kk, vv))
-    got = r.output.cpu().numpy()
+    got = host(r.output)
     qh = q.float().cpu().numpy()
     kn = kk.float().cpu().numpy()
     vn = vv.float().cpu().numpy()
@@ -264,7 +266,7 @@ def test_engine_decode_is_deterministic(cuda):
         q = torch.randn((2, 32, 1, 128), generator=g, device="cuda").to(tdt)
         kk = torch.randn((2, 8, 1, 128), generator=g, device="cuda").to(tdt)
         r = eng.step(0, cuda.StepInput("decode", q, kk, kk))
-        outs.append((r.output.cpu().numpy(), r.lse.cpu().numpy(), eng.maw_host()))
+        outs.append((host(r.output), host(r.lse), eng.maw_host()))
     for a, b in zip(*outs):
         np.testing.assert_array_equal(a, b)
 
@@ -390,7 +392,7 @@ def test_bf16_append_tensor_core_path_matches_reference_path(cuda, nq, Hq, Hkv, 
         lo, nxt = ls.lo, ls.nxt
         r = eng.step(0, cuda.StepInput("append", q, kk, -kk))
         torch.cuda.synchronize()
-        res.append((r.output.cpu().numpy(), r.lse.cpu().numpy(), ls.maw[:, :nxt + nq].cpu().numpy(), lo, nxt))
+        res.append((host(r.output), host(r.lse), ls.maw[:, :nxt + nq].cpu().numpy(), lo, nxt))
     (o1, l1, m1, lo, nxt), (o2, l2, m2, _, _) = res
     assert rel_err(o2, o1) <= 1e-3
     np.testing.assert_allclose(l2, l1, rtol=0, atol=1e-4)

@@ -203,3 +203,33 @@ def test_engine_port_matches_reference_c1_prefix(beta, cores, golden):
             np.testing.assert_array_equal(r.output[:, -1, :], g[f"{name}_out"][out_idx[i]])
             checked += 1
     assert checked == 6 and eng.archive_size > 0
+
+
+HARNESS_CASES = {
+    # (layers, heads, head_dim, blk_num, blk_size, alpha, beta, core_count, spec kwargs) = make_golden.HARNESS_CASES
+    "h1": (1, 4, 64, 4, 16, 0.5, 1.0, 8, dict(seed=5, steps=300, prefill_len=16, append_events=((150, 8),))),
+    "h2": (2, 4, 64, 3, 8, 0.7, 0.5, 2, dict(seed=6, steps=200, prefill_len=8, heavy_hitter_boost=0.6,
+                                             append_events=((90, 4),))),
+}
+
+
+@pytest.mark.parametrize("name", sorted(HARNESS_CASES))
+def test_harness_restatement_matches_reference(name, golden):
+    """oracle/harness.py over the oracle port reproduces tierkv.harness.run_experiment's
+    per-head metric rows and summary (tests/golden/harness.npz) bitwise."""
+    from oracle import harness as oh
+
+    g = golden("harness.npz")
+    L, H, d, bn, bs, alpha, beta, cores, spec_kw = HARNESS_CASES[name]
+    steps = owl.gen_workload(owl.WorkloadSpec(**spec_kw), H, d, 1 / math.sqrt(d), L)
+    total = sum(s.n_q for s in steps)
+    engines = [port.OracleEngine(H, d, bn, bs, alpha, beta, core_count=cores, batch=1, max_len=total)
+               for _ in range(L)]
+    probe = oh.MetricsProbe(L, H, d, total, 1 / math.sqrt(d))
+    oh.run_port_sequence(engines, steps, probe.on_step)
+    np.testing.assert_array_equal(np.array(probe.rows, np.float64), g[f"{name}_rows"])
+    summ = probe.summary()
+    ref = dict(zip(g[f"{name}_summary_keys"].tolist(), g[f"{name}_summary"].tolist()))
+    assert set(summ) == set(ref)
+    for k, v in summ.items():
+        assert float(v) == ref[k], (k, v, ref[k])
