@@ -1,23 +1,37 @@
 #!/usr/bin/env python
 """Hybrid decode-attention benchmark (BASELINE.json metric).
 
-Workload (N=1): BASELINE.json configs[1] = "C2": Llama-3-8B GQA shape
-(32 query / 8 KV heads, d=128), batch 16, 32K context, bf16, one attention
-layer; 512-token dense window (16 blocks x 32) + per-head threshold-selected
-context over the 32,256-entry archive with ~10% of entries per query head
-selected (SURVEY.md §8(d) Config 2). A "step" is one decode layer-step of the
-whole batch through the device engine: kv_in write, fused dense + sparse
-partial kernel, merge + MAW EMA kernel, and (every 32 steps) eviction ->
-ingest -> union rebuild. tokens/s = batch / step time.
+Workload (the line's `config`): BASELINE.json configs[2] = "C3", the north
+star's target: Llama-3-8B GQA shape (32 query / 8 KV heads, d=128), batch 4,
+128K context, bf16, one attention layer; 512-token dense window (16 blocks x
+32) + per-head threshold-selected context over the 130,560-entry archive with
+~10% of entries per query head selected (SURVEY.md §8(d) Config 3). At N > 1
+the KV sequence is sharded over the ranks (block-cyclic archive, one exchange
+of packed (out, lse) partials per step: the one-shot NVLink push fused into
+the merge kernel, or the NCCL all-gather) -- strong scaling of the same job.
+A second object ("c2") repeats the measurement at N = 1 on configs[1] = C2
+(batch 16, 32K context).
+
+A "step" is one decode layer-step of the whole batch through the device
+engine: kv_in write, fused dense + sparse partial kernel, merge + MAW EMA
+kernel, and (every 32 steps) eviction -> ingest -> union rebuild; the staged
+window is placed so that at least one eviction falls inside the timed steps.
+tokens/s = batch / step time.
 
 value : inputs resident in HBM, CUDA events on the launching stream.
-e2e   : the same step through HybridEngine.decode_host (C ABI) with pinned HOST
-        q/k/v copied in and out/lse copied back + synchronized every step.
+e2e   : the same step through HybridEngine.decode_host_packed (C ABI) with a
+        pinned HOST q|k|v buffer copied in and out|lse copied back +
+        synchronized every step.
+roofline.achieved : SURVEY.md §8(d) algorithmic bytes of the step (dense
+        window K|V + unique selected archive K|V rows + their 4-byte index
+        entries + q + out + lse + window MAW read/write) / the CUDA-event time
+        of the step's decode + merge kernels. Partials and dense scores the
+        kernels write and re-read are reported as overhead, not counted.
 L2    : K/V (2.1 GB) >> L2 (126 MB): inputs larger than L2, no flush needed.
 
 --impl reference: the reference's own CPU hot path (oracle/_ref compiled from
-the reference's _core.pyx, else the oracle's C restatement) on every host
-core, same workload/metric (bench arm for the driver's ratio).
+the reference's _core.pyx, else the oracle's C restatement) on the host
+cores, same workload / metric (the driver's reference arm).
 """
 
 from __future__ import annotations
@@ -36,8 +50,24 @@ sys.path.insert(0, ROOT)
 
 C2 = dict(batch=16, heads=32, kv_heads=8, head_dim=128, context=32768, blk_num=16, blk_size=32,
           beta=1.0, alpha=0.5, frac=0.10, dtype="bfloat16")
-WORKLOAD = ("C2: Llama-3-8B GQA 32q/8kv d128, batch 16, 32K context, bf16, 512-token dense window "
-            "+ threshold-selected 10%/head archive context, 1 layer")
+C3 = dict(C2, batch=4, context=131072)
+WORKLOADS = {
+    "C3": ("C3: Llama-3-8B GQA 32q/8kv d128, batch 4, 128K context, bf16, 512-token dense window "
+           "+ threshold-selected 10%/head archive context, 1 layer"),
+    "C2": ("C2: Llama-3-8B GQA 32q/8kv d128, batch 16, 32K context, bf16, 512-token dense window "
+           "+ threshold-selected 10%/head archive context, 1 layer"),
+}
+METRIC = "hybrid-attn decode tokens/s (1 layer, C3: Llama-3-8B GQA, batch 4, 128K context)"
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def parse():
@@ -47,11 +77,12 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c2", action="store_true", help="skip the secondary C2 measurement at N = 1")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--shard", default="seq", choices=["seq", "batch"],
-                    help="N>1: 'seq' shards the KV sequence of the C2 batch over the ranks (one NCCL "
-                         "all-gather of (out, lse) partials per step; strong scaling, the north star's "
-                         "mode); 'batch' runs one independent C2 batch per rank (weak scaling)")
+                    help="N>1: 'seq' shards the KV sequence of the C3 batch over the ranks (one exchange of "
+                         "(out, lse) partials per step; strong scaling, the north star's mode); 'batch' runs "
+                         "one independent C3 batch per rank (weak scaling, the heads/batch comparison point)")
     ap.add_argument("--exchange", default="push", choices=["push", "allgather"],
                     help="--shard seq: 'push' = the merge kernel stores each rank's (out, lse) partial into "
                          "every peer's HBM box over NVLink (CUDA IPC) and the P-way merge waits on device "
@@ -108,12 +139,14 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------- ours
-def stage_engine(hg, torch, cfgd, max_positions, seed=0, sharded=False, layers=1, exchange="allgather"):
-    """Build the engine and stage a 32K context: bulk-ingest the archive with
+def stage_engine(hg, torch, cfgd, max_positions, seed=0, sharded=False, layers=1, exchange="allgather",
+                 window=None):
+    """Build the engine and stage the context: bulk-ingest the archive with
     MAW drawn so that ~frac of entries per query head pass beta/divisor, then
-    decode until the window reaches its steady state. sharded: every rank
-    stages the same sequence (same seed) into a ShardedHybridEngine, which
-    keeps only its own archive blocks selectable."""
+    decode until the window holds `window` entries (default capacity - 1,
+    the step before an eviction). sharded: every rank stages the same
+    sequence (same seed) into a ShardedHybridEngine, which keeps only its own
+    archive blocks selectable."""
     B, Hq, Hkv, D = cfgd["batch"], cfgd["heads"], cfgd["kv_heads"], cfgd["head_dim"]
     cap = cfgd["blk_num"] * cfgd["blk_size"]
     cfg = hg.EngineConfig(layers=layers, heads=Hq, kv_heads=Hkv, head_dim=D, batch=B, dtype=cfgd["dtype"],
@@ -140,7 +173,7 @@ def stage_engine(hg, torch, cfgd, max_positions, seed=0, sharded=False, layers=1
         maw = torch.where(u < cfgd["frac"], thr * (1.0 + u), thr * u)
         eng.bulk_ingest(layer, k, v, maw, divisor)
         del k, v, u, maw
-    for _ in range(cap - 1):
+    for _ in range(cap - 1 if window is None else window):
         q = torch.randn((B, Hq, 1, D), generator=g, device="cuda").to(tdt)
         kk = torch.randn((B, Hkv, 1, D), generator=g, device="cuda").to(tdt)
         for layer in range(layers):
@@ -149,51 +182,37 @@ def stage_engine(hg, torch, cfgd, max_positions, seed=0, sharded=False, layers=1
     return eng, g
 
 
-def partial_bytes(eng, W_avg, U_avg, n_items):
-    """Algorithmic HBM bytes of one decode kernel launch:
-    dense K|V rows of the window, unique union K|V rows + their 4-byte union
-    entries, the queries, the dense scores (written, re-read by the dense
-    epilogue), the per-item partials (written + re-read by the fold), the MAW
-    of the window (read + written, fp64) and out/lse."""
+def step_bytes(eng, W_avg, U_avg, n_items):
+    """SURVEY.md §8(d) algorithmic HBM bytes of one decode layer-step:
+    dense K|V rows of the window, unique selected archive K|V rows (the
+    per-kv-head union) + their 4-byte index entries, q, out + lse, and the
+    window MAW (fp64, read + written). Also returns the kernels' own overhead
+    traffic (per-item partials and dense scores, written and re-read), which
+    is NOT counted in the roofline."""
     B, Hq, Hkv, D, G = eng.B, eng.Hq, eng.Hkv, eng.D, eng.G
-    e = 2 if eng.tdtype.itemsize == 2 else 4
+    e = eng.tdtype.itemsize
     sc = 4 if e == 2 else 8
     dense = B * Hkv * W_avg * D * 2 * e
-    sparse = U_avg * (D * 2 * e + 4)
+    sparse = U_avg * D * 2 * e
+    idx = U_avg * 4
     q = B * Hq * D * e
-    dsc = B * Hq * W_avg * sc * 2
-    partials = n_items * G * (D * 4 + 16) * 2
-    maw = B * Hq * W_avg * 8 * 2
     out = B * Hq * (D * 4 + 8)
-    return dense + sparse + q + dsc + partials + maw + out, dense, sparse
+    maw = B * Hq * W_avg * 8 * 2
+    overhead = B * Hq * W_avg * sc * 2 + n_items * G * (D * 4 + 16) * 2
+    return dense + sparse + idx + q + out + maw, dense, sparse, overhead
 
 
-def run_ours(args, rank, world):
-    import numpy as np
-    import torch
-
-    import paper_2507_03153_b200 as hg
-
-    local = int(os.environ.get("LOCAL_RANK", 0)) % max(torch.cuda.device_count(), 1)
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist  # noqa: F811
-        backend = os.environ.get("HGCA_DIST_BACKEND", "nccl")  # gloo: multi-rank smoke runs on one GPU
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
-    cfgd = dict(C2)
-    K, Wm = args.steps, args.warmup
-    e2e_steps = args.e2e_steps if args.e2e_steps is not None else min(K, 200)
+def measure(hg, torch, np, cfgd, K, Wm, e2e_steps, rank, world, dist, seq, exchange):
+    """Stage cfgd, time K decode steps (device, CUDA events) and e2e_steps
+    host-buffer steps; returns the raw numbers (max over ranks)."""
     cap = cfgd["blk_num"] * cfgd["blk_size"]
+    blk = cfgd["blk_size"]
+    # place the window so that the middle timed step evicts a block (ingest +
+    # union rebuild inside the timed region): steps j with j = r (mod blk) evict
+    r = (Wm + K // 2) % blk
     max_positions = cfgd["context"] + Wm + K + e2e_steps + 64
-    seq = world > 1 and args.shard == "seq"
-    clocks = ClockSampler(local)
-    clocks.start()
     eng, g = stage_engine(hg, torch, cfgd, max_positions, seed=1234 if seq else 1234 + rank, sharded=seq,
-                          exchange=args.exchange)
+                          exchange=exchange, window=cap - 1 - r)
     B, Hq, Hkv, D = eng.B, eng.Hq, eng.Hkv, eng.D
     tdt = eng.tdtype
     qs = torch.randn((Wm + K, B, Hq, 1, D), generator=g, device="cuda").to(tdt)
@@ -218,6 +237,7 @@ def run_ours(args, rank, world):
             eng.xchg = None
     U0 = int(ls.u_cnt.sum())
     Ws = []
+    lo0 = ls.lo
     eng.step_events = []
     launches0 = eng.launches
     if dist:
@@ -237,9 +257,11 @@ def run_ours(args, rank, world):
     t_wall1 = time.perf_counter()
     if dist:
         dist.barrier()
+    evictions = (ls.lo - lo0) // blk
     launches = eng.launches - launches0
     ms = e0.elapsed_time(e1) / K
-    part_ms = statistics.mean(a.elapsed_time(b) for a, b in eng.step_events)
+    pair = sorted(a.elapsed_time(b) for a, b in eng.step_events)
+    pair_ms = statistics.mean(pair)
     eng.step_events = None
     U1 = int(ls.u_cnt.sum())
     ms_max = ms
@@ -267,41 +289,86 @@ def run_ours(args, rank, world):
         t = torch.tensor([e2e_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t)
-    clocks.stop()
     if getattr(eng, "xchg", None) is not None:
         eng.check_exchange()  # a push timeout in the timed or e2e steps poisons (NaN) and raises here
     oh = out_h[: B * Hq * D * 4].view(torch.float32)
     if not np.isfinite(oh.numpy()).all() and not os.environ.get("HGCA_LIB"):  # HGCA_LIB: experimental builds
         raise RuntimeError("non-finite decode output")
-    # ---- roofline of the dominant kernels: one hgca_decode_step = decode kernel + merge kernel
+    W_avg = statistics.mean(Ws)
+    U_avg = (U0 + U1) / 2
+    BK = eng.B * eng.Hkv
+    n_items = BK * -(-int(W_avg) // 256) + int(ls.item_off[2 * BK + 1])
+    sbytes, dense_b, sparse_b, overhead_b = step_bytes(eng, W_avg, U_avg, n_items)
+    res = dict(B=B, Hq=Hq, Hkv=Hkv, D=D, ms=ms_max, pair_ms=pair_ms, pair_p50=pair[len(pair) // 2],
+               e2e_ms=e2e_ms, launches=launches, evictions=evictions, bytes=sbytes, dense=dense_b,
+               sparse=sparse_b, overhead=overhead_b, W_avg=W_avg, U_avg=U_avg, t_wall=(t_wall0, t_wall1),
+               h2d=int(in_h.numel() * in_h.element_size()), d2h=int(out_h.numel()), exchange_note=exchange_note,
+               xchg=getattr(eng, "xchg", None) is not None)
+    del eng
+    torch.cuda.empty_cache()
+    return res
+
+
+def run_ours(args, rank, world):
+    import numpy as np
+    import torch
+
+    import paper_2507_03153_b200 as hg
+
+    local = int(os.environ.get("LOCAL_RANK", 0)) % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist  # noqa: F811
+        backend = os.environ.get("HGCA_DIST_BACKEND", "nccl")  # gloo: multi-rank smoke runs on one GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    K, Wm = args.steps, args.warmup
+    e2e_steps = args.e2e_steps if args.e2e_steps is not None else min(K, 200)
+    seq = world > 1 and args.shard == "seq"
+    clocks = ClockSampler(local)
+    clocks.start()
+    m = measure(hg, torch, np, C3, K, Wm, e2e_steps, rank, world, dist, seq, args.exchange)
+    c2 = None
+    if world == 1 and not args.no_c2:
+        c2 = measure(hg, torch, np, C2, min(K, 200), Wm, min(e2e_steps, 100), rank, world, dist, False,
+                     args.exchange)
+    clocks.stop()
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak = peaks.get("hbm_gbs", 6650.0)
     tpath = os.path.join(ROOT, "profiles", "traffic.json")  # dram bytes per launch from the ncu --set full captures
     traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
-    W_avg = statistics.mean(Ws)
-    U_avg = (U0 + U1) / 2
-    BK = eng.B * eng.Hkv
-    n_items = BK + int(ls.item_off[2 * BK + 1])  # dense items + sparse items of the current selection
-    pbytes, dense_b, sparse_b = partial_bytes(eng, W_avg, U_avg, n_items)
-    achieved = pbytes / (part_ms * 1e-3) / 1e9
     result = None
     if rank == 0:
+        B = m["B"]
         units = B if seq else world * B  # tokens the whole job decodes per step
-        tok_s = units / (ms_max * 1e-3)
+        tok_s = units / (m["ms"] * 1e-3)
+        achieved = m["bytes"] / (m["pair_ms"] * 1e-3) / 1e9
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             from oracle import cpu_bench  # checker / baseline only
-            cpu = cpu_bench.time_single(Hq, Hkv, D, cfgd["context"] - cap, cap, cfgd["frac"],
-                                        sequences=8, reps=30)  # ~10 s of single-thread CPU work
+            cap = C3["blk_num"] * C3["blk_size"]
+            cpu = cpu_bench.time_single(C3["heads"], C3["kv_heads"], C3["head_dim"], C3["context"] - cap, cap,
+                                        C3["frac"], sequences=2, reps=20)  # ~10-20 s of single-thread CPU work
+            cpu["cpu_model"] = cpu_model()
+        par = ("1 GPU" if world == 1 else
+               f"KV-sequence sharded x{world} (block-cyclic archive; "
+               + ("one-shot push of packed (out, lse) partials from the merge kernel into the peers' HBM "
+                  "(CUDA IPC / NVLink) + flag-waiting P-way merge" if m["xchg"] else
+                  ((m["exchange_note"] + "; ") if m["exchange_note"] else "")
+                  + "NCCL all-gather of packed (out, lse) partials + P-way merge") + ")"
+               if seq else f"batch replicas x{world} (one C3 batch per GPU, no collective)")
         result = {
-            "metric": "hybrid-attn decode tokens/s (1 layer, C2)",
+            "metric": METRIC,
             "value": round(tok_s, 1),
             "unit": "tokens/s",
             "n_gpus": world,
             "steps": K,
             "warmup": Wm,
-            "ms_per_step": round(ms_max, 5),
+            "ms_per_step": round(m["ms"], 5),
             "higher_is_better": True,
             "scaling": "strong" if seq else "weak",
             "vs_baseline": None,
@@ -309,41 +376,45 @@ def run_ours(args, rank, world):
             "numerics": "bf16 storage; QK^T and P.V on mma.sync (fp32 accumulate, P as bf16 hi+lo), "
                         "fp32 softmax, fp64 MAW/merge",
             "data": "synthetic (torch.randn K/V/q, MAW drawn for 10% threshold selection per query head)",
-            "config": {"workload": WORKLOAD, "batch": B, "q_heads": Hq, "kv_heads": Hkv, "head_dim": D,
-                       "context": cfgd["context"], "window_blocks": f"{cfgd['blk_num']}x{cfgd['blk_size']}",
-                       "selected_frac": cfgd["frac"],
-                       "parallelism": ("1 GPU" if world == 1 else
-                                       f"KV-sequence sharded x{world} (block-cyclic archive; "
-                                       + ("one-shot push of packed (out, lse) partials from the merge kernel into "
-                                          "the peers' HBM (CUDA IPC / NVLink) + flag-waiting P-way merge"
-                                          if getattr(eng, "xchg", None) is not None else
-                                          ((exchange_note + "; ") if exchange_note else "") +
-                                          "NCCL all-gather of packed (out, lse) partials + P-way merge") + ")"
-                                       if seq else
-                                       f"batch replicas x{world} (one C2 batch per GPU, no collective)"),
+            "config": {"workload": WORKLOADS["C3"], "batch": B, "q_heads": m["Hq"], "kv_heads": m["Hkv"],
+                       "head_dim": m["D"], "context": C3["context"],
+                       "window_blocks": f"{C3['blk_num']}x{C3['blk_size']}", "selected_frac": C3["frac"],
+                       "parallelism": par, "evictions_in_timed_steps": m["evictions"],
                        "l2": "inputs larger than L2 (K/V 2.1 GB per GPU), no flush"},
-            "hbm_gbs_step": round(pbytes / (ms_max * 1e-3) / 1e9, 1),
+            "hbm_gbs_step": round(m["bytes"] / (m["ms"] * 1e-3) / 1e9, 1),
             "roofline": {"bound": "hbm",
                          "kernel": "hgca::decode_bf16_kernel + hgca::decode_merge_kernel (one hgca_decode_step)",
                          "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
+                         "frac_of_step": round(m["bytes"] / (m["ms"] * 1e-3) / 1e9 / peak, 4),
                          "traffic": traffic.get("decode_step_bytes"),
                          "traffic_source": traffic.get("source"),
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)",
-                         "kernel_ms": round(part_ms, 5), "bytes_per_launch": int(pbytes),
-                         "dense_bytes": int(dense_b), "sparse_unique_bytes": int(sparse_b),
-                         "kernel_share_of_step": round(part_ms / ms, 3)},
-            "e2e": {"value": round(units / (e2e_ms * 1e-3), 1), "unit": "tokens/s",
-                    "ms_per_step": round(e2e_ms, 4), "steps": e2e_steps,
-                    "h2d_bytes_per_step": int(in_h.numel() * in_h.element_size()),
-                    "d2h_bytes_per_step": int(out_h.numel()),
+                         "kernel_ms": round(m["pair_ms"], 5), "kernel_ms_p50": round(m["pair_p50"], 5),
+                         "bytes_per_launch": int(m["bytes"]),
+                         "bytes_definition": "SURVEY.md 8(d): dense window K|V + unique selected archive K|V + "
+                                             "4 B/entry index + q + out/lse + window MAW r/w",
+                         "dense_bytes": int(m["dense"]), "sparse_unique_bytes": int(m["sparse"]),
+                         "overhead_bytes_not_counted": int(m["overhead"]),
+                         "kernel_share_of_step": round(m["pair_ms"] / m["ms"], 3)},
+            "e2e": {"value": round(units / (m["e2e_ms"] * 1e-3), 1), "unit": "tokens/s",
+                    "ms_per_step": round(m["e2e_ms"], 4), "steps": e2e_steps,
+                    "h2d_bytes_per_step": m["h2d"], "d2h_bytes_per_step": m["d2h"],
                     "api": "HybridEngine.decode_host_packed (pinned host q|k|v in, out|lse back, sync)"},
-            "gpu_launches": launches,
-            "clocks": clocks.summary(t_wall0 - 1.0, t_wall1),
+            "gpu_launches": m["launches"],
+            "clocks": clocks.summary(m["t_wall"][0] - 1.0, (c2 or m)["t_wall"][1]),
             "cpu_baseline": cpu,
         }
         if cpu:
             result["cpu_baseline"]["speedup_e2e"] = round(result["e2e"]["value"] / cpu["value"], 1)
+        if c2:
+            a2 = c2["bytes"] / (c2["pair_ms"] * 1e-3) / 1e9
+            result["c2"] = {"workload": WORKLOADS["C2"], "value": round(c2["B"] / (c2["ms"] * 1e-3), 1),
+                            "unit": "tokens/s", "ms_per_step": round(c2["ms"], 5),
+                            "roofline_achieved_gbs": round(a2, 1), "roofline_frac": round(a2 / peak, 4),
+                            "kernel_ms": round(c2["pair_ms"], 5), "bytes_per_launch": int(c2["bytes"]),
+                            "e2e_value": round(c2["B"] / (c2["e2e_ms"] * 1e-3), 1),
+                            "evictions_in_timed_steps": c2["evictions"], "gpu_launches": c2["launches"]}
     if dist:
         dist.destroy_process_group()
     return result
@@ -355,9 +426,9 @@ def run_reference(args, rank, world):
         return None
     from oracle import cpu_bench
 
-    cfgd = dict(C2)
+    cfgd = dict(C3)
     cap = cfgd["blk_num"] * cfgd["blk_size"]
-    steps = max(1, min(args.steps, 40))  # ~3 s of work on the box's host cores
+    steps = max(1, min(args.steps, 20))  # ~10-20 s of work on the box's host cores
     warm = 1
     r = cpu_bench.pool_bench(cfgd["heads"], cfgd["kv_heads"], cfgd["head_dim"], cfgd["context"] - cap, cap,
                              cfgd["frac"], batch=cfgd["batch"], steps=steps, warmup=warm)
@@ -365,16 +436,21 @@ def run_reference(args, rank, world):
     tok = cfgd["batch"] / (ms * 1e-3)
     return {
         "impl": "reference",
-        "metric": "hybrid-attn decode tokens/s (1 layer, C2)",
+        "metric": METRIC,
         "value": round(tok, 3), "unit": "tokens/s", "n_gpus": world, "steps": steps, "warmup": warm,
         "ms_per_step": round(ms, 2), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32",
         "numerics": "fp32 (bf16-rounded values upcast), fp64 accumulation (reference _core)",
-        "data": "synthetic", "config": {"workload": WORKLOAD, "batch": cfgd["batch"]},
+        "data": "synthetic",
+        "config": {"workload": WORKLOADS["C3"], "batch": cfgd["batch"], "q_heads": cfgd["heads"],
+                   "kv_heads": cfgd["kv_heads"], "head_dim": cfgd["head_dim"], "context": cfgd["context"],
+                   "window_blocks": f"{cfgd['blk_num']}x{cfgd['blk_size']}", "selected_frac": cfgd["frac"],
+                   "parallelism": f"host CPU, {r['workers']} processes"},
         "cpu_baseline": {"value": round(tok, 3), "unit": "tokens/s", "cores": r["workers"], "kind": r["kind"],
-                         "sample": f"{steps} step(s) x full batch of {cfgd['batch']} sequences, one process "
-                                   f"per sequence over {r['workers']} host cores (reference is single-threaded "
-                                   f"per engine, engine.py:10-11)"},
+                         "cpu_model": cpu_model(),
+                         "sample": f"{steps} step(s) x full batch of {cfgd['batch']} sequences, each split into "
+                                   f"{r['tasks'] // cfgd['batch']} head-group tasks over {r['workers']} host "
+                                   f"processes (the reference is single-threaded per engine, engine.py:10-11)"},
         "e2e": {"value": round(tok, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 

@@ -23,7 +23,7 @@
  *   hgca_write_rows            WindowCache.append_kv          kv_cache.py:122-169
  *   hgca_maw_update            WindowCache.update_maw / StoreTier.reevaluate kv_cache.py:171-187, sparsifier.py:158-177
  *   hgca_maw_ema               WindowCache.update_maw on fp64 weights   kv_cache.py:171-187
- *   hgca_union_build           (device layout of the context cache for the decode kernel)
+ *   hgca_union_build(_items)   (device layout of the context cache for the decode kernel)
  *   hgca_decode_step           HybridEngine._run_step, decode mode engine.py:151-195
  *   hgca_decode_step_host      the same step with host q|k|v in / out|lse back (one call)
  *   hgca_merge_partials        P-way merge of sharded (out, lse) partials
@@ -180,7 +180,9 @@ int hgca_maw_ema(double* maw, int64_t rows, int64_t ld, int64_t n, const double*
  * mask value (grouped = 1), in position order (0), or position-class
  * interleaved (2: position order, each aligned window of 32 entries permuted
  * to (rank within class p & 7, class) order so groups of 8 have distinct p & 7
- * where the window's classes allow; the bfloat16 decode layout); u_cnt [B*Hkv]; and
+ * where the window's classes allow; the bfloat16 decode layout), or grouped by
+ * mask value and then class-interleaved per window (3: the float32 decode
+ * layout); u_cnt [B*Hkv]; and
  * the sparse work items: each list is cut into items of sparse_rows entries
  * followed by tail items of sparse_rows/4 entries covering its last sixth or
  * more (all full items first, then all tail items, so the step ends on small
@@ -190,6 +192,16 @@ int hgca_maw_ema(double* maw, int64_t rows, int64_t ld, int64_t n, const double*
 int hgca_union_build(const uint32_t* sel_mask, int64_t B, int64_t Hq, int64_t Hkv, int64_t words,
                      int64_t n_arch, int64_t T, int32_t* u_ent, int32_t* u_cnt, int32_t* item_off,
                      int32_t* item_tab, int64_t sparse_rows, int grouped, hgca_stream_t stream);
+/* The same with step-adaptive items: item rows = the largest power-of-two
+ * fraction of max_rows, not below min_rows, that still cuts the whole union
+ * into >= item_target items (chosen on the device from u_cnt and stored at
+ * item_off[2*(B*Hkv+1)]; item_off needs 2*(B*Hkv+1)+1 entries). Big steps keep
+ * long items (few partials), small steps give every decode warp work. Pass
+ * the same item_target in the step descriptor (it sizes the partials check). */
+int hgca_union_build_items(const uint32_t* sel_mask, int64_t B, int64_t Hq, int64_t Hkv, int64_t words,
+                           int64_t n_arch, int64_t T, int32_t* u_ent, int32_t* u_cnt, int32_t* item_off,
+                           int32_t* item_tab, int64_t max_rows, int64_t min_rows, int64_t item_target, int grouped,
+                           hgca_stream_t stream);
 
 typedef struct hgca_decode_desc {
   int32_t dtype;            /* HGCA_DTYPE_F32 or HGCA_DTYPE_BF16 (storage) */
@@ -238,6 +250,7 @@ typedef struct hgca_decode_desc {
   uint64_t* push_flag[8];
   uint64_t epoch;
   uint32_t* push_cnt;
+  int64_t item_target;      /* item_target of hgca_union_build_items (0: fixed sparse_rows items) */
 } hgca_decode_desc;
 
 /* One decode step = two kernels on `stream`: the decode kernel (dense items =

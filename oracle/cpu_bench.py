@@ -46,32 +46,36 @@ def make_sequence(Hq, Hkv, D, n_arch, W, frac, seed):
     return dict(K=K, V=V, q=q, sel=sel, maw=maw, n_arch=n_arch, W=W, Hq=Hq, Hkv=Hkv, D=D)
 
 
-def sequence_step(s, kernels):
-    """One reference hot-path layer-step for one sequence; returns output."""
+def sequence_step(s, kernels, h0=0, h1=None):
+    """One reference hot-path layer-step for one sequence (query heads
+    [h0, h1), default all); returns output."""
     Hq, Hkv, D, n, W = s["Hq"], s["Hkv"], s["D"], s["n_arch"], s["W"]
+    h1 = Hq if h1 is None else h1
     G = Hq // Hkv
     scale = 1.0 / math.sqrt(D)
     K, V, q = s["K"], s["V"], s["q"]
-    s_out = np.zeros((Hq, 1, D), np.float32)
-    s_lse = np.full((Hq, 1), -np.inf)
-    for h in range(Hq):
+    H = h1 - h0
+    s_out = np.zeros((H, 1, D), np.float32)
+    s_lse = np.full((H, 1), -np.inf)
+    for h in range(h0, h1):
         o, l, _ = port.attend_indexed(q[h][None], K[h // G, :n], V[h // G, :n], s["sel"][h], scale, True,
                                       kernels=kernels)
-        s_out[h], s_lse[h] = o, l
-    kw = np.repeat(K[:, n:n + W], G, axis=0)
-    vw = np.repeat(V[:, n:n + W], G, axis=0)
-    d_out, d_lse, a_gpu = port.attend_dense(q[:, None], kw, vw, scale, True, kernels=kernels)
+        s_out[h - h0], s_lse[h - h0] = o, l
+    heads = np.arange(h0, h1) // G
+    kw = np.ascontiguousarray(K[heads, n:n + W])
+    vw = np.ascontiguousarray(V[heads, n:n + W])
+    d_out, d_lse, a_gpu = port.attend_dense(q[h0:h1, None], kw, vw, scale, True, kernels=kernels)
     out, lse = port.merge_states(s_out, s_lse, d_out, d_lse)
     a_mean = a_gpu.mean(axis=1, dtype=np.float64)
-    s["maw"] = 0.5 * s["maw"] + 0.5 * a_mean
+    s["maw"][h0:h1] = 0.5 * s["maw"][h0:h1] + 0.5 * a_mean
     return out
 
 
 def _worker(args):
-    idx, kernels = args
+    idx, kernels, h0, h1 = args
     s = _SHARED["seqs"][idx % len(_SHARED["seqs"])]
     t0 = time.perf_counter()
-    sequence_step(s, kernels)
+    sequence_step(s, kernels, h0, h1)
     return time.perf_counter() - t0
 
 
@@ -92,20 +96,26 @@ def time_single(Hq, Hkv, D, n_arch, W, frac, sequences=2, reps=2, seed=0):
 
 
 def pool_bench(Hq, Hkv, D, n_arch, W, frac, batch, steps, warmup, workers=None, seed=0):
-    """--impl reference: all host cores, one process per sequence slot.
-    Each step runs the full batch (B sequences) across the pool; returns
-    per-step wall times."""
+    """--impl reference: all host cores. Each step runs the full batch: every
+    sequence's layer-step split into per-head-group tasks (the reference's
+    HeadGroupTask unit, sparsifier.py:90-102; each task runs the reference's
+    own per-head loops), spread over a process pool so B * groups >= cores;
+    returns per-step wall times."""
     kernels = kind()
     workers = workers or len(os.sched_getaffinity(0))
-    n_seq = min(batch, workers)
-    _SHARED["seqs"] = [make_sequence(Hq, Hkv, D, n_arch, W, frac, seed + i) for i in range(n_seq)]
+    groups = max(1, min(Hq, -(-workers // batch)))          # head groups per sequence
+    bounds = np.linspace(0, Hq, groups + 1).astype(int)
+    tasks = [(b, kernels, int(bounds[i]), int(bounds[i + 1])) for b in range(batch) for i in range(groups)
+             if bounds[i + 1] > bounds[i]]
+    _SHARED["seqs"] = [make_sequence(Hq, Hkv, D, n_arch, W, frac, seed + i) for i in range(batch)]
     ctx = mp.get_context("fork")
     times = []
-    with ctx.Pool(processes=min(workers, batch)) as pool:
+    procs = min(workers, len(tasks))
+    with ctx.Pool(processes=procs) as pool:
         for it in range(warmup + steps):
             t0 = time.perf_counter()
-            pool.map(_worker, [(b, kernels) for b in range(batch)], chunksize=1)
+            pool.map(_worker, tasks, chunksize=1)
             dt = time.perf_counter() - t0
             if it >= warmup:
                 times.append(dt)
-    return dict(times=times, workers=min(workers, batch), kind=kernels)
+    return dict(times=times, workers=procs, kind=kernels, tasks=len(tasks))

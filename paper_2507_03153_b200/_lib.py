@@ -42,6 +42,7 @@ class DecodeDesc(ctypes.Structure):
         ("out", P), ("lse", P), ("wts_out", P), ("out_sparse", P), ("lse_sparse", P),
         ("push_n", ctypes.c_int32), ("push_sparse", ctypes.c_int32),
         ("push_dst", P * 8), ("push_flag", P * 8), ("epoch", ctypes.c_uint64), ("push_cnt", P),
+        ("item_target", I64),
     ]
 
 
@@ -75,6 +76,7 @@ _SIGS = {
     "hgca_maw_update": [P, I64, I64, I64, I64, P, I64, I64, I64, D, I32, P],
     "hgca_maw_ema": [P, I64, I64, I64, P, I64, D, P],
     "hgca_union_build": [P, I64, I64, I64, I64, I64, I64, P, P, P, P, I64, I32, P],
+    "hgca_union_build_items": [P, I64, I64, I64, I64, I64, I64, P, P, P, P, I64, I64, I64, I32, P],
     "hgca_decode_step": [ctypes.POINTER(DecodeDesc), P],
     "hgca_decode_step_host": [ctypes.POINTER(DecodeDesc), P, P, I64, P, P, I64, P],
     "hgca_append_ws_bytes": [I64, I64, I64, I64, I64, I64, I64],

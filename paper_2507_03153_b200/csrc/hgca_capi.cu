@@ -200,7 +200,7 @@ int hgca_attend_gqa(int dtype, const void* q, const void* KV, int64_t B, int64_t
   a.q = q; a.k = KV; a.v = reinterpret_cast<const unsigned char*>(KV) + d * esz;
   a.Hq = Hq; a.Hkv = Hkv; a.G = Hq / Hkv;
   a.nq = nq; a.d = d; a.ld_head = T * 2 * d; a.ld_row = 2 * d; a.row0 = row0; a.n = n;
-  a.rot = dtype == HGCA_DTYPE_BF16 ? 1 : 0;  // the engine stores bf16 K|V rows position-rotated
+  a.rot = 1;  // the engine stores K|V rows position-rotated (both storage dtypes)
   a.scale = scale;
   a.out = out; a.lse = lse;
   a.wts = weights; a.wts_ld = wts_ld;
@@ -223,7 +223,7 @@ int hgca_attend_gqa_indexed(int dtype, const void* q, const void* KV, int64_t B,
   a.q = q; a.k = KV; a.v = reinterpret_cast<const unsigned char*>(KV) + d * esz;
   a.Hq = Hq; a.Hkv = Hkv; a.G = Hq / Hkv;
   a.nq = nq; a.d = d; a.ld_head = T * 2 * d; a.ld_row = 2 * d; a.row0 = 0; a.n = 0;
-  a.rot = dtype == HGCA_DTYPE_BF16 ? 1 : 0;
+  a.rot = 1;
   a.idx = idx; a.idx_off = idx_off; a.idx_cnt = idx_cnt;
   a.scale = scale;
   a.out = out; a.lse = lse;
@@ -397,18 +397,27 @@ int hgca_maw_ema(double* maw, int64_t rows, int64_t ld, int64_t n, const double*
   return cuda_status(launch_maw_ema(maw, rows, ld, n, a, lda, alpha, S(stream)), "maw_ema");
 }
 
-int hgca_union_build(const uint32_t* sel_mask, int64_t B, int64_t Hq, int64_t Hkv, int64_t words,
-                     int64_t n_arch, int64_t T, int32_t* u_ent, int32_t* u_cnt, int32_t* item_off,
-                     int32_t* item_tab, int64_t sparse_rows, int grouped, hgca_stream_t stream) {
+int hgca_union_build_items(const uint32_t* sel_mask, int64_t B, int64_t Hq, int64_t Hkv, int64_t words,
+                           int64_t n_arch, int64_t T, int32_t* u_ent, int32_t* u_cnt, int32_t* item_off,
+                           int32_t* item_tab, int64_t max_rows, int64_t min_rows, int64_t item_target, int grouped,
+                           hgca_stream_t stream) {
   if (B < 1 || Hkv < 1 || Hq % Hkv || Hq / Hkv > 8 || n_arch < 0 || n_arch > T || words * 32 < n_arch ||
-      sparse_rows < 4 || sparse_rows % 4 || T >= (1 << 24))
+      max_rows < 16 || max_rows % 16 || min_rows < 16 || min_rows % 16 || min_rows > max_rows || item_target < 0 ||
+      T >= (1 << 24))
     return fail(HGCA_EINVAL, "union_build: bad shape");
   if (!item_tab || !u_ent || !u_cnt || !item_off) return fail(HGCA_EINVAL, "union_build: null output");
   return cuda_status(launch_union_build(sel_mask, B, Hq, Hkv, words, n_arch, T, u_ent, u_cnt, item_off,
-                                        reinterpret_cast<int4*>(item_tab), sparse_rows,
-                                        grouped == 2 ? 2 : (grouped ? 1 : 0),
+                                        reinterpret_cast<int4*>(item_tab), max_rows, min_rows, item_target,
+                                        (grouped == 2 || grouped == 3) ? grouped : (grouped ? 1 : 0),
                                         S(stream)),
                      "union_build");
+}
+
+int hgca_union_build(const uint32_t* sel_mask, int64_t B, int64_t Hq, int64_t Hkv, int64_t words,
+                     int64_t n_arch, int64_t T, int32_t* u_ent, int32_t* u_cnt, int32_t* item_off,
+                     int32_t* item_tab, int64_t sparse_rows, int grouped, hgca_stream_t stream) {
+  return hgca_union_build_items(sel_mask, B, Hq, Hkv, words, n_arch, T, u_ent, u_cnt, item_off, item_tab,
+                                sparse_rows, sparse_rows, 0, grouped, stream);
 }
 
 static int decode_prepare(const hgca_decode_desc* d, DecodeArgs& a, DecodeMergeArgs& m) {
@@ -423,12 +432,17 @@ static int decode_prepare(const hgca_decode_desc* d, DecodeArgs& a, DecodeMergeA
   const int64_t W = d->dhi - d->dlo;
   if (d->dlo < 0 || W < 1 || d->dhi > d->T || d->w_old < 0 || d->w_old > W || d->dsc_ld < W)
     return fail(HGCA_EINVAL, "decode_step: bad dense range");
-  if (d->sparse_rows < 4 || d->sparse_rows % 4) return fail(HGCA_EINVAL, "decode_step: sparse_rows must be a positive multiple of 4");
+  if (d->sparse_rows < 16 || d->sparse_rows % 16)
+    return fail(HGCA_EINVAL, "decode_step: sparse_rows must be a positive multiple of 16");
   const int64_t DR = dense_rows_of(d->dtype);
   const int64_t Sd = (W + DR - 1) / DR;  // dense items (window parts) per (batch, kv-head)
   const int64_t n_dense = d->B * d->Hkv * Sd;
-  // every item but the last full and last tail item of a list holds >= sparse_rows/4 rows
-  const int64_t max_sparse = d->B * d->Hkv * ((4 * d->T + d->sparse_rows - 1) / d->sparse_rows + 2);
+  // every item but the last full and last tail item of a list holds >= sparse_rows/4 rows; adaptive
+  // items (hgca_union_build_items, rows >= union / item_target): <= 5/3 item_target + 5 per list
+  if (d->item_target < 0) return fail(HGCA_EINVAL, "decode_step: item_target must be >= 0");
+  const int64_t BKd = d->B * d->Hkv;
+  const int64_t max_sparse = BKd * ((4 * d->T + d->sparse_rows - 1) / d->sparse_rows + 2) +
+                             (d->item_target ? (5 * d->item_target + 2) / 3 + 5 * BKd : 0);
   if (d->max_items < n_dense + max_sparse)
     return fail(HGCA_EINVAL, "decode_step: partial buffers hold %lld items, need %lld",
                 (long long)d->max_items, (long long)(n_dense + max_sparse));

@@ -86,7 +86,12 @@ struct Cursor {
   int item, bk, lo, hi, row, dense;
 };
 
-__device__ __forceinline__ StageDesc cursor_next(Cursor& c, const DecodeArgs& a, int total, int W, int lane) {
+// Static first wave: a warp's first item is its global warp index (cur.nxt
+// preset by the caller, no contended atomic before the first gather); every
+// later item is atomicAdd(counter) + nwarps, prefetched while the current
+// item runs.
+__device__ __forceinline__ StageDesc cursor_next_off(Cursor& c, const DecodeArgs& a, int total, int W, int lane,
+                                                     int nwarps) {
   StageDesc d;
   if (c.item < 0 || c.row >= c.hi) {
     const int it = __shfl_sync(FULL, c.nxt, 0);
@@ -96,15 +101,15 @@ __device__ __forceinline__ StageDesc cursor_next(Cursor& c, const DecodeArgs& a,
       return d;
     }
     c.item = it;
-    if (lane == 0) c.nxt = atomicAdd(a.counter, 1);
-    if (it < (int)a.n_dense_items) {  // dense item: window rows [part*DR, (part+1)*DR) of bk
+    if (lane == 0) c.nxt = atomicAdd(a.counter, 1) + nwarps;
+    if (it < (int)a.n_dense_items) {
       c.dense = 1;
       c.bk = it / (int)a.Sd;
       c.lo = (it % (int)a.Sd) * (int)a.dense_rows;
       c.hi = min(W, c.lo + (int)a.dense_rows);
     } else {
       c.dense = 0;
-      const int4 e = __ldg(a.item_tab + (it - (int)a.n_dense_items));  // (bk, lo, hi, -)
+      const int4 e = __ldg(a.item_tab + (it - (int)a.n_dense_items));
       c.bk = e.x;
       c.lo = e.y;
       c.hi = e.z;
@@ -126,7 +131,7 @@ __device__ __forceinline__ StageDesc cursor_next(Cursor& c, const DecodeArgs& a,
 // kv_in (engine.py:161-163, append_kv kv_cache.py:122-169): the step's new K
 // and V rows of (batch, kv-head) bk are written at position dhi-1 by the warp
 // that issues the dense sub-chunk holding that row, right before its gather
-// (generic-proxy stores fenced before the async-proxy TMA read). bf16 rows are
+// (generic-proxy stores fenced before the async-proxy TMA read). Rows are
 // stored position-rotated (see rotoff). Every lane writes 16-byte chunks.
 template <int D, bool BF16>
 __device__ __forceinline__ void write_new_row(const DecodeArgs& a, const StageDesc& d, int lane) {
@@ -137,7 +142,7 @@ __device__ __forceinline__ void write_new_row(const DecodeArgs& a, const StageDe
   for (int c = lane; c < CH; c += 32) {
     const unsigned char* src = reinterpret_cast<const unsigned char*>(c < CH / 2 ? a.k_new : a.v_new) +
                                (int64_t)d.bk * ROWB + (c % (CH / 2)) * 16;
-    const int pc = BF16 ? ((c & ~7) | ((c ^ (int)pos) & 7)) : c;
+    const int pc = (c & ~7) | ((c ^ (int)pos) & 7);  // rotated rows (both storage dtypes)
     *reinterpret_cast<uint4*>(dst + pc * 16) = *reinterpret_cast<const uint4*>(src);
   }
   fence_proxy_async_global();
@@ -485,12 +490,14 @@ __global__ void __launch_bounds__(Bf16Cfg<D, G, S, NPAIR>::NW * 32, 1)
     int32_t* cmeta = reinterpret_cast<int32_t*>(cw + C::OFF_META);
     uint64_t* cfull = reinterpret_cast<uint64_t*>(cw + C::OFF_FULL);
     uint64_t* cempty = reinterpret_cast<uint64_t*>(cw + C::OFF_EMPTY);
+    // static first wave: this producer's first item is its consumer's global
+    // index; later items come from the work counter (cursor_next_off)
+    const int nwarps = (int)gridDim.x * C::NC;
     Cursor cur;
-    cur.nxt = 0;
-    if (lane == 0) cur.nxt = atomicAdd(a.counter, 1);
+    cur.nxt = (int)blockIdx.x * C::NC + (warp - C::NC);
     cur.item = -1;
     cur.row = cur.hi = cur.lo = cur.bk = cur.dense = 0;
-    StageDesc pend = cursor_next(cur, a, total, W, lane);
+    StageDesc pend = cursor_next_off(cur, a, total, W, lane, nwarps);
     int32_t pend_ent = sub_entry<G>(pend, a, lane);
     const uint64_t evict_first = l2_evict_first_policy();
     for (int k = 0;; ++k) {
@@ -522,7 +529,7 @@ __global__ void __launch_bounds__(Bf16Cfg<D, G, S, NPAIR>::NW * 32, 1)
         const int64_t b = d.bk / a.Hkv, kvh = d.bk % a.Hkv;
         bulk_g2s(cw + C::OFF_Q + s * C::QSLOT, Qg + (b * a.Hq + kvh * G) * (int64_t)C::ROWB, C::QB, &cfull[s]);
       }
-      pend = cursor_next(cur, a, total, W, lane);
+      pend = cursor_next_off(cur, a, total, W, lane, nwarps);
       pend_ent = sub_entry<G>(pend, a, lane);
     }
     return;
@@ -713,31 +720,34 @@ __global__ void __launch_bounds__(Bf16Cfg<D, G, S, NPAIR>::NW * 32, 1)
 }
 
 // =========================================================== fp32 (reference-exact) kernel
+// Self-issuing warps (one CTA per SM, NC warps, each with its own S-stage ring).
+// fp32 K|V rows are stored position-rotated like the bf16 ones (16-byte chunk
+// c of position p at (c & ~7) | ((c ^ p) & 7)), so one tile::gather4 op moves
+// four whole 2*D*4-byte row pairs (8 ops per 32-row stage) and both compute
+// phases read shared memory without bank conflicts: the score phase (lane =
+// row, 16-byte chunks, rows of a quarter-warp in distinct p & 7 classes) and
+// P.V (lanes = head dims of one row).
 template <int D, int G>
 struct F32Cfg {
-  static constexpr int ROWB = D * 4;
-  static constexpr int NKC = ROWB / 128;                // 128-byte tiles per K (or V) row
-  static constexpr int TILE = SUB * 128;                // 32 rows x 128 B, 128B-swizzled
-  static constexpr int PIECES = ROWB / 16;
-  static constexpr int DPL = D / 32;
+  static constexpr int ROWB = D * 4;                    // bytes of one K (or V) row
+  static constexpr int PAIR = 2 * ROWB;                 // one rotated K|V row pair
+  static constexpr int DPL = D / 32;                    // head dims per lane in P.V
   static constexpr int S = 2;
-  static constexpr int STAGE = 2 * NKC * TILE;
-  static constexpr int NOPS = SUB / 4 * 2 * NKC;        // gather4 ops per stage
-  static_assert(NOPS % 32 == 0, "whole gather4 ops per lane");
+  static constexpr int STAGE = SUB * PAIR;
+  static constexpr int NOPS = SUB / 4;                  // gather4 ops per stage
   static constexpr int QB = G * ROWB;
   static constexpr int OFF_Q = S * STAGE;                   // raw queries [S][G][D] f32
   static constexpr int OFF_QK = OFF_Q + S * QB;             // queries [G][D] fp64
-  static constexpr int OFF_SC = OFF_QK + G * D * 8;         // scores [G][32] fp64
-  static constexpr int OFF_ACC = OFF_SC + G * SUB * 8;      // P.V accumulators [G][D] fp32
-  static constexpr int OFF_MZ = OFF_ACC + G * D * 4;        // running (m, z) [G][2] fp64
-  static constexpr int OFF_META = OFF_MZ + G * 16;          // entries [S][32]
+  static constexpr int OFF_ACC = OFF_QK + G * D * 8;        // P.V accumulators [G][D] fp32
+  static constexpr int OFF_META = OFF_ACC + G * D * 4;      // entries [S][32]
   static constexpr int OFF_DESC = OFF_META + S * SUB * 4;
   static constexpr int OFF_BAR = OFF_DESC + S * 32;
-  static constexpr int WARP_SMEM = (OFF_BAR + S * 8 + 1023) / 1024 * 1024;
+  static constexpr int WARP_SMEM = (OFF_BAR + S * 8 + 127) / 128 * 128;
   static constexpr int NC0 = (SMEM_MAX - 1024) / WARP_SMEM;
   static constexpr int NC = NC0 > 8 ? 8 : NC0;
   static constexpr int SMEM = NC * WARP_SMEM + 1024;
   static_assert(NC >= 1, "fp32 decode pipeline does not fit shared memory");
+  static_assert(D == 64 || D == 128, "fp32 decode: head_dim 64 or 128");
 };
 
 template <int D, int G>
@@ -752,9 +762,7 @@ __global__ void __launch_bounds__(F32Cfg<D, G>::NC * 32, 1) decode_f32_kernel(co
   uint64_t* bar = reinterpret_cast<uint64_t*>(wsm + C::OFF_BAR);
   int32_t* meta = reinterpret_cast<int32_t*>(wsm + C::OFF_META);
   double* qk = reinterpret_cast<double*>(wsm + C::OFF_QK);
-  double* sc = reinterpret_cast<double*>(wsm + C::OFF_SC);
   float* accs = reinterpret_cast<float*>(wsm + C::OFF_ACC);
-  double* mz = reinterpret_cast<double*>(wsm + C::OFF_MZ);
   const int W = (int)(a.dhi - a.dlo);
   const int total = (int)(a.n_dense_items + (int64_t)a.item_off[2 * a.B * a.Hkv + 1]);
   const unsigned char* Qg = reinterpret_cast<const unsigned char*>(a.q);
@@ -767,13 +775,16 @@ __global__ void __launch_bounds__(F32Cfg<D, G>::NC * 32, 1) decode_f32_kernel(co
   __syncwarp();
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // see decode_bf16_kernel
 
+  // first item: this warp's global index (no atomic on the critical path);
+  // later items come from the work counter, offset past the first wave
+  const int nwarps = (int)gridDim.x * C::NC;
   Cursor cur;
-  cur.nxt = 0;
-  if (lane == 0) cur.nxt = atomicAdd(a.counter, 1);
+  cur.nxt = (int)blockIdx.x * C::NC + warp;
   cur.item = -1;
   cur.row = cur.hi = cur.lo = cur.bk = cur.dense = 0;
-  StageDesc pend = cursor_next(cur, a, total, W, lane);
+  StageDesc pend = cursor_next_off(cur, a, total, W, lane, nwarps);
   int32_t pend_ent = sub_entry<G>(pend, a, lane);
+  const uint64_t evict_first = l2_evict_first_policy();
 
   auto issue = [&](int s) {
     const StageDesc d = pend;
@@ -791,19 +802,15 @@ __global__ void __launch_bounds__(F32Cfg<D, G>::NC * 32, 1) decode_f32_kernel(co
       const int q3 = __shfl_sync(FULL, pos, rg * 4 + 3);
       if (lane == 0) mbar_expect_tx(&bar[s], C::STAGE + (d.first ? C::QB : 0));
       __syncwarp();
-#pragma unroll
-      for (int op = lane; op < C::NOPS; op += 32) {
-        const int tile = op >> 3;  // 128-byte column tile: K tiles then V tiles
-        const int col = tile < C::NKC ? tile * 32 : D + (tile - C::NKC) * 32;
-        tma_gather4(wsm_u + s * C::STAGE + tile * C::TILE + rg * 512, &a.kmap, col, rowbase + q0, rowbase + q1,
-                    rowbase + q2, rowbase + q3, &bar[s]);
-      }
+      if (lane < C::NOPS)
+        tma_gather4_hint(wsm_u + s * C::STAGE + rg * 4 * C::PAIR, &a.kmap, 0, rowbase + q0, rowbase + q1,
+                         rowbase + q2, rowbase + q3, &bar[s], evict_first);
       if (lane == 8 && d.first) {
         const int64_t b = d.bk / a.Hkv, kvh = d.bk % a.Hkv;
         bulk_g2s(wsm + C::OFF_Q + s * C::QB, Qg + (b * a.Hq + kvh * G) * (int64_t)C::ROWB, C::QB, &bar[s]);
       }
     }
-    pend = cursor_next(cur, a, total, W, lane);
+    pend = cursor_next_off(cur, a, total, W, lane, nwarps);
     pend_ent = sub_entry<G>(pend, a, lane);
   };
 
@@ -812,6 +819,7 @@ __global__ void __launch_bounds__(F32Cfg<D, G>::NC * 32, 1) decode_f32_kernel(co
   for (int s = 0; s < C::S; ++s) issue(s);
   TL(tl_issue += clock64() - ci0;)
 
+  double m_run[G], z_run[G];  // running (m, z) of the current item, per head (warp-uniform)
   for (int k = 0;; ++k) {
     const int s = k % C::S;
     __syncwarp();
@@ -820,78 +828,93 @@ __global__ void __launch_bounds__(F32Cfg<D, G>::NC * 32, 1) decode_f32_kernel(co
     TL(long long c0 = clock64();)
     mbar_wait(&bar[s], (k / C::S) & 1);
     TL(long long c1 = clock64(); tl_wait += c1 - c0; ++tl_sub; if (!tl_first) tl_first = gtimer();)
-    const unsigned char* st = wsm + s * C::STAGE;  // tiles: K[NKC] then V[NKC], rows swizzled
+    const unsigned char* st = wsm + s * C::STAGE;
     const int32_t myent = meta[s * SUB + lane];
     const uint32_t qm = (uint32_t)myent >> 24;
-    const uint32_t wq = __reduce_or_sync(FULL, qm);
+    const uint32_t wq = G == 1 ? 1u : __reduce_or_sync(FULL, qm);
+    const int myrot = myent & 7;
     if (d.first) {
       const float* qr = reinterpret_cast<const float*>(wsm + C::OFF_Q + s * C::QB);
       for (int t = lane; t < G * D; t += 32) qk[t] = (double)qr[t];
       for (int t = lane; t < G * D; t += 32) accs[t] = 0.f;
-      if (lane < G) {
-        mz[2 * lane] = -INFINITY;
-        mz[2 * lane + 1] = 0.0;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        m_run[g] = -INFINITY;
+        z_run[g] = 0.0;
       }
       __syncwarp();
     }
     // ---- scores: lane = row, exact fp64 products summed in the reference's
-    // sequential order over the head dimension (_core.pyx:59-65); the swizzle
-    // spreads one piece index over 8 banks groups, so lane = row is conflict-free
+    // sequential order over the head dimension (_core.pyx:59-65)
     double sacc[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) sacc[g] = 0.0;
     {
-#pragma unroll 4
-      for (int p = 0; p < C::PIECES; ++p) {
-        const float4 kv = *reinterpret_cast<const float4*>(st + (p >> 3) * C::TILE + swz128(lane, p & 7));
+      // batches of 16 elements: the 16 loads and fp32 -> fp64 conversions are
+      // issued ahead of the batch's dependent DFMA chain (the chain, ~8
+      // cycles per DFMA, is what bounds a stage)
+      const unsigned char* kr = st + lane * C::PAIR;
+#pragma unroll 2
+      for (int c0 = 0; c0 < D / 4; c0 += 4) {
+        float4 kv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = c0 + u;
+          kv[u] = *reinterpret_cast<const float4*>(kr + (((c & ~7) | ((c ^ myrot) & 7)) << 4));
+        }
+        double kd[16];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          kd[4 * u + 0] = (double)kv[u].x;
+          kd[4 * u + 1] = (double)kv[u].y;
+          kd[4 * u + 2] = (double)kv[u].z;
+          kd[4 * u + 3] = (double)kv[u].w;
+        }
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-          if ((wq >> g) & 1u) {
-            const double2 qa = *reinterpret_cast<const double2*>(qk + g * D + p * 4);
-            const double2 qb = *reinterpret_cast<const double2*>(qk + g * D + p * 4 + 2);
-            sacc[g] = fma(qa.x, (double)kv.x, sacc[g]);  // exact products: one rounding per add
-            sacc[g] = fma(qa.y, (double)kv.y, sacc[g]);
-            sacc[g] = fma(qb.x, (double)kv.z, sacc[g]);
-            sacc[g] = fma(qb.y, (double)kv.w, sacc[g]);
+          if (G == 1 || ((wq >> g) & 1u)) {
+            const double* qg = qk + g * D + c0 * 4;
+#pragma unroll
+            for (int e = 0; e < 16; e += 2) {
+              const double2 qq = *reinterpret_cast<const double2*>(qg + e);
+              sacc[g] = fma(qq.x, kd[e], sacc[g]);  // exact products: one rounding per add
+              sacc[g] = fma(qq.y, kd[e + 1], sacc[g]);
+            }
           }
         }
       }
     }
     const int64_t b = d.bk / a.Hkv, kvh = d.bk % a.Hkv;
     TL(long long c2 = clock64(); tl_score += c2 - c1;)
+    // ---- per active head: online softmax (fp64 exp, the weights the MAW
+    // needs) and P.V in fp32 with lanes over head dims
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      if (!((wq >> g) & 1u)) continue;
+      if (G > 1 && !((wq >> g) & 1u)) continue;
       const double sv = (lane < d.n && ((qm >> g) & 1u)) ? sacc[g] * a.scale : -INFINITY;
-      sc[g * SUB + lane] = sv;
       if (d.dense && lane < d.n)
         reinterpret_cast<double*>(a.dsc)[(b * a.Hq + kvh * G + g) * a.dsc_ld + d.r0 + lane] = sv;
-    }
-    __syncwarp();
-    // ---- per active head: online softmax (fp64) + P.V (fp32, lanes over dims)
-    for (uint32_t hm = wq; hm; hm &= hm - 1) {
-      const int g = __ffs(hm) - 1;
-      const double sv = sc[g * SUB + lane];
       const double cm = warp_max_f64(sv);
-      const double m_old = mz[2 * g];
-      const double mnew = fmax(m_old, cm);
+      const double mnew = fmax(m_run[g], cm);
       if (mnew == -INFINITY) continue;
-      const double scal = exp(m_old - mnew);
-      const double p = exp(sv - mnew);
-      const double zs = warp_sum_f64(p);
+      const double scal = exp(m_run[g] - mnew);
+      const double p = sv == -INFINITY ? 0.0 : exp(sv - mnew);
+      z_run[g] = z_run[g] * scal + warp_sum_f64(p);
+      m_run[g] = mnew;
       const float pf = (float)p;
       const float sf = (float)scal;
       float acc[C::DPL];
       float* ag = accs + g * D + lane * C::DPL;
 #pragma unroll
       for (int i = 0; i < C::DPL; ++i) acc[i] = ag[i] * sf;
+      // V chunk of this lane's dims; 16-byte chunk index inside the row pair
+      constexpr int VC0 = D / 4;
+      const int vc = VC0 + lane * C::DPL / 4, vo = (lane * C::DPL) % 4;
 #pragma unroll 8
       for (int r = 0; r < SUB; ++r) {
         const float pr = __shfl_sync(FULL, pf, r);
-        if (r >= d.n) break;
-        const int pc = lane * C::DPL / 4;  // 16-byte piece of the V row holding this lane's dims
-        const float* vr = reinterpret_cast<const float*>(st + (C::NKC + (pc >> 3)) * C::TILE + swz128(r, pc & 7)) +
-                          (lane * C::DPL) % 4;
+        const int rr = meta[s * SUB + r] & 7;
+        const float* vr = reinterpret_cast<const float*>(st + r * C::PAIR + (((vc & ~7) | ((vc ^ rr) & 7)) << 4)) + vo;
         if constexpr (C::DPL == 4) {
           const float4 v = *reinterpret_cast<const float4*>(vr);
           acc[0] = fmaf(pr, v.x, acc[0]); acc[1] = fmaf(pr, v.y, acc[1]);
@@ -903,20 +926,18 @@ __global__ void __launch_bounds__(F32Cfg<D, G>::NC * 32, 1) decode_f32_kernel(co
       }
 #pragma unroll
       for (int i = 0; i < C::DPL; ++i) ag[i] = acc[i];
-      __syncwarp();
-      if (lane == 0) {
-        mz[2 * g] = mnew;
-        mz[2 * g + 1] = mz[2 * g + 1] * scal + zs;
-      }
-      __syncwarp();
     }
     TL(long long c3 = clock64(); tl_pv += c3 - c2;)
     if (d.last) {
       TL(++tl_items;)
+      __syncwarp();
       for (int t = lane; t < G * D; t += 32) a.part_acc[((t / D) * a.m.MI + d.item) * D + t % D] = accs[t];
-      if (lane < G) {
-        a.part_m[lane * a.m.MI + d.item] = mz[2 * lane];
-        a.part_z[lane * a.m.MI + d.item] = mz[2 * lane + 1];
+      if (lane == 0) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          a.part_m[g * a.m.MI + d.item] = m_run[g];
+          a.part_z[g * a.m.MI + d.item] = z_run[g];
+        }
       }
     }
     __syncwarp();
@@ -1084,6 +1105,10 @@ __global__ void __launch_bounds__(1024) union_window_classes_kernel(int32_t* u_e
 #endif
 constexpr int TAIL_DIV = HGCA_TAIL_DIV;      // the last >= 1/TAIL_DIV of each list is tail items
 constexpr int TAIL_SPLIT = HGCA_TAIL_SPLIT;  // of rows / TAIL_SPLIT entries each
+// the host's item capacities (hgca_decode_step, sparse_capacity) assume tail
+// items of >= rows / 4 entries, and rows >= 16 keeps them >= 4 entries
+static_assert(TAIL_SPLIT >= 1 && TAIL_SPLIT <= 4, "tail items must hold >= rows / 4 entries");
+static_assert(TAIL_DIV >= 2, "the tail is at most half of a list");
 __device__ __forceinline__ void item_counts(int64_t cnt, int64_t rows, int& nbig, int& nsmall) {
   const int64_t big = (cnt - cnt / TAIL_DIV) / rows * rows;
   const int64_t small = rows / TAIL_SPLIT;
@@ -1091,12 +1116,29 @@ __device__ __forceinline__ void item_counts(int64_t cnt, int64_t rows, int& nbig
   nsmall = (int)((cnt - big + small - 1) / small);
 }
 
-__global__ void item_offsets_kernel(const int32_t* u_cnt, int64_t BK, int64_t rows, int32_t* off) {
+// Item granularity adapts to the step (off[2*(BK+1)] = rows chosen): the
+// largest power-of-two fraction of max_rows, not below min_rows, that still
+// yields >= target items over the union -- big steps keep long items (few
+// partials to fold), small steps get enough items for every warp.
+__global__ void item_offsets_kernel(const int32_t* u_cnt, int64_t BK, int64_t max_rows, int64_t min_rows,
+                                    int64_t target, int32_t* off) {
   __shared__ int32_t carry[2];
   __shared__ int wsum[2][32];
+  __shared__ long long utot;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarp = blockDim.x >> 5;
+  if (tid == 0) utot = 0;
+  __syncthreads();
+  {
+    long long u = 0;
+    for (int64_t x = tid; x < BK; x += blockDim.x) u += u_cnt[x];
+    for (int o = 16; o; o >>= 1) u += __shfl_xor_sync(0xffffffffu, u, o);
+    if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&utot), (unsigned long long)u);
+  }
   if (tid < 2) carry[tid] = 0;
   __syncthreads();
+  int64_t rows = max_rows;
+  while (rows / 2 >= min_rows && utot < rows * target) rows /= 2;
+  if (tid == 0) off[2 * (BK + 1)] = (int32_t)rows;
   for (int pass = 0; pass < 2; ++pass) {
     for (int64_t x0 = 0; x0 < BK; x0 += blockDim.x) {
       const int64_t x = x0 + tid;
@@ -1133,9 +1175,10 @@ __global__ void item_offsets_kernel(const int32_t* u_cnt, int64_t BK, int64_t ro
 }
 
 // item_tab[id] = (bk, lo, hi, 0) for the full and tail items of bk
-__global__ void item_table_kernel(const int32_t* u_cnt, const int32_t* off, int64_t BK, int64_t rows, int4* tab) {
+__global__ void item_table_kernel(const int32_t* u_cnt, const int32_t* off, int64_t BK, int4* tab) {
   const int64_t bk = blockIdx.x;
   if (bk >= BK) return;
+  const int64_t rows = off[2 * (BK + 1)];
   int nb = 0, ns = 0;
   item_counts(u_cnt[bk], rows, nb, ns);
   const int cnt = u_cnt[bk], small = (int)(rows / TAIL_SPLIT), big = nb * (int)rows;
@@ -1172,9 +1215,9 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 // 2-D tensor map over KV viewed as [rows = B*Hkv*T, 2*D elements] for
-// tile::gather4. bf16: box = one whole (rotated) K|V row pair, no swizzle --
-// TMA gather cost is per gathered row, so whole rows keep it at 8 ops per
-// 32-row stage. fp32: box = one 128-byte column tile, 128B swizzle.
+// tile::gather4: box = one whole (rotated) K|V row pair, no swizzle -- TMA
+// gather cost is per gathered row, so whole rows keep it at 8 ops per 32-row
+// stage (both storage dtypes).
 static int make_row_map(CUtensorMap* map, const void* base, int64_t rows, int64_t D, bool bf16) {
   static EncodeTiledFn encode = nullptr;
   if (!encode) {
@@ -1186,11 +1229,11 @@ static int make_row_map(CUtensorMap* map, const void* base, int64_t rows, int64_
   const int esz = bf16 ? 2 : 4;
   cuuint64_t gdim[2] = {(cuuint64_t)(2 * D), (cuuint64_t)rows};
   cuuint64_t gstr[1] = {(cuuint64_t)(2 * D * esz)};
-  cuuint32_t box[2] = {bf16 ? (cuuint32_t)(2 * D) : 32u, 1};
+  cuuint32_t box[2] = {(cuuint32_t)(2 * D), 1};
   cuuint32_t es[2] = {1, 1};
   CUresult r = encode(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                       const_cast<void*>(base), gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                      bf16 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
+                      CU_TENSOR_MAP_SWIZZLE_NONE,
                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : -3001;
 }
@@ -1279,21 +1322,21 @@ int launch_decode_partial(int dtype, const DecodeArgs& a, cudaStream_t s) {
 
 int launch_union_build(const uint32_t* sel, int64_t B, int64_t Hq, int64_t Hkv, int64_t words, int64_t n_arch,
                        int64_t T, int32_t* u_ent, int32_t* u_cnt, int32_t* item_off, int4* item_tab,
-                       int64_t sparse_rows, int grouped, cudaStream_t s) {
+                       int64_t sparse_rows, int64_t min_rows, int64_t target, int grouped, cudaStream_t s) {
   const int64_t G = Hq / Hkv;
   union_build_kernel<<<(unsigned)(B * Hkv), 1024, 0, s>>>(sel, Hq, Hkv, G, words, n_arch, T, u_ent, u_cnt,
-                                                          grouped == 1 ? 1 : 0);
-  if (grouped == 2) {
+                                                          (grouped == 1 || grouped == 3) ? 1 : 0);
+  if (grouped >= 2) {
     const cudaError_t e0 = cudaGetLastError();
     if (e0 != cudaSuccess) return (int)e0;
     union_window_classes_kernel<<<(unsigned)(B * Hkv), 1024, 0, s>>>(u_ent, u_cnt, T);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
-  item_offsets_kernel<<<1, 1024, 0, s>>>(u_cnt, B * Hkv, sparse_rows, item_off);
+  item_offsets_kernel<<<1, 1024, 0, s>>>(u_cnt, B * Hkv, sparse_rows, min_rows, target, item_off);
   e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
-  item_table_kernel<<<(unsigned)(B * Hkv), 128, 0, s>>>(u_cnt, item_off, B * Hkv, sparse_rows, item_tab);
+  item_table_kernel<<<(unsigned)(B * Hkv), 128, 0, s>>>(u_cnt, item_off, B * Hkv, item_tab);
   return (int)cudaGetLastError();
 }
 
@@ -1307,7 +1350,7 @@ int launch_write_rows(int dtype, void* KV, int64_t BH, int64_t T, int64_t D, int
   const int64_t nb = (total + 255) / 256;
   const int blocks = (int)(nb < 148 * 8 ? nb : 148 * 8);
   write_rows_kernel<<<blocks, 256, 0, s>>>((unsigned char*)KV, BH, T, rowb, pos, (const unsigned char*)k_new,
-                                           (const unsigned char*)v_new, n, dtype == kBF16 ? 1 : 0);
+                                           (const unsigned char*)v_new, n, 1);
   return (int)cudaGetLastError();
 }
 

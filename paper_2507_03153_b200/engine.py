@@ -27,6 +27,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass, field, replace
 
 import numpy as np
@@ -43,6 +44,27 @@ __all__ = ["CacheConfig", "EngineConfig", "StepInput", "StepOutput", "LayerState
            "StoreView", "run_sequence"]
 
 MODES = ("decode", "append")
+
+
+# smallest adaptive sparse item; HGCA_MIN_ITEM_ROWS / HGCA_ITEMS_PER_WARP are A/B knobs for tools
+MIN_ITEM_ROWS = int(os.environ.get("HGCA_MIN_ITEM_ROWS", "64"))
+ITEMS_PER_WARP = float(os.environ.get("HGCA_ITEMS_PER_WARP", "2"))
+
+
+def item_target(dtype: str, G: int, D: int, dev) -> int:
+    """Sparse work items a union rebuild aims for: ITEMS_PER_WARP per decode
+    warp (hgca_decode_config consumer warps x SMs), so small steps spread over
+    the whole GPU while big steps keep long items (hgca_union_build_items)."""
+    cfg = (ctypes.c_int64 * 5)()
+    _lib.call("hgca_decode_config", DTYPE_CODE[torch.bfloat16 if dtype == "bfloat16" else torch.float32], D, G, cfg)
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count if torch.device(dev).type == "cuda" else 148
+    return int(ITEMS_PER_WARP * int(cfg[0]) * nsm)
+
+
+def sparse_capacity(BK: int, T: int, max_rows: int, target: int) -> int:
+    """Upper bound on sparse items (hgca_decode_step's partials check): fixed
+    max_rows items (tail items of max_rows / 4) or adaptive ones."""
+    return BK * (-(-4 * T // max_rows) + 2) + (5 * target + 2) // 3 + 5 * BK
 
 
 def item_rows(dtype: str) -> tuple[int, int]:
@@ -190,10 +212,11 @@ class LayerState:
         self.sel = torch.zeros((B * Hq, words), dtype=torch.int32, device=dev)
         self.u_ent = torch.zeros((B * Hkv, T), dtype=torch.int32, device=dev)
         self.u_cnt = torch.zeros(B * Hkv, dtype=torch.int32, device=dev)
-        self.item_off = torch.zeros(2 * (B * Hkv + 1), dtype=torch.int32, device=dev)
-        self.sparse_rows = item_rows(cfg.dtype)[1]
-        self.item_tab = torch.zeros((B * Hkv * (-(-4 * T // self.sparse_rows) + 2), 4), dtype=torch.int32,
-                                    device=dev)
+        self.item_off = torch.zeros(2 * (B * Hkv + 1) + 1, dtype=torch.int32, device=dev)
+        self.sparse_rows = item_rows(cfg.dtype)[1]   # the longest sparse item; shorter when the union is small
+        self.item_target = item_target(cfg.dtype, Hq // Hkv, D, dev)
+        self.item_tab = torch.zeros((sparse_capacity(B * Hkv, T, self.sparse_rows, self.item_target), 4),
+                                    dtype=torch.int32, device=dev)
         self.lo = 0    # archive size
         self.nxt = 0   # next position
         self.desc = None  # cached hgca_decode_desc (engine-owned)
@@ -204,18 +227,17 @@ class LayerState:
             self.keep = torch.from_numpy(bits.view(np.int32)).to(dev)
 
     def rows(self):
-        """Logical [B*Hkv, T, 2, D] view of KV (a copy for bfloat16 storage,
-        whose rows are stored position-rotated: 16-byte chunk c of the row pair
-        of position p at chunk (c & ~7) | ((c ^ p) & 7), hgca_write_rows)."""
-        if self.KV.dtype != torch.bfloat16:
-            return self.KV
+        """Logical [B*Hkv, T, 2, D] copy of KV, whose rows are stored
+        position-rotated: 16-byte chunk c of the row pair of position p at
+        chunk (c & ~7) | ((c ^ p) & 7) (hgca_write_rows)."""
         BH, T, _, D = self.KV.shape
-        ch = 2 * D // 8
+        epc = 16 // self.KV.element_size()   # elements per 16-byte chunk
+        ch = 2 * D // epc
         c = torch.arange(ch, device=self.KV.device)
         p = torch.arange(T, device=self.KV.device)
         phys = (c[None, :] & ~7) | ((c[None, :] ^ p[:, None]) & 7)          # [T, ch]
-        flat = self.KV.view(BH, T, ch, 8)
-        idx = phys[None, :, :, None].expand(BH, T, ch, 8)
+        flat = self.KV.view(BH, T, ch, epc)
+        idx = phys[None, :, :, None].expand(BH, T, ch, epc)
         return torch.gather(flat, 2, idx).view(BH, T, 2, D)
 
     @property
@@ -448,7 +470,7 @@ class HybridEngine:
         self.dsc = torch.zeros((BHq, self.dsc_ld), dtype=torch.float64, device=self.dev)
         dense_rows, sparse_rows = item_rows(c.dtype)
         n_dense = self.B * self.Hkv * math.ceil(self.dsc_ld / dense_rows)
-        n_sparse = self.B * self.Hkv * (math.ceil(4 * self.T / sparse_rows) + 2)
+        n_sparse = sparse_capacity(self.B * self.Hkv, self.T, sparse_rows, self.layers[0].item_target)
         self.max_items = n_dense + n_sparse
         # per-item partials, head-major ([G, max_items] / [G, max_items, D])
         self.part_m = torch.empty(self.G * self.max_items, dtype=torch.float64, device=self.dev)
@@ -500,13 +522,14 @@ class HybridEngine:
         else:
             ls.sel = ls.ctx.clone()  # a fresh tensor: a StepOutput may hold the old one
         self.launches += 2 + (3 if (self.g_pad > 1 and n) else 0) + (1 if self.config.selection == "topk" and n else 0)
-        # fp32 kernel: group union rows by query-head mask (single-head
-        # sub-chunks); bf16 kernel: position-class interleaved (conflict-free
-        # ldmatrix over the position-rotated rows; it scores every head)
-        grouped = 1 if self.tdtype == torch.float32 else 2
-        _lib.call("hgca_union_build", ls.sel.data_ptr(), self.B, self.Hq, self.Hkv, words, n, self.T,
+        # fp32 kernel: union rows grouped by query-head mask (single-head
+        # sub-chunks), bf16 kernel: position order; both then position-class
+        # interleaved per 32-entry window (conflict-free shared-memory reads of
+        # the position-rotated rows)
+        grouped = 3 if self.tdtype == torch.float32 else 2
+        _lib.call("hgca_union_build_items", ls.sel.data_ptr(), self.B, self.Hq, self.Hkv, words, n, self.T,
                   ls.u_ent.data_ptr(), ls.u_cnt.data_ptr(), ls.item_off.data_ptr(), ls.item_tab.data_ptr(),
-                  ls.sparse_rows, grouped, s)
+                  ls.sparse_rows, MIN_ITEM_ROWS, ls.item_target, grouped, s)
 
     def _ingest(self, ls: LayerState, lo, hi, divisor):
         """StoreTier.ingest_evicted of positions [lo, hi) (sparsifier.py:127-156)."""
@@ -675,7 +698,7 @@ class HybridEngine:
             d.B, d.Hq, d.Hkv, d.D, d.T = self.B, self.Hq, self.Hkv, self.D, self.T
             d.KV = ls.KV.data_ptr()
             d.scale = float(self.shape.scale)
-            d.sparse_rows = ls.sparse_rows
+            d.sparse_rows, d.item_target = ls.sparse_rows, ls.item_target
             d.u_ent, d.u_cnt, d.item_off = ls.u_ent.data_ptr(), ls.u_cnt.data_ptr(), ls.item_off.data_ptr()
             d.item_tab = ls.item_tab.data_ptr()
             d.dsc, d.dsc_ld = self.dsc.data_ptr(), self.dsc_ld

@@ -1,4 +1,4 @@
-"""The other BASELINE.json configs on one B200 (manual runs; bench.py's driver line is C2).
+"""The other BASELINE.json configs on one B200 (manual runs; bench.py's driver line is C3, with C2 beside it).
 
   python tools/bench_configs.py C1      the reference's fp32 case (32 heads, 4K context, batch 1) vs its CPU path
   python tools/bench_configs.py C3      B=4, 128K context (the N=1 point of the sequence-sharded scaling run)
@@ -7,7 +7,7 @@
   python tools/bench_configs.py C5      sparsity sweep at 64K context: window 256..8K x selected 1..20%
 
 Each prints one JSON line per measured point: tokens/s, ms per step, achieved GB/s of the decode step
-kernels over the algorithmic bytes (bench.partial_bytes) and the fraction of MEASURED_PEAKS hbm_gbs.
+kernels over the algorithmic bytes (bench.step_bytes) and the fraction of MEASURED_PEAKS hbm_gbs.
 Data: synthetic randn K/V/q, MAW drawn so the threshold selects the stated fraction per query head.
 """
 import json
@@ -57,7 +57,7 @@ def measure(cfgd, layers=1, steps=50, warmup=5, name=""):
     ms = e0.elapsed_time(e1) / steps
     kern_ms = statistics.mean(a.elapsed_time(b) for a, b in eng.step_events)  # per layer-step
     eng.step_events = None
-    pbytes, dense_b, sparse_b = bench.partial_bytes(eng, Wavg, U, n_items)
+    pbytes, dense_b, sparse_b, _ = bench.step_bytes(eng, Wavg, U, n_items)
     gbs = pbytes / (kern_ms * 1e-3) / 1e9
     return {"config": name, "batch": B, "q_heads": Hq, "kv_heads": Hkv, "context": cfgd["context"],
             "window": Wavg, "selected_frac": cfgd["frac"], "layers": layers,
