@@ -90,7 +90,7 @@ __global__ void __launch_bounds__((AMAXW + 1) * 32, 1) append_attend_kernel(cons
   using C = AppendCfg<D, PASS>;
   constexpr int KC = D / 16;
   extern __shared__ unsigned char sm_raw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sm = smem_align1024(sm_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);
   uint64_t* empty = full + AS;
   float* wbuf = reinterpret_cast<float*>(sm + C::OFF_W);
@@ -384,7 +384,7 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
   constexpr int D = 128;
   constexpr uint32_t O_COL = 2 * T5_KEYS;
   extern __shared__ unsigned char sm_raw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sm = smem_align1024(sm_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);
   uint64_t* qfull = bars;
   uint64_t* full = bars + 1;
@@ -642,7 +642,7 @@ __global__ void __launch_bounds__(Tc5x2Cfg::THREADS, 1) append_tc5x2_kernel(cons
   constexpr int D = 128;
   constexpr uint32_t O_COL = 4 * T5_KEYS;
   extern __shared__ unsigned char sm_raw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sm = smem_align1024(sm_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);
   uint64_t* qfull = bars;
   uint64_t* full = bars + 1;
@@ -904,7 +904,7 @@ __global__ void __launch_bounds__(Tc5MCfg::THREADS, 1) append_tc5_mean_kernel(co
   constexpr int D = 128;
   constexpr uint32_t M_COL = 2 * T5_KEYS;
   extern __shared__ unsigned char sm_raw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sm = smem_align1024(sm_raw);
   int64_t bk, rg, chunk;
   int seg;
   append_item(a, blockIdx.x, bk, rg, seg, chunk);
@@ -1147,7 +1147,7 @@ __global__ void __launch_bounds__(Tc5Mx2Cfg::THREADS, 1) append_tc5_mean_x2_kern
   constexpr int D = 128;
   constexpr uint32_t M_COL = 4 * T5_KEYS;
   extern __shared__ unsigned char sm_raw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sm = smem_align1024(sm_raw);
   const int64_t nc = a.nch[0] + a.nch[1], npair = (a.n_rg + 1) / 2;
   const int64_t cidx = blockIdx.x % nc, t_ = blockIdx.x / nc;
   const int64_t pair = t_ % npair, bk = t_ / npair;

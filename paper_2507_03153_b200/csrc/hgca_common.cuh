@@ -27,6 +27,12 @@ template <> __device__ __forceinline__ __nv_bfloat16 from_f64<__nv_bfloat16>(dou
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
+// 1024-byte-aligned base inside dynamic shared memory. Offsetting the shared
+// array (instead of rounding an integer-cast address) keeps the pointer in the
+// shared state space, so the compiler emits LDS/STS, not generic LD/ST.
+__device__ __forceinline__ unsigned char* smem_align1024(unsigned char* raw) {
+  return raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
+}
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem_dst)), "l"(gmem_src)
                : "memory");

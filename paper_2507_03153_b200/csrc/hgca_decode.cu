@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(Bf16Cfg<D, G, S, NPAIR>::NW * 32, 1)
   using C = Bf16Cfg<D, G, S, NPAIR>;
   constexpr int KC = D / 16;  // k16 chunks of the head dim (QK) == m16 tiles of the head dim (PV)
   extern __shared__ unsigned char sm_raw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sm = smem_align1024(sm_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int W = (int)(a.dhi - a.dlo);
   const int total = (int)(a.n_dense_items + (int64_t)a.item_off[2 * a.B * a.Hkv + 1]);
@@ -754,7 +754,7 @@ template <int D, int G>
 __global__ void __launch_bounds__(F32Cfg<D, G>::NC * 32, 1) decode_f32_kernel(const __grid_constant__ DecodeArgs a) {
   using C = F32Cfg<D, G>;
   extern __shared__ unsigned char sm_raw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sm = smem_align1024(sm_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* wsm = sm + warp * C::WARP_SMEM;
   const uint32_t wsm_u = smem_u32(wsm);

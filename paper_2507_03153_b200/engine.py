@@ -46,9 +46,13 @@ __all__ = ["CacheConfig", "EngineConfig", "StepInput", "StepOutput", "LayerState
 MODES = ("decode", "append")
 
 
-# smallest adaptive sparse item; HGCA_MIN_ITEM_ROWS / HGCA_ITEMS_PER_WARP are A/B knobs for tools
+# Step-adaptive sparse items (hgca_union_build_items): HGCA_ITEMS_PER_WARP > 0
+# shortens items of small unions to give every decode warp that many items.
+# Measured on B200 (profiles/r02_item_ab.txt): fixed full-length items were
+# fastest even for the small C5 step (29.5 us vs 31-35 us), so it is off by
+# default -- the per-item q load, partial write and fold outweigh the balance.
 MIN_ITEM_ROWS = int(os.environ.get("HGCA_MIN_ITEM_ROWS", "64"))
-ITEMS_PER_WARP = float(os.environ.get("HGCA_ITEMS_PER_WARP", "2"))
+ITEMS_PER_WARP = float(os.environ.get("HGCA_ITEMS_PER_WARP", "0"))
 
 
 def item_target(dtype: str, G: int, D: int, dev) -> int:
@@ -450,7 +454,9 @@ class HybridEngine:
     def __init__(self, config: EngineConfig, dev=None):
         self.config = config
         self.shape = config.head_shape
-        self.dev = dev or device()
+        self.dev = torch.device(dev) if dev is not None else device()
+        if self.dev.type == "cuda" and self.dev.index is None:
+            self.dev = torch.device("cuda", torch.cuda.current_device())
         c = config
         self.B, self.Hq, self.Hkv, self.D = c.batch, c.heads, c.n_kv_heads, c.head_dim
         self.G = self.Hq // self.Hkv
@@ -529,7 +535,7 @@ class HybridEngine:
         grouped = 3 if self.tdtype == torch.float32 else 2
         _lib.call("hgca_union_build_items", ls.sel.data_ptr(), self.B, self.Hq, self.Hkv, words, n, self.T,
                   ls.u_ent.data_ptr(), ls.u_cnt.data_ptr(), ls.item_off.data_ptr(), ls.item_tab.data_ptr(),
-                  ls.sparse_rows, MIN_ITEM_ROWS, ls.item_target, grouped, s)
+                  ls.sparse_rows, min(MIN_ITEM_ROWS, ls.sparse_rows), ls.item_target, grouped, s)
 
     def _ingest(self, ls: LayerState, lo, hi, divisor):
         """StoreTier.ingest_evicted of positions [lo, hi) (sparsifier.py:127-156)."""
@@ -661,9 +667,16 @@ class HybridEngine:
         out_sparse / lse_sparse (optional) receive the sparse-only partial
         (the per-rank contribution under sequence sharding)."""
         ls = self.layers[layer_idx]
-        if not (q.is_contiguous() and k.is_contiguous() and v.is_contiguous()) or k.dtype != self.tdtype:
-            raise ContractError("decode_device takes contiguous device tensors in the storage dtype")
         BHq = self.B * self.Hq
+        nq_el, nk_el = BHq * self.D, self.B * self.Hkv * self.D
+        for name, t, n in (("q", q, nq_el), ("k", k, nk_el), ("v", v, nk_el)):
+            if not isinstance(t, torch.Tensor) or t.dtype != self.tdtype or not t.is_contiguous() \
+                    or t.device != self.dev or t.numel() != n:
+                raise ContractError(f"decode_device: {name} must be a contiguous {self.tdtype} tensor of {n} "
+                                    f"elements on {self.dev}")
+        for name, t, dt, n in (("out", out, torch.float32, BHq * self.D), ("lse", lse, torch.float64, BHq)):
+            if t is not None and (t.dtype != dt or not t.is_contiguous() or t.device != self.dev or t.numel() != n):
+                raise ContractError(f"decode_device: {name} must be a contiguous {dt} tensor of {n} elements")
         if out is None:
             out = torch.empty((BHq, self.D), dtype=torch.float32, device=self.dev)
         if lse is None:

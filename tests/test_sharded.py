@@ -262,16 +262,21 @@ def test_gpu_push_exchange_matches_allgather(cuda, world, dtype):
         e.close()
 
 
-def _gpu_worker(rank, world, port_no, q, exchange="allgather", steps=400):
+def _gpu_worker(rank, world, port_no, q, exchange="allgather", steps=400, own_device=False):
     import torch.distributed as dist
 
     import paper_2507_03153_b200 as hg
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port_no)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    if own_device:  # one physical GPU per rank: NCCL over NVLink, CUDA IPC between devices
+        torch.cuda.set_device(rank)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        torch.cuda.set_device(0)
+        if not own_device:
+            torch.cuda.set_device(0)
         cfg = hg.EngineConfig(layers=1, heads=8, kv_heads=2, head_dim=128, batch=2, dtype="bfloat16",
                               cache=hg.CacheConfig(blk_num=4, blk_size=32, beta=1.0), core_count=64,
                               max_positions=1024)
@@ -330,3 +335,41 @@ def test_gpu_sharded_engine_two_processes(cuda, exchange, steps):
     np.testing.assert_array_equal(res[0][0], res[1][0])
     err = np.abs(res[0][0] - ref).max() / np.abs(ref).max()
     assert err <= 1e-2, err
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not (torch.cuda.is_available() and torch.cuda.device_count() >= 2),
+                    reason="needs two physical GPUs")
+@pytest.mark.parametrize("exchange", ["allgather", "push"])
+def test_multi_gpu_sharded_engine(cuda, exchange):
+    """Two ranks on two physical GPUs (NCCL process group): the NCCL all-gather
+    and the one-shot push over NVLink (receive boxes mapped across devices with
+    CUDA IPC) both return, on every rank, the single-GPU engine's output within
+    bf16 tolerance -- identical on both ranks."""
+    import torch.multiprocessing as mp
+
+    hg = cuda
+    steps = 300
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port_no = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port_no, q, exchange, steps, True)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((r[0], r[1:]) for r in (q.get(timeout=600) for _ in range(2)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cfg = hg.EngineConfig(layers=1, heads=8, kv_heads=2, head_dim=128, batch=2, dtype="bfloat16",
+                          cache=hg.CacheConfig(blk_num=4, blk_size=32, beta=1.0), core_count=64, max_positions=1024)
+    single = hg.HybridEngine(cfg)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    ref = []
+    for _ in range(steps):
+        qq = torch.randn((2, 8, 1, 128), generator=g, device="cuda").to(torch.bfloat16)
+        kk = torch.randn((2, 2, 1, 128), generator=g, device="cuda").to(torch.bfloat16)
+        o, _, _ = single.decode_device(0, qq, kk, -kk)
+        ref.append(o.cpu().numpy().copy())
+    ref = np.stack(ref)
+    np.testing.assert_array_equal(res[0][0], res[1][0])
+    assert np.abs(res[0][0] - ref).max() / np.abs(ref).max() <= 1e-2
