@@ -251,7 +251,19 @@ typedef struct hgca_decode_desc {
   uint64_t epoch;
   uint32_t* push_cnt;
   int64_t item_target;      /* item_target of hgca_union_build_items (0: fixed sparse_rows items) */
+  /* Graph mode (optional, NULL = off): a device int64[4] step state
+   * {dlo, dhi, epoch, 0} (hgca_step_state_set). When set, both kernels read
+   * the window range [dlo, dhi) (and the push epoch) from it at run time --
+   * dlo / dhi / w_old / epoch above are only validated (dhi - dlo <= dsc_ld)
+   * -- and the merge kernel advances dhi and epoch by one after the step, so
+   * one captured launch sequence (CUDA graph) replays step after step. The
+   * caller re-sets the state when the window moves otherwise (eviction). */
+  int64_t* state;
 } hgca_decode_desc;
+
+/* Graph mode: state[0..3] = {dlo, dhi, epoch, 0}, in stream order (one tiny
+ * kernel, so it can be captured too). */
+int hgca_step_state_set(int64_t* state, int64_t dlo, int64_t dhi, uint64_t epoch, hgca_stream_t stream);
 
 /* One decode step = two kernels on `stream`: the decode kernel (dense items =
  * window parts of hgca_item_rows(dtype)[0] rows, sparse items = union slices

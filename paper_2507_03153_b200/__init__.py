@@ -13,7 +13,7 @@ from .backends import CUDA, install
 from .kv_cache import CacheConfig, KvBlock, WindowCache, offload
 from .sparsifier import (ContextCache, HeadGroupTask, StoreTier, pack_head_groups, renormalize, select_salient,
                          select_topk)
-from .engine import EngineConfig, HybridEngine, LayerState, StepInput, StepOutput, run_sequence
+from .engine import DecodeGraph, EngineConfig, HybridEngine, LayerState, StepInput, StepOutput, run_sequence
 from .sharded import ShardedHybridEngine, packed_stride, shard_owner
 from .workload import Workload, WorkloadSpec, gen_workload_device, load_workload, save_workload
 from . import _lib

@@ -43,6 +43,7 @@ class DecodeDesc(ctypes.Structure):
         ("push_n", ctypes.c_int32), ("push_sparse", ctypes.c_int32),
         ("push_dst", P * 8), ("push_flag", P * 8), ("epoch", ctypes.c_uint64), ("push_cnt", P),
         ("item_target", I64),
+        ("state", P),
     ]
 
 
@@ -78,6 +79,7 @@ _SIGS = {
     "hgca_union_build": [P, I64, I64, I64, I64, I64, I64, P, P, P, P, I64, I32, P],
     "hgca_union_build_items": [P, I64, I64, I64, I64, I64, I64, P, P, P, P, I64, I64, I64, I32, P],
     "hgca_decode_step": [ctypes.POINTER(DecodeDesc), P],
+    "hgca_step_state_set": [P, I64, I64, ctypes.c_uint64, P],
     "hgca_decode_step_host": [ctypes.POINTER(DecodeDesc), P, P, I64, P, P, I64, P],
     "hgca_append_ws_bytes": [I64, I64, I64, I64, I64, I64, I64],
     "hgca_append_bf16": [P, I64, I64, I64, I64, I64, P, I64, D, I64, I64, P, P, P, P, P, I64, P],

@@ -432,10 +432,13 @@ static int decode_prepare(const hgca_decode_desc* d, DecodeArgs& a, DecodeMergeA
   const int64_t W = d->dhi - d->dlo;
   if (d->dlo < 0 || W < 1 || d->dhi > d->T || d->w_old < 0 || d->w_old > W || d->dsc_ld < W)
     return fail(HGCA_EINVAL, "decode_step: bad dense range");
+  // graph mode: the range comes from the device state at run time; size the
+  // item capacity check for the largest window the scratch allows
+  const int64_t Wcap = d->state ? d->dsc_ld : W;
   if (d->sparse_rows < 16 || d->sparse_rows % 16)
     return fail(HGCA_EINVAL, "decode_step: sparse_rows must be a positive multiple of 16");
   const int64_t DR = dense_rows_of(d->dtype);
-  const int64_t Sd = (W + DR - 1) / DR;  // dense items (window parts) per (batch, kv-head)
+  const int64_t Sd = (Wcap + DR - 1) / DR;  // dense items (window parts) per (batch, kv-head)
   const int64_t n_dense = d->B * d->Hkv * Sd;
   // every item but the last full and last tail item of a list holds >= sparse_rows/4 rows; adaptive
   // items (hgca_union_build_items, rows >= union / item_target): <= 5/3 item_target + 5 per list
@@ -470,6 +473,7 @@ static int decode_prepare(const hgca_decode_desc* d, DecodeArgs& a, DecodeMergeA
   a.maw = d->maw;
   a.one_minus_alpha = 1.0 - d->alpha; a.alpha = d->alpha;
   a.wts_out = d->wts_out;
+  a.state = d->state;
   m = DecodeMergeArgs{};
   m.B = d->B; m.Hq = d->Hq; m.Hkv = d->Hkv; m.G = G; m.D = d->D;
   m.n_dense_items = n_dense; m.item_off = d->item_off;
@@ -555,6 +559,11 @@ int hgca_decode_step_host(const hgca_decode_desc* d, const void* in_host, void* 
     if (rc) return rc;
   }
   return cuda_status((int)cudaStreamSynchronize(s), "decode_step_host: sync");
+}
+
+int hgca_step_state_set(int64_t* state, int64_t dlo, int64_t dhi, uint64_t epoch, hgca_stream_t stream) {
+  if (!state || dlo < 0 || dhi <= dlo) return fail(HGCA_EINVAL, "step_state_set: bad state or range");
+  return cuda_status(launch_step_state_set(state, dlo, dhi, epoch, S(stream)), "step_state_set");
 }
 
 int hgca_decode_step(const hgca_decode_desc* d, hgca_stream_t stream) {

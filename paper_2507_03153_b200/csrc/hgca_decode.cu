@@ -77,6 +77,38 @@ struct StageDesc {
   int first, last, dense, pad;
 };
 
+// ------------------------------------------------------------------ step positions
+// The step's window range: from the descriptor (eager launches), or -- when
+// a.state is set (graph-replayable steps, hgca_decode_desc.state) -- from the
+// device-resident step state {dlo, dhi, epoch, arrivals}, which the merge
+// kernel advances by one position after every step. Everything derived from
+// the range (dense item count, MAW EMA extent) is computed here, on device.
+struct StepPos {
+  int64_t dlo, dhi, w_old;
+  int W, Sd, nd;  // window + kv_in rows, dense items per (b, kv-head), dense items
+};
+__device__ __forceinline__ int64_t ld_relaxed_i64(const int64_t* p) {
+  int64_t v;
+  asm volatile("ld.relaxed.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ StepPos step_pos(const DecodeArgs& a) {
+  StepPos p;
+  if (a.state) {
+    p.dlo = ld_relaxed_i64(a.state);
+    p.dhi = ld_relaxed_i64(a.state + 1);
+    p.w_old = p.dhi - 1 - p.dlo;  // a decode step adds exactly one entry
+  } else {
+    p.dlo = a.dlo;
+    p.dhi = a.dhi;
+    p.w_old = a.w_old;
+  }
+  p.W = (int)(p.dhi - p.dlo);
+  p.Sd = (p.W + (int)a.dense_rows - 1) / (int)a.dense_rows;
+  p.nd = (int)(a.B * a.Hkv) * p.Sd;
+  return p;
+}
+
 // ------------------------------------------------------------------ work items
 // Item ids: [0, B*Hkv*Sd) dense (bk = id / Sd; window rows of part id % Sd,
 // a.dense_rows each), then the sparse items of item_tab. The cursor walks a warp through items in
@@ -90,8 +122,8 @@ struct Cursor {
 // preset by the caller, no contended atomic before the first gather); every
 // later item is atomicAdd(counter) + nwarps, prefetched while the current
 // item runs.
-__device__ __forceinline__ StageDesc cursor_next_off(Cursor& c, const DecodeArgs& a, int total, int W, int lane,
-                                                     int nwarps) {
+__device__ __forceinline__ StageDesc cursor_next_off(Cursor& c, const DecodeArgs& a, const StepPos& sp, int total,
+                                                     int lane, int nwarps) {
   StageDesc d;
   if (c.item < 0 || c.row >= c.hi) {
     const int it = __shfl_sync(FULL, c.nxt, 0);
@@ -102,14 +134,14 @@ __device__ __forceinline__ StageDesc cursor_next_off(Cursor& c, const DecodeArgs
     }
     c.item = it;
     if (lane == 0) c.nxt = atomicAdd(a.counter, 1) + nwarps;
-    if (it < (int)a.n_dense_items) {
+    if (it < sp.nd) {
       c.dense = 1;
-      c.bk = it / (int)a.Sd;
-      c.lo = (it % (int)a.Sd) * (int)a.dense_rows;
-      c.hi = min(W, c.lo + (int)a.dense_rows);
+      c.bk = it / sp.Sd;
+      c.lo = (it % sp.Sd) * (int)a.dense_rows;
+      c.hi = min(sp.W, c.lo + (int)a.dense_rows);
     } else {
       c.dense = 0;
-      const int4 e = __ldg(a.item_tab + (it - (int)a.n_dense_items));
+      const int4 e = __ldg(a.item_tab + (it - sp.nd));
       c.bk = e.x;
       c.lo = e.y;
       c.hi = e.z;
@@ -134,10 +166,10 @@ __device__ __forceinline__ StageDesc cursor_next_off(Cursor& c, const DecodeArgs
 // (generic-proxy stores fenced before the async-proxy TMA read). Rows are
 // stored position-rotated (see rotoff). Every lane writes 16-byte chunks.
 template <int D, bool BF16>
-__device__ __forceinline__ void write_new_row(const DecodeArgs& a, const StageDesc& d, int lane) {
-  if (!a.k_new || !d.dense || d.r0 + d.n != (int)(a.dhi - a.dlo)) return;
+__device__ __forceinline__ void write_new_row(const DecodeArgs& a, const StepPos& sp, const StageDesc& d, int lane) {
+  if (!a.k_new || !d.dense || d.r0 + d.n != sp.W) return;
   constexpr int ROWB = D * (BF16 ? 2 : 4), CH = 2 * ROWB / 16;  // 16-byte chunks of the K|V row pair
-  const int64_t pos = a.dhi - 1;
+  const int64_t pos = sp.dhi - 1;
   unsigned char* dst = reinterpret_cast<unsigned char*>(const_cast<void*>(a.KV)) + ((int64_t)d.bk * a.T + pos) * 2 * ROWB;
   for (int c = lane; c < CH; c += 32) {
     const unsigned char* src = reinterpret_cast<const unsigned char*>(c < CH / 2 ? a.k_new : a.v_new) +
@@ -151,9 +183,9 @@ __device__ __forceinline__ void write_new_row(const DecodeArgs& a, const StageDe
 // Union entry of lane's row of sub-chunk d: position | (query-head mask << 24).
 // Rows past the sub-chunk end get position 0 and an empty mask.
 template <int G>
-__device__ __forceinline__ int32_t sub_entry(const StageDesc& d, const DecodeArgs& a, int lane) {
+__device__ __forceinline__ int32_t sub_entry(const StageDesc& d, const DecodeArgs& a, const StepPos& sp, int lane) {
   if (d.item < 0 || lane >= d.n) return 0;
-  if (d.dense) return (int32_t)(a.dlo + d.r0 + lane) | (int32_t)(((1u << G) - 1u) << 24);
+  if (d.dense) return (int32_t)(sp.dlo + d.r0 + lane) | (int32_t)(((1u << G) - 1u) << 24);
   return __ldg(a.u_ent + (int64_t)d.bk * a.T + d.r0 + lane);
 }
 
@@ -209,28 +241,32 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
   // Everything that does not depend on this step's decode grid is read before
   // griddepcontrol.wait: the item ranges (built at the last selection change)
   // and the window MAW (only this kernel writes it).
-  const int64_t BK = m.B * m.Hkv, nd = m.n_dense_items;
+  // (the step state, in graph mode, was last written by the previous step's
+  // merge, which completed before this step's decode grid passed its wait)
+  const StepPos sp = step_pos(a);
+  const uint64_t epoch = a.state ? (uint64_t)ld_relaxed_i64(a.state + 2) : m.epoch;
+  const int64_t BK = m.B * m.Hkv, nd = sp.nd, Sd = sp.Sd;
   const int64_t o0 = m.item_off[bk], o1 = m.item_off[bk + 1];
   const int64_t t0 = m.item_off[BK + 1 + bk], t1 = m.item_off[BK + 1 + bk + 1];
-  const int64_t nf = o1 - o0, ns = nf + (t1 - t0), n = ns + a.Sd;
+  const int64_t nf = o1 - o0, ns = nf + (t1 - t0), n = ns + Sd;
   auto item_id = [&](int64_t i) {
-    return i < nf ? nd + o0 + i : (i < ns ? nd + t0 + (i - nf) : bk * a.Sd + (i - ns));
+    return i < nf ? nd + o0 + i : (i < ns ? nd + t0 + (i - nf) : bk * Sd + (i - ns));
   };
   const double* pm = m.part_m + g * m.MI;
   const double* pz = m.part_z + g * m.MI;
   const float* pacc = m.part_acc + g * m.MI * D;
   constexpr int EB = 8;  // window entries per thread per epilogue batch (one batch covers 8*D)
   const bool epi = a.maw != nullptr || a.wts_out != nullptr;
-  const int64_t W = a.dhi - a.dlo, n_el = epi ? W : 0;
+  const int64_t W = sp.W, n_el = epi ? W : 0, w_old = sp.w_old;
   const SC* dsc = reinterpret_cast<const SC*>(a.dsc) + bq * a.dsc_ld;
-  double* maw = a.maw ? a.maw + bq * a.T + a.dlo : nullptr;
+  double* maw = a.maw ? a.maw + bq * a.T + sp.dlo : nullptr;
   SC sv[EB];
   double mo[EB];
   auto maw_load = [&](int64_t x0) {
 #pragma unroll
     for (int u = 0; u < EB; ++u) {
       const int64_t j = x0 + u * C::NT + tid;
-      mo[u] = (maw && j < n_el && j < a.w_old) ? maw[j] : 0.0;
+      mo[u] = (maw && j < n_el && j < w_old) ? maw[j] : 0.0;
     }
   };
   auto dsc_load = [&](int64_t x0) {
@@ -252,6 +288,9 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
   __syncthreads();
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   TL(if (tid == 0) g_tlm[blockIdx.x * 8 + 1] = gtimer();)
+  // the next step's decode grid may launch now (it waits for this grid in
+  // its own griddepcontrol.wait before touching anything)
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   // the decode grid is complete: re-arm its work counter for the next step
   if (blockIdx.x == 0 && tid == 0) *a.counter = 0;
   // One fold pass over the concatenated item list [full items, tail items |
@@ -378,7 +417,7 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
           *m.push_cnt = 0;  // re-armed for the next step (stream order)
           __threadfence_system();
           for (int p = 0; p < m.push_n; ++p)
-            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(m.push_flag[p]), "l"(m.epoch) : "memory");
+            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(m.push_flag[p]), "l"(epoch) : "memory");
         }
       }
     }
@@ -407,11 +446,88 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
       if (a.wts_out) a.wts_out[bq * W + j] = w32;
       if (maw) {
         const double aw = (double)w32;
-        maw[j] = j < a.w_old ? __dadd_rn(__dmul_rn(a.one_minus_alpha, mo[u]), __dmul_rn(a.alpha, aw)) : aw;
+        maw[j] = j < w_old ? __dadd_rn(__dmul_rn(a.one_minus_alpha, mo[u]), __dmul_rn(a.alpha, aw)) : aw;
       }
     }
   }
   TL(__syncthreads(); if (tid == 0) g_tlm[blockIdx.x * 8 + 5] = gtimer();)
+  if (a.state) {
+    // graph mode: advance the step state once every CTA has read it (the
+    // last CTA to arrive moves dhi and the exchange epoch forward)
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      unsigned long long* arrivals = reinterpret_cast<unsigned long long*>(a.state + 3);
+      if (atomicAdd(arrivals, 1ull) == (unsigned long long)gridDim.x - 1) {
+        *arrivals = 0;
+        a.state[1] = sp.dhi + 1;
+        a.state[2] = (int64_t)(epoch + 1);
+        __threadfence();
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ producer warp
+// Warp-specialized decode CTAs pair every consumer warp with a producer warp
+// that runs the consumer's work cursor and fills its S-stage ring: per stage
+// the StageDesc + the 32 union entries, kv_in (written before its gather), 8
+// tile::gather4 ops of whole K|V row pairs (L2 evict-first), and the item's
+// query rows with the first stage of an item. The consumer only computes.
+// (A producer costs ~1.1K cycles per stage -- 8 gather4 ops at ~70 cycles
+// each plus the cursor, whose atomic and item-table reads are dependent
+// global loads -- which used to sit on the fp32 kernel's critical path.)
+template <int D, int G, bool BF16, typename C>
+__device__ __forceinline__ void decode_producer(const DecodeArgs& a, const StepPos& sp, unsigned char* cw,
+                                                int first_item, int nwarps, int total, int lane) {
+  constexpr int S = C::S;
+  const uint32_t cw_u = smem_u32(cw);
+  const unsigned char* Qg = reinterpret_cast<const unsigned char*>(a.q);
+  StageDesc* cdesc = reinterpret_cast<StageDesc*>(cw + C::OFF_DESC);
+  int32_t* cmeta = reinterpret_cast<int32_t*>(cw + C::OFF_META);
+  uint64_t* cfull = reinterpret_cast<uint64_t*>(cw + C::OFF_FULL);
+  uint64_t* cempty = reinterpret_cast<uint64_t*>(cw + C::OFF_EMPTY);
+  // static first wave: this producer's first item is its consumer's global
+  // index; later items come from the work counter (cursor_next_off)
+  Cursor cur;
+  cur.nxt = first_item;
+  cur.item = -1;
+  cur.row = cur.hi = cur.lo = cur.bk = cur.dense = 0;
+  StageDesc pend = cursor_next_off(cur, a, sp, total, lane, nwarps);
+  int32_t pend_ent = sub_entry<G>(pend, a, sp, lane);
+  const uint64_t evict_first = l2_evict_first_policy();
+  for (int k = 0;; ++k) {
+    const int s = k % S;
+    if (k >= S) mbar_wait(&cempty[s], ((k / S) - 1) & 1);
+    const StageDesc d = pend;
+    const int32_t ent = pend_ent;
+    if (lane == 0) cdesc[s] = d;
+    cmeta[s * SUB + lane] = ent;
+    __syncwarp();  // desc/meta stores before lane 0's (release) arrive
+    if (d.item < 0) {
+      if (lane == 0) mbar_arrive(&cfull[s]);  // wake the consumer: no more work
+      break;
+    }
+    write_new_row<D, BF16>(a, sp, d, lane);
+    const int pos = ent & 0xffffff;
+    const int rg = lane & 7;  // 4-row group of this lane's gather4 op
+    const int rowbase = d.bk * (int)a.T;
+    const int q0 = __shfl_sync(FULL, pos, rg * 4 + 0);
+    const int q1 = __shfl_sync(FULL, pos, rg * 4 + 1);
+    const int q2 = __shfl_sync(FULL, pos, rg * 4 + 2);
+    const int q3 = __shfl_sync(FULL, pos, rg * 4 + 3);
+    if (lane == 0) mbar_expect_tx(&cfull[s], C::STAGE + (d.first ? C::QB : 0));
+    __syncwarp();
+    if (lane < C::NOPS)
+      tma_gather4_hint(cw_u + s * C::STAGE + rg * 4 * 2 * C::ROWB, &a.kmap, 0, rowbase + q0, rowbase + q1,
+                       rowbase + q2, rowbase + q3, &cfull[s], evict_first);
+    if (lane == 0 && d.first) {
+      const int64_t b = d.bk / a.Hkv, kvh = d.bk % a.Hkv;
+      bulk_g2s(cw + C::OFF_Q + s * C::QSLOT, Qg + (b * a.Hq + kvh * G) * (int64_t)C::ROWB, C::QB, &cfull[s]);
+    }
+    pend = cursor_next_off(cur, a, sp, total, lane, nwarps);
+    pend_ent = sub_entry<G>(pend, a, sp, lane);
+  }
 }
 
 // =========================================================== bf16 (tensor-core) kernel
@@ -421,8 +537,9 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
 // compute. (A producer costs ~1.1K cycles per stage -- 8 gather4 ops at ~70
 // cycles each plus the cursor -- so sharing producers between consumers makes
 // the producers the bottleneck; measured on B200.)
-template <int D, int G, int S, int NPAIR>
+template <int D, int G, int S_, int NPAIR>
 struct Bf16Cfg {
+  static constexpr int S = S_;
   static constexpr int ROWB = D * 2;                    // bytes of one K (or V) row
   static constexpr int STAGE = SUB * 2 * ROWB;          // 32 rotated K|V row pairs
   static constexpr int NOPS = SUB / 4;                  // gather4 ops per stage (whole row pairs)
@@ -465,8 +582,6 @@ __global__ void __launch_bounds__(Bf16Cfg<D, G, S, NPAIR>::NW * 32, 1)
   extern __shared__ unsigned char sm_raw[];
   unsigned char* sm = smem_align1024(sm_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int W = (int)(a.dhi - a.dlo);
-  const int total = (int)(a.n_dense_items + (int64_t)a.item_off[2 * a.B * a.Hkv + 1]);
   if (warp < C::NC) {  // each consumer warp initialises its own ring's barriers
     unsigned char* wsm = sm + warp * C::WARP_SMEM;
     if (lane < S) {
@@ -476,62 +591,20 @@ __global__ void __launch_bounds__(Bf16Cfg<D, G, S, NPAIR>::NW * 32, 1)
     fence_mbar_init();
   }
   __syncthreads();
+  // This grid may have been launched early behind the previous step's merge
+  // (programmatic dependent launch): everything above overlapped its tail;
+  // nothing the previous kernels wrote (step state, union lists, work counter,
+  // queries, partial slots) is read or written before this wait.
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   // let the merge grid launch now: its CTAs take SMs as decode CTAs exit and
   // wait in griddepcontrol.wait until this whole grid has completed
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  const StepPos sp = step_pos(a);
+  const int total = sp.nd + a.item_off[2 * a.B * a.Hkv + 1];
 
   if (warp >= C::NC) {
-    // ================================================================ producer
-    // serves consumer warp (warp - NC): its work cursor, its ring's stages
-    unsigned char* cw = sm + (warp - C::NC) * C::WARP_SMEM;
-    const uint32_t cw_u = smem_u32(cw);
-    const unsigned char* Qg = reinterpret_cast<const unsigned char*>(a.q);
-    StageDesc* cdesc = reinterpret_cast<StageDesc*>(cw + C::OFF_DESC);
-    int32_t* cmeta = reinterpret_cast<int32_t*>(cw + C::OFF_META);
-    uint64_t* cfull = reinterpret_cast<uint64_t*>(cw + C::OFF_FULL);
-    uint64_t* cempty = reinterpret_cast<uint64_t*>(cw + C::OFF_EMPTY);
-    // static first wave: this producer's first item is its consumer's global
-    // index; later items come from the work counter (cursor_next_off)
-    const int nwarps = (int)gridDim.x * C::NC;
-    Cursor cur;
-    cur.nxt = (int)blockIdx.x * C::NC + (warp - C::NC);
-    cur.item = -1;
-    cur.row = cur.hi = cur.lo = cur.bk = cur.dense = 0;
-    StageDesc pend = cursor_next_off(cur, a, total, W, lane, nwarps);
-    int32_t pend_ent = sub_entry<G>(pend, a, lane);
-    const uint64_t evict_first = l2_evict_first_policy();
-    for (int k = 0;; ++k) {
-      const int s = k % S;
-      if (k >= S) mbar_wait(&cempty[s], ((k / S) - 1) & 1);
-      const StageDesc d = pend;
-      const int32_t ent = pend_ent;
-      if (lane == 0) cdesc[s] = d;
-      cmeta[s * SUB + lane] = ent;
-      __syncwarp();  // desc/meta stores before lane 0's (release) arrive
-      if (d.item < 0) {
-        if (lane == 0) mbar_arrive(&cfull[s]);  // wake the consumer: no more work
-        break;
-      }
-      write_new_row<D, true>(a, d, lane);
-      const int pos = ent & 0xffffff;
-      const int rg = lane & 7;  // 4-row group of this lane's gather4 op
-      const int rowbase = d.bk * (int)a.T;
-      const int q0 = __shfl_sync(FULL, pos, rg * 4 + 0);
-      const int q1 = __shfl_sync(FULL, pos, rg * 4 + 1);
-      const int q2 = __shfl_sync(FULL, pos, rg * 4 + 2);
-      const int q3 = __shfl_sync(FULL, pos, rg * 4 + 3);
-      if (lane == 0) mbar_expect_tx(&cfull[s], C::STAGE + (d.first ? C::QB : 0));
-      __syncwarp();
-      if (lane < C::NOPS)
-        tma_gather4_hint(cw_u + s * C::STAGE + rg * 4 * 2 * C::ROWB, &a.kmap, 0, rowbase + q0, rowbase + q1,
-                         rowbase + q2, rowbase + q3, &cfull[s], evict_first);
-      if (lane == 0 && d.first) {
-        const int64_t b = d.bk / a.Hkv, kvh = d.bk % a.Hkv;
-        bulk_g2s(cw + C::OFF_Q + s * C::QSLOT, Qg + (b * a.Hq + kvh * G) * (int64_t)C::ROWB, C::QB, &cfull[s]);
-      }
-      pend = cursor_next_off(cur, a, total, W, lane, nwarps);
-      pend_ent = sub_entry<G>(pend, a, lane);
-    }
+    decode_producer<D, G, true, C>(a, sp, sm + (warp - C::NC) * C::WARP_SMEM,
+                                   (int)blockIdx.x * C::NC + (warp - C::NC), (int)gridDim.x * C::NC, total, lane);
     return;
   }
 
@@ -720,7 +793,12 @@ __global__ void __launch_bounds__(Bf16Cfg<D, G, S, NPAIR>::NW * 32, 1)
 }
 
 // =========================================================== fp32 (reference-exact) kernel
-// Self-issuing warps (one CTA per SM, NC warps, each with its own S-stage ring).
+// Warp-specialized like the bf16 kernel: NC consumer warps, each with its own
+// S-stage ring, and NC producer warps (decode_producer) that run the
+// consumers' cursors and issue their gathers, so the dependent global loads of
+// the cursor (work-counter atomic, item table, union entries) and the TMA
+// issue stay off the consumer's per-stage critical path (a self-issuing warp
+// spent ~2.1K of ~6.8K cycles per stage there at C1).
 // fp32 K|V rows are stored position-rotated like the bf16 ones (16-byte chunk
 // c of position p at (c & ~7) | ((c ^ p) & 7)), so one tile::gather4 op moves
 // four whole 2*D*4-byte row pairs (8 ops per 32-row stage) and both compute
@@ -736,97 +814,69 @@ struct F32Cfg {
   static constexpr int STAGE = SUB * PAIR;
   static constexpr int NOPS = SUB / 4;                  // gather4 ops per stage
   static constexpr int QB = G * ROWB;
+  static constexpr int QSLOT = QB;                      // (a multiple of 128 bytes)
   static constexpr int OFF_Q = S * STAGE;                   // raw queries [S][G][D] f32
-  static constexpr int OFF_QK = OFF_Q + S * QB;             // queries [G][D] fp64
+  static constexpr int OFF_QK = OFF_Q + S * QSLOT;          // queries [G][D] fp64
   static constexpr int OFF_ACC = OFF_QK + G * D * 8;        // P.V accumulators [G][D] fp32
   static constexpr int OFF_META = OFF_ACC + G * D * 4;      // entries [S][32]
   static constexpr int OFF_DESC = OFF_META + S * SUB * 4;
-  static constexpr int OFF_BAR = OFF_DESC + S * 32;
-  static constexpr int WARP_SMEM = (OFF_BAR + S * 8 + 127) / 128 * 128;
+  static constexpr int OFF_FULL = OFF_DESC + S * 32;        // mbarriers: stage landed (TMA tx)
+  static constexpr int OFF_EMPTY = OFF_FULL + S * 8;        // mbarriers: stage consumed
+  static constexpr int WARP_SMEM = (OFF_EMPTY + S * 8 + 127) / 128 * 128;
   static constexpr int NC0 = (SMEM_MAX - 1024) / WARP_SMEM;
-  static constexpr int NC = NC0 > 8 ? 8 : NC0;
+  static constexpr int NC = NC0 > 8 ? 8 : NC0;          // consumer warps
+  static constexpr int NW = 2 * NC;                     // + one producer warp per consumer
   static constexpr int SMEM = NC * WARP_SMEM + 1024;
   static_assert(NC >= 1, "fp32 decode pipeline does not fit shared memory");
   static_assert(D == 64 || D == 128, "fp32 decode: head_dim 64 or 128");
+  static_assert(QB % 128 == 0, "query slot alignment");
 };
 
 template <int D, int G>
-__global__ void __launch_bounds__(F32Cfg<D, G>::NC * 32, 1) decode_f32_kernel(const __grid_constant__ DecodeArgs a) {
+__global__ void __launch_bounds__(F32Cfg<D, G>::NW * 32, 1) decode_f32_kernel(const __grid_constant__ DecodeArgs a) {
   using C = F32Cfg<D, G>;
   extern __shared__ unsigned char sm_raw[];
   unsigned char* sm = smem_align1024(sm_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp < C::NC) {  // each consumer warp initialises its own ring's barriers
+    unsigned char* wsm = sm + warp * C::WARP_SMEM;
+    if (lane < C::S) {
+      mbar_init(reinterpret_cast<uint64_t*>(wsm + C::OFF_FULL) + lane, 1);
+      mbar_init(reinterpret_cast<uint64_t*>(wsm + C::OFF_EMPTY) + lane, 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");               // see decode_bf16_kernel
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  const StepPos sp = step_pos(a);
+  const int total = sp.nd + a.item_off[2 * a.B * a.Hkv + 1];
+  if (warp >= C::NC) {
+    decode_producer<D, G, false, C>(a, sp, sm + (warp - C::NC) * C::WARP_SMEM,
+                                    (int)blockIdx.x * C::NC + (warp - C::NC), (int)gridDim.x * C::NC, total, lane);
+    return;
+  }
+
+  // ================================================================== consumer
   unsigned char* wsm = sm + warp * C::WARP_SMEM;
-  const uint32_t wsm_u = smem_u32(wsm);
   StageDesc* desc = reinterpret_cast<StageDesc*>(wsm + C::OFF_DESC);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(wsm + C::OFF_BAR);
+  uint64_t* full = reinterpret_cast<uint64_t*>(wsm + C::OFF_FULL);
+  uint64_t* empty = reinterpret_cast<uint64_t*>(wsm + C::OFF_EMPTY);
   int32_t* meta = reinterpret_cast<int32_t*>(wsm + C::OFF_META);
   double* qk = reinterpret_cast<double*>(wsm + C::OFF_QK);
   float* accs = reinterpret_cast<float*>(wsm + C::OFF_ACC);
-  const int W = (int)(a.dhi - a.dlo);
-  const int total = (int)(a.n_dense_items + (int64_t)a.item_off[2 * a.B * a.Hkv + 1]);
-  const unsigned char* Qg = reinterpret_cast<const unsigned char*>(a.q);
   TL(unsigned long long* tl = g_tl + ((int64_t)blockIdx.x * C::NC + warp) * TL_SLOTS;
      unsigned long long tl_wait = 0, tl_score = 0, tl_pv = 0, tl_issue = 0, tl_part = 0, tl_sub = 0, tl_items = 0,
                         tl_first = 0;
      if (lane == 0) tl[0] = gtimer(););
-  if (lane < C::S) mbar_init(&bar[lane], 1);
-  fence_mbar_init();
-  __syncwarp();
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // see decode_bf16_kernel
-
-  // first item: this warp's global index (no atomic on the critical path);
-  // later items come from the work counter, offset past the first wave
-  const int nwarps = (int)gridDim.x * C::NC;
-  Cursor cur;
-  cur.nxt = (int)blockIdx.x * C::NC + warp;
-  cur.item = -1;
-  cur.row = cur.hi = cur.lo = cur.bk = cur.dense = 0;
-  StageDesc pend = cursor_next_off(cur, a, total, W, lane, nwarps);
-  int32_t pend_ent = sub_entry<G>(pend, a, lane);
-  const uint64_t evict_first = l2_evict_first_policy();
-
-  auto issue = [&](int s) {
-    const StageDesc d = pend;
-    const int32_t ent = pend_ent;
-    if (lane == 0) desc[s] = d;
-    meta[s * SUB + lane] = ent;
-    if (d.item >= 0) {
-      write_new_row<D, false>(a, d, lane);
-      const int pos = ent & 0xffffff;
-      const int rg = lane & 7;
-      const int rowbase = d.bk * (int)a.T;
-      const int q0 = __shfl_sync(FULL, pos, rg * 4 + 0);
-      const int q1 = __shfl_sync(FULL, pos, rg * 4 + 1);
-      const int q2 = __shfl_sync(FULL, pos, rg * 4 + 2);
-      const int q3 = __shfl_sync(FULL, pos, rg * 4 + 3);
-      if (lane == 0) mbar_expect_tx(&bar[s], C::STAGE + (d.first ? C::QB : 0));
-      __syncwarp();
-      if (lane < C::NOPS)
-        tma_gather4_hint(wsm_u + s * C::STAGE + rg * 4 * C::PAIR, &a.kmap, 0, rowbase + q0, rowbase + q1,
-                         rowbase + q2, rowbase + q3, &bar[s], evict_first);
-      if (lane == 8 && d.first) {
-        const int64_t b = d.bk / a.Hkv, kvh = d.bk % a.Hkv;
-        bulk_g2s(wsm + C::OFF_Q + s * C::QB, Qg + (b * a.Hq + kvh * G) * (int64_t)C::ROWB, C::QB, &bar[s]);
-      }
-    }
-    pend = cursor_next_off(cur, a, total, W, lane, nwarps);
-    pend_ent = sub_entry<G>(pend, a, lane);
-  };
-
-  TL(long long ci0 = clock64();)
-#pragma unroll
-  for (int s = 0; s < C::S; ++s) issue(s);
-  TL(tl_issue += clock64() - ci0;)
 
   double m_run[G], z_run[G];  // running (m, z) of the current item, per head (warp-uniform)
   for (int k = 0;; ++k) {
     const int s = k % C::S;
-    __syncwarp();
+    TL(long long c0 = clock64();)
+    mbar_wait(&full[s], (k / C::S) & 1);
     const StageDesc d = desc[s];
     if (d.item < 0) break;
-    TL(long long c0 = clock64();)
-    mbar_wait(&bar[s], (k / C::S) & 1);
     TL(long long c1 = clock64(); tl_wait += c1 - c0; ++tl_sub; if (!tl_first) tl_first = gtimer();)
     const unsigned char* st = wsm + s * C::STAGE;
     const int32_t myent = meta[s * SUB + lane];
@@ -834,7 +884,7 @@ __global__ void __launch_bounds__(F32Cfg<D, G>::NC * 32, 1) decode_f32_kernel(co
     const uint32_t wq = G == 1 ? 1u : __reduce_or_sync(FULL, qm);
     const int myrot = myent & 7;
     if (d.first) {
-      const float* qr = reinterpret_cast<const float*>(wsm + C::OFF_Q + s * C::QB);
+      const float* qr = reinterpret_cast<const float*>(wsm + C::OFF_Q + s * C::QSLOT);
       for (int t = lane; t < G * D; t += 32) qk[t] = (double)qr[t];
       for (int t = lane; t < G * D; t += 32) accs[t] = 0.f;
 #pragma unroll
@@ -851,8 +901,8 @@ __global__ void __launch_bounds__(F32Cfg<D, G>::NC * 32, 1) decode_f32_kernel(co
     for (int g = 0; g < G; ++g) sacc[g] = 0.0;
     {
       // batches of 16 elements: the 16 loads and fp32 -> fp64 conversions are
-      // issued ahead of the batch's dependent DFMA chain (the chain, ~8
-      // cycles per DFMA, is what bounds a stage)
+      // issued ahead of the batch's dependent DFMA chain (the chain is what
+      // bounds a stage)
       const unsigned char* kr = st + lane * C::PAIR;
 #pragma unroll 2
       for (int c0 = 0; c0 < D / 4; c0 += 4) {
@@ -928,9 +978,10 @@ __global__ void __launch_bounds__(F32Cfg<D, G>::NC * 32, 1) decode_f32_kernel(co
       for (int i = 0; i < C::DPL; ++i) ag[i] = acc[i];
     }
     TL(long long c3 = clock64(); tl_pv += c3 - c2;)
+    __syncwarp();  // every lane's reads of the stage are done
+    if (lane == 0) mbar_arrive(&empty[s]);  // the producer may refill it
     if (d.last) {
       TL(++tl_items;)
-      __syncwarp();
       for (int t = lane; t < G * D; t += 32) a.part_acc[((t / D) * a.m.MI + d.item) * D + t % D] = accs[t];
       if (lane == 0) {
 #pragma unroll
@@ -942,8 +993,6 @@ __global__ void __launch_bounds__(F32Cfg<D, G>::NC * 32, 1) decode_f32_kernel(co
     }
     __syncwarp();
     TL(long long c4 = clock64(); tl_part += c4 - c3;)
-    issue(s);
-    TL(tl_issue += clock64() - c4;)
   }
   TL(if (lane == 0) {
     tl[1] = gtimer(); tl[2] = tl_sub; tl[3] = tl_wait; tl[4] = tl_score; tl[5] = tl_pv; tl[6] = tl_issue;
@@ -1253,20 +1302,35 @@ static int launch_decode_t(const DecodeArgs& a_in, cudaStream_t s) {
                                    [&](CUtensorMap* m) { return make_row_map(m, a.KV, rows, D, BF16); });
     if (rc) return rc;
   }
-  int dev = 0, nsm = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int nsm = sm_count();
   static DevFlags attr;
+  // decode grid: programmatic dependent launch too -- it may start behind the
+  // previous step's merge (launch, barrier init) and waits for it in
+  // griddepcontrol.wait before reading anything
+  cudaLaunchConfig_t dcfg = {};
+  dcfg.gridDim = dim3((unsigned)nsm);
+  dcfg.stream = s;
+  cudaLaunchAttribute dat[1];
+  dat[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  dat[0].val.programmaticStreamSerializationAllowed = 1;
+  dcfg.attrs = dat;
+  dcfg.numAttrs = 1;
   if constexpr (BF16) {
     using C = Bf16Cfg<D, G, HGCA_BF16_STAGES, HGCA_BF16_PAIRS>;
     const int rc = set_smem_dev(decode_bf16_kernel<D, G, HGCA_BF16_STAGES, HGCA_BF16_PAIRS>, C::SMEM, attr);
     if (rc) return rc;
-    decode_bf16_kernel<D, G, HGCA_BF16_STAGES, HGCA_BF16_PAIRS><<<nsm, C::NW * 32, C::SMEM, s>>>(a);
+    dcfg.blockDim = dim3(C::NW * 32);
+    dcfg.dynamicSmemBytes = C::SMEM;
+    const cudaError_t e0 = cudaLaunchKernelEx(&dcfg, decode_bf16_kernel<D, G, HGCA_BF16_STAGES, HGCA_BF16_PAIRS>, a);
+    if (e0 != cudaSuccess) return (int)e0;
   } else {
     using C = F32Cfg<D, G>;
     const int rc = set_smem_dev(decode_f32_kernel<D, G>, C::SMEM, attr);
     if (rc) return rc;
-    decode_f32_kernel<D, G><<<nsm, C::NC * 32, C::SMEM, s>>>(a);
+    dcfg.blockDim = dim3(C::NW * 32);
+    dcfg.dynamicSmemBytes = C::SMEM;
+    const cudaError_t e0 = cudaLaunchKernelEx(&dcfg, decode_f32_kernel<D, G>, a);
+    if (e0 != cudaSuccess) return (int)e0;
   }
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
@@ -1299,6 +1363,18 @@ static int launch_decode_g(const DecodeArgs& a, cudaStream_t s) {
     case 8: return launch_decode_t<BF16, D, 8>(a, s);
   }
   return -1000;
+}
+
+__global__ void step_state_set_kernel(int64_t* state, int64_t dlo, int64_t dhi, uint64_t epoch) {
+  state[0] = dlo;
+  state[1] = dhi;
+  state[2] = (int64_t)epoch;
+  state[3] = 0;
+}
+
+int launch_step_state_set(int64_t* state, int64_t dlo, int64_t dhi, uint64_t epoch, cudaStream_t s) {
+  step_state_set_kernel<<<1, 1, 0, s>>>(state, dlo, dhi, epoch);
+  return (int)cudaGetLastError();
 }
 
 int decode_chunk_rows(int dtype, int64_t D) {

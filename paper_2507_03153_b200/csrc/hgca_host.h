@@ -20,6 +20,19 @@ inline int current_device() {
   return dev;
 }
 
+// SM count of the current device, cached per ordinal (< 64).
+inline int sm_count() {
+  static std::atomic<int> cache[64];
+  const int dev = current_device() & 63;
+  int n = cache[dev].load(std::memory_order_relaxed);
+  if (n <= 0) {
+    n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev].store(n, std::memory_order_relaxed);
+  }
+  return n;
+}
+
 // One bit per device ordinal (< 64): set once the kernel's attribute is set there.
 struct DevFlags {
   std::atomic<uint64_t> bits{0};
@@ -50,15 +63,21 @@ class MapCache {
   template <typename Enc>
   int get(const MapKey& k, CUtensorMap* out, Enc encode) {
     std::lock_guard<std::mutex> lock(mu_);
+    if (last_ < n_ && keys_[last_] == k) {  // the common case: the same layer again
+      *out = maps_[last_];
+      return 0;
+    }
     for (int i = 0; i < n_; ++i)
       if (keys_[i] == k) {
         *out = maps_[i];
+        last_ = i;
         return 0;
       }
     CUtensorMap m;
     const int rc = encode(&m);
     if (rc) return rc;
     const int slot = n_ < kCap ? n_++ : (next_++ % kCap);
+    last_ = slot;
     keys_[slot] = k;
     maps_[slot] = m;
     *out = m;
@@ -70,7 +89,7 @@ class MapCache {
   std::mutex mu_;
   MapKey keys_[kCap];
   CUtensorMap maps_[kCap];
-  int n_ = 0, next_ = 0;
+  int n_ = 0, next_ = 0, last_ = 0;
 };
 
 inline MapKey map_key(int kind, const void* base, int64_t rows, int64_t cols, int64_t box0, int64_t box1) {

@@ -94,6 +94,10 @@ struct DecodeArgs {
   double* maw;            // [B*Hq, T] or nullptr (no MAW maintenance)
   double one_minus_alpha, alpha;
   float* wts_out;         // optional dense weights [B*Hq, dhi - dlo]
+  // graph mode (optional): device step state {dlo, dhi, epoch, arrivals};
+  // when set the kernels take the window range from it (dlo/dhi/w_old above
+  // are ignored) and the merge kernel advances dhi and epoch after the step
+  int64_t* state;
 };
 
 
@@ -121,6 +125,7 @@ int launch_union_build(const uint32_t* sel, int64_t B, int64_t Hq, int64_t Hkv, 
 int launch_write_rows(int dtype, void* KV, int64_t BH, int64_t T, int64_t D, int64_t pos,
                       const void* k_new, const void* v_new, int64_t n, cudaStream_t s);
 int decode_chunk_rows(int dtype, int64_t D);
+int launch_step_state_set(int64_t* state, int64_t dlo, int64_t dhi, uint64_t epoch, cudaStream_t s);
 int64_t append_ws_bytes(int64_t B, int64_t Hq, int64_t Hkv, int64_t D, int64_t nq, int64_t lo, int64_t hi);
 int launch_append_bf16(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, int64_t T, int64_t D, const void* q,
                        int64_t nq, double scale, int64_t lo, int64_t hi, float* out, double* lse, float* mean_archive,

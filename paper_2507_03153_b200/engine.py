@@ -224,6 +224,8 @@ class LayerState:
         self.lo = 0    # archive size
         self.nxt = 0   # next position
         self.desc = None  # cached hgca_decode_desc (engine-owned)
+        self.state = None  # graph mode: device step state {dlo, dhi, epoch, arrivals} (DecodeGraph)
+        self.state_mirror = None  # (dlo, dhi) the device state holds, as far as the host knows
         self.keep = None
         if cfg.shard_world > 1:
             # ownership bits: archive block j (positions [j*blk, (j+1)*blk)) lives on rank j % world
@@ -967,3 +969,75 @@ def run_sequence(config: EngineConfig, workload, on_step=None, collect: bool = F
         if collect:
             outputs.append(per_layer)
     return engine, outputs
+
+
+class DecodeGraph:
+    """Decode steps of `layers` replayed from ONE captured CUDA graph.
+
+    Graph mode of hgca_decode_step (include/hgca_b200.h, desc.state): the
+    window range lives in a device step state per layer that the merge
+    kernel advances after every step, so a single captured launch sequence
+    (decode + merge per layer, chained by programmatic dependent launch)
+    replays step after step; the host only replays the graph and keeps its
+    mirror of the positions. Eviction / ingest (every blk_size steps) runs
+    eagerly between replays, and the state is re-set when the window moved.
+    The queries and kv_in rows are read from fixed device buffers (`q`, `k`,
+    `v`: [B, Hq|Hkv, 1, D] per layer, the storage dtype) that the caller
+    fills before each step; `out` [B*Hq, D] f32 and `lse` [B*Hq] f64 per layer
+    receive the results. Same kernels and results as decode_device."""
+
+    def __init__(self, eng: "HybridEngine", layers=None, q=None, k=None, v=None):
+        if eng.config.keep_weights or eng._push is not None:
+            raise ContractError("DecodeGraph: keep_weights and the push exchange are eager-only")
+        self.eng = eng
+        self.layers = list(range(len(eng.layers))) if layers is None else list(layers)
+        B, Hq, Hkv, D, dev, tdt = eng.B, eng.Hq, eng.Hkv, eng.D, eng.dev, eng.tdtype
+        n = len(self.layers)
+        self.q = q if q is not None else torch.zeros((n, B, Hq, 1, D), dtype=tdt, device=dev)
+        self.k = k if k is not None else torch.zeros((n, B, Hkv, 1, D), dtype=tdt, device=dev)
+        self.v = v if v is not None else torch.zeros((n, B, Hkv, 1, D), dtype=tdt, device=dev)
+        self.out = torch.empty((n, B * Hq, D), dtype=torch.float32, device=dev)
+        self.lse = torch.empty((n, B * Hq), dtype=torch.float64, device=dev)
+        self.descs = []
+        for i, li in enumerate(self.layers):
+            ls = eng.layers[li]
+            if ls.state is None:
+                ls.state = torch.zeros(4, dtype=torch.int64, device=dev)
+            self._sync(ls)
+            d = _lib.DecodeDesc.from_buffer_copy(eng._step_desc(ls, self.q[i].data_ptr(), self.k[i].data_ptr(),
+                                                                self.v[i].data_ptr(), self.out[i].data_ptr(),
+                                                                self.lse[i].data_ptr()))
+            d.state = ls.state.data_ptr()
+            self.descs.append(d)
+        # capture on a side stream (the C launchers read the current stream)
+        torch.cuda.synchronize(dev)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, capture_error_mode="thread_local"):
+            s = eng._stream()
+            for d in self.descs:
+                _lib.call("hgca_decode_step", d, s)
+        torch.cuda.synchronize(dev)
+
+    def _sync(self, ls: LayerState):
+        want = (ls.lo, ls.nxt + 1)
+        if ls.state_mirror != want:
+            _lib.call("hgca_step_state_set", ls.state.data_ptr(), want[0], want[1], 0, self.eng._stream())
+            self.eng.launches += 1
+            ls.state_mirror = want
+
+    def step(self):
+        """One decode step of every captured layer: (out, lse) views."""
+        eng = self.eng
+        for li in self.layers:
+            ls = eng.layers[li]
+            if ls.nxt + 1 > eng.T:
+                raise ContractError("max_positions exceeded")
+            if ls.state_mirror != (ls.lo, ls.nxt + 1):
+                self._sync(ls)
+        self.graph.replay()
+        for li in self.layers:
+            ls = eng.layers[li]
+            lo0 = ls.lo
+            eng._step_done(ls)
+            ls.state_mirror = (lo0, ls.nxt + 1)  # the merge kernel advanced dhi; an eviction moved lo
+        return self.out, self.lse

@@ -30,12 +30,14 @@ CFGS = {
     "C5S": dict(bench.C2, batch=4, context=65536, blk_num=8, frac=0.01),
     # near-empty: batch 1, 8 heads, window 64, archive 64, 1%
     "EMPTY": dict(bench.C2, batch=1, heads=8, kv_heads=8, context=128, blk_num=2, frac=0.01, dtype="float32"),
+    # the same on bf16 storage, GQA 4:1 (the tensor-core kernel)
+    "EMPTYB": dict(bench.C2, batch=1, heads=32, kv_heads=8, context=128, blk_num=2, frac=0.01),
 }
 
 
 def run(name, steps=200, warmup=20):
     cfgd = CFGS[name]
-    eng, g = bench.stage_engine(hg, torch, cfgd, cfgd["context"] + steps + warmup + 64, seed=7)
+    eng, g = bench.stage_engine(hg, torch, cfgd, cfgd["context"] + 2 * (steps + warmup) + 128, seed=7)
     B, Hq, Hkv, D = eng.B, eng.Hq, eng.Hkv, eng.D
     tdt = eng.tdtype
     qs = torch.randn((warmup + steps, B, Hq, 1, D), generator=g, device="cuda").to(tdt)
@@ -65,14 +67,36 @@ def run(name, steps=200, warmup=20):
     torch.cuda.synchronize()
     pair_us = statistics.median(a.elapsed_time(b) for a, b in eng.step_events) * 1e3
     eng.step_events = None
+    # graph mode: one captured decode step replayed back to back (the host
+    # only replays + mirrors positions; evictions run eagerly in between)
+    gr = hg.DecodeGraph(eng, layers=[0])
+    gr.q[0].copy_(qs[0])
+    gr.k[0].copy_(ks[0])
+    gr.v[0].copy_(ks[0])
+    for _ in range(warmup):
+        gr.step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.nvtx.range_push("timed_graph")
+    g0.record()
+    for _ in range(steps):
+        gr.step()
+    g1.record()
+    torch.cuda.nvtx.range_pop()
+    t1 = time.perf_counter()
+    torch.cuda.synchronize()
+    graph_host_us = (t1 - t0) * 1e6 / steps
+    graph_us = g0.elapsed_time(g1) * 1e3 / steps
     ls = eng.layers[0]
     print(json.dumps({"cfg": name, "dtype": cfgd["dtype"], "B": B, "Hq": Hq, "Hkv": Hkv,
                       "window": ls.window_size, "archive": ls.archive_size, "union_rows": int(ls.u_cnt.sum()),
                       "host_issue_us_per_step": round(host_us, 2), "device_us_per_step": round(dev_us, 2),
-                      "pair_us_median": round(pair_us, 2)}), flush=True)
+                      "pair_us_median": round(pair_us, 2), "graph_host_us_per_step": round(graph_host_us, 2),
+                      "graph_device_us_per_step": round(graph_us, 2)}), flush=True)
 
 
 if __name__ == "__main__":
     torch.cuda.set_device(0)
-    for n in (sys.argv[1:] or ["EMPTY", "C1", "C1B", "C5S"]):
+    for n in (sys.argv[1:] or ["EMPTY", "EMPTYB", "C1", "C1B", "C5S"]):
         run(n)
