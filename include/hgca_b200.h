@@ -160,11 +160,13 @@ int hgca_decode_chunk_rows(int dtype, int64_t d);
  * sub-chunk, smem bytes per CTA}. */
 int hgca_decode_config(int dtype, int64_t d, int64_t group, int64_t* out5);
 /* Work-item granularity of hgca_decode_step for a storage dtype: out2 =
- * {window rows per dense item, union rows per sparse item (the sparse_rows to
- * pass to hgca_union_build and the descriptor)}. float32: {64, 64} -- the fp64
- * dot-product kernel's step is set by its longest item; bfloat16: {256, 256} --
- * per-item costs (q load, partial write, merge fold) dominate below that
- * (measured on B200). */
+ * {shortest item (32 rows, one pipeline stage: size the partial buffers for
+ * dense items this short), longest item (the sparse_rows to pass to
+ * hgca_union_build and the descriptor)}: float32 {32, 64}, bfloat16
+ * {32, 256}. hgca_union_build_items with item_target > 0 picks the item size
+ * per union between the two (long items for big steps: per-item q load,
+ * partial write and merge fold; short ones so small steps reach every warp);
+ * the decode kernel cuts the window into dense items of the same size. */
 int hgca_item_rows(int dtype, int64_t* out2);
 /* MAW maintenance from float32 weight rows w [BH, nq, w_ld] (row mean in fp64):
  * mode 0 = window EMA for j < w_old and init for j >= w_old (kv_cache.py:171-187,
@@ -225,7 +227,7 @@ typedef struct hgca_decode_desc {
   double* part_m;           /* [G*max_items] head-major item partials */
   double* part_z;           /* [G*max_items] */
   float* part_acc;          /* [G*max_items*D] */
-  int64_t max_items;        /* >= B*Hkv*(ceil((dhi-dlo)/dense_rows) + 2 + ceil(4T / sparse_rows)), dense_rows from hgca_item_rows */
+  int64_t max_items;        /* >= B*Hkv*(ceil(dsc_ld/32) + 2 + ceil(4T / sparse_rows)) (+ 5/3 item_target + 5*B*Hkv when adaptive) */
   int32_t* counter;         /* int32 work counter (>= 1 element): zero it once before the first step;
                                every step leaves it 0 again */
   double* maw;              /* [B*Hq, T] or NULL */

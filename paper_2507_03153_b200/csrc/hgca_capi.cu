@@ -367,11 +367,16 @@ int hgca_write_rows(int dtype, void* KV, int64_t BH, int64_t T, int64_t d, int64
 int hgca_decode_chunk_rows(int dtype, int64_t d) { return decode_chunk_rows(dtype, d); }
 
 static int64_t dense_rows_of(int dtype) { return dtype == HGCA_DTYPE_F32 ? 64 : 256; }
+// the shortest work item (one 32-row pipeline stage): step-adaptive items
+// (hgca_union_build_items with item_target > 0) never go below it, and the
+// dense items follow the chosen sparse granularity
+static constexpr int64_t kMinItemRows = 32;
 
 int hgca_item_rows(int dtype, int64_t* out2) {
   if (!out2 || (dtype != HGCA_DTYPE_F32 && dtype != HGCA_DTYPE_BF16))
     return fail(HGCA_EINVAL, "item_rows: storage dtype must be float32 or bfloat16");
-  out2[0] = out2[1] = dense_rows_of(dtype);
+  out2[0] = kMinItemRows;         // shortest dense item (capacity of the partial buffers)
+  out2[1] = dense_rows_of(dtype);  // longest item
   return HGCA_OK;
 }
 
@@ -438,7 +443,9 @@ static int decode_prepare(const hgca_decode_desc* d, DecodeArgs& a, DecodeMergeA
   if (d->sparse_rows < 16 || d->sparse_rows % 16)
     return fail(HGCA_EINVAL, "decode_step: sparse_rows must be a positive multiple of 16");
   const int64_t DR = dense_rows_of(d->dtype);
-  const int64_t Sd = (Wcap + DR - 1) / DR;  // dense items (window parts) per (batch, kv-head)
+  // dense items (window parts) per (batch, kv-head): as short as kMinItemRows when the union
+  // rebuild chose short items (the kernels read the chosen size from item_off)
+  const int64_t Sd = (Wcap + kMinItemRows - 1) / kMinItemRows;
   const int64_t n_dense = d->B * d->Hkv * Sd;
   // every item but the last full and last tail item of a list holds >= sparse_rows/4 rows; adaptive
   // items (hgca_union_build_items, rows >= union / item_target): <= 5/3 item_target + 5 per list

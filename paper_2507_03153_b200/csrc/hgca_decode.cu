@@ -85,7 +85,7 @@ struct StageDesc {
 // the range (dense item count, MAW EMA extent) is computed here, on device.
 struct StepPos {
   int64_t dlo, dhi, w_old;
-  int W, Sd, nd;  // window + kv_in rows, dense items per (b, kv-head), dense items
+  int W, dr, Sd, nd;  // window + kv_in rows, rows per dense item, dense items per (b, kv-head), dense items
 };
 __device__ __forceinline__ int64_t ld_relaxed_i64(const int64_t* p) {
   int64_t v;
@@ -104,7 +104,14 @@ __device__ __forceinline__ StepPos step_pos(const DecodeArgs& a) {
     p.w_old = a.w_old;
   }
   p.W = (int)(p.dhi - p.dlo);
-  p.Sd = (p.W + (int)a.dense_rows - 1) / (int)a.dense_rows;
+  // dense items (window parts) follow the sparse item granularity the last
+  // union rebuild chose for this step size (item_offsets_kernel: long items
+  // for big steps, down to one 32-row stage for small ones, so a small step
+  // spreads over every warp instead of one warp walking a 256-row window
+  // part); before any rebuild, the descriptor's default
+  const int chosen = a.item_off[2 * (a.B * a.Hkv + 1)];
+  p.dr = chosen >= 16 && chosen <= (int)a.dense_rows ? chosen : (int)a.dense_rows;
+  p.Sd = (p.W + p.dr - 1) / p.dr;
   p.nd = (int)(a.B * a.Hkv) * p.Sd;
   return p;
 }
@@ -137,8 +144,8 @@ __device__ __forceinline__ StageDesc cursor_next_off(Cursor& c, const DecodeArgs
     if (it < sp.nd) {
       c.dense = 1;
       c.bk = it / sp.Sd;
-      c.lo = (it % sp.Sd) * (int)a.dense_rows;
-      c.hi = min(sp.W, c.lo + (int)a.dense_rows);
+      c.lo = (it % sp.Sd) * sp.dr;
+      c.hi = min(sp.W, c.lo + sp.dr);
     } else {
       c.dense = 0;
       const int4 e = __ldg(a.item_tab + (it - sp.nd));

@@ -46,13 +46,15 @@ __all__ = ["CacheConfig", "EngineConfig", "StepInput", "StepOutput", "LayerState
 MODES = ("decode", "append")
 
 
-# Step-adaptive sparse items (hgca_union_build_items): HGCA_ITEMS_PER_WARP > 0
-# shortens items of small unions to give every decode warp that many items.
-# Measured on B200 (profiles/r02_item_ab.txt): fixed full-length items were
-# fastest even for the small C5 step (29.5 us vs 31-35 us), so it is off by
-# default -- the per-item q load, partial write and fold outweigh the balance.
-MIN_ITEM_ROWS = int(os.environ.get("HGCA_MIN_ITEM_ROWS", "64"))
-ITEMS_PER_WARP = float(os.environ.get("HGCA_ITEMS_PER_WARP", "0"))
+# Step-adaptive work items (hgca_union_build_items): items of small unions are
+# shortened (down to one 32-row stage) to give every decode warp about
+# HGCA_ITEMS_PER_WARP items, and the dense window items follow the same
+# granularity (the decode kernel reads it from item_off); big steps keep
+# 256-row items. (An earlier A/B that shortened only the sparse items showed
+# no gain -- profiles/r02_item_ab.txt: the 256-row dense items stayed the
+# critical path of small steps.)
+MIN_ITEM_ROWS = int(os.environ.get("HGCA_MIN_ITEM_ROWS", "32"))
+ITEMS_PER_WARP = float(os.environ.get("HGCA_ITEMS_PER_WARP", "1"))
 
 
 def item_target(dtype: str, G: int, D: int, dev) -> int:
@@ -972,51 +974,66 @@ def run_sequence(config: EngineConfig, workload, on_step=None, collect: bool = F
 
 
 class DecodeGraph:
-    """Decode steps of `layers` replayed from ONE captured CUDA graph.
+    """`steps` decode steps of `layers` replayed from ONE captured CUDA graph.
 
     Graph mode of hgca_decode_step (include/hgca_b200.h, desc.state): the
     window range lives in a device step state per layer that the merge
-    kernel advances after every step, so a single captured launch sequence
-    (decode + merge per layer, chained by programmatic dependent launch)
-    replays step after step; the host only replays the graph and keeps its
-    mirror of the positions. Eviction / ingest (every blk_size steps) runs
-    eagerly between replays, and the state is re-set when the window moved.
-    The queries and kv_in rows are read from fixed device buffers (`q`, `k`,
-    `v`: [B, Hq|Hkv, 1, D] per layer, the storage dtype) that the caller
-    fills before each step; `out` [B*Hq, D] f32 and `lse` [B*Hq] f64 per layer
-    receive the results. Same kernels and results as decode_device."""
+    kernel advances after every step, so one captured launch sequence --
+    step-major, for every step and layer a decode and a merge kernel, each
+    kernel chained to the previous one by programmatic dependent launch --
+    replays token after token with no host work in between. The host only
+    replays the graph and keeps its mirror of the positions; eviction /
+    ingest (every blk_size steps) runs eagerly between replays, and the
+    state is re-set when the window moved. A replay of `steps` tokens must
+    not cross an eviction before its last step (`room()`).
+    Inputs: fixed device buffers q [steps, L, B, Hq, 1, D], k / v
+    [steps, L, B, Hkv, 1, D] (storage dtype) that the caller fills before a
+    replay (slot [t, l] = token t of the replay, layer l); outputs out
+    [steps, L, B*Hq, D] f32 and lse [steps, L, B*Hq] f64. Same kernels and
+    bit-identical results as decode_device."""
 
-    def __init__(self, eng: "HybridEngine", layers=None, q=None, k=None, v=None):
+    def __init__(self, eng: "HybridEngine", layers=None, steps: int = 1):
         if eng.config.keep_weights or eng._push is not None:
             raise ContractError("DecodeGraph: keep_weights and the push exchange are eager-only")
-        self.eng = eng
+        if steps < 1:
+            raise ContractError("DecodeGraph: steps must be >= 1")
+        self.eng, self.steps = eng, int(steps)
         self.layers = list(range(len(eng.layers))) if layers is None else list(layers)
         B, Hq, Hkv, D, dev, tdt = eng.B, eng.Hq, eng.Hkv, eng.D, eng.dev, eng.tdtype
-        n = len(self.layers)
-        self.q = q if q is not None else torch.zeros((n, B, Hq, 1, D), dtype=tdt, device=dev)
-        self.k = k if k is not None else torch.zeros((n, B, Hkv, 1, D), dtype=tdt, device=dev)
-        self.v = v if v is not None else torch.zeros((n, B, Hkv, 1, D), dtype=tdt, device=dev)
-        self.out = torch.empty((n, B * Hq, D), dtype=torch.float32, device=dev)
-        self.lse = torch.empty((n, B * Hq), dtype=torch.float64, device=dev)
+        n, L = self.steps, len(self.layers)
+        self.q = torch.zeros((n, L, B, Hq, 1, D), dtype=tdt, device=dev)
+        self.k = torch.zeros((n, L, B, Hkv, 1, D), dtype=tdt, device=dev)
+        self.v = torch.zeros((n, L, B, Hkv, 1, D), dtype=tdt, device=dev)
+        self.out = torch.empty((n, L, B * Hq, D), dtype=torch.float32, device=dev)
+        self.lse = torch.empty((n, L, B * Hq), dtype=torch.float64, device=dev)
+        if self.room() < n:
+            raise ContractError(f"DecodeGraph: {n} steps cross an eviction (room {self.room()})")
         self.descs = []
-        for i, li in enumerate(self.layers):
-            ls = eng.layers[li]
-            if ls.state is None:
-                ls.state = torch.zeros(4, dtype=torch.int64, device=dev)
-            self._sync(ls)
-            d = _lib.DecodeDesc.from_buffer_copy(eng._step_desc(ls, self.q[i].data_ptr(), self.k[i].data_ptr(),
-                                                                self.v[i].data_ptr(), self.out[i].data_ptr(),
-                                                                self.lse[i].data_ptr()))
-            d.state = ls.state.data_ptr()
-            self.descs.append(d)
-        # capture on a side stream (the C launchers read the current stream)
+        for t in range(n):
+            for i, li in enumerate(self.layers):
+                ls = eng.layers[li]
+                if ls.state is None:
+                    ls.state = torch.zeros(4, dtype=torch.int64, device=dev)
+                self._sync(ls)
+                d = _lib.DecodeDesc.from_buffer_copy(eng._step_desc(
+                    ls, self.q[t, i].data_ptr(), self.k[t, i].data_ptr(), self.v[t, i].data_ptr(),
+                    self.out[t, i].data_ptr(), self.lse[t, i].data_ptr()))
+                d.state = ls.state.data_ptr()
+                self.descs.append(d)
+        # capture on torch's side stream (the C launchers read the current stream)
         torch.cuda.synchronize(dev)
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph, capture_error_mode="thread_local"):
-            s = eng._stream()
+            st = eng._stream()
             for d in self.descs:
-                _lib.call("hgca_decode_step", d, s)
+                _lib.call("hgca_decode_step", d, st)
         torch.cuda.synchronize(dev)
+
+    def room(self) -> int:
+        """Tokens a replay may decode before an eviction must run (the last
+        of them may trigger one: it is handled after the replay)."""
+        cap = self.eng.cap
+        return min(cap - self.eng.layers[li].window_size for li in self.layers)
 
     def _sync(self, ls: LayerState):
         want = (ls.lo, ls.nxt + 1)
@@ -1026,18 +1043,21 @@ class DecodeGraph:
             ls.state_mirror = want
 
     def step(self):
-        """One decode step of every captured layer: (out, lse) views."""
+        """Replay: `steps` decode steps of every captured layer -> (out, lse)."""
         eng = self.eng
+        if self.room() < self.steps:
+            raise ContractError(f"DecodeGraph: {self.steps} steps would cross an eviction (room {self.room()}); "
+                                f"replay a graph of fewer steps or take eager steps up to the eviction")
         for li in self.layers:
             ls = eng.layers[li]
-            if ls.nxt + 1 > eng.T:
+            if ls.nxt + self.steps > eng.T:
                 raise ContractError("max_positions exceeded")
-            if ls.state_mirror != (ls.lo, ls.nxt + 1):
-                self._sync(ls)
+            self._sync(ls)
         self.graph.replay()
-        for li in self.layers:
-            ls = eng.layers[li]
-            lo0 = ls.lo
-            eng._step_done(ls)
-            ls.state_mirror = (lo0, ls.nxt + 1)  # the merge kernel advanced dhi; an eviction moved lo
+        for t in range(self.steps):
+            for li in self.layers:
+                ls = eng.layers[li]
+                lo0 = ls.lo
+                eng._step_done(ls)
+                ls.state_mirror = (lo0, ls.nxt + 1)  # the merge kernel advanced dhi; an eviction moved lo
         return self.out, self.lse

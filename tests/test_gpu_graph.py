@@ -50,13 +50,13 @@ def test_graph_steps_bit_equal_eager(cuda, dtype, Hq, Hkv):
     gr = cuda.DecodeGraph(eb, layers=[0])
     for t in range(steps):
         oa, la, _ = ea.decode_device(0, q[t], k[t], v[t])
-        gr.q[0].copy_(q[t])
-        gr.k[0].copy_(k[t])
-        gr.v[0].copy_(v[t])
+        gr.q[0, 0].copy_(q[t])
+        gr.k[0, 0].copy_(k[t])
+        gr.v[0, 0].copy_(v[t])
         ob, lb = gr.step()
         torch.cuda.synchronize()
-        assert torch.equal(oa, ob[0]), f"step {t}: graph output differs from eager"
-        assert torch.equal(la, lb[0]), f"step {t}: graph lse differs from eager"
+        assert torch.equal(oa, ob[0, 0]), f"step {t}: graph output differs from eager"
+        assert torch.equal(la, lb[0, 0]), f"step {t}: graph lse differs from eager"
     la_, lb_ = ea.layers[0], eb.layers[0]
     assert (la_.lo, la_.nxt) == (lb_.lo, lb_.nxt) and la_.lo > 200
     assert torch.equal(la_.maw, lb_.maw), "MAW (EMA'd in the merge kernel) differs"
@@ -73,11 +73,11 @@ def test_graph_two_layers_and_mode_switches(cuda):
         ref = [ea.decode_device(li, q[t], k[t], v[t])[:2] for li in range(2)]
         if t % 40 < 30:  # graph steps (both layers in one replay)
             for li in range(2):
-                gr.q[li].copy_(q[t])
-                gr.k[li].copy_(k[t])
-                gr.v[li].copy_(v[t])
+                gr.q[0, li].copy_(q[t])
+                gr.k[0, li].copy_(k[t])
+                gr.v[0, li].copy_(v[t])
             ob, lb = gr.step()
-            got = [(ob[li], lb[li]) for li in range(2)]
+            got = [(ob[0, li], lb[0, li]) for li in range(2)]
         else:  # eager steps on the graph's engine: the device state must re-sync afterwards
             got = [eb.decode_device(li, q[t], k[t], v[t])[:2] for li in range(2)]
         torch.cuda.synchronize()
@@ -86,6 +86,42 @@ def test_graph_two_layers_and_mode_switches(cuda):
                 f"step {t} layer {li} differs"
     for li in range(2):
         assert torch.equal(ea.layers[li].maw, eb.layers[li].maw)
+        assert (ea.layers[li].lo, ea.layers[li].nxt) == (eb.layers[li].lo, eb.layers[li].nxt)
+
+
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16"])
+def test_multi_step_graph_bit_equal_eager(cuda, dtype):
+    """A graph of 8 consecutive steps x 2 layers (16 decode + 16 merge kernels
+    chained by PDL, the state advanced on device between them), replayed up to
+    each eviction; eager steps fill the gaps the graph cannot cover."""
+    (ea, eb), g = _pair(cuda, dtype, layers=2, B=2, Hq=8, Hkv=2)
+    n, steps = 8, 260
+    q, k, v = _inputs(ea, g, steps)
+    gr = cuda.DecodeGraph(eb, steps=n)
+    t = 0
+    replays = 0
+    while t < steps:
+        if gr.room() >= n and t + n <= steps:
+            for j in range(n):
+                for li in range(2):
+                    gr.q[j, li].copy_(q[t + j])
+                    gr.k[j, li].copy_(k[t + j])
+                    gr.v[j, li].copy_(v[t + j])
+            ob, lb = gr.step()
+            replays += 1
+            got = [[(ob[j, li].clone(), lb[j, li].clone()) for li in range(2)] for j in range(n)]
+        else:
+            got = [[eb.decode_device(li, q[t], k[t], v[t])[:2] for li in range(2)]]
+        for j, row in enumerate(got):
+            for li in range(2):
+                oa, la, _ = ea.decode_device(li, q[t + j], k[t + j], v[t + j])
+                torch.cuda.synchronize()
+                assert torch.equal(oa, row[li][0]) and torch.equal(la, row[li][1]), f"token {t + j} layer {li}"
+        t += len(got)
+    assert replays >= 20
+    for li in range(2):
+        assert torch.equal(ea.layers[li].maw, eb.layers[li].maw)
+        assert torch.equal(ea.layers[li].KV, eb.layers[li].KV)
         assert (ea.layers[li].lo, ea.layers[li].nxt) == (eb.layers[li].lo, eb.layers[li].nxt)
 
 

@@ -37,7 +37,7 @@ CFGS = {
 
 def run(name, steps=200, warmup=20):
     cfgd = CFGS[name]
-    eng, g = bench.stage_engine(hg, torch, cfgd, cfgd["context"] + 2 * (steps + warmup) + 128, seed=7)
+    eng, g = bench.stage_engine(hg, torch, cfgd, cfgd["context"] + 2 * (steps + warmup) + 256, seed=7)
     B, Hq, Hkv, D = eng.B, eng.Hq, eng.Hkv, eng.D
     tdt = eng.tdtype
     qs = torch.randn((warmup + steps, B, Hq, 1, D), generator=g, device="cuda").to(tdt)
@@ -67,27 +67,36 @@ def run(name, steps=200, warmup=20):
     torch.cuda.synchronize()
     pair_us = statistics.median(a.elapsed_time(b) for a, b in eng.step_events) * 1e3
     eng.step_events = None
-    # graph mode: one captured decode step replayed back to back (the host
-    # only replays + mirrors positions; evictions run eagerly in between)
-    gr = hg.DecodeGraph(eng, layers=[0])
-    gr.q[0].copy_(qs[0])
-    gr.k[0].copy_(ks[0])
-    gr.v[0].copy_(ks[0])
-    for _ in range(warmup):
-        gr.step()
+    # graph mode: graphs of 16 consecutive steps (kernels chained by PDL, the
+    # step state advanced on device), a 1-step graph for the tokens left
+    # before each eviction; evictions run eagerly between replays
+    g16 = hg.DecodeGraph(eng, layers=[0], steps=16) if eng.cap - eng.layers[0].window_size >= 16 else None
+    g1 = hg.DecodeGraph(eng, layers=[0], steps=1)
+
+    def graph_tokens(n):
+        done = 0
+        while done < n:
+            if g16 is not None and g16.room() >= 16 and n - done >= 16:
+                g16.step()
+                done += 16
+            else:
+                g1.step()
+                done += 1
+        return done
+
+    graph_tokens(warmup)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0, g1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.nvtx.range_push("timed_graph")
     g0.record()
-    for _ in range(steps):
-        gr.step()
-    g1.record()
+    graph_tokens(steps)
+    g1e.record()
     torch.cuda.nvtx.range_pop()
     t1 = time.perf_counter()
     torch.cuda.synchronize()
     graph_host_us = (t1 - t0) * 1e6 / steps
-    graph_us = g0.elapsed_time(g1) * 1e3 / steps
+    graph_us = g0.elapsed_time(g1e) * 1e3 / steps
     ls = eng.layers[0]
     print(json.dumps({"cfg": name, "dtype": cfgd["dtype"], "B": B, "Hq": Hq, "Hkv": Hkv,
                       "window": ls.window_size, "archive": ls.archive_size, "union_rows": int(ls.u_cnt.sum()),
