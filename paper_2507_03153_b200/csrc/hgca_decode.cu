@@ -56,12 +56,22 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #define TL(...) __VA_ARGS__
 __device__ unsigned long long g_tlm[4096 * 8];  // merge kernel: per CTA phase stamps
+// step boundary (graph mode): per decode CTA {entry, wait released, previous
+// merge grid's last CTA end}; the merge CTAs atomicMax their end into g_mend
+__device__ unsigned long long g_gap[1024 * 4];
+__device__ unsigned long long g_mend;
 #else
 #define TL(...)
 #endif
 
 #ifndef HGCA_BF16_STAGES
 #define HGCA_BF16_STAGES 2
+#endif
+#ifndef HGCA_F32_STAGES
+#define HGCA_F32_STAGES 2
+#endif
+#ifndef HGCA_F32_NC
+#define HGCA_F32_NC 8  // consumer warps per CTA cap (shared memory decides below it)
 #endif
 #ifndef HGCA_BF16_PAIRS
 #define HGCA_BF16_PAIRS 6  // consumer warps per CTA, each paired with its own producer warp
@@ -86,6 +96,7 @@ struct StageDesc {
 struct StepPos {
   int64_t dlo, dhi, w_old;
   int W, dr, Sd, nd;  // window + kv_in rows, rows per dense item, dense items per (b, kv-head), dense items
+  int nf;             // full-length sparse items (they come first, see Cursor)
 };
 __device__ __forceinline__ int64_t ld_relaxed_i64(const int64_t* p) {
   int64_t v;
@@ -113,48 +124,44 @@ __device__ __forceinline__ StepPos step_pos(const DecodeArgs& a) {
   p.dr = chosen >= 16 && chosen <= (int)a.dense_rows ? chosen : (int)a.dense_rows;
   p.Sd = (p.W + p.dr - 1) / p.dr;
   p.nd = (int)(a.B * a.Hkv) * p.Sd;
+  p.nf = a.item_off[a.B * a.Hkv];
   return p;
 }
 
 // ------------------------------------------------------------------ work items
-// Item ids: [0, B*Hkv*Sd) dense (bk = id / Sd; window rows of part id % Sd,
-// a.dense_rows each), then the sparse items of item_tab. The cursor walks a warp through items in
-// sub-chunks of SUB rows; lane 0 holds the prefetched id of the next item.
+// Item ids: [0, nf) the full-length sparse items (item_tab[id]), then
+// [nf, nf + nd) the dense items (bk = (id - nf) / Sd; window rows of part
+// (id - nf) % Sd, sp.dr each), then the sparse tail items (item_tab[id - nd]).
+// The full sparse items depend only on the last union rebuild, not on the
+// step's window range, so a warp whose first item is one of them can start
+// gathering it before the previous step's kernels finish (graph mode, see
+// producer_prefetch); the short tail items come last so the step ends
+// balanced. The cursor walks a warp through items in sub-chunks of SUB rows;
+// lane 0 holds the prefetched id of the next item.
 struct Cursor {
   int nxt;  // lane 0
   int item, bk, lo, hi, row, dense;
 };
 
-// Static first wave: a warp's first item is its global warp index (cur.nxt
-// preset by the caller, no contended atomic before the first gather); every
-// later item is atomicAdd(counter) + nwarps, prefetched while the current
-// item runs.
-__device__ __forceinline__ StageDesc cursor_next_off(Cursor& c, const DecodeArgs& a, const StepPos& sp, int total,
-                                                     int lane, int nwarps) {
-  StageDesc d;
-  if (c.item < 0 || c.row >= c.hi) {
-    const int it = __shfl_sync(FULL, c.nxt, 0);
-    if (it >= total) {
-      d.item = -1;
-      d.bk = d.r0 = d.n = d.first = d.last = d.dense = d.pad = 0;
-      return d;
-    }
-    c.item = it;
-    if (lane == 0) c.nxt = atomicAdd(a.counter, 1) + nwarps;
-    if (it < sp.nd) {
-      c.dense = 1;
-      c.bk = it / sp.Sd;
-      c.lo = (it % sp.Sd) * sp.dr;
-      c.hi = min(sp.W, c.lo + sp.dr);
-    } else {
-      c.dense = 0;
-      const int4 e = __ldg(a.item_tab + (it - sp.nd));
-      c.bk = e.x;
-      c.lo = e.y;
-      c.hi = e.z;
-    }
-    c.row = c.lo;
+__device__ __forceinline__ void cursor_item(Cursor& c, const DecodeArgs& a, const StepPos& sp, int it) {
+  c.item = it;
+  if (it >= sp.nf && it < sp.nf + sp.nd) {
+    c.dense = 1;
+    c.bk = (it - sp.nf) / sp.Sd;
+    c.lo = ((it - sp.nf) % sp.Sd) * sp.dr;
+    c.hi = min(sp.W, c.lo + sp.dr);
+  } else {
+    c.dense = 0;
+    const int4 e = __ldg(a.item_tab + (it < sp.nf ? it : it - sp.nd));
+    c.bk = e.x;
+    c.lo = e.y;
+    c.hi = e.z;
   }
+  c.row = c.lo;
+}
+
+__device__ __forceinline__ StageDesc cursor_stage(Cursor& c) {
+  StageDesc d;
   d.item = c.item;
   d.bk = c.bk;
   d.r0 = c.row;
@@ -165,6 +172,26 @@ __device__ __forceinline__ StageDesc cursor_next_off(Cursor& c, const DecodeArgs
   d.pad = 0;
   c.row += SUB;
   return d;
+}
+
+// Static first wave: a warp's first item is its global warp index (cur.nxt
+// preset by the caller, no contended atomic before the first gather); every
+// later item is atomicAdd(counter) + nwarps, prefetched while the current
+// item runs.
+__device__ __forceinline__ StageDesc cursor_next_off(Cursor& c, const DecodeArgs& a, const StepPos& sp, int total,
+                                                     int lane, int nwarps) {
+  if (c.item < 0 || c.row >= c.hi) {
+    const int it = __shfl_sync(FULL, c.nxt, 0);
+    if (it >= total) {
+      StageDesc d;
+      d.item = -1;
+      d.bk = d.r0 = d.n = d.first = d.last = d.dense = d.pad = 0;
+      return d;
+    }
+    if (lane == 0) c.nxt = atomicAdd(a.counter, 1) + nwarps;
+    cursor_item(c, a, sp, it);
+  }
+  return cursor_stage(c);
 }
 
 // kv_in (engine.py:161-163, append_kv kv_cache.py:122-169): the step's new K
@@ -256,8 +283,10 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
   const int64_t o0 = m.item_off[bk], o1 = m.item_off[bk + 1];
   const int64_t t0 = m.item_off[BK + 1 + bk], t1 = m.item_off[BK + 1 + bk + 1];
   const int64_t nf = o1 - o0, ns = nf + (t1 - t0), n = ns + Sd;
+  // item ids (see Cursor): full sparse items [0, NF), dense [NF, NF + nd), tails after
+  const int64_t NF = sp.nf;
   auto item_id = [&](int64_t i) {
-    return i < nf ? nd + o0 + i : (i < ns ? nd + t0 + (i - nf) : bk * Sd + (i - ns));
+    return i < nf ? o0 + i : (i < ns ? nd + t0 + (i - nf) : NF + bk * Sd + (i - ns));
   };
   const double* pm = m.part_m + g * m.MI;
   const double* pz = m.part_z + g * m.MI;
@@ -290,6 +319,41 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
   }
   double acc_s = 0.0, acc_d = 0.0;
   uint32_t phase = 0;
+  // ---- window weights + MAW maintenance from the stored dense scores and
+  // the dense (m, z) (batches of EB entries per thread; batch 0 is loaded
+  // before the folds). Needs only the final dense stats, so it runs inside the
+  // last fold chunk, before that chunk's bulk-copy wait (its latency hides
+  // the copies); with a push exchange pending it runs after the push instead.
+  bool epi_done = false;
+  auto window_epilogue = [&]() {
+    epi_done = true;
+    const double md = hM[1], zd = hZ[1];
+    const bool d_ok = (zd > 0.0) && md != -INFINITY;
+    const double rz = 1.0 / zd;
+    for (int64_t x0 = 0; x0 < n_el; x0 += (int64_t)EB * C::NT) {
+      if (x0) {
+        maw_load(x0);
+        dsc_load(x0);
+      }
+#pragma unroll
+      for (int u = 0; u < EB; ++u) {
+        const int64_t j = x0 + u * C::NT + tid;
+        if (j >= n_el) continue;
+        float w32;
+        if constexpr (sizeof(SC) == 8) {  // fp32 storage: reference-exact fp64 weights (_core.pyx:81-82)
+          w32 = d_ok ? (float)(exp((double)sv[u] - md) / zd) : 0.f;
+        } else {  // bf16 storage: fp32 math (no bit-exactness contract on this path)
+          w32 = d_ok ? __expf((float)sv[u] - (float)md) * (float)rz : 0.f;
+        }
+        if (a.wts_out) a.wts_out[bq * W + j] = w32;
+        if (maw) {
+          const double aw = (double)w32;
+          maw[j] = j < w_old ? __dadd_rn(__dmul_rn(a.one_minus_alpha, mo[u]), __dmul_rn(a.alpha, aw)) : aw;
+        }
+      }
+    }
+  };
+
   // the mbarrier init and the running stats are visible to every warp before
   // any of them folds (griddepcontrol.wait is not a CTA barrier)
   __syncthreads();
@@ -363,6 +427,8 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
     }
     __syncthreads();
     TL(if (tid == 0 && c0 == 0) g_tlm[blockIdx.x * 8 + 7] = gtimer();)
+    if (c1 == n && !m.push_n) window_epilogue();  // dense stats final: overlap the copies
+    TL(if (tid == 0 && c1 == n) g_tlm[blockIdx.x * 8 + 3] = gtimer();)
     mbar_wait(bar, phase);
     phase ^= 1;
     const float* src = sacc + tid;
@@ -382,23 +448,25 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
     if (cn > ce) acc_d = acc_d * hS[1] + dot(ce, cn);
     __syncthreads();  // the next chunk's copies overwrite sacc / sw
   }
-  TL(if (tid == 0) g_tlm[blockIdx.x * 8 + 2] = gtimer(); if (tid == 0) g_tlm[blockIdx.x * 8 + 3] = gtimer();)
+  TL(if (tid == 0) g_tlm[blockIdx.x * 8 + 2] = gtimer();)
   const double Ms = hM[0], Zs = hZ[0], md = hM[1], zd = hZ[1];
   {
+    // merge_states(sparse, dense) (attention.py:153-188) in the equivalent
+    // flash form -- both partials rescaled to M = max(m_s, m_d), one exp
+    // each, one log -- so the dependent fp64 transcendental chain is three
+    // deep instead of five (its latency is the tail of every step); equal to
+    // the reference's lse-space form up to fp64 rounding
     const bool s_empty = !(Zs > 0.0) || Ms == -INFINITY;
-    const double lse_s = s_empty ? -INFINITY : Ms + log(Zs);
     const bool d_empty = !(zd > 0.0) || md == -INFINITY;
-    const double lse_d = d_empty ? -INFINITY : md + log(zd);
-    const double mm = fmax(lse_s, lse_d);
-    const bool both_empty = mm == -INFINITY;
-    const double ms = both_empty ? 0.0 : mm;
-    const double wa = exp(lse_s - ms), wb = exp(lse_d - ms);
-    const double zs = both_empty ? 1.0 : wa + wb;
-    const float ca = (float)(wa / zs), cb = (float)(wb / zs);
-    const float os = s_empty ? 0.f : (float)(acc_s / Zs);
-    const float od = d_empty ? 0.f : (float)(acc_d / zd);
-    const float ov = __fadd_rn(__fmul_rn(ca, os), __fmul_rn(cb, od));
-    const double lv = both_empty ? -INFINITY : ms + log(zs);
+    const double M = fmax(s_empty ? -INFINITY : Ms, d_empty ? -INFINITY : md);
+    const bool both_empty = M == -INFINITY;
+    const double es = s_empty ? 0.0 : exp(Ms - M), ed = d_empty ? 0.0 : exp(md - M);
+    const double Zt = both_empty ? 1.0 : fma(Zs, es, zd * ed);
+    const float ov = both_empty ? 0.f : (float)(fma(acc_s, es, acc_d * ed) / Zt);
+    const double lv = both_empty ? -INFINITY : M + log(Zt);
+    const bool want_s = m.out_sparse || m.lse_sparse || (m.push_n && m.push_sparse);
+    const double lse_s = (want_s && !s_empty) ? Ms + log(Zs) : -INFINITY;
+    const float os = (want_s && !s_empty) ? (float)(acc_s / Zs) : 0.f;
     m.out[bq * D + tid] = ov;
     if (m.out_sparse) m.out_sparse[bq * D + tid] = os;
     if (tid == 0) {
@@ -430,46 +498,24 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
     }
   }
   TL(if (tid == 0) g_tlm[blockIdx.x * 8 + 4] = gtimer();)
-  // ---- window weights + MAW maintenance from the stored dense scores
-  // (batches of EB entries per thread; batch 0 was loaded before the folds)
-  if (n == 0) dsc_load(0);  // (no fold chunk ran)
-  const bool d_ok = (zd > 0.0) && md != -INFINITY;
-  const double rz = 1.0 / zd;
-  for (int64_t x0 = 0; x0 < n_el; x0 += (int64_t)EB * C::NT) {
-    if (x0) {
-      maw_load(x0);
-      dsc_load(x0);
-    }
-#pragma unroll
-    for (int u = 0; u < EB; ++u) {
-      const int64_t j = x0 + u * C::NT + tid;
-      if (j >= n_el) continue;
-      float w32;
-      if constexpr (sizeof(SC) == 8) {  // fp32 storage: reference-exact fp64 weights (_core.pyx:81-82)
-        w32 = d_ok ? (float)(exp((double)sv[u] - md) / zd) : 0.f;
-      } else {  // bf16 storage: fp32 math (no bit-exactness contract on this path)
-        w32 = d_ok ? __expf((float)sv[u] - (float)md) * (float)rz : 0.f;
-      }
-      if (a.wts_out) a.wts_out[bq * W + j] = w32;
-      if (maw) {
-        const double aw = (double)w32;
-        maw[j] = j < w_old ? __dadd_rn(__dmul_rn(a.one_minus_alpha, mo[u]), __dmul_rn(a.alpha, aw)) : aw;
-      }
-    }
+  if (!epi_done) {
+    if (n == 0) dsc_load(0);  // (no fold chunk ran)
+    window_epilogue();
   }
-  TL(__syncthreads(); if (tid == 0) g_tlm[blockIdx.x * 8 + 5] = gtimer();)
+  TL(__syncthreads(); if (tid == 0) { g_tlm[blockIdx.x * 8 + 5] = gtimer(); atomicMax(&g_mend, gtimer()); })
   if (a.state) {
     // graph mode: advance the step state once every CTA has read it (the
-    // last CTA to arrive moves dhi and the exchange epoch forward)
+    // last CTA to arrive moves dhi and the exchange epoch forward). Every
+    // thread consumed its state loads at the top of the kernel, so the
+    // arrival needs no fence; the next kernel reads the state after this
+    // grid completes (griddepcontrol.wait), which orders the stores.
     __syncthreads();
     if (tid == 0) {
-      __threadfence();
       unsigned long long* arrivals = reinterpret_cast<unsigned long long*>(a.state + 3);
       if (atomicAdd(arrivals, 1ull) == (unsigned long long)gridDim.x - 1) {
         *arrivals = 0;
         a.state[1] = sp.dhi + 1;
         a.state[2] = (int64_t)(epoch + 1);
-        __threadfence();
       }
     }
   }
@@ -484,9 +530,17 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
 // (A producer costs ~1.1K cycles per stage -- 8 gather4 ops at ~70 cycles
 // each plus the cursor, whose atomic and item-table reads are dependent
 // global loads -- which used to sit on the fp32 kernel's critical path.)
+//
+// Producers run ahead of the programmatic-launch wait: in graph mode
+// (a.state) a producer whose first item is a full sparse item (rebuild-time
+// data only: item table, union entries, archive rows -- nothing the previous
+// step's kernels write, and a graph replay starts after all earlier stream
+// work) issues that item's first gathers while the previous step's merge
+// still runs; the item's queries, the work counter and everything that
+// depends on the step's window wait for griddepcontrol.wait.
 template <int D, int G, bool BF16, typename C>
-__device__ __forceinline__ void decode_producer(const DecodeArgs& a, const StepPos& sp, unsigned char* cw,
-                                                int first_item, int nwarps, int total, int lane) {
+__device__ __forceinline__ void decode_producer(const DecodeArgs& a, unsigned char* cw, int first_item, int nwarps,
+                                                int lane) {
   constexpr int S = C::S;
   const uint32_t cw_u = smem_u32(cw);
   const unsigned char* Qg = reinterpret_cast<const unsigned char*>(a.q);
@@ -500,22 +554,8 @@ __device__ __forceinline__ void decode_producer(const DecodeArgs& a, const StepP
   cur.nxt = first_item;
   cur.item = -1;
   cur.row = cur.hi = cur.lo = cur.bk = cur.dense = 0;
-  StageDesc pend = cursor_next_off(cur, a, sp, total, lane, nwarps);
-  int32_t pend_ent = sub_entry<G>(pend, a, sp, lane);
   const uint64_t evict_first = l2_evict_first_policy();
-  for (int k = 0;; ++k) {
-    const int s = k % S;
-    if (k >= S) mbar_wait(&cempty[s], ((k / S) - 1) & 1);
-    const StageDesc d = pend;
-    const int32_t ent = pend_ent;
-    if (lane == 0) cdesc[s] = d;
-    cmeta[s * SUB + lane] = ent;
-    __syncwarp();  // desc/meta stores before lane 0's (release) arrive
-    if (d.item < 0) {
-      if (lane == 0) mbar_arrive(&cfull[s]);  // wake the consumer: no more work
-      break;
-    }
-    write_new_row<D, BF16>(a, sp, d, lane);
+  auto issue_gathers = [&](int s, const StageDesc& d, int32_t ent) {
     const int pos = ent & 0xffffff;
     const int rg = lane & 7;  // 4-row group of this lane's gather4 op
     const int rowbase = d.bk * (int)a.T;
@@ -528,10 +568,56 @@ __device__ __forceinline__ void decode_producer(const DecodeArgs& a, const StepP
     if (lane < C::NOPS)
       tma_gather4_hint(cw_u + s * C::STAGE + rg * 4 * 2 * C::ROWB, &a.kmap, 0, rowbase + q0, rowbase + q1,
                        rowbase + q2, rowbase + q3, &cfull[s], evict_first);
+  };
+  auto issue_q = [&](int s, const StageDesc& d) {
     if (lane == 0 && d.first) {
       const int64_t b = d.bk / a.Hkv, kvh = d.bk % a.Hkv;
       bulk_g2s(cw + C::OFF_Q + s * C::QSLOT, Qg + (b * a.Hq + kvh * G) * (int64_t)C::ROWB, C::QB, &cfull[s]);
     }
+  };
+  bool pre = false;
+  StageDesc pend;
+  int32_t pend_ent = 0;
+  if (a.state) {
+    StepPos sp0;  // only nf matters for a full sparse item
+    sp0.nf = a.item_off[a.B * a.Hkv];
+    sp0.nd = 0;
+    if (first_item < sp0.nf) {
+      cursor_item(cur, a, sp0, first_item);
+      pend = cursor_stage(cur);
+      pend_ent = lane < pend.n ? __ldg(a.u_ent + (int64_t)pend.bk * a.T + pend.r0 + lane) : 0;
+      if (lane == 0) cdesc[0] = pend;
+      cmeta[lane] = pend_ent;
+      __syncwarp();  // desc/meta stores before lane 0's (release) arrive
+      issue_gathers(0, pend, pend_ent);
+      pre = true;
+    }
+  }
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  const StepPos sp = step_pos(a);
+  const int total = sp.nd + a.item_off[2 * a.B * a.Hkv + 1];
+  if (pre) {
+    issue_q(0, pend);
+    if (lane == 0) cur.nxt = atomicAdd(a.counter, 1) + nwarps;  // the prefetched item's deferred fetch
+  }
+  pend = cursor_next_off(cur, a, sp, total, lane, nwarps);  // (after a prefetched stage: the next one)
+  pend_ent = sub_entry<G>(pend, a, sp, lane);
+  for (int k = pre ? 1 : 0;; ++k) {
+    const int s = k % S;
+    if (k >= S) mbar_wait(&cempty[s], ((k / S) - 1) & 1);
+    const StageDesc d = pend;
+    const int32_t ent = pend_ent;
+    if (lane == 0) cdesc[s] = d;
+    cmeta[s * SUB + lane] = ent;
+    __syncwarp();  // desc/meta stores before lane 0's (release) arrive
+    if (d.item < 0) {
+      if (lane == 0) mbar_arrive(&cfull[s]);  // wake the consumer: no more work
+      break;
+    }
+    write_new_row<D, BF16>(a, sp, d, lane);
+    issue_gathers(s, d, ent);
+    issue_q(s, d);
     pend = cursor_next_off(cur, a, sp, total, lane, nwarps);
     pend_ent = sub_entry<G>(pend, a, sp, lane);
   }
@@ -597,23 +683,25 @@ __global__ void __launch_bounds__(Bf16Cfg<D, G, S, NPAIR>::NW * 32, 1)
     }
     fence_mbar_init();
   }
+  TL(const unsigned long long tl_entry = gtimer();)
   __syncthreads();
+  if (warp >= C::NC) {  // producers: their own programmatic-launch wait (decode_producer)
+    decode_producer<D, G, true, C>(a, sm + (warp - C::NC) * C::WARP_SMEM, (int)blockIdx.x * C::NC + (warp - C::NC),
+                                   (int)gridDim.x * C::NC, lane);
+    return;
+  }
   // This grid may have been launched early behind the previous step's merge
   // (programmatic dependent launch): everything above overlapped its tail;
   // nothing the previous kernels wrote (step state, union lists, work counter,
   // queries, partial slots) is read or written before this wait.
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  TL(if (threadIdx.x == 0) {
+    g_gap[blockIdx.x * 4 + 0] = tl_entry; g_gap[blockIdx.x * 4 + 1] = gtimer();
+    g_gap[blockIdx.x * 4 + 2] = *(volatile unsigned long long*)&g_mend;
+  })
   // let the merge grid launch now: its CTAs take SMs as decode CTAs exit and
   // wait in griddepcontrol.wait until this whole grid has completed
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-  const StepPos sp = step_pos(a);
-  const int total = sp.nd + a.item_off[2 * a.B * a.Hkv + 1];
-
-  if (warp >= C::NC) {
-    decode_producer<D, G, true, C>(a, sp, sm + (warp - C::NC) * C::WARP_SMEM,
-                                   (int)blockIdx.x * C::NC + (warp - C::NC), (int)gridDim.x * C::NC, total, lane);
-    return;
-  }
 
   // ================================================================== consumer
   unsigned char* wsm = sm + warp * C::WARP_SMEM;
@@ -817,7 +905,7 @@ struct F32Cfg {
   static constexpr int ROWB = D * 4;                    // bytes of one K (or V) row
   static constexpr int PAIR = 2 * ROWB;                 // one rotated K|V row pair
   static constexpr int DPL = D / 32;                    // head dims per lane in P.V
-  static constexpr int S = 2;
+  static constexpr int S = HGCA_F32_STAGES;
   static constexpr int STAGE = SUB * PAIR;
   static constexpr int NOPS = SUB / 4;                  // gather4 ops per stage
   static constexpr int QB = G * ROWB;
@@ -831,7 +919,7 @@ struct F32Cfg {
   static constexpr int OFF_EMPTY = OFF_FULL + S * 8;        // mbarriers: stage consumed
   static constexpr int WARP_SMEM = (OFF_EMPTY + S * 8 + 127) / 128 * 128;
   static constexpr int NC0 = (SMEM_MAX - 1024) / WARP_SMEM;
-  static constexpr int NC = NC0 > 8 ? 8 : NC0;          // consumer warps
+  static constexpr int NC = NC0 > HGCA_F32_NC ? HGCA_F32_NC : NC0;  // consumer warps
   static constexpr int NW = 2 * NC;                     // + one producer warp per consumer
   static constexpr int SMEM = NC * WARP_SMEM + 1024;
   static_assert(NC >= 1, "fp32 decode pipeline does not fit shared memory");
@@ -853,16 +941,19 @@ __global__ void __launch_bounds__(F32Cfg<D, G>::NW * 32, 1) decode_f32_kernel(co
     }
     fence_mbar_init();
   }
+  TL(const unsigned long long tl_entry = gtimer();)
   __syncthreads();
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");               // see decode_bf16_kernel
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-  const StepPos sp = step_pos(a);
-  const int total = sp.nd + a.item_off[2 * a.B * a.Hkv + 1];
-  if (warp >= C::NC) {
-    decode_producer<D, G, false, C>(a, sp, sm + (warp - C::NC) * C::WARP_SMEM,
-                                    (int)blockIdx.x * C::NC + (warp - C::NC), (int)gridDim.x * C::NC, total, lane);
+  if (warp >= C::NC) {  // producers: their own programmatic-launch wait (decode_producer)
+    decode_producer<D, G, false, C>(a, sm + (warp - C::NC) * C::WARP_SMEM, (int)blockIdx.x * C::NC + (warp - C::NC),
+                                    (int)gridDim.x * C::NC, lane);
     return;
   }
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");               // see decode_bf16_kernel
+  TL(if (threadIdx.x == 0) {
+    g_gap[blockIdx.x * 4 + 0] = tl_entry; g_gap[blockIdx.x * 4 + 1] = gtimer();
+    g_gap[blockIdx.x * 4 + 2] = *(volatile unsigned long long*)&g_mend;
+  })
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 
   // ================================================================== consumer
   unsigned char* wsm = sm + warp * C::WARP_SMEM;
@@ -1468,6 +1559,9 @@ int decode_config(int dtype, int64_t D, int64_t G, int64_t* o) {
 }  // namespace hgca
 
 #ifdef HGCA_TIMELINE
+extern "C" int hgca_debug_gaps(void* host) {
+  return (int)cudaMemcpyFromSymbol(host, hgca::g_gap, sizeof(hgca::g_gap));
+}
 extern "C" int hgca_debug_timeline_merge(void* host) {
   return (int)cudaMemcpyFromSymbol(host, hgca::g_tlm, sizeof(hgca::g_tlm));
 }
