@@ -202,6 +202,44 @@ def step_bytes(eng, W_avg, U_avg, n_items):
     return dense + sparse + idx + q + out + maw, dense, sparse, overhead
 
 
+def graph_time(hg, torch, eng, steps, chunk=16):
+    """Graph mode (hg.DecodeGraph, the engine's public replay API): `steps`
+    decode steps of every layer replayed from captured graphs of `chunk` (or
+    1) steps -- kernels chained by programmatic dependent launch, the window
+    advanced on device -- with the evictions (ingest + union rebuild) run
+    eagerly between replays, inside the timed region. Returns ms per step
+    (CUDA events on the engine's stream around the whole run)."""
+    room0 = min(eng.cap - ls.window_size for ls in eng.layers)
+    gc = hg.DecodeGraph(eng, steps=min(chunk, room0)) if room0 >= 2 else None
+    g1 = hg.DecodeGraph(eng, steps=1)
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    for gr in (gc, g1):
+        if gr is not None:
+            for t in (gr.q, gr.k, gr.v):
+                t.copy_(torch.randn(t.shape, generator=gen, device="cuda").to(t.dtype))
+
+    def run(n):
+        done = 0
+        while done < n:
+            if gc is not None and gc.room() >= gc.steps and n - done >= gc.steps:
+                gc.step()
+                done += gc.steps
+            else:
+                g1.step()
+                done += 1
+
+    run(min(steps, 8))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.nvtx.range_push("timed_graph")
+    e0.record()
+    run(steps)
+    e1.record()
+    torch.cuda.nvtx.range_pop()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
 def measure(hg, torch, np, cfgd, K, Wm, e2e_steps, rank, world, dist, seq, exchange):
     """Stage cfgd, time K decode steps (device, CUDA events) and e2e_steps
     host-buffer steps; returns the raw numbers (max over ranks)."""
@@ -210,7 +248,7 @@ def measure(hg, torch, np, cfgd, K, Wm, e2e_steps, rank, world, dist, seq, excha
     # place the window so that the middle timed step evicts a block (ingest +
     # union rebuild inside the timed region): steps j with j = r (mod blk) evict
     r = (Wm + K // 2) % blk
-    max_positions = cfgd["context"] + Wm + K + e2e_steps + 64
+    max_positions = cfgd["context"] + Wm + 2 * K + e2e_steps + 96
     eng, g = stage_engine(hg, torch, cfgd, max_positions, seed=1234 if seq else 1234 + rank, sharded=seq,
                           exchange=exchange, window=cap - 1 - r)
     B, Hq, Hkv, D = eng.B, eng.Hq, eng.Hkv, eng.D
@@ -269,6 +307,8 @@ def measure(hg, torch, np, cfgd, K, Wm, e2e_steps, rank, world, dist, seq, excha
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_max = float(t)
+    # ---- the same workload replayed from CUDA graphs (single GPU: DecodeGraph)
+    graph_ms = graph_time(hg, torch, eng, K) if world == 1 else None
     # ---- e2e through the public API with HOST buffers: one pinned H2D copy of
     # q|k|v in, the step, one D2H copy of out|lse back, synchronize -- every step
     nin = B * (Hq + 2 * Hkv) * D
@@ -303,7 +343,7 @@ def measure(hg, torch, np, cfgd, K, Wm, e2e_steps, rank, world, dist, seq, excha
                e2e_ms=e2e_ms, launches=launches, evictions=evictions, bytes=sbytes, dense=dense_b,
                sparse=sparse_b, overhead=overhead_b, W_avg=W_avg, U_avg=U_avg, t_wall=(t_wall0, t_wall1),
                h2d=int(in_h.numel() * in_h.element_size()), d2h=int(out_h.numel()), exchange_note=exchange_note,
-               xchg=getattr(eng, "xchg", None) is not None)
+               xchg=getattr(eng, "xchg", None) is not None, graph_ms=graph_ms)
     del eng
     torch.cuda.empty_cache()
     return res
@@ -402,6 +442,12 @@ def run_ours(args, rank, world):
                     "h2d_bytes_per_step": m["h2d"], "d2h_bytes_per_step": m["d2h"],
                     "api": "HybridEngine.decode_host_packed (pinned host q|k|v in, out|lse back, sync)"},
             "gpu_launches": m["launches"],
+            "graph": None if m["graph_ms"] is None else {
+                "value": round(units / (m["graph_ms"] * 1e-3), 1), "unit": "tokens/s",
+                "ms_per_step": round(m["graph_ms"], 5), "steps": K,
+                "frac_of_step": round(m["bytes"] / (m["graph_ms"] * 1e-3) / 1e9 / peak, 4),
+                "api": "DecodeGraph: 16-step CUDA-graph replays (PDL-chained kernels, window advanced on device), "
+                       "evictions eager between replays, timed with CUDA events"},
             "clocks": clocks.summary(m["t_wall"][0] - 1.0, (c2 or m)["t_wall"][1]),
             "cpu_baseline": cpu,
         }
@@ -414,6 +460,7 @@ def run_ours(args, rank, world):
                             "roofline_achieved_gbs": round(a2, 1), "roofline_frac": round(a2 / peak, 4),
                             "kernel_ms": round(c2["pair_ms"], 5), "bytes_per_launch": int(c2["bytes"]),
                             "e2e_value": round(c2["B"] / (c2["e2e_ms"] * 1e-3), 1),
+                            "graph_value": round(c2["B"] / (c2["graph_ms"] * 1e-3), 1),
                             "evictions_in_timed_steps": c2["evictions"], "gpu_launches": c2["launches"]}
     if dist:
         dist.destroy_process_group()
