@@ -409,11 +409,23 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&sfull[b], 1);
-      mbar_init(&pfull[b], 4);  // one arrive per softmax warp
+      mbar_init(&pfull[b], (int)((a.RG + 31) / 32));  // one arrive per softmax warp that owns rows
     }
     mbar_init(&pvdone[0], 1);
     mbar_init(&pvdone[1], 1);
     fence_mbar_init();
+  }
+  // Row groups of < 128 rows (e.g. n_q = 16 at G = 4: 64 rows): the softmax
+  // warps of the padding quarters skip the stages entirely; their P rows stay
+  // zero (written once here), so the padding O rows are zero and unused.
+  if (warp >= 2 && warp < 6 && (warp & 3) * 32 >= a.RG) {
+    const int r = (warp & 3) * 32 + lane;
+    unsigned char* prow0 = sm + C::OFF_P + (r >> 3) * 1024 + (r & 7) * 128;
+#pragma unroll
+    for (int bb = 0; bb < 4; ++bb)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) *reinterpret_cast<uint4*>(prow0 + bb * C::PBUF + c * 16) = make_uint4(0, 0, 0, 0);
+    umma::fence_smem_async();
   }
   if (warp == 1) umma::tmem_alloc<C::TMEM_COLS>(smem_u32(tm_holder));
   umma::fence_before_sync();
@@ -487,7 +499,7 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
       }
     }
     __syncwarp();
-  } else {  // ------------------------------------------------------- softmax warps
+  } else if ((warp & 3) * 32 < a.RG) {  // ---------------------------- softmax warps (rows)
     const int quarter = warp & 3;
     const int r = quarter * 32 + lane;          // row of the group == TMEM lane
     const uint32_t tl = (uint32_t)(quarter * 32) << 16;
@@ -932,10 +944,20 @@ __global__ void __launch_bounds__(Tc5MCfg::THREADS, 1) append_tc5_mean_kernel(co
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&sfull[b], 1);
-      mbar_init(&wfull[b], 4);
+      mbar_init(&wfull[b], (int)((a.RG + 31) / 32));  // one arrive per row warp that owns rows
       mbar_init(&mdone[b], 1);
     }
     fence_mbar_init();
+  }
+  // padding quarters (row groups of < 128 rows): their W rows stay zero
+  // (A is zero there too, but 0 * garbage could be NaN) and they skip the stages
+  if (warp >= 2 && warp < 6 && (warp & 3) * 32 >= a.RG) {
+    const int r = (warp & 3) * 32 + lane;
+    unsigned char* wrow0 = sm + C::OFF_W + (r >> 3) * 1024 + (r & 7) * 128;
+#pragma unroll
+    for (int bb = 0; bb < 4; ++bb)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) *reinterpret_cast<uint4*>(wrow0 + bb * C::WBUF + c * 16) = make_uint4(0, 0, 0, 0);
   }
   if (warp >= 2 && warp < 6) {  // head-membership matrix A [128 heads][128 rows], K-major SW128 (row warps)
     const int h = threadIdx.x - 64;
@@ -1002,6 +1024,7 @@ __global__ void __launch_bounds__(Tc5MCfg::THREADS, 1) append_tc5_mean_kernel(co
           umma::commit(smem_u32(&empty[s]));  // K is read by this GEMM only
         }
       } else {
+        const int ksteps = (int)((a.RG + 15) / 16);  // rows past the group are zero: skip their K steps
         for (int st = 0; st < nst; ++st) {
           const int b = st & 1;
           mbar_wait(&wfull[b], (st >> 1) & 1);
@@ -1011,9 +1034,11 @@ __global__ void __launch_bounds__(Tc5MCfg::THREADS, 1) append_tc5_mean_kernel(co
             const uint32_t wb = sW + (b * 2 + h) * C::WBUF;
 #pragma unroll
             for (int k = 0; k < 8; ++k) {  // 16 rows per step
-              const uint64_t ad = umma::smem_desc(sA + (k / 4) * C::QATOM + (k % 4) * 32, 16, 1024);
-              const uint64_t bd = umma::smem_desc(wb + k * 16 * 128, C::WBUF, 1024);
-              umma::mma_bf16(tmem + M_COL + b * T5_KEYS, ad, bd, IDESC_M, h > 0 || k > 0);
+              if (k < ksteps) {
+                const uint64_t ad = umma::smem_desc(sA + (k / 4) * C::QATOM + (k % 4) * 32, 16, 1024);
+                const uint64_t bd = umma::smem_desc(wb + k * 16 * 128, C::WBUF, 1024);
+                umma::mma_bf16(tmem + M_COL + b * T5_KEYS, ad, bd, IDESC_M, h > 0 || k > 0);
+              }
             }
           }
           umma::commit(smem_u32(&mdone[b]));
@@ -1021,7 +1046,7 @@ __global__ void __launch_bounds__(Tc5MCfg::THREADS, 1) append_tc5_mean_kernel(co
       }
     }
     __syncwarp();
-  } else {  // ------------------------------------------------------- row warps
+  } else if ((warp & 3) * 32 < a.RG) {  // ---------------------------- row warps (rows)
     const int quarter = warp & 3;
     const int r = quarter * 32 + lane;
     const uint32_t tl = (uint32_t)(quarter * 32) << 16;

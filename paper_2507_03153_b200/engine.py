@@ -868,7 +868,7 @@ class HybridEngine:
         a_list = [a_cpu[r] for r in range(BHq)] if a_cpu is not None else [
             torch.zeros((nq, 0), dtype=odt, device=self.dev) for _ in range(BHq)]
         return self._output(not isinstance(inp.q, torch.Tensor), o, l, ag, a_list,
-                            np.arange(lo, nxt + nq, dtype=np.int64), store=self._archive_positions(lo))
+                            np.arange(lo, nxt + nq, dtype=np.int64), store_fn=lambda: self._archive_positions(lo))
 
     def _archive_positions(self, lo):
         """Append-mode store_positions: every head attends the whole archive (engine.py:131)."""
@@ -920,7 +920,7 @@ class HybridEngine:
         if squeeze:
             o, l = o[0], l[0]
         return self._output(to_np, o, l, None, None, np.arange(lo, nxt + nq, dtype=np.int64),
-                            store=self._archive_positions(lo))
+                            store_fn=lambda: self._archive_positions(lo))
 
     # ------------------------------------------------------------ inspection
     def context_indices(self, layer_idx=0):
