@@ -417,6 +417,7 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
           }
         }
         zl = warp_sum_f64(zl);
+        __syncwarp();  // every lane's read of hM[wid] before lane 0 rewrites it
         if (lane == 0) {
           const double so = (mold == -INFINITY || mn == -INFINITY) ? 0.0 : exp(mold - mn);
           hS[wid] = so;

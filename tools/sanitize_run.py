@@ -12,7 +12,7 @@ sys.path.insert(0, ROOT)
 import paper_2507_03153_b200 as hg  # noqa: E402
 
 
-def run(dtype, steps=150, append_at=60, append_nq=8):
+def run(dtype, steps=150, append_at=60, append_nq=8, graph=False):
     cfg = hg.EngineConfig(layers=1, heads=8, kv_heads=2, head_dim=128, batch=2, dtype=dtype,
                           cache=hg.CacheConfig(blk_num=4, blk_size=32, beta=1.0), core_count=4,
                           max_positions=1024)
@@ -32,6 +32,16 @@ def run(dtype, steps=150, append_at=60, append_nq=8):
         q = torch.randn((2, 8, 1, 128), generator=g, device="cuda").to(tdt)
         k = torch.randn((2, 2, 1, 128), generator=g, device="cuda").to(tdt)
         eng.decode_device(0, q, k, k)
+    if graph:  # graph mode: PDL-chained replays, first stages gathered before the launch wait
+        while eng.cap - eng.layers[0].window_size < 16:
+            q = torch.randn((2, 8, 1, 128), generator=g, device="cuda").to(tdt)
+            k = torch.randn((2, 2, 1, 128), generator=g, device="cuda").to(tdt)
+            eng.decode_device(0, q, k, k)
+        gr = hg.DecodeGraph(eng, steps=8)
+        for t in (gr.q, gr.k, gr.v):
+            t.copy_(torch.randn(t.shape, generator=g, device="cuda").to(tdt))
+        gr.step()
+        gr.step()
     torch.cuda.synchronize()
     print(dtype, "ok, archive", eng.layers[0].archive_size, flush=True)
 
@@ -48,3 +58,6 @@ if __name__ == "__main__":
         run("bfloat16", steps=3, append_at=0, append_nq=64)
     if mode in ("all", "f32"):
         run("float32", steps=80)
+    if mode in ("all", "graph"):
+        run("bfloat16", steps=40, append_at=-1, graph=True)
+        run("float32", steps=40, append_at=-1, graph=True)
