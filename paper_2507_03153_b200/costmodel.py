@@ -39,7 +39,7 @@ __all__ = [
     "DeviceSpec", "LinkSpec", "WorkloadShape", "BaselineBreakdown", "HybridBreakdown",
     "attention_cost", "kv_bytes", "merge_bytes", "time_offload_baseline", "time_hybrid",
     "speedup_heatmap", "heatmap_rows", "HEATMAP_COLUMNS", "DEFAULT_GPU", "DEFAULT_CPU", "DEFAULT_LINK",
-    "B200", "B200_DECODE", "FIXED_S", "NVLINK5", "PCIE5", "b200_spec", "DecodeShape", "DecodeBreakdown", "union_rows",
+    "B200", "B200_DECODE", "FIXED_S", "B200_DECODE_GRAPH", "FIXED_GRAPH_S", "NVLINK5", "PCIE5", "b200_spec", "DecodeShape", "DecodeBreakdown", "union_rows",
     "predict_decode", "predict_sharded", "fit_decode",
 ]
 
@@ -280,6 +280,11 @@ class DecodeBreakdown:
 # reaches 7.19 TB/s, the copy peak counts reads and writes). Median |error| 6%.
 FIXED_S = 24.5e-6   # per layer-step: launch, pipeline fill, merge tail
 B200_DECODE = DeviceSpec("b200-decode-fit", peak_flops=2.25e15, mem_bw=7.35e12)
+# Round 2, graph mode (DecodeGraph: PDL-chained replays, whole step incl. launch gaps and
+# evictions), 21 bf16 points of profiles/r02_configs_timing.jsonl (C3, C4, C5 sweep):
+# t = 18.4 us + bytes / 6.73 TB/s, median |error| 6.5% (profiles/r02_costmodel_check_graph.txt).
+FIXED_GRAPH_S = 18.4e-6
+B200_DECODE_GRAPH = DeviceSpec("b200-decode-graph-fit", peak_flops=2.25e15, mem_bw=6.73e12)
 
 
 def _decode_bytes(s: DecodeShape, union: float):

@@ -1,6 +1,10 @@
 """Predicted vs measured decode layer-steps (paper_2507_03153_b200.costmodel).
 
-  python tools/costmodel_check.py [profiles/r01_configs_timing.jsonl]
+  python tools/costmodel_check.py [profiles/r01_configs_timing.jsonl] [--graph]
+
+--graph: fit and compare the whole graph-mode step (graph_ms_per_step / layers: the
+step's kernels replayed from CUDA graphs, launch gaps and evictions included) instead
+of the decode + merge pair time of eager steps.
 
 1. Fits t = fixed + bytes/bw to the measured bf16 points (tools/bench_configs.py output:
    bytes_per_layer_step, layer_step_kernel_ms).
@@ -26,8 +30,15 @@ def shape_of(r):
 
 
 def main():
-    path = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "profiles", "r01_configs_timing.jsonl")
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    graph = "--graph" in sys.argv
+    path = args[0] if args else os.path.join(ROOT, "profiles", "r01_configs_timing.jsonl")
     rows = [json.loads(l) for l in open(path) if l.startswith("{")]
+    if graph:
+        rows = [r for r in rows if "graph_ms_per_step" in r]
+        for r in rows:
+            r["layer_step_kernel_ms"] = r["graph_ms_per_step"] / r.get("layers", 1)
+        print("graph mode: whole-step time per layer-step (DecodeGraph replays)")
     bf = [r for r in rows if r.get("dtype") == "bfloat16"]
     fixed, bw = cm.fit_decode((r["bytes_per_layer_step"], r["layer_step_kernel_ms"] * 1e-3) for r in bf)
     print(f"fit over {len(bf)} bf16 points: fixed {fixed * 1e6:.1f} us + bytes / {bw / 1e9:.0f} GB/s "
