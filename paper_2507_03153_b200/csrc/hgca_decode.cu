@@ -914,7 +914,8 @@ struct F32Cfg {
   static constexpr int OFF_Q = S * STAGE;                   // raw queries [S][G][D] f32
   static constexpr int OFF_QK = OFF_Q + S * QSLOT;          // queries [G][D] fp64
   static constexpr int OFF_ACC = OFF_QK + G * D * 8;        // P.V accumulators [G][D] fp32
-  static constexpr int OFF_META = OFF_ACC + G * D * 4;      // entries [S][32]
+  static constexpr int OFF_PF = OFF_ACC + G * D * 4;        // this stage's fp32 weights [32] (P.V broadcast)
+  static constexpr int OFF_META = OFF_PF + SUB * 4;         // entries [S][32]
   static constexpr int OFF_DESC = OFF_META + S * SUB * 4;
   static constexpr int OFF_FULL = OFF_DESC + S * 32;        // mbarriers: stage landed (TMA tx)
   static constexpr int OFF_EMPTY = OFF_FULL + S * 8;        // mbarriers: stage consumed
@@ -1044,35 +1045,47 @@ __global__ void __launch_bounds__(F32Cfg<D, G>::NW * 32, 1) decode_f32_kernel(co
       if (d.dense && lane < d.n)
         reinterpret_cast<double*>(a.dsc)[(b * a.Hq + kvh * G + g) * a.dsc_ld + d.r0 + lane] = sv;
       const double cm = warp_max_f64(sv);
-      const double mnew = fmax(m_run[g], cm);
+      const double mold = m_run[g], mnew = fmax(mold, cm);
       if (mnew == -INFINITY) continue;
-      const double scal = exp(m_run[g] - mnew);
+      // exp(0) = 1 and exp(-inf) = 0 exactly: skip the fp64 exp when the max
+      // did not move or this is the item's first stage (the common case)
+      const double scal = mold == -INFINITY ? 0.0 : (mold == mnew ? 1.0 : exp(mold - mnew));
       const double p = sv == -INFINITY ? 0.0 : exp(sv - mnew);
       z_run[g] = z_run[g] * scal + warp_sum_f64(p);
       m_run[g] = mnew;
-      const float pf = (float)p;
+      float* pfs = reinterpret_cast<float*>(wsm + C::OFF_PF);
+      pfs[lane] = (float)p;  // the stage's weights, broadcast to every lane below
       const float sf = (float)scal;
       float acc[C::DPL];
       float* ag = accs + g * D + lane * C::DPL;
 #pragma unroll
-      for (int i = 0; i < C::DPL; ++i) acc[i] = ag[i] * sf;
+      for (int i = 0; i < C::DPL; ++i) acc[i] = mold == -INFINITY ? 0.f : ag[i] * sf;
+      __syncwarp();
       // V chunk of this lane's dims; 16-byte chunk index inside the row pair
       constexpr int VC0 = D / 4;
       const int vc = VC0 + lane * C::DPL / 4, vo = (lane * C::DPL) % 4;
-#pragma unroll 8
-      for (int r = 0; r < SUB; ++r) {
-        const float pr = __shfl_sync(FULL, pf, r);
-        const int rr = meta[s * SUB + r] & 7;
-        const float* vr = reinterpret_cast<const float*>(st + r * C::PAIR + (((vc & ~7) | ((vc ^ rr) & 7)) << 4)) + vo;
-        if constexpr (C::DPL == 4) {
-          const float4 v = *reinterpret_cast<const float4*>(vr);
-          acc[0] = fmaf(pr, v.x, acc[0]); acc[1] = fmaf(pr, v.y, acc[1]);
-          acc[2] = fmaf(pr, v.z, acc[2]); acc[3] = fmaf(pr, v.w, acc[3]);
-        } else {
-          const float2 v = *reinterpret_cast<const float2*>(vr);
-          acc[0] = fmaf(pr, v.x, acc[0]); acc[1] = fmaf(pr, v.y, acc[1]);
+#pragma unroll 2
+      for (int r4 = 0; r4 < SUB; r4 += 4) {
+        const float4 p4 = *reinterpret_cast<const float4*>(pfs + r4);  // 4 weights, 4 row rotations per load
+        const int4 m4 = *reinterpret_cast<const int4*>(meta + s * SUB + r4);
+        const float pr4[4] = {p4.x, p4.y, p4.z, p4.w};
+        const int rr4[4] = {m4.x & 7, m4.y & 7, m4.z & 7, m4.w & 7};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float pr = pr4[u];
+          const float* vr =
+              reinterpret_cast<const float*>(st + (r4 + u) * C::PAIR + (((vc & ~7) | ((vc ^ rr4[u]) & 7)) << 4)) + vo;
+          if constexpr (C::DPL == 4) {
+            const float4 v = *reinterpret_cast<const float4*>(vr);
+            acc[0] = fmaf(pr, v.x, acc[0]); acc[1] = fmaf(pr, v.y, acc[1]);
+            acc[2] = fmaf(pr, v.z, acc[2]); acc[3] = fmaf(pr, v.w, acc[3]);
+          } else {
+            const float2 v = *reinterpret_cast<const float2*>(vr);
+            acc[0] = fmaf(pr, v.x, acc[0]); acc[1] = fmaf(pr, v.y, acc[1]);
+          }
         }
       }
+      __syncwarp();  // pfs is rewritten by the next head / stage
 #pragma unroll
       for (int i = 0; i < C::DPL; ++i) ag[i] = acc[i];
     }
