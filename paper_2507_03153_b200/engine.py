@@ -453,7 +453,14 @@ class StoreView:
 
 
 class HybridEngine:
-    """engine.py:87-195 on the B200, for `layers` layers."""
+    """engine.py:87-195 on the B200, for `layers` layers.
+
+    Streams: every launch goes to torch's current stream on the engine's
+    device, and the layers share one set of per-step scratch (dense scores,
+    item partials, the work counter), so all calls on one engine must be
+    issued in order on ONE stream (the reference engine is single-threaded
+    too, engine.py:10-11). Run independent engines for concurrent streams.
+    """
 
     def __init__(self, config: EngineConfig, dev=None):
         self.config = config
