@@ -364,7 +364,7 @@ struct Tc5Cfg {               // D = 128
   static constexpr int OFF_KV = OFF_Q + 2 * QATOM;
   static constexpr int OFF_P = OFF_KV + T5_S * STAGE;   // [2 buffers][hi, lo]
   static constexpr int OFF_BAR = OFF_P + 4 * PBUF;
-  static constexpr int NBAR = 1 + 2 * T5_S + 6;         // qfull, full[S], empty[S], sfull[2], pfull[2], pvdone[2]
+  static constexpr int NBAR = 1 + 2 * T5_S + 8;         // qfull, full[S], empty[S], sfull[2], pfull[2], pvdone[2], sfree[2]
   static constexpr int OFF_TM = OFF_BAR + NBAR * 8;
   static constexpr int SMEM = OFF_TM + 16 + 1024;       // + alignment slack
   static constexpr int TMEM_COLS = 256;                 // S[2] x 64 | O 128
@@ -392,6 +392,7 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
   uint64_t* sfull = empty + T5_S;
   uint64_t* pfull = sfull + 2;
   uint64_t* pvdone = pfull + 2;
+  uint64_t* sfree = pvdone + 2;  // S buffer read out of TMEM by every softmax warp (QK may overwrite it)
   uint32_t* tm_holder = reinterpret_cast<uint32_t*>(sm + C::OFF_TM);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int64_t bk, rg, chunk;
@@ -410,6 +411,7 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
     for (int b = 0; b < 2; ++b) {
       mbar_init(&sfull[b], 1);
       mbar_init(&pfull[b], (int)((a.RG + 31) / 32));  // one arrive per softmax warp that owns rows
+      mbar_init(&sfree[b], (int)((a.RG + 31) / 32));
     }
     mbar_init(&pvdone[0], 1);
     mbar_init(&pvdone[1], 1);
@@ -464,8 +466,8 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
         for (int st = 0; st < nst; ++st) {
           const int s = st % T5_S, b = st & 1;
           mbar_wait(&full[s], (st / T5_S) & 1);
-          // S buffer b was read by softmax(st-2): its P of stage st-2 is out
-          if (st >= 2) mbar_wait(&pfull[b], ((st - 2) >> 1) & 1);
+          // S buffer b was read out of TMEM by softmax(st-2)
+          if (st >= 2) mbar_wait(&sfree[b], ((st - 2) >> 1) & 1);
           umma::fence_after_sync();
           const uint32_t kb = sKV + s * C::STAGE;
 #pragma unroll
@@ -520,6 +522,9 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
 #pragma unroll
         for (int c = 0; c < 4; ++c) umma::ld_32x32b_x16(tmem + tl + b * T5_KEYS + c * 16, v[c]);
         umma::ld_wait();
+        umma::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sfree[b]);  // S(st) is in registers: QK(st + 2) may overwrite it
 #pragma unroll
         for (int c = 0; c < 4; ++c)
 #pragma unroll
@@ -904,12 +909,19 @@ struct Tc5MCfg {               // D = 128
   static constexpr int OFF_W = OFF_K + S * STAGE;       // [2 buffers][hi, lo]
   static constexpr int OFF_A = OFF_W + 4 * WBUF;        // head-membership matrix, 2 atoms
   static constexpr int OFF_BAR = OFF_A + 2 * QATOM;
-  static constexpr int NBAR = 1 + 2 * S + 6;            // qfull, full[S], empty[S], sfull[2], wfull[2], mdone[2]
+  static constexpr int NBAR = 1 + 2 * S + 8;            // qfull, full[S], empty[S], sfull[2], wfull[2], mdone[2], sfree[2]
   static constexpr int OFF_TM = OFF_BAR + NBAR * 8;
   static constexpr int SMEM = OFF_TM + 16 + 1024;
   static constexpr int TMEM_COLS = 256;                 // S[2] x 64 | MEAN[2] x 64
-  static constexpr int THREADS = 7 * 32;               // TMA, QK issuer, 4 row warps, GEMM issuer
+  static constexpr int THREADS = 11 * 32;              // TMA, QK issuer, 4 row warps, GEMM issuer, 4 more row warps
 };
+// Row warps of pass 2: warps 2-5 and 7-10, two per TMEM lane quarter (warp w
+// may only touch lanes 32*(w%4)..+31): the pair of a quarter splits every
+// stage's 64 keys (half 0: warps 2-5, half 1: warps 7-10), so a row's
+// per-stage work (S read, weights, W hi/lo) is halved. Quarters past the row
+// group (e.g. rows 64-127 for n_q = 16 at G = 4) idle.
+__device__ __forceinline__ bool tc5m_row_warp(int warp) { return (warp >= 2 && warp < 6) || warp >= 7; }
+__device__ __forceinline__ int tc5m_half(int warp) { return warp >= 7 ? 1 : 0; }
 
 __global__ void __launch_bounds__(Tc5MCfg::THREADS, 1) append_tc5_mean_kernel(const __grid_constant__ AppendArgs a) {
   using C = Tc5MCfg;
@@ -928,6 +940,7 @@ __global__ void __launch_bounds__(Tc5MCfg::THREADS, 1) append_tc5_mean_kernel(co
   uint64_t* sfull = empty + C::S;
   uint64_t* wfull = sfull + 2;
   uint64_t* mdone = wfull + 2;
+  uint64_t* sfree = mdone + 2;  // S buffer read out of TMEM by every row warp (QK may overwrite it)
   uint32_t* tm_holder = reinterpret_cast<uint32_t*>(sm + C::OFF_TM);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t p0 = a.seg_lo[seg] + chunk * ACHUNK;
@@ -944,20 +957,21 @@ __global__ void __launch_bounds__(Tc5MCfg::THREADS, 1) append_tc5_mean_kernel(co
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&sfull[b], 1);
-      mbar_init(&wfull[b], (int)((a.RG + 31) / 32));  // one arrive per row warp that owns rows
+      mbar_init(&wfull[b], 2 * (int)((a.RG + 31) / 32));  // one arrive per row warp that owns rows
+      mbar_init(&sfree[b], 2 * (int)((a.RG + 31) / 32));
       mbar_init(&mdone[b], 1);
     }
     fence_mbar_init();
   }
   // padding quarters (row groups of < 128 rows): their W rows stay zero
   // (A is zero there too, but 0 * garbage could be NaN) and they skip the stages
-  if (warp >= 2 && warp < 6 && (warp & 3) * 32 >= a.RG) {
-    const int r = (warp & 3) * 32 + lane;
+  if (tc5m_row_warp(warp) && (warp & 3) * 32 >= a.RG) {
+    const int r = (warp & 3) * 32 + lane, c0 = tc5m_half(warp) * 4;
     unsigned char* wrow0 = sm + C::OFF_W + (r >> 3) * 1024 + (r & 7) * 128;
 #pragma unroll
     for (int bb = 0; bb < 4; ++bb)
 #pragma unroll
-      for (int c = 0; c < 8; ++c) *reinterpret_cast<uint4*>(wrow0 + bb * C::WBUF + c * 16) = make_uint4(0, 0, 0, 0);
+      for (int c = c0; c < c0 + 4; ++c) *reinterpret_cast<uint4*>(wrow0 + bb * C::WBUF + c * 16) = make_uint4(0, 0, 0, 0);
   }
   if (warp >= 2 && warp < 6) {  // head-membership matrix A [128 heads][128 rows], K-major SW128 (row warps)
     const int h = threadIdx.x - 64;
@@ -1011,7 +1025,7 @@ __global__ void __launch_bounds__(Tc5MCfg::THREADS, 1) append_tc5_mean_kernel(co
         for (int st = 0; st < nst; ++st) {
           const int s = st % C::S, b = st & 1;
           mbar_wait(&full[s], (st / C::S) & 1);
-          if (st >= 2) mbar_wait(&wfull[b], ((st - 2) >> 1) & 1);  // S buffer b read by the rows of stage st-2
+          if (st >= 2) mbar_wait(&sfree[b], ((st - 2) >> 1) & 1);  // S buffer b read out by the rows of stage st-2
           umma::fence_after_sync();
           const uint32_t kb = sK + s * C::STAGE;
 #pragma unroll
@@ -1046,8 +1060,10 @@ __global__ void __launch_bounds__(Tc5MCfg::THREADS, 1) append_tc5_mean_kernel(co
       }
     }
     __syncwarp();
-  } else if ((warp & 3) * 32 < a.RG) {  // ---------------------------- row warps (rows)
+  } else if (tc5m_row_warp(warp) && (warp & 3) * 32 < a.RG) {  // ------- row warps (rows x half the keys)
     const int quarter = warp & 3;
+    const int half = tc5m_half(warp);
+    constexpr int HK = T5_KEYS / 2;  // keys per row warp per stage
     const int r = quarter * 32 + lane;
     const uint32_t tl = (uint32_t)(quarter * 32) << 16;
     const float sl2 = a.scale * 1.4426950408889634f;
@@ -1093,25 +1109,28 @@ __global__ void __launch_bounds__(Tc5MCfg::THREADS, 1) append_tc5_mean_kernel(co
       const int b = st & 1;
       mbar_wait(&sfull[b], (st >> 1) & 1);
       umma::fence_after_sync();
-      float x[T5_KEYS];
+      float x[HK];
       {
-        uint32_t v[4][16];
+        uint32_t v[2][16];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) umma::ld_32x32b_x16(tmem + tl + b * T5_KEYS + c * 16, v[c]);
+        for (int c = 0; c < 2; ++c) umma::ld_32x32b_x16(tmem + tl + b * T5_KEYS + half * HK + c * 16, v[c]);
         umma::ld_wait();
+        umma::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sfree[b]);  // S(st) is in registers: QK(st + 2) may overwrite it
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
+        for (int c = 0; c < 2; ++c)
 #pragma unroll
           for (int j = 0; j < 16; ++j) x[c * 16 + j] = __uint_as_float(v[c][j]);
       }
-      const int64_t kp0 = p0a + (int64_t)st * T5_KEYS;
-      if (kp0 >= p0 && kp0 + T5_KEYS <= p1) {
+      const int64_t kp0 = p0a + (int64_t)st * T5_KEYS + half * HK;
+      if (kp0 >= p0 && kp0 + HK <= p1) {
 #pragma unroll
-        for (int j = 0; j < T5_KEYS; ++j) x[j] = ex2_approx(fmaf(x[j], sl2, -m2)) * rz;
+        for (int j = 0; j < HK; ++j) x[j] = ex2_approx(fmaf(x[j], sl2, -m2)) * rz;
       } else {
-        const int jlo = (int)max(p0 - kp0, (int64_t)0), jhi = (int)min(p1 - kp0, (int64_t)T5_KEYS);
+        const int jlo = (int)max(p0 - kp0, (int64_t)0), jhi = (int)min(p1 - kp0, (int64_t)HK);
 #pragma unroll
-        for (int j = 0; j < T5_KEYS; ++j) {
+        for (int j = 0; j < HK; ++j) {
           const float w = ex2_approx(fmaf(x[j], sl2, -m2)) * rz;
           x[j] = (j >= jlo && j < jhi) ? w : 0.f;
         }
@@ -1120,14 +1139,14 @@ __global__ void __launch_bounds__(Tc5MCfg::THREADS, 1) append_tc5_mean_kernel(co
       unsigned char* wh = sm + C::OFF_W + (b * 2) * C::WBUF + prow;
       unsigned char* wl = wh + C::WBUF;
 #pragma unroll
-      for (int c = 0; c < T5_KEYS / 8; ++c) {
+      for (int c = 0; c < HK / 8; ++c) {
         uint32_t hi[4], lo[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           hi[e] = pack_bf16(x[c * 8 + 2 * e], x[c * 8 + 2 * e + 1]);
           lo[e] = pack_bf16(x[c * 8 + 2 * e] - bf16_lo_f(hi[e]), x[c * 8 + 2 * e + 1] - bf16_hi_f(hi[e]));
         }
-        const uint32_t off = (uint32_t)((c ^ (r & 7)) << 4);
+        const uint32_t off = (uint32_t)(((c + half * (HK / 8)) ^ (r & 7)) << 4);
         *reinterpret_cast<uint4*>(wh + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
         *reinterpret_cast<uint4*>(wl + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
       }
@@ -1135,9 +1154,9 @@ __global__ void __launch_bounds__(Tc5MCfg::THREADS, 1) append_tc5_mean_kernel(co
       umma::fence_before_sync();
       __syncwarp();
       if (lane == 0) mbar_arrive(&wfull[b]);
-      if (quarter == 0 && st >= 1) readout(st - 1);
+      if (quarter == 0 && half == 0 && st >= 1) readout(st - 1);
     }
-    if (quarter == 0) readout(nst - 1);
+    if (quarter == 0 && half == 0) readout(nst - 1);
   }
   umma::fence_before_sync();
   __syncthreads();
