@@ -26,6 +26,7 @@
  *   hgca_union_build(_items)   (device layout of the context cache for the decode kernel)
  *   hgca_decode_step           HybridEngine._run_step, decode mode engine.py:151-195
  *   hgca_decode_step_host      the same step with host q|k|v in / out|lse back (one call)
+ *   hgca_decode_step_host_async  ... without the final stream synchronization
  *   hgca_merge_partials        P-way merge of sharded (out, lse) partials
  *   hgca_merge_packed          P-way merge of the allgathered packed partials
  *   hgca_merge_packed_wait     the same merge behind the one-shot NVLink push (flags), hgca_peer_*
@@ -301,6 +302,13 @@ int hgca_append_bf16(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, int64_t
  * out_dev is copied back. */
 int hgca_decode_step_host(const hgca_decode_desc* desc, const void* in_host, void* in_dev, int64_t in_bytes,
                           void* out_host, const void* out_dev, int64_t out_bytes, hgca_stream_t stream);
+
+/* The same step without the final synchronization: everything is enqueued on
+ * `stream` and out_host holds the result once the stream reaches this point
+ * (the caller synchronizes), so host work for the next step -- bookkeeping,
+ * the next descriptor -- can overlap this one. */
+int hgca_decode_step_host_async(const hgca_decode_desc* desc, const void* in_host, void* in_dev, int64_t in_bytes,
+                                void* out_host, const void* out_dev, int64_t out_bytes, hgca_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -81,6 +81,7 @@ _SIGS = {
     "hgca_decode_step": [ctypes.POINTER(DecodeDesc), P],
     "hgca_step_state_set": [P, I64, I64, ctypes.c_uint64, P],
     "hgca_decode_step_host": [ctypes.POINTER(DecodeDesc), P, P, I64, P, P, I64, P],
+    "hgca_decode_step_host_async": [ctypes.POINTER(DecodeDesc), P, P, I64, P, P, I64, P],
     "hgca_append_ws_bytes": [I64, I64, I64, I64, I64, I64, I64],
     "hgca_append_bf16": [P, I64, I64, I64, I64, I64, P, I64, D, I64, I64, P, P, P, P, P, I64, P],
 }

@@ -523,8 +523,9 @@ int hgca_append_bf16(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, int64_t
                      "append_bf16");
 }
 
-int hgca_decode_step_host(const hgca_decode_desc* d, const void* in_host, void* in_dev, int64_t in_bytes,
-                          void* out_host, const void* out_dev, int64_t out_bytes, hgca_stream_t stream) {
+static int decode_step_host_impl(const hgca_decode_desc* d, const void* in_host, void* in_dev, int64_t in_bytes,
+                                 void* out_host, const void* out_dev, int64_t out_bytes, hgca_stream_t stream,
+                                 bool sync) {
   if (in_bytes < 0 || out_bytes < 0 || (in_bytes && (!in_host || !in_dev)) || (out_bytes && (!out_host || !out_dev)))
     return fail(HGCA_EINVAL, "decode_step_host: bad staging buffers");
   DecodeArgs a;
@@ -565,7 +566,17 @@ int hgca_decode_step_host(const hgca_decode_desc* d, const void* in_host, void* 
                      "decode_step_host: D2H");
     if (rc) return rc;
   }
-  return cuda_status((int)cudaStreamSynchronize(s), "decode_step_host: sync");
+  return sync ? cuda_status((int)cudaStreamSynchronize(s), "decode_step_host: sync") : 0;
+}
+
+int hgca_decode_step_host(const hgca_decode_desc* d, const void* in_host, void* in_dev, int64_t in_bytes,
+                          void* out_host, const void* out_dev, int64_t out_bytes, hgca_stream_t stream) {
+  return decode_step_host_impl(d, in_host, in_dev, in_bytes, out_host, out_dev, out_bytes, stream, true);
+}
+
+int hgca_decode_step_host_async(const hgca_decode_desc* d, const void* in_host, void* in_dev, int64_t in_bytes,
+                                void* out_host, const void* out_dev, int64_t out_bytes, hgca_stream_t stream) {
+  return decode_step_host_impl(d, in_host, in_dev, in_bytes, out_host, out_dev, out_bytes, stream, false);
 }
 
 int hgca_step_state_set(int64_t* state, int64_t dlo, int64_t dhi, uint64_t epoch, hgca_stream_t stream) {

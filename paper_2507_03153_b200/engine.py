@@ -763,8 +763,10 @@ class HybridEngine:
         holding q [B,Hq,D] | k [B,Hkv,D] | v [B,Hkv,D] in the storage dtype back
         to back; out_host a pinned uint8 buffer of B*Hq*(4*D + 8) bytes that
         receives out f32 [B*Hq, D] followed by lse f64 [B*Hq].
-        hgca_decode_step_host copies in, runs the step, copies out and
-        synchronizes (the host owns the result on return)."""
+        hgca_decode_step_host_async copies in, runs the step and delivers out
+        | lse; the host bookkeeping of the step (eviction / ingest) is issued
+        while the GPU runs it, then the stream is synchronized (the host owns
+        the result on return)."""
         B, Hq, Hkv, D = self.B, self.Hq, self.Hkv, self.D
         nq, nk = B * Hq * D, B * Hkv * D
         if in_host.numel() != nq + 2 * nk or in_host.dtype != self.tdtype:
@@ -780,9 +782,12 @@ class HybridEngine:
         e = self.tdtype.itemsize
         pi, po = dev_in.data_ptr(), dev_out.data_ptr()
         d = self._step_desc(ls, pi, pi + nq * e, pi + (nq + nk) * e, po, po + B * Hq * D * 4)
-        _lib.call("hgca_decode_step_host", d, in_host.data_ptr(), pi, (nq + 2 * nk) * e, out_host.data_ptr(), po,
-                  nout, self._stream())
+        # enqueue the step, do this step's host bookkeeping (eviction / ingest
+        # launches go behind it on the stream) while the GPU runs it, then wait
+        _lib.call("hgca_decode_step_host_async", d, in_host.data_ptr(), pi, (nq + 2 * nk) * e, out_host.data_ptr(),
+                  po, nout, self._stream())
         self._step_done(ls)
+        torch.cuda.current_stream(self.dev).synchronize()
         return out_host
 
     def decode_host(self, layer_idx, q_host, k_host, v_host, out_host, lse_host, staging=None):
