@@ -536,8 +536,8 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
 // (a.state) a producer whose first item is a full sparse item (rebuild-time
 // data only: item table, union entries, archive rows -- nothing the previous
 // step's kernels write, and a graph replay starts after all earlier stream
-// work) issues that item's first gathers while the previous step's merge
-// still runs; the item's queries, the work counter and everything that
+// work) gathers that item's first stages -- its whole ring -- while the
+// previous step's merge still runs; the item's queries, the work counter and everything that
 // depends on the step's window wait for griddepcontrol.wait.
 template <int D, int G, bool BF16, typename C>
 __device__ __forceinline__ void decode_producer(const DecodeArgs& a, unsigned char* cw, int first_item, int nwarps,
@@ -576,8 +576,8 @@ __device__ __forceinline__ void decode_producer(const DecodeArgs& a, unsigned ch
       bulk_g2s(cw + C::OFF_Q + s * C::QSLOT, Qg + (b * a.Hq + kvh * G) * (int64_t)C::ROWB, C::QB, &cfull[s]);
     }
   };
-  bool pre = false;
-  StageDesc pend;
+  int npre = 0;  // stages of the first item gathered before the wait (graph mode)
+  StageDesc pend, first;
   int32_t pend_ent = 0;
   if (a.state) {
     StepPos sp0;  // only nf matters for a full sparse item
@@ -585,26 +585,28 @@ __device__ __forceinline__ void decode_producer(const DecodeArgs& a, unsigned ch
     sp0.nd = 0;
     if (first_item < sp0.nf) {
       cursor_item(cur, a, sp0, first_item);
-      pend = cursor_stage(cur);
-      pend_ent = lane < pend.n ? __ldg(a.u_ent + (int64_t)pend.bk * a.T + pend.r0 + lane) : 0;
-      if (lane == 0) cdesc[0] = pend;
-      cmeta[lane] = pend_ent;
-      __syncwarp();  // desc/meta stores before lane 0's (release) arrive
-      issue_gathers(0, pend, pend_ent);
-      pre = true;
+      for (; npre < S && cur.row < cur.hi; ++npre) {  // fill the whole ring if the item is long enough
+        pend = cursor_stage(cur);
+        if (npre == 0) first = pend;
+        pend_ent = lane < pend.n ? __ldg(a.u_ent + (int64_t)pend.bk * a.T + pend.r0 + lane) : 0;
+        if (lane == 0) cdesc[npre] = pend;
+        cmeta[npre * SUB + lane] = pend_ent;
+        __syncwarp();  // desc/meta stores before lane 0's (release) arrive
+        issue_gathers(npre, pend, pend_ent);
+      }
     }
   }
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   const StepPos sp = step_pos(a);
   const int total = sp.nd + a.item_off[2 * a.B * a.Hkv + 1];
-  if (pre) {
-    issue_q(0, pend);
+  if (npre) {
+    issue_q(0, first);
     if (lane == 0) cur.nxt = atomicAdd(a.counter, 1) + nwarps;  // the prefetched item's deferred fetch
   }
-  pend = cursor_next_off(cur, a, sp, total, lane, nwarps);  // (after a prefetched stage: the next one)
+  pend = cursor_next_off(cur, a, sp, total, lane, nwarps);  // (after prefetched stages: the next one)
   pend_ent = sub_entry<G>(pend, a, sp, lane);
-  for (int k = pre ? 1 : 0;; ++k) {
+  for (int k = npre;; ++k) {
     const int s = k % S;
     if (k >= S) mbar_wait(&cempty[s], ((k / S) - 1) & 1);
     const StageDesc d = pend;
