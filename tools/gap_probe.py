@@ -72,6 +72,12 @@ def run(name):
     print(f"  decode CTA entry          {pct(us(gp[:, 0]))}")
     print(f"  decode wait released      {pct(us(gp[:, 1]))}")
     print(f"  consumer warps end        {pct(us(t[busy, 1]))}")
+    if cfgd["dtype"] == "float32":  # decode_f32_kernel slots: 2 stages, 3 wait, 4 score, 5 softmax+pv, 7 partial
+        bz = t[busy]
+        nsub = max(bz[:, 2].sum(), 1)
+        print(f"  fp32 consumer cycles per stage: wait {bz[:, 3].sum() / nsub:.0f}, score {bz[:, 4].sum() / nsub:.0f}, "
+              f"softmax+pv {bz[:, 5].sum() / nsub:.0f}, partial {bz[:, 7].sum() / nsub:.0f}; stages per busy warp "
+              f"max {bz[:, 2].max():.0f}; first stage data {pct(us(bz[:, 8]))}")
     print(f"  merge CTA resident        {pct(us(tm[:, 0]))}")
     print(f"  merge wait released       {pct(us(tm[:, 1]))}")
     print(f"  merge CTA end (epilogue)  {pct(us(tm[:, 5]))}")
