@@ -200,6 +200,9 @@ class StepOutput:
         return self._store
 
 
+APPEND_MAX_NQ = 128  # queries per hgca_append_bf16 call (include/hgca_b200.h)
+
+
 def _np(x):
     return x.detach().cpu().numpy() if isinstance(x, torch.Tensor) else x
 
@@ -827,7 +830,7 @@ class HybridEngine:
         w_size = nxt - lo
         W = w_size + nq
         odt = torch.float32
-        if self.tdtype == torch.bfloat16 and not self.config.keep_weights and nq <= 128:
+        if self.tdtype == torch.bfloat16 and not self.config.keep_weights:
             return self._append_tc(ls, q, nq, squeeze, not isinstance(inp.q, torch.Tensor))
         # sparse partial over the whole archive, with weights (engine.py:127-132)
         s_out = torch.zeros((BHq, nq, self.D), dtype=odt, device=self.dev)
@@ -903,11 +906,38 @@ class HybridEngine:
         lse = torch.empty((BHq, nq), dtype=torch.float64, device=self.dev)
         mean_a = torch.empty((BHq, max(lo, 1)), dtype=torch.float32, device=self.dev)
         mean_w = torch.empty((BHq, W), dtype=torch.float32, device=self.dev)
-        nb = int(_lib.load().hgca_append_ws_bytes(self.B, self.Hq, self.Hkv, self.D, nq, lo, hi))
-        ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=self.dev)
-        _lib.call("hgca_append_bf16", ls.KV.data_ptr(), self.B, self.Hq, self.Hkv, self.T, self.D, q.data_ptr(), nq,
-                  float(self.shape.scale), lo, hi, out.data_ptr(), lse.data_ptr(),
-                  mean_a.data_ptr() if lo else None, mean_w.data_ptr(), ws.data_ptr(), nb, s)
+        # hgca_append_bf16 takes <= APPEND_MAX_NQ queries per call (row groups of whole
+        # heads, <= 128 rows). Longer appends run as query chunks against the same keys
+        # (every kv_in row is already written, so each chunk sees the full key set, as
+        # the reference's non-causal attend_dense does): the outputs are per query, and
+        # the per-head row-mean weights combine as sum_c (nq_c / nq) * mean_c.
+        n_ch = -(-nq // APPEND_MAX_NQ)
+        step = -(-nq // n_ch)
+        for c0 in range(0, nq, step):
+            nc = min(step, nq - c0)
+            if n_ch == 1:
+                qc, oc, lc, ma, mw = q, out, lse, mean_a, mean_w
+            else:
+                qc = q[:, :, c0:c0 + nc].contiguous()
+                oc = torch.empty((BHq, nc, self.D), dtype=torch.float32, device=self.dev)
+                lc = torch.empty((BHq, nc), dtype=torch.float64, device=self.dev)
+                ma, mw = torch.empty_like(mean_a), torch.empty_like(mean_w)
+            nb = int(_lib.load().hgca_append_ws_bytes(self.B, self.Hq, self.Hkv, self.D, nc, lo, hi))
+            ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=self.dev)
+            _lib.call("hgca_append_bf16", ls.KV.data_ptr(), self.B, self.Hq, self.Hkv, self.T, self.D, qc.data_ptr(),
+                      nc, float(self.shape.scale), lo, hi, oc.data_ptr(), lc.data_ptr(),
+                      ma.data_ptr() if lo else None, mw.data_ptr(), ws.data_ptr(), nb, s)
+            self.launches += 3
+            if n_ch > 1:
+                out[:, c0:c0 + nc].copy_(oc)
+                lse[:, c0:c0 + nc].copy_(lc)
+                wgt = nc / nq
+                if c0 == 0:
+                    mean_a.copy_(ma).mul_(wgt)
+                    mean_w.copy_(mw).mul_(wgt)
+                else:
+                    mean_a.add_(ma, alpha=wgt)
+                    mean_w.add_(mw, alpha=wgt)
         # maintenance (engine.py:175-186): the kernel already took the row means
         _lib.call("hgca_maw_update", mean_w.data_ptr(), BHq, 1, W, W, ls.maw.data_ptr(), self.T, lo, w_size,
                   float(self.config.cache.alpha), 0, s)
@@ -926,7 +956,7 @@ class HybridEngine:
         if ls.window_size + nq > self.cap:
             raise ContractError(f"append of {nq} entries overflows window capacity {self.cap}")
         ls.nxt += nq
-        self.launches += 5
+        self.launches += 2
         o = out.view(self.B, self.Hq, nq, self.D)
         l = lse.view(self.B, self.Hq, nq)
         if squeeze:

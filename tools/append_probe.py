@@ -17,7 +17,7 @@ if len(sys.argv) > 1:
     cfgd["context"] = int(sys.argv[1])
 eng, g = bench.stage_engine(hg, torch, cfgd, cfgd["context"] + 2048, seed=3)
 B, Hq, Hkv, D = eng.B, eng.Hq, eng.Hkv, eng.D
-for nq in (1, 16, 64, 1, 16, 64):
+for nq in [int(x) for x in os.environ.get("HGCA_APPEND_NQ", "1,16,64,1,16,64").split(",")]:
     q = torch.randn((B, Hq, nq, D), generator=g, device="cuda").to(eng.tdtype)
     k = torch.randn((B, Hkv, nq, D), generator=g, device="cuda").to(eng.tdtype)
     torch.cuda.synchronize()
