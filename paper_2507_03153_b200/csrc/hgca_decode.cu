@@ -1272,9 +1272,17 @@ constexpr int TAIL_SPLIT = HGCA_TAIL_SPLIT;  // of rows / TAIL_SPLIT entries eac
 // items of >= rows / 4 entries, and rows >= 16 keeps them >= 4 entries
 static_assert(TAIL_SPLIT >= 1 && TAIL_SPLIT <= 4, "tail items must hold >= rows / 4 entries");
 static_assert(TAIL_DIV >= 2, "the tail is at most half of a list");
+// tail items hold rows / TAIL_SPLIT entries, but never less than one 32-row
+// stage: the short items of small steps (adaptive rows 32-128) would otherwise
+// be partial stages whose per-item cost (q load, partial write, merge fold)
+// buys no balance
+__device__ __forceinline__ int64_t tail_rows(int64_t rows) {
+  const int64_t t = rows / TAIL_SPLIT;
+  return t >= SUB ? t : (rows < SUB ? rows : SUB);
+}
 __device__ __forceinline__ void item_counts(int64_t cnt, int64_t rows, int& nbig, int& nsmall) {
   const int64_t big = (cnt - cnt / TAIL_DIV) / rows * rows;
-  const int64_t small = rows / TAIL_SPLIT;
+  const int64_t small = tail_rows(rows);
   nbig = (int)(big / rows);
   nsmall = (int)((cnt - big + small - 1) / small);
 }
@@ -1344,7 +1352,7 @@ __global__ void item_table_kernel(const int32_t* u_cnt, const int32_t* off, int6
   const int64_t rows = off[2 * (BK + 1)];
   int nb = 0, ns = 0;
   item_counts(u_cnt[bk], rows, nb, ns);
-  const int cnt = u_cnt[bk], small = (int)(rows / TAIL_SPLIT), big = nb * (int)rows;
+  const int cnt = u_cnt[bk], small = (int)tail_rows(rows), big = nb * (int)rows;
   for (int i = threadIdx.x; i < nb; i += blockDim.x)
     tab[off[bk] + i] = make_int4((int)bk, i * (int)rows, (i + 1) * (int)rows, 0);
   for (int i = threadIdx.x; i < ns; i += blockDim.x)

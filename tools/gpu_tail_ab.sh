@@ -1,6 +1,6 @@
 #!/bin/bash
 # tail-share A/B (HGCA_TAIL_DIV build variants) on graph-mode steps: C4 layer, C3, C2-shape, C5 small
-for v in base td4 td3 td2; do
+for v in ${VARIANTS:-base td4 td3 td2}; do
   lib=paper_2507_03153_b200/_lib/libhgca_b200.so; [ $v != base ] && lib=paper_2507_03153_b200/_lib/libhgca_b200_$v.so
   echo "== $v"; HGCA_LIB=$lib python tools/fixed_cost_probe.py C4L C5S 2>&1 | python -c "
 import sys,json
