@@ -12,9 +12,9 @@ sys.path.insert(0, ROOT)
 import paper_2507_03153_b200 as hg  # noqa: E402
 
 
-def run(dtype, steps=150, append_at=60, append_nq=8, graph=False):
+def run(dtype, steps=150, append_at=60, append_nq=8, graph=False, bn=4):
     cfg = hg.EngineConfig(layers=1, heads=8, kv_heads=2, head_dim=128, batch=2, dtype=dtype,
-                          cache=hg.CacheConfig(blk_num=4, blk_size=32, beta=1.0), core_count=4,
+                          cache=hg.CacheConfig(blk_num=bn, blk_size=32, beta=1.0), core_count=4,
                           max_positions=1024)
     eng = hg.HybridEngine(cfg)
     g = torch.Generator(device="cuda").manual_seed(1)
@@ -56,6 +56,8 @@ if __name__ == "__main__":
         run("bfloat16", steps=3, append_at=0, append_nq=16)
     if mode in ("all", "bf16-append-tc5x2"):  # G*n_q = 256 rows: the two-tile tcgen05 passes
         run("bfloat16", steps=3, append_at=0, append_nq=64)
+    if mode in ("all", "bf16-append-long"):  # n_q = 160 > 128: chunked tcgen05 passes
+        run("bfloat16", steps=3, append_at=0, append_nq=160, bn=8)
     if mode in ("all", "f32"):
         run("float32", steps=80)
     if mode in ("all", "graph"):
