@@ -366,7 +366,10 @@ int hgca_write_rows(int dtype, void* KV, int64_t BH, int64_t T, int64_t d, int64
 
 int hgca_decode_chunk_rows(int dtype, int64_t d) { return decode_chunk_rows(dtype, d); }
 
-static int64_t dense_rows_of(int dtype) { return dtype == HGCA_DTYPE_F32 ? 64 : 256; }
+#ifndef HGCA_BF16_ITEM_ROWS
+#define HGCA_BF16_ITEM_ROWS 256  // longest bf16 work item (rows); the fp32 kernel's is 64
+#endif
+static int64_t dense_rows_of(int dtype) { return dtype == HGCA_DTYPE_F32 ? 64 : HGCA_BF16_ITEM_ROWS; }
 // the shortest work item (one 32-row pipeline stage): step-adaptive items
 // (hgca_union_build_items with item_target > 0) never go below it, and the
 // dense items follow the chosen sparse granularity
