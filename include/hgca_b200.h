@@ -262,7 +262,20 @@ typedef struct hgca_decode_desc {
    * one captured launch sequence (CUDA graph) replays step after step. The
    * caller re-sets the state when the window moves otherwise (eviction). */
   int64_t* state;
+  /* Split merge (optional; merge_split <= 1 = off): long per-head item lists
+   * are folded by merge_split CTAs per query head (contiguous shares of the
+   * sparse items, the last share with the dense window items), whose partials
+   * the last CTA to arrive combines in share order -- deterministic, and the
+   * merge of a 128K-context step is spread over the GPU instead of one CTA per
+   * head walking ~300 partials. merge_scratch: hgca_merge_scratch_bytes(B, Hq,
+   * D, merge_split) bytes, zeroed once before the first step (every step
+   * leaves its counters zero). */
+  int64_t merge_split;
+  void* merge_scratch;
 } hgca_decode_desc;
+
+/* Device scratch of the split merge (hgca_decode_desc.merge_split / merge_scratch). */
+int64_t hgca_merge_scratch_bytes(int64_t B, int64_t Hq, int64_t D, int64_t split);
 
 /* Graph mode: state[0..3] = {dlo, dhi, epoch, 0}, in stream order (one tiny
  * kernel, so it can be captured too). */

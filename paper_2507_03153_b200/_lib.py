@@ -44,12 +44,14 @@ class DecodeDesc(ctypes.Structure):
         ("push_dst", P * 8), ("push_flag", P * 8), ("epoch", ctypes.c_uint64), ("push_cnt", P),
         ("item_target", I64),
         ("state", P),
+        ("merge_split", I64), ("merge_scratch", P),
     ]
 
 
 # name -> argtypes (all return int unless listed in _RESTYPES)
 _SIGS = {
     "hgca_version": [],
+    "hgca_merge_scratch_bytes": [I64, I64, I64, I64],
     "hgca_last_error": [],
     "hgca_attend_ws_bytes": [I64, I64],
     "hgca_attend_dense": [I32, P, P, P, I64, I64, I64, I64, D, I32, P, P, P, P, P],
@@ -85,7 +87,8 @@ _SIGS = {
     "hgca_append_ws_bytes": [I64, I64, I64, I64, I64, I64, I64],
     "hgca_append_bf16": [P, I64, I64, I64, I64, I64, P, I64, D, I64, I64, P, P, P, P, P, I64, P],
 }
-_RESTYPES = {"hgca_last_error": ctypes.c_char_p, "hgca_attend_ws_bytes": I64, "hgca_append_ws_bytes": I64}
+_RESTYPES = {"hgca_last_error": ctypes.c_char_p, "hgca_attend_ws_bytes": I64, "hgca_append_ws_bytes": I64,
+             "hgca_merge_scratch_bytes": I64}
 
 _lib = None
 

@@ -501,6 +501,17 @@ static int decode_prepare(const hgca_decode_desc* d, DecodeArgs& a, DecodeMergeA
   }
   m.epoch = d->epoch;
   m.push_cnt = d->push_cnt;
+  m.split = 1;
+  if (d->merge_split > 1) {
+    if (d->merge_split > 16 || !d->merge_scratch)
+      return fail(HGCA_EINVAL, "decode_step: merge_split must be in [1, 16] with a merge_scratch");
+    unsigned char* xs = static_cast<unsigned char*>(d->merge_scratch);
+    const int64_t heads = d->B * d->Hq, cnt_b = (heads * 4 + 255) / 256 * 256;
+    m.split = (int)d->merge_split;
+    m.xcnt = reinterpret_cast<unsigned int*>(xs);
+    m.xmz = reinterpret_cast<double*>(xs + cnt_b);
+    m.xacc = reinterpret_cast<double*>(xs + cnt_b + heads * d->merge_split * 4 * 8);
+  }
   return HGCA_OK;
 }
 
@@ -580,6 +591,12 @@ int hgca_decode_step_host(const hgca_decode_desc* d, const void* in_host, void* 
 int hgca_decode_step_host_async(const hgca_decode_desc* d, const void* in_host, void* in_dev, int64_t in_bytes,
                                 void* out_host, const void* out_dev, int64_t out_bytes, hgca_stream_t stream) {
   return decode_step_host_impl(d, in_host, in_dev, in_bytes, out_host, out_dev, out_bytes, stream, false);
+}
+
+int64_t hgca_merge_scratch_bytes(int64_t B, int64_t Hq, int64_t D, int64_t split) {
+  if (B < 1 || Hq < 1 || D < 1 || split < 1 || split > 16) return -1;
+  const int64_t heads = B * Hq, cnt_b = (heads * 4 + 255) / 256 * 256;
+  return cnt_b + heads * split * 4 * 8 + heads * split * 2 * D * 8;
 }
 
 int hgca_step_state_set(int64_t* state, int64_t dlo, int64_t dhi, uint64_t epoch, hgca_stream_t stream) {

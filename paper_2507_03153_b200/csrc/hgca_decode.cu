@@ -263,7 +263,10 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
   double* sw = reinterpret_cast<double*>(msm + C::OFF_W);
   uint64_t* bar = reinterpret_cast<uint64_t*>(msm + C::OFF_BAR);
   __shared__ double hM[2], hZ[2], hS[2];  // [0] sparse, [1] dense running stats
-  const int64_t bq = blockIdx.x;          // b * Hq + kv-head * G + g
+  __shared__ int x_last;                  // split merge: this CTA combines the head's partials
+  const int S = m.split;                  // CTAs per query head (split merge), 1 = off
+  const int js = (int)(blockIdx.x % S);   // this CTA's share of the head's items
+  const int64_t bq = blockIdx.x / S;      // b * Hq + kv-head * G + g
   const int64_t b = bq / m.Hq, kvh = (bq % m.Hq) / G, bk = b * m.Hkv + kvh;
   const int g = (int)(bq % m.Hq) % G;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -283,6 +286,10 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
   const int64_t o0 = m.item_off[bk], o1 = m.item_off[bk + 1];
   const int64_t t0 = m.item_off[BK + 1 + bk], t1 = m.item_off[BK + 1 + bk + 1];
   const int64_t nf = o1 - o0, ns = nf + (t1 - t0), n = ns + Sd;
+  // this CTA's items: a contiguous share of the sparse items; the last share
+  // also holds the dense (window) items, so its dense stats are final locally
+  const int64_t r0 = ns * js / S, r1 = js == S - 1 ? n : ns * (js + 1) / S;
+  const bool dense_here = js == S - 1;
   // item ids (see Cursor): full sparse items [0, NF), dense [NF, NF + nd), tails after
   const int64_t NF = sp.nf;
   auto item_id = [&](int64_t i) {
@@ -366,8 +373,8 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
   if (blockIdx.x == 0 && tid == 0) *a.counter = 0;
   // One fold pass over the concatenated item list [full items, tail items |
   // dense parts]: the first ns items are sparse, the rest dense.
-  for (int64_t c0 = 0; c0 < n; c0 += C::NI) {
-    const int64_t c1 = min(n, c0 + C::NI), cn = c1 - c0;
+  for (int64_t c0 = r0; c0 < r1; c0 += C::NI) {
+    const int64_t c1 = min(r1, c0 + C::NI), cn = c1 - c0;
     const int64_t lo[3] = {0, nf, ns}, hi[3] = {nf, ns, n};
     if (tid == 0) {
       uint32_t bytes = 0;
@@ -382,8 +389,8 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
           bulk_g2s(sacc + (x0 - c0) * D, pacc + item_id(x0) * D, (uint32_t)((x1 - x0) * D * 4), bar);
       }
     }
-    if (c0 == 0) dsc_load(0);  // the window scores of the epilogue: in flight during the fold
-    TL(if (tid == 0 && c0 == 0) g_tlm[blockIdx.x * 8 + 6] = gtimer();)
+    if (c0 == r0 && dense_here) dsc_load(0);  // the window scores of the epilogue: in flight during the fold
+    TL(if (tid == 0 && c0 == r0) g_tlm[blockIdx.x * 8 + 6] = gtimer();)
     // the chunk's sparse items [0, ce) (warp 0) and dense items [ce, cn) (warp 1)
     const int64_t ce = min(cn, max((int64_t)0, ns - c0));
     if (wid < 2) {
@@ -427,8 +434,8 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
       }
     }
     __syncthreads();
-    TL(if (tid == 0 && c0 == 0) g_tlm[blockIdx.x * 8 + 7] = gtimer();)
-    if (c1 == n && !m.push_n) window_epilogue();  // dense stats final: overlap the copies
+    TL(if (tid == 0 && c0 == r0) g_tlm[blockIdx.x * 8 + 7] = gtimer();)
+    if (c1 == n && (!m.push_n || S > 1)) window_epilogue();  // dense stats final: overlap the copies
     TL(if (tid == 0 && c1 == n) g_tlm[blockIdx.x * 8 + 3] = gtimer();)
     mbar_wait(bar, phase);
     phase ^= 1;
@@ -450,8 +457,57 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
     __syncthreads();  // the next chunk's copies overwrite sacc / sw
   }
   TL(if (tid == 0) g_tlm[blockIdx.x * 8 + 2] = gtimer();)
+  if (S > 1) {
+    // split merge: the dense share runs the window epilogue now (its dense
+    // stats are final), every share publishes its partial, and the last CTA
+    // to arrive folds the shares in order (so the result does not depend on
+    // arrival order)
+    if (dense_here && !epi_done) {
+      if (r1 == r0) dsc_load(0);
+      window_epilogue();
+    }
+    double* xm = m.xmz + (bq * S + js) * 4;
+    double* xa = m.xacc + (bq * S + js) * 2 * D;
+    xa[tid] = acc_s;
+    xa[D + tid] = acc_d;
+    if (tid == 0) {
+      xm[0] = hM[0];
+      xm[1] = hZ[0];
+      xm[2] = hM[1];
+      xm[3] = hZ[1];
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) x_last = atomicAdd(m.xcnt + bq, 1u) == (unsigned)(S - 1);
+    __syncthreads();
+    if (x_last) {
+      __threadfence();
+      const double* xm0 = m.xmz + bq * S * 4;
+      const double* xa0 = m.xacc + bq * S * 2 * D;
+      double M = -INFINITY;
+      for (int j = 0; j < S; ++j) M = fmax(M, __ldcg(xm0 + j * 4));
+      double Z = 0.0, A = 0.0;
+      for (int j = 0; j < S; ++j) {
+        const double mj = __ldcg(xm0 + j * 4);
+        const double w = (mj == -INFINITY || M == -INFINITY) ? 0.0 : exp(mj - M);
+        Z = fma(__ldcg(xm0 + j * 4 + 1), w, Z);
+        A = fma(__ldcg(xa0 + j * 2 * D + tid), w, A);
+      }
+      acc_s = A;
+      acc_d = __ldcg(xa0 + (S - 1) * 2 * D + D + tid);
+      __syncthreads();  // every thread has read hM / hZ above (through xm of its own share)
+      if (tid == 0) {
+        hM[0] = M;
+        hZ[0] = Z;
+        hM[1] = __ldcg(xm0 + (S - 1) * 4 + 2);
+        hZ[1] = __ldcg(xm0 + (S - 1) * 4 + 3);
+        m.xcnt[bq] = 0;  // re-armed for the next step
+      }
+      __syncthreads();
+    }
+  }
   const double Ms = hM[0], Zs = hZ[0], md = hM[1], zd = hZ[1];
-  {
+  if (S == 1 || x_last) {
     // merge_states(sparse, dense) (attention.py:153-188) in the equivalent
     // flash form -- both partials rescaled to M = max(m_s, m_d), one exp
     // each, one log -- so the dependent fp64 transcendental chain is three
@@ -489,7 +545,7 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
       __syncthreads();
       if (tid == 0) {
         const unsigned prev = atomicAdd(m.push_cnt, 1u);
-        if (prev == gridDim.x - 1) {
+        if (prev == gridDim.x / S - 1) {  // every head's combining CTA has pushed
           *m.push_cnt = 0;  // re-armed for the next step (stream order)
           __threadfence_system();
           for (int p = 0; p < m.push_n; ++p)
@@ -499,8 +555,8 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
     }
   }
   TL(if (tid == 0) g_tlm[blockIdx.x * 8 + 4] = gtimer();)
-  if (!epi_done) {
-    if (n == 0) dsc_load(0);  // (no fold chunk ran)
+  if (!epi_done && dense_here) {
+    if (r1 == r0) dsc_load(0);  // (no fold chunk ran)
     window_epilogue();
   }
   TL(__syncthreads(); if (tid == 0) { g_tlm[blockIdx.x * 8 + 5] = gtimer(); atomicMax(&g_mend, gtimer()); })
@@ -1464,7 +1520,7 @@ static int launch_decode_t(const DecodeArgs& a_in, cudaStream_t s) {
     const int rc = set_smem_dev(decode_merge_kernel<D, G, SC>, MergeCfg<D>::SMEM, mattr);
     if (rc) return rc;
   }
-  cfg.gridDim = dim3((unsigned)(a.B * a.Hq));
+  cfg.gridDim = dim3((unsigned)(a.B * a.Hq * a.m.split));
   cfg.blockDim = dim3(MergeCfg<D>::NT);
   cfg.dynamicSmemBytes = MergeCfg<D>::SMEM;
   cfg.stream = s;

@@ -62,6 +62,13 @@ struct DecodeMergeArgs {
   unsigned long long* push_flag[8];
   unsigned long long epoch;
   unsigned int* push_cnt;
+  // split merge (long item lists): `split` CTAs per query head each fold a
+  // contiguous share of the sparse items (the last also the dense ones) into a
+  // partial in the scratch; the last to arrive combines them in split order
+  int split;
+  unsigned int* xcnt;     // [B*Hq] arrival counters (0 between steps)
+  double* xmz;            // [B*Hq, split, 4]: m_s, z_s, m_d, z_d
+  double* xacc;           // [B*Hq, split, 2, D]: acc_s, acc_d
 };
 
 // Fused decode step: dense window items + sparse union chunks, merged in-kernel.

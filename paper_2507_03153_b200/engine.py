@@ -54,6 +54,12 @@ MODES = ("decode", "append")
 # no gain -- profiles/r02_item_ab.txt: the 256-row dense items stayed the
 # critical path of small steps.)
 MIN_ITEM_ROWS = int(os.environ.get("HGCA_MIN_ITEM_ROWS", "32"))
+# Split merge (hgca_decode_desc.merge_split): per-head item lists longer than
+# MERGE_ITEMS are folded by ceil(items / MERGE_ITEMS) CTAs per query head (at
+# most MERGE_SPLIT_MAX) whose partials the last one combines; the host takes
+# the item counts from an asynchronous copy of each union rebuild's item table.
+MERGE_ITEMS = int(os.environ.get("HGCA_MERGE_ITEMS", "96"))
+MERGE_SPLIT_MAX = 8
 ITEMS_PER_WARP = float(os.environ.get("HGCA_ITEMS_PER_WARP", "1"))
 
 
@@ -229,6 +235,9 @@ class LayerState:
         self.lo = 0    # archive size
         self.nxt = 0   # next position
         self.desc = None  # cached hgca_decode_desc (engine-owned)
+        self.merge_split = 1       # CTAs per query head in the merge kernel (split merge)
+        self.off_host = None       # pinned copy of the item table offsets of the last union rebuild
+        self.off_event = None      # ... and the event that says it has landed
         self.state = None  # graph mode: device step state {dlo, dhi, epoch, arrivals} (DecodeGraph)
         self.state_mirror = None  # (dlo, dhi) the device state holds, as far as the host knows
         self.keep = None
@@ -497,6 +506,9 @@ class HybridEngine:
         self.part_z = torch.empty(self.G * self.max_items, dtype=torch.float64, device=self.dev)
         self.part_acc = torch.empty(self.max_items * self.G * self.D, dtype=torch.float32, device=self.dev)
         self.counter = torch.zeros(4, dtype=torch.int32, device=self.dev)  # decode work counter
+        nb = int(_lib.load().hgca_merge_scratch_bytes(self.B, self.Hq, self.D, MERGE_SPLIT_MAX))
+        self.merge_scratch = torch.zeros(nb // 8 + 1, dtype=torch.int64, device=self.dev)  # split-merge partials
+        self.merge_items = MERGE_ITEMS  # items per merge CTA share (split merge)
         self.launches = 0          # kernels of libhgca_b200 launched by this engine
         self.step_events = None     # list -> (start, end) CUDA events around the decode kernel
         self._push = None           # per-step push descriptor (ShardedHybridEngine, exchange="push")
@@ -550,6 +562,14 @@ class HybridEngine:
         _lib.call("hgca_union_build_items", ls.sel.data_ptr(), self.B, self.Hq, self.Hkv, words, n, self.T,
                   ls.u_ent.data_ptr(), ls.u_cnt.data_ptr(), ls.item_off.data_ptr(), ls.item_tab.data_ptr(),
                   ls.sparse_rows, min(MIN_ITEM_ROWS, ls.sparse_rows), ls.item_target, grouped, s)
+        # the new item counts, for the merge's split factor: copied behind the rebuild and
+        # picked up by a later step once the copy has landed (no host synchronization)
+        nbk = 2 * self.B * self.Hkv + 3
+        if ls.off_host is None:
+            ls.off_host = torch.empty(nbk, dtype=torch.int32).pin_memory()
+        ls.off_host.copy_(ls.item_off[:nbk], non_blocking=True)
+        ls.off_event = torch.cuda.Event()
+        ls.off_event.record()
 
     def _ingest(self, ls: LayerState, lo, hi, divisor):
         """StoreTier.ingest_evicted of positions [lo, hi) (sparsifier.py:127-156)."""
@@ -733,6 +753,11 @@ class HybridEngine:
             d.max_items = self.max_items
             d.counter = self.counter.data_ptr()
             d.maw, d.alpha = ls.maw.data_ptr(), float(self.config.cache.alpha)
+            d.merge_scratch = self.merge_scratch.data_ptr()
+        if ls.off_event is not None and ls.off_event.query():
+            ls.merge_split = self._merge_split(ls)
+            ls.off_event = None
+        d.merge_split = ls.merge_split
         # per step: the queries, kv_in (the kernel writes it at position nxt, append_kv's slot,
         # before the dense pass), the window range and the outputs
         d.q, d.k_new, d.v_new = q, k, v
@@ -748,6 +773,17 @@ class HybridEngine:
             d.epoch, d.push_cnt = push["epoch"], push["cnt"]
             d.push_n = len(push["dst"])
         return d
+
+    def _merge_split(self, ls):
+        """CTAs per query head for the merge: the longest per-(batch, kv-head)
+        item list of the last rebuild (full + tail sparse items + window parts)
+        in shares of MERGE_ITEMS."""
+        off = ls.off_host.numpy().astype(np.int64)
+        BK = self.B * self.Hkv
+        rows = max(int(off[2 * (BK + 1)]), 16)
+        items = (off[1:BK + 1] - off[:BK]) + (off[BK + 2:2 * BK + 2] - off[BK + 1:2 * BK + 1])
+        n = int(items.max()) + -(-self.cap // rows) if BK else 0
+        return int(min(MERGE_SPLIT_MAX, max(1, -(-n // self.merge_items))))
 
     def _step_done(self, ls):
         """Host bookkeeping after a launched decode step (engine.py:175-191): the

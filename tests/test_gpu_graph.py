@@ -130,3 +130,29 @@ def test_graph_refuses_eager_only_features(cuda):
                             cache=cuda.CacheConfig(blk_num=2, blk_size=32), core_count=10 ** 6, max_positions=256)
     with pytest.raises(cuda.ContractError):
         cuda.DecodeGraph(cuda.HybridEngine(cfg))
+
+
+@pytest.mark.parametrize("dtype,Hq,Hkv", [("float32", 8, 2), ("bfloat16", 32, 8)])
+def test_split_merge_matches_single_cta_merge(cuda, dtype, Hq, Hkv):
+    """Split merge (hgca_decode_desc.merge_split: several CTAs per query head
+    fold shares of the item list, the last one combines them in share order)
+    against the one-CTA-per-head merge on the same inputs: outputs and lse to
+    fp64 rounding of the re-associated fold, the window MAW and the context
+    sets (dense stats stay in one share) identical. Shares of 4 items force
+    the split on this small shape."""
+    (ea, eb), g = _pair(cuda, dtype, Hq=Hq, Hkv=Hkv, arch=600, T=2048)
+    ea.merge_items, eb.merge_items = 10 ** 9, 4
+    steps = 160
+    q, k, v = _inputs(ea, g, steps)
+    splits = set()
+    for t in range(steps):
+        oa, la, _ = ea.decode_device(0, q[t], k[t], v[t])
+        ob, lb, _ = eb.decode_device(0, q[t], k[t], v[t])
+        torch.cuda.synchronize()
+        splits.add(eb.layers[0].merge_split)
+        assert torch.allclose(oa, ob, rtol=1e-5, atol=1e-6), f"step {t}: split-merge output differs"
+        assert torch.allclose(la, lb, rtol=1e-12, atol=1e-12), f"step {t}: split-merge lse differs"
+    assert max(splits) > 1, "the split merge never engaged"
+    la_, lb_ = ea.layers[0], eb.layers[0]
+    assert torch.equal(la_.ctx, lb_.ctx), "context sets differ"
+    assert torch.allclose(la_.maw, lb_.maw, rtol=1e-15, atol=0), "MAW differs"
