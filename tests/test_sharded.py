@@ -211,12 +211,13 @@ def test_gpu_sharded_shards_match_single_engine(cuda, world, dtype):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,dtype", [(2, "bfloat16"), (3, "float32")])
-def test_gpu_push_exchange_matches_allgather(cuda, world, dtype):
+@pytest.mark.parametrize("world,dtype,split", [(2, "bfloat16", False), (3, "float32", False), (2, "bfloat16", True)])
+def test_gpu_push_exchange_matches_allgather(cuda, world, dtype, split):
     """exchange="push" with `world` ranks in one process (one stream each, the
     peers' boxes as plain device pointers): the merge kernels push their packed
     partials into every box and the flag-waiting merge folds them -- bit-equal
-    to the all-gather exchange of the same partials, on every rank."""
+    to the all-gather exchange of the same partials, on every rank. split: the
+    split merge (several CTAs per head, the combining one pushes) on both."""
     hg = cuda
     H, Hkv, d, B = 8, 2, 128, 2
     cfg = hg.EngineConfig(layers=1, heads=H, kv_heads=Hkv, head_dim=d, batch=B, dtype=dtype,
@@ -227,6 +228,9 @@ def test_gpu_push_exchange_matches_allgather(cuda, world, dtype):
     for e in push:
         e.xchg.connect_local(bases)
     ref = [hg.ShardedHybridEngine(cfg, rank=r, world=world) for r in range(world)]
+    if split:
+        for e in push + ref:
+            e.merge_items = 4
     streams = [torch.cuda.Stream() for _ in range(world)]
     outs = [(torch.empty((B * H, d), dtype=torch.float32, device="cuda"),
              torch.empty(B * H, dtype=torch.float64, device="cuda")) for _ in range(world)]
@@ -258,6 +262,8 @@ def test_gpu_push_exchange_matches_allgather(cuda, world, dtype):
         e.check_exchange()
         assert e.collectives == 300
     assert push[0].layers[0].archive_size > 100
+    if split:
+        assert push[0].layers[0].merge_split > 1, "the split merge never engaged"
     for e in push:
         e.close()
 
