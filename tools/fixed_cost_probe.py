@@ -30,6 +30,8 @@ CFGS = {
     "C5S": dict(bench.C2, batch=4, context=65536, blk_num=8, frac=0.01),
     # near-empty: batch 1, 8 heads, window 64, archive 64, 1%
     "EMPTY": dict(bench.C2, batch=1, heads=8, kv_heads=8, context=128, blk_num=2, frac=0.01, dtype="float32"),
+    # the north-star shape: B=4, 128K context (bench.py's line)
+    "C3": dict(bench.C2, batch=4, context=131072),
     # one layer of the C4 shape (70B GQA 64q/8kv, per-GPU batch shard 8, 16K)
     "C4L": dict(bench.C2, batch=8, heads=64, kv_heads=8, context=16384),
     # the same on bf16 storage, GQA 4:1 (the tensor-core kernel)
