@@ -260,7 +260,11 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
   const DecodeMergeArgs& m = a.m;
   extern __shared__ __align__(128) unsigned char msm[];
   float* sacc = reinterpret_cast<float*>(msm);
-  double* sw = reinterpret_cast<double*>(msm + C::OFF_W);
+  // fold arithmetic: fp64 on the reference-exact fp32 path; fp32 weights and
+  // partial sums on the bf16 path (its 1e-2 contract; the (m, z) stats stay
+  // fp64), which takes the fp64 exp / convert / FMA chains off every merge
+  using AT = typename std::conditional<sizeof(SC) == 8, double, float>::type;
+  AT* sw = reinterpret_cast<AT*>(msm + C::OFF_W);
   uint64_t* bar = reinterpret_cast<uint64_t*>(msm + C::OFF_BAR);
   __shared__ double hM[2], hZ[2], hS[2];  // [0] sparse, [1] dense running stats
   __shared__ int x_last;                  // split merge: this CTA combines the head's partials
@@ -418,8 +422,15 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
         for (int u = 0; u < C::IPL; ++u) {
           const int64_t i = i0 + u * 32 + lane;
           if (i < i1) {
-            const double w = (mv[u] == -INFINITY || mn == -INFINITY) ? 0.0 : exp(mv[u] - mn);
-            sw[i] = w;
+            double w;
+            if constexpr (sizeof(AT) == 8) {
+              w = (mv[u] == -INFINITY || mn == -INFINITY) ? 0.0 : exp(mv[u] - mn);
+              sw[i] = w;
+            } else {
+              const float wf = (mv[u] == -INFINITY || mn == -INFINITY) ? 0.f : __expf((float)(mv[u] - mn));
+              sw[i] = wf;
+              w = wf;
+            }
             zl += zv[u] * w;
           }
         }
@@ -441,16 +452,16 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
     phase ^= 1;
     const float* src = sacc + tid;
     auto dot = [&](int64_t i0, int64_t i1) {  // 4 interleaved partial sums, combined in a fixed order
-      double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+      AT p0 = 0, p1 = 0, p2 = 0, p3 = 0;
       int64_t i = i0;
       for (; i + 4 <= i1; i += 4) {
-        p0 += sw[i] * (double)src[i * D];
-        p1 += sw[i + 1] * (double)src[(i + 1) * D];
-        p2 += sw[i + 2] * (double)src[(i + 2) * D];
-        p3 += sw[i + 3] * (double)src[(i + 3) * D];
+        p0 += sw[i] * (AT)src[i * D];
+        p1 += sw[i + 1] * (AT)src[(i + 1) * D];
+        p2 += sw[i + 2] * (AT)src[(i + 2) * D];
+        p3 += sw[i + 3] * (AT)src[(i + 3) * D];
       }
-      for (; i < i1; ++i) p0 += sw[i] * (double)src[i * D];
-      return (p0 + p1) + (p2 + p3);
+      for (; i < i1; ++i) p0 += sw[i] * (AT)src[i * D];
+      return (double)((p0 + p1) + (p2 + p3));
     };
     if (ce > 0) acc_s = acc_s * hS[0] + dot(0, ce);
     if (cn > ce) acc_d = acc_d * hS[1] + dot(ce, cn);

@@ -137,8 +137,9 @@ def test_split_merge_matches_single_cta_merge(cuda, dtype, Hq, Hkv):
     """Split merge (hgca_decode_desc.merge_split: several CTAs per query head
     fold shares of the item list, the last one combines them in share order)
     against the one-CTA-per-head merge on the same inputs: outputs and lse to
-    fp64 rounding of the re-associated fold, the window MAW and the context
-    sets (dense stats stay in one share) identical. Shares of 4 items force
+    the rounding of the re-associated fold (fp64 on the fp32 path, fp32 fold
+    weights on the bf16 path), the window MAW and the context sets (dense
+    stats stay in one share) identical. Shares of 4 items force
     the split on this small shape."""
     (ea, eb), g = _pair(cuda, dtype, Hq=Hq, Hkv=Hkv, arch=600, T=2048)
     ea.merge_items, eb.merge_items = 10 ** 9, 4
@@ -150,8 +151,10 @@ def test_split_merge_matches_single_cta_merge(cuda, dtype, Hq, Hkv):
         ob, lb, _ = eb.decode_device(0, q[t], k[t], v[t])
         torch.cuda.synchronize()
         splits.add(eb.layers[0].merge_split)
-        assert torch.allclose(oa, ob, rtol=1e-5, atol=1e-6), f"step {t}: split-merge output differs"
-        assert torch.allclose(la, lb, rtol=1e-12, atol=1e-12), f"step {t}: split-merge lse differs"
+        # fp32 path: fp64 folds (re-association only); bf16 path: fp32 fold weights
+        o_tol, l_tol = (1e-5, 1e-12) if dtype == "float32" else (1e-4, 1e-6)
+        assert torch.allclose(oa, ob, rtol=o_tol, atol=o_tol), f"step {t}: split-merge output differs"
+        assert torch.allclose(la, lb, rtol=l_tol, atol=l_tol), f"step {t}: split-merge lse differs"
     assert max(splits) > 1, "the split merge never engaged"
     la_, lb_ = ea.layers[0], eb.layers[0]
     assert torch.equal(la_.ctx, lb_.ctx), "context sets differ"
