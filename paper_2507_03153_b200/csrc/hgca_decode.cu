@@ -413,9 +413,18 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
           }
         }
         double mx = -INFINITY;
+        if constexpr (sizeof(AT) == 8) {
 #pragma unroll
-        for (int u = 0; u < C::IPL; ++u) mx = fmax(mx, mv[u]);
-        mx = warp_max_f64(mx);
+          for (int u = 0; u < C::IPL; ++u) mx = fmax(mx, mv[u]);
+          mx = warp_max_f64(mx);
+        } else {  // bf16 path: the items' m are fp32 values (exact in fp32): a 32-bit reduction
+          float mf = -INFINITY;
+#pragma unroll
+          for (int u = 0; u < C::IPL; ++u) mf = fmaxf(mf, (float)mv[u]);
+#pragma unroll
+          for (int o = 16; o; o >>= 1) mf = fmaxf(mf, __shfl_xor_sync(FULL, mf, o));
+          mx = mf;
+        }
         const double mold = hM[wid], mn = fmax(mold, mx);
         double zl = 0.0;
 #pragma unroll
@@ -437,7 +446,11 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
         zl = warp_sum_f64(zl);
         __syncwarp();  // every lane's read of hM[wid] before lane 0 rewrites it
         if (lane == 0) {
-          const double so = (mold == -INFINITY || mn == -INFINITY) ? 0.0 : exp(mold - mn);
+          double so;
+          if constexpr (sizeof(AT) == 8)
+            so = (mold == -INFINITY || mn == -INFINITY) ? 0.0 : exp(mold - mn);
+          else
+            so = (mold == -INFINITY || mn == -INFINITY) ? 0.0 : (double)__expf((float)(mold - mn));
           hS[wid] = so;
           hZ[wid] = hZ[wid] * so + zl;
           hM[wid] = mn;
@@ -528,12 +541,15 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
     const bool d_empty = !(zd > 0.0) || md == -INFINITY;
     const double M = fmax(s_empty ? -INFINITY : Ms, d_empty ? -INFINITY : md);
     const bool both_empty = M == -INFINITY;
-    const double es = s_empty ? 0.0 : exp(Ms - M), ed = d_empty ? 0.0 : exp(md - M);
+    // (bf16 path: fp32 transcendentals, its 1e-2 contract)
+    auto exp_ = [](double x) { return sizeof(AT) == 8 ? exp(x) : (double)__expf((float)x); };
+    auto log_ = [](double x) { return sizeof(AT) == 8 ? log(x) : (double)__logf((float)x); };
+    const double es = s_empty ? 0.0 : exp_(Ms - M), ed = d_empty ? 0.0 : exp_(md - M);
     const double Zt = both_empty ? 1.0 : fma(Zs, es, zd * ed);
     const float ov = both_empty ? 0.f : (float)(fma(acc_s, es, acc_d * ed) / Zt);
-    const double lv = both_empty ? -INFINITY : M + log(Zt);
+    const double lv = both_empty ? -INFINITY : M + log_(Zt);
     const bool want_s = m.out_sparse || m.lse_sparse || (m.push_n && m.push_sparse);
-    const double lse_s = (want_s && !s_empty) ? Ms + log(Zs) : -INFINITY;
+    const double lse_s = (want_s && !s_empty) ? Ms + log_(Zs) : -INFINITY;
     const float os = (want_s && !s_empty) ? (float)(acc_s / Zs) : 0.f;
     m.out[bq * D + tid] = ov;
     if (m.out_sparse) m.out_sparse[bq * D + tid] = os;
