@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
     }
     __syncthreads();
     TL(if (tid == 0 && c0 == r0) g_tlm[blockIdx.x * 8 + 7] = gtimer();)
-    if (c1 == n && (!m.push_n || S > 1)) window_epilogue();  // dense stats final: overlap the copies
+    if (c1 == n && !m.push_n && S == 1) window_epilogue();  // dense stats final: overlap the copies
     TL(if (tid == 0 && c1 == n) g_tlm[blockIdx.x * 8 + 3] = gtimer();)
     mbar_wait(bar, phase);
     phase ^= 1;
@@ -482,14 +482,10 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
   }
   TL(if (tid == 0) g_tlm[blockIdx.x * 8 + 2] = gtimer();)
   if (S > 1) {
-    // split merge: the dense share runs the window epilogue now (its dense
-    // stats are final), every share publishes its partial, and the last CTA
+    // split merge: every share publishes its partial at once and the last CTA
     // to arrive folds the shares in order (so the result does not depend on
-    // arrival order)
-    if (dense_here && !epi_done) {
-      if (r1 == r0) dsc_load(0);
-      window_epilogue();
-    }
+    // arrival order); the dense share runs the window epilogue afterwards,
+    // off the output's critical path
     double* xm = m.xmz + (bq * S + js) * 4;
     double* xa = m.xacc + (bq * S + js) * 2 * D;
     xa[tid] = acc_s;
