@@ -27,6 +27,8 @@ def main():
         cfgd.update(batch=8, heads=64, kv_heads=8, context=16384)
     elif os.environ.get("HGCA_TL_CFG") == "C5S":  # a small step: C5 at 64K, window 256, 1% selected
         cfgd.update(batch=4, context=65536, blk_num=8, frac=0.01)
+    elif os.environ.get("HGCA_TL_CFG") == "C3":  # the north-star shape: B=4, 128K context
+        cfgd.update(batch=4, context=131072)
     elif os.environ.get("HGCA_TL_CFG") == "EMPTYB":  # a near-empty bf16 step (tools/fixed_cost_probe.py)
         cfgd.update(batch=1, heads=32, kv_heads=8, context=128, blk_num=2, frac=0.01)
     eng, g = bench.stage_engine(hg, torch, cfgd, cfgd["context"] + 64)
