@@ -240,7 +240,9 @@ __device__ __forceinline__ int32_t sub_entry(const StageDesc& d, const DecodeArg
 //   * MAW maintenance, 3 separately rounded fp64 ops (kv_cache.py:186), new
 //     entries maw = w (engine.py:177-191).
 // Fixed order throughout: deterministic. (B*Hq CTAs of ~50 KB: four per SM,
-// so the whole merge of a C2/C4 step is one wave.)
+// so the whole merge of a C2/C4 step is one wave.) Long item lists (128K
+// context: ~300 items per head) are split over m.split CTAs per head whose
+// partials the last to arrive combines in share order (split merge).
 constexpr int MERGE_NI = 96;  // items per fold chunk
 
 template <int D>
