@@ -7,6 +7,10 @@
 
 #include "hgca_common.cuh"
 #include "hgca_internal.h"
+
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include "../../include/hgca_b200.h"
 
 namespace hgca {
@@ -537,9 +541,28 @@ int hgca_append_bf16(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, int64_t
                      "append_bf16");
 }
 
+// HGCA_HOST_PROF=1 (diagnostics): host time of the host-buffer step's parts,
+// averaged and printed to stderr every 64 calls
+namespace {
+struct HostProf {
+  bool on = getenv("HGCA_HOST_PROF") != nullptr;
+  double t[5] = {0, 0, 0, 0, 0};
+  long n = 0;
+};
+HostProf& host_prof() {
+  static HostProf p;
+  return p;
+}
+double now_us() {
+  return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+}  // namespace
+
 static int decode_step_host_impl(const hgca_decode_desc* d, const void* in_host, void* in_dev, int64_t in_bytes,
                                  void* out_host, const void* out_dev, int64_t out_bytes, hgca_stream_t stream,
                                  bool sync) {
+  HostProf& hp = host_prof();
+  double tp0 = hp.on ? now_us() : 0.0, tp1 = 0, tp2 = 0, tp3 = 0;
   if (in_bytes < 0 || out_bytes < 0 || (in_bytes && (!in_host || !in_dev)) || (out_bytes && (!out_host || !out_dev)))
     return fail(HGCA_EINVAL, "decode_step_host: bad staging buffers");
   DecodeArgs a;
@@ -548,11 +571,13 @@ static int decode_step_host_impl(const hgca_decode_desc* d, const void* in_host,
   if (rc) return rc;
   a.m = m;
   cudaStream_t s = S(stream);
+  if (hp.on) tp1 = now_us();
   if (in_bytes) {
     rc = cuda_status((int)cudaMemcpyAsync(in_dev, in_host, (size_t)in_bytes, cudaMemcpyHostToDevice, s),
                      "decode_step_host: H2D");
     if (rc) return rc;
   }
+  if (hp.on) tp2 = now_us();
   // Results straight to the host: when out_host is pinned and mapped (UVA), the
   // merge kernel writes out / lse (which the descriptor places inside
   // out_dev) into their mirror locations in out_host over the bus, so no D2H
@@ -573,8 +598,16 @@ static int decode_step_host_impl(const hgca_decode_desc* d, const void* in_host,
       (void)cudaGetLastError();  // not mapped: clear the lookup error, use the staged copy
     }
   }
+  if (hp.on) tp3 = now_us();
   rc = cuda_status(launch_decode_partial(d->dtype, a, s), "decode_step_host");
   if (rc) return rc;
+  if (hp.on) {
+    const double tp4 = now_us();
+    hp.t[0] += tp1 - tp0; hp.t[1] += tp2 - tp1; hp.t[2] += tp3 - tp2; hp.t[3] += tp4 - tp3;
+    if (++hp.n % 64 == 0)
+      fprintf(stderr, "[hgca host prof] us/call: prepare %.2f H2D-issue %.2f map %.2f launch(2 kernels) %.2f\n",
+              hp.t[0] / hp.n, hp.t[1] / hp.n, hp.t[2] / hp.n, hp.t[3] / hp.n);
+  }
   if (out_bytes && !direct) {
     rc = cuda_status((int)cudaMemcpyAsync(out_host, out_dev, (size_t)out_bytes, cudaMemcpyDeviceToHost, s),
                      "decode_step_host: D2H");
