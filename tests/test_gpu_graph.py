@@ -159,3 +159,33 @@ def test_split_merge_matches_single_cta_merge(cuda, dtype, Hq, Hkv):
     la_, lb_ = ea.layers[0], eb.layers[0]
     assert torch.equal(la_.ctx, lb_.ctx), "context sets differ"
     assert torch.allclose(la_.maw, lb_.maw, rtol=1e-15, atol=0), "MAW differs"
+
+
+def test_split_merge_keep_weights_window_weights_equal(cuda):
+    """keep_weights with the split merge: the dense share writes the window
+    weights (a_gpu) and the MAW exactly as the one-CTA merge does."""
+    cfg = cuda.EngineConfig(layers=1, heads=8, kv_heads=2, head_dim=128, batch=2, dtype="float32",
+                            cache=cuda.CacheConfig(blk_num=4, blk_size=32, alpha=0.5, beta=1.0),
+                            core_count=10 ** 6, max_positions=2048, keep_weights=True)
+    ea, eb = cuda.HybridEngine(cfg), cuda.HybridEngine(cfg)
+    ea.merge_items, eb.merge_items = 10 ** 9, 4
+    g = torch.Generator(device="cuda").manual_seed(9)
+    arch = 600
+    k = torch.randn((2, 2, arch, 128), generator=g, device="cuda")
+    v = torch.randn((2, 2, arch, 128), generator=g, device="cuda")
+    u = torch.rand((2, 8, arch), generator=g, device="cuda", dtype=torch.float64)
+    maw = torch.where(u < 0.2, (1.0 / 128) * (1.0 + u), 1e-6 * u)
+    for e in (ea, eb):
+        e.bulk_ingest(0, k, v, maw, 128)
+    splits = set()
+    for t in range(100):
+        q = torch.randn((2, 8, 1, 128), generator=g, device="cuda")
+        kk = torch.randn((2, 2, 1, 128), generator=g, device="cuda")
+        oa, la, wa = ea.decode_device(0, q, kk, -kk)
+        ob, lb, wb = eb.decode_device(0, q, kk, -kk)
+        torch.cuda.synchronize()
+        splits.add(eb.layers[0].merge_split)
+        assert torch.equal(wa, wb), f"step {t}: window weights differ"
+        assert torch.allclose(oa, ob, rtol=1e-5, atol=1e-6) and torch.allclose(la, lb, rtol=1e-12, atol=1e-12)
+    assert max(splits) > 1
+    assert torch.equal(ea.layers[0].maw, eb.layers[0].maw)
