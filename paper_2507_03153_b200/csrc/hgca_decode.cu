@@ -122,6 +122,13 @@ __device__ __forceinline__ StepPos step_pos(const DecodeArgs& a) {
   // part); before any rebuild, the descriptor's default
   const int chosen = a.item_off[2 * (a.B * a.Hkv + 1)];
   p.dr = chosen >= 16 && chosen <= (int)a.dense_rows ? chosen : (int)a.dense_rows;
+#ifndef HGCA_DENSE_DIV
+#define HGCA_DENSE_DIV 2
+#endif
+  // the window parts come right after the full sparse items, so a long one
+  // could still run when the short tail items are gone: halve them (at least
+  // one 32-row stage; quarter-length parts measured worse at C3)
+  p.dr = max(min(p.dr, SUB), p.dr / HGCA_DENSE_DIV);
   p.Sd = (p.W + p.dr - 1) / p.dr;
   p.nd = (int)(a.B * a.Hkv) * p.Sd;
   p.nf = a.item_off[a.B * a.Hkv];
