@@ -823,7 +823,8 @@ __global__ void __launch_bounds__(Bf16Cfg<D, G, S, NPAIR>::NW * 32, 1)
     mbar_wait(&full[s], (k / S) & 1);
     const StageDesc d = desc[s];
     if (d.item < 0) break;
-    TL(long long c1 = clock64(); tl_wait += c1 - c0; ++tl_sub;)
+    TL(long long c1 = clock64(); tl_wait += c1 - c0; ++tl_sub;
+       if (d.first && lane == 0) { tl[18] = gtimer(); tl[19] = (unsigned long long)d.item; })
 #ifdef HGCA_NOCOMPUTE
     // experiment: data movement only (results are garbage)
     __syncwarp();

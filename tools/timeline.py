@@ -94,6 +94,20 @@ def main():
                   np.median(tm[:, 5] - tm[:, 4])))
         print("  merge fold detail (median per CTA, us): m/z loads + issue %.1f, bulk wait %.1f, stats+acc %.1f" % (
             np.median(tm[:, 6] - tm[:, 1]), np.median(tm[:, 7] - tm[:, 6]), np.median(tm[:, 2] - tm[:, 7])))
+        # the last items: when did the finishers start them, and what were they
+        BK = B * Hkv
+        off = ls_off = eng.layers[0].item_off.cpu().numpy()
+        NF, NS = int(off[BK]), int(off[2 * BK + 1])
+        rows = int(off[2 * (BK + 1)])
+        W = eng.layers[0].window_size
+        dr = max(min(rows, 32), rows // 2)
+        ND = BK * -(-W // dr)
+        kind = lambda it: "full" if it < NF else ("dense" if it < NF + ND else "tail")  # noqa: E731
+        last_start = (t[:, 18] - t0) / 1e3
+        order = np.argsort(end)
+        print("  last 8 finishers: end / last item start / kind: " + ", ".join(
+            f"{end[i]:.1f}/{last_start[i]:.1f}/{kind(int(t[i, 19]))}" for i in order[-8:]))
+        print(f"  items: {NF} full, {ND} dense (est.), {NS - NF} tail")
         # early finishers: what were they doing?
         order = np.argsort(end)
         print(f"  first 5 finishers: end {np.round(end[order[:5]], 1)} subs {cyc['sub'][order[:5]]}; "
