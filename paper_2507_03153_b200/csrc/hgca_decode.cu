@@ -67,6 +67,9 @@ __device__ unsigned long long g_mend;
 #ifndef HGCA_BF16_STAGES
 #define HGCA_BF16_STAGES 2
 #endif
+#ifndef HGCA_LAZY_CLAIM
+#define HGCA_LAZY_CLAIM 1
+#endif
 #ifndef HGCA_F32_STAGES
 #define HGCA_F32_STAGES 2
 #endif
@@ -188,6 +191,12 @@ __device__ __forceinline__ StageDesc cursor_stage(Cursor& c) {
 __device__ __forceinline__ StageDesc cursor_next_off(Cursor& c, const DecodeArgs& a, const StepPos& sp, int total,
                                                      int lane, int nwarps) {
   if (c.item < 0 || c.row >= c.hi) {
+#if HGCA_LAZY_CLAIM
+    // claim the next item only once the current one is fully issued: a warp
+    // then holds at most one item it has not started, so the last items of
+    // the queue go to the warps that are actually about to be free
+    if (lane == 0 && c.nxt < 0) c.nxt = atomicAdd(a.counter, 1) + nwarps;
+#endif
     const int it = __shfl_sync(FULL, c.nxt, 0);
     if (it >= total) {
       StageDesc d;
@@ -195,7 +204,11 @@ __device__ __forceinline__ StageDesc cursor_next_off(Cursor& c, const DecodeArgs
       d.bk = d.r0 = d.n = d.first = d.last = d.dense = d.pad = 0;
       return d;
     }
+#if HGCA_LAZY_CLAIM
+    if (lane == 0) c.nxt = -1;
+#else
     if (lane == 0) c.nxt = atomicAdd(a.counter, 1) + nwarps;
+#endif
     cursor_item(c, a, sp, it);
   }
   return cursor_stage(c);
@@ -690,7 +703,11 @@ __device__ __forceinline__ void decode_producer(const DecodeArgs& a, unsigned ch
   const int total = sp.nd + a.item_off[2 * a.B * a.Hkv + 1];
   if (npre) {
     issue_q(0, first);
+#if HGCA_LAZY_CLAIM
+    if (lane == 0) cur.nxt = -1;  // the next item is claimed when the prefetched one is fully issued
+#else
     if (lane == 0) cur.nxt = atomicAdd(a.counter, 1) + nwarps;  // the prefetched item's deferred fetch
+#endif
   }
   pend = cursor_next_off(cur, a, sp, total, lane, nwarps);  // (after prefetched stages: the next one)
   pend_ent = sub_entry<G>(pend, a, sp, lane);
