@@ -205,6 +205,14 @@ int hgca_union_build_items(const uint32_t* sel_mask, int64_t B, int64_t Hq, int6
                            int64_t n_arch, int64_t T, int32_t* u_ent, int32_t* u_cnt, int32_t* item_off,
                            int32_t* item_tab, int64_t max_rows, int64_t min_rows, int64_t item_target, int grouped,
                            hgca_stream_t stream);
+/* The same counting the step's dense window (window_rows per (batch, kv
+ * head), e.g. the window capacity) into the work the item size is chosen for:
+ * the window parts share the item granularity, so a big window beside a small
+ * union keeps long items. */
+int hgca_union_build_items_w(const uint32_t* sel_mask, int64_t B, int64_t Hq, int64_t Hkv, int64_t words,
+                             int64_t n_arch, int64_t T, int32_t* u_ent, int32_t* u_cnt, int32_t* item_off,
+                             int32_t* item_tab, int64_t max_rows, int64_t min_rows, int64_t item_target,
+                             int64_t window_rows, int grouped, hgca_stream_t stream);
 
 typedef struct hgca_decode_desc {
   int32_t dtype;            /* HGCA_DTYPE_F32 or HGCA_DTYPE_BF16 (storage) */

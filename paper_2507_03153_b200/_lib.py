@@ -80,6 +80,7 @@ _SIGS = {
     "hgca_maw_ema": [P, I64, I64, I64, P, I64, D, P],
     "hgca_union_build": [P, I64, I64, I64, I64, I64, I64, P, P, P, P, I64, I32, P],
     "hgca_union_build_items": [P, I64, I64, I64, I64, I64, I64, P, P, P, P, I64, I64, I64, I32, P],
+    "hgca_union_build_items_w": [P, I64, I64, I64, I64, I64, I64, P, P, P, P, I64, I64, I64, I64, I32, P],
     "hgca_decode_step": [ctypes.POINTER(DecodeDesc), P],
     "hgca_step_state_set": [P, I64, I64, ctypes.c_uint64, P],
     "hgca_decode_step_host": [ctypes.POINTER(DecodeDesc), P, P, I64, P, P, I64, P],

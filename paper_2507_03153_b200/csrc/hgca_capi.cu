@@ -409,10 +409,11 @@ int hgca_maw_ema(double* maw, int64_t rows, int64_t ld, int64_t n, const double*
   return cuda_status(launch_maw_ema(maw, rows, ld, n, a, lda, alpha, S(stream)), "maw_ema");
 }
 
-int hgca_union_build_items(const uint32_t* sel_mask, int64_t B, int64_t Hq, int64_t Hkv, int64_t words,
-                           int64_t n_arch, int64_t T, int32_t* u_ent, int32_t* u_cnt, int32_t* item_off,
-                           int32_t* item_tab, int64_t max_rows, int64_t min_rows, int64_t item_target, int grouped,
-                           hgca_stream_t stream) {
+int hgca_union_build_items_w(const uint32_t* sel_mask, int64_t B, int64_t Hq, int64_t Hkv, int64_t words,
+                             int64_t n_arch, int64_t T, int32_t* u_ent, int32_t* u_cnt, int32_t* item_off,
+                             int32_t* item_tab, int64_t max_rows, int64_t min_rows, int64_t item_target,
+                             int64_t window_rows, int grouped, hgca_stream_t stream) {
+  if (window_rows < 0 || window_rows > T) return fail(HGCA_EINVAL, "union_build: bad window_rows");
   if (B < 1 || Hkv < 1 || Hq % Hkv || Hq / Hkv > 8 || n_arch < 0 || n_arch > T || words * 32 < n_arch ||
       max_rows < 16 || max_rows % 16 || min_rows < 16 || min_rows % 16 || min_rows > max_rows || item_target < 0 ||
       T >= (1 << 24))
@@ -420,9 +421,17 @@ int hgca_union_build_items(const uint32_t* sel_mask, int64_t B, int64_t Hq, int6
   if (!item_tab || !u_ent || !u_cnt || !item_off) return fail(HGCA_EINVAL, "union_build: null output");
   return cuda_status(launch_union_build(sel_mask, B, Hq, Hkv, words, n_arch, T, u_ent, u_cnt, item_off,
                                         reinterpret_cast<int4*>(item_tab), max_rows, min_rows, item_target,
-                                        (grouped == 2 || grouped == 3) ? grouped : (grouped ? 1 : 0),
+                                        window_rows, (grouped == 2 || grouped == 3) ? grouped : (grouped ? 1 : 0),
                                         S(stream)),
                      "union_build");
+}
+
+int hgca_union_build_items(const uint32_t* sel_mask, int64_t B, int64_t Hq, int64_t Hkv, int64_t words,
+                           int64_t n_arch, int64_t T, int32_t* u_ent, int32_t* u_cnt, int32_t* item_off,
+                           int32_t* item_tab, int64_t max_rows, int64_t min_rows, int64_t item_target, int grouped,
+                           hgca_stream_t stream) {
+  return hgca_union_build_items_w(sel_mask, B, Hq, Hkv, words, n_arch, T, u_ent, u_cnt, item_off, item_tab,
+                                  max_rows, min_rows, item_target, 0, grouped, stream);
 }
 
 int hgca_union_build(const uint32_t* sel_mask, int64_t B, int64_t Hq, int64_t Hkv, int64_t words,

@@ -1398,12 +1398,14 @@ __device__ __forceinline__ void item_counts(int64_t cnt, int64_t rows, int& nbig
 // yields >= target items over the union -- big steps keep long items (few
 // partials to fold), small steps get enough items for every warp.
 __global__ void item_offsets_kernel(const int32_t* u_cnt, int64_t BK, int64_t max_rows, int64_t min_rows,
-                                    int64_t target, int32_t* off) {
+                                    int64_t target, int64_t window_rows, int32_t* off) {
   __shared__ int32_t carry[2];
   __shared__ int wsum[2][32];
   __shared__ long long utot;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarp = blockDim.x >> 5;
-  if (tid == 0) utot = 0;
+  // the step's work = the unions + the dense windows (window parts use the
+  // same granularity), so a big window with a small union keeps long items
+  if (tid == 0) utot = (long long)BK * window_rows;
   __syncthreads();
   {
     long long u = 0;
@@ -1626,7 +1628,8 @@ int launch_decode_partial(int dtype, const DecodeArgs& a, cudaStream_t s) {
 
 int launch_union_build(const uint32_t* sel, int64_t B, int64_t Hq, int64_t Hkv, int64_t words, int64_t n_arch,
                        int64_t T, int32_t* u_ent, int32_t* u_cnt, int32_t* item_off, int4* item_tab,
-                       int64_t sparse_rows, int64_t min_rows, int64_t target, int grouped, cudaStream_t s) {
+                       int64_t sparse_rows, int64_t min_rows, int64_t target, int64_t window_rows, int grouped,
+                       cudaStream_t s) {
   const int64_t G = Hq / Hkv;
   union_build_kernel<<<(unsigned)(B * Hkv), 1024, 0, s>>>(sel, Hq, Hkv, G, words, n_arch, T, u_ent, u_cnt,
                                                           (grouped == 1 || grouped == 3) ? 1 : 0);
@@ -1637,7 +1640,7 @@ int launch_union_build(const uint32_t* sel, int64_t B, int64_t Hq, int64_t Hkv, 
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
-  item_offsets_kernel<<<1, 1024, 0, s>>>(u_cnt, B * Hkv, sparse_rows, min_rows, target, item_off);
+  item_offsets_kernel<<<1, 1024, 0, s>>>(u_cnt, B * Hkv, sparse_rows, min_rows, target, window_rows, item_off);
   e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
   item_table_kernel<<<(unsigned)(B * Hkv), 128, 0, s>>>(u_cnt, item_off, B * Hkv, item_tab);

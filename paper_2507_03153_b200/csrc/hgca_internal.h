@@ -127,8 +127,8 @@ int launch_topk_mask(const double* maw, int64_t rows, int64_t ld, int64_t n, con
 int launch_decode_partial(int dtype, const DecodeArgs& a, cudaStream_t s);
 int launch_union_build(const uint32_t* sel, int64_t B, int64_t Hq, int64_t Hkv, int64_t words,
                        int64_t n_arch, int64_t T, int32_t* u_ent, int32_t* u_cnt, int32_t* item_off,
-                       int4* item_tab, int64_t sparse_rows, int64_t min_rows, int64_t target, int grouped,
-                       cudaStream_t s);
+                       int4* item_tab, int64_t sparse_rows, int64_t min_rows, int64_t target, int64_t window_rows,
+                       int grouped, cudaStream_t s);
 int launch_write_rows(int dtype, void* KV, int64_t BH, int64_t T, int64_t D, int64_t pos,
                       const void* k_new, const void* v_new, int64_t n, cudaStream_t s);
 int decode_chunk_rows(int dtype, int64_t D);

@@ -60,6 +60,7 @@ MIN_ITEM_ROWS = int(os.environ.get("HGCA_MIN_ITEM_ROWS", "32"))
 # the item counts from an asynchronous copy of each union rebuild's item table.
 MERGE_ITEMS = int(os.environ.get("HGCA_MERGE_ITEMS", "96"))
 MERGE_SPLIT_MAX = 8
+COUNT_WINDOW = os.environ.get("HGCA_ITEMS_COUNT_WINDOW", "1") != "0"  # A/B knob: window in the item sizing
 ITEMS_PER_WARP = float(os.environ.get("HGCA_ITEMS_PER_WARP", "1"))
 
 
@@ -559,9 +560,10 @@ class HybridEngine:
         # interleaved per 32-entry window (conflict-free shared-memory reads of
         # the position-rotated rows)
         grouped = 3 if self.tdtype == torch.float32 else 2
-        _lib.call("hgca_union_build_items", ls.sel.data_ptr(), self.B, self.Hq, self.Hkv, words, n, self.T,
+        _lib.call("hgca_union_build_items_w", ls.sel.data_ptr(), self.B, self.Hq, self.Hkv, words, n, self.T,
                   ls.u_ent.data_ptr(), ls.u_cnt.data_ptr(), ls.item_off.data_ptr(), ls.item_tab.data_ptr(),
-                  ls.sparse_rows, min(MIN_ITEM_ROWS, ls.sparse_rows), ls.item_target, grouped, s)
+                  ls.sparse_rows, min(MIN_ITEM_ROWS, ls.sparse_rows), ls.item_target,
+                  min(self.cap, self.T) if COUNT_WINDOW else 0, grouped, s)
         # the new item counts, for the merge's split factor: copied behind the rebuild and
         # picked up by a later step once the copy has landed (no host synchronization)
         nbk = 2 * self.B * self.Hkv + 3
