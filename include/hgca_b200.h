@@ -187,7 +187,7 @@ int hgca_maw_ema(double* maw, int64_t rows, int64_t ld, int64_t n, const double*
  * mask value and then class-interleaved per window (3: the float32 decode
  * layout); u_cnt [B*Hkv]; and
  * the sparse work items: each list is cut into items of sparse_rows entries
- * followed by tail items of sparse_rows/4 entries covering its last sixth or
+ * followed by tail items of sparse_rows/4 entries covering its last twelfth or
  * more (all full items first, then all tail items, so the step ends on small
  * items). item_off
  * [2, B*Hkv+1] holds the full-item and tail-item prefixes, item_tab

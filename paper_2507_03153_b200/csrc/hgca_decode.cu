@@ -1367,7 +1367,7 @@ __global__ void __launch_bounds__(1024) union_window_classes_kernel(int32_t* u_e
 // item_off [2][BK+1]: row 0 = full-item prefix (row 0 [BK] = number of full
 // items), row 1 = absolute start of each bk's tail items (row 1 [BK] = total).
 #ifndef HGCA_TAIL_DIV
-#define HGCA_TAIL_DIV 6
+#define HGCA_TAIL_DIV 12  // with lazy claims a twelfth of each list suffices (6 before: round-2 A/B)
 #endif
 #ifndef HGCA_TAIL_SPLIT
 #define HGCA_TAIL_SPLIT 4
