@@ -373,7 +373,10 @@ int hgca_decode_chunk_rows(int dtype, int64_t d) { return decode_chunk_rows(dtyp
 #ifndef HGCA_BF16_ITEM_ROWS
 #define HGCA_BF16_ITEM_ROWS 256  // longest bf16 work item (rows); the fp32 kernel's is 64
 #endif
-static int64_t dense_rows_of(int dtype) { return dtype == HGCA_DTYPE_F32 ? 64 : HGCA_BF16_ITEM_ROWS; }
+#ifndef HGCA_F32_ITEM_ROWS
+#define HGCA_F32_ITEM_ROWS 64  // longest fp32 work item (rows)
+#endif
+static int64_t dense_rows_of(int dtype) { return dtype == HGCA_DTYPE_F32 ? HGCA_F32_ITEM_ROWS : HGCA_BF16_ITEM_ROWS; }
 // the shortest work item (one 32-row pipeline stage): step-adaptive items
 // (hgca_union_build_items with item_target > 0) never go below it, and the
 // dense items follow the chosen sparse granularity
