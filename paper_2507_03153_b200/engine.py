@@ -46,12 +46,12 @@ __all__ = ["CacheConfig", "EngineConfig", "StepInput", "StepOutput", "LayerState
 MODES = ("decode", "append")
 
 
-# Step-adaptive work items (hgca_union_build_items): items of small unions are
-# shortened (down to one 32-row stage) so that the union and the window give
-# every decode warp about HGCA_ITEMS_PER_WARP items (0.5: the window's items
-# count too, and half an item per warp measured best), and the dense window items follow the same
-# granularity (the decode kernel reads it from item_off); big steps keep
-# 256-row items. (An earlier A/B that shortened only the sparse items showed
+# Step-adaptive work items (hgca_union_build_items_w): items of small steps
+# are shortened (down to one 32-row stage) so that the union and the window
+# give every decode warp about HGCA_ITEMS_PER_WARP items (half an item per warp
+# measured best once the window counts), and the dense window parts follow the
+# same granularity at half length (the decode kernel reads it from item_off);
+# big steps keep 256-row items. (An earlier A/B that shortened only the sparse items showed
 # no gain -- profiles/r02_item_ab.txt: the 256-row dense items stayed the
 # critical path of small steps.)
 MIN_ITEM_ROWS = int(os.environ.get("HGCA_MIN_ITEM_ROWS", "32"))
@@ -785,7 +785,8 @@ class HybridEngine:
         BK = self.B * self.Hkv
         rows = max(int(off[2 * (BK + 1)]), 16)
         items = (off[1:BK + 1] - off[:BK]) + (off[BK + 2:2 * BK + 2] - off[BK + 1:2 * BK + 1])
-        n = int(items.max()) + -(-self.cap // rows) if BK else 0
+        dense_rows = max(min(rows, 32), rows // 2)  # window parts: half the item length (HGCA_DENSE_DIV)
+        n = int(items.max()) + -(-self.cap // dense_rows) if BK else 0
         return int(min(MERGE_SPLIT_MAX, max(1, -(-n // self.merge_items))))
 
     def _step_done(self, ls):
