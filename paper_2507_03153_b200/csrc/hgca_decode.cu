@@ -356,7 +356,8 @@ __global__ void __launch_bounds__(MergeCfg<D>::NT) decode_merge_kernel(const __g
   // the dense (m, z) (batches of EB entries per thread; batch 0 is loaded
   // before the folds). Needs only the final dense stats, so it runs inside the
   // last fold chunk, before that chunk's bulk-copy wait (its latency hides
-  // the copies); with a push exchange pending it runs after the push instead.
+  // the copies); with a push exchange pending it runs after the push, and in
+  // a split merge the dense share runs it after publishing its partial.
   bool epi_done = false;
   auto window_epilogue = [&]() {
     epi_done = true;
