@@ -48,8 +48,8 @@ MODES = ("decode", "append")
 
 # Step-adaptive work items (hgca_union_build_items_w): items of small steps
 # are shortened (down to one 32-row stage) so that the union and the window
-# give every decode warp about HGCA_ITEMS_PER_WARP items (half an item per warp
-# measured best once the window counts), and the dense window parts follow the
+# give every decode warp about HGCA_ITEMS_PER_WARP items (0.75 measured best
+# once the window counts: 0.5 shortchanges mid-size steps, 1 small ones), and the dense window parts follow the
 # same granularity at half length (the decode kernel reads it from item_off);
 # big steps keep 256-row items. (An earlier A/B that shortened only the sparse items showed
 # no gain -- profiles/r02_item_ab.txt: the 256-row dense items stayed the
@@ -62,7 +62,7 @@ MIN_ITEM_ROWS = int(os.environ.get("HGCA_MIN_ITEM_ROWS", "32"))
 MERGE_ITEMS = int(os.environ.get("HGCA_MERGE_ITEMS", "96"))
 MERGE_SPLIT_MAX = 8
 COUNT_WINDOW = os.environ.get("HGCA_ITEMS_COUNT_WINDOW", "1") != "0"  # A/B knob: window in the item sizing
-ITEMS_PER_WARP = float(os.environ.get("HGCA_ITEMS_PER_WARP", "0.5"))
+ITEMS_PER_WARP = float(os.environ.get("HGCA_ITEMS_PER_WARP", "0.75"))
 
 
 def item_target(dtype: str, G: int, D: int, dev) -> int:

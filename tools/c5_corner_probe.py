@@ -8,7 +8,7 @@ import bench  # noqa: E402
 import bench_configs  # noqa: E402
 
 out = []
-for blk, frac in ((256, 0.01), (128, 0.01), (256, 0.05), (8, 0.01)):
+for blk, frac in ((256, 0.01), (128, 0.01), (256, 0.05), (8, 0.01), (32, 0.01), (32, 0.05)):
     cfgd = dict(bench.C2, batch=4, context=65536, blk_num=blk, frac=frac)
     r = bench_configs.measure(cfgd, steps=20, warmup=3, name="C5", graph_steps=100)
     out.append(f"W{blk * 32}/{frac}: {r['graph_ms_per_step'] * 1e3:.1f}")
