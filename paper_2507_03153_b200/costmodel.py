@@ -282,9 +282,9 @@ FIXED_S = 24.5e-6   # per layer-step: launch, pipeline fill, merge tail
 B200_DECODE = DeviceSpec("b200-decode-fit", peak_flops=2.25e15, mem_bw=7.35e12)
 # Round 2, graph mode (DecodeGraph: PDL-chained replays, whole step incl. launch gaps and
 # evictions), 18 bf16 points of profiles/r02_configs_timing_final.jsonl (C3, C4, C5 sweep):
-# t = 13.4 us + bytes / 6.69 TB/s, median |error| 5.3% (profiles/r02_costmodel_check_graph.txt).
-FIXED_GRAPH_S = 13.4e-6
-B200_DECODE_GRAPH = DeviceSpec("b200-decode-graph-fit", peak_flops=2.25e15, mem_bw=6.69e12)
+# t = 13.0 us + bytes / 6.66 TB/s, median |error| 6.0% (profiles/r02_costmodel_check_graph.txt).
+FIXED_GRAPH_S = 13.0e-6
+B200_DECODE_GRAPH = DeviceSpec("b200-decode-graph-fit", peak_flops=2.25e15, mem_bw=6.66e12)
 
 
 def _decode_bytes(s: DecodeShape, union: float):
