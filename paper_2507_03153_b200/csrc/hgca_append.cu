@@ -1424,6 +1424,250 @@ __global__ void __launch_bounds__(Tc5Mx2Cfg::THREADS, 1) append_tc5_mean_x2_kern
   if (warp == 1) umma::tmem_dealloc<C::TMEM_COLS>(tmem);
 }
 
+// ------------------------------------------------------------------ tcgen05 pass 2, key-major
+// The mean-weight pass with the GEMM transposed: S^T = K Q^T puts 128 keys on
+// the TMEM lanes and NT row groups (NT * RG <= 256 query rows) on the
+// columns, so every thread owns one key and sums its weights
+// w = 2^(s * scale * log2e - (m2 + log2 z)) over each head's n_q columns in
+// registers: no cross-row reduction, no second GEMM, no weight tile in shared
+// memory. The per-row constants c = m2 + log2 z (from the fold) sit in
+// shared memory and are read as broadcasts. Only K is loaded; the two
+// accumulators are double-buffered so the QK of stage st + 1 overlaps the
+// exponentials of stage st. Warps: 0 TMA, 1 MMA issuer, 2-17 four sets of
+// four key warps (lane quarter = warp % 4): sets 0 / 2 take the even stages
+// (accumulator 0), sets 1 / 3 the odd ones, and the two sets of an
+// accumulator split its columns at a head boundary.
+template <int NT>
+struct Tc5KCfg {               // D = 128
+  static constexpr int KEYS = 128;                      // keys per stage (the M = 128 tile)
+  static constexpr int QH = NT * 128 * 128;             // one 64-column half of Q: NT*128 rows x 128 B
+  static constexpr int KH = KEYS * 128;                 // one 64-column half of a K stage
+  static constexpr int S = 4;
+  static constexpr int STAGE = 2 * KH;
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = OFF_Q + 2 * QH;
+  static constexpr int OFF_C = OFF_K + S * STAGE;       // c[NT * 128] fp32
+  static constexpr int OFF_BAR = OFF_C + NT * 128 * 4;
+  static constexpr int NBAR = 1 + 2 * S + 4;            // qfull, full[S], empty[S], afull[2], afree[2]
+  static constexpr int OFF_TM = OFF_BAR + NBAR * 8;
+  static constexpr int SMEM = OFF_TM + 16 + 1024;
+  static constexpr int ACOLS = NT * 128;                // TMEM columns per accumulator
+  static constexpr int TMEM_COLS = 2 * ACOLS;
+  static constexpr int THREADS = 18 * 32;             // TMA, MMA, 4 x 4 key warps
+};
+
+template <int NT>
+__global__ void __launch_bounds__(Tc5KCfg<NT>::THREADS, 1) append_tc5_mean_k_kernel(const __grid_constant__ AppendArgs a) {
+  using C = Tc5KCfg<NT>;
+  constexpr int D = 128;
+  extern __shared__ unsigned char sm_raw[];
+  unsigned char* sm = smem_align1024(sm_raw);
+  const int64_t nc = a.nch[0] + a.nch[1], ngrp = (a.n_rg + NT - 1) / NT;
+  const int64_t cidx = blockIdx.x % nc, t_ = blockIdx.x / nc;
+  const int64_t rg0 = (t_ % ngrp) * NT, bk = t_ / ngrp;
+  const int seg = cidx < a.nch[0] ? 0 : 1;
+  const int64_t chunk = seg ? cidx - a.nch[0] : cidx;
+  if (!a.mean[seg]) return;  // (uniform) no means wanted for this segment
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);
+  uint64_t* qfull = bars;
+  uint64_t* full = bars + 1;
+  uint64_t* empty = full + C::S;
+  uint64_t* afull = empty + C::S;
+  uint64_t* afree = afull + 2;
+  float* cst = reinterpret_cast<float*>(sm + C::OFF_C);
+  uint32_t* tm_holder = reinterpret_cast<uint32_t*>(sm + C::OFF_TM);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t p0 = a.seg_lo[seg] + chunk * ACHUNK;
+  const int64_t p1 = min(a.seg_hi[seg], p0 + ACHUNK);
+  const int64_t p0a = p0 & ~(int64_t)7;
+  const int nst = (int)((p1 - p0a + C::KEYS - 1) / C::KEYS);
+  const int64_t row0 = rg0 * a.RG;                          // first query row (of the bk's R) in this CTA
+  const int ncol = (int)min((int64_t)NT * a.RG, a.R - row0);  // whole heads (RG and R are multiples of n_q)
+  const int npad = (ncol + 15) & ~15;                       // MMA N
+  const int64_t b_ = bk / a.Hkv, kvh = bk % a.Hkv;
+  if (threadIdx.x == 0) {
+    mbar_init(qfull, 1);
+    for (int s = 0; s < C::S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&afull[b], 1);
+      mbar_init(&afree[b], 8);  // the 2 x 4 key warps of accumulator b
+    }
+    fence_mbar_init();
+  }
+  if (warp >= 2) {  // per-row exponent offsets c = m * log2e + log2 z
+    for (int j = threadIdx.x - 64; j < NT * 128; j += 512) {
+      float c = INFINITY;
+      if (j < ncol) {
+        const float* f = a.fin + ((bk * a.R + row0 + j) * 2 + seg) * 2;
+        c = f[0] * 1.4426950408889634f + log2f(f[1]);
+      }
+      cst[j] = c;
+    }
+  }
+  if (warp == 1) umma::tmem_alloc<C::TMEM_COLS>(smem_u32(tm_holder));
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+  const uint32_t tmem = *tm_holder;
+  const uint32_t sQ = smem_u32(sm + C::OFF_Q), sK = smem_u32(sm + C::OFF_K);
+
+  if (warp == 0) {  // ------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const uint64_t policy = l2_evict_first_policy();
+      const int qrow = (int)((b_ * a.Hq + kvh * a.G) * a.nq + row0);
+      mbar_expect_tx(qfull, 2 * C::QH);
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        tma_load_2d(sQ + t * 128 * 128, &a.qmap5, 0, qrow + t * 128, qfull, policy);
+        tma_load_2d(sQ + C::QH + t * 128 * 128, &a.qmap5, 64, qrow + t * 128, qfull, policy);
+      }
+      const int rowbase = (int)(bk * a.T + p0a);
+      for (int st = 0; st < nst; ++st) {
+        const int s = st % C::S;
+        if (st >= C::S) mbar_wait(&empty[s], ((st / C::S) - 1) & 1);
+        mbar_expect_tx(&full[s], C::STAGE);
+        const uint32_t kb = sK + s * C::STAGE;
+        const int r = rowbase + st * C::KEYS;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          tma_load_2d(kb + h * C::KH, &a.kvmap5, 64 * h, r, &full[s], policy);
+          tma_load_2d(kb + h * C::KH + T5_KEYS * 128, &a.kvmap5, 64 * h, r + T5_KEYS, &full[s], policy);
+        }
+      }
+    }
+  } else if (warp == 1) {  // ------------------------------------------- MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = umma::idesc_bf16_f32(128, npad, false, false);
+      mbar_wait(qfull, 0);
+      umma::fence_after_sync();
+      for (int st = 0; st < nst; ++st) {
+        const int s = st % C::S, b = st & 1;
+        mbar_wait(&full[s], (st / C::S) & 1);
+        if (st >= 2) mbar_wait(&afree[b], ((st - 2) >> 1) & 1);  // accumulator b read out (stage st - 2)
+        umma::fence_after_sync();
+        const uint32_t kb = sK + s * C::STAGE;
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint64_t ad = umma::smem_desc(kb + (k / 4) * C::KH + (k % 4) * 32, 16, 1024);
+          const uint64_t bd = umma::smem_desc(sQ + (k / 4) * C::QH + (k % 4) * 32, 16, 1024);
+          umma::mma_bf16(tmem + b * C::ACOLS, ad, bd, idesc, k > 0);
+        }
+        umma::commit(smem_u32(&afull[b]));
+        umma::commit(smem_u32(&empty[s]));
+      }
+    }
+    __syncwarp();
+  } else {  // ---------------------------------------------------------- key warps
+    const int set = (warp - 2) >> 2, quarter = warp & 3;
+    const int b = set & 1;  // this set's stages st = b, b + 2, ... (accumulator b)
+    const uint32_t tl = (uint32_t)(quarter * 32) << 16;
+    const float sl2 = a.scale * 1.4426950408889634f;
+    const float inv_nq = 1.f / (float)a.nq;
+    const int nq = (int)a.nq;
+    const int64_t ld = a.mean_ld[seg];
+    const int W = nq % 32 == 0 ? 32 : nq == 16 ? 16 : nq == 8 ? 8 : 0;  // whole heads per sum group
+    // the two sets of an accumulator split its columns at a head boundary
+    // (when that boundary is a 32-column one; else the first set takes all)
+    const int csplit = (ncol / nq / 2) * nq;
+    const bool split = csplit > 0 && csplit % 32 == 0;
+    const int cbeg = (set >> 1) ? (split ? csplit : ncol) : 0;
+    const int cend = (set >> 1) ? ncol : (split ? csplit : ncol);
+    float* const mrow = a.mean[seg] + (b_ * a.Hq + kvh * a.G + (row0 + cbeg) / a.nq) * ld - a.seg_lo[seg];
+    for (int st = b; st < nst; st += 2) {
+      const int64_t key = p0a + (int64_t)st * C::KEYS + quarter * 32 + lane;
+      const bool mine = key >= p0 && key < p1;
+      float* mp = mrow + key;
+      mbar_wait(&afull[b], (st >> 1) & 1);
+      umma::fence_after_sync();
+      if (cbeg >= cend) {  // (uniform) nothing for this set
+        umma::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&afree[b]);
+        continue;
+      }
+      float hs = 0.f;
+      int left = nq;
+      for (int c0 = cbeg; c0 < cend; c0 += 32) {
+        float x[32];
+        {
+          uint32_t v[2][16];
+          umma::ld_32x32b_x16(tmem + tl + b * C::ACOLS + c0, v[0]);
+          umma::ld_32x32b_x16(tmem + tl + b * C::ACOLS + c0 + 16, v[1]);
+          umma::ld_wait();
+          if (c0 + 32 >= cend) {  // the accumulator is in registers: QK(st + 2) may overwrite it
+            umma::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&afree[b]);
+          }
+#pragma unroll
+          for (int e = 0; e < 32; ++e) x[e] = __uint_as_float(v[e >> 4][e & 15]);
+        }
+        // exponents first, then the exponentials: independent chains for the scheduler
+#pragma unroll
+        for (int e4 = 0; e4 < 8; ++e4) {
+          const float4 c4 = *reinterpret_cast<const float4*>(cst + c0 + e4 * 4);
+          x[e4 * 4 + 0] = fmaf(x[e4 * 4 + 0], sl2, -c4.x);
+          x[e4 * 4 + 1] = fmaf(x[e4 * 4 + 1], sl2, -c4.y);
+          x[e4 * 4 + 2] = fmaf(x[e4 * 4 + 2], sl2, -c4.z);
+          x[e4 * 4 + 3] = fmaf(x[e4 * 4 + 3], sl2, -c4.w);
+        }
+#pragma unroll
+        for (int e = 0; e < 32; ++e) x[e] = ex2_approx(x[e]);
+        if (W) {  // sum groups of 8 columns (a tree each); heads are whole groups
+          float g8[4];
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+            g8[g] = ((x[g * 8] + x[g * 8 + 1]) + (x[g * 8 + 2] + x[g * 8 + 3])) +
+                    ((x[g * 8 + 4] + x[g * 8 + 5]) + (x[g * 8 + 6] + x[g * 8 + 7]));
+          if (W == 8) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g)
+              if (c0 + g * 8 < cend) {
+                if (mine) *mp = g8[g] * inv_nq;
+                mp += ld;
+              }
+          } else if (W == 16) {
+#pragma unroll
+            for (int g = 0; g < 2; ++g)
+              if (c0 + g * 16 < cend) {
+                if (mine) *mp = (g8[2 * g] + g8[2 * g + 1]) * inv_nq;
+                mp += ld;
+              }
+          } else {
+            hs += (g8[0] + g8[1]) + (g8[2] + g8[3]);
+            left -= 32;
+            if (left == 0) {
+              if (mine) *mp = hs * inv_nq;
+              mp += ld;
+              hs = 0.f;
+              left = nq;
+            }
+          }
+        } else {  // other n_q: column by column
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            if (c0 + e < cend) {
+              hs += x[e];
+              if (--left == 0) {
+                if (mine) *mp = hs * inv_nq;
+                mp += ld;
+                hs = 0.f;
+                left = nq;
+              }
+            }
+          }
+        }
+      }
+    }
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  if (warp == 1) umma::tmem_dealloc<C::TMEM_COLS>(tmem);
+}
+
 // One warp per (b, kv-head, row): fold the chunk partials of both segments,
 // merge_states(archive, window) (attention.py:153-188), out / lse, and the
 // row's final (m, z) per segment for pass 2.
@@ -1636,7 +1880,22 @@ static int launch_append_d(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, i
         if (const int em = set_smem_dev(append_tc5_mean_kernel, Tc5MCfg::SMEM, attr_m)) return em;
         if (const int em2 = set_smem_dev(append_tc5_mean_x2_kernel, Tc5Mx2Cfg::SMEM, attr_m2)) return em2;
       }
-      if (tc5_mean && p.RG == 128 && p.n_rg >= 2)  // pairs of 128-row groups share the K stream
+      // key-major pass (default; HGCA_APPEND_MEAN_OLD=1: the row-major pass with the head-sum GEMM);
+      // two row groups per CTA share the K stream (HGCA_APPEND_MEAN_NT=1: one)
+      const char* old_mean = getenv("HGCA_APPEND_MEAN_OLD");
+      const char* nt_env = getenv("HGCA_APPEND_MEAN_NT");
+      const bool km = tc5_mean && !(old_mean && *old_mean && *old_mean != '0');
+      const bool km2 = km && p.n_rg >= 2 && !(nt_env && *nt_env == '1');
+      static DevFlags attr_k1, attr_k2;
+      const int64_t nc = p.nch0 + p.nch1;
+      if (km2) {
+        if (const int ek = set_smem_dev(append_tc5_mean_k_kernel<2>, Tc5KCfg<2>::SMEM, attr_k2)) return ek;
+        append_tc5_mean_k_kernel<2><<<(unsigned)(B * Hkv * ((p.n_rg + 1) / 2) * nc), Tc5KCfg<2>::THREADS,
+                                      Tc5KCfg<2>::SMEM, s>>>(a);
+      } else if (km) {
+        if (const int ek = set_smem_dev(append_tc5_mean_k_kernel<1>, Tc5KCfg<1>::SMEM, attr_k1)) return ek;
+        append_tc5_mean_k_kernel<1><<<(unsigned)(B * Hkv * p.n_rg * nc), Tc5KCfg<1>::THREADS, Tc5KCfg<1>::SMEM, s>>>(a);
+      } else if (tc5_mean && p.RG == 128 && p.n_rg >= 2)  // pairs of 128-row groups share the K stream
         append_tc5_mean_x2_kernel<<<(unsigned)(B * Hkv * ((p.n_rg + 1) / 2) * (p.nch0 + p.nch1)), Tc5Mx2Cfg::THREADS,
                                     Tc5Mx2Cfg::SMEM, s>>>(a);
       else if (tc5_mean)
