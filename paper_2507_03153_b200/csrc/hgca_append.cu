@@ -29,6 +29,7 @@
 
 #include <cuda.h>
 #include <cstdlib>
+#include <type_traits>
 
 namespace hgca {
 
@@ -42,6 +43,7 @@ struct AppendArgs {
   CUtensorMap kmap;             // 2-D tile map over KV [B*Hkv*T rows, 2D], box {2D, 32}
   CUtensorMap kvmap5;           // tcgen05 pass: over KV [B*Hkv*T rows, 2D], box {64, 64}, no swizzle
   CUtensorMap qmap5;            // tcgen05 pass: over q [B*Hq*nq rows, D], box {64, 128}, 128-byte swizzle
+  CUtensorMap qmap5h;           // the same with box {64, 64}: a 64-row group loaded twice (split-key pass 1)
   const __nv_bfloat16* q;       // [B*Hq, nq, D]
   int64_t B, Hq, Hkv, G, T, nq;
   float scale;
@@ -57,6 +59,7 @@ struct AppendArgs {
   double* lse;                   // [B*Hq, nq]
   float* mean[2];                // [B*Hq, mean_ld] mean weights per position, or null
   int64_t mean_ld[2];
+  int split_keys;                // pass 1 on 64-row groups: the split-key mode (HGCA_APPEND_SPLIT_KEYS=0: off)
 };
 
 template <int D, int PASS>
@@ -402,6 +405,13 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
   const int64_t p1 = min(a.seg_hi[seg], p0 + ACHUNK);
   const int64_t p0a = p0 & ~(int64_t)7;  // 8-aligned stage base: rotation == swizzle phase
   const int nst = (int)((p1 - p0a + T5_KEYS - 1) / T5_KEYS);
+  // split-key mode for 64-row groups: the group is loaded twice (TMEM lanes
+  // 0-63 and 64-127), the first copy's softmax threads take keys 0-31 of every
+  // stage, the second copy's keys 32-63 (their other P half stays zero), so
+  // all four softmax warps work and each row's per-stage chain is halved; the
+  // two copies' (m, z, O) are merged in the epilogue
+  const bool dup = a.RG == 64 && a.split_keys;
+  const int nsw = dup ? 4 : (int)((a.RG + 31) / 32);
   if (threadIdx.x == 0) {
     mbar_init(qfull, 1);
     for (int s = 0; s < T5_S; ++s) {
@@ -410,8 +420,8 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&sfull[b], 1);
-      mbar_init(&pfull[b], (int)((a.RG + 31) / 32));  // one arrive per softmax warp that owns rows
-      mbar_init(&sfree[b], (int)((a.RG + 31) / 32));
+      mbar_init(&pfull[b], nsw);  // one arrive per softmax warp that owns rows
+      mbar_init(&sfree[b], nsw);
     }
     mbar_init(&pvdone[0], 1);
     mbar_init(&pvdone[1], 1);
@@ -420,13 +430,23 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
   // Row groups of < 128 rows (e.g. n_q = 16 at G = 4: 64 rows): the softmax
   // warps of the padding quarters skip the stages entirely; their P rows stay
   // zero (written once here), so the padding O rows are zero and unused.
-  if (warp >= 2 && warp < 6 && (warp & 3) * 32 >= a.RG) {
+  if (warp >= 2 && warp < 6 && !dup && (warp & 3) * 32 >= a.RG) {
     const int r = (warp & 3) * 32 + lane;
     unsigned char* prow0 = sm + C::OFF_P + (r >> 3) * 1024 + (r & 7) * 128;
 #pragma unroll
     for (int bb = 0; bb < 4; ++bb)
 #pragma unroll
       for (int c = 0; c < 8; ++c) *reinterpret_cast<uint4*>(prow0 + bb * C::PBUF + c * 16) = make_uint4(0, 0, 0, 0);
+    umma::fence_smem_async();
+  }
+  if (warp >= 2 && warp < 6 && dup) {  // split keys: zero the half of each P row this copy never writes
+    const int L = (warp & 3) * 32 + lane, oh = 1 - ((warp & 3) >> 1);
+    unsigned char* prow0 = sm + C::OFF_P + (L >> 3) * 1024 + (L & 7) * 128;
+#pragma unroll
+    for (int bb = 0; bb < 4; ++bb)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        *reinterpret_cast<uint4*>(prow0 + bb * C::PBUF + (((oh * 4 + c) ^ (L & 7)) << 4)) = make_uint4(0, 0, 0, 0);
     umma::fence_smem_async();
   }
   if (warp == 1) umma::tmem_alloc<C::TMEM_COLS>(smem_u32(tm_holder));
@@ -442,8 +462,16 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
       const int64_t b = bk / a.Hkv, kvh = bk % a.Hkv;
       const int qrow = (int)((b * a.Hq + kvh * a.G) * a.nq + rg * a.RG);
       mbar_expect_tx(qfull, 2 * C::QATOM);
-      tma_load_2d(sQ, &a.qmap5, 0, qrow, qfull, policy);
-      tma_load_2d(sQ + C::QATOM, &a.qmap5, 64, qrow, qfull, policy);
+      if (dup) {  // rows 0-63 and again 64-127 (same swizzle phase: 8 KB apart)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          tma_load_2d(sQ + h * C::QATOM, &a.qmap5h, 64 * h, qrow, qfull, policy);
+          tma_load_2d(sQ + h * C::QATOM + 64 * 128, &a.qmap5h, 64 * h, qrow, qfull, policy);
+        }
+      } else {
+        tma_load_2d(sQ, &a.qmap5, 0, qrow, qfull, policy);
+        tma_load_2d(sQ + C::QATOM, &a.qmap5, 64, qrow, qfull, policy);
+      }
       const int rowbase = (int)(bk * a.T + p0a);
       for (int st = 0; st < nst; ++st) {
         const int s = st % T5_S;
@@ -501,123 +529,165 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
       }
     }
     __syncwarp();
-  } else if ((warp & 3) * 32 < a.RG) {  // ---------------------------- softmax warps (rows)
+  } else if (dup || (warp & 3) * 32 < a.RG) {  // -------------------- softmax warps (rows)
     const int quarter = warp & 3;
-    const int r = quarter * 32 + lane;          // row of the group == TMEM lane
+    const int L = quarter * 32 + lane;                   // TMEM lane == P row
+    const int hh = dup ? (quarter >> 1) : 0;             // split keys: which half of each stage
+    const int r = dup ? (quarter & 1) * 32 + lane : L;   // row of the group
     const uint32_t tl = (uint32_t)(quarter * 32) << 16;
     // softmax in log2 units: x = s * log2(e), p = 2^(x - mu2) == exp(s - mu2 * ln 2)
     const float sl2 = a.scale * 1.4426950408889634f;
     float mu2 = -INFINITY, z = 0.f;             // reference max (log2 units), sum of p
-    const uint32_t prow = (uint32_t)((r >> 3) * 1024 + (r & 7) * 128);
+    const uint32_t prow = (uint32_t)((L >> 3) * 1024 + (L & 7) * 128);
     P5(long long w_s = 0, w_pv = 0, t_s0 = clock64();)
-    for (int st = 0; st < nst; ++st) {
-      const int b = st & 1;
-      P5(long long c0 = clock64();)
-      mbar_wait(&sfull[b], (st >> 1) & 1);
-      P5(w_s += clock64() - c0;)
-      umma::fence_after_sync();
-      float x[T5_KEYS];
-      {
-        uint32_t v[4][16];  // all four loads in flight, one wait
+    auto stages = [&](auto nk_c) {
+      constexpr int NK = decltype(nk_c)::value;  // keys of a stage this thread takes
+      for (int st = 0; st < nst; ++st) {
+        const int b = st & 1;
+        P5(long long c0 = clock64();)
+        mbar_wait(&sfull[b], (st >> 1) & 1);
+        P5(w_s += clock64() - c0;)
+        umma::fence_after_sync();
+        float x[NK];
+        {
+          uint32_t v[NK / 16][16];  // all loads in flight, one wait
 #pragma unroll
-        for (int c = 0; c < 4; ++c) umma::ld_32x32b_x16(tmem + tl + b * T5_KEYS + c * 16, v[c]);
-        umma::ld_wait();
+          for (int c = 0; c < NK / 16; ++c) umma::ld_32x32b_x16(tmem + tl + b * T5_KEYS + hh * 32 + c * 16, v[c]);
+          umma::ld_wait();
+          umma::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sfree[b]);  // S(st) is in registers: QK(st + 2) may overwrite it
+#pragma unroll
+          for (int c = 0; c < NK / 16; ++c)
+#pragma unroll
+            for (int j = 0; j < 16; ++j) x[c * 16 + j] = __uint_as_float(v[c][j]);
+        }
+        const int64_t kp0 = p0a + (int64_t)st * T5_KEYS + hh * 32;
+        float mx = -INFINITY;
+        if (kp0 >= p0 && kp0 + NK <= p1) {  // every key of the part is in range (warp-uniform)
+#pragma unroll
+          for (int j = 0; j < NK; ++j) {
+            x[j] *= sl2;
+            mx = fmaxf(mx, x[j]);
+          }
+        } else {
+          const int jlo = (int)max(min(p0 - kp0, (int64_t)NK), (int64_t)0);
+          const int jhi = (int)max(min(p1 - kp0, (int64_t)NK), (int64_t)0);
+#pragma unroll
+          for (int j = 0; j < NK; ++j) {
+            x[j] = (j >= jlo && j < jhi) ? x[j] * sl2 : -INFINITY;
+            mx = fmaxf(mx, x[j]);
+          }
+        }
+        float alpha = 1.f;
+        if (mx > mu2 + T5_HEADROOM2) {  // raise the reference max (also the first finite score)
+          alpha = mu2 == -INFINITY ? 0.f : ex2_approx(mu2 - mx);
+          mu2 = mx;
+        }
+        float sum = 0.f;
+        const float mref = mu2 == -INFINITY ? 0.f : mu2;  // a split-key half may not have seen a key yet
+#pragma unroll
+        for (int j = 0; j < NK; ++j) {
+          x[j] = ex2_approx(x[j] - mref);  // masked keys: 2^-inf = 0
+          sum += x[j];
+        }
+        z = z * alpha + sum;
+        // P buffer b was last read by PV(st-2)
+        P5(long long c1 = clock64();)
+        if (st >= 2) mbar_wait(&pvdone[b], ((st - 2) >> 1) & 1);
+        P5(w_pv += clock64() - c1;)
+        if (st >= 1 && __any_sync(FULL_MASK, alpha != 1.f)) {
+          // rescale the rows' O once PV(st-1) has completed (PV(st) waits for this
+          // stage's P, released below); warp-collective TMEM ld / st
+          mbar_wait(&pvdone[b ^ 1], ((st - 1) >> 1) & 1);
+          umma::fence_after_sync();
+          {
+#pragma unroll
+            for (int c0 = 0; c0 < D; c0 += 16) {
+              uint32_t v[16];
+              umma::ld_32x32b_x16(tmem + tl + O_COL + c0, v);
+              umma::ld_wait();
+#pragma unroll
+              for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * alpha);
+              umma::st_32x32b_x16(tmem + tl + O_COL + c0, v);
+            }
+            umma::st_wait();
+          }
+        }
+        unsigned char* ph = sm + C::OFF_P + (b * 2) * C::PBUF + prow;
+        unsigned char* pl = ph + C::PBUF;
+#pragma unroll
+        for (int c = 0; c < NK / 8; ++c) {
+          uint32_t hi[4], lo[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            hi[e] = pack_bf16(x[c * 8 + 2 * e], x[c * 8 + 2 * e + 1]);
+            lo[e] = pack_bf16(x[c * 8 + 2 * e] - bf16_lo_f(hi[e]), x[c * 8 + 2 * e + 1] - bf16_hi_f(hi[e]));
+          }
+          const uint32_t off = (uint32_t)(((hh * 4 + c) ^ (L & 7)) << 4);
+          *reinterpret_cast<uint4*>(ph + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+          *reinterpret_cast<uint4*>(pl + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        }
+        umma::fence_smem_async();  // P (generic stores) -> visible to the tensor core
         umma::fence_before_sync();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sfree[b]);  // S(st) is in registers: QK(st + 2) may overwrite it
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-#pragma unroll
-          for (int j = 0; j < 16; ++j) x[c * 16 + j] = __uint_as_float(v[c][j]);
+        if (lane == 0) mbar_arrive(&pfull[b]);
       }
-      const int64_t kp0 = p0a + (int64_t)st * T5_KEYS;
-      float mx = -INFINITY;
-      if (kp0 >= p0 && kp0 + T5_KEYS <= p1) {  // every key of the stage is in range (warp-uniform)
-#pragma unroll
-        for (int j = 0; j < T5_KEYS; ++j) {
-          x[j] *= sl2;
-          mx = fmaxf(mx, x[j]);
-        }
-      } else {
-        const int jlo = (int)max(p0 - kp0, (int64_t)0), jhi = (int)min(p1 - kp0, (int64_t)T5_KEYS);
-#pragma unroll
-        for (int j = 0; j < T5_KEYS; ++j) {
-          x[j] = (j >= jlo && j < jhi) ? x[j] * sl2 : -INFINITY;
-          mx = fmaxf(mx, x[j]);
-        }
-      }
-      float alpha = 1.f;
-      if (mx > mu2 + T5_HEADROOM2) {  // raise the reference max (also the first finite score)
-        alpha = mu2 == -INFINITY ? 0.f : ex2_approx(mu2 - mx);
-        mu2 = mx;
-      }
-      float sum = 0.f;
-#pragma unroll
-      for (int j = 0; j < T5_KEYS; ++j) {
-        x[j] = ex2_approx(x[j] - mu2);  // masked keys: 2^-inf = 0
-        sum += x[j];
-      }
-      z = z * alpha + sum;
-      // P buffer b was last read by PV(st-2)
-      P5(long long c1 = clock64();)
-      if (st >= 2) mbar_wait(&pvdone[b], ((st - 2) >> 1) & 1);
-      P5(w_pv += clock64() - c1;)
-      if (st >= 1 && __any_sync(FULL_MASK, alpha != 1.f)) {
-        // rescale the rows' O once PV(st-1) has completed (PV(st) waits for this
-        // stage's P, released below); warp-collective TMEM ld / st
-        mbar_wait(&pvdone[b ^ 1], ((st - 1) >> 1) & 1);
-        umma::fence_after_sync();
-        {
-#pragma unroll
-          for (int c0 = 0; c0 < D; c0 += 16) {
-            uint32_t v[16];
-            umma::ld_32x32b_x16(tmem + tl + O_COL + c0, v);
-            umma::ld_wait();
-#pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * alpha);
-            umma::st_32x32b_x16(tmem + tl + O_COL + c0, v);
-          }
-          umma::st_wait();
-        }
-      }
-      unsigned char* ph = sm + C::OFF_P + (b * 2) * C::PBUF + prow;
-      unsigned char* pl = ph + C::PBUF;
-#pragma unroll
-      for (int c = 0; c < T5_KEYS / 8; ++c) {
-        uint32_t hi[4], lo[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          hi[e] = pack_bf16(x[c * 8 + 2 * e], x[c * 8 + 2 * e + 1]);
-          lo[e] = pack_bf16(x[c * 8 + 2 * e] - bf16_lo_f(hi[e]), x[c * 8 + 2 * e + 1] - bf16_hi_f(hi[e]));
-        }
-        const uint32_t off = (uint32_t)((c ^ (r & 7)) << 4);
-        *reinterpret_cast<uint4*>(ph + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-        *reinterpret_cast<uint4*>(pl + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-      }
-      umma::fence_smem_async();  // P (generic stores) -> visible to the tensor core
-      umma::fence_before_sync();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&pfull[b]);
-    }
+    };
+    if (dup) stages(std::integral_constant<int, 32>{});
+    else stages(std::integral_constant<int, T5_KEYS>{});
     mbar_wait(&pvdone[(nst - 1) & 1], ((nst - 1) >> 1) & 1);  // the last PV (and all before it)
     P5(if (warp == 2 && lane == 0) { atomicAdd(&g_tc5prof[3], (unsigned long long)w_s);
        atomicAdd(&g_tc5prof[6], (unsigned long long)nst);
        atomicAdd(&g_tc5prof[4], (unsigned long long)w_pv); atomicAdd(&g_tc5prof[5], (unsigned long long)(clock64() - t_s0)); })
     umma::fence_after_sync();
-    // this row's partial (m, z, acc), as append_attend_kernel<D, 1> writes it
-    const bool mine = r < a.RG && rg * a.RG + r < a.R;
+    // this row's partial (m, z, acc), as append_attend_kernel<D, 1> writes it;
+    // split keys: the second copy (lanes 64-127) hands its (m, z, O) to the
+    // first through shared memory (the P buffers: every PV is complete)
+    float fa = 1.f, fb = 0.f;
+    float* ob = reinterpret_cast<float*>(sm + C::OFF_P);  // [D][64] column-major: conflict-free
+    float* mzb = ob + D * 64;                             // [64][2]
+    if (dup) {
+      if (hh) {
+#pragma unroll
+        for (int c0 = 0; c0 < D; c0 += 16) {
+          uint32_t v[16];
+          umma::ld_32x32b_x16(tmem + tl + O_COL + c0, v);
+          umma::ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) ob[(c0 + j) * 64 + r] = __uint_as_float(v[j]);
+        }
+        mzb[r * 2] = mu2;
+        mzb[r * 2 + 1] = z;
+      }
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");  // the four softmax warps
+      if (!hh) {
+        const float mb = mzb[r * 2], zb = mzb[r * 2 + 1];
+        const float mm = fmaxf(mu2, mb);
+        if (mm != -INFINITY) {
+          fa = mu2 == -INFINITY ? 0.f : ex2_approx(mu2 - mm);
+          fb = mb == -INFINITY ? 0.f : ex2_approx(mb - mm);
+        }
+        z = z * fa + zb * fb;
+        mu2 = mm;
+      }
+    }
+    const bool mine = (!dup || !hh) && r < a.RG && rg * a.RG + r < a.R;
     const int64_t item = blockIdx.x;
     float4* pa = reinterpret_cast<float4*>(a.part_acc + (item * a.RG + r) * D);
+    if (!dup || !hh) {
 #pragma unroll
-    for (int c0 = 0; c0 < D; c0 += 16) {
-      uint32_t v[16];
-      umma::ld_32x32b_x16(tmem + tl + O_COL + c0, v);
-      umma::ld_wait();
-      if (mine) {
+      for (int c0 = 0; c0 < D; c0 += 16) {
+        uint32_t v[16];
+        umma::ld_32x32b_x16(tmem + tl + O_COL + c0, v);
+        umma::ld_wait();
+        float o[16];
 #pragma unroll
-        for (int j = 0; j < 16; j += 4)
-          pa[(c0 + j) / 4] = make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
-                                         __uint_as_float(v[j + 3]));
+        for (int j = 0; j < 16; ++j) o[j] = dup ? __uint_as_float(v[j]) * fa + ob[(c0 + j) * 64 + r] * fb : __uint_as_float(v[j]);
+        if (mine) {
+#pragma unroll
+          for (int j = 0; j < 16; j += 4) pa[(c0 + j) / 4] = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
+        }
       }
     }
     if (mine) {
@@ -1845,6 +1915,10 @@ static int launch_append_d(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, i
       if (rc5) return rc5;
       const int rc = make_map2d(&a.qmap5, q, B * Hq * nq, D, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
       if (rc) return rc;
+      const int rch = make_map2d(&a.qmap5h, q, B * Hq * nq, D, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B);
+      if (rch) return rch;
+      const char* sk = getenv("HGCA_APPEND_SPLIT_KEYS");
+      a.split_keys = !(sk && *sk == '0');
     }
     static DevFlags attr5;
     if (const int e5 = set_smem_dev(append_tc5_kernel, Tc5Cfg::SMEM, attr5)) return e5;
