@@ -648,6 +648,9 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
     float* ob = reinterpret_cast<float*>(sm + C::OFF_P);  // [D][64] column-major: conflict-free
     float* mzb = ob + D * 64;                             // [64][2]
     if (dup) {
+      // (ordered already through pfull -> PV -> pvdone; the barrier makes the
+      // P-region reuse explicit for the race checker, once per CTA)
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");
       if (hh) {
 #pragma unroll
         for (int c0 = 0; c0 < D; c0 += 16) {
