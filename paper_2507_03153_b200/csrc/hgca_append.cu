@@ -358,6 +358,32 @@ __device__ __forceinline__ float ex2_approx(float x) {  // 2^x; 2^-inf = +0
   return y;
 }
 
+// max / sum of a register row with 8 independent chains (a serial chain of
+// N dependent FMNMX / FADD was a large part of the per-stage softmax latency)
+template <int N>
+__device__ __forceinline__ float row_max8(const float (&x)[N]) {
+  static_assert(N % 8 == 0, "row_max8");
+  float m[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) m[i] = x[i];
+#pragma unroll
+  for (int j = 8; j < N; j += 8)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) m[i] = fmaxf(m[i], x[j + i]);
+  return fmaxf(fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3])), fmaxf(fmaxf(m[4], m[5]), fmaxf(m[6], m[7])));
+}
+template <int N>
+__device__ __forceinline__ float row_sum8(const float (&x)[N]) {
+  float m[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) m[i] = x[i];
+#pragma unroll
+  for (int j = 8; j < N; j += 8)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) m[i] += x[j + i];
+  return ((m[0] + m[1]) + (m[2] + m[3])) + ((m[4] + m[5]) + (m[6] + m[7]));
+}
+
 struct Tc5Cfg {               // D = 128
   static constexpr int QATOM = 128 * 128;               // 128 rows x 64 bf16 (16 KB)
   static constexpr int KVQ = T5_KEYS * 128;             // 64 keys x 64 bf16 (8 KB)
@@ -563,35 +589,22 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
             for (int j = 0; j < 16; ++j) x[c * 16 + j] = __uint_as_float(v[c][j]);
         }
         const int64_t kp0 = p0a + (int64_t)st * T5_KEYS + hh * 32;
-        float mx = -INFINITY;
-        if (kp0 >= p0 && kp0 + NK <= p1) {  // every key of the part is in range (warp-uniform)
-#pragma unroll
-          for (int j = 0; j < NK; ++j) {
-            x[j] *= sl2;
-            mx = fmaxf(mx, x[j]);
-          }
-        } else {
+        if (!(kp0 >= p0 && kp0 + NK <= p1)) {  // a partial part (warp-uniform): mask the keys out of range
           const int jlo = (int)max(min(p0 - kp0, (int64_t)NK), (int64_t)0);
           const int jhi = (int)max(min(p1 - kp0, (int64_t)NK), (int64_t)0);
 #pragma unroll
-          for (int j = 0; j < NK; ++j) {
-            x[j] = (j >= jlo && j < jhi) ? x[j] * sl2 : -INFINITY;
-            mx = fmaxf(mx, x[j]);
-          }
+          for (int j = 0; j < NK; ++j) x[j] = (j >= jlo && j < jhi) ? x[j] : -INFINITY;
         }
+        const float mx = row_max8(x) * sl2;  // the scale is positive: max commutes with it
         float alpha = 1.f;
         if (mx > mu2 + T5_HEADROOM2) {  // raise the reference max (also the first finite score)
           alpha = mu2 == -INFINITY ? 0.f : ex2_approx(mu2 - mx);
           mu2 = mx;
         }
-        float sum = 0.f;
         const float mref = mu2 == -INFINITY ? 0.f : mu2;  // a split-key half may not have seen a key yet
 #pragma unroll
-        for (int j = 0; j < NK; ++j) {
-          x[j] = ex2_approx(x[j] - mref);  // masked keys: 2^-inf = 0
-          sum += x[j];
-        }
-        z = z * alpha + sum;
+        for (int j = 0; j < NK; ++j) x[j] = ex2_approx(fmaf(x[j], sl2, -mref));  // masked keys: 2^-inf = 0
+        z = z * alpha + row_sum8(x);
         // P buffer b was last read by PV(st-2)
         P5(long long c1 = clock64();)
         if (st >= 2) mbar_wait(&pvdone[b], ((st - 2) >> 1) & 1);
@@ -871,33 +884,20 @@ __global__ void __launch_bounds__(Tc5x2Cfg::THREADS, 1) append_tc5x2_kernel(cons
             for (int j = 0; j < 16; ++j) x[c * 16 + j] = __uint_as_float(v[c][j]);
         }
         const int64_t kp0 = p0a + (int64_t)st * T5_KEYS;
-        float mx = -INFINITY;
-        if (kp0 >= p0 && kp0 + T5_KEYS <= p1) {
-#pragma unroll
-          for (int j = 0; j < T5_KEYS; ++j) {
-            x[j] *= sl2;
-            mx = fmaxf(mx, x[j]);
-          }
-        } else {
+        if (!(kp0 >= p0 && kp0 + T5_KEYS <= p1)) {
           const int jlo = (int)max(p0 - kp0, (int64_t)0), jhi = (int)min(p1 - kp0, (int64_t)T5_KEYS);
 #pragma unroll
-          for (int j = 0; j < T5_KEYS; ++j) {
-            x[j] = (j >= jlo && j < jhi) ? x[j] * sl2 : -INFINITY;
-            mx = fmaxf(mx, x[j]);
-          }
+          for (int j = 0; j < T5_KEYS; ++j) x[j] = (j >= jlo && j < jhi) ? x[j] : -INFINITY;
         }
+        const float mx = row_max8(x) * sl2;
         float alpha = 1.f;
         if (mx > mu2 + T5_HEADROOM2) {
           alpha = mu2 == -INFINITY ? 0.f : ex2_approx(mu2 - mx);
           mu2 = mx;
         }
-        float sum = 0.f;
 #pragma unroll
-        for (int j = 0; j < T5_KEYS; ++j) {
-          x[j] = ex2_approx(x[j] - mu2);
-          sum += x[j];
-        }
-        z = z * alpha + sum;
+        for (int j = 0; j < T5_KEYS; ++j) x[j] = ex2_approx(fmaf(x[j], sl2, -mu2));
+        z = z * alpha + row_sum8(x);
         if (st >= 1) {  // the tile's PV(st-1): P free again, O stable for a rescale
           mbar_wait(&pvdone[t * 2 + (b ^ 1)], ((st - 1) >> 1) & 1);
           umma::fence_after_sync();
