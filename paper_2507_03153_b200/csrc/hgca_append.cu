@@ -721,18 +721,21 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
 // takes two row groups (tiles) against the same keys, so each K|V stage is
 // loaded once for both, and the tiles' softmax warps (4 each) run side by side
 // while the tensor core works on the other tile (as FA4 ping-pongs two Q tiles).
-// Per tile: S double-buffered in TMEM, P (hi, lo) single-buffered in shared
-// memory (rewritten after the tile's previous P V completed), O in TMEM.
+// Per tile: S double-buffered in TMEM; P (bf16 hi, lo: 32 + 32 columns) is
+// written back over its own S buffer and P V reads the A operand from TMEM
+// (no shared-memory P, so a tile's softmax never waits for its previous P V
+// except to rescale O; the freed shared memory holds more K|V stages); O in TMEM.
+#ifndef HGCA_X2_STAGES
+#define HGCA_X2_STAGES 4
+#endif
 struct Tc5x2Cfg {              // D = 128
   static constexpr int QATOM = 128 * 128;
   static constexpr int KVQ = T5_KEYS * 128;
-  static constexpr int S = 3;
+  static constexpr int S = HGCA_X2_STAGES;
   static constexpr int STAGE = 4 * KVQ;                 // K0 K1 V0 V1
-  static constexpr int PBUF = 128 * 128;
   static constexpr int OFF_Q = 0;                       // [tile][2 atoms]
   static constexpr int OFF_KV = OFF_Q + 4 * QATOM;
-  static constexpr int OFF_P = OFF_KV + S * STAGE;      // [tile][hi, lo]
-  static constexpr int OFF_BAR = OFF_P + 4 * PBUF;
+  static constexpr int OFF_BAR = OFF_KV + S * STAGE;    // (P lives in TMEM, over S)
   static constexpr int NBAR = 1 + 2 * S + 2 + 8;        // qfull, full[S], empty[S], sfull[2], pfull[2][2], pvdone[2][2]
   static constexpr int OFF_TM = OFF_BAR + NBAR * 8;
   static constexpr int SMEM = OFF_TM + 16 + 1024;
@@ -786,7 +789,7 @@ __global__ void __launch_bounds__(Tc5x2Cfg::THREADS, 1) append_tc5x2_kernel(cons
   __syncthreads();
   umma::fence_after_sync();
   const uint32_t tmem = *tm_holder;
-  const uint32_t sQ = smem_u32(sm + C::OFF_Q), sKV = smem_u32(sm + C::OFF_KV), sP = smem_u32(sm + C::OFF_P);
+  const uint32_t sQ = smem_u32(sm + C::OFF_Q), sKV = smem_u32(sm + C::OFF_KV);
 
   if (warp == 0) {  // ------------------------------------------------ TMA producer
     if (lane == 0) {
@@ -819,8 +822,8 @@ __global__ void __launch_bounds__(Tc5x2Cfg::THREADS, 1) append_tc5x2_kernel(cons
         for (int st = 0; st < nst; ++st) {
           const int s = st % C::S, b = st & 1;
           mbar_wait(&full[s], (st / C::S) & 1);
-          for (int t = 0; t < 2; ++t)  // S[t][b] was read by the tile's softmax of stage st-2
-            if (valid[t] && st >= 2) mbar_wait(&pfull[t * 2 + b], ((st - 2) >> 1) & 1);
+          for (int t = 0; t < 2; ++t)  // S[t][b] holds P(st-2) until the tile's PV(st-2) has read it
+            if (valid[t] && st >= 2) mbar_wait(&pvdone[t * 2 + b], ((st - 2) >> 1) & 1);
           umma::fence_after_sync();
           const uint32_t kb = sKV + s * C::STAGE;
           for (int t = 0; t < 2; ++t) {
@@ -843,13 +846,12 @@ __global__ void __launch_bounds__(Tc5x2Cfg::THREADS, 1) append_tc5x2_kernel(cons
             mbar_wait(&pfull[t * 2 + b], (st >> 1) & 1);
             umma::fence_after_sync();
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const uint32_t pb = sP + (t * 2 + h) * C::PBUF;
+            for (int h = 0; h < 2; ++h) {  // P hi in columns 0-31 of S[t][b], P lo in 32-63
 #pragma unroll
               for (int j = 0; j < T5_KEYS / 16; ++j) {
-                const uint64_t ad = umma::smem_desc(pb + j * 32, 16, 1024);
                 const uint64_t bd = umma::smem_desc(vb + j * 16 * 128, C::KVQ, 1024);
-                umma::mma_bf16(tmem + O_COL + t * D, ad, bd, IDESC_PV, st > 0 || h > 0 || j > 0);
+                umma::mma_bf16_ts(tmem + O_COL + t * D, tmem + (t * 2 + b) * T5_KEYS + h * 32 + j * 8, bd, IDESC_PV,
+                                  st > 0 || h > 0 || j > 0);
               }
             }
             umma::commit(smem_u32(&pvdone[t * 2 + b]));
@@ -867,7 +869,6 @@ __global__ void __launch_bounds__(Tc5x2Cfg::THREADS, 1) append_tc5x2_kernel(cons
       const uint32_t tl = (uint32_t)(quarter * 32) << 16;
       const float sl2 = a.scale * 1.4426950408889634f;
       float mu2 = -INFINITY, z = 0.f;
-      const uint32_t prow = (uint32_t)((r >> 3) * 1024 + (r & 7) * 128);
       for (int st = 0; st < nst; ++st) {
         const int b = st & 1;
         mbar_wait(&sfull[b], (st >> 1) & 1);
@@ -898,37 +899,34 @@ __global__ void __launch_bounds__(Tc5x2Cfg::THREADS, 1) append_tc5x2_kernel(cons
 #pragma unroll
         for (int j = 0; j < T5_KEYS; ++j) x[j] = ex2_approx(fmaf(x[j], sl2, -mu2));
         z = z * alpha + row_sum8(x);
-        if (st >= 1) {  // the tile's PV(st-1): P free again, O stable for a rescale
+        if (st >= 1 && __any_sync(FULL_MASK, alpha != 1.f)) {
+          // rescale O once the tile's PV(st-1) has completed (PV(st) waits for this stage's P)
           mbar_wait(&pvdone[t * 2 + (b ^ 1)], ((st - 1) >> 1) & 1);
           umma::fence_after_sync();
-          if (__any_sync(FULL_MASK, alpha != 1.f)) {
 #pragma unroll
-            for (int c0 = 0; c0 < D; c0 += 16) {
-              uint32_t v[16];
-              umma::ld_32x32b_x16(tmem + tl + O_COL + t * D + c0, v);
-              umma::ld_wait();
+          for (int c0 = 0; c0 < D; c0 += 16) {
+            uint32_t v[16];
+            umma::ld_32x32b_x16(tmem + tl + O_COL + t * D + c0, v);
+            umma::ld_wait();
 #pragma unroll
-              for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * alpha);
-              umma::st_32x32b_x16(tmem + tl + O_COL + t * D + c0, v);
-            }
-            umma::st_wait();
+            for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * alpha);
+            umma::st_32x32b_x16(tmem + tl + O_COL + t * D + c0, v);
           }
         }
-        unsigned char* ph = sm + C::OFF_P + (t * 2) * C::PBUF + prow;
-        unsigned char* pl = ph + C::PBUF;
+        {  // P(st) as bf16 hi / lo pairs over this row's S columns: the A operand of PV from TMEM
+          uint32_t hi[32], lo[32];
 #pragma unroll
-        for (int c = 0; c < T5_KEYS / 8; ++c) {
-          uint32_t hi[4], lo[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            hi[e] = pack_bf16(x[c * 8 + 2 * e], x[c * 8 + 2 * e + 1]);
-            lo[e] = pack_bf16(x[c * 8 + 2 * e] - bf16_lo_f(hi[e]), x[c * 8 + 2 * e + 1] - bf16_hi_f(hi[e]));
+          for (int e = 0; e < 32; ++e) {
+            hi[e] = pack_bf16(x[2 * e], x[2 * e + 1]);
+            lo[e] = pack_bf16(x[2 * e] - bf16_lo_f(hi[e]), x[2 * e + 1] - bf16_hi_f(hi[e]));
           }
-          const uint32_t off = (uint32_t)((c ^ (r & 7)) << 4);
-          *reinterpret_cast<uint4*>(ph + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-          *reinterpret_cast<uint4*>(pl + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+          const uint32_t sc = tmem + tl + (t * 2 + b) * T5_KEYS;
+          umma::st_32x32b_x16(sc, *reinterpret_cast<const uint32_t(*)[16]>(&hi[0]));
+          umma::st_32x32b_x16(sc + 16, *reinterpret_cast<const uint32_t(*)[16]>(&hi[16]));
+          umma::st_32x32b_x16(sc + 32, *reinterpret_cast<const uint32_t(*)[16]>(&lo[0]));
+          umma::st_32x32b_x16(sc + 48, *reinterpret_cast<const uint32_t(*)[16]>(&lo[16]));
+          umma::st_wait();
         }
-        umma::fence_smem_async();
         umma::fence_before_sync();
         __syncwarp();
         if (lane == 0) mbar_arrive(&pfull[t * 2 + b]);
