@@ -431,12 +431,14 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
   const int64_t p1 = min(a.seg_hi[seg], p0 + ACHUNK);
   const int64_t p0a = p0 & ~(int64_t)7;  // 8-aligned stage base: rotation == swizzle phase
   const int nst = (int)((p1 - p0a + T5_KEYS - 1) / T5_KEYS);
-  // split-key mode for 64-row groups: the group is loaded twice (TMEM lanes
-  // 0-63 and 64-127), the first copy's softmax threads take keys 0-31 of every
-  // stage, the second copy's keys 32-63 (their other P half stays zero), so
-  // all four softmax warps work and each row's per-stage chain is halved; the
-  // two copies' (m, z, O) are merged in the epilogue
-  const bool dup = a.RG == 64 && a.split_keys;
+  // split-key mode for groups of 64 or <= 32 rows: the group is loaded ncp = 2
+  // or 4 times (TMEM lanes 0-63 / 64-127, or one lane quarter per copy), copy c's
+  // softmax threads take keys [c * 64 / ncp, (c + 1) * 64 / ncp) of every stage
+  // (the rest of their P row stays zero), so all four softmax warps work and
+  // each row's per-stage chain is 1 / ncp; the copies' (m, z, O) are merged in
+  // the epilogue
+  const int ncp = !a.split_keys ? 1 : a.RG == 64 ? 2 : a.RG <= 32 ? 4 : 1;
+  const bool dup = ncp > 1;
   const int nsw = dup ? 4 : (int)((a.RG + 31) / 32);
   if (threadIdx.x == 0) {
     mbar_init(qfull, 1);
@@ -465,14 +467,15 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
       for (int c = 0; c < 8; ++c) *reinterpret_cast<uint4*>(prow0 + bb * C::PBUF + c * 16) = make_uint4(0, 0, 0, 0);
     umma::fence_smem_async();
   }
-  if (warp >= 2 && warp < 6 && dup) {  // split keys: zero the half of each P row this copy never writes
-    const int L = (warp & 3) * 32 + lane, oh = 1 - ((warp & 3) >> 1);
+  if (warp >= 2 && warp < 6 && dup) {  // split keys: zero the part of each P row this copy never writes
+    const int L = (warp & 3) * 32 + lane, cp = (warp & 3) * ncp / 4, cpc = 8 / ncp;  // 16-byte chunks per copy
     unsigned char* prow0 = sm + C::OFF_P + (L >> 3) * 1024 + (L & 7) * 128;
 #pragma unroll
     for (int bb = 0; bb < 4; ++bb)
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
-        *reinterpret_cast<uint4*>(prow0 + bb * C::PBUF + (((oh * 4 + c) ^ (L & 7)) << 4)) = make_uint4(0, 0, 0, 0);
+      for (int c = 0; c < 8; ++c)
+        if (c / cpc != cp)
+          *reinterpret_cast<uint4*>(prow0 + bb * C::PBUF + ((c ^ (L & 7)) << 4)) = make_uint4(0, 0, 0, 0);
     umma::fence_smem_async();
   }
   if (warp == 1) umma::tmem_alloc<C::TMEM_COLS>(smem_u32(tm_holder));
@@ -488,12 +491,10 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
       const int64_t b = bk / a.Hkv, kvh = bk % a.Hkv;
       const int qrow = (int)((b * a.Hq + kvh * a.G) * a.nq + rg * a.RG);
       mbar_expect_tx(qfull, 2 * C::QATOM);
-      if (dup) {  // rows 0-63 and again 64-127 (same swizzle phase: 8 KB apart)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          tma_load_2d(sQ + h * C::QATOM, &a.qmap5h, 64 * h, qrow, qfull, policy);
-          tma_load_2d(sQ + h * C::QATOM + 64 * 128, &a.qmap5h, 64 * h, qrow, qfull, policy);
-        }
+      if (dup) {  // the group at lanes 0, 128 / ncp, ...: same swizzle phase (multiples of 1 KB apart)
+        for (int h = 0; h < 2; ++h)
+          for (int cp = 0; cp < ncp; ++cp)
+            tma_load_2d(sQ + h * C::QATOM + cp * (128 / ncp) * 128, &a.qmap5h, 64 * h, qrow, qfull, policy);
       } else {
         tma_load_2d(sQ, &a.qmap5, 0, qrow, qfull, policy);
         tma_load_2d(sQ + C::QATOM, &a.qmap5, 64, qrow, qfull, policy);
@@ -558,8 +559,8 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
   } else if (dup || (warp & 3) * 32 < a.RG) {  // -------------------- softmax warps (rows)
     const int quarter = warp & 3;
     const int L = quarter * 32 + lane;                   // TMEM lane == P row
-    const int hh = dup ? (quarter >> 1) : 0;             // split keys: which half of each stage
-    const int r = dup ? (quarter & 1) * 32 + lane : L;   // row of the group
+    const int hh = dup ? quarter * ncp / 4 : 0;          // split keys: this thread's copy (part of each stage)
+    const int r = dup ? L % (128 / ncp) : L;             // row of the group
     const uint32_t tl = (uint32_t)(quarter * 32) << 16;
     // softmax in log2 units: x = s * log2(e), p = 2^(x - mu2) == exp(s - mu2 * ln 2)
     const float sl2 = a.scale * 1.4426950408889634f;
@@ -578,7 +579,7 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
         {
           uint32_t v[NK / 16][16];  // all loads in flight, one wait
 #pragma unroll
-          for (int c = 0; c < NK / 16; ++c) umma::ld_32x32b_x16(tmem + tl + b * T5_KEYS + hh * 32 + c * 16, v[c]);
+          for (int c = 0; c < NK / 16; ++c) umma::ld_32x32b_x16(tmem + tl + b * T5_KEYS + hh * NK + c * 16, v[c]);
           umma::ld_wait();
           umma::fence_before_sync();
           __syncwarp();
@@ -588,7 +589,7 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
 #pragma unroll
             for (int j = 0; j < 16; ++j) x[c * 16 + j] = __uint_as_float(v[c][j]);
         }
-        const int64_t kp0 = p0a + (int64_t)st * T5_KEYS + hh * 32;
+        const int64_t kp0 = p0a + (int64_t)st * T5_KEYS + hh * NK;
         if (!(kp0 >= p0 && kp0 + NK <= p1)) {  // a partial part (warp-uniform): mask the keys out of range
           const int jlo = (int)max(min(p0 - kp0, (int64_t)NK), (int64_t)0);
           const int jhi = (int)max(min(p1 - kp0, (int64_t)NK), (int64_t)0);
@@ -637,7 +638,7 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
             hi[e] = pack_bf16(x[c * 8 + 2 * e], x[c * 8 + 2 * e + 1]);
             lo[e] = pack_bf16(x[c * 8 + 2 * e] - bf16_lo_f(hi[e]), x[c * 8 + 2 * e + 1] - bf16_hi_f(hi[e]));
           }
-          const uint32_t off = (uint32_t)(((hh * 4 + c) ^ (L & 7)) << 4);
+          const uint32_t off = (uint32_t)(((hh * (NK / 8) + c) ^ (L & 7)) << 4);
           *reinterpret_cast<uint4*>(ph + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
           *reinterpret_cast<uint4*>(pl + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
         }
@@ -647,7 +648,8 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
         if (lane == 0) mbar_arrive(&pfull[b]);
       }
     };
-    if (dup) stages(std::integral_constant<int, 32>{});
+    if (ncp == 4) stages(std::integral_constant<int, 16>{});
+    else if (dup) stages(std::integral_constant<int, 32>{});
     else stages(std::integral_constant<int, T5_KEYS>{});
     mbar_wait(&pvdone[(nst - 1) & 1], ((nst - 1) >> 1) & 1);  // the last PV (and all before it)
     P5(if (warp == 2 && lane == 0) { atomicAdd(&g_tc5prof[3], (unsigned long long)w_s);
@@ -657,34 +659,44 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
     // this row's partial (m, z, acc), as append_attend_kernel<D, 1> writes it;
     // split keys: the second copy (lanes 64-127) hands its (m, z, O) to the
     // first through shared memory (the P buffers: every PV is complete)
-    float fa = 1.f, fb = 0.f;
-    float* ob = reinterpret_cast<float*>(sm + C::OFF_P);  // [D][64] column-major: conflict-free
-    float* mzb = ob + D * 64;                             // [64][2]
+    // split keys: copies 1.. hand their (m, z, O) to copy 0 through shared
+    // memory (the P buffers: every PV is complete); copy 0 merges them
+    const int rw = 128 / ncp;                             // rows per copy (lanes)
+    float* ob = reinterpret_cast<float*>(sm + C::OFF_P);  // [copy - 1][D][rw] column-major: conflict-free
+    float* mzb = ob + 3 * D * 32;                         // [copy - 1][rw][2] (past the largest O area)
+    float fc[4] = {1.f, 0.f, 0.f, 0.f};
     if (dup) {
       // (ordered already through pfull -> PV -> pvdone; the barrier makes the
       // P-region reuse explicit for the race checker, once per CTA)
       asm volatile("bar.sync 1, 128;\n" ::: "memory");
       if (hh) {
+        float* obc = ob + (hh - 1) * D * rw;
 #pragma unroll
         for (int c0 = 0; c0 < D; c0 += 16) {
           uint32_t v[16];
           umma::ld_32x32b_x16(tmem + tl + O_COL + c0, v);
           umma::ld_wait();
 #pragma unroll
-          for (int j = 0; j < 16; ++j) ob[(c0 + j) * 64 + r] = __uint_as_float(v[j]);
+          for (int j = 0; j < 16; ++j) obc[(c0 + j) * rw + r] = __uint_as_float(v[j]);
         }
-        mzb[r * 2] = mu2;
-        mzb[r * 2 + 1] = z;
+        mzb[((hh - 1) * rw + r) * 2] = mu2;
+        mzb[((hh - 1) * rw + r) * 2 + 1] = z;
       }
       asm volatile("bar.sync 1, 128;\n" ::: "memory");  // the four softmax warps
       if (!hh) {
-        const float mb = mzb[r * 2], zb = mzb[r * 2 + 1];
-        const float mm = fmaxf(mu2, mb);
-        if (mm != -INFINITY) {
-          fa = mu2 == -INFINITY ? 0.f : ex2_approx(mu2 - mm);
-          fb = mb == -INFINITY ? 0.f : ex2_approx(mb - mm);
+        float mc[4] = {mu2, -INFINITY, -INFINITY, -INFINITY}, zc[4] = {z, 0.f, 0.f, 0.f};
+        float mm = mu2;
+        for (int c = 1; c < ncp; ++c) {
+          mc[c] = mzb[((c - 1) * rw + r) * 2];
+          zc[c] = mzb[((c - 1) * rw + r) * 2 + 1];
+          mm = fmaxf(mm, mc[c]);
         }
-        z = z * fa + zb * fb;
+        z = 0.f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          fc[c] = (c < ncp && mc[c] != -INFINITY) ? ex2_approx(mc[c] - mm) : 0.f;
+          z += zc[c] * fc[c];
+        }
         mu2 = mm;
       }
     }
@@ -699,7 +711,11 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
         umma::ld_wait();
         float o[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) o[j] = dup ? __uint_as_float(v[j]) * fa + ob[(c0 + j) * 64 + r] * fb : __uint_as_float(v[j]);
+        for (int j = 0; j < 16; ++j) {
+          float acc = __uint_as_float(v[j]) * fc[0];
+          for (int c = 1; c < ncp; ++c) acc += ob[((c - 1) * D + c0 + j) * rw + r] * fc[c];
+          o[j] = dup ? acc : __uint_as_float(v[j]);
+        }
         if (mine) {
 #pragma unroll
           for (int j = 0; j < 16; j += 4) pa[(c0 + j) / 4] = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
@@ -1916,16 +1932,18 @@ static int launch_append_d(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, i
       if (rc5) return rc5;
       const int rc = make_map2d(&a.qmap5, q, B * Hq * nq, D, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
       if (rc) return rc;
-      const int rch = make_map2d(&a.qmap5h, q, B * Hq * nq, D, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B);
-      if (rch) return rch;
       const char* sk = getenv("HGCA_APPEND_SPLIT_KEYS");
       a.split_keys = !(sk && *sk == '0');
+      // split keys: one box per copy of the group (64 rows for 2 copies, 32 for 4)
+      const int rch = make_map2d(&a.qmap5h, q, B * Hq * nq, D, 64, p.RG == 64 ? 64 : 32, CU_TENSOR_MAP_SWIZZLE_128B);
+      if (rch) return rch;
     }
     static DevFlags attr5;
     if (const int e5 = set_smem_dev(append_tc5_kernel, Tc5Cfg::SMEM, attr5)) return e5;
-    // row groups of >= 64 rows (the M = 128 tile's cost is per item; tiny groups stay on mma.sync)
+    // row groups of >= 64 rows, or <= 32 rows in split-key mode (four copies of the group fill
+    // the 128-row tile); groups of 33-63 rows stay on mma.sync
     const char* force_mma = getenv("HGCA_APPEND_MMA_SYNC");  // A/B switch: 1 = the mma.sync pass for every group
-    const bool tc5 = p.RG >= 64 && !(force_mma && *force_mma && *force_mma != '0');
+    const bool tc5 = (p.RG >= 64 || (a.split_keys && p.RG <= 32)) && !(force_mma && *force_mma && *force_mma != '0');
     static DevFlags attr52;
     if (const int e52 = set_smem_dev(append_tc5x2_kernel, Tc5x2Cfg::SMEM, attr52)) return e52;
     const bool two_tiles = tc5 && p.RG == 128 && p.n_rg >= 2;  // pairs of 128-row groups share the K|V stream
@@ -1948,20 +1966,19 @@ static int launch_append_d(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, i
   if ((mean_archive || mean_window) && p.n_items > 0) {
     bool tc5_mean = false;
     if constexpr (D == 128) {
+      // key-major tcgen05 pass for every row group (default); HGCA_APPEND_MEAN_OLD=1: the
+      // row-major pass with the head-sum GEMM (groups of >= 64 rows); HGCA_APPEND_MMA_SYNC=1:
+      // the mma.sync pass. Two row groups per CTA share the K stream (HGCA_APPEND_MEAN_NT=1: one)
       const char* force_mma = getenv("HGCA_APPEND_MMA_SYNC");
-      tc5_mean = p.RG >= 64 && !(force_mma && *force_mma && *force_mma != '0');
-      static DevFlags attr_m, attr_m2;
-      if (tc5_mean) {
-        if (const int em = set_smem_dev(append_tc5_mean_kernel, Tc5MCfg::SMEM, attr_m)) return em;
-        if (const int em2 = set_smem_dev(append_tc5_mean_x2_kernel, Tc5Mx2Cfg::SMEM, attr_m2)) return em2;
-      }
-      // key-major pass (default; HGCA_APPEND_MEAN_OLD=1: the row-major pass with the head-sum GEMM);
-      // two row groups per CTA share the K stream (HGCA_APPEND_MEAN_NT=1: one)
       const char* old_mean = getenv("HGCA_APPEND_MEAN_OLD");
       const char* nt_env = getenv("HGCA_APPEND_MEAN_NT");
-      const bool km = tc5_mean && !(old_mean && *old_mean && *old_mean != '0');
+      const bool forced = force_mma && *force_mma && *force_mma != '0';
+      const bool oldm = old_mean && *old_mean && *old_mean != '0';
+      const bool km = !forced && !oldm;
       const bool km2 = km && p.n_rg >= 2 && !(nt_env && *nt_env == '1');
-      static DevFlags attr_k1, attr_k2;
+      const bool rowmajor = !forced && oldm && p.RG >= 64;
+      tc5_mean = km || rowmajor;
+      static DevFlags attr_m, attr_m2, attr_k1, attr_k2;
       const int64_t nc = p.nch0 + p.nch1;
       if (km2) {
         if (const int ek = set_smem_dev(append_tc5_mean_k_kernel<2>, Tc5KCfg<2>::SMEM, attr_k2)) return ek;
@@ -1970,11 +1987,15 @@ static int launch_append_d(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, i
       } else if (km) {
         if (const int ek = set_smem_dev(append_tc5_mean_k_kernel<1>, Tc5KCfg<1>::SMEM, attr_k1)) return ek;
         append_tc5_mean_k_kernel<1><<<(unsigned)(B * Hkv * p.n_rg * nc), Tc5KCfg<1>::THREADS, Tc5KCfg<1>::SMEM, s>>>(a);
-      } else if (tc5_mean && p.RG == 128 && p.n_rg >= 2)  // pairs of 128-row groups share the K stream
-        append_tc5_mean_x2_kernel<<<(unsigned)(B * Hkv * ((p.n_rg + 1) / 2) * (p.nch0 + p.nch1)), Tc5Mx2Cfg::THREADS,
-                                    Tc5Mx2Cfg::SMEM, s>>>(a);
-      else if (tc5_mean)
-        append_tc5_mean_kernel<<<(unsigned)p.n_items, Tc5MCfg::THREADS, Tc5MCfg::SMEM, s>>>(a);
+      } else if (rowmajor) {
+        if (const int em = set_smem_dev(append_tc5_mean_kernel, Tc5MCfg::SMEM, attr_m)) return em;
+        if (const int em2 = set_smem_dev(append_tc5_mean_x2_kernel, Tc5Mx2Cfg::SMEM, attr_m2)) return em2;
+        if (p.RG == 128 && p.n_rg >= 2)  // pairs of 128-row groups share the K stream
+          append_tc5_mean_x2_kernel<<<(unsigned)(B * Hkv * ((p.n_rg + 1) / 2) * nc), Tc5Mx2Cfg::THREADS,
+                                      Tc5Mx2Cfg::SMEM, s>>>(a);
+        else
+          append_tc5_mean_kernel<<<(unsigned)p.n_items, Tc5MCfg::THREADS, Tc5MCfg::SMEM, s>>>(a);
+      }
     }
     if (!tc5_mean) append_attend_kernel<D, 2><<<(unsigned)p.n_items, (nw + 1) * 32, C2::SMEM, s>>>(a);
   }
