@@ -56,6 +56,8 @@ if __name__ == "__main__":
         run("bfloat16", steps=3, append_at=0, append_nq=16)
     if mode in ("all", "bf16-append-tc5x2"):  # G*n_q = 256 rows: the two-tile tcgen05 passes
         run("bfloat16", steps=3, append_at=0, append_nq=64)
+    if mode in ("all", "bf16-append-small"):  # G*n_q = 12 rows: split-key pass 1 with four copies
+        run("bfloat16", steps=3, append_at=0, append_nq=3)
     if mode in ("all", "bf16-append-long"):  # n_q = 160 > 128: chunked tcgen05 passes
         run("bfloat16", steps=3, append_at=0, append_nq=160, bn=8)
     if mode in ("all", "f32"):
