@@ -431,13 +431,13 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
   const int64_t p1 = min(a.seg_hi[seg], p0 + ACHUNK);
   const int64_t p0a = p0 & ~(int64_t)7;  // 8-aligned stage base: rotation == swizzle phase
   const int nst = (int)((p1 - p0a + T5_KEYS - 1) / T5_KEYS);
-  // split-key mode for groups of 64 or <= 32 rows: the group is loaded ncp = 2
+  // split-key mode for groups of <= 64 rows: the group is loaded ncp = 2
   // or 4 times (TMEM lanes 0-63 / 64-127, or one lane quarter per copy), copy c's
   // softmax threads take keys [c * 64 / ncp, (c + 1) * 64 / ncp) of every stage
   // (the rest of their P row stays zero), so all four softmax warps work and
   // each row's per-stage chain is 1 / ncp; the copies' (m, z, O) are merged in
   // the epilogue
-  const int ncp = !a.split_keys ? 1 : a.RG == 64 ? 2 : a.RG <= 32 ? 4 : 1;
+  const int ncp = !a.split_keys ? 1 : a.RG <= 32 ? 4 : a.RG <= 64 ? 2 : 1;
   const bool dup = ncp > 1;
   const int nsw = dup ? 4 : (int)((a.RG + 31) / 32);
   if (threadIdx.x == 0) {
@@ -1935,15 +1935,15 @@ static int launch_append_d(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, i
       const char* sk = getenv("HGCA_APPEND_SPLIT_KEYS");
       a.split_keys = !(sk && *sk == '0');
       // split keys: one box per copy of the group (64 rows for 2 copies, 32 for 4)
-      const int rch = make_map2d(&a.qmap5h, q, B * Hq * nq, D, 64, p.RG == 64 ? 64 : 32, CU_TENSOR_MAP_SWIZZLE_128B);
+      const int rch = make_map2d(&a.qmap5h, q, B * Hq * nq, D, 64, p.RG > 32 ? 64 : 32, CU_TENSOR_MAP_SWIZZLE_128B);
       if (rch) return rch;
     }
     static DevFlags attr5;
     if (const int e5 = set_smem_dev(append_tc5_kernel, Tc5Cfg::SMEM, attr5)) return e5;
-    // row groups of >= 64 rows, or <= 32 rows in split-key mode (four copies of the group fill
-    // the 128-row tile); groups of 33-63 rows stay on mma.sync
+    // every row group: >= 64 rows as one tile, smaller ones in split-key mode (2 or 4 copies of
+    // the group fill the 128-row tile); without split keys groups of < 64 rows stay on mma.sync
     const char* force_mma = getenv("HGCA_APPEND_MMA_SYNC");  // A/B switch: 1 = the mma.sync pass for every group
-    const bool tc5 = (p.RG >= 64 || (a.split_keys && p.RG <= 32)) && !(force_mma && *force_mma && *force_mma != '0');
+    const bool tc5 = (p.RG >= 64 || a.split_keys) && !(force_mma && *force_mma && *force_mma != '0');
     static DevFlags attr52;
     if (const int e52 = set_smem_dev(append_tc5x2_kernel, Tc5x2Cfg::SMEM, attr52)) return e52;
     const bool two_tiles = tc5 && p.RG == 128 && p.n_rg >= 2;  // pairs of 128-row groups share the K|V stream
