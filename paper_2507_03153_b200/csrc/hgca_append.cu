@@ -408,6 +408,7 @@ __device__ unsigned long long g_tc5prof[8];
 #else
 #define P5(...)
 #endif
+template <int NCP>  // copies of the row group in the tile: 1, or 2 / 4 in split-key mode
 __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __grid_constant__ AppendArgs a) {
   using C = Tc5Cfg;
   constexpr int D = 128;
@@ -437,8 +438,8 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
   // (the rest of their P row stays zero), so all four softmax warps work and
   // each row's per-stage chain is 1 / ncp; the copies' (m, z, O) are merged in
   // the epilogue
-  const int ncp = !a.split_keys ? 1 : a.RG <= 32 ? 4 : a.RG <= 64 ? 2 : 1;
-  const bool dup = ncp > 1;
+  constexpr int ncp = NCP;
+  constexpr bool dup = ncp > 1;
   const int nsw = dup ? 4 : (int)((a.RG + 31) / 32);
   if (threadIdx.x == 0) {
     mbar_init(qfull, 1);
@@ -648,9 +649,7 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
         if (lane == 0) mbar_arrive(&pfull[b]);
       }
     };
-    if (ncp == 4) stages(std::integral_constant<int, 16>{});
-    else if (dup) stages(std::integral_constant<int, 32>{});
-    else stages(std::integral_constant<int, T5_KEYS>{});
+    stages(std::integral_constant<int, T5_KEYS / NCP>{});
     mbar_wait(&pvdone[(nst - 1) & 1], ((nst - 1) >> 1) & 1);  // the last PV (and all before it)
     P5(if (warp == 2 && lane == 0) { atomicAdd(&g_tc5prof[3], (unsigned long long)w_s);
        atomicAdd(&g_tc5prof[6], (unsigned long long)nst);
@@ -686,11 +685,13 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
       if (!hh) {
         float mc[4] = {mu2, -INFINITY, -INFINITY, -INFINITY}, zc[4] = {z, 0.f, 0.f, 0.f};
         float mm = mu2;
-        for (int c = 1; c < ncp; ++c) {
-          mc[c] = mzb[((c - 1) * rw + r) * 2];
-          zc[c] = mzb[((c - 1) * rw + r) * 2 + 1];
-          mm = fmaxf(mm, mc[c]);
-        }
+#pragma unroll
+        for (int c = 1; c < 4; ++c)
+          if (c < ncp) {
+            mc[c] = mzb[((c - 1) * rw + r) * 2];
+            zc[c] = mzb[((c - 1) * rw + r) * 2 + 1];
+            mm = fmaxf(mm, mc[c]);
+          }
         z = 0.f;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -713,7 +714,9 @@ __global__ void __launch_bounds__(Tc5Cfg::THREADS, 1) append_tc5_kernel(const __
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           float acc = __uint_as_float(v[j]) * fc[0];
-          for (int c = 1; c < ncp; ++c) acc += ob[((c - 1) * D + c0 + j) * rw + r] * fc[c];
+#pragma unroll
+          for (int c = 1; c < 4; ++c)  // unrolled: the copies' loads are independent
+            if (c < ncp) acc += ob[((c - 1) * D + c0 + j) * rw + r] * fc[c];
           o[j] = dup ? acc : __uint_as_float(v[j]);
         }
         if (mine) {
@@ -1655,7 +1658,7 @@ __global__ void __launch_bounds__(Tc5KCfg<NT>::THREADS, 1) append_tc5_mean_k_ker
     const float inv_nq = 1.f / (float)a.nq;
     const int nq = (int)a.nq;
     const int64_t ld = a.mean_ld[seg];
-    const int W = nq % 32 == 0 ? 32 : nq == 16 ? 16 : nq == 8 ? 8 : 0;  // whole heads per sum group
+    const int W = nq % 32 == 0 ? 32 : nq % 8 == 0 ? 8 : nq % 4 == 0 ? 4 : 0;  // columns per sum group
     // the two sets of an accumulator split its columns at a head boundary
     // (when that boundary is a 32-column one; else the first set takes all)
     const int csplit = (ncol / nq / 2) * nq;
@@ -1703,47 +1706,43 @@ __global__ void __launch_bounds__(Tc5KCfg<NT>::THREADS, 1) append_tc5_mean_k_ker
         }
 #pragma unroll
         for (int e = 0; e < 32; ++e) x[e] = ex2_approx(x[e]);
-        if (W) {  // sum groups of 8 columns (a tree each); heads are whole groups
+        // heads of n_q columns end on group boundaries: a tree per group of W columns, then
+        // the groups accumulate into the head's sum
+        auto flush = [&]() {
+          if (mine) *mp = hs * inv_nq;
+          mp += ld;
+          hs = 0.f;
+          left = nq;
+        };
+        if (W == 32) {  // whole chunks of one head: one check per chunk
           float g8[4];
 #pragma unroll
           for (int g = 0; g < 4; ++g)
             g8[g] = ((x[g * 8] + x[g * 8 + 1]) + (x[g * 8 + 2] + x[g * 8 + 3])) +
                     ((x[g * 8 + 4] + x[g * 8 + 5]) + (x[g * 8 + 6] + x[g * 8 + 7]));
-          if (W == 8) {
+          hs += (g8[0] + g8[1]) + (g8[2] + g8[3]);
+          if ((left -= 32) == 0) flush();
+        } else if (W == 8) {
 #pragma unroll
-            for (int g = 0; g < 4; ++g)
-              if (c0 + g * 8 < cend) {
-                if (mine) *mp = g8[g] * inv_nq;
-                mp += ld;
-              }
-          } else if (W == 16) {
-#pragma unroll
-            for (int g = 0; g < 2; ++g)
-              if (c0 + g * 16 < cend) {
-                if (mine) *mp = (g8[2 * g] + g8[2 * g + 1]) * inv_nq;
-                mp += ld;
-              }
-          } else {
-            hs += (g8[0] + g8[1]) + (g8[2] + g8[3]);
-            left -= 32;
-            if (left == 0) {
-              if (mine) *mp = hs * inv_nq;
-              mp += ld;
-              hs = 0.f;
-              left = nq;
+          for (int g = 0; g < 4; ++g)
+            if (c0 + g * 8 < cend) {
+              hs += ((x[g * 8] + x[g * 8 + 1]) + (x[g * 8 + 2] + x[g * 8 + 3])) +
+                    ((x[g * 8 + 4] + x[g * 8 + 5]) + (x[g * 8 + 6] + x[g * 8 + 7]));
+              if ((left -= 8) == 0) flush();
             }
-          }
+        } else if (W == 4) {
+#pragma unroll
+          for (int g = 0; g < 8; ++g)
+            if (c0 + g * 4 < cend) {
+              hs += (x[g * 4] + x[g * 4 + 1]) + (x[g * 4 + 2] + x[g * 4 + 3]);
+              if ((left -= 4) == 0) flush();
+            }
         } else {  // other n_q: column by column
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
             if (c0 + e < cend) {
               hs += x[e];
-              if (--left == 0) {
-                if (mine) *mp = hs * inv_nq;
-                mp += ld;
-                hs = 0.f;
-                left = nq;
-              }
+              if (--left == 0) flush();
             }
           }
         }
@@ -1938,8 +1937,10 @@ static int launch_append_d(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, i
       const int rch = make_map2d(&a.qmap5h, q, B * Hq * nq, D, 64, p.RG > 32 ? 64 : 32, CU_TENSOR_MAP_SWIZZLE_128B);
       if (rch) return rch;
     }
-    static DevFlags attr5;
-    if (const int e5 = set_smem_dev(append_tc5_kernel, Tc5Cfg::SMEM, attr5)) return e5;
+    static DevFlags attr5[3];
+    const int ncp = !a.split_keys ? 1 : p.RG <= 32 ? 4 : p.RG <= 64 ? 2 : 1;
+    auto tc5k = ncp == 4 ? append_tc5_kernel<4> : ncp == 2 ? append_tc5_kernel<2> : append_tc5_kernel<1>;
+    if (const int e5 = set_smem_dev(tc5k, Tc5Cfg::SMEM, attr5[ncp >> 1])) return e5;
     // every row group: >= 64 rows as one tile, smaller ones in split-key mode (2 or 4 copies of
     // the group fill the 128-row tile); without split keys groups of < 64 rows stay on mma.sync
     const char* force_mma = getenv("HGCA_APPEND_MMA_SYNC");  // A/B switch: 1 = the mma.sync pass for every group
@@ -1951,7 +1952,7 @@ static int launch_append_d(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, i
       append_tc5x2_kernel<<<(unsigned)(B * Hkv * ((p.n_rg + 1) / 2) * (p.nch0 + p.nch1)), Tc5x2Cfg::THREADS,
                             Tc5x2Cfg::SMEM, s>>>(a);
     else if (p.n_items > 0 && tc5)
-      append_tc5_kernel<<<(unsigned)p.n_items, Tc5Cfg::THREADS, Tc5Cfg::SMEM, s>>>(a);
+      tc5k<<<(unsigned)p.n_items, Tc5Cfg::THREADS, Tc5Cfg::SMEM, s>>>(a);
     else if (p.n_items > 0)
       append_attend_kernel<D, 1><<<(unsigned)p.n_items, (nw + 1) * 32, C1::SMEM, s>>>(a);
   } else {
