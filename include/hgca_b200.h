@@ -305,9 +305,11 @@ int hgca_decode_step(const hgca_decode_desc* desc, hgca_stream_t stream);
  * [B*Hq, lo] and mean_window [B*Hq, hi-lo] (optional) receive, per query head
  * and position, the mean attention weight over the nq rows (a_cpu / a_gpu
  * row means). ws: hgca_append_ws_bytes(...) bytes of device scratch.
- * Kernels: D = 128 with >= 64 query rows per row group (G * nq >= 64) runs
- * both passes on tcgen05 (TMEM accumulators; two 128-row groups per CTA when
- * a kv head has two); otherwise mma.sync. Same results contract either way. */
+ * Kernels: D = 128 runs both passes on tcgen05 for every row group (TMEM
+ * accumulators; groups of < 64 rows loaded 2 or 4 times into the 128-row tile
+ * with the keys split between the copies; two 128-row groups per CTA when a kv
+ * head has two; the mean-weight pass key-major); D = 64 uses mma.sync. Same
+ * results contract either way. */
 int64_t hgca_append_ws_bytes(int64_t B, int64_t Hq, int64_t Hkv, int64_t D, int64_t nq, int64_t lo, int64_t hi);
 int hgca_append_bf16(const void* KV, int64_t B, int64_t Hq, int64_t Hkv, int64_t T, int64_t D, const void* q,
                      int64_t nq, double scale, int64_t lo, int64_t hi, float* out, double* lse, float* mean_archive,
