@@ -365,7 +365,7 @@ def test_decode_host_packed_matches_device_path(cuda):
 
 
 @pytest.mark.parametrize("nq,Hq,Hkv,d", [(16, 8, 2, 128), (5, 8, 4, 128), (1, 4, 4, 64), (40, 8, 2, 64),
-                                         (8, 8, 2, 128), (1, 8, 2, 128), (3, 8, 2, 128), (12, 8, 2, 128),  # split keys
+                                         (8, 8, 2, 128), (1, 8, 2, 128), (3, 8, 2, 128), (12, 8, 2, 128), (1, 4, 4, 128), (2, 4, 4, 128),  # split keys
                                          (32, 8, 2, 128), (64, 8, 2, 128),  # tcgen05 pass 1
                                          (160, 8, 2, 128), (200, 4, 4, 128), (150, 4, 4, 64)])  # > 128: chunks
 def test_bf16_append_tensor_core_path_matches_reference_path(cuda, nq, Hq, Hkv, d):
