@@ -1267,6 +1267,58 @@ __global__ void __launch_bounds__(1024) union_build_kernel(const uint32_t* __res
   __syncthreads();
   if (tid == 0) base_s = 0;
   __syncthreads();
+  const int64_t per = (nw + blockDim.x - 1) / blockDim.x;
+  if (!grouped && per <= 8) {
+    // position order, every word of the list in one pass: thread t owns words
+    // [t * per, (t + 1) * per) (all loads in flight at once), one block scan of
+    // the per-thread counts, then the thread writes its entries in order (the
+    // masks re-read from cache). The chunked loop below needs nw / 1024 rounds of
+    // load -> scan -> write latency.
+    int c = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int64_t w = tid * per + k;
+      if (k < per && w < nw) {
+        uint32_t mg[8];
+        c += __popc(word_masks(w, mg));
+      }
+    }
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      int x = lane < nwarp ? wsum[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane < nwarp) wsum[lane] = x;
+    }
+    __syncthreads();
+    int pos = (wid ? wsum[wid - 1] : 0) + (incl - c);
+    for (int k = 0; k < per; ++k) {
+      const int64_t w = tid * per + k;
+      if (w >= nw) break;
+      uint32_t mg[8];
+      uint32_t hit = word_masks(w, mg);
+      while (hit) {
+        const int bit = __ffs(hit) - 1;
+        hit &= hit - 1;
+        uint32_t qm = 0;
+        for (int g = 0; g < G; ++g) qm |= ((mg[g] >> bit) & 1u) << g;
+        u_ent[bk * T + pos] = (int32_t)((uint32_t)((w << 5) + bit) | (qm << 24));
+        ++pos;
+      }
+    }
+    if (tid == 0) u_cnt[bk] = wsum[nwarp - 1];
+    return;
+  }
   const int nbins = grouped ? (1 << G) : 2;
   for (int v = 1; v < nbins; ++v) {
     if (grouped && hist[v] == 0) continue;  // uniform: hist is stable after the barrier
@@ -1333,25 +1385,33 @@ __global__ void __launch_bounds__(1024) union_build_kernel(const uint32_t* __res
 // as close in HBM as plain position order (interleaving classes over the
 // whole list let the j-th entries of different classes drift apart: 2.3%
 // slower on C2). One warp per window; keys (rank, class) are unique, the slot
-// is the number of smaller keys.
+// is the number of smaller keys. Grid (B * Hkv, windows / 32): every window of
+// every list is independent, so the whole GPU takes them (one CTA per list
+// left ~4/5 of the SMs idle at C3).
 __global__ void __launch_bounds__(1024) union_window_classes_kernel(int32_t* u_ent, const int32_t* u_cnt, int64_t T) {
   const int64_t bk = blockIdx.x;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const int cnt = u_cnt[bk];
   int32_t* ent = u_ent + bk * T;
-  for (int w0 = wid * 32; w0 < cnt; w0 += nwarp * 32) {
+  const int w_first = (int)(blockIdx.y * nwarp + wid) * 32;
+  for (int w0 = w_first; w0 < cnt; w0 += (int)gridDim.y * nwarp * 32) {
     const int n = min(32, cnt - w0);
     const bool ok = lane < n;
     const int32_t e = ok ? ent[w0 + lane] : 0;
     const int cls = ok ? (e & 7) : 8;  // positions are the low 24 bits; p & 7 = e & 7
-    const uint32_t same = __match_any_sync(FULL, cls);
-    const int rank = __popc(same & ((1u << lane) - 1u));
-    const int key = rank * 16 + cls;
-    int slot = 0;
+    // slot = number of entries with a smaller (rank, class) key: those of a lower
+    // rank in any class (min(count_c, rank) per class) plus those of the same
+    // rank in a lower class (count_c > rank)
+    int rank = 0, slot = 0;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const int kj = __shfl_sync(FULL, key, j);
-      slot += (j < n && kj < key) ? 1 : 0;
+    for (int c = 0; c < 8; ++c) {
+      const uint32_t m = __ballot_sync(FULL, cls == c);
+      if (cls == c) rank = __popc(m & ((1u << lane) - 1u));
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int cnt_c = __popc(__ballot_sync(FULL, cls == c));
+      slot += min(cnt_c, rank) + ((c < cls && cnt_c > rank) ? 1 : 0);
     }
     __syncwarp();
     if (ok) ent[w0 + slot] = e;
@@ -1637,7 +1697,9 @@ int launch_union_build(const uint32_t* sel, int64_t B, int64_t Hq, int64_t Hkv, 
   if (grouped >= 2) {
     const cudaError_t e0 = cudaGetLastError();
     if (e0 != cudaSuccess) return (int)e0;
-    union_window_classes_kernel<<<(unsigned)(B * Hkv), 1024, 0, s>>>(u_ent, u_cnt, T);
+    // 8-warp CTAs, ~8 windows per warp at a full archive (the lists are at most n_arch long)
+    const unsigned chunks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n_arch + 2047) / 2048, 65535));
+    union_window_classes_kernel<<<dim3((unsigned)(B * Hkv), chunks), 256, 0, s>>>(u_ent, u_cnt, T);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
