@@ -1302,18 +1302,21 @@ __global__ void __launch_bounds__(1024) union_build_kernel(const uint32_t* __res
     }
     __syncthreads();
     int pos = (wid ? wsum[wid - 1] : 0) + (incl - c);
+    int32_t* out = u_ent + bk * T;
     for (int k = 0; k < per; ++k) {
       const int64_t w = tid * per + k;
       if (w >= nw) break;
       uint32_t mg[8];
       uint32_t hit = word_masks(w, mg);
+      const uint32_t wbase = (uint32_t)(w << 5);
       while (hit) {
         const int bit = __ffs(hit) - 1;
         hit &= hit - 1;
         uint32_t qm = 0;
-        for (int g = 0; g < G; ++g) qm |= ((mg[g] >> bit) & 1u) << g;
-        u_ent[bk * T + pos] = (int32_t)((uint32_t)((w << 5) + bit) | (qm << 24));
-        ++pos;
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+          if (g < G) qm |= ((mg[g] >> bit) & 1u) << g;
+        out[pos++] = (int32_t)((wbase + bit) | (qm << 24));
       }
     }
     if (tid == 0) u_cnt[bk] = wsum[nwarp - 1];
